@@ -1,0 +1,363 @@
+"""TEST INFRASTRUCTURE ONLY -- numpy/ctypes front end of the CPU oracle.
+
+Two libraries sit behind this module:
+
+* ``liboracle.so`` -- the CPU restatement in ``oracle/oracle.cpp`` (each
+  function cites the reference file:line it follows).
+* ``_ref/libtcsref.so`` -- the reference's own headers compiled unmodified
+  behind a C-ABI shim (``oracle/ref_shim.cpp``), built here where
+  ``/root/reference`` exists and shipped prebuilt to the GPU box.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline /
+``--impl reference`` legs may import this package; the product library never
+does (and has no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_u32p = C.POINTER(C.c_uint32)
+_f32p = C.POINTER(C.c_float)
+_u64p = C.POINTER(C.c_uint64)
+
+FP16, TF32 = 0, 1
+K_OF = {FP16: 8, TF32: 4}
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def _load(name):
+    path = os.path.join(_HERE, name)
+    if not os.path.exists(path):
+        raise FileNotFoundError(f"{path} missing: run `make -C oracle`")
+    return C.CDLL(path)
+
+
+_orc = None
+_ref = None
+
+
+def lib():
+    global _orc
+    if _orc is None:
+        _orc = _load("liboracle.so")
+        _orc.orc_round_fp16.restype = C.c_float
+        _orc.orc_round_fp16.argtypes = [C.c_float]
+        _orc.orc_round_tf32.restype = C.c_float
+        _orc.orc_round_tf32.argtypes = [C.c_float]
+        _orc.orc_generate_random_sparse.restype = C.c_int64
+        _orc.orc_generate_random_sparse.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+                                                    C.c_int, C.POINTER(_u32p), C.POINTER(_u32p),
+                                                    C.POINTER(_f32p)]
+        _orc.orc_generate_random_dense.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _f32p]
+        _orc.orc_mebcrs_row_pointers.restype = C.c_int64
+        _orc.orc_mebcrs_row_pointers.argtypes = [C.c_uint64, _u32p, _u32p, _u32p]
+        _orc.orc_mebcrs_fill.argtypes = [C.c_uint64, _u32p, _u32p, _f32p, C.c_uint32, _u32p, _u32p, _f32p]
+        _orc.orc_mebcrs_to_dense.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, _u32p, _u32p, _f32p, _f32p]
+        _orc.orc_spmm.argtypes = [C.c_uint64, C.c_uint32, C.c_int, _u32p, _u32p, _f32p, _f32p,
+                                  C.c_uint64, C.c_uint64, _f32p, C.c_uint64, C.c_int]
+        _orc.orc_sddmm.argtypes = [C.c_uint64, C.c_uint32, C.c_int, _u32p, _u32p, _f32p, _f32p,
+                                   C.c_uint64, _f32p, C.c_uint64, C.c_uint64, _f32p]
+        _orc.orc_count_mma_spmm.restype = C.c_uint64
+        _orc.orc_count_mma_spmm.argtypes = [C.c_uint64, _u32p, C.c_uint32, C.c_uint64]
+        _orc.orc_count_mma_sddmm.restype = C.c_uint64
+        _orc.orc_count_mma_sddmm.argtypes = [C.c_uint64, _u32p, C.c_uint32, C.c_uint64]
+        _orc.orc_num_threads.restype = C.c_int
+        _orc.orc_mt19937.argtypes = [C.c_uint32, C.c_uint64, _u32p]
+        _orc.orc_free.argtypes = [C.c_void_p]
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(os.path.join(_HERE, "_ref", "libtcsref.so"))
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        _ref = _load(os.path.join("_ref", "libtcsref.so"))
+        _ref.ref_round_fp16.restype = C.c_float
+        _ref.ref_round_fp16.argtypes = [C.c_float]
+        _ref.ref_round_tf32.restype = C.c_float
+        _ref.ref_round_tf32.argtypes = [C.c_float]
+        _ref.ref_generate_random_sparse.restype = C.c_int64
+        _ref.ref_generate_random_sparse.argtypes = [C.c_uint64, C.c_uint64, C.c_double, C.c_uint64,
+                                                    C.c_int, C.POINTER(_u32p), C.POINTER(_u32p),
+                                                    C.POINTER(_f32p)]
+        _ref.ref_generate_random_dense.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _f32p]
+        _ref.ref_encode_mebcrs.restype = C.c_int64
+        _ref.ref_encode_mebcrs.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_int,
+                                           C.POINTER(_u32p), C.POINTER(_u32p), C.POINTER(_f32p)]
+        _ref.ref_decode_mebcrs.restype = C.c_int64
+        _ref.ref_decode_mebcrs.argtypes = [C.c_uint64, C.c_uint64, C.c_int, _u32p, _u32p, _f32p,
+                                           C.POINTER(_u32p), C.POINTER(_u32p), C.POINTER(_f32p)]
+        _ref.ref_spmm.restype = C.c_int
+        _ref.ref_spmm.argtypes = [C.c_uint64, C.c_uint64, C.c_int, _u32p, _u32p, _f32p, _f32p,
+                                  C.c_uint64, C.c_uint64, C.c_int, C.c_uint64, C.c_int, _f32p, _u64p]
+        _ref.ref_sddmm.restype = C.c_int
+        _ref.ref_sddmm.argtypes = [C.c_uint64, C.c_uint64, C.c_int, _u32p, _u32p, _f32p, _f32p,
+                                   C.c_uint64, _f32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                                   _f32p, _u64p]
+        _ref.ref_sddmm_output_offsets.restype = C.c_uint64
+        _ref.ref_sddmm_output_offsets.argtypes = [C.c_uint64, C.c_int]
+        _ref.ref_free.argtypes = [C.c_void_p]
+    return _ref
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def _take(lib_, ptr, n, dtype):
+    out = np.ctypeslib.as_array(ptr, shape=(max(n, 1),))[:n].astype(dtype, copy=True)
+    lib_free = lib_.orc_free if hasattr(lib_, "orc_free") else lib_.ref_free
+    lib_free(C.cast(ptr, C.c_void_p))
+    return out
+
+
+class Csr:
+    """CSR matrix (inc/matrix.hpp:20-49): u32 row_ptr / col_idx, f32 values."""
+
+    def __init__(self, rows, cols, row_ptr, col_idx, values):
+        self.rows, self.cols = int(rows), int(cols)
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.uint32)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.uint32)
+        self.values = np.ascontiguousarray(values, dtype=np.float32)
+
+    @property
+    def nnz(self):
+        return int(self.col_idx.shape[0])
+
+    def to_dense(self):
+        d = np.zeros((self.rows, self.cols), np.float32)
+        r = np.repeat(np.arange(self.rows), np.diff(self.row_ptr.astype(np.int64)))
+        d[r, self.col_idx] = self.values
+        return d
+
+    @staticmethod
+    def from_dense(d):
+        d = np.asarray(d, np.float32)
+        rows, cols = d.shape
+        r, c = np.nonzero(d)
+        rp = np.zeros(rows + 1, np.uint32)
+        np.cumsum(np.bincount(r, minlength=rows), out=rp[1:])
+        return Csr(rows, cols, rp, c.astype(np.uint32), d[r, c])
+
+    @staticmethod
+    def from_coords(rows, cols, coords):
+        """csr_from_coords (inc/matrix.hpp:100-128): duplicates summed, explicit zeros kept."""
+        acc = {}
+        for r, c, v in coords:
+            acc[(r, c)] = acc.get((r, c), np.float32(0)) + np.float32(v)
+        keys = sorted(acc)
+        rp = np.zeros(rows + 1, np.uint32)
+        for r, _ in keys:
+            rp[r + 1] += 1
+        rp = np.cumsum(rp).astype(np.uint32)
+        return Csr(rows, cols, rp, [c for _, c in keys], [acc[k] for k in keys])
+
+
+class MeBcrs:
+    """ME-BCRS (inc/mebcrs.hpp:23-78) with f32 values (reference storage)."""
+
+    def __init__(self, rows, cols, precision, row_pointers, column_indices, values):
+        self.rows, self.cols, self.precision = int(rows), int(cols), int(precision)
+        self.k = K_OF[self.precision]
+        self.row_pointers = np.ascontiguousarray(row_pointers, dtype=np.uint32)
+        self.column_indices = np.ascontiguousarray(column_indices, dtype=np.uint32)
+        self.values = np.ascontiguousarray(values, dtype=np.float32)
+
+    @property
+    def num_windows(self):
+        return self.row_pointers.shape[0] - 1
+
+    @property
+    def nv(self):
+        return int(self.column_indices.shape[0])
+
+
+# ---------------------------------------------------------------- restatement
+def generate_random_sparse(rows, cols, density, seed, real=False) -> Csr:
+    rp, ci, v = _u32p(), _u32p(), _f32p()
+    nnz = lib().orc_generate_random_sparse(rows, cols, density, seed, int(real),
+                                           C.byref(rp), C.byref(ci), C.byref(v))
+    if nnz < 0:
+        raise ValueError("ArgumentError: bad generator arguments")
+    o = lib()
+    return Csr(rows, cols, _take(o, rp, rows + 1, np.uint32), _take(o, ci, nnz, np.uint32),
+               _take(o, v, nnz, np.float32))
+
+
+def generate_random_dense(rows, cols, seed, real=False) -> np.ndarray:
+    out = np.empty((rows, cols), np.float32)
+    lib().orc_generate_random_dense(rows, cols, seed, int(real), _p(out, _f32p))
+    return out
+
+
+def encode_mebcrs(m: Csr, precision: int) -> MeBcrs:
+    W = (m.rows + 7) // 8
+    rp = np.empty(W + 1, np.uint32)
+    nv = lib().orc_mebcrs_row_pointers(m.rows, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(rp, _u32p))
+    ci = np.empty(max(nv, 1), np.uint32)
+    vals = np.empty(max(8 * nv, 1), np.float32)
+    lib().orc_mebcrs_fill(m.rows, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(m.values, _f32p),
+                          K_OF[precision], _p(rp, _u32p), _p(ci, _u32p), _p(vals, _f32p))
+    return MeBcrs(m.rows, m.cols, precision, rp, ci[:nv], vals[:8 * nv])
+
+
+def mebcrs_to_dense(me: MeBcrs) -> np.ndarray:
+    d = np.empty((me.rows, me.cols), np.float32)
+    lib().orc_mebcrs_to_dense(me.rows, me.cols, me.k, _p(me.row_pointers, _u32p),
+                              _p(me.column_indices, _u32p), _p(me.values, _f32p), _p(d, _f32p))
+    return d
+
+
+def spmm(me: MeBcrs, B: np.ndarray, strict=False) -> np.ndarray:
+    B = np.ascontiguousarray(B, np.float32)
+    N = B.shape[1]
+    Cm = np.zeros((me.rows, N), np.float32)
+    lib().orc_spmm(me.rows, me.k, me.precision, _p(me.row_pointers, _u32p), _p(me.column_indices, _u32p),
+                   _p(me.values, _f32p), _p(B, _f32p), N, N, _p(Cm, _f32p), N, int(strict))
+    return Cm
+
+
+def sddmm(mask: MeBcrs, A: np.ndarray, Bt: np.ndarray) -> np.ndarray:
+    A = np.ascontiguousarray(A, np.float32)
+    Bt = np.ascontiguousarray(Bt, np.float32)
+    F = A.shape[1]
+    out = np.zeros(max(8 * mask.nv, 1), np.float32)
+    lib().orc_sddmm(mask.rows, mask.k, mask.precision, _p(mask.row_pointers, _u32p),
+                    _p(mask.column_indices, _u32p), _p(mask.values, _f32p), _p(A, _f32p), F,
+                    _p(Bt, _f32p), F, F, _p(out, _f32p))
+    return out[:8 * mask.nv]
+
+
+def count_mma_spmm(me: MeBcrs, N: int) -> int:
+    return int(lib().orc_count_mma_spmm(me.num_windows, _p(me.row_pointers, _u32p), me.k, N))
+
+
+def count_mma_sddmm(me: MeBcrs, F: int) -> int:
+    return int(lib().orc_count_mma_sddmm(me.num_windows, _p(me.row_pointers, _u32p), me.k, F))
+
+
+def mt19937(seed: int, n: int) -> np.ndarray:
+    out = np.empty(n, np.uint32)
+    lib().orc_mt19937(seed, n, _p(out, _u32p))
+    return out
+
+
+class Mt:
+    """Sequential std::mt19937 stream (replays reference tests' draw order)."""
+
+    def __init__(self, seed):
+        self.seed, self.n = seed, 0
+        self.buf = mt19937(seed, 1 << 16)
+
+    def __call__(self):
+        if self.n == self.buf.shape[0]:
+            self.buf = mt19937(self.seed, 2 * self.buf.shape[0])
+        v = int(self.buf[self.n])
+        self.n += 1
+        return v
+
+
+def round_fp16(x: float) -> float:
+    return lib().orc_round_fp16(x)
+
+
+def round_tf32(x: float) -> float:
+    return lib().orc_round_tf32(x)
+
+
+# ------------------------------------------------------ the reference itself
+class Ref:
+    """The unmodified reference (oracle/_ref/libtcsref.so)."""
+
+    @staticmethod
+    def generate_random_sparse(rows, cols, density, seed, real=False) -> Csr:
+        r = ref()
+        rp, ci, v = _u32p(), _u32p(), _f32p()
+        nnz = r.ref_generate_random_sparse(rows, cols, density, seed, int(real),
+                                           C.byref(rp), C.byref(ci), C.byref(v))
+        if nnz < 0:
+            raise ValueError("ArgumentError")
+        return Csr(rows, cols, _take(r, rp, rows + 1, np.uint32), _take(r, ci, nnz, np.uint32),
+                   _take(r, v, nnz, np.float32))
+
+    @staticmethod
+    def generate_random_dense(rows, cols, seed, real=False):
+        out = np.empty((rows, cols), np.float32)
+        ref().ref_generate_random_dense(rows, cols, seed, int(real), _p(out, _f32p))
+        return out
+
+    @staticmethod
+    def encode_mebcrs(m: Csr, precision: int) -> MeBcrs:
+        r = ref()
+        rp, ci, v = _u32p(), _u32p(), _f32p()
+        nv = r.ref_encode_mebcrs(m.rows, m.cols, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p),
+                                 _p(m.values, _f32p), precision, C.byref(rp), C.byref(ci), C.byref(v))
+        if nv < 0:
+            raise ValueError("encode failed")
+        W = (m.rows + 7) // 8
+        return MeBcrs(m.rows, m.cols, precision, _take(r, rp, W + 1, np.uint32),
+                      _take(r, ci, nv, np.uint32), _take(r, v, 8 * nv, np.float32))
+
+    @staticmethod
+    def decode_mebcrs(me: MeBcrs) -> Csr:
+        r = ref()
+        rp, ci, v = _u32p(), _u32p(), _f32p()
+        nnz = r.ref_decode_mebcrs(me.rows, me.cols, me.precision, _p(me.row_pointers, _u32p),
+                                  _p(me.column_indices, _u32p), _p(me.values, _f32p),
+                                  C.byref(rp), C.byref(ci), C.byref(v))
+        if nnz < 0:
+            raise ValueError("FormatError")
+        return Csr(me.rows, me.cols, _take(r, rp, me.rows + 1, np.uint32), _take(r, ci, nnz, np.uint32),
+                   _take(r, v, nnz, np.float32))
+
+    @staticmethod
+    def spmm(me: MeBcrs, B, mapping=1, cfg_precision=None, vector_height=8):
+        B = np.ascontiguousarray(B, np.float32)
+        Cm = np.zeros((me.rows, B.shape[1]), np.float32)
+        cnt = C.c_uint64(0)
+        rc = ref().ref_spmm(me.rows, me.cols, me.precision, _p(me.row_pointers, _u32p),
+                            _p(me.column_indices, _u32p), _p(me.values, _f32p), _p(B, _f32p),
+                            B.shape[0], B.shape[1],
+                            me.precision if cfg_precision is None else cfg_precision,
+                            vector_height, mapping, _p(Cm, _f32p), C.byref(cnt))
+        if rc:
+            raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
+        return Cm, int(cnt.value)
+
+    @staticmethod
+    def sddmm(mask: MeBcrs, A, Bt, cfg_precision=None):
+        A = np.ascontiguousarray(A, np.float32)
+        Bt = np.ascontiguousarray(Bt, np.float32)
+        out = np.zeros(max(8 * mask.nv, 1), np.float32)
+        cnt = C.c_uint64(0)
+        rc = ref().ref_sddmm(mask.rows, mask.cols, mask.precision, _p(mask.row_pointers, _u32p),
+                             _p(mask.column_indices, _u32p), _p(mask.values, _f32p), _p(A, _f32p),
+                             A.shape[0], _p(Bt, _f32p), Bt.shape[0], A.shape[1], Bt.shape[1],
+                             mask.precision if cfg_precision is None else cfg_precision,
+                             _p(out, _f32p), C.byref(cnt))
+        if rc:
+            raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
+        return out[:8 * mask.nv], int(cnt.value)
+
+    @staticmethod
+    def sddmm_output_offsets(lane, kind):
+        return int(ref().ref_sddmm_output_offsets(lane, kind))
+
+    @staticmethod
+    def round_fp16(x):
+        return ref().ref_round_fp16(x)
+
+    @staticmethod
+    def round_tf32(x):
+        return ref().ref_round_tf32(x)

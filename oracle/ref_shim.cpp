@@ -1,0 +1,172 @@
+// ============================================================================
+// TEST INFRASTRUCTURE ONLY -- C-ABI shim over the *unmodified* reference
+// headers (/root/reference/proj/include/tcsparse).  oracle/Makefile compiles
+// this file against the reference sources where they lie and writes the
+// result to oracle/_ref/libtcsref.so (git-ignored; it travels to the GPU box
+// as a prebuilt file).  It is used to (1) generate the golden vectors under
+// tests/golden/, (2) pin the restatement in oracle/oracle.cpp, and (3) time
+// the reference's own CPU path in bench.py (--impl reference / cpu_baseline).
+// No reference source is copied into this repository.
+// ============================================================================
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "tcsparse/tcsparse.hpp"
+
+using namespace tcsparse;
+
+namespace {
+
+template <typename T>
+T* dup(const std::vector<T>& v) {
+    T* p = static_cast<T*>(std::malloc(sizeof(T) * (v.empty() ? 1 : v.size())));
+    if (!v.empty()) std::memcpy(p, v.data(), sizeof(T) * v.size());
+    return p;
+}
+
+CsrMatrix make_csr(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci,
+                   const float* vals) {
+    CsrMatrix m;
+    m.rows = rows;
+    m.cols = cols;
+    m.row_ptr.assign(rp, rp + rows + 1);
+    const uint64_t nnz = rp[rows];
+    m.col_idx.assign(ci, ci + nnz);
+    m.values.assign(vals, vals + nnz);
+    return m;
+}
+
+MeBcrsMatrix make_me(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp,
+                     const uint32_t* ci, const float* vals) {
+    MeBcrsMatrix me;
+    const Precision p = static_cast<Precision>(precision);
+    const MmaShape s = shape_for(p);
+    me.rows = rows;
+    me.cols = cols;
+    me.vector_height = s.n;
+    me.k = s.k;
+    me.precision = p;
+    const uint64_t W = (rows + 7) / 8;
+    me.row_pointers.assign(rp, rp + W + 1);
+    const uint64_t nv = rp[W];
+    me.column_indices.assign(ci, ci + nv);
+    me.values.assign(vals, vals + 8 * nv);
+    return me;
+}
+
+}  // namespace
+
+extern "C" {
+
+void ref_free(void* p) { std::free(p); }
+float ref_round_fp16(float x) { return round_to_fp16(x); }
+float ref_round_tf32(float x) { return round_to_tf32(x); }
+
+int64_t ref_generate_random_sparse(uint64_t rows, uint64_t cols, double density, uint64_t seed,
+                                   int real, uint32_t** rp, uint32_t** ci, float** vals) {
+    try {
+        const CsrMatrix m = real ? generate_random_sparse_real(rows, cols, density, seed)
+                                 : generate_random_sparse(rows, cols, density, seed);
+        *rp = dup(m.row_ptr);
+        *ci = dup(m.col_idx);
+        *vals = dup(m.values);
+        return static_cast<int64_t>(m.nnz());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+void ref_generate_random_dense(uint64_t rows, uint64_t cols, uint64_t seed, int real, float* out) {
+    const DenseMatrix d = real ? generate_random_dense_real(rows, cols, seed)
+                               : generate_random_dense(rows, cols, seed);
+    std::memcpy(out, d.data.data(), sizeof(float) * d.data.size());
+}
+
+// encode_mebcrs (inc/mebcrs.hpp:80). Returns nv, or -1 on error.
+int64_t ref_encode_mebcrs(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci,
+                          const float* vals, int precision, uint32_t** out_rp, uint32_t** out_ci,
+                          float** out_vals) {
+    try {
+        const MeBcrsMatrix me = encode_mebcrs(make_csr(rows, cols, rp, ci, vals),
+                                              static_cast<Precision>(precision));
+        *out_rp = dup(me.row_pointers);
+        *out_ci = dup(me.column_indices);
+        *out_vals = dup(me.values);
+        return static_cast<int64_t>(me.column_indices.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// decode_mebcrs (inc/mebcrs.hpp:118). Returns nnz, or -1 (FormatError).
+int64_t ref_decode_mebcrs(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp,
+                          const uint32_t* ci, const float* vals, uint32_t** out_rp,
+                          uint32_t** out_ci, float** out_vals) {
+    try {
+        const CsrMatrix m = decode_mebcrs(make_me(rows, cols, precision, rp, ci, vals));
+        *out_rp = dup(m.row_ptr);
+        *out_ci = dup(m.col_idx);
+        *out_vals = dup(m.values);
+        return static_cast<int64_t>(m.nnz());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// spmm(MeBcrsMatrix) (inc/spmm.hpp:173). C is rows x N. Returns 0, or
+// 1 = ArgumentError, 2 = ShapeError, 3 = other.
+int ref_spmm(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp, const uint32_t* ci,
+             const float* vals, const float* B, uint64_t b_rows, uint64_t N, int cfg_precision,
+             uint64_t vector_height, int mapping, float* C, uint64_t* mma_invocations) {
+    try {
+        DenseMatrix b(b_rows, N);
+        std::memcpy(b.data.data(), B, sizeof(float) * b_rows * N);
+        const KernelConfig cfg{static_cast<Precision>(cfg_precision), vector_height,
+                               static_cast<ThreadMapping>(mapping)};
+        const SpmmResult res = spmm(make_me(rows, cols, precision, rp, ci, vals), b, cfg);
+        std::memcpy(C, res.output.data.data(), sizeof(float) * rows * N);
+        if (mma_invocations) *mma_invocations = res.counters.mma_invocations;
+        return 0;
+    } catch (const ArgumentError&) {
+        return 1;
+    } catch (const ShapeError&) {
+        return 2;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+// sddmm (inc/sddmm.hpp:84). out_vals has 8*nv floats.
+int ref_sddmm(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp, const uint32_t* ci,
+              const float* mask_vals, const float* A, uint64_t a_rows, const float* Bt,
+              uint64_t bt_rows, uint64_t F_a, uint64_t F_b, int cfg_precision, float* out_vals,
+              uint64_t* mma_invocations) {
+    try {
+        SddmmOperands ops;
+        ops.mask = make_me(rows, cols, precision, rp, ci, mask_vals);
+        ops.a = DenseMatrix(a_rows, F_a);
+        std::memcpy(ops.a.data.data(), A, sizeof(float) * a_rows * F_a);
+        ops.b_t = DenseMatrix(bt_rows, F_b);
+        std::memcpy(ops.b_t.data.data(), Bt, sizeof(float) * bt_rows * F_b);
+        const KernelConfig cfg{static_cast<Precision>(cfg_precision), 8, ThreadMapping::coalesced};
+        const SddmmResult res = sddmm(ops, cfg);
+        std::memcpy(out_vals, res.output.values.data(), sizeof(float) * res.output.values.size());
+        if (mma_invocations) *mma_invocations = res.counters.mma_invocations;
+        return 0;
+    } catch (const ArgumentError&) {
+        return 1;
+    } catch (const ShapeError&) {
+        return 2;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
+uint64_t ref_sddmm_output_offsets(uint64_t lane, int kind) {
+    return sddmm_output_offsets(lane, kind == 0 ? SubBlockKind::b8x8 : SubBlockKind::b8x4);
+}
+
+}  // extern "C"
