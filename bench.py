@@ -1,0 +1,446 @@
+#!/usr/bin/env python
+"""FlashSparse-on-B200 benchmark (BASELINE.json metric: effective GFLOP/s =
+2*nnz*N / t, plus the HBM-roofline fraction).
+
+Workload (BASELINE.json configs[2], the north star's target): SpMM FP16,
+N = 128, on a Reddit-shaped synthetic power-law graph (Chung-Lu, 232,965
+nodes, ~115 M nnz, uniform [-1,1) values, seeded) -- generated on the GPU,
+converted CSR -> ME-BCRS once on the GPU (timed separately as encode_ms).
+One step = one SpMM over the resident ME-BCRS and dense B (the hot path).
+L2 is flushed (256 MB write) before every timed step.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+N > 1 (torchrun, one rank per GPU): row windows are sharded into contiguous
+ranges balanced by nnz; B is broadcast once over NCCL (timed separately);
+each rank runs its shard; the step time is the max over ranks (strong
+scaling of one graph).  --impl reference times the reference's own CPU
+implementation (oracle/_ref: the unmodified reference headers) on bounded
+samples of the same workload, on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SpMM/SDDMM effective GFLOP/s (2·nnz·N) and % HBM roofline at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=100)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--n", type=int, default=128)
+    p.add_argument("--precision", default="fp16", choices=["fp16", "tf32"])
+    p.add_argument("--workload", default="c3", choices=["c3", "c1"])
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample budget")
+    p.add_argument("--quick", action="store_true", help="kernel timing only (for ncu runs)")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "50", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, f[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def shard_windows(row_ptr: torch.Tensor, rows: int, rank: int, world: int):
+    """Contiguous window range [w0, w1) of `rank`, cut at nnz quantiles."""
+    W = (rows + 7) // 8
+    starts = row_ptr[torch.clamp(torch.arange(W + 1, device=row_ptr.device) * 8, max=rows)].to(torch.int64)
+    total = int(starts[-1])
+    cuts = [0] + [int(torch.searchsorted(starts, total * r // world)) for r in range(1, world)] + [W]
+    return cuts[rank], cuts[rank + 1]
+
+
+def bytes_alg_spmm(W, nv, rows, N, vwA, vwB):
+    """row pointers + column indices + sparse values (no padding)
+    + one N-wide dense row per stored vector + the fp32 C write."""
+    return 4 * (W + 1) + 4 * nv + 8 * nv * vwA + nv * N * vwB + 4 * rows * N
+
+
+# --------------------------------------------------------------- workloads
+def build_graph(args, device):
+    from paper_2412_11007_b200 import graphs as G
+
+    if args.workload == "c3":
+        rows, cols, rp, ci, v = G.power_law_csr(G.C3_REDDIT, values="real", device=device)
+        desc = "C3 SpMM on Reddit-shaped synthetic power-law graph (Chung-Lu alpha=1.2, hub cap 60x mean)"
+    else:
+        rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real", device=device)
+        desc = "C1 SpMM on uniform-random 4096x4096 (16 nnz/row)"
+    return rows, cols, rp, ci, v, desc
+
+
+# ---------------------------------------------------------------- ours
+def run_ours(args, rank, world, device):
+    import paper_2412_11007_b200.tcsparse as T
+    from paper_2412_11007_b200 import _abi, graphs as G
+
+    prec = T.Precision.fp16 if args.precision == "fp16" else T.Precision.tf32
+    N = args.n
+    rows, cols, rp, ci, v, desc = build_graph(args, device)
+    nnz_total = int(ci.numel())
+    w0, w1 = shard_windows(rp, rows, rank, world)
+    r0, r1 = 8 * w0, min(8 * w1, rows)
+    lrp, lci, lv = G.row_slice(rp, ci, v, r0, r1)
+    l_rows = r1 - r0
+    local_csr = T.CsrMatrix(l_rows, cols, lrp.contiguous(), lci.contiguous(), lv.contiguous())
+    del rp, ci, v
+
+    # dense operand: generated on rank 0, broadcast over NCCL (timed separately)
+    dt = torch.float16 if prec == T.Precision.fp16 else torch.float32
+    B = G.dense(cols, N, 3, values="real", dtype=dt, device=device) if rank == 0 else \
+        torch.empty(cols, N, dtype=dt, device=device)
+    bcast_ms = 0.0
+    if world > 1:
+        torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.distributed.broadcast(B, src=0)
+        e1.record()
+        torch.cuda.synchronize()
+        bcast_ms = e0.elapsed_time(e1)
+
+    # CSR -> ME-BCRS on the GPU (timed once, after one warm-up conversion)
+    me = T.encode_mebcrs(local_csr, prec)
+    me.free()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    me = T.encode_mebcrs(local_csr, prec)
+    e1.record()
+    torch.cuda.synchronize()
+    encode_ms = e0.elapsed_time(e1)
+    nv, W = me.num_vectors, me.num_windows
+    nnz_local = local_csr.nnz
+
+    out = torch.empty(l_rows, N, dtype=torch.float32, device=device)
+    cfg = T.KernelConfig(prec)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=device)  # 256 MB > 126 MB L2
+    for _ in range(args.warmup):
+        flush.zero_()
+        T.spmm(me, B, cfg, out=out)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    sampler = ClockSampler(device.index if device.index is not None else 0)
+    sampler.start()
+    time.sleep(0.15)
+    l0 = T.launch_count()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for a, b in evs:
+        flush.zero_()
+        a.record()
+        T.spmm(me, B, cfg, out=out)
+        b.record()
+    torch.cuda.synchronize()
+    launches = T.launch_count() - l0
+    clocks = sampler.stop()
+    times = [a.elapsed_time(b) for a, b in evs]
+    step_ms = sum(times) / len(times)
+    t = torch.tensor([step_ms], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.barrier()
+    step_ms_max = float(t.item())
+
+    # back-to-back (no flush) for reference
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        T.spmm(me, B, cfg, out=out)
+    b.record()
+    torch.cuda.synchronize()
+    b2b_ms = a.elapsed_time(b) / 10
+
+    vwA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
+    vwB = 2 if dt == torch.float16 else 4
+    balg = bytes_alg_spmm(W, nv, l_rows, N, vwA, vwB)
+    bmin = 4 * (W + 1) + 4 * nv + 8 * nv * vwA + cols * N * vwB + 4 * l_rows * N
+    peak, peak_src = peaks()
+    achieved = balg / (step_ms / 1e3) / 1e9
+
+    e2e = None
+    if not args.quick:
+        e2e = run_e2e(args, T, _abi, local_csr, B, l_rows, cols, N, prec, device, world)
+
+    res = {"rank": rank, "nnz": nnz_local, "nv": nv, "W": W, "step_ms": step_ms, "encode_ms": encode_ms,
+           "bytes_alg": balg, "bytes_min": bmin, "achieved": achieved}
+    gathered = [res]
+    if world > 1:
+        gathered = [None] * world
+        torch.distributed.all_gather_object(gathered, res)
+    if rank != 0:
+        return None
+    value = 2.0 * nnz_total * N / (step_ms_max / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        key = f"{args.workload}_{args.precision}_n{N}_g{world}"
+        traffic = tj.get(key)
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(step_ms_max, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+        "config": {"workload": desc + f", {args.precision.upper()} N={N}", "nodes": rows, "nnz": nnz_total,
+                   "nv_8x1": sum(g["nv"] for g in gathered), "N": N, "precision": args.precision,
+                   "values": "uniform [-1,1) (seeded)", "l2": "flushed before every timed step (256 MB write)",
+                   "parallelism": f"row-window shards x{world} (nnz-balanced), B broadcast over NCCL"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
+                     "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
+                     "kernel": "spmm_f16_kernel<2,8> (+ spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
+        "back_to_back_ms": round(b2b_ms, 4),
+        "broadcast_ms": round(bcast_ms, 3),
+        "shards": [{"nnz": g["nnz"], "nv": g["nv"], "step_ms": round(g["step_ms"], 4)} for g in gathered],
+    }
+    if e2e:
+        line["e2e"] = e2e
+    return line
+
+
+def run_e2e(args, T, _abi, local_csr, B, rows, cols, N, prec, device, world):
+    """Same metric through the reference-facing C-ABI call with HOST buffers:
+    tcs_spmm_csr_host (ref CLI pipeline: encode_mebcrs + spmm) -- H2D of the
+    CSR and f32 B, GPU conversion, SpMM, D2H of C, every step."""
+    lib = _abi.load()
+    rp = local_csr.row_ptr.cpu().pin_memory()
+    ci = local_csr.col_idx.cpu().pin_memory()
+    vals = local_csr.values.cpu().pin_memory()
+    Bh = B.float().cpu().pin_memory()
+    Ch = torch.empty(rows, N, dtype=torch.float32).pin_memory()
+    csr = _abi.tcs_csr(rows, cols, local_csr.nnz, rp.data_ptr(), ci.data_ptr(), vals.data_ptr())
+    cfg = _abi.tcs_kernel_config(int(prec), 8, 1, 0)
+    stream = torch.cuda.current_stream()
+    sp = C.c_void_p(stream.cuda_stream)
+    rc = lib.tcs_spmm_csr_host(C.byref(csr), int(prec), Bh.data_ptr(), N, Ch.data_ptr(), C.byref(cfg), None, sp)
+    assert rc == 0, lib.tcs_last_error()
+    times = []
+    for _ in range(args.e2e_steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        rc = lib.tcs_spmm_csr_host(C.byref(csr), int(prec), Bh.data_ptr(), N, Ch.data_ptr(), C.byref(cfg), None, sp)
+        b.record(stream)
+        torch.cuda.synchronize()
+        assert rc == 0, lib.tcs_last_error()
+        times.append(a.elapsed_time(b))
+    ms = sum(times) / len(times)
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    nnz = torch.tensor([local_csr.nnz], dtype=torch.float64, device=device)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(nnz)
+    h2d = (rows + 1) * 4 + local_csr.nnz * 8 + cols * N * 4
+    d2h = rows * N * 4
+    return {"value": round(2.0 * float(nnz.item()) * N / (float(t.item()) / 1e3) / 1e9, 2), "unit": "GFLOP/s",
+            "ms_per_step": round(float(t.item()), 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "call": "tcs_spmm_csr_host (host CSR + host f32 B -> host f32 C; GPU encode + SpMM)"}
+
+
+# ----------------------------------------------------------- reference arm
+def reference_sample_runner(args, device):
+    """Returns (run_step(budget_s) -> (flops, seconds, nnz), description,
+    threads).  Each step: the reference's encode_mebcrs + spmm
+    (oracle/_ref = the unmodified reference headers) over disjoint 64-row
+    slices (8 windows) of the workload, one slice per host thread."""
+    import oracle as O
+    from paper_2412_11007_b200 import graphs as G
+
+    rows, cols, rp, ci, v, _ = build_graph(args, device)
+    N = args.n
+    rp_h = rp.cpu().numpy().view(np.uint32)
+    ci_h = ci.cpu().numpy().view(np.uint32)
+    v_h = v.cpu().numpy()
+    dt = torch.float16 if args.precision == "fp16" else torch.float32
+    Bh = np.ascontiguousarray(G.dense(cols, N, 3, values="real", dtype=dt, device=device).float().cpu().numpy())
+    del rp, ci, v
+    threads = max(1, min(os.cpu_count() or 1, 32))
+    prec = 0 if args.precision == "fp16" else 1
+    lib = O.ref()
+    nslices = (rows + 63) // 64
+    stride = max(1, nslices // 997)  # spread slices over the whole graph
+    state = {"next": 0}
+    lock = threading.Lock()
+
+    def one_slice(idx):
+        r0 = (idx * stride % nslices) * 64
+        r1 = min(rows, r0 + 64)
+        b, e = int(rp_h[r0]), int(rp_h[r1])
+        srp = (rp_h[r0:r1 + 1] - rp_h[r0]).astype(np.uint32)
+        sci = np.ascontiguousarray(ci_h[b:e])
+        sv = np.ascontiguousarray(v_h[b:e])
+        up = O._u32p
+        orp, oci, ov = up(), up(), O._f32p()
+        nv = lib.ref_encode_mebcrs(r1 - r0, cols, srp.ctypes.data_as(up), sci.ctypes.data_as(up),
+                                   sv.ctypes.data_as(O._f32p), prec, C.byref(orp), C.byref(oci), C.byref(ov))
+        Cm = np.empty((r1 - r0, N), np.float32)
+        cnt = C.c_uint64(0)
+        rc = lib.ref_spmm(r1 - r0, cols, prec, orp, oci, ov, Bh.ctypes.data_as(O._f32p), cols, N, prec, 8, 1,
+                          Cm.ctypes.data_as(O._f32p), C.byref(cnt))
+        for p in (orp, oci, ov):
+            lib.ref_free(C.cast(p, C.c_void_p))
+        assert nv >= 0 and rc == 0
+        return e - b
+
+    def run_step(budget_s):
+        done = {"nnz": 0}
+        t0 = time.perf_counter()
+
+        def worker():
+            while time.perf_counter() - t0 < budget_s:
+                with lock:
+                    idx = state["next"]
+                    state["next"] += 1
+                n = one_slice(idx)
+                with lock:
+                    done["nnz"] += n
+
+        ths = [threading.Thread(target=worker) for _ in range(threads)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        secs = time.perf_counter() - t0
+        return 2.0 * done["nnz"] * N, secs, done["nnz"]
+
+    desc = (f"reference encode_mebcrs+spmm (oracle/_ref, -O3, unmodified headers) on 64-row slices "
+            f"(8 windows) spread over the graph, {threads} threads")
+    return run_step, desc, threads
+
+
+def run_reference(args, rank, world, device):
+    if rank != 0:
+        return None
+    run_step, desc, threads = reference_sample_runner(args, device)
+    budget = max(0.5, min(4.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        run_step(budget)
+    flops = secs = 0.0
+    for _ in range(args.steps):
+        f, s, _ = run_step(budget)
+        flops += f
+        secs += s
+    value = flops / secs / 1e9
+    return {"impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 2),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": args.precision,
+            "data": "synthetic",
+            "config": {"workload": "C3 SpMM on Reddit-shaped synthetic power-law graph" if args.workload == "c3"
+                       else "C1 SpMM uniform 4096x4096", "N": args.n, "precision": args.precision},
+            "cpu_baseline": {"value": round(value, 5), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                             "sample": desc + f", {budget:.1f}s per step"},
+            "e2e": {"value": round(value, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def cpu_baseline(args, device):
+    run_step, desc, threads = reference_sample_runner(args, device)
+    run_step(1.0)
+    f, s, nnz = run_step(args.cpu_seconds)
+    return {"value": round(f / s / 1e9, 5), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+            "sample": desc + f", {s:.1f}s wall, {nnz} nnz"}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    if args.impl == "reference":
+        line = run_reference(args, rank, world, device)
+    else:
+        line = run_ours(args, rank, world, device)
+        if line is not None and world == 1 and not args.quick:
+            line["cpu_baseline"] = cpu_baseline(args, device)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

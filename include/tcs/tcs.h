@@ -1,0 +1,217 @@
+/*
+ * tcs.h -- C-ABI of the B200-native FlashSparse hot path
+ *          (CSR -> ME-BCRS conversion, SpMM, SDDMM; sm_100a).
+ *
+ * This is the drop-in boundary for the reference's C++ API in
+ * /root/reference/proj/include/tcsparse ("ref:" below).  Every entry point is
+ * extern "C", takes plain pointers and sizes, throws nothing, and reports
+ * errors through tcs_status plus a thread-local message (tcs_last_error).
+ * The status codes map one-to-one onto the reference's exception taxonomy
+ * (ref: errors.hpp:11-38); include/tcsparse/gpu.hpp rethrows them as those
+ * exact types.
+ *
+ * Device entry points (tcs_mebcrs_encode, tcs_spmm, tcs_sddmm) take DEVICE
+ * pointers and are stream-ordered: they enqueue work on `stream` and return.
+ * tcs_mebcrs_encode synchronises once (the output sizes are data dependent).
+ * The *_host entry points take HOST pointers (pinned for full bandwidth),
+ * copy, compute and copy back on `stream`, and synchronise before returning
+ * -- the value semantics of the reference API.
+ *
+ * There is no CPU fallback: without a CUDA device every call returns
+ * TCS_ERR_CUDA.
+ */
+#ifndef TCS_TCS_H_
+#define TCS_TCS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* tcs_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+/* ref: errors.hpp -- FormatError(:24), ShapeError(:30), ArgumentError(:36). */
+typedef enum tcs_status {
+    TCS_OK = 0,
+    TCS_ERR_ARGUMENT = 1, /* ref ArgumentError: bad precision / vector height / null pointer */
+    TCS_ERR_SHAPE = 2,    /* ref ShapeError: operand dimensions disagree               */
+    TCS_ERR_FORMAT = 3,   /* ref FormatError: ME-BCRS / CSR invariants violated         */
+    TCS_ERR_CUDA = 4,     /* CUDA runtime error (no device, launch failure, ...)        */
+    TCS_ERR_NCCL = 5,     /* reserved for the multi-GPU layer                           */
+    TCS_ERR_OOM = 6       /* device allocation failed                                   */
+} tcs_status;
+
+/* ref: precision.hpp:13 (Precision{fp16=0, tf32=1}). */
+typedef enum tcs_precision { TCS_FP16 = 0, TCS_TF32 = 1 } tcs_precision;
+
+/* Element type of a buffer. */
+typedef enum tcs_dtype { TCS_DTYPE_F16 = 0, TCS_DTYPE_F32 = 1 } tcs_dtype;
+
+/* ref: access_pattern.hpp:15 (ThreadMapping). No numerical effect
+ * (ref tests/acceptance.cpp:103-104); both run the coalesced kernel. */
+typedef enum tcs_mapping { TCS_MAP_DIRECT = 0, TCS_MAP_COALESCED = 1 } tcs_mapping;
+
+/* ref: matrix.hpp:20-49 (CsrMatrix). u32 indices, f32 values; column
+ * indices strictly ascending within a row; explicit zeros are entries. */
+typedef struct tcs_csr {
+    uint64_t rows;
+    uint64_t cols;
+    uint64_t nnz;
+    const uint32_t* row_ptr; /* rows+1 */
+    const uint32_t* col_idx; /* nnz    */
+    const float* values;     /* nnz    */
+} tcs_csr;
+
+/* ref: mebcrs.hpp:23-78 (MeBcrsMatrix).  Windows of 8 rows; vector v of
+ * window w (0-based, ascending column) sits in block b = v / k at
+ *   values[8 * (row_pointers[w] + b * k) + r * width_b + v % k],
+ *   width_b = min(k, nv_w - b * k)                 (ref mebcrs.hpp:46-56).
+ * value_dtype F16 stores RNE-rounded binary16 (bit-identical to the
+ * reference's round_to_fp16, applied by the reference at MMA time); F32
+ * stores the reference's raw binary32 values.  TF32 always uses F32. */
+typedef struct tcs_mebcrs {
+    uint64_t rows;
+    uint64_t cols;
+    uint32_t vector_height; /* 8 */
+    uint32_t k;             /* storage block width: 8 (FP16), 4 (TF32); ref mma.hpp:23 */
+    tcs_precision precision;
+    tcs_dtype value_dtype;
+    uint64_t num_windows;     /* ceil(rows / 8)                   */
+    uint64_t num_vectors;     /* nv = row_pointers[num_windows]   */
+    uint32_t* row_pointers;   /* device, num_windows + 1           */
+    uint32_t* column_indices; /* device, num_vectors               */
+    void* values;             /* device, 8 * num_vectors elements  */
+    uint32_t flags;           /* TCS_MEBCRS_OWN_* : which arrays tcs_mebcrs_free releases */
+    uint32_t max_window_vectors; /* filled by tcs_mebcrs_prepare      */
+    uint64_t num_blocks;         /* sum_w ceil(nv_w / k)              */
+    uint64_t num_groups16;       /* sum_w ceil(nv_w / 16)             */
+    void* plan;                  /* library-private work list; NULL until prepared */
+} tcs_mebcrs;
+
+#define TCS_MEBCRS_OWN_STRUCTURE 0x1u /* row_pointers + column_indices */
+#define TCS_MEBCRS_OWN_VALUES 0x2u
+
+/* ref: spmm.hpp:17-21 (KernelConfig). */
+typedef struct tcs_kernel_config {
+    tcs_precision precision;
+    uint32_t vector_height; /* must be 8 (ref spmm.hpp:106) */
+    tcs_mapping mapping;
+    uint32_t flags; /* TCS_CFG_* */
+} tcs_kernel_config;
+
+/* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
+ * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);
+ * the transaction fields belong to the reference's analytic cost model and
+ * are left 0 (coalescing is measured with ncu instead). */
+typedef struct tcs_counters {
+    uint64_t mma_invocations;
+    uint64_t transactions;
+    uint64_t transaction_bytes;
+    uint64_t useful_bytes;
+} tcs_counters;
+
+/* ------------------------------------------------------------------ misc */
+const char* tcs_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* tcs_last_error(void);
+/* Number of kernels this library has launched in this process (a monotone
+ * counter, used by benchmarks to report gpu_launches). */
+uint64_t tcs_launch_count(void);
+
+/* Diagnostics: applies, on the device, exactly the operand rounding the
+ * kernels use -- RNE to binary16 (__float2half_rn; ref round_to_fp16,
+ * precision.hpp:51-64) or RNE to TF32 (cvt.rn.tf32.f32; ref round_to_tf32,
+ * precision.hpp:42-46) -- and widens back to f32.  in/out are device arrays
+ * of n floats. */
+tcs_status tcs_round_values(tcs_precision precision, const float* in, float* out, uint64_t n, tcs_stream_t stream);
+
+/* ------------------------------------------------------------- conversion */
+/* ref: encode_mebcrs(const CsrMatrix&, Precision)  (mebcrs.hpp:80).
+ * Device CSR in; ME-BCRS out with library-allocated device arrays (release
+ * with tcs_mebcrs_free).  value_dtype: F16 or F32 for TCS_FP16, F32 for
+ * TCS_TF32.  row_pointers / column_indices are bit-identical to the
+ * reference's; values are bit-identical (F32) or equal to the reference's
+ * round_to_fp16 of them (F16).  Also prepares the SpMM/SDDMM work list. */
+tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
+                             tcs_mebcrs* out, tcs_stream_t stream);
+
+/* Builds (or rebuilds) the work list and the block/group counts for an
+ * ME-BCRS whose arrays were filled by the caller.  Synchronises. */
+tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream);
+
+/* Host-side structural checks of ref mebcrs.hpp:58-77 on device arrays
+ * (copies them back; test/debug use).  Returns TCS_ERR_FORMAT on violation. */
+tcs_status tcs_mebcrs_validate(const tcs_mebcrs* m, tcs_stream_t stream);
+
+/* Releases the arrays flagged as owned and the work list; zeroes *m. */
+tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream);
+
+/* ------------------------------------------------------------------- SpMM */
+/* ref: spmm(const MeBcrsMatrix&, const DenseMatrix&, const KernelConfig&)
+ * (spmm.hpp:173).  C[rows x n] (f32, row stride ldc) = A * B, B is
+ * [b_rows x n] with row stride ldb in b_dtype.  Errors as the reference:
+ * cfg->vector_height != 8 or cfg->precision != a->precision -> ARGUMENT;
+ * a->cols != b_rows -> SHAPE.  Empty windows produce zero rows.
+ * FP16 needs b_dtype F16 (or F32, converted with RNE into a workspace);
+ * TF32 needs F32 (rounded RNE to TF32 in-register). */
+tcs_status tcs_spmm(const tcs_mebcrs* a, const void* b, tcs_dtype b_dtype, int64_t ldb, int64_t b_rows,
+                    int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
+                    tcs_counters* counters, tcs_stream_t stream);
+
+/* ------------------------------------------------------------------ SDDMM */
+/* ref: sddmm(const SddmmOperands&, const KernelConfig&)  (sddmm.hpp:84).
+ * out.values[pos] = sum_l A[i][l] * Bt[j][l] at every mask position whose
+ * stored value is != 0; every other slot of the output blocks is 0.
+ * A is [a_rows x f_a] (row stride lda), Bt = B^T is [bt_rows x f_b]
+ * (row stride ldbt).  `out` receives the mask's structure (aliased, not
+ * owned) and values of out_dtype; if out->values is NULL they are
+ * library-allocated (owned).  Errors: cfg precision != mask precision ->
+ * ARGUMENT; a_rows != mask rows, bt_rows != mask cols, f_a != f_b -> SHAPE. */
+tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda, int64_t a_rows,
+                     int64_t f_a, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows,
+                     int64_t f_b, tcs_mebcrs* out, tcs_dtype out_dtype, const tcs_kernel_config* cfg,
+                     tcs_counters* counters, tcs_stream_t stream);
+
+/* ------------------------------------------------- host-buffer entry points */
+/* Value semantics of the reference API: host arrays in, host arrays out.  */
+
+/* Host CSR -> device ME-BCRS (then tcs_mebcrs_download for host arrays). */
+tcs_status tcs_mebcrs_encode_host(const tcs_csr* host_csr, tcs_precision precision, tcs_dtype value_dtype,
+                                  tcs_mebcrs* out, tcs_stream_t stream);
+/* Copies a device ME-BCRS into caller-sized host arrays (values widened to
+ * f32).  Any pointer may be NULL to skip that array.  Synchronises. */
+tcs_status tcs_mebcrs_download(const tcs_mebcrs* m, uint32_t* row_pointers, uint32_t* column_indices,
+                               float* values, tcs_stream_t stream);
+/* Host arrays -> device ME-BCRS (values uploaded as F32) + prepare. */
+tcs_status tcs_mebcrs_upload(uint64_t rows, uint64_t cols, tcs_precision precision,
+                             const uint32_t* row_pointers, const uint32_t* column_indices,
+                             const float* values, tcs_mebcrs* out, tcs_stream_t stream);
+
+/* ref spmm with host operands: A given by host ME-BCRS arrays (f32 values),
+ * B host f32 [b_rows x n], C host f32 [rows x n]. */
+tcs_status tcs_spmm_host(uint64_t rows, uint64_t cols, tcs_precision precision, const uint32_t* row_pointers,
+                         const uint32_t* column_indices, const float* values, const float* b, int64_t b_rows,
+                         int64_t n, float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
+                         tcs_stream_t stream);
+
+/* ref sddmm with host operands; out_values has 8 * nv floats. */
+tcs_status tcs_sddmm_host(uint64_t rows, uint64_t cols, tcs_precision precision, const uint32_t* row_pointers,
+                          const uint32_t* column_indices, const float* mask_values, const float* a,
+                          int64_t a_rows, int64_t f_a, const float* bt, int64_t bt_rows, int64_t f_b,
+                          float* out_values, const tcs_kernel_config* cfg, tcs_counters* counters,
+                          tcs_stream_t stream);
+
+/* The reference CLI's spmm pipeline (ref cli.hpp:162-200: encode_mebcrs
+ * then spmm) from host buffers: host CSR + host f32 B -> host f32 C.  H2D,
+ * GPU conversion, SpMM and D2H all run on `stream`. */
+tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision precision, const float* b, int64_t n,
+                             float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
+                             tcs_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TCS_TCS_H_ */

@@ -71,6 +71,7 @@ def lib():
         _orc.orc_count_mma_sddmm.argtypes = [C.c_uint64, _u32p, C.c_uint32, C.c_uint64]
         _orc.orc_num_threads.restype = C.c_int
         _orc.orc_mt19937.argtypes = [C.c_uint32, C.c_uint64, _u32p]
+        _orc.orc_round_array.argtypes = [C.c_int, _f32p, _f32p, C.c_uint64]
         _orc.orc_free.argtypes = [C.c_void_p]
     return _orc
 
@@ -266,6 +267,13 @@ class Mt:
         v = int(self.buf[self.n])
         self.n += 1
         return v
+
+
+def round_array(x: np.ndarray, precision: int) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty_like(x)
+    lib().orc_round_array(precision, _p(x, _f32p), _p(out, _f32p), x.size)
+    return out
 
 
 def round_fp16(x: float) -> float:

@@ -80,6 +80,12 @@ float orc_round_tf32(float x) { return rnd_tf32(x); }
 
 void orc_free(void* p) { std::free(p); }
 
+// Vectorised round_to_precision (inc/precision.hpp:66-68).
+void orc_round_array(int precision, const float* in, float* out, uint64_t n) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < static_cast<int64_t>(n); ++i) out[i] = rnd(in[i], precision);
+}
+
 // generate_random_sparse / _real (generate.hpp:29-59).  Returns nnz; the
 // three arrays are malloc'd and released with orc_free.  Returns -1 on an
 // argument error (the reference throws ArgumentError).

@@ -1,0 +1,354 @@
+// SDDMM over the ME-BCRS mask with the same 8x1 granularity
+// (ref sddmm.hpp:84-136, paper §3.4):
+//
+//   acc^T (16 vectors x 8 window rows) += Bt_gathered (16 vectors x K)
+//                                         * A_window^T (K x 8 rows)
+//
+// i.e. the sampled B columns are the m=16 operand and the window's 8 A rows
+// the n=8 operand -- the orientation of ref sddmm.hpp:107-120.  One warp owns
+// one work item (<= plan.seg vectors of one window); each group of 16
+// consecutive vectors (ref :104) is one accumulator tile.
+//
+// The inner (feature) dimension is permuted identically in both operands so
+// every lane reads 16 contiguous bytes per gathered row (FP16: features
+// 8t..8t+7 feed two m16n8k16 MMAs; TF32: 4t..4t+3 feed two m16n8k8 MMAs).
+// Features are zero-padded (0*0 adds exactly 0, as the reference's padded
+// K tiles, ref :110-118).
+//
+// Write-back follows Algorithm 1 (ref sddmm.hpp:28-63): accumulator element
+// (vector v, row r) lands at 8*(rp[w]+b*k) + r*width_b + v%k, b = v/k; it is
+// written only where the mask's stored value is != 0 (ref :131) and every
+// other slot of the output blocks is 0.
+#include <algorithm>
+
+#include "tcs_internal.cuh"
+
+namespace tcs {
+namespace {
+
+using namespace dev;
+
+struct SddmmArgs {
+    const WorkItem* items;
+    uint64_t n_items;
+    const uint32_t* rp;
+    const uint32_t* ci;
+    const void* mask;   // mask values (F16 or F32)
+    const void* A;      // [rows][lda], feature padded
+    int64_t lda;
+    const void* Bt;     // [cols][ldbt], feature padded
+    int64_t ldbt;
+    void* out;          // output values (F16 or F32)
+    uint64_t rows;
+    int passes;         // feature passes of NSC super-chunks
+    uint32_t k;         // storage block width (8 / 4)
+};
+
+constexpr int kWarps = 4;
+
+template <bool MF32>
+__device__ __forceinline__ bool mask_live(const void* mask, uint64_t pos) {
+    if constexpr (MF32) return __ldg(static_cast<const float*>(mask) + pos) != 0.f;
+    else return __half2float(__ldg(static_cast<const __half*>(mask) + pos)) != 0.f;
+}
+
+template <bool OF32>
+__device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
+    if constexpr (OF32) static_cast<float*>(out)[pos] = v;
+    else static_cast<__half*>(out)[pos] = __float2half_rn(v);
+}
+
+// Writes the 16x8 accumulator tile of the vector group starting at s.
+template <bool MF32, bool OF32>
+__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], uint64_t vbase, uint32_t nvw,
+                                            uint32_t vend, uint32_t s, uint32_t g, uint32_t t) {
+    const uint32_t k = a.k;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+        const uint32_t r = 2 * t + (q & 1);
+        if (v >= vend) continue;
+        const uint32_t b = v / k, j = v - b * k, width = min(k, nvw - b * k);
+        const uint64_t pos = vbase + 8ull * b * k + r * width + j;
+        out_store<OF32>(a.out, pos, mask_live<MF32>(a.mask, pos) ? acc[q] : 0.f);
+    }
+}
+
+// ---------------------------------------------------------------- FP16
+template <int NSC>
+struct F16Tile {
+    uint4 q0[NSC], q1[NSC], ar[NSC];  // Bt rows of vectors g, g+8; A row g
+};
+
+template <int NSC>
+__device__ __forceinline__ void f16_tile_load(const SddmmArgs& a, const __half* __restrict__ arow, bool arow_ok,
+                                              uint32_t c0, bool ok0, uint32_t c1, bool ok1, int pass, uint32_t t,
+                                              F16Tile<NSC>& x) {
+    const __half* bt = static_cast<const __half*>(a.Bt);
+#pragma unroll
+    for (int sc = 0; sc < NSC; ++sc) {
+        const int64_t f = (static_cast<int64_t>(pass) * NSC + sc) * 32 + 8 * t;
+        x.q0[sc] = ok0 ? ld_gather_128(bt + static_cast<uint64_t>(c0) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
+        x.q1[sc] = ok1 ? ld_gather_128(bt + static_cast<uint64_t>(c1) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
+        x.ar[sc] = arow_ok ? ld_gather_128(arow + f) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <int NSC>
+__device__ __forceinline__ void f16_tile_mma(const F16Tile<NSC>& x, float (&acc)[4]) {
+#pragma unroll
+    for (int sc = 0; sc < NSC; ++sc) {
+        // chunk 0: k = {2t,2t+1} <-> features 8t+0,1 ; k = {2t+8,2t+9} <-> 8t+2,3
+        mma_f16_16816(acc, x.q0[sc].x, x.q1[sc].x, x.q0[sc].y, x.q1[sc].y, x.ar[sc].x, x.ar[sc].y);
+        // chunk 1: features 8t+4,5 and 8t+6,7
+        mma_f16_16816(acc, x.q0[sc].z, x.q1[sc].z, x.q0[sc].w, x.q1[sc].w, x.ar[sc].z, x.ar[sc].w);
+    }
+}
+
+// ---------------------------------------------------------------- TF32
+template <int NSC>
+struct Tf32Tile {
+    uint4 q0[NSC], q1[NSC], ar[NSC];  // 4 f32 features each
+};
+
+template <int NSC>
+__device__ __forceinline__ void tf32_tile_load(const SddmmArgs& a, const float* __restrict__ arow, bool arow_ok,
+                                               uint32_t c0, bool ok0, uint32_t c1, bool ok1, int pass, uint32_t t,
+                                               Tf32Tile<NSC>& x) {
+    const float* bt = static_cast<const float*>(a.Bt);
+#pragma unroll
+    for (int sc = 0; sc < NSC; ++sc) {
+        const int64_t f = (static_cast<int64_t>(pass) * NSC + sc) * 16 + 4 * t;
+        x.q0[sc] = ok0 ? ld_gather_128(bt + static_cast<uint64_t>(c0) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
+        x.q1[sc] = ok1 ? ld_gather_128(bt + static_cast<uint64_t>(c1) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
+        x.ar[sc] = arow_ok ? ld_gather_128(arow + f) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+__device__ __forceinline__ uint32_t tf(uint32_t bits) { return to_tf32(__uint_as_float(bits)); }
+
+template <int NSC>
+__device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, float (&acc)[4]) {
+#pragma unroll
+    for (int sc = 0; sc < NSC; ++sc) {
+        // chunk 0: k = t <-> feature 4t, k = t+4 <-> 4t+1 ; chunk 1: 4t+2, 4t+3
+        mma_tf32_1688(acc, tf(x.q0[sc].x), tf(x.q1[sc].x), tf(x.q0[sc].y), tf(x.q1[sc].y), tf(x.ar[sc].x),
+                      tf(x.ar[sc].y));
+        mma_tf32_1688(acc, tf(x.q0[sc].z), tf(x.q1[sc].z), tf(x.q0[sc].w), tf(x.q1[sc].w), tf(x.ar[sc].z),
+                      tf(x.ar[sc].w));
+    }
+}
+
+// One kernel body for both precisions; Tile/loader/mma chosen by TF32.
+template <bool TF32, int NSC, bool MF32, bool OF32>
+__global__ void __launch_bounds__(kWarps * 32, 4) sddmm_kernel(const SddmmArgs a) {
+    using Elem = typename std::conditional<TF32, float, __half>::type;
+    using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+    if (idx >= a.n_items) return;
+    const WorkItem it = a.items[idx];
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t base = __ldg(a.rp + it.window);
+    const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+    const uint32_t* ci = a.ci + base;
+    const uint64_t vbase = 8ull * base;
+    const uint32_t vend = it.vend;
+    const uint64_t arow_i = 8ull * it.window + g;
+    const bool arow_ok = arow_i < a.rows;
+    const Elem* arow = static_cast<const Elem*>(a.A) + (arow_ok ? arow_i : 0) * a.lda;
+
+    auto load = [&](uint32_t s, const uint32_t (&c)[2], int pass, Tile& x) {
+        if constexpr (TF32)
+            tf32_tile_load<NSC>(a, arow, arow_ok, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
+        else
+            f16_tile_load<NSC>(a, arow, arow_ok, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
+    };
+    auto mma = [&](const Tile& x, float (&acc)[4]) {
+        if constexpr (TF32) tf32_tile_mma<NSC>(x, acc);
+        else f16_tile_mma<NSC>(x, acc);
+    };
+    auto cols = [&](uint32_t s, uint32_t (&c)[2]) {
+        c[0] = s + g < vend ? __ldg(ci + s + g) : 0u;
+        c[1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
+    };
+    // one group: prefetched pass 0 + (rare) extra passes loaded in place
+    auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0) {
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        mma(x0, acc);
+        for (int p = 1; p < a.passes; ++p) {
+            Tile x;
+            load(s, c, p, x);
+            mma(x, acc);
+        }
+        sddmm_store<MF32, OF32>(a, acc, vbase, nvw, vend, s, g, t);
+    };
+
+    Tile ta, tb;
+    uint32_t ca[2], cb[2], cc[2];
+    uint32_t s = it.vbeg;
+    if (s < vend) {
+        cols(s, ca);
+        load(s, ca, 0, ta);
+        cols(s + 16, cb);
+    }
+    for (; s < vend; s += 32) {
+        if (s + 16 < vend) load(s + 16, cb, 0, tb);
+        cols(s + 32, cc);
+        group(s, ca, ta);
+        if (s + 16 >= vend) break;
+        if (s + 32 < vend) load(s + 32, cc, 0, ta);
+        cols(s + 48, ca);
+        group(s + 16, cb, tb);
+        cb[0] = ca[0]; cb[1] = ca[1];
+        ca[0] = cc[0]; ca[1] = cc[1];
+    }
+}
+
+template <bool TF32, int NSC>
+void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((a.n_items + kWarps - 1) / kWarps));
+    if (mf32 && of32) sddmm_kernel<TF32, NSC, true, true><<<grid, kWarps * 32, 0, s>>>(a);
+    else if (mf32) sddmm_kernel<TF32, NSC, true, false><<<grid, kWarps * 32, 0, s>>>(a);
+    else if (of32) sddmm_kernel<TF32, NSC, false, true><<<grid, kWarps * 32, 0, s>>>(a);
+    else sddmm_kernel<TF32, NSC, false, false><<<grid, kWarps * 32, 0, s>>>(a);
+    TCS_LAUNCHED(TF32 ? "sddmm_tf32" : "sddmm_f16");
+}
+
+}  // namespace
+}  // namespace tcs
+
+using namespace tcs;
+
+extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda,
+                                int64_t a_rows, int64_t f_a, const void* bt, tcs_dtype bt_dtype, int64_t ldbt,
+                                int64_t bt_rows, int64_t f_b, tcs_mebcrs* out, tcs_dtype out_dtype,
+                                const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
+    return guard([&] {
+        if (!cfg || !out) fail(TCS_ERR_ARGUMENT, "null argument");
+        check_mebcrs(mask);
+        // ref sddmm.hpp:86-90
+        if (cfg->precision != mask->precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded mask");
+        if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "SDDMM requires vector height 8");
+        if (a_rows != static_cast<int64_t>(mask->rows)) fail(TCS_ERR_SHAPE, "A rows must equal mask rows");
+        if (bt_rows != static_cast<int64_t>(mask->cols)) fail(TCS_ERR_SHAPE, "B cols must equal mask cols");
+        if (f_a != f_b) fail(TCS_ERR_SHAPE, "inner dimensions of A and B must agree");
+        if (f_a < 0) fail(TCS_ERR_SHAPE, "negative inner dimension");
+        if (out_dtype != TCS_DTYPE_F16 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown output dtype");
+        if ((a_rows && f_a && (!a || lda < f_a)) || (bt_rows && f_b && (!bt || ldbt < f_b)))
+            fail(TCS_ERR_ARGUMENT, "bad dense operand / leading dimension");
+        cudaStream_t s = st(stream);
+        const int64_t F = f_a;
+        const bool tf32 = mask->precision == TCS_TF32;
+        if (tf32 && (a_dtype != TCS_DTYPE_F32 || bt_dtype != TCS_DTYPE_F32))
+            fail(TCS_ERR_ARGUMENT, "TF32 SDDMM needs f32 dense operands");
+
+        // output: the mask's structure, fresh values
+        const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4;
+        void* caller_values = out->values;
+        tcs_mebcrs o = *mask;
+        o.flags = 0;
+        o.plan = nullptr;
+        o.value_dtype = out_dtype;
+        if (tf32 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
+        if (caller_values) {
+            o.values = caller_values;
+        } else {
+            o.values = dalloc(std::max<uint64_t>(1, 8 * mask->num_vectors) * ow, s);
+            o.flags = TCS_MEBCRS_OWN_VALUES;
+        }
+        if (counters) *counters = tcs_counters{};
+        const uint64_t nv = mask->num_vectors;
+        if (nv) {
+            if (F == 0) {
+                TCS_CUDA(cudaMemsetAsync(o.values, 0, 8 * nv * ow, s));
+            } else {
+                Plan* plan = static_cast<Plan*>(mask->plan);
+                Plan* tmp_plan = nullptr;
+                if (!plan) plan = tmp_plan = build_plan(mask, s, nullptr, nullptr, nullptr);
+                struct PlanGuard {
+                    Plan* p;
+                    cudaStream_t s;
+                    ~PlanGuard() { free_plan(p, s); }
+                } pg{tmp_plan, s};
+                // feature padding: super-chunk = 32 (FP16) / 16 (TF32) features
+                const int64_t sc = tf32 ? 16 : 32;
+                int64_t fpad = (F + sc - 1) / sc * sc;
+                // NSC super-chunks per pass (double-buffered in registers);
+                // wider inner dimensions take several passes.
+                int nsc = 1;
+                if (fpad > sc) {
+                    nsc = 2;
+                    fpad = (F + 2 * sc - 1) / (2 * sc) * (2 * sc);
+                }
+                const tcs_dtype need = tf32 ? TCS_DTYPE_F32 : TCS_DTYPE_F16;
+                const int64_t al = tf32 ? 4 : 8;
+                auto prep = [&](const void* src, tcs_dtype dt, int64_t ld, int64_t nrows, DBuf& buf,
+                                int64_t& out_ld) -> const void* {
+                    if (dt == need && ld >= fpad && ld % al == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+                        out_ld = ld;
+                        return src;
+                    }
+                    out_ld = fpad;
+                    buf = DBuf(std::max<int64_t>(1, nrows) * fpad * (tf32 ? 4 : 2), s);
+                    pad_convert(src, dt, ld, buf.p, need, fpad, nrows, F, fpad, s);
+                    return buf.p;
+                };
+                DBuf abuf, bbuf;
+                int64_t alda = 0, bldb = 0;
+                const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
+                const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
+                SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
+                               ap, alda, bp, bldb, o.values, mask->rows,
+                               static_cast<int>(fpad / (nsc * sc)), mask->k};
+                const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
+                if (plan->n_items) {
+                    if (tf32) {
+                        if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
+                        else launch_sddmm<true, 2>(args, mf32, of32, s);
+                    } else {
+                        if (nsc == 1) launch_sddmm<false, 1>(args, mf32, of32, s);
+                        else launch_sddmm<false, 2>(args, mf32, of32, s);
+                    }
+                }
+            }
+        }
+        // ref sddmm.hpp:121: one MMA per (16-vector group, k-step)
+        if (counters) counters->mma_invocations = mask->num_groups16 * ((F + mask->k - 1) / mask->k);
+        *out = o;
+    });
+}
+
+extern "C" tcs_status tcs_sddmm_host(uint64_t rows, uint64_t cols, tcs_precision precision,
+                                     const uint32_t* row_pointers, const uint32_t* column_indices,
+                                     const float* mask_values, const float* a, int64_t a_rows, int64_t f_a,
+                                     const float* bt, int64_t bt_rows, int64_t f_b, float* out_values,
+                                     const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
+    return guard([&] {
+        if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
+        if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded mask");
+        if (a_rows != static_cast<int64_t>(rows)) fail(TCS_ERR_SHAPE, "A rows must equal mask rows");
+        if (bt_rows != static_cast<int64_t>(cols)) fail(TCS_ERR_SHAPE, "B cols must equal mask cols");
+        if (f_a != f_b) fail(TCS_ERR_SHAPE, "inner dimensions of A and B must agree");
+        cudaStream_t s = st(stream);
+        tcs_mebcrs m{};
+        tcs_status rc = tcs_mebcrs_upload(rows, cols, precision, row_pointers, column_indices, mask_values, &m, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        struct Free {
+            tcs_mebcrs* m;
+            tcs_stream_t s;
+            ~Free() { tcs_mebcrs_free(m, s); }
+        } fr{&m, stream};
+        DBuf da(std::max<int64_t>(1, a_rows * f_a) * 4, s), db(std::max<int64_t>(1, bt_rows * f_b) * 4, s);
+        if (a_rows > 0 && f_a > 0) TCS_CUDA(cudaMemcpyAsync(da.p, a, a_rows * f_a * 4, cudaMemcpyHostToDevice, s));
+        if (bt_rows > 0 && f_b > 0) TCS_CUDA(cudaMemcpyAsync(db.p, bt, bt_rows * f_b * 4, cudaMemcpyHostToDevice, s));
+        tcs_mebcrs o{};
+        rc = tcs_sddmm(&m, da.p, TCS_DTYPE_F32, std::max<int64_t>(1, f_a), a_rows, f_a, db.p, TCS_DTYPE_F32,
+                       std::max<int64_t>(1, f_b), bt_rows, f_b, &o, TCS_DTYPE_F32, cfg, counters, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        if (m.num_vectors)
+            TCS_CUDA(cudaMemcpyAsync(out_values, o.values, 8 * m.num_vectors * 4, cudaMemcpyDeviceToHost, s));
+        TCS_CUDA(cudaStreamSynchronize(s));
+        tcs_mebcrs_free(&o, stream);
+    });
+}

@@ -1,0 +1,510 @@
+// SpMM C = A_sparse * B over ME-BCRS with the FlashSparse 8x1
+// swap-and-transpose strategy (ref spmm.hpp:103-177, mma.hpp:67-73):
+//
+//   C^T (features x 8 window rows) += B_gathered^T (features x vectors)
+//                                     * A_block^T (vectors x 8 rows)
+//
+// so the 8-row sparse vectors are the n=8 MMA operand and the dense
+// features fill m=16.  One warp owns one work item (<= plan.seg vectors of
+// one window) and one feature slab (128/64/32 features).
+//
+// FP16: mma.sync.m16n8k16 consumes TWO reference k=8 blocks per instruction
+// (storage k stays the reference k, instruction k=16).
+// TF32: mma.sync.m16n8k8 consumes two k=4 blocks; operands are rounded
+// RNE with cvt.rn.tf32.f32 (ref precision.hpp:42-46).
+//
+// Memory-efficient coalesced mapping (paper §3.3): the MMA's m dimension
+// (features) is permuted so that lane (g = lane/4) owns FPL consecutive
+// features of each gathered row: ONE 128-bit load per (lane, vector, chunk)
+// feeds FPL/2 MMAs, 8 lanes cover 128 contiguous bytes of a B row, and the
+// same permutation gives 128-bit fp32 stores of C.  The two vectors that
+// share an A register (k = 2t, 2t+1) are packed with PRMT.
+//
+// Residue (ref spmm.hpp:40-45, paper §3.5): vector slots at or past the
+// window's nv_w contribute zero registers and no loads are issued.
+// Windows longer than plan.seg are split; partial sums are reduced in
+// segment order by spmm_reduce_split (deterministic, no atomics).
+#include <algorithm>
+#include <type_traits>
+
+#include "tcs_internal.cuh"
+
+namespace tcs {
+namespace {
+
+using namespace dev;
+
+struct SpmmArgs {
+    const WorkItem* items;
+    uint64_t n_items;
+    const uint32_t* rp;
+    const uint32_t* ci;
+    const void* vals;
+    const void* B;   // feature-padded, 16-byte aligned rows
+    int64_t ldb;
+    float* C;
+    int64_t ldc;
+    uint64_t rows;
+    int64_t N;
+    float* partial;  // [slot][8][ldp]
+    int64_t ldp;
+};
+
+constexpr int kWarps = 4;
+
+// ------------------------------------------------------------- FP16 path
+template <int NCHUNK, int FPL, bool VF32>
+struct F16Step {
+    static constexpr int NJ = FPL / 2;  // MMAs per chunk == u32 regs per (vector, chunk)
+    uint32_t L[4][NCHUNK][NJ];          // gathered B rows of vectors 2t, 2t+1, 2t+8, 2t+9
+    uint32_t b[2];                      // sparse fragment: rows g, vectors {2t,2t+1}, {2t+8,2t+9}
+};
+
+template <int NCHUNK, int FPL, bool VF32>
+__device__ __forceinline__ void f16_load_cols(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
+                                              uint32_t t, uint32_t (&col)[4]) {
+    const uint32_t v0 = s + 2 * t;
+    col[0] = v0 < vend ? __ldg(ci + v0) : 0u;
+    col[1] = v0 + 1 < vend ? __ldg(ci + v0 + 1) : 0u;
+    col[2] = v0 + 8 < vend ? __ldg(ci + v0 + 8) : 0u;
+    col[3] = v0 + 9 < vend ? __ldg(ci + v0 + 9) : 0u;
+}
+
+template <int NCHUNK, int FPL, bool VF32>
+__device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t vbase, uint32_t nvw, uint32_t v,
+                                                    uint32_t g) {
+    if (v >= nvw) return 0u;
+    const uint32_t b = v >> 3, j = v & 7u, width = min(8u, nvw - 8 * b);
+    const uint64_t off = vbase + 64ull * b + g * width + j;
+    if constexpr (VF32) {
+        return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(static_cast<const float*>(vals)[off])));
+    } else {
+        return static_cast<uint32_t>(static_cast<const unsigned short*>(vals)[off]);
+    }
+}
+
+template <int NCHUNK, int FPL, bool VF32>
+__device__ __forceinline__ void f16_load_step(const SpmmArgs& a, const __half* __restrict__ Bl, uint64_t vbase,
+                                              uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
+                                              const uint32_t (&col)[4], F16Step<NCHUNK, FPL, VF32>& st) {
+    constexpr int CHUNK = 8 * FPL;
+    const uint32_t v0 = s + 2 * t;
+    const uint32_t vv[4] = {v0, v0 + 1, v0 + 8, v0 + 9};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bool ok = vv[i] < vend;
+        const __half* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            if constexpr (FPL == 8) {
+                uint4 x = ok ? ld_gather_128(row + c * CHUNK) : make_uint4(0, 0, 0, 0);
+                st.L[i][c][0] = x.x; st.L[i][c][1] = x.y; st.L[i][c][2] = x.z; st.L[i][c][3] = x.w;
+            } else {
+                uint2 x = ok ? ld_gather_64(row + c * CHUNK) : make_uint2(0, 0);
+                st.L[i][c][0] = x.x; st.L[i][c][1] = x.y;
+            }
+        }
+    }
+    if (s + 16 <= vend && s + 16 <= nvw) {
+        // both k=8 blocks are full width: rows g, slots 2t..2t+1 of blocks s/8, s/8+1
+        const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;
+        if constexpr (VF32) {
+            const float* fv = static_cast<const float*>(a.vals);
+            const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
+            st.b[0] = f2_to_h2(__uint_as_float(x.x), __uint_as_float(x.y));
+            st.b[1] = f2_to_h2(__uint_as_float(y.x), __uint_as_float(y.y));
+        } else {
+            const __half* hv = static_cast<const __half*>(a.vals);
+            st.b[0] = ld_stream_u32(hv + off);
+            st.b[1] = ld_stream_u32(hv + off + 64);
+        }
+    } else {
+        const uint32_t e0 = vv[0] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[0], g) : 0u;
+        const uint32_t e1 = vv[1] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[1], g) : 0u;
+        const uint32_t e2 = vv[2] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[2], g) : 0u;
+        const uint32_t e3 = vv[3] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[3], g) : 0u;
+        st.b[0] = e0 | (e1 << 16);
+        st.b[1] = e2 | (e3 << 16);
+    }
+}
+
+template <int NCHUNK, int FPL, bool VF32>
+__device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st, float (&acc)[NCHUNK][FPL / 2][4]) {
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+        for (int j = 0; j < FPL / 2; ++j)
+            mma_f16_16816(acc[c][j], pack_lo(st.L[0][c][j], st.L[1][c][j]), pack_hi(st.L[0][c][j], st.L[1][c][j]),
+                          pack_lo(st.L[2][c][j], st.L[3][c][j]), pack_hi(st.L[2][c][j], st.L[3][c][j]), st.b[0],
+                          st.b[1]);
+}
+
+// Stores FPL consecutive features of one output row (row-major, stride ld).
+template <int FPL>
+__device__ __forceinline__ void store_row(float* __restrict__ dst, const float (&v)[FPL], int64_t feat,
+                                          int64_t N, bool vec_ok) {
+    if (vec_ok && feat + FPL <= N) {
+#pragma unroll
+        for (int q = 0; q < FPL; q += 4) st_stream_f4(dst + q, v[q], v[q + 1], v[q + 2], v[q + 3]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < FPL; ++q)
+            if (feat + q < N) dst[q] = v[q];
+    }
+}
+
+template <int NCHUNK, int FPL, bool VF32>
+__global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_kernel(const SpmmArgs a) {
+    constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+    if (idx >= a.n_items) return;
+    const WorkItem it = a.items[idx];
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t base = __ldg(a.rp + it.window);
+    const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+    const uint32_t* ci = a.ci + base;
+    const uint64_t vbase = 8ull * base;
+    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const __half* Bl = static_cast<const __half*>(a.B) + feat0 + g * FPL;
+    const uint32_t vend = it.vend;
+
+    float acc[NCHUNK][NJ][4];
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+
+    // Software pipeline: column indices two steps ahead, gathered rows and
+    // sparse values one step ahead of the MMAs.
+    F16Step<NCHUNK, FPL, VF32> sa, sb;
+    uint32_t ca[4], cb[4];
+    uint32_t s = it.vbeg;
+    if (s < vend) {
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s, vend, t, ca);
+        f16_load_step(a, Bl, vbase, nvw, vend, s, g, t, ca, sa);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 16, vend, t, cb);
+    }
+    for (; s < vend; s += 32) {
+        f16_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, cb, sb);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 32, vend, t, ca);
+        f16_compute(sa, acc);
+        if (s + 16 >= vend) break;
+        f16_load_step(a, Bl, vbase, nvw, vend, s + 32, g, t, ca, sa);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 48, vend, t, cb);
+        f16_compute(sb, acc);
+    }
+
+    // Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
+    // of every chunk (accumulator layout, ref fragment.hpp:60-66).
+    const bool split = it.slot != kNoSlot;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t r = 2 * t + rr;
+        const uint64_t row = 8ull * it.window + r;
+        float* dst;
+        bool vec_ok;
+        if (split) {
+            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+            vec_ok = true;
+        } else {
+            if (row >= a.rows) continue;
+            dst = a.C + row * a.ldc;
+            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            float v[FPL];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                v[2 * j] = acc[c][j][rr];
+                v[2 * j + 1] = acc[c][j][2 + rr];
+            }
+            const int64_t feat = feat0 + c * CHUNK + FPL * g;
+            store_row<FPL>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        }
+    }
+}
+
+// ------------------------------------------------------------- TF32 path
+template <int NCHUNK>
+struct Tf32Step {
+    uint4 L[2][NCHUNK];  // rows of vectors t, t+4; 4 consecutive features per chunk
+    uint32_t b[2];       // sparse fragment: row g, vectors t, t+4
+};
+
+__device__ __forceinline__ float tf32_val_general(const float* vals, uint64_t vbase, uint32_t nvw, uint32_t v,
+                                                  uint32_t g) {
+    if (v >= nvw) return 0.f;
+    const uint32_t b = v >> 2, j = v & 3u, width = min(4u, nvw - 4 * b);
+    return __ldg(vals + vbase + 32ull * b + g * width + j);
+}
+
+template <int NCHUNK>
+__device__ __forceinline__ void tf32_load_step(const SpmmArgs& a, const float* __restrict__ Bl, uint64_t vbase,
+                                               uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
+                                               const uint32_t (&col)[2], Tf32Step<NCHUNK>& st) {
+    const uint32_t vv[2] = {s + t, s + t + 4};
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const bool ok = vv[i] < vend;
+        const float* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) st.L[i][c] = ok ? ld_gather_128(row + c * 32) : make_uint4(0, 0, 0, 0);
+    }
+    const float* fv = static_cast<const float*>(a.vals);
+    float x0, x1;
+    if (s + 8 <= vend && s + 8 <= nvw) {
+        const uint64_t off = vbase + 8ull * s + 4 * g + t;
+        x0 = __uint_as_float(ld_stream_u32(fv + off));
+        x1 = __uint_as_float(ld_stream_u32(fv + off + 32));
+    } else {
+        x0 = vv[0] < vend ? tf32_val_general(fv, vbase, nvw, vv[0], g) : 0.f;
+        x1 = vv[1] < vend ? tf32_val_general(fv, vbase, nvw, vv[1], g) : 0.f;
+    }
+    st.b[0] = to_tf32(x0);
+    st.b[1] = to_tf32(x1);
+}
+
+template <int NCHUNK>
+__device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (&acc)[NCHUNK][2][4]) {
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c) {
+        const uint4 x = st.L[0][c], y = st.L[1][c];
+        mma_tf32_1688(acc[c][0], to_tf32(__uint_as_float(x.x)), to_tf32(__uint_as_float(x.y)),
+                      to_tf32(__uint_as_float(y.x)), to_tf32(__uint_as_float(y.y)), st.b[0], st.b[1]);
+        mma_tf32_1688(acc[c][1], to_tf32(__uint_as_float(x.z)), to_tf32(__uint_as_float(x.w)),
+                      to_tf32(__uint_as_float(y.z)), to_tf32(__uint_as_float(y.w)), st.b[0], st.b[1]);
+    }
+}
+
+template <int NCHUNK>
+__global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArgs a) {
+    constexpr int SLAB = NCHUNK * 32;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+    if (idx >= a.n_items) return;
+    const WorkItem it = a.items[idx];
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t base = __ldg(a.rp + it.window);
+    const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+    const uint32_t* ci = a.ci + base;
+    const uint64_t vbase = 8ull * base;
+    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * g;
+    const uint32_t vend = it.vend;
+
+    float acc[NCHUNK][2][4];
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+
+    auto cols = [&](uint32_t s, uint32_t (&c)[2]) {
+        c[0] = s + t < vend ? __ldg(ci + s + t) : 0u;
+        c[1] = s + t + 4 < vend ? __ldg(ci + s + t + 4) : 0u;
+    };
+    Tf32Step<NCHUNK> sa, sb;
+    uint32_t ca[2], cb[2];
+    uint32_t s = it.vbeg;
+    if (s < vend) {
+        cols(s, ca);
+        tf32_load_step(a, Bl, vbase, nvw, vend, s, g, t, ca, sa);
+        cols(s + 8, cb);
+    }
+    for (; s < vend; s += 16) {
+        tf32_load_step(a, Bl, vbase, nvw, vend, s + 8, g, t, cb, sb);
+        cols(s + 16, ca);
+        tf32_compute(sa, acc);
+        if (s + 8 >= vend) break;
+        tf32_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, ca, sa);
+        cols(s + 24, cb);
+        tf32_compute(sb, acc);
+    }
+
+    const bool split = it.slot != kNoSlot;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t r = 2 * t + rr;
+        const uint64_t row = 8ull * it.window + r;
+        float* dst;
+        bool vec_ok;
+        if (split) {
+            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+            vec_ok = true;
+        } else {
+            if (row >= a.rows) continue;
+            dst = a.C + row * a.ldc;
+            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            const float v[4] = {acc[c][0][rr], acc[c][0][2 + rr], acc[c][1][rr], acc[c][1][2 + rr]};
+            const int64_t feat = feat0 + c * 32 + 4 * g;
+            store_row<4>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        }
+    }
+}
+
+// Sums the segments of split windows in segment order (deterministic).
+__global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __restrict__ split, uint64_t n_split,
+                                                         const float* __restrict__ partial, int64_t ldp, float* C,
+                                                         int64_t ldc, uint64_t rows, int64_t N) {
+    for (uint64_t sw = blockIdx.x; sw < n_split; sw += gridDim.x) {
+        const SplitWindow x = split[sw];
+        for (int64_t e = threadIdx.x; e < 8 * N; e += blockDim.x) {
+            const int64_t r = e / N, f = e - r * N;
+            const uint64_t row = 8ull * x.window + r;
+            if (row >= rows) continue;
+            float acc = 0.f;
+            for (uint32_t q = 0; q < x.nseg; ++q) acc += partial[((uint64_t)(x.first_slot + q) * 8 + r) * ldp + f];
+            C[row * ldc + f] = acc;
+        }
+    }
+}
+
+template <typename K>
+void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name) {
+    const dim3 grid(static_cast<unsigned>((a.n_items + kWarps - 1) / kWarps), slabs);
+    kernel<<<grid, kWarps * 32, 0, s>>>(a);
+    TCS_LAUNCHED(name);
+}
+
+}  // namespace
+}  // namespace tcs
+
+using namespace tcs;
+
+extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_dtype, int64_t ldb, int64_t b_rows,
+                               int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
+                               tcs_counters* counters, tcs_stream_t stream) {
+    return guard([&] {
+        if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
+        // ref spmm.hpp:106-109
+        if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
+        check_mebcrs(A);
+        if (cfg->precision != A->precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");
+        if (static_cast<int64_t>(A->cols) != b_rows) fail(TCS_ERR_SHAPE, "sparse cols must equal dense rows");
+        if (n < 0 || b_rows < 0) fail(TCS_ERR_SHAPE, "negative dimension");
+        if (n > 0 && A->rows > 0 && (!c || ldc < n)) fail(TCS_ERR_ARGUMENT, "bad output buffer / ldc");
+        if (n > 0 && b_rows > 0 && (!b || ldb < n)) fail(TCS_ERR_ARGUMENT, "bad dense buffer / ldb");
+        if (b_dtype != TCS_DTYPE_F16 && b_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown dtype");
+        if (A->precision == TCS_TF32 && b_dtype != TCS_DTYPE_F32)
+            fail(TCS_ERR_ARGUMENT, "TF32 SpMM needs an f32 dense operand");
+        if (counters) {
+            *counters = tcs_counters{};
+        }
+        cudaStream_t s = st(stream);
+        if (n == 0 || A->rows == 0) return;
+
+        Plan* plan = static_cast<Plan*>(A->plan);
+        Plan* tmp_plan = nullptr;
+        if (!plan) plan = tmp_plan = build_plan(A, s, nullptr, nullptr, nullptr);
+        struct PlanGuard {
+            Plan* p;
+            cudaStream_t s;
+            ~PlanGuard() { free_plan(p, s); }
+        } pg{tmp_plan, s};
+
+        // Feature padding: 32 / 64 / multiple of 128.
+        const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
+        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : 128;
+        const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
+        const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
+        const bool direct = b_dtype == need && ldb >= npad && ldb % align_elems == 0 &&
+                            (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+        DBuf bpad;
+        const void* bp = b;
+        int64_t bld = ldb;
+        if (!direct) {
+            bld = npad;
+            bpad = DBuf(static_cast<size_t>(std::max<int64_t>(1, b_rows)) * npad * (need == TCS_DTYPE_F16 ? 2 : 4), s);
+            pad_convert(b, b_dtype, ldb, bpad.p, need, npad, b_rows, n, npad, s);
+            bp = bpad.p;
+        }
+        DBuf partial;
+        if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
+
+        SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
+                   c, ldc, A->rows, n, partial.as<float>(), npad};
+        const int slabs = static_cast<int>(npad / slab);
+        if (plan->n_items) {
+            if (A->precision == TCS_FP16) {
+                const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
+                if (slab == 128)
+                    vf32 ? launch(spmm_f16_kernel<2, 8, true>, a, slabs, s, "spmm_f16<128,f32v>")
+                         : launch(spmm_f16_kernel<2, 8, false>, a, slabs, s, "spmm_f16<128>");
+                else if (slab == 64)
+                    vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>")
+                         : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>");
+                else
+                    vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>")
+                         : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>");
+            } else {
+                if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
+                else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>");
+                else launch(spmm_tf32_kernel<1>, a, slabs, s, "spmm_tf32<32>");
+            }
+        }
+        if (plan->n_split) {
+            const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
+            spmm_reduce_split<<<grid, 256, 0, s>>>(plan->split, plan->n_split, partial.as<float>(), npad, c, ldc,
+                                                  A->rows, n);
+            TCS_LAUNCHED("spmm_reduce_split");
+        }
+        if (counters) counters->mma_invocations = A->num_blocks * ((n + 15) / 16);  // ref analysis.hpp:34-38
+    });
+}
+
+extern "C" tcs_status tcs_spmm_host(uint64_t rows, uint64_t cols, tcs_precision precision,
+                                    const uint32_t* row_pointers, const uint32_t* column_indices, const float* values,
+                                    const float* b, int64_t b_rows, int64_t n, float* c,
+                                    const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
+    return guard([&] {
+        if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
+        if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
+        if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");
+        if (static_cast<int64_t>(cols) != b_rows) fail(TCS_ERR_SHAPE, "sparse cols must equal dense rows");
+        cudaStream_t s = st(stream);
+        tcs_mebcrs m{};
+        tcs_status rc = tcs_mebcrs_upload(rows, cols, precision, row_pointers, column_indices, values, &m, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        struct Free {
+            tcs_mebcrs* m;
+            tcs_stream_t s;
+            ~Free() { tcs_mebcrs_free(m, s); }
+        } fr{&m, stream};
+        DBuf db(std::max<int64_t>(1, b_rows * n) * 4, s), dc(std::max<uint64_t>(1, rows * n) * 4, s);
+        if (b_rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(db.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, s));
+        rc = tcs_spmm(&m, db.p, TCS_DTYPE_F32, n, b_rows, n, dc.as<float>(), n, cfg, counters, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        if (rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(c, dc.p, rows * n * 4, cudaMemcpyDeviceToHost, s));
+        TCS_CUDA(cudaStreamSynchronize(s));
+    });
+}
+
+extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision precision, const float* b, int64_t n,
+                                        float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
+                                        tcs_stream_t stream) {
+    return guard([&] {
+        if (!host_csr || !cfg) fail(TCS_ERR_ARGUMENT, "null argument");
+        cudaStream_t s = st(stream);
+        const uint64_t rows = host_csr->rows;
+        const int64_t b_rows = static_cast<int64_t>(host_csr->cols);
+        tcs_mebcrs m{};
+        tcs_status rc = tcs_mebcrs_encode_host(host_csr, precision,
+                                               precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        struct Free {
+            tcs_mebcrs* m;
+            tcs_stream_t s;
+            ~Free() { tcs_mebcrs_free(m, s); }
+        } fr{&m, stream};
+        DBuf db(std::max<int64_t>(1, b_rows * n) * 4, s), dc(std::max<uint64_t>(1, rows * n) * 4, s);
+        if (b_rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(db.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, s));
+        rc = tcs_spmm(&m, db.p, TCS_DTYPE_F32, n, b_rows, n, dc.as<float>(), n, cfg, counters, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        if (rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(c, dc.p, rows * n * 4, cudaMemcpyDeviceToHost, s));
+        TCS_CUDA(cudaStreamSynchronize(s));
+    });
+}

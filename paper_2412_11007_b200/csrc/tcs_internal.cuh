@@ -1,0 +1,232 @@
+// Internal helpers shared by the sm_100a kernels and the C-ABI glue.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <stdexcept>
+#include <string>
+
+#include "tcs/tcs.h"
+
+namespace tcs {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+    tcs_status code;
+    Error(tcs_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void set_last_error(const std::string& msg);
+extern std::atomic<uint64_t> g_launches;
+
+[[noreturn]] inline void fail(tcs_status c, const std::string& m) { throw Error(c, m); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        if (e == cudaErrorMemoryAllocation) fail(TCS_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+        fail(TCS_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define TCS_CUDA(x) ::tcs::cuda_check((x), #x)
+// After every kernel launch: counts it and surfaces launch errors.
+#define TCS_LAUNCHED(name)                                   \
+    do {                                                     \
+        ::tcs::g_launches.fetch_add(1, std::memory_order_relaxed); \
+        ::tcs::cuda_check(cudaGetLastError(), name);         \
+    } while (0)
+
+// Runs `body`, mapping exceptions onto status codes (no exception crosses
+// the C-ABI).
+template <typename F>
+tcs_status guard(F&& body) {
+    try {
+        body();
+        set_last_error("");
+        return TCS_OK;
+    } catch (const Error& e) {
+        set_last_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_last_error("host allocation failed");
+        return TCS_ERR_OOM;
+    } catch (const std::exception& e) {
+        set_last_error(e.what());
+        return TCS_ERR_CUDA;
+    }
+}
+
+// ------------------------------------------------- stream-ordered memory
+void* dalloc(size_t bytes, cudaStream_t s);
+void dfree(void* p, cudaStream_t s);
+int num_sms();
+
+// RAII device buffer (stream-ordered).
+struct DBuf {
+    void* p = nullptr;
+    cudaStream_t s = nullptr;
+    DBuf() = default;
+    DBuf(size_t bytes, cudaStream_t st) : p(dalloc(bytes, st)), s(st) {}
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    DBuf(DBuf&& o) noexcept : p(o.p), s(o.s) { o.p = nullptr; }
+    DBuf& operator=(DBuf&& o) noexcept {
+        reset();
+        p = o.p; s = o.s; o.p = nullptr;
+        return *this;
+    }
+    ~DBuf() { reset(); }
+    void reset() {
+        if (p) dfree(p, s);
+        p = nullptr;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// ------------------------------------------------------------ scan / plan
+// Exclusive prefix sum of n u32 values into out (n+1 entries, out[n] =
+// total).  Totals must fit in u32 (the reference's u32 row pointers).
+void exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, cudaStream_t s);
+
+// Work list for SpMM / SDDMM: items of at most `seg` vectors (a multiple of
+// 16) of one window.  Windows longer than `seg` are split; their partial
+// SpMM sums are reduced in segment order (deterministic).
+struct WorkItem {
+    uint32_t window;
+    uint32_t vbeg;  // window-relative vector range [vbeg, vend)
+    uint32_t vend;
+    uint32_t slot;  // partial-sum slot for split windows, else kNoSlot
+};
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;
+struct SplitWindow {
+    uint32_t window;
+    uint32_t first_slot;
+    uint32_t nseg;
+    uint32_t pad;
+};
+struct Plan {
+    uint32_t seg = 0;
+    uint64_t n_items = 0;
+    uint64_t n_slots = 0;
+    uint64_t n_split = 0;
+    WorkItem* items = nullptr;      // device
+    SplitWindow* split = nullptr;   // device
+};
+Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
+                 uint64_t* groups16);
+void free_plan(Plan* p, cudaStream_t s);
+
+// ------------------------------------------------------------ conversions
+// dst[r][c] (ld_dst, dst dtype) = src[r][c] for c < cols, 0 for cols <= c < cols_pad.
+void pad_convert(const void* src, tcs_dtype sdt, int64_t lds, void* dst, tcs_dtype ddt, int64_t ldd,
+                 int64_t rows, int64_t cols, int64_t cols_pad, cudaStream_t s);
+
+void check_mebcrs(const tcs_mebcrs* m);
+inline cudaStream_t st(tcs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+}  // namespace tcs
+
+// ============================================================ device helpers
+namespace tcs::dev {
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// RNE fp32 -> tf32 (cvt.rn.tf32.f32, sm_90+); matches the reference's
+// round_to_tf32 (ref precision.hpp:42-46; inf/NaN pass through).
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rn.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+
+// D = A(16x16 f16, row) * B(16x8 f16, col) + D, fp32 accumulate.
+__device__ __forceinline__ void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                              uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// D = A(16x8 tf32, row) * B(8x8 tf32, col) + D.
+__device__ __forceinline__ void mma_tf32_1688(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                              uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t pack_lo(uint32_t x, uint32_t y) { return __byte_perm(x, y, 0x5410); }
+__device__ __forceinline__ uint32_t pack_hi(uint32_t x, uint32_t y) { return __byte_perm(x, y, 0x7632); }
+
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// Two f32 -> packed f16x2 with RNE (lo = a, hi = b).
+__device__ __forceinline__ uint32_t f2_to_h2(float a, float b) { return h2_bits(__floats2half2_rn(a, b)); }
+
+// Streaming (read-once) loads of the sparse arrays: keep them out of L1 so
+// L1 holds the reused dense rows.
+__device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_stream_u64(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+// Dense-row gathers: read-only path, L1-allocating (hub rows are reused).
+__device__ __forceinline__ uint4 ld_gather_128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_gather_64(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_stream_f4(float* p, float a, float b, float c, float d) {
+    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d));
+}
+
+// Block-wide exclusive scan of one u32 per thread (blockDim.x a multiple of
+// 32, <= 1024); returns the exclusive prefix, *total = block sum.  Contains
+// __syncthreads: call from all threads of the block.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* total) {
+    __shared__ uint32_t warp_sums[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_sums[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t s = lane < nwarps ? warp_sums[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += y;
+        }
+        warp_sums[lane] = s;  // inclusive over warps
+    }
+    __syncthreads();
+    const uint32_t warp_prefix = warp ? warp_sums[warp - 1] : 0;
+    *total = warp_sums[nwarps - 1];
+    __syncthreads();
+    return warp_prefix + x - v;
+}
+
+}  // namespace tcs::dev

@@ -1,0 +1,264 @@
+"""Python front end of the B200 FlashSparse path, mirroring the reference's
+C++ API (``tcsparse::encode_mebcrs / spmm / sddmm``, ref
+proj/include/tcsparse) on torch CUDA tensors.
+
+Every call goes through the C-ABI (include/tcs/tcs.h) into
+libtcsparse_b200.so; torch supplies device memory and the current stream
+only.  Errors are raised as the reference's exception types
+(ref errors.hpp): ArgumentError, ShapeError, FormatError; CUDA failures as
+CudaError.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+
+import torch
+
+from . import _abi
+
+
+class TcsError(RuntimeError):
+    pass
+
+
+class ArgumentError(TcsError, ValueError):
+    """ref errors.hpp:36 (std::invalid_argument)."""
+
+
+class ShapeError(TcsError):
+    """ref errors.hpp:30."""
+
+
+class FormatError(TcsError):
+    """ref errors.hpp:24."""
+
+
+class CudaError(TcsError):
+    pass
+
+
+_ERR = {_abi.TCS_ERR_ARGUMENT: ArgumentError, _abi.TCS_ERR_SHAPE: ShapeError, _abi.TCS_ERR_FORMAT: FormatError,
+        _abi.TCS_ERR_CUDA: CudaError, _abi.TCS_ERR_OOM: CudaError, _abi.TCS_ERR_NCCL: CudaError}
+
+
+def _check(rc: int):
+    if rc != _abi.TCS_OK:
+        msg = _abi.load().tcs_last_error().decode()
+        raise _ERR.get(rc, TcsError)(msg)
+
+
+class Precision(enum.IntEnum):
+    """ref precision.hpp:13."""
+    fp16 = 0
+    tf32 = 1
+
+
+class ThreadMapping(enum.IntEnum):
+    """ref access_pattern.hpp:15."""
+    direct = 0
+    coalesced = 1
+
+
+@dataclass
+class KernelConfig:
+    """ref spmm.hpp:17-21."""
+    precision: Precision = Precision.fp16
+    vector_height: int = 8
+    mapping: ThreadMapping = ThreadMapping.coalesced
+
+    def _c(self):
+        return _abi.tcs_kernel_config(int(self.precision), int(self.vector_height), int(self.mapping), 0)
+
+
+@dataclass
+class KernelCounters:
+    """ref spmm.hpp:23-28."""
+    mma_invocations: int = 0
+    transactions: int = 0
+    transaction_bytes: int = 0
+    useful_bytes: int = 0
+
+    @staticmethod
+    def _from(c):
+        return KernelCounters(c.mma_invocations, c.transactions, c.transaction_bytes, c.useful_bytes)
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _u32(t: torch.Tensor) -> torch.Tensor:
+    if t.dtype == torch.uint32:
+        return t.contiguous()
+    return t.to(torch.int32).contiguous()
+
+
+@dataclass
+class CsrMatrix:
+    """ref matrix.hpp:20-49 on the device (u32 indices as int32/uint32 tensors)."""
+    rows: int
+    cols: int
+    row_ptr: torch.Tensor
+    col_idx: torch.Tensor
+    values: torch.Tensor
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col_idx.numel())
+
+    def _c(self):
+        self.row_ptr, self.col_idx = _u32(self.row_ptr), _u32(self.col_idx)
+        self.values = self.values.to(torch.float32).contiguous()
+        return _abi.tcs_csr(self.rows, self.cols, self.nnz, self.row_ptr.data_ptr(), self.col_idx.data_ptr(),
+                            self.values.data_ptr())
+
+
+class MeBcrsMatrix:
+    """Device ME-BCRS (ref mebcrs.hpp:23-78) owned by the C library."""
+
+    def __init__(self, handle: _abi.tcs_mebcrs, keepalive=()):
+        self._h = handle
+        self._keep = list(keepalive)
+
+    # reference accessors
+    rows = property(lambda self: self._h.rows)
+    cols = property(lambda self: self._h.cols)
+    k = property(lambda self: self._h.k)
+    vector_height = property(lambda self: self._h.vector_height)
+    precision = property(lambda self: Precision(self._h.precision))
+    num_windows = property(lambda self: self._h.num_windows)
+    num_vectors = property(lambda self: self._h.num_vectors)
+    num_blocks = property(lambda self: self._h.num_blocks)
+    max_window_vectors = property(lambda self: self._h.max_window_vectors)
+    value_dtype = property(lambda self: self._h.value_dtype)
+
+    def to_host(self):
+        """(row_pointers, column_indices, values[f32]) as numpy arrays."""
+        import numpy as np
+
+        rp = np.empty(self.num_windows + 1, np.uint32)
+        ci = np.empty(max(1, self.num_vectors), np.uint32)
+        v = np.empty(max(1, 8 * self.num_vectors), np.float32)
+        _check(_abi.load().tcs_mebcrs_download(C.byref(self._h), rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                               _stream()))
+        return rp, ci[: self.num_vectors], v[: 8 * self.num_vectors]
+
+    def validate(self):
+        _check(_abi.load().tcs_mebcrs_validate(C.byref(self._h), _stream()))
+
+    def free(self):
+        if getattr(self, "_h", None) is not None and (self._h.flags or self._h.plan):
+            _abi.load().tcs_mebcrs_free(C.byref(self._h), _stream())
+        self._keep = []
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_host(rows, cols, precision, row_pointers, column_indices, values) -> "MeBcrsMatrix":
+        import numpy as np
+
+        rp = np.ascontiguousarray(row_pointers, np.uint32)
+        ci = np.ascontiguousarray(column_indices, np.uint32)
+        v = np.ascontiguousarray(values, np.float32)
+        h = _abi.tcs_mebcrs()
+        _check(_abi.load().tcs_mebcrs_upload(rows, cols, int(precision), rp.ctypes.data, ci.ctypes.data,
+                                             v.ctypes.data, C.byref(h), _stream()))
+        return MeBcrsMatrix(h)
+
+
+def encode_mebcrs(csr: CsrMatrix, precision: Precision, value_dtype: int | None = None) -> MeBcrsMatrix:
+    """ref mebcrs.hpp:80.  value_dtype: TCS_DTYPE_F16 (default for fp16) or TCS_DTYPE_F32."""
+    if value_dtype is None:
+        value_dtype = _abi.TCS_DTYPE_F16 if int(precision) == 0 else _abi.TCS_DTYPE_F32
+    c = csr._c()
+    h = _abi.tcs_mebcrs()
+    _check(_abi.load().tcs_mebcrs_encode(C.byref(c), int(precision), int(value_dtype), C.byref(h), _stream()))
+    return MeBcrsMatrix(h)
+
+
+@dataclass
+class SpmmResult:
+    output: torch.Tensor
+    counters: KernelCounters = field(default_factory=KernelCounters)
+
+
+def _dtype_tag(t: torch.Tensor) -> int:
+    if t.dtype == torch.float16:
+        return _abi.TCS_DTYPE_F16
+    if t.dtype == torch.float32:
+        return _abi.TCS_DTYPE_F32
+    raise ArgumentError(f"unsupported dense dtype {t.dtype}")
+
+
+def spmm(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = KernelConfig(),
+         out: torch.Tensor | None = None) -> SpmmResult:
+    """ref spmm.hpp:173.  dense: [K, N] f16 (FP16) or f32 CUDA tensor, row-major
+    (any row stride).  Returns C [M, N] f32."""
+    if dense.dim() != 2 or dense.stride(1) != 1:
+        dense = dense.contiguous()
+    m, n = sparse.rows, dense.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    cnt = _abi.tcs_counters()
+    _check(_abi.load().tcs_spmm(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
+                                dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()), C.byref(cnt),
+                                _stream()))
+    return SpmmResult(out, KernelCounters._from(cnt))
+
+
+@dataclass
+class SddmmOperands:
+    """ref sddmm.hpp:16-20: mask (ME-BCRS), a [M, F], b_t [N, F]."""
+    mask: MeBcrsMatrix
+    a: torch.Tensor
+    b_t: torch.Tensor
+
+
+@dataclass
+class SddmmResult:
+    output: MeBcrsMatrix
+    counters: KernelCounters = field(default_factory=KernelCounters)
+
+
+def sddmm(ops: SddmmOperands, cfg: KernelConfig = KernelConfig(), out_dtype: int = _abi.TCS_DTYPE_F32,
+          out_values: torch.Tensor | None = None) -> SddmmResult:
+    """ref sddmm.hpp:84.  The output shares the mask's structure (kept alive).
+    ``out_values`` (optional): caller-owned device tensor of 8 * nv elements
+    of out_dtype receiving the values (else the library allocates them)."""
+    a = ops.a if ops.a.stride(-1) == 1 else ops.a.contiguous()
+    b = ops.b_t if ops.b_t.stride(-1) == 1 else ops.b_t.contiguous()
+    h = _abi.tcs_mebcrs()
+    keep = [ops.mask]
+    if out_values is not None:
+        need = 8 * ops.mask.num_vectors
+        if out_values.numel() < need or not out_values.is_contiguous():
+            raise ArgumentError("out_values too small or not contiguous")
+        h.values = out_values.data_ptr()
+        keep.append(out_values)
+    cnt = _abi.tcs_counters()
+    _check(_abi.load().tcs_sddmm(C.byref(ops.mask._h), a.data_ptr(), _dtype_tag(a), a.stride(0), a.shape[0],
+                                 a.shape[1], b.data_ptr(), _dtype_tag(b), b.stride(0), b.shape[0], b.shape[1],
+                                 C.byref(h), int(out_dtype), C.byref(cfg._c()), C.byref(cnt), _stream()))
+    return SddmmResult(MeBcrsMatrix(h, keepalive=keep), KernelCounters._from(cnt))
+
+
+def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
+    """Device operand rounding used by the kernels (diagnostics)."""
+    x = x.to(torch.float32).contiguous()
+    out = torch.empty_like(x)
+    _check(_abi.load().tcs_round_values(int(precision), x.data_ptr(), out.data_ptr(), x.numel(), _stream()))
+    return out
+
+
+def launch_count() -> int:
+    return int(_abi.load().tcs_launch_count())
+
+
+def version() -> str:
+    return _abi.load().tcs_version().decode()

@@ -1,0 +1,181 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the
+reference's own outputs (golden hashes from oracle/_ref) and the pinned CPU
+oracle.  Bar: bit-exact for the ME-BCRS arrays and for small-integer inputs
+(ref generate.hpp:13-18 makes every product and sum exact); rel-L2 <= 1e-2
+(FP16) / 1e-3 (TF32) for real-valued inputs (BASELINE.json north star).
+"""
+import numpy as np
+import pytest
+import torch
+
+import cases
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+T = None  # paper_2412_11007_b200.tcsparse, imported lazily (needs the built .so)
+F16, F32 = 0, 1
+REL_TOL = {0: 1e-2, 1: 1e-3}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    global T
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_11007_b200.tcsparse as tcs
+
+    T = tcs
+
+
+def dev_csr(m: O.Csr):
+    return T.CsrMatrix(m.rows, m.cols, torch.from_numpy(m.row_ptr.view(np.int32)).cuda(),
+                       torch.from_numpy(m.col_idx.view(np.int32)).cuda(), torch.from_numpy(m.values).cuda())
+
+
+def rel_l2(got, want):
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    den = np.linalg.norm(want)
+    return np.linalg.norm(got - want) / (den if den else 1.0)
+
+
+def check_case(case, rec, value_dtype):
+    for p in case.precisions:
+        if p == 1 and value_dtype == F16:
+            continue
+        tag = "fp16" if p == 0 else "tf32"
+        me = T.encode_mebcrs(dev_csr(case.csr), T.Precision(p), value_dtype)
+        rp, ci, v = me.to_host()
+        assert cases.sha(rp) == rec[f"me_{tag}"]["rp_sha"], case.name
+        assert cases.sha(ci) == rec[f"me_{tag}"]["ci_sha"], case.name
+        ref_me = O.encode_mebcrs(case.csr, p)  # pinned == reference (test_oracle.py)
+        if value_dtype == F32:
+            assert cases.sha(rp, ci, v) == rec[f"me_{tag}"]["sha"], case.name
+        else:  # binary16 storage == the reference's round_to_fp16 of its values
+            assert np.array_equal(v.view(np.uint32), O.round_array(ref_me.values, 0).view(np.uint32)), case.name
+        cfg = T.KernelConfig(T.Precision(p))
+        if case.B is not None:
+            for dense in ([torch.from_numpy(case.B).cuda()] +
+                          ([torch.from_numpy(case.B).cuda().half()] if p == 0 else [])):
+                res = T.spmm(me, dense, cfg)
+                got = res.output.cpu().numpy()
+                assert cases.sha(got) == rec[f"spmm_{tag}"]["sha"], (case.name, dense.dtype)
+                assert res.counters.mma_invocations == rec[f"spmm_{tag}"]["mma"]
+        if case.A is not None:
+            ops = T.SddmmOperands(me, torch.from_numpy(case.A).cuda(), torch.from_numpy(case.Bt).cuda())
+            res = T.sddmm(ops, cfg)
+            out = res.output.to_host()[2]
+            assert cases.sha(out) == rec[f"sddmm_{tag}"]["sha"], case.name
+            assert res.counters.mma_invocations == rec[f"sddmm_{tag}"]["mma"]
+            if case.D is not None:  # pipeline closure: SDDMM output drives SpMM (ref tests/test_kernels.cpp:313)
+                chained = T.spmm(res.output, torch.from_numpy(case.D).cuda(), cfg).output.cpu().numpy()
+                assert cases.sha(chained) == rec[f"chain_{tag}"]["sha"], case.name
+        me.free()
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_known_answer_cases(golden, value_dtype):
+    for case in cases.kat_cases():
+        check_case(case, golden["cases"][case.name], value_dtype)
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_acceptance2_replay(golden, value_dtype):
+    """tests/acceptance.cpp criterion 2: 200 seeded matrices, both precisions, bit-exact."""
+    params = cases.acceptance2_params()
+    for i in range(200):
+        check_case(cases.acceptance2_case(i, params), golden["cases"][f"acc2_{i:03d}"], value_dtype)
+
+
+def test_acceptance6_replay(golden):
+    """tests/acceptance.cpp criterion 6: 100 SDDMM triples + chained SpMM."""
+    params = cases.acceptance6_params()
+    for i in range(100):
+        check_case(cases.acceptance6_case(i, params), golden["cases"][f"acc6_{i:03d}"], F32)
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_config1_small_int_bit_exact(golden, value_dtype):
+    c = cases.c1_case(False)
+    check_case(c, golden["cases"]["c1"], value_dtype)
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_config1_real_mode_tolerance(golden, p):
+    """C1/C2 with uniform [-1,1) values: rel-L2 vs the reference's fp32 result."""
+    c = cases.c1_case(True)
+    me_ref = O.encode_mebcrs(c.csr, p)
+    me = T.encode_mebcrs(dev_csr(c.csr), T.Precision(p))
+    cfg = T.KernelConfig(T.Precision(p))
+    got = T.spmm(me, torch.from_numpy(c.B).cuda(), cfg).output.cpu().numpy()
+    want = O.spmm(me_ref, c.B)
+    assert cases.sha(want) == golden["cases"]["c1_real"][f"spmm_{'fp16' if p == 0 else 'tf32'}"]["sha"]
+    err = rel_l2(got, want)
+    assert err <= REL_TOL[p], err
+    assert err < 1e-5  # only summation order differs from the reference
+    out = T.sddmm(T.SddmmOperands(me, torch.from_numpy(c.A).cuda(), torch.from_numpy(c.Bt).cuda()), cfg)
+    err2 = rel_l2(out.output.to_host()[2], O.sddmm(me_ref, c.A, c.Bt))
+    assert err2 <= REL_TOL[p] and err2 < 1e-5, err2
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_rounding_exhaustive_on_device(p):
+    """Every binary32 bit pattern: device RNE (__float2half_rn / cvt.rn.tf32)
+    == the reference's round_to_fp16 / round_to_tf32.
+    The reference formula is restated with torch integer ops on the GPU and
+    pinned to the oracle on a random sample first."""
+
+    def ref_round(bits: torch.Tensor) -> torch.Tensor:  # int64 bit patterns -> int64 result bits
+        sign = bits & 0x80000000
+        mag = bits & 0x7FFFFFFF
+        rne = lambda b: (b + 0xFFF + ((b >> 13) & 1)) & ~0x1FFF  # noqa: E731
+        if p == 1:
+            return torch.where((bits & 0x7F800000) == 0x7F800000, bits, rne(bits) & 0xFFFFFFFF)
+        x = (bits & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
+        sub = (torch.round(x.double() * 2.0**24) / 2.0**24).float().view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        out = torch.where(mag >= 0x38800000, sign | rne(mag), sub)
+        out = torch.where(mag >= 0x477FF000, sign | 0x7F800000, out)
+        return torch.where(mag >= 0x7F800000, bits, out)
+
+    rng = np.random.default_rng(7)
+    sample = rng.integers(0, 2**32, 100000, dtype=np.uint64).astype(np.uint32)
+    want = O.round_array(sample.view(np.float32), p).view(np.uint32)
+    got = ref_round(torch.from_numpy(sample.astype(np.int64)).cuda()).cpu().numpy().astype(np.uint32)
+    nan = np.isnan(sample.view(np.float32))
+    assert np.array_equal(got[~nan], want[~nan])
+    chunk = 1 << 28
+    for start in range(0, 1 << 32, chunk):
+        bits = torch.arange(start, start + chunk, dtype=torch.int64, device="cuda")
+        x = (bits & 0xFFFFFFFF).to(torch.int32).view(torch.float32)
+        dev = T.round_values(x, T.Precision(p)).view(torch.int32).to(torch.int64) & 0xFFFFFFFF
+        ref = ref_round(bits)
+        isnan = torch.isnan(x)
+        bad = (dev != ref) & ~isnan
+        assert int(bad.sum()) == 0, f"mismatch at {int(bits[bad][0]):#x}"
+        assert bool(torch.isnan(dev.to(torch.int32).view(torch.float32))[isnan].all())
+
+
+def test_reference_error_taxonomy():
+    """ref tests/test_kernels.cpp:127-137, 303-312."""
+    ident = O.Csr.from_coords(8, 8, [(i, i, 1.0) for i in range(8)])
+    me = T.encode_mebcrs(dev_csr(ident), T.Precision.fp16)
+    dense = torch.ones(8, 16, device="cuda")
+    with pytest.raises(T.ArgumentError):
+        T.spmm(me, dense, T.KernelConfig(T.Precision.fp16, 16))
+    with pytest.raises(T.ArgumentError):
+        T.spmm(me, dense, T.KernelConfig(T.Precision.tf32, 8))
+    with pytest.raises(T.ShapeError):
+        T.spmm(me, torch.ones(9, 16, device="cuda"), T.KernelConfig())
+    mask = T.encode_mebcrs(dev_csr(O.generate_random_sparse(16, 16, 0.2, 81)), T.Precision.fp16)
+    a, b = torch.ones(16, 8, device="cuda"), torch.ones(16, 8, device="cuda")
+    with pytest.raises(T.ArgumentError):
+        T.sddmm(T.SddmmOperands(mask, a, b), T.KernelConfig(T.Precision.tf32))
+    with pytest.raises(T.ShapeError):
+        T.sddmm(T.SddmmOperands(mask, torch.ones(15, 8, device="cuda"), b))
+    with pytest.raises(T.ShapeError):
+        T.sddmm(T.SddmmOperands(mask, torch.ones(16, 9, device="cuda"), b))
+    # malformed CSR -> FormatError (ref matrix.hpp:31-48)
+    bad = T.CsrMatrix(2, 4, torch.tensor([0, 2, 2], dtype=torch.int32, device="cuda"),
+                      torch.tensor([3, 1], dtype=torch.int32, device="cuda"), torch.ones(2, device="cuda"))
+    with pytest.raises(T.FormatError):
+        T.encode_mebcrs(bad, T.Precision.fp16)

@@ -1,0 +1,179 @@
+"""GPU parity beyond the reference's desk-scale cases.
+
+* mid-size power-law graphs and hub-heavy windows (split windows, the
+  512-thread and global-scratch merge paths) against the pinned oracle,
+  bit-exact with small-integer values;
+* BASELINE config 3 at full size (Reddit-shaped, ~115 M nnz) through
+  size-independent properties: ME-BCRS row pointers equal an independent
+  torch count of distinct (window, column) pairs; integer-valued SpMM equals
+  an independent exact fp32 product (every partial sum is an integer below
+  2^24, so any summation order gives the same bits); SDDMM equals direct
+  dot products at sampled positions;
+* the host-buffer entry points (value semantics of the reference API).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+T = None
+G = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    global T, G
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_11007_b200.graphs as graphs
+    import paper_2412_11007_b200.tcsparse as tcs
+
+    T, G = tcs, graphs
+
+
+def to_oracle(rows, cols, rp, ci, v):
+    return O.Csr(rows, cols, rp.cpu().numpy().view(np.uint32), ci.cpu().numpy().view(np.uint32), v.cpu().numpy())
+
+
+def dev(m: O.Csr):
+    return T.CsrMatrix(m.rows, m.cols, torch.from_numpy(m.row_ptr.view(np.int32)).cuda(),
+                       torch.from_numpy(m.col_idx.view(np.int32)).cuda(), torch.from_numpy(m.values).cuda())
+
+
+def hub_matrix():
+    """Windows of every size class: tiny, > 2048 entries (512-thread merge),
+    > 12288 entries (global scratch), plus windows longer than the SpMM
+    segment (split + deterministic reduction) and empty windows."""
+    rng = np.random.default_rng(11)
+    rows, cols = 96, 40000
+    per_row = [3] * 8 + [400] * 8 + [0] * 8 + [2500] * 8 + [12] * 8 + [6000] * 8 + [1] * 8 + [0] * 8 + \
+              [900] * 8 + [30000] * 8 + [5] * 8 + [2] * 8
+    rp = np.zeros(rows + 1, np.uint32)
+    ci_list = []
+    for r, d in enumerate(per_row):
+        c = np.sort(rng.choice(cols, size=d, replace=False)).astype(np.uint32)
+        ci_list.append(c)
+        rp[r + 1] = rp[r] + d
+    ci = np.concatenate(ci_list)
+    vals = rng.integers(1, 5, ci.size).astype(np.float32) * rng.choice([-1, 1], ci.size).astype(np.float32)
+    return O.Csr(rows, cols, rp, ci, vals)
+
+
+@pytest.mark.parametrize("p", [0, 1])
+@pytest.mark.parametrize("n", [128, 64, 32, 256, 40])
+def test_hub_windows_bit_exact(p, n):
+    m = hub_matrix()
+    ref = O.encode_mebcrs(m, p)
+    me = T.encode_mebcrs(dev(m), T.Precision(p), 1)
+    rp, ci, v = me.to_host()
+    assert np.array_equal(rp, ref.row_pointers) and np.array_equal(ci, ref.column_indices)
+    assert np.array_equal(v.view(np.uint32), ref.values.view(np.uint32))
+    B = O.generate_random_dense(m.cols, n, 5)
+    got = T.spmm(me, torch.from_numpy(B).cuda(), T.KernelConfig(T.Precision(p))).output.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), O.spmm(ref, B).view(np.uint32))
+    A = O.generate_random_dense(m.rows, 32, 6)
+    Bt = O.generate_random_dense(m.cols, 32, 7)
+    out = T.sddmm(T.SddmmOperands(me, torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda()),
+                  T.KernelConfig(T.Precision(p))).output.to_host()[2]
+    assert np.array_equal(out.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32))
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_power_law_midsize_bit_exact(p):
+    spec = G.GraphSpec("mid", 60_000, 3_000_000, alpha=1.2, cap=60.0, seed=5)
+    rows, cols, rp, ci, v = G.power_law_csr(spec, values="int")
+    m = to_oracle(rows, cols, rp, ci, v)
+    ref = O.encode_mebcrs(m, p)
+    me = T.encode_mebcrs(T.CsrMatrix(rows, cols, rp, ci, v), T.Precision(p))
+    h_rp, h_ci, h_v = me.to_host()
+    assert np.array_equal(h_rp, ref.row_pointers) and np.array_equal(h_ci, ref.column_indices)
+    B = O.generate_random_dense(cols, 128, 9)
+    Bd = torch.from_numpy(B).cuda()
+    got = T.spmm(me, Bd.half() if p == 0 else Bd, T.KernelConfig(T.Precision(p))).output.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), O.spmm(ref, B).view(np.uint32))
+
+
+def test_config3_full_size_properties():
+    rows, cols, rp, ci, v = G.power_law_csr(G.C3_REDDIT, values="int")
+    nnz = ci.numel()
+    assert 100e6 < nnz < 130e6
+    me = T.encode_mebcrs(T.CsrMatrix(rows, cols, rp, ci, v), T.Precision.fp16)
+    # (1) row pointers == independent count of distinct (window, column) pairs
+    r_of = torch.repeat_interleave(torch.arange(rows, device="cuda"), (rp[1:] - rp[:-1]).long())
+    keys = torch.unique((r_of // 8) * cols + ci.long())
+    counts = torch.bincount(keys // cols, minlength=me.num_windows)
+    del keys
+    import paper_2412_11007_b200._abi as abi
+
+    nv = me.num_vectors
+    rp_host = np.empty(me.num_windows + 1, np.uint32)
+    ci_host = np.empty(nv, np.uint32)
+    assert abi.load().tcs_mebcrs_download(C.byref(me._h), rp_host.ctypes.data, ci_host.ctypes.data, None,
+                                          C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    want_rp = np.concatenate([[0], np.cumsum(counts.cpu().numpy())]).astype(np.uint32)
+    assert np.array_equal(rp_host, want_rp)
+    # (2) integer SpMM == exact independent product
+    B = G.dense(cols, 128, 3, values="int", dtype=torch.float32)
+    got = T.spmm(me, B.half(), T.KernelConfig()).output
+    A = torch.sparse_csr_tensor(rp.long(), ci.long(), v, size=(rows, cols))
+    assert torch.equal(got, A @ B)
+    del got, A, B
+    # (3) SDDMM at 20k sampled vectors == direct dot products where the
+    # pattern has an entry, 0 elsewhere (ref sddmm.hpp:131)
+    Af = G.dense(rows, 32, 4, values="int", dtype=torch.float32)
+    Bt = G.dense(cols, 32, 5, values="int", dtype=torch.float32)
+    out_vals = torch.empty(8 * nv, dtype=torch.float32, device="cuda")
+    T.sddmm(T.SddmmOperands(me, Af, Bt), T.KernelConfig(), out_values=out_vals)
+    rng = np.random.default_rng(3)
+    vid = np.sort(rng.choice(nv, 20000, replace=False))
+    w = np.searchsorted(rp_host, vid, side="right") - 1
+    vl = vid - rp_host[w]
+    nvw = rp_host[w + 1] - rp_host[w]
+    b, j = vl // 8, vl % 8
+    width = np.minimum(8, nvw - 8 * b)
+    col = ci_host[vid].astype(np.int64)
+    entry_keys = (r_of * cols + ci.long())  # CSR order == sorted
+    for r in range(8):
+        row = 8 * w + r
+        ok = row < rows
+        pos = 8 * (rp_host[w].astype(np.int64) + 8 * b) + r * width + j
+        got_r = out_vals[torch.from_numpy(pos).cuda()].cpu().numpy()
+        q = torch.from_numpy(np.where(ok, row, 0) * cols + col).cuda()
+        idx = torch.searchsorted(entry_keys, q).clamp(max=entry_keys.numel() - 1)
+        present = ((entry_keys[idx] == q).cpu().numpy()) & ok
+        dots = (Af[torch.from_numpy(np.where(ok, row, 0)).cuda()] * Bt[torch.from_numpy(col).cuda()]).sum(1)
+        want_r = np.where(present, dots.cpu().numpy(), 0.0).astype(np.float32)
+        assert np.array_equal(got_r, want_r), r
+    me.free()
+
+
+def test_host_entry_points_match_device_path():
+    m = O.generate_random_sparse(300, 200, 0.05, 3)
+    B = O.generate_random_dense(200, 48, 4)
+    lib = __import__("paper_2412_11007_b200._abi", fromlist=["x"]).load()
+    cfg = __import__("paper_2412_11007_b200._abi", fromlist=["x"]).tcs_kernel_config(0, 8, 1, 0)
+    for p in (0, 1):
+        cfg.precision = p
+        ref = O.encode_mebcrs(m, p)
+        want = O.spmm(ref, B)
+        Cm = np.empty((300, 48), np.float32)
+        rc = lib.tcs_spmm_host(300, 200, p, ref.row_pointers.ctypes.data, ref.column_indices.ctypes.data,
+                               ref.values.ctypes.data, B.ctypes.data, 200, 48, Cm.ctypes.data, C.byref(cfg), None,
+                               None)
+        assert rc == 0 and np.array_equal(Cm.view(np.uint32), want.view(np.uint32))
+        csr = __import__("paper_2412_11007_b200._abi", fromlist=["x"]).tcs_csr(
+            300, 200, m.nnz, m.row_ptr.ctypes.data, m.col_idx.ctypes.data, m.values.ctypes.data)
+        C2 = np.empty((300, 48), np.float32)
+        rc = lib.tcs_spmm_csr_host(C.byref(csr), p, B.ctypes.data, 48, C2.ctypes.data, C.byref(cfg), None, None)
+        assert rc == 0 and np.array_equal(C2.view(np.uint32), want.view(np.uint32))
+        A = O.generate_random_dense(300, 20, 5)
+        Bt = O.generate_random_dense(200, 20, 6)
+        out = np.empty(8 * ref.nv, np.float32)
+        rc = lib.tcs_sddmm_host(300, 200, p, ref.row_pointers.ctypes.data, ref.column_indices.ctypes.data,
+                                ref.values.ctypes.data, A.ctypes.data, 300, 20, Bt.ctypes.data, 200, 20,
+                                out.ctypes.data, C.byref(cfg), None, None)
+        assert rc == 0 and np.array_equal(out.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32))
