@@ -226,6 +226,25 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     b2b_ms = a.elapsed_time(b) / 10
 
+    # instruction-path comparison (north star: mma.sync weighed against tcgen05)
+    paths = {}
+    if not args.quick:
+        for path in ("mma_sync", "tcgen05"):
+            pc = T.KernelConfig(prec, path=path)
+            try:
+                T.spmm(me, B, pc, out=out)
+            except T.TcsError:
+                continue
+            ts = []
+            for _ in range(10):
+                flush.zero_()
+                a.record()
+                T.spmm(me, B, pc, out=out)
+                b.record()
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            paths[path] = round(sum(ts) / len(ts), 4)
+
     vwA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
     vwB = 2 if dt == torch.float16 else 4
     balg = bytes_alg_spmm(W, nv, l_rows, N, vwA, vwB)
@@ -266,11 +285,12 @@ def run_ours(args, rank, world, device):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
-                     "kernel": "spmm_f16_kernel<2,8> (+ spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
+                     "kernel": "spmm_tc05_kernel<2> (TMA gather4 + tcgen05; + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
         "gpu_launches": launches,
         "clocks": clocks,
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
         "back_to_back_ms": round(b2b_ms, 4),
+        "path_ms": paths,
         "broadcast_ms": round(bcast_ms, 3),
         "shards": [{"nnz": g["nnz"], "nv": g["nv"], "step_ms": round(g["step_ms"], 4)} for g in gathered],
     }

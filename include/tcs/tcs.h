@@ -101,6 +101,11 @@ typedef struct tcs_kernel_config {
     uint32_t flags; /* TCS_CFG_* */
 } tcs_kernel_config;
 
+/* SpMM instruction path (default: tcgen05 + TMA gather where it applies --
+ * FP16 with binary16 values, N <= 256 -- else mma.sync). */
+#define TCS_CFG_PATH_MMA_SYNC 0x1u /* force warp-level mma.sync + 128-bit LDG gathers */
+#define TCS_CFG_PATH_TCGEN05 0x2u  /* require tcgen05.mma + TMA gather4 (ARGUMENT error if inapplicable) */
+
 /* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
  * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);
  * the transaction fields belong to the reference's analytic cost model and

@@ -141,7 +141,7 @@ __device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, float (&ac
 
 // One kernel body for both precisions; Tile/loader/mma chosen by TF32.
 template <bool TF32, int NSC, bool MF32, bool OF32>
-__global__ void __launch_bounds__(kWarps * 32, 4) sddmm_kernel(const SddmmArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
     using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -411,8 +411,15 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : 128;
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
-        const bool direct = b_dtype == need && ldb >= npad && ldb % align_elems == 0 &&
-                            (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+        const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+        // tcgen05 + TMA gather (FP16, binary16 values, N <= 256) unless mma.sync is forced
+        const bool want_tc = A->precision == TCS_FP16 && A->value_dtype == TCS_DTYPE_F16 && n <= 256 &&
+                             !(cfg->flags & TCS_CFG_PATH_MMA_SYNC);
+        if ((cfg->flags & TCS_CFG_PATH_TCGEN05) && !want_tc)
+            fail(TCS_ERR_ARGUMENT, "tcgen05 path needs FP16 with binary16 values and N <= 256");
+        // the TMA path reads B through a tensor map (OOB features zero-filled),
+        // the mma.sync path needs rows padded to npad features
+        const bool direct = b_dtype == need && ldb % align_elems == 0 && aligned && (want_tc || ldb >= npad);
         DBuf bpad;
         const void* bp = b;
         int64_t bld = ldb;
@@ -425,10 +432,23 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         DBuf partial;
         if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
 
+        bool launched = false;
+        if (want_tc)
+            launched = spmm_tc05(A, plan, static_cast<const __half*>(bp), bld, b_rows, n, c, ldc, partial.as<float>(),
+                                 npad, s);
+        if (!launched && (cfg->flags & TCS_CFG_PATH_TCGEN05))
+            fail(TCS_ERR_ARGUMENT, "tcgen05 path unavailable for these operands");
+        if (!launched && bld < npad) {  // fall back to mma.sync: needs padded rows
+            DBuf p2(static_cast<size_t>(std::max<int64_t>(1, b_rows)) * npad * 2, s);
+            pad_convert(bp, TCS_DTYPE_F16, bld, p2.p, TCS_DTYPE_F16, npad, b_rows, n, npad, s);
+            bpad = std::move(p2);
+            bp = bpad.p;
+            bld = npad;
+        }
         SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
                    c, ldc, A->rows, n, partial.as<float>(), npad};
         const int slabs = static_cast<int>(npad / slab);
-        if (plan->n_items) {
+        if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
                 if (slab == 128)

@@ -125,6 +125,10 @@ void pad_convert(const void* src, tcs_dtype sdt, int64_t lds, void* dst, tcs_dty
                  int64_t rows, int64_t cols, int64_t cols_pad, cudaStream_t s);
 
 void check_mebcrs(const tcs_mebcrs* m);
+
+// TMA-gather + tcgen05 SpMM (spmm_tc05.cu); false = not applicable, nothing launched.
+bool spmm_tc05(const tcs_mebcrs* A, const Plan* plan, const __half* B, int64_t ldb, int64_t b_rows, int64_t n,
+               float* c, int64_t ldc, float* partial, int64_t ldp, cudaStream_t s);
 inline cudaStream_t st(tcs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 }  // namespace tcs

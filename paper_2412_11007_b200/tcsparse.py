@@ -67,9 +67,11 @@ class KernelConfig:
     precision: Precision = Precision.fp16
     vector_height: int = 8
     mapping: ThreadMapping = ThreadMapping.coalesced
+    path: str = "auto"  # SpMM instruction path: auto | mma_sync | tcgen05 (tcs.h TCS_CFG_PATH_*)
 
     def _c(self):
-        return _abi.tcs_kernel_config(int(self.precision), int(self.vector_height), int(self.mapping), 0)
+        flags = {"auto": 0, "mma_sync": 1, "tcgen05": 2}[self.path]
+        return _abi.tcs_kernel_config(int(self.precision), int(self.vector_height), int(self.mapping), flags)
 
 
 @dataclass

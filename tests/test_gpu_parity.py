@@ -39,7 +39,7 @@ def rel_l2(got, want):
     return np.linalg.norm(got - want) / (den if den else 1.0)
 
 
-def check_case(case, rec, value_dtype):
+def check_case(case, rec, value_dtype, path="auto"):
     for p in case.precisions:
         if p == 1 and value_dtype == F16:
             continue
@@ -54,10 +54,11 @@ def check_case(case, rec, value_dtype):
         else:  # binary16 storage == the reference's round_to_fp16 of its values
             assert np.array_equal(v.view(np.uint32), O.round_array(ref_me.values, 0).view(np.uint32)), case.name
         cfg = T.KernelConfig(T.Precision(p))
+        scfg = T.KernelConfig(T.Precision(p), path=path if (p == 0 and value_dtype == F16) else "auto")
         if case.B is not None:
             for dense in ([torch.from_numpy(case.B).cuda()] +
                           ([torch.from_numpy(case.B).cuda().half()] if p == 0 else [])):
-                res = T.spmm(me, dense, cfg)
+                res = T.spmm(me, dense, scfg)
                 got = res.output.cpu().numpy()
                 assert cases.sha(got) == rec[f"spmm_{tag}"]["sha"], (case.name, dense.dtype)
                 assert res.counters.mma_invocations == rec[f"spmm_{tag}"]["mma"]
@@ -85,6 +86,18 @@ def test_acceptance2_replay(golden, value_dtype):
     params = cases.acceptance2_params()
     for i in range(200):
         check_case(cases.acceptance2_case(i, params), golden["cases"][f"acc2_{i:03d}"], value_dtype)
+
+
+@pytest.mark.parametrize("path", ["mma_sync", "tcgen05"])
+def test_spmm_instruction_paths_bit_exact(golden, path):
+    """Both SpMM instruction paths (warp mma.sync vs TMA-gather + tcgen05) on
+    the replayed acceptance matrices and C1, FP16 with binary16 values."""
+    params = cases.acceptance2_params()
+    for i in range(0, 200, 3):
+        check_case(cases.acceptance2_case(i, params), golden["cases"][f"acc2_{i:03d}"], F16, path)
+    for case in cases.kat_cases():
+        check_case(case, golden["cases"][case.name], F16, path)
+    check_case(cases.c1_case(False), golden["cases"]["c1"], F16, path)
 
 
 def test_acceptance6_replay(golden):

@@ -64,7 +64,7 @@ def hub_matrix():
 
 
 @pytest.mark.parametrize("p", [0, 1])
-@pytest.mark.parametrize("n", [128, 64, 32, 256, 40])
+@pytest.mark.parametrize("n", [128, 64, 32, 256, 40, 200])
 def test_hub_windows_bit_exact(p, n):
     m = hub_matrix()
     ref = O.encode_mebcrs(m, p)
@@ -73,8 +73,15 @@ def test_hub_windows_bit_exact(p, n):
     assert np.array_equal(rp, ref.row_pointers) and np.array_equal(ci, ref.column_indices)
     assert np.array_equal(v.view(np.uint32), ref.values.view(np.uint32))
     B = O.generate_random_dense(m.cols, n, 5)
+    want = O.spmm(ref, B)
     got = T.spmm(me, torch.from_numpy(B).cuda(), T.KernelConfig(T.Precision(p))).output.cpu().numpy()
-    assert np.array_equal(got.view(np.uint32), O.spmm(ref, B).view(np.uint32))
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if p == 0:  # binary16 storage: both instruction paths, f16 and f32 dense operands
+        me16 = T.encode_mebcrs(dev(m), T.Precision(p), 0)
+        for path in ("mma_sync", "tcgen05"):
+            for dense in (torch.from_numpy(B).cuda(), torch.from_numpy(B).cuda().half()):
+                got = T.spmm(me16, dense, T.KernelConfig(T.Precision(p), path=path)).output.cpu().numpy()
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (path, dense.dtype)
     A = O.generate_random_dense(m.rows, 32, 6)
     Bt = O.generate_random_dense(m.cols, 32, 7)
     out = T.sddmm(T.SddmmOperands(me, torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda()),
