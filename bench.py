@@ -285,7 +285,7 @@ def run_ours(args, rank, world, device):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
-                     "kernel": "spmm_tc05_kernel<2> (TMA gather4 + tcgen05; + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
+                     "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
         "gpu_launches": launches,
         "clocks": clocks,
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),

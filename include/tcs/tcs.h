@@ -101,10 +101,13 @@ typedef struct tcs_kernel_config {
     uint32_t flags; /* TCS_CFG_* */
 } tcs_kernel_config;
 
-/* SpMM instruction path (default: tcgen05 + TMA gather where it applies --
- * FP16 with binary16 values, N <= 256 -- else mma.sync). */
-#define TCS_CFG_PATH_MMA_SYNC 0x1u /* force warp-level mma.sync + 128-bit LDG gathers */
-#define TCS_CFG_PATH_TCGEN05 0x2u  /* require tcgen05.mma + TMA gather4 (ARGUMENT error if inapplicable) */
+/* SpMM instruction path.  Default (0 or TCS_CFG_PATH_MMA_SYNC): warp-level
+ * mma.sync fed by quarter-warp-coalesced 128-bit gathers -- the faster path
+ * on B200 for 8x1 vectors.  TCS_CFG_PATH_TCGEN05 selects
+ * tcgen05.mma (TMEM accumulators) fed by TMA gather4 (FP16, binary16
+ * values, N <= 256; ARGUMENT error otherwise). */
+#define TCS_CFG_PATH_MMA_SYNC 0x1u
+#define TCS_CFG_PATH_TCGEN05 0x2u
 
 /* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
  * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);

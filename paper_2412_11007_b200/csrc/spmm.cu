@@ -53,21 +53,34 @@ struct SpmmArgs {
 constexpr int kWarps = 4;
 
 // ------------------------------------------------------------- FP16 path
+//
+// Gather mapping.  Loads are issued "quarter-warp coalesced": in load slot u
+// (0..3) the 8 lanes of quarter q = lane/8 read ONE 128-byte segment (FPL
+// features per lane) of vector  v(u, q) = 2q + (u & 1) + 8 (u >> 1)  of the
+// 16-vector step -- one L1 wavefront per quarter, the pattern that reaches
+// ~14 TB/s of L2 gather bandwidth on B200 (tools/gather_bench.cu).  The MMA
+// fragment wants lane (g, t) = (lane/4, lane%4) to own vectors 2t, 2t+1,
+// 2t+8, 2t+9 (k slots 0..3) at features FPL*g + [0, FPL): exactly what lane
+// 8t + g loaded in slot u = k-slot, so one shuffle per register moves the
+// data into place and the vector (k) order stays the identity -- the sparse
+// fragment is the natural ME-BCRS pair at 8g + 2t.
 template <int NCHUNK, int FPL, bool VF32>
 struct F16Step {
     static constexpr int NJ = FPL / 2;  // MMAs per chunk == u32 regs per (vector, chunk)
-    uint32_t L[4][NCHUNK][NJ];          // gathered B rows of vectors 2t, 2t+1, 2t+8, 2t+9
+    uint32_t L[4][NCHUNK][NJ];          // loader slots u = 0..3 (vector v(u, lane/8), features FPL*(lane%8))
     uint32_t b[2];                      // sparse fragment: rows g, vectors {2t,2t+1}, {2t+8,2t+9}
 };
 
+__device__ __forceinline__ uint32_t loader_vec(uint32_t u, uint32_t q) { return 2 * q + (u & 1) + 8 * (u >> 1); }
+
 template <int NCHUNK, int FPL, bool VF32>
 __device__ __forceinline__ void f16_load_cols(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
-                                              uint32_t t, uint32_t (&col)[4]) {
-    const uint32_t v0 = s + 2 * t;
-    col[0] = v0 < vend ? __ldg(ci + v0) : 0u;
-    col[1] = v0 + 1 < vend ? __ldg(ci + v0 + 1) : 0u;
-    col[2] = v0 + 8 < vend ? __ldg(ci + v0 + 8) : 0u;
-    col[3] = v0 + 9 < vend ? __ldg(ci + v0 + 9) : 0u;
+                                              uint32_t q, uint32_t (&col)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint32_t v = s + loader_vec(u, q);
+        col[u] = v < vend ? __ldg(ci + v) : 0u;
+    }
 }
 
 template <int NCHUNK, int FPL, bool VF32>
@@ -89,10 +102,11 @@ __device__ __forceinline__ void f16_load_step(const SpmmArgs& a, const __half* _
                                               const uint32_t (&col)[4], F16Step<NCHUNK, FPL, VF32>& st) {
     constexpr int CHUNK = 8 * FPL;
     const uint32_t v0 = s + 2 * t;
-    const uint32_t vv[4] = {v0, v0 + 1, v0 + 8, v0 + 9};
+    const uint32_t vv[4] = {v0, v0 + 1, v0 + 8, v0 + 9};  // fragment vectors (sparse values)
+    const uint32_t q = (4 * g + t) >> 3;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const bool ok = vv[i] < vend;
+        const bool ok = s + loader_vec(i, q) < vend;
         const __half* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
 #pragma unroll
         for (int c = 0; c < NCHUNK; ++c) {
@@ -129,14 +143,20 @@ __device__ __forceinline__ void f16_load_step(const SpmmArgs& a, const __half* _
 }
 
 template <int NCHUNK, int FPL, bool VF32>
-__device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st, float (&acc)[NCHUNK][FPL / 2][4]) {
+__device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st, float (&acc)[NCHUNK][FPL / 2][4],
+                                            uint32_t src_lane) {
 #pragma unroll
     for (int c = 0; c < NCHUNK; ++c)
 #pragma unroll
-        for (int j = 0; j < FPL / 2; ++j)
-            mma_f16_16816(acc[c][j], pack_lo(st.L[0][c][j], st.L[1][c][j]), pack_hi(st.L[0][c][j], st.L[1][c][j]),
-                          pack_lo(st.L[2][c][j], st.L[3][c][j]), pack_hi(st.L[2][c][j], st.L[3][c][j]), st.b[0],
+        for (int j = 0; j < FPL / 2; ++j) {
+            // slot u of lane 8t+g = k-slot u of this lane (see the mapping note above)
+            const uint32_t x0 = __shfl_sync(0xffffffffu, st.L[0][c][j], src_lane);
+            const uint32_t x1 = __shfl_sync(0xffffffffu, st.L[1][c][j], src_lane);
+            const uint32_t x2 = __shfl_sync(0xffffffffu, st.L[2][c][j], src_lane);
+            const uint32_t x3 = __shfl_sync(0xffffffffu, st.L[3][c][j], src_lane);
+            mma_f16_16816(acc[c][j], pack_lo(x0, x1), pack_hi(x0, x1), pack_lo(x2, x3), pack_hi(x2, x3), st.b[0],
                           st.b[1]);
+        }
 }
 
 // Stores FPL consecutive features of one output row (row-major, stride ld).
@@ -166,7 +186,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_kernel(const SpmmArgs
     const uint32_t* ci = a.ci + base;
     const uint64_t vbase = 8ull * base;
     const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
-    const __half* Bl = static_cast<const __half*>(a.B) + feat0 + g * FPL;
+    const uint32_t q = lane >> 3, p = lane & 7;            // loader coordinates (quarter, lane in quarter)
+    const uint32_t src_lane = 8 * t + g;                   // where this lane's fragment data was loaded
+    const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
     const uint32_t vend = it.vend;
 
     float acc[NCHUNK][NJ][4];
@@ -181,18 +203,18 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_kernel(const SpmmArgs
     uint32_t ca[4], cb[4];
     uint32_t s = it.vbeg;
     if (s < vend) {
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s, vend, t, ca);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s, vend, q, ca);
         f16_load_step(a, Bl, vbase, nvw, vend, s, g, t, ca, sa);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 16, vend, t, cb);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 16, vend, q, cb);
     }
     for (; s < vend; s += 32) {
         f16_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, cb, sb);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 32, vend, t, ca);
-        f16_compute(sa, acc);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 32, vend, q, ca);
+        f16_compute(sa, acc, src_lane);
         if (s + 16 >= vend) break;
         f16_load_step(a, Bl, vbase, nvw, vend, s + 32, g, t, ca, sa);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 48, vend, t, cb);
-        f16_compute(sb, acc);
+        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 48, vend, q, cb);
+        f16_compute(sb, acc, src_lane);
     }
 
     // Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
@@ -244,10 +266,12 @@ template <int NCHUNK>
 __device__ __forceinline__ void tf32_load_step(const SpmmArgs& a, const float* __restrict__ Bl, uint64_t vbase,
                                                uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
                                                const uint32_t (&col)[2], Tf32Step<NCHUNK>& st) {
-    const uint32_t vv[2] = {s + t, s + t + 4};
+    const uint32_t vv[2] = {s + t, s + t + 4};  // fragment vectors (sparse values)
+    const uint32_t q = (4 * g + t) >> 3;
 #pragma unroll
     for (int i = 0; i < 2; ++i) {
-        const bool ok = vv[i] < vend;
+        // loader slot i: quarter q reads 128 B (32 features) of vector q + 4i
+        const bool ok = s + q + 4 * i < vend;
         const float* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
 #pragma unroll
         for (int c = 0; c < NCHUNK; ++c) st.L[i][c] = ok ? ld_gather_128(row + c * 32) : make_uint4(0, 0, 0, 0);
@@ -266,11 +290,19 @@ __device__ __forceinline__ void tf32_load_step(const SpmmArgs& a, const float* _
     st.b[1] = to_tf32(x1);
 }
 
+__device__ __forceinline__ uint4 shfl4(uint4 v, uint32_t src) {
+    return make_uint4(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src),
+                      __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
+}
+
+// Loader slot u of lane 8t+g holds vector t + 4u at features 4g..4g+3: the
+// fragment of lane (g, t) for k = t (u = 0) and k = t + 4 (u = 1).
 template <int NCHUNK>
-__device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (&acc)[NCHUNK][2][4]) {
+__device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (&acc)[NCHUNK][2][4],
+                                             uint32_t src_lane) {
 #pragma unroll
     for (int c = 0; c < NCHUNK; ++c) {
-        const uint4 x = st.L[0][c], y = st.L[1][c];
+        const uint4 x = shfl4(st.L[0][c], src_lane), y = shfl4(st.L[1][c], src_lane);
         mma_tf32_1688(acc[c][0], to_tf32(__uint_as_float(x.x)), to_tf32(__uint_as_float(x.y)),
                       to_tf32(__uint_as_float(y.x)), to_tf32(__uint_as_float(y.y)), st.b[0], st.b[1]);
         mma_tf32_1688(acc[c][1], to_tf32(__uint_as_float(x.z)), to_tf32(__uint_as_float(x.w)),
@@ -291,7 +323,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArg
     const uint32_t* ci = a.ci + base;
     const uint64_t vbase = 8ull * base;
     const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
-    const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * g;
+    const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
     const uint32_t vend = it.vend;
 
     float acc[NCHUNK][2][4];
@@ -301,8 +334,8 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArg
         for (int j = 0; j < 2; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
 
     auto cols = [&](uint32_t s, uint32_t (&c)[2]) {
-        c[0] = s + t < vend ? __ldg(ci + s + t) : 0u;
-        c[1] = s + t + 4 < vend ? __ldg(ci + s + t + 4) : 0u;
+        c[0] = s + q < vend ? __ldg(ci + s + q) : 0u;
+        c[1] = s + q + 4 < vend ? __ldg(ci + s + q + 4) : 0u;
     };
     Tf32Step<NCHUNK> sa, sb;
     uint32_t ca[2], cb[2];
@@ -315,11 +348,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArg
     for (; s < vend; s += 16) {
         tf32_load_step(a, Bl, vbase, nvw, vend, s + 8, g, t, cb, sb);
         cols(s + 16, ca);
-        tf32_compute(sa, acc);
+        tf32_compute(sa, acc, src_lane);
         if (s + 8 >= vend) break;
         tf32_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, ca, sa);
         cols(s + 24, cb);
-        tf32_compute(sb, acc);
+        tf32_compute(sb, acc, src_lane);
     }
 
     const bool split = it.slot != kNoSlot;
@@ -412,9 +445,12 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
         const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
-        // tcgen05 + TMA gather (FP16, binary16 values, N <= 256) unless mma.sync is forced
+        // Instruction path.  Default: warp mma.sync fed by quarter-warp-coalesced
+        // LDG.128 gathers (measured faster on B200: 256-B row gathers are
+        // TMA-op-rate bound, tools/gather_bench.cu).  tcgen05 + TMA gather4 on
+        // request (FP16, binary16 values, N <= 256).
         const bool want_tc = A->precision == TCS_FP16 && A->value_dtype == TCS_DTYPE_F16 && n <= 256 &&
-                             !(cfg->flags & TCS_CFG_PATH_MMA_SYNC);
+                             (cfg->flags & TCS_CFG_PATH_TCGEN05);
         if ((cfg->flags & TCS_CFG_PATH_TCGEN05) && !want_tc)
             fail(TCS_ERR_ARGUMENT, "tcgen05 path needs FP16 with binary16 values and N <= 256");
         // the TMA path reads B through a tensor map (OOB features zero-filled),
