@@ -48,9 +48,28 @@ struct SpmmArgs {
     int64_t N;
     float* partial;  // [slot][8][ldp]
     int64_t ldp;
+    uint32_t* counter;  // per-slab work-item counters (zeroed before launch)
 };
 
 constexpr int kWarps = 4;
+
+// ------------------------------------------------------------- scheduling
+// Persistent warps: each warp claims work items from a per-slab counter
+// (atomicAdd by lane 0, broadcast by shuffle) until the list is exhausted,
+// so no warp slot idles behind a long item of a sibling warp.  Items are
+// ordered longest-first by the planner (split-window segments lead).
+__device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1u);
+    return __shfl_sync(0xffffffffu, i, 0);
+}
+
+// Column indices of a 2-step (32-vector) window of the item, one per lane,
+// loaded coalesced; slots pick theirs with a shuffle.
+__device__ __forceinline__ uint32_t load_colpair(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
+                                                 uint32_t lane) {
+    return s + lane < vend ? __ldg(ci + s + lane) : 0u;
+}
 
 // ------------------------------------------------------------- FP16 path
 //
@@ -73,17 +92,7 @@ struct F16Step {
 
 __device__ __forceinline__ uint32_t loader_vec(uint32_t u, uint32_t q) { return 2 * q + (u & 1) + 8 * (u >> 1); }
 
-template <int NCHUNK, int FPL, bool VF32>
-__device__ __forceinline__ void f16_load_cols(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
-                                              uint32_t q, uint32_t (&col)[4]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const uint32_t v = s + loader_vec(u, q);
-        col[u] = v < vend ? __ldg(ci + v) : 0u;
-    }
-}
-
-template <int NCHUNK, int FPL, bool VF32>
+template <bool VF32>
 __device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t vbase, uint32_t nvw, uint32_t v,
                                                     uint32_t g) {
     if (v >= nvw) return 0u;
@@ -96,32 +105,33 @@ __device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t v
     }
 }
 
+// Issues the gathers + sparse-value loads of the 16-vector step at s.
+// colpair holds the column indices of vectors [s - 16*half, +32).
 template <int NCHUNK, int FPL, bool VF32>
-__device__ __forceinline__ void f16_load_step(const SpmmArgs& a, const __half* __restrict__ Bl, uint64_t vbase,
-                                              uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
-                                              const uint32_t (&col)[4], F16Step<NCHUNK, FPL, VF32>& st) {
+__device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __restrict__ Bl, uint64_t vbase,
+                                          uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t, uint32_t q,
+                                          uint32_t colpair, uint32_t half, F16Step<NCHUNK, FPL, VF32>& st) {
     constexpr int CHUNK = 8 * FPL;
-    const uint32_t v0 = s + 2 * t;
-    const uint32_t vv[4] = {v0, v0 + 1, v0 + 8, v0 + 9};  // fragment vectors (sparse values)
-    const uint32_t q = (4 * g + t) >> 3;
+    uint32_t col[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const bool ok = s + loader_vec(i, q) < vend;
-        const __half* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
+    for (int u = 0; u < 4; ++u) col[u] = __shfl_sync(0xffffffffu, colpair, 16 * half + loader_vec(u, q));
+    if (s + 16 <= vend) {
+        // full step (warp-uniform): no predicates; both k=8 blocks are full width
 #pragma unroll
-        for (int c = 0; c < NCHUNK; ++c) {
-            if constexpr (FPL == 8) {
-                uint4 x = ok ? ld_gather_128(row + c * CHUNK) : make_uint4(0, 0, 0, 0);
-                st.L[i][c][0] = x.x; st.L[i][c][1] = x.y; st.L[i][c][2] = x.z; st.L[i][c][3] = x.w;
-            } else {
-                uint2 x = ok ? ld_gather_64(row + c * CHUNK) : make_uint2(0, 0);
-                st.L[i][c][0] = x.x; st.L[i][c][1] = x.y;
+        for (int u = 0; u < 4; ++u) {
+            const __half* row = Bl + static_cast<uint64_t>(col[u]) * a.ldb;
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                if constexpr (FPL == 8) {
+                    const uint4 x = ld_gather_128(row + c * CHUNK);
+                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y; st.L[u][c][2] = x.z; st.L[u][c][3] = x.w;
+                } else {
+                    const uint2 x = ld_gather_64(row + c * CHUNK);
+                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y;
+                }
             }
         }
-    }
-    if (s + 16 <= vend && s + 16 <= nvw) {
-        // both k=8 blocks are full width: rows g, slots 2t..2t+1 of blocks s/8, s/8+1
-        const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;
+        const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;  // rows g, slots 2t..2t+1 of blocks s/8, s/8+1
         if constexpr (VF32) {
             const float* fv = static_cast<const float*>(a.vals);
             const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
@@ -133,10 +143,27 @@ __device__ __forceinline__ void f16_load_step(const SpmmArgs& a, const __half* _
             st.b[1] = ld_stream_u32(hv + off + 64);
         }
     } else {
-        const uint32_t e0 = vv[0] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[0], g) : 0u;
-        const uint32_t e1 = vv[1] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[1], g) : 0u;
-        const uint32_t e2 = vv[2] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[2], g) : 0u;
-        const uint32_t e3 = vv[3] < vend ? f16_val_general<NCHUNK, FPL, VF32>(a.vals, vbase, nvw, vv[3], g) : 0u;
+        // residue step: vectors at or past vend contribute zero registers
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const bool ok = s + loader_vec(u, q) < vend;
+            const __half* row = Bl + static_cast<uint64_t>(col[u]) * a.ldb;
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                if constexpr (FPL == 8) {
+                    const uint4 x = ok ? ld_gather_128(row + c * CHUNK) : make_uint4(0, 0, 0, 0);
+                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y; st.L[u][c][2] = x.z; st.L[u][c][3] = x.w;
+                } else {
+                    const uint2 x = ok ? ld_gather_64(row + c * CHUNK) : make_uint2(0, 0);
+                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y;
+                }
+            }
+        }
+        const uint32_t v0 = s + 2 * t;
+        const uint32_t e0 = v0 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0, g) : 0u;
+        const uint32_t e1 = v0 + 1 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 1, g) : 0u;
+        const uint32_t e2 = v0 + 8 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 8, g) : 0u;
+        const uint32_t e3 = v0 + 9 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 9, g) : 0u;
         st.b[0] = e0 | (e1 << 16);
         st.b[1] = e2 | (e3 << 16);
     }
@@ -176,82 +203,90 @@ __device__ __forceinline__ void store_row(float* __restrict__ dst, const float (
 template <int NCHUNK, int FPL, bool VF32>
 __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
-    if (idx >= a.n_items) return;
-    const WorkItem it = a.items[idx];
-    const uint32_t g = lane >> 2, t = lane & 3;
-    const uint32_t base = __ldg(a.rp + it.window);
-    const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
-    const uint32_t* ci = a.ci + base;
-    const uint64_t vbase = 8ull * base;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;             // fragment coordinates
+    const uint32_t q = lane >> 3, p = lane & 7;             // loader coordinates (quarter, lane in quarter)
+    const uint32_t src_lane = 8 * t + g;                    // where this lane's fragment data was loaded
     const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
-    const uint32_t q = lane >> 3, p = lane & 7;            // loader coordinates (quarter, lane in quarter)
-    const uint32_t src_lane = 8 * t + g;                   // where this lane's fragment data was loaded
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    const uint32_t vend = it.vend;
+    uint32_t* counter = a.counter + blockIdx.y;
 
-    float acc[NCHUNK][NJ][4];
-#pragma unroll
-    for (int c = 0; c < NCHUNK; ++c)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
 
-    // Software pipeline: column indices two steps ahead, gathered rows and
-    // sparse values one step ahead of the MMAs.
-    F16Step<NCHUNK, FPL, VF32> sa, sb;
-    uint32_t ca[4], cb[4];
-    uint32_t s = it.vbeg;
-    if (s < vend) {
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s, vend, q, ca);
-        f16_load_step(a, Bl, vbase, nvw, vend, s, g, t, ca, sa);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 16, vend, q, cb);
-    }
-    for (; s < vend; s += 32) {
-        f16_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, cb, sb);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 32, vend, q, ca);
-        f16_compute(sa, acc, src_lane);
-        if (s + 16 >= vend) break;
-        f16_load_step(a, Bl, vbase, nvw, vend, s + 32, g, t, ca, sa);
-        f16_load_cols<NCHUNK, FPL, VF32>(ci, s + 48, vend, q, cb);
-        f16_compute(sb, acc, src_lane);
-    }
+        float acc[NCHUNK][NJ][4];
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
 
-    // Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
-    // of every chunk (accumulator layout, ref fragment.hpp:60-66).
-    const bool split = it.slot != kNoSlot;
-#pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-        const uint32_t r = 2 * t + rr;
-        const uint64_t row = 8ull * it.window + r;
-        float* dst;
-        bool vec_ok;
-        if (split) {
-            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
-            vec_ok = true;
-        } else {
-            if (row >= a.rows) continue;
-            dst = a.C + row * a.ldc;
-            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
-        }
-#pragma unroll
-        for (int c = 0; c < NCHUNK; ++c) {
-            float v[FPL];
-#pragma unroll
-            for (int j = 0; j < NJ; ++j) {
-                v[2 * j] = acc[c][j][rr];
-                v[2 * j + 1] = acc[c][j][2 + rr];
+        // Software pipeline: gathers one step ahead of the MMAs, column
+        // indices (coalesced, 32 per load) two steps ahead of the gathers.
+        F16Step<NCHUNK, FPL, VF32> sa, sb;
+        uint32_t s = it.vbeg;
+        if (s < vend) {
+            uint32_t cp0 = load_colpair(ci, s, vend, lane);       // steps s, s+16
+            uint32_t cp1 = load_colpair(ci, s + 32, vend, lane);  // steps s+32, s+48
+            f16_issue(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa);
+            for (;;) {
+                if (s + 16 < vend) f16_issue(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb);
+                f16_compute(sa, acc, src_lane);
+                if (s + 16 >= vend) break;
+                if (s + 32 < vend) f16_issue(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa);
+                cp0 = cp1;
+                cp1 = load_colpair(ci, s + 64, vend, lane);
+                f16_compute(sb, acc, src_lane);
+                s += 32;
+                if (s >= vend) break;
             }
-            const int64_t feat = feat0 + c * CHUNK + FPL * g;
-            store_row<FPL>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        }
+
+        // Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
+        // of every chunk (accumulator layout, ref fragment.hpp:60-66).
+        const bool split = it.slot != kNoSlot;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const uint32_t r = 2 * t + rr;
+            const uint64_t row = 8ull * it.window + r;
+            float* dst;
+            bool vec_ok;
+            if (split) {
+                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+                vec_ok = true;
+            } else {
+                if (row >= a.rows) continue;
+                dst = a.C + row * a.ldc;
+                vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+            }
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                float v[FPL];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    v[2 * j] = acc[c][j][rr];
+                    v[2 * j + 1] = acc[c][j][2 + rr];
+                }
+                const int64_t feat = feat0 + c * CHUNK + FPL * g;
+                store_row<FPL>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+            }
         }
     }
 }
 
 // ------------------------------------------------------------- TF32 path
+//
+// Same scheme with m16n8k8.tf32: an 8-vector step; loader slot u (0, 1) of
+// quarter q reads 128 B (32 features) of vector q + 4u; lane 8t + g then
+// holds exactly the (vector t + 4u, features 4g..4g+3) fragment data of
+// lane (g, t).  Operands are rounded RNE with cvt.rn.tf32.f32.
 template <int NCHUNK>
 struct Tf32Step {
-    uint4 L[2][NCHUNK];  // rows of vectors t, t+4; 4 consecutive features per chunk
+    uint4 L[2][NCHUNK];  // loader slots: vector q + 4u, features 32c + 4p .. +3
     uint32_t b[2];       // sparse fragment: row g, vectors t, t+4
 };
 
@@ -262,29 +297,37 @@ __device__ __forceinline__ float tf32_val_general(const float* vals, uint64_t vb
     return __ldg(vals + vbase + 32ull * b + g * width + j);
 }
 
+// colquad holds the column indices of vectors [s - 8*sub, +32) (4 steps).
 template <int NCHUNK>
-__device__ __forceinline__ void tf32_load_step(const SpmmArgs& a, const float* __restrict__ Bl, uint64_t vbase,
-                                               uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
-                                               const uint32_t (&col)[2], Tf32Step<NCHUNK>& st) {
-    const uint32_t vv[2] = {s + t, s + t + 4};  // fragment vectors (sparse values)
-    const uint32_t q = (4 * g + t) >> 3;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        // loader slot i: quarter q reads 128 B (32 features) of vector q + 4i
-        const bool ok = s + q + 4 * i < vend;
-        const float* row = Bl + static_cast<uint64_t>(col[i]) * a.ldb;
-#pragma unroll
-        for (int c = 0; c < NCHUNK; ++c) st.L[i][c] = ok ? ld_gather_128(row + c * 32) : make_uint4(0, 0, 0, 0);
-    }
+__device__ __forceinline__ void tf32_issue(const SpmmArgs& a, const float* __restrict__ Bl, uint64_t vbase,
+                                           uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t,
+                                           uint32_t q, uint32_t colquad, uint32_t sub, Tf32Step<NCHUNK>& st) {
+    const uint32_t c0 = __shfl_sync(0xffffffffu, colquad, 8 * sub + q);
+    const uint32_t c1 = __shfl_sync(0xffffffffu, colquad, 8 * sub + q + 4);
     const float* fv = static_cast<const float*>(a.vals);
     float x0, x1;
-    if (s + 8 <= vend && s + 8 <= nvw) {
+    if (s + 8 <= vend) {
+        const float* r0 = Bl + static_cast<uint64_t>(c0) * a.ldb;
+        const float* r1 = Bl + static_cast<uint64_t>(c1) * a.ldb;
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            st.L[0][c] = ld_gather_128(r0 + c * 32);
+            st.L[1][c] = ld_gather_128(r1 + c * 32);
+        }
         const uint64_t off = vbase + 8ull * s + 4 * g + t;
         x0 = __uint_as_float(ld_stream_u32(fv + off));
         x1 = __uint_as_float(ld_stream_u32(fv + off + 32));
     } else {
-        x0 = vv[0] < vend ? tf32_val_general(fv, vbase, nvw, vv[0], g) : 0.f;
-        x1 = vv[1] < vend ? tf32_val_general(fv, vbase, nvw, vv[1], g) : 0.f;
+        const bool ok0 = s + q < vend, ok1 = s + q + 4 < vend;
+        const float* r0 = Bl + static_cast<uint64_t>(c0) * a.ldb;
+        const float* r1 = Bl + static_cast<uint64_t>(c1) * a.ldb;
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            st.L[0][c] = ok0 ? ld_gather_128(r0 + c * 32) : make_uint4(0, 0, 0, 0);
+            st.L[1][c] = ok1 ? ld_gather_128(r1 + c * 32) : make_uint4(0, 0, 0, 0);
+        }
+        x0 = s + t < vend ? tf32_val_general(fv, vbase, nvw, s + t, g) : 0.f;
+        x1 = s + t + 4 < vend ? tf32_val_general(fv, vbase, nvw, s + t + 4, g) : 0.f;
     }
     st.b[0] = to_tf32(x0);
     st.b[1] = to_tf32(x1);
@@ -295,8 +338,6 @@ __device__ __forceinline__ uint4 shfl4(uint4 v, uint32_t src) {
                       __shfl_sync(0xffffffffu, v.z, src), __shfl_sync(0xffffffffu, v.w, src));
 }
 
-// Loader slot u of lane 8t+g holds vector t + 4u at features 4g..4g+3: the
-// fragment of lane (g, t) for k = t (u = 0) and k = t + 4 (u = 1).
 template <int NCHUNK>
 __device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (&acc)[NCHUNK][2][4],
                                              uint32_t src_lane) {
@@ -313,68 +354,80 @@ __device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (
 template <int NCHUNK>
 __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArgs a) {
     constexpr int SLAB = NCHUNK * 32;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
-    if (idx >= a.n_items) return;
-    const WorkItem it = a.items[idx];
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
-    const uint32_t base = __ldg(a.rp + it.window);
-    const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
-    const uint32_t* ci = a.ci + base;
-    const uint64_t vbase = 8ull * base;
-    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
     const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
-    const uint32_t vend = it.vend;
+    uint32_t* counter = a.counter + blockIdx.y;
 
-    float acc[NCHUNK][2][4];
-#pragma unroll
-    for (int c = 0; c < NCHUNK; ++c)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
 
-    auto cols = [&](uint32_t s, uint32_t (&c)[2]) {
-        c[0] = s + q < vend ? __ldg(ci + s + q) : 0u;
-        c[1] = s + q + 4 < vend ? __ldg(ci + s + q + 4) : 0u;
-    };
-    Tf32Step<NCHUNK> sa, sb;
-    uint32_t ca[2], cb[2];
-    uint32_t s = it.vbeg;
-    if (s < vend) {
-        cols(s, ca);
-        tf32_load_step(a, Bl, vbase, nvw, vend, s, g, t, ca, sa);
-        cols(s + 8, cb);
-    }
-    for (; s < vend; s += 16) {
-        tf32_load_step(a, Bl, vbase, nvw, vend, s + 8, g, t, cb, sb);
-        cols(s + 16, ca);
-        tf32_compute(sa, acc, src_lane);
-        if (s + 8 >= vend) break;
-        tf32_load_step(a, Bl, vbase, nvw, vend, s + 16, g, t, ca, sa);
-        cols(s + 24, cb);
-        tf32_compute(sb, acc, src_lane);
-    }
-
-    const bool split = it.slot != kNoSlot;
+        float acc[NCHUNK][2][4];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-        const uint32_t r = 2 * t + rr;
-        const uint64_t row = 8ull * it.window + r;
-        float* dst;
-        bool vec_ok;
-        if (split) {
-            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
-            vec_ok = true;
-        } else {
-            if (row >= a.rows) continue;
-            dst = a.C + row * a.ldc;
-            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+        for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+
+        Tf32Step<NCHUNK> sa, sb;
+        uint32_t s = it.vbeg;
+        if (s < vend) {
+            // colquad: 32 vectors = 4 steps; cur covers [s0, s0+32), nxt the next 32
+            uint32_t s0 = s;
+            uint32_t cur = load_colpair(ci, s0, vend, lane);
+            uint32_t nxt = load_colpair(ci, s0 + 32, vend, lane);
+            tf32_issue(a, Bl, vbase, nvw, vend, s, g, t, q, cur, 0, sa);
+            for (;;) {
+                // issue s + 8 into sb
+                if (s + 8 < vend) {
+                    const uint32_t sub = (s + 8 - s0) >> 3;
+                    tf32_issue(a, Bl, vbase, nvw, vend, s + 8, g, t, q, sub < 4 ? cur : nxt, sub & 3, sb);
+                }
+                tf32_compute(sa, acc, src_lane);
+                if (s + 8 >= vend) break;
+                if (s + 16 < vend) {
+                    uint32_t sub = (s + 16 - s0) >> 3;
+                    if (sub >= 4) {  // advance the column window
+                        s0 += 32;
+                        cur = nxt;
+                        nxt = load_colpair(ci, s0 + 32, vend, lane);
+                        sub -= 4;
+                    }
+                    tf32_issue(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cur, sub, sa);
+                }
+                tf32_compute(sb, acc, src_lane);
+                s += 16;
+                if (s >= vend) break;
+            }
         }
+
+        const bool split = it.slot != kNoSlot;
 #pragma unroll
-        for (int c = 0; c < NCHUNK; ++c) {
-            const float v[4] = {acc[c][0][rr], acc[c][0][2 + rr], acc[c][1][rr], acc[c][1][2 + rr]};
-            const int64_t feat = feat0 + c * 32 + 4 * g;
-            store_row<4>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        for (int rr = 0; rr < 2; ++rr) {
+            const uint32_t r = 2 * t + rr;
+            const uint64_t row = 8ull * it.window + r;
+            float* dst;
+            bool vec_ok;
+            if (split) {
+                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+                vec_ok = true;
+            } else {
+                if (row >= a.rows) continue;
+                dst = a.C + row * a.ldc;
+                vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+            }
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                const float v[4] = {acc[c][0][rr], acc[c][0][2 + rr], acc[c][1][rr], acc[c][1][2 + rr]};
+                const int64_t feat = feat0 + c * 32 + 4 * g;
+                store_row<4>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+            }
         }
     }
 }
@@ -396,9 +449,13 @@ __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __re
     }
 }
 
+// Persistent launch: up to 4 CTAs (16 warps) per SM per slab; warps pull
+// items from the slab's counter.
 template <typename K>
 void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name) {
-    const dim3 grid(static_cast<unsigned>((a.n_items + kWarps - 1) / kWarps), slabs);
+    const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * 4 / std::max(1, slabs));
+    const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
+    const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
     TCS_LAUNCHED(name);
 }
@@ -481,9 +538,14 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
             bp = bpad.p;
             bld = npad;
         }
-        SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
-                   c, ldc, A->rows, n, partial.as<float>(), npad};
         const int slabs = static_cast<int>(npad / slab);
+        DBuf item_ctr;
+        if (!launched && plan->n_items) {
+            item_ctr = DBuf(slabs * sizeof(uint32_t), s);
+            TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * sizeof(uint32_t), s));
+        }
+        SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
+                   c, ldc, A->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>()};
         if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
