@@ -1,24 +1,33 @@
 // CSR -> ME-BCRS conversion as a GPU pipeline, bit-exact with the reference
 // encoder (ref mebcrs.hpp:80-114, partition.hpp:40-66).
 //
-//   K0 csr_check     one thread per row: CSR invariants (ref matrix.hpp:31-48)
-//                    + longest window (entries) -> picks the merge kernel.
-//   K1 window_merge  one CTA per 8-row window: the window's 8 rows are 8
-//                    sorted runs of column indices; three rounds of CTA-wide
-//                    merge-path merging (keys = col<<32 | entry) give the
-//                    window's entries in (column, row) order; a block scan of
-//                    "first of its column" flags yields, per entry, the rank
-//                    of its column among the window's distinct columns (its
-//                    vector slot) and the window's vector count nv_w.
-//                    Runs in shared memory (<= 2048 entries, 128 threads;
-//                    <= 12288 entries, 512 threads) or, for hub windows,
-//                    in a global scratch buffer with the same code.
-//   K2 scan          row_pointers = exclusive scan of nv_w (u32, as the ref).
-//   K3 window_scatter one CTA per window: writes column_indices and places
-//                    every CSR value at 8*(rp[w]+b*k) + r*width_b + j,
-//                    width_b = min(k, nv_w - b*k) (ref mebcrs.hpp:46-56), all
-//                    other slots 0.  F16 storage rounds with __float2half_rn
-//                    (bit-identical to ref round_to_fp16); F32 keeps raw bits.
+// The reference partitions each 8-row window by concatenating its rows'
+// column lists, sorting and de-duplicating (ref partition.hpp:55-64); the
+// k-th distinct column is vector slot k (ascending).  Here every window is
+// one CTA task and the per-entry output is the RANK of its column among the
+// window's distinct columns:
+//
+//   K0 window_stats   thread per window: row_ptr invariants (ref
+//                     matrix.hpp:31-48) and the longest window -> kernel pick.
+//   K1 window ranks, one of:
+//      window_sort    <= 2048 entries (128 thr) / <= 12288 (512 thr, 192 KB smem)
+//                     / longer (global scratch): the window's 8 rows are 8
+//                     sorted runs; three rounds of CTA-wide merge-path merging
+//                     (keys col<<32 | entry) + a block scan of "first of its
+//                     column" flags give each entry's rank and nv_w.
+//      window_bitmap  long windows when the column space fits shared memory
+//                     (<= 819,200 columns): set one bit per column, prefix-
+//                     popcount the words -> rank(c) = prefix[c/32] +
+//                     popc(word & below(c)); sorted unique columns fall out of
+//                     the word scan.  O(cols/32 + entries) per window.
+//                     Both validate the column indices of their window (range,
+//                     strictly ascending within a row).
+//   K2 scan           row_pointers = exclusive scan of nv_w (u32, as the ref).
+//   K3 window_scatter CTA per window: column_indices, and every CSR value to
+//                     8*(rp[w]+b*k) + r*width_b + j, width_b = min(k, nv_w-b*k)
+//                     (ref mebcrs.hpp:46-56); all other slots 0.  F16 storage
+//                     rounds with __float2half_rn (== ref round_to_fp16, checked
+//                     exhaustively on device by the tests); F32 keeps raw bits.
 #include <algorithm>
 
 #include "tcs_internal.cuh"
@@ -30,29 +39,28 @@ constexpr uint32_t kSmallCap = 2048;    // entries per window, 128-thread CTA, 3
 constexpr uint32_t kSmallThreads = 128;
 constexpr uint32_t kBigCap = 12288;     // 512-thread CTA, 192 KB smem
 constexpr uint32_t kBigThreads = 512;
+constexpr uint32_t kBitmapThreads = 512;
+constexpr uint32_t kBitmapMaxWords = 25600;  // 2 x 100 KB of smem -> <= 819,200 columns
 constexpr uint64_t kSentinel = ~0ull;
 
 struct CheckOut {
     uint32_t max_window_entries;
-    uint32_t bad;  // nonzero = first violated invariant code
+    uint32_t bad;  // nonzero = violated invariant code (see kBadMsg)
 };
 
-__global__ void csr_check(const uint32_t* __restrict__ rp, const uint32_t* __restrict__ ci, uint64_t rows,
-                          uint64_t cols, uint64_t nnz, CheckOut* out) {
+__global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uint64_t W, uint64_t nnz,
+                             CheckOut* out) {
     uint32_t mx = 0, bad = 0;
-    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows;
-         r += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t b = rp[r], e = rp[r + 1];
-        if (b > e) { bad = 1; continue; }
-        if (e > nnz) { bad = 2; continue; }
-        uint32_t prev = 0;
-        for (uint32_t p = b; p < e; ++p) {
-            const uint32_t c = ci[p];
-            if (c >= cols) bad = 3;
-            if (p > b && prev >= c) bad = 4;
-            prev = c;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r0 = 8 * w, r1 = min(r0 + 8, rows);
+        uint32_t prev = rp[r0];
+        for (uint64_t r = r0 + 1; r <= r1; ++r) {
+            const uint32_t x = rp[r];
+            if (x < prev) bad = max(bad, 1u);
+            prev = x;
         }
-        if ((r & 7) == 0) mx = max(mx, rp[min(r + 8, rows)] - b);
+        if (prev > nnz) bad = max(bad, 2u);
+        if (!bad) mx = max(mx, prev - rp[r0]);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -63,6 +71,18 @@ __global__ void csr_check(const uint32_t* __restrict__ rp, const uint32_t* __res
         atomicMax(&out->max_window_entries, mx);
         if (bad) atomicMax(&out->bad, bad);
     }
+}
+
+// Column index i (window-local) of the window whose row boundaries are rb[0..8]:
+// in range and strictly greater than its predecessor in the same row.
+__device__ __forceinline__ uint32_t check_col(const uint32_t* __restrict__ ci, uint32_t e0, uint32_t i, uint32_t c,
+                                              const uint32_t* rb, uint64_t cols) {
+    uint32_t bad = c >= cols ? 3u : 0u;
+    bool row_start = false;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) row_start |= (i == rb[r]);
+    if (!row_start && __ldg(ci + e0 + i - 1) >= c) bad = 4u;
+    return bad;
 }
 
 // Merge adjacent pairs of sorted runs src[bnd[2q] .. bnd[2q+1]) and
@@ -107,9 +127,9 @@ __device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restric
 // One window's merge + unique + rank, executed by the whole CTA.
 // bufA/bufB hold >= n keys each (shared or global).
 __device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint32_t* __restrict__ ci,
-                                 uint64_t rows, uint64_t w, uint64_t* bufA, uint64_t* bufB,
+                                 uint64_t rows, uint64_t cols, uint64_t w, uint64_t* bufA, uint64_t* bufB,
                                  uint32_t* __restrict__ tmp_cols, uint32_t* __restrict__ rank,
-                                 uint32_t* __restrict__ nv_out) {
+                                 uint32_t* __restrict__ nv_out, CheckOut* chk) {
     __shared__ uint32_t bnd[9];
     __shared__ uint32_t bnd2[5];
     __shared__ uint32_t bnd3[3];
@@ -120,8 +140,13 @@ __device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint
     const uint32_t n = bnd[8];
     if (threadIdx.x < 5) bnd2[threadIdx.x] = bnd[2 * threadIdx.x];
     if (threadIdx.x < 3) bnd3[threadIdx.x] = bnd[4 * threadIdx.x];
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-        bufA[i] = (static_cast<uint64_t>(ci[e0 + i]) << 32) | i;
+    uint32_t bad = 0;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t c = ci[e0 + i];
+        bad = max(bad, check_col(ci, e0, i, c, bnd, cols));
+        bufA[i] = (static_cast<uint64_t>(c) << 32) | i;
+    }
+    if (bad) atomicMax(&chk->bad, bad);
     __syncthreads();
     merge_pass(bufA, bufB, bnd, 8, n);
     __syncthreads();
@@ -152,26 +177,28 @@ __device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint
     __syncthreads();  // bnd / buffers are reused by the next window
 }
 
-__global__ void __launch_bounds__(kSmallThreads) window_merge_small(const uint32_t* __restrict__ csr_rp,
-                                                                    const uint32_t* __restrict__ ci, uint64_t rows,
-                                                                    uint64_t W, uint32_t* __restrict__ tmp_cols,
-                                                                    uint32_t* __restrict__ rank,
-                                                                    uint32_t* __restrict__ nv_out) {
+__global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_t* __restrict__ csr_rp,
+                                                                   const uint32_t* __restrict__ ci, uint64_t rows,
+                                                                   uint64_t cols, uint64_t W,
+                                                                   uint32_t* __restrict__ tmp_cols,
+                                                                   uint32_t* __restrict__ rank,
+                                                                   uint32_t* __restrict__ nv_out, CheckOut* chk) {
     __shared__ uint64_t bufA[kSmallCap];
     __shared__ uint64_t bufB[kSmallCap];
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
         const uint32_t n = csr_rp[min(8 * w + 8, rows)] - csr_rp[8 * w];
         if (n > kSmallCap) continue;  // block-uniform
-        window_sort_rank(csr_rp, ci, rows, w, bufA, bufB, tmp_cols, rank, nv_out);
+        window_sort_rank(csr_rp, ci, rows, cols, w, bufA, bufB, tmp_cols, rank, nv_out, chk);
     }
 }
 
-__global__ void __launch_bounds__(kBigThreads) window_merge_big(const uint32_t* __restrict__ csr_rp,
-                                                                const uint32_t* __restrict__ ci, uint64_t rows,
-                                                                uint64_t W, uint64_t* __restrict__ scratch,
-                                                                uint32_t* __restrict__ tmp_cols,
-                                                                uint32_t* __restrict__ rank,
-                                                                uint32_t* __restrict__ nv_out) {
+__global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* __restrict__ csr_rp,
+                                                               const uint32_t* __restrict__ ci, uint64_t rows,
+                                                               uint64_t cols, uint64_t W,
+                                                               uint64_t* __restrict__ scratch,
+                                                               uint32_t* __restrict__ tmp_cols,
+                                                               uint32_t* __restrict__ rank,
+                                                               uint32_t* __restrict__ nv_out, CheckOut* chk) {
     extern __shared__ uint64_t smem_keys[];
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
         const uint32_t e0 = csr_rp[8 * w];
@@ -185,7 +212,62 @@ __global__ void __launch_bounds__(kBigThreads) window_merge_big(const uint32_t* 
             a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
             b = a + n;
         }
-        window_sort_rank(csr_rp, ci, rows, w, a, b, tmp_cols, rank, nv_out);
+        window_sort_rank(csr_rp, ci, rows, cols, w, a, b, tmp_cols, rank, nv_out, chk);
+    }
+}
+
+// Bitmap ranking for windows with more than kSmallCap entries.
+__global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* __restrict__ csr_rp,
+                                                                const uint32_t* __restrict__ ci, uint64_t rows,
+                                                                uint64_t cols, uint64_t W,
+                                                                uint32_t* __restrict__ tmp_cols,
+                                                                uint32_t* __restrict__ rank,
+                                                                uint32_t* __restrict__ nv_out, CheckOut* chk) {
+    extern __shared__ uint32_t bm_smem[];
+    const uint32_t words = static_cast<uint32_t>((cols + 31) / 32);
+    uint32_t* bm = bm_smem;
+    uint32_t* pre = bm_smem + words;
+    __shared__ uint32_t rb[9];
+    const uint32_t nt = blockDim.x, wpt = (words + nt - 1) / nt;
+    for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+        const uint64_t r0 = 8 * w;
+        const uint32_t e0 = csr_rp[r0];
+        const uint32_t n = csr_rp[min(r0 + 8, rows)] - e0;
+        if (n <= kSmallCap) continue;  // block-uniform
+        if (threadIdx.x < 9) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
+        for (uint32_t i = threadIdx.x; i < words; i += nt) bm[i] = 0u;
+        __syncthreads();
+        uint32_t bad = 0;
+        for (uint32_t i = threadIdx.x; i < n; i += nt) {
+            const uint32_t c = ci[e0 + i];
+            const uint32_t b = check_col(ci, e0, i, c, rb, cols);
+            bad = max(bad, b);
+            if (!b || b == 4u) atomicOr(&bm[c >> 5], 1u << (c & 31));
+        }
+        if (bad) atomicMax(&chk->bad, bad);
+        __syncthreads();
+        // prefix popcount over this thread's contiguous chunk of words
+        const uint32_t w0 = min(words, threadIdx.x * wpt), w1 = min(words, w0 + wpt);
+        uint32_t cnt = 0;
+        for (uint32_t i = w0; i < w1; ++i) cnt += __popc(bm[i]);
+        uint32_t total;
+        uint32_t run = dev::block_exclusive_scan(cnt, &total);
+        for (uint32_t i = w0; i < w1; ++i) {
+            pre[i] = run;
+            uint32_t bits = bm[i];
+            while (bits) {  // sorted unique columns of the window
+                const uint32_t b = __ffs(bits) - 1;
+                tmp_cols[e0 + run++] = 32 * i + b;
+                bits &= bits - 1;
+            }
+        }
+        if (threadIdx.x == 0) nv_out[w] = total;
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < n; i += nt) {
+            const uint32_t c = ci[e0 + i];
+            if (c < cols) rank[e0 + i] = pre[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
+        }
+        __syncthreads();
     }
 }
 
@@ -196,6 +278,12 @@ __device__ __forceinline__ float store_cvt<float>(float x) { return x; }
 template <>
 __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2half_rn(x); }
 
+// The value blocks of a window are contiguous ([8*rp[w], 8*rp[w+1])); they
+// are assembled in shared memory a tile of kScatterTile vectors at a time
+// (zero fill + scatter of the tile's entries) and written out with 16-byte
+// coalesced stores -- every value byte hits global memory exactly once.
+constexpr uint32_t kScatterTile = 4096;  // vectors per smem tile (multiple of k)
+
 template <typename V>
 __global__ void __launch_bounds__(256) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
@@ -203,6 +291,8 @@ __global__ void __launch_bounds__(256) window_scatter(const uint32_t* __restrict
                                                       const uint32_t* __restrict__ tmp_cols,
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals) {
+    extern __shared__ uint4 tile_raw[];
+    V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[9];
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
         const uint64_t r0 = 8 * w;
@@ -212,20 +302,32 @@ __global__ void __launch_bounds__(256) window_scatter(const uint32_t* __restrict
         const uint32_t e0 = rb[0], e1 = rb[8];
         for (uint32_t i = threadIdx.x; i < nvw; i += blockDim.x) out_ci[base + i] = tmp_cols[e0 + i];
         V* vals = out_vals + 8ull * base;
-        for (uint32_t i = threadIdx.x; i < 8 * nvw; i += blockDim.x) vals[i] = store_cvt<V>(0.0f);
-        __syncthreads();
-        for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-            uint32_t r = 0;
+        for (uint32_t t0 = 0; t0 < nvw; t0 += kScatterTile) {
+            const uint32_t tn = min(kScatterTile, nvw - t0);  // vectors in this tile
+            const uint32_t n16 = (8 * tn * sizeof(V) + 15) / 16;
+            for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) tile_raw[i] = make_uint4(0, 0, 0, 0);
+            __syncthreads();
+            for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+                const uint32_t v = rank[e];
+                if (v < t0 || v >= t0 + tn) continue;
+                uint32_t r = 0;
 #pragma unroll
-            for (int q = 1; q < 8; ++q) r += (e >= rb[q]) ? 1u : 0u;
-            const uint32_t v = rank[e];
-            const uint32_t b = v / k, j = v - b * k;
-            const uint32_t width = min(k, nvw - b * k);
-            vals[static_cast<uint64_t>(b) * k * 8 + r * width + j] = store_cvt<V>(csr_vals[e]);
+                for (int q = 1; q < 8; ++q) r += (e >= rb[q]) ? 1u : 0u;
+                const uint32_t b = v / k, j = v - b * k;
+                const uint32_t width = min(k, nvw - b * k);
+                tile[(b * k - t0) * 8 + r * width + j] = store_cvt<V>(csr_vals[e]);
+            }
+            __syncthreads();
+            uint4* dst = reinterpret_cast<uint4*>(vals + 8ull * t0);  // 16-B aligned: 8*(base+t0)*sizeof(V)
+            const uint32_t full16 = (8 * tn * sizeof(V)) / 16;
+            for (uint32_t i = threadIdx.x; i < full16; i += blockDim.x) dst[i] = tile_raw[i];
+            __syncthreads();
         }
-        __syncthreads();
     }
 }
+
+const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
+                         "column indices must be strictly ascending within a row"};
 
 }  // namespace
 }  // namespace tcs
@@ -243,13 +345,13 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
         if (!csr->row_ptr || (csr->nnz && (!csr->col_idx || !csr->values))) fail(TCS_ERR_ARGUMENT, "null CSR array");
         if (csr->nnz >= (1ull << 32)) fail(TCS_ERR_FORMAT, "nnz exceeds u32 row_ptr");
         cudaStream_t s = st(stream);
-        const uint64_t rows = csr->rows, W = (rows + 7) / 8, nnz = csr->nnz;
+        const uint64_t rows = csr->rows, W = (rows + 7) / 8, nnz = csr->nnz, cols = csr->cols;
         const uint32_t k = precision == TCS_FP16 ? 8 : 4;
         const int sms = num_sms();
 
         tcs_mebcrs m{};
         m.rows = rows;
-        m.cols = csr->cols;
+        m.cols = cols;
         m.vector_height = 8;
         m.k = k;
         m.precision = precision;
@@ -257,75 +359,103 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
         m.num_windows = W;
         m.flags = TCS_MEBCRS_OWN_STRUCTURE | TCS_MEBCRS_OWN_VALUES;
         m.row_pointers = static_cast<uint32_t*>(dalloc((W + 1) * 4, s));
+        struct Cleanup {
+            tcs_mebcrs* m;
+            cudaStream_t s;
+            bool armed = true;
+            ~Cleanup() {
+                if (armed) {
+                    dfree(m->row_pointers, s);
+                    dfree(m->column_indices, s);
+                    dfree(m->values, s);
+                }
+            }
+        } cleanup{&m, s};
 
         uint32_t nv = 0;
         if (W) {
-            // K0: validate + longest window
+            // K0: row_ptr invariants + longest window
             DBuf chk(sizeof(CheckOut), s);
             TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
-            const int g0 = static_cast<int>(std::min<uint64_t>((rows + 255) / 256, uint64_t(sms) * 8));
-            csr_check<<<g0, 256, 0, s>>>(csr->row_ptr, csr->col_idx, rows, csr->cols, nnz, chk.as<CheckOut>());
-            TCS_LAUNCHED("csr_check");
+            const int g0 = static_cast<int>(std::min<uint64_t>((W + 255) / 256, uint64_t(sms) * 8));
+            window_stats<<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>());
+            TCS_LAUNCHED("window_stats");
             CheckOut h{};
-            uint32_t last = 0;
+            uint32_t ends[2] = {0, 0};
             TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaMemcpyAsync(&last, csr->row_ptr + rows, 4, cudaMemcpyDeviceToHost, s));
-            uint32_t first = 0;
-            TCS_CUDA(cudaMemcpyAsync(&first, csr->row_ptr, 4, cudaMemcpyDeviceToHost, s));
+            TCS_CUDA(cudaMemcpyAsync(&ends[0], csr->row_ptr, 4, cudaMemcpyDeviceToHost, s));
+            TCS_CUDA(cudaMemcpyAsync(&ends[1], csr->row_ptr + rows, 4, cudaMemcpyDeviceToHost, s));
             TCS_CUDA(cudaStreamSynchronize(s));
-            if (first != 0 || last != nnz) {
-                dfree(m.row_pointers, s);
-                fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
-            }
-            if (h.bad) {
-                dfree(m.row_pointers, s);
-                static const char* msg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz",
-                                            "column index out of range",
-                                            "column indices must be strictly ascending within a row"};
-                fail(TCS_ERR_FORMAT, msg[h.bad < 5 ? h.bad : 0]);
-            }
+            if (ends[0] != 0 || ends[1] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
+            if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
 
             DBuf tmp_cols(std::max<uint64_t>(1, nnz) * 4, s), rank(std::max<uint64_t>(1, nnz) * 4, s);
             DBuf nvw(W * 4, s);
+            CheckOut* dchk = chk.as<CheckOut>();
             const int g1 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * 16));
-            window_merge_small<<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, W,
-                                                            tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                            nvw.as<uint32_t>());
-            TCS_LAUNCHED("window_merge_small");
+            window_sort_small<<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                                                           tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
+                                                           nvw.as<uint32_t>(), dchk);
+            TCS_LAUNCHED("window_sort_small");
             if (h.max_window_entries > kSmallCap) {
-                DBuf scratch;
-                if (h.max_window_entries > kBigCap) scratch = DBuf(2 * nnz * 8, s);
-                const size_t smem = 2 * kBigCap * sizeof(uint64_t);
-                TCS_CUDA(cudaFuncSetAttribute(window_merge_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(smem)));
-                const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms)));
-                window_merge_big<<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, W,
-                                                                scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
-                                                                rank.as<uint32_t>(), nvw.as<uint32_t>());
-                TCS_LAUNCHED("window_merge_big");
+                const uint64_t words = (cols + 31) / 32;
+                if (words <= kBitmapMaxWords) {
+                    const size_t smem = 2 * words * sizeof(uint32_t);
+                    TCS_CUDA(cudaFuncSetAttribute(window_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(std::max<size_t>(smem, 1))));
+                    const int per_sm = std::max<int>(1, std::min<int>(4, int(200 * 1024 / std::max<size_t>(smem, 1))));
+                    const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
+                    window_bitmap<<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                                                                   tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
+                                                                   nvw.as<uint32_t>(), dchk);
+                    TCS_LAUNCHED("window_bitmap");
+                } else {
+                    DBuf scratch;
+                    if (h.max_window_entries > kBigCap) scratch = DBuf(2 * nnz * 8, s);
+                    const size_t smem = 2 * kBigCap * sizeof(uint64_t);
+                    TCS_CUDA(cudaFuncSetAttribute(window_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  static_cast<int>(smem)));
+                    const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms)));
+                    window_sort_big<<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                                                                   scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
+                                                                   rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk);
+                    TCS_LAUNCHED("window_sort_big");
+                }
             }
             exclusive_scan_u32(nvw.as<uint32_t>(), m.row_pointers, W, s);
             TCS_CUDA(cudaMemcpyAsync(&nv, m.row_pointers + W, 4, cudaMemcpyDeviceToHost, s));
+            TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
             TCS_CUDA(cudaStreamSynchronize(s));
+            if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
             m.num_vectors = nv;
             const size_t vw = value_dtype == TCS_DTYPE_F16 ? 2 : 4;
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
             m.values = dalloc(std::max<uint64_t>(1, 8ull * nv) * vw, s);
-            const int g3 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * 8));
-            if (value_dtype == TCS_DTYPE_F16)
-                window_scatter<__half><<<g3, 256, 0, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
-                                                          tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                          m.column_indices, static_cast<__half*>(m.values));
-            else
-                window_scatter<float><<<g3, 256, 0, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
-                                                         tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                         m.column_indices, static_cast<float*>(m.values));
+            const size_t tile_smem = size_t(kScatterTile) * 8 * vw;
+            const int per_sm = static_cast<int>(std::max<size_t>(1, (200 * 1024) / tile_smem));
+            const int g3 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
+            if (value_dtype == TCS_DTYPE_F16) {
+                TCS_CUDA(cudaFuncSetAttribute(window_scatter<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(tile_smem)));
+                window_scatter<__half><<<g3, 256, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                                                                  m.row_pointers, tmp_cols.as<uint32_t>(),
+                                                                  rank.as<uint32_t>(), m.column_indices,
+                                                                  static_cast<__half*>(m.values));
+            } else {
+                TCS_CUDA(cudaFuncSetAttribute(window_scatter<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(tile_smem)));
+                window_scatter<float><<<g3, 256, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                                                                 m.row_pointers, tmp_cols.as<uint32_t>(),
+                                                                 rank.as<uint32_t>(), m.column_indices,
+                                                                 static_cast<float*>(m.values));
+            }
             TCS_LAUNCHED("window_scatter");
         } else {
             TCS_CUDA(cudaMemsetAsync(m.row_pointers, 0, 4, s));
             m.column_indices = static_cast<uint32_t*>(dalloc(4, s));
             m.values = dalloc(4, s);
         }
+        cleanup.armed = false;
         *out = m;
         const tcs_status rc = tcs_mebcrs_prepare(out, stream);
         if (rc != TCS_OK) {
