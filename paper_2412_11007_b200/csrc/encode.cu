@@ -285,7 +285,7 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 constexpr uint32_t kScatterTile = 4096;  // vectors per smem tile (multiple of k)
 
 template <typename V>
-__global__ void __launch_bounds__(256) window_scatter(const uint32_t* __restrict__ csr_rp,
+__global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
                                                       uint32_t k, const uint32_t* __restrict__ rp,
                                                       const uint32_t* __restrict__ tmp_cols,
@@ -307,15 +307,27 @@ __global__ void __launch_bounds__(256) window_scatter(const uint32_t* __restrict
             const uint32_t n16 = (8 * tn * sizeof(V) + 15) / 16;
             for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) tile_raw[i] = make_uint4(0, 0, 0, 0);
             __syncthreads();
-            for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-                const uint32_t v = rank[e];
-                if (v < t0 || v >= t0 + tn) continue;
-                uint32_t r = 0;
+            // 4 entries in flight per thread (coalesced per sub-step)
+            for (uint32_t e4 = e0; e4 < e1; e4 += 4 * blockDim.x) {
+                uint32_t v[4];
+                float x[4];
 #pragma unroll
-                for (int q = 1; q < 8; ++q) r += (e >= rb[q]) ? 1u : 0u;
-                const uint32_t b = v / k, j = v - b * k;
-                const uint32_t width = min(k, nvw - b * k);
-                tile[(b * k - t0) * 8 + r * width + j] = store_cvt<V>(csr_vals[e]);
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e4 + u * blockDim.x + threadIdx.x;
+                    v[u] = e < e1 ? __ldg(rank + e) : 0xFFFFFFFFu;
+                    x[u] = e < e1 ? __ldg(csr_vals + e) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t e = e4 + u * blockDim.x + threadIdx.x;
+                    if (v[u] < t0 || v[u] >= t0 + tn) continue;
+                    uint32_t r = 0;
+#pragma unroll
+                    for (int q = 1; q < 8; ++q) r += (e >= rb[q]) ? 1u : 0u;
+                    const uint32_t b = v[u] / k, j = v[u] - b * k;
+                    const uint32_t width = min(k, nvw - b * k);
+                    tile[(b * k - t0) * 8 + r * width + j] = store_cvt<V>(x[u]);
+                }
             }
             __syncthreads();
             uint4* dst = reinterpret_cast<uint4*>(vals + 8ull * t0);  // 16-B aligned: 8*(base+t0)*sizeof(V)
@@ -437,14 +449,14 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
             if (value_dtype == TCS_DTYPE_F16) {
                 TCS_CUDA(cudaFuncSetAttribute(window_scatter<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<__half><<<g3, 256, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<__half><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                   m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                   rank.as<uint32_t>(), m.column_indices,
                                                                   static_cast<__half*>(m.values));
             } else {
                 TCS_CUDA(cudaFuncSetAttribute(window_scatter<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<float><<<g3, 256, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<float><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                  m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                  rank.as<uint32_t>(), m.column_indices,
                                                                  static_cast<float*>(m.values));
