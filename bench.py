@@ -245,6 +245,33 @@ def run_ours(args, rank, world, device):
                 ts.append(a.elapsed_time(b))
             paths[path] = round(sum(ts) / len(ts), 4)
 
+    # SDDMM on the same pattern (BASELINE metric covers SpMM/SDDMM; F = 32 as configs[1])
+    sddmm = None
+    if not args.quick:
+        F = 32
+        Ad = G.dense(l_rows, F, 4, values="real", dtype=dt, device=device)
+        Btd = G.dense(cols, F, 5, values="real", dtype=dt, device=device)
+        ov = torch.empty(8 * nv, dtype=torch.float32, device=device)
+        ops = T.SddmmOperands(me, Ad, Btd)
+        T.sddmm(ops, cfg, out_values=ov)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            a.record()
+            T.sddmm(ops, cfg, out_values=ov)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        sd_ms = sum(ts) / len(ts)
+        vA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
+        vB = 2 if dt == torch.float16 else 4
+        sd_bytes = 4 * (W + 1) + 4 * nv + 8 * nv * vA + l_rows * F * vB + nv * F * vB + 8 * nv * 4
+        peak_, _ = peaks()
+        sddmm = {"F": F, "ms": round(sd_ms, 4), "gflops": round(2.0 * nnz_local * F / (sd_ms / 1e3) / 1e9, 1),
+                 "bytes_alg_per_launch": sd_bytes, "achieved_gbs": round(sd_bytes / (sd_ms / 1e3) / 1e9, 1),
+                 "frac": round(sd_bytes / (sd_ms / 1e3) / 1e9 / peak_, 4), "out": "f32 ME-BCRS values"}
+        del Ad, Btd, ov
+
     vwA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
     vwB = 2 if dt == torch.float16 else 4
     balg = bytes_alg_spmm(W, nv, l_rows, N, vwA, vwB)
@@ -291,6 +318,7 @@ def run_ours(args, rank, world, device):
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
         "back_to_back_ms": round(b2b_ms, 4),
         "path_ms": paths,
+        "sddmm": sddmm,
         "broadcast_ms": round(bcast_ms, 3),
         "shards": [{"nnz": g["nnz"], "nv": g["nv"], "step_ms": round(g["step_ms"], 4)} for g in gathered],
     }

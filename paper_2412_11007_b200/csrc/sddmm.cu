@@ -42,6 +42,7 @@ struct SddmmArgs {
     uint64_t rows;
     int passes;         // feature passes of NSC super-chunks
     uint32_t k;         // storage block width (8 / 4)
+    uint32_t* counter;  // work-item counter (zeroed before launch)
 };
 
 constexpr int kWarps = 4;
@@ -144,11 +145,15 @@ template <bool TF32, int NSC, bool MF32, bool OF32>
 __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
     using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
-    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint64_t idx = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
-    if (idx >= a.n_items) return;
-    const WorkItem it = a.items[idx];
+    const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
+    // persistent warps pulling work items (cf. spmm.cu next_item)
+    for (;;) {
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(a.counter, 1u);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx >= a.n_items) break;
+    const WorkItem it = a.items[idx];
     const uint32_t base = __ldg(a.rp + it.window);
     const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
     const uint32_t* ci = a.ci + base;
@@ -203,11 +208,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
         cb[0] = ca[0]; cb[1] = ca[1];
         ca[0] = cc[0]; ca[1] = cc[1];
     }
+    }  // work items
 }
 
 template <bool TF32, int NSC>
 void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>((a.n_items + kWarps - 1) / kWarps));
+    const dim3 grid(static_cast<unsigned>(std::min<uint64_t>((a.n_items + kWarps - 1) / kWarps,
+                                                             uint64_t(num_sms()) * 3)));
     if (mf32 && of32) sddmm_kernel<TF32, NSC, true, true><<<grid, kWarps * 32, 0, s>>>(a);
     else if (mf32) sddmm_kernel<TF32, NSC, true, false><<<grid, kWarps * 32, 0, s>>>(a);
     else if (of32) sddmm_kernel<TF32, NSC, false, true><<<grid, kWarps * 32, 0, s>>>(a);
@@ -298,9 +305,11 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
                 int64_t alda = 0, bldb = 0;
                 const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
                 const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
+                DBuf item_ctr(sizeof(uint32_t), s);
+                TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, sizeof(uint32_t), s));
                 SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
                                ap, alda, bp, bldb, o.values, mask->rows,
-                               static_cast<int>(fpad / (nsc * sc)), mask->k};
+                               static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>()};
                 const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
                 if (plan->n_items) {
                     if (tf32) {
