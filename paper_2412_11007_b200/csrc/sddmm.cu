@@ -47,10 +47,33 @@ struct SddmmArgs {
 
 constexpr int kWarps = 4;
 
+// Storage position of accumulator element q (vector g or g+8, row 2t or
+// 2t+1) of the group at s -- Algorithm 1's offsets for full blocks, the
+// general block_width form for a narrow last block (ref sddmm.hpp:125-130).
+__device__ __forceinline__ uint64_t acc_pos(uint32_t k, uint64_t vbase, uint32_t nvw, uint32_t s, uint32_t g,
+                                            uint32_t t, int q) {
+    const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+    const uint32_t r = 2 * t + (q & 1);
+    const uint32_t b = v / k, j = v - b * k, width = min(k, nvw - b * k);
+    return vbase + 8ull * b * k + r * width + j;
+}
+
+// Liveness bits of the mask values at the group's 4 accumulator positions
+// (nonzero magnitude == the reference's `mask.values[pos] != 0`; -0.0 is not
+// live, ref sddmm.hpp:131).  Issued one group ahead of use.
 template <bool MF32>
-__device__ __forceinline__ bool mask_live(const void* mask, uint64_t pos) {
-    if constexpr (MF32) return __ldg(static_cast<const float*>(mask) + pos) != 0.f;
-    else return __half2float(__ldg(static_cast<const __half*>(mask) + pos)) != 0.f;
+__device__ __forceinline__ void mask_prefetch(const SddmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend,
+                                              uint32_t s, uint32_t g, uint32_t t, uint32_t (&mk)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+        mk[q] = 0u;
+        if (v < vend) {
+            const uint64_t pos = acc_pos(a.k, vbase, nvw, s, g, t, q);
+            if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos)) & 0x7FFFFFFFu;
+            else mk[q] = static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos)) & 0x7FFFu;
+        }
+    }
 }
 
 template <bool OF32>
@@ -60,18 +83,15 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
 }
 
 // Writes the 16x8 accumulator tile of the vector group starting at s.
-template <bool MF32, bool OF32>
-__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], uint64_t vbase, uint32_t nvw,
-                                            uint32_t vend, uint32_t s, uint32_t g, uint32_t t) {
-    const uint32_t k = a.k;
+template <bool OF32>
+__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], const uint32_t (&mk)[4],
+                                            uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g,
+                                            uint32_t t) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
-        const uint32_t r = 2 * t + (q & 1);
         if (v >= vend) continue;
-        const uint32_t b = v / k, j = v - b * k, width = min(k, nvw - b * k);
-        const uint64_t pos = vbase + 8ull * b * k + r * width + j;
-        out_store<OF32>(a.out, pos, mask_live<MF32>(a.mask, pos) ? acc[q] : 0.f);
+        out_store<OF32>(a.out, acc_pos(a.k, vbase, nvw, s, g, t, q), mk[q] ? acc[q] : 0.f);
     }
 }
 
@@ -178,7 +198,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
         c[1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
     };
     // one group: prefetched pass 0 + (rare) extra passes loaded in place
-    auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0) {
+    auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0, const uint32_t (&mk)[4]) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         mma(x0, acc);
         for (int p = 1; p < a.passes; ++p) {
@@ -186,25 +206,33 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
             load(s, c, p, x);
             mma(x, acc);
         }
-        sddmm_store<MF32, OF32>(a, acc, vbase, nvw, vend, s, g, t);
+        sddmm_store<OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
     };
 
     Tile ta, tb;
+    uint32_t ma[4], mb[4];
     uint32_t ca[2], cb[2], cc[2];
     uint32_t s = it.vbeg;
     if (s < vend) {
         cols(s, ca);
         load(s, ca, 0, ta);
+        mask_prefetch<MF32>(a, vbase, nvw, vend, s, g, t, ma);
         cols(s + 16, cb);
     }
     for (; s < vend; s += 32) {
-        if (s + 16 < vend) load(s + 16, cb, 0, tb);
+        if (s + 16 < vend) {
+            load(s + 16, cb, 0, tb);
+            mask_prefetch<MF32>(a, vbase, nvw, vend, s + 16, g, t, mb);
+        }
         cols(s + 32, cc);
-        group(s, ca, ta);
+        group(s, ca, ta, ma);
         if (s + 16 >= vend) break;
-        if (s + 32 < vend) load(s + 32, cc, 0, ta);
+        if (s + 32 < vend) {
+            load(s + 32, cc, 0, ta);
+            mask_prefetch<MF32>(a, vbase, nvw, vend, s + 32, g, t, ma);
+        }
         cols(s + 48, ca);
-        group(s + 16, cb, tb);
+        group(s + 16, cb, tb, mb);
         cb[0] = ca[0]; cb[1] = ca[1];
         ca[0] = cc[0]; ca[1] = cc[1];
     }
