@@ -98,65 +98,74 @@ __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&ac
 // ---------------------------------------------------------------- FP16
 template <int NSC>
 struct F16Tile {
-    uint4 q0[NSC], q1[NSC], ar[NSC];  // Bt rows of vectors g, g+8; A row g
+    uint4 q0[NSC], q1[NSC];  // Bt rows of vectors g, g+8 (the window's A row g is hoisted per item)
 };
 
 template <int NSC>
-__device__ __forceinline__ void f16_tile_load(const SddmmArgs& a, const __half* __restrict__ arow, bool arow_ok,
-                                              uint32_t c0, bool ok0, uint32_t c1, bool ok1, int pass, uint32_t t,
-                                              F16Tile<NSC>& x) {
+__device__ __forceinline__ void f16_tile_load(const SddmmArgs& a, uint32_t c0, bool ok0, uint32_t c1, bool ok1,
+                                              int pass, uint32_t t, F16Tile<NSC>& x) {
     const __half* bt = static_cast<const __half*>(a.Bt);
 #pragma unroll
     for (int sc = 0; sc < NSC; ++sc) {
         const int64_t f = (static_cast<int64_t>(pass) * NSC + sc) * 32 + 8 * t;
         x.q0[sc] = ok0 ? ld_gather_128(bt + static_cast<uint64_t>(c0) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
         x.q1[sc] = ok1 ? ld_gather_128(bt + static_cast<uint64_t>(c1) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
-        x.ar[sc] = arow_ok ? ld_gather_128(arow + f) : make_uint4(0, 0, 0, 0);
+    }
+}
+
+// A row g of the window, features of pass `pass` (same K permutation as the tiles).
+template <int NSC, typename Elem>
+__device__ __forceinline__ void arow_load(const Elem* __restrict__ arow, bool ok, int pass, uint32_t t,
+                                          uint4 (&ar)[NSC]) {
+    constexpr int SC = sizeof(Elem) == 2 ? 32 : 16;  // features per super-chunk
+    constexpr int PER_LANE = sizeof(Elem) == 2 ? 8 : 4;
+#pragma unroll
+    for (int sc = 0; sc < NSC; ++sc) {
+        const int64_t f = (static_cast<int64_t>(pass) * NSC + sc) * SC + PER_LANE * t;
+        ar[sc] = ok ? ld_gather_128(arow + f) : make_uint4(0, 0, 0, 0);
     }
 }
 
 template <int NSC>
-__device__ __forceinline__ void f16_tile_mma(const F16Tile<NSC>& x, float (&acc)[4]) {
+__device__ __forceinline__ void f16_tile_mma(const F16Tile<NSC>& x, const uint4 (&ar)[NSC], float (&acc)[4]) {
 #pragma unroll
     for (int sc = 0; sc < NSC; ++sc) {
         // chunk 0: k = {2t,2t+1} <-> features 8t+0,1 ; k = {2t+8,2t+9} <-> 8t+2,3
-        mma_f16_16816(acc, x.q0[sc].x, x.q1[sc].x, x.q0[sc].y, x.q1[sc].y, x.ar[sc].x, x.ar[sc].y);
+        mma_f16_16816(acc, x.q0[sc].x, x.q1[sc].x, x.q0[sc].y, x.q1[sc].y, ar[sc].x, ar[sc].y);
         // chunk 1: features 8t+4,5 and 8t+6,7
-        mma_f16_16816(acc, x.q0[sc].z, x.q1[sc].z, x.q0[sc].w, x.q1[sc].w, x.ar[sc].z, x.ar[sc].w);
+        mma_f16_16816(acc, x.q0[sc].z, x.q1[sc].z, x.q0[sc].w, x.q1[sc].w, ar[sc].z, ar[sc].w);
     }
 }
 
 // ---------------------------------------------------------------- TF32
 template <int NSC>
 struct Tf32Tile {
-    uint4 q0[NSC], q1[NSC], ar[NSC];  // 4 f32 features each
+    uint4 q0[NSC], q1[NSC];  // 4 f32 features each
 };
 
 template <int NSC>
-__device__ __forceinline__ void tf32_tile_load(const SddmmArgs& a, const float* __restrict__ arow, bool arow_ok,
-                                               uint32_t c0, bool ok0, uint32_t c1, bool ok1, int pass, uint32_t t,
-                                               Tf32Tile<NSC>& x) {
+__device__ __forceinline__ void tf32_tile_load(const SddmmArgs& a, uint32_t c0, bool ok0, uint32_t c1, bool ok1,
+                                               int pass, uint32_t t, Tf32Tile<NSC>& x) {
     const float* bt = static_cast<const float*>(a.Bt);
 #pragma unroll
     for (int sc = 0; sc < NSC; ++sc) {
         const int64_t f = (static_cast<int64_t>(pass) * NSC + sc) * 16 + 4 * t;
         x.q0[sc] = ok0 ? ld_gather_128(bt + static_cast<uint64_t>(c0) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
         x.q1[sc] = ok1 ? ld_gather_128(bt + static_cast<uint64_t>(c1) * a.ldbt + f) : make_uint4(0, 0, 0, 0);
-        x.ar[sc] = arow_ok ? ld_gather_128(arow + f) : make_uint4(0, 0, 0, 0);
     }
 }
 
 __device__ __forceinline__ uint32_t tf(uint32_t bits) { return to_tf32(__uint_as_float(bits)); }
 
 template <int NSC>
-__device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, float (&acc)[4]) {
+__device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, const uint4 (&ar)[NSC], float (&acc)[4]) {
 #pragma unroll
     for (int sc = 0; sc < NSC; ++sc) {
         // chunk 0: k = t <-> feature 4t, k = t+4 <-> 4t+1 ; chunk 1: 4t+2, 4t+3
-        mma_tf32_1688(acc, tf(x.q0[sc].x), tf(x.q1[sc].x), tf(x.q0[sc].y), tf(x.q1[sc].y), tf(x.ar[sc].x),
-                      tf(x.ar[sc].y));
-        mma_tf32_1688(acc, tf(x.q0[sc].z), tf(x.q1[sc].z), tf(x.q0[sc].w), tf(x.q1[sc].w), tf(x.ar[sc].z),
-                      tf(x.ar[sc].w));
+        mma_tf32_1688(acc, tf(x.q0[sc].x), tf(x.q1[sc].x), tf(x.q0[sc].y), tf(x.q1[sc].y), tf(ar[sc].x),
+                      tf(ar[sc].y));
+        mma_tf32_1688(acc, tf(x.q0[sc].z), tf(x.q1[sc].z), tf(x.q0[sc].w), tf(x.q1[sc].w), tf(ar[sc].z),
+                      tf(ar[sc].w));
     }
 }
 
@@ -185,14 +194,16 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
 
     auto load = [&](uint32_t s, const uint32_t (&c)[2], int pass, Tile& x) {
         if constexpr (TF32)
-            tf32_tile_load<NSC>(a, arow, arow_ok, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
+            tf32_tile_load<NSC>(a, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
         else
-            f16_tile_load<NSC>(a, arow, arow_ok, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
+            f16_tile_load<NSC>(a, c[0], s + g < vend, c[1], s + g + 8 < vend, pass, t, x);
     };
-    auto mma = [&](const Tile& x, float (&acc)[4]) {
-        if constexpr (TF32) tf32_tile_mma<NSC>(x, acc);
-        else f16_tile_mma<NSC>(x, acc);
+    auto mma = [&](const Tile& x, const uint4 (&ar)[NSC], float (&acc)[4]) {
+        if constexpr (TF32) tf32_tile_mma<NSC>(x, ar, acc);
+        else f16_tile_mma<NSC>(x, ar, acc);
     };
+    uint4 ar0[NSC];  // A row g, pass 0: shared by every group of the item
+    arow_load<NSC>(arow, arow_ok, 0, t, ar0);
     auto cols = [&](uint32_t s, uint32_t (&c)[2]) {
         c[0] = s + g < vend ? __ldg(ci + s + g) : 0u;
         c[1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
@@ -200,41 +211,70 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
     // one group: prefetched pass 0 + (rare) extra passes loaded in place
     auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0, const uint32_t (&mk)[4]) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-        mma(x0, acc);
-        for (int p = 1; p < a.passes; ++p) {
-            Tile x;
-            load(s, c, p, x);
-            mma(x, acc);
+        mma(x0, ar0, acc);
+        if constexpr (NSC > 1) {  // NSC == 1 <=> the inner dimension fits one pass
+            for (int p = 1; p < a.passes; ++p) {
+                Tile x;
+                uint4 arp[NSC];
+                load(s, c, p, x);
+                arow_load<NSC>(arow, arow_ok, p, t, arp);
+                mma(x, arp, acc);
+            }
         }
         sddmm_store<OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
     };
 
-    Tile ta, tb;
-    uint32_t ma[4], mb[4];
-    uint32_t ca[2], cb[2], cc[2];
+    // Double-buffered batches of D groups (16*D vectors): the gathers and
+    // mask bits of batch i+1 are in flight while batch i is consumed; the
+    // column indices of a batch are loaded coalesced (one per lane per 32
+    // vectors) a full batch ahead and distributed by shuffle.
+    constexpr int D = NSC == 1 ? 4 : 2;
+    constexpr int CW = (D + 1) / 2;  // coalesced column words per batch
+    auto batch_cols = [&](uint32_t sb, uint32_t (&cw)[CW]) {
+#pragma unroll
+        for (int h = 0; h < CW; ++h) {
+            const uint32_t v = sb + 32 * h + lane;
+            cw[h] = v < vend ? __ldg(ci + v) : 0u;
+        }
+    };
+    auto issue = [&](uint32_t sb, const uint32_t (&cw)[CW], Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const uint32_t s = sb + 16 * d;
+            cg[d][0] = __shfl_sync(0xffffffffu, cw[d / 2], 16 * (d & 1) + g);
+            cg[d][1] = __shfl_sync(0xffffffffu, cw[d / 2], 16 * (d & 1) + g + 8);
+            if (s < vend) {
+                load(s, cg[d], 0, x[d]);
+                mask_prefetch<MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
+            }
+        }
+    };
+    auto consume = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&mk)[D][4], const uint32_t (&cg)[D][2]) {
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (sb + 16 * d < vend) group(sb + 16 * d, cg[d], x[d], mk[d]);
+    };
+
+    Tile ta[D], tb[D];
+    uint32_t ma[D][4], mb[D][4], ga[D][2], gb[D][2];
+    uint32_t c0[CW], c1[CW];
+    constexpr uint32_t BV = 16 * D;
     uint32_t s = it.vbeg;
     if (s < vend) {
-        cols(s, ca);
-        load(s, ca, 0, ta);
-        mask_prefetch<MF32>(a, vbase, nvw, vend, s, g, t, ma);
-        cols(s + 16, cb);
-    }
-    for (; s < vend; s += 32) {
-        if (s + 16 < vend) {
-            load(s + 16, cb, 0, tb);
-            mask_prefetch<MF32>(a, vbase, nvw, vend, s + 16, g, t, mb);
+        batch_cols(s, c0);
+        batch_cols(s + BV, c1);
+        issue(s, c0, ta, ma, ga);
+        for (;;) {
+            if (s + BV < vend) issue(s + BV, c1, tb, mb, gb);
+            batch_cols(s + 2 * BV, c0);
+            consume(s, ta, ma, ga);
+            if (s + BV >= vend) break;
+            if (s + 2 * BV < vend) issue(s + 2 * BV, c0, ta, ma, ga);
+            batch_cols(s + 3 * BV, c1);
+            consume(s + BV, tb, mb, gb);
+            s += 2 * BV;
+            if (s >= vend) break;
         }
-        cols(s + 32, cc);
-        group(s, ca, ta, ma);
-        if (s + 16 >= vend) break;
-        if (s + 32 < vend) {
-            load(s + 32, cc, 0, ta);
-            mask_prefetch<MF32>(a, vbase, nvw, vend, s + 32, g, t, ma);
-        }
-        cols(s + 48, ca);
-        group(s + 16, cb, tb, mb);
-        cb[0] = ca[0]; cb[1] = ca[1];
-        ca[0] = cc[0]; ca[1] = cc[1];
     }
     }  // work items
 }
