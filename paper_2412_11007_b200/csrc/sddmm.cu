@@ -48,28 +48,35 @@ struct SddmmArgs {
 constexpr int kWarps = 4;
 
 // Storage position of accumulator element q (vector g or g+8, row 2t or
-// 2t+1) of the group at s -- Algorithm 1's offsets for full blocks, the
-// general block_width form for a narrow last block (ref sddmm.hpp:125-130).
-__device__ __forceinline__ uint64_t acc_pos(uint32_t k, uint64_t vbase, uint32_t nvw, uint32_t s, uint32_t g,
+// 2t+1) of the group at s.  K (storage block width) is a compile-time
+// constant.  Full groups use Algorithm 1's offsets (ref sddmm.hpp:28-33):
+// inside the 16-vector group's 128 contiguous values, vector v / row r sits
+// at 8K*(v/K) + K*r + v%K; a narrow last block uses its block_width
+// (ref sddmm.hpp:125-130).
+template <uint32_t K>
+__device__ __forceinline__ uint64_t acc_pos(uint64_t vbase, uint32_t nvw, uint32_t s, bool full, uint32_t g,
                                             uint32_t t, int q) {
-    const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+    const uint32_t vl = g + (q >= 2 ? 8u : 0u);  // vector within the group
     const uint32_t r = 2 * t + (q & 1);
-    const uint32_t b = v / k, j = v - b * k, width = min(k, nvw - b * k);
-    return vbase + 8ull * b * k + r * width + j;
+    if (full) return vbase + 8ull * s + 8 * K * (vl / K) + K * r + (vl % K);
+    const uint32_t v = s + vl;
+    const uint32_t b = v / K, j = v % K, width = min(K, nvw - b * K);
+    return vbase + 8ull * b * K + r * width + j;
 }
 
 // Liveness bits of the mask values at the group's 4 accumulator positions
 // (nonzero magnitude == the reference's `mask.values[pos] != 0`; -0.0 is not
 // live, ref sddmm.hpp:131).  Issued one group ahead of use.
-template <bool MF32>
+template <uint32_t K, bool MF32>
 __device__ __forceinline__ void mask_prefetch(const SddmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend,
                                               uint32_t s, uint32_t g, uint32_t t, uint32_t (&mk)[4]) {
+    const bool full = s + 16 <= vend;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
         mk[q] = 0u;
         if (v < vend) {
-            const uint64_t pos = acc_pos(a.k, vbase, nvw, s, g, t, q);
+            const uint64_t pos = acc_pos<K>(vbase, nvw, s, full, g, t, q);
             if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos)) & 0x7FFFFFFFu;
             else mk[q] = static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos)) & 0x7FFFu;
         }
@@ -83,15 +90,16 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
 }
 
 // Writes the 16x8 accumulator tile of the vector group starting at s.
-template <bool OF32>
+template <uint32_t K, bool OF32>
 __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], const uint32_t (&mk)[4],
                                             uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g,
                                             uint32_t t) {
+    const bool full = s + 16 <= vend;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
         if (v >= vend) continue;
-        out_store<OF32>(a.out, acc_pos(a.k, vbase, nvw, s, g, t, q), mk[q] ? acc[q] : 0.f);
+        out_store<OF32>(a.out, acc_pos<K>(vbase, nvw, s, full, g, t, q), mk[q] ? acc[q] : 0.f);
     }
 }
 
@@ -221,7 +229,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
                 mma(x, arp, acc);
             }
         }
-        sddmm_store<OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
+        sddmm_store<TF32 ? 4u : 8u, OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
     };
 
     // Double-buffered batches of D groups (16*D vectors): the gathers and
@@ -245,7 +253,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
             cg[d][1] = __shfl_sync(0xffffffffu, cw[d / 2], 16 * (d & 1) + g + 8);
             if (s < vend) {
                 load(s, cg[d], 0, x[d]);
-                mask_prefetch<MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
+                mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
             }
         }
     };
