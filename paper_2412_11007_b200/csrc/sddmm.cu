@@ -46,6 +46,7 @@ struct SddmmArgs {
 };
 
 constexpr int kWarps = 4;
+constexpr int kRing = 4;  // column-index batches staged per warp
 
 // Storage position of accumulator element q (vector g or g+8, row 2t or
 // 2t+1) of the group at s.  K (storage block width) is a compile-time
@@ -182,8 +183,9 @@ template <bool TF32, int NSC, bool MF32, bool OF32>
 __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
     using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t g = lane >> 2, t = lane & 3;
+    __shared__ uint32_t colring_all[kWarps * kRing * 64];  // per-warp column-index ring
     // persistent warps pulling work items (cf. spmm.cu next_item)
     for (;;) {
     uint32_t idx = 0;
@@ -233,24 +235,31 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
     };
 
     // Double-buffered batches of D groups (16*D vectors): the gathers and
-    // mask bits of batch i+1 are in flight while batch i is consumed; the
-    // column indices of a batch are loaded coalesced (one per lane per 32
-    // vectors) a full batch ahead and distributed by shuffle.
+    // mask bits of batch i+1 are in flight while batch i is consumed.  The
+    // column indices feeding the gathers are staged through a per-warp
+    // shared-memory ring by cp.async, RING-1 batches ahead, so no gather
+    // waits on a dependent global load.
     constexpr int D = NSC == 1 ? 4 : 2;
-    constexpr int CW = (D + 1) / 2;  // coalesced column words per batch
-    auto batch_cols = [&](uint32_t sb, uint32_t (&cw)[CW]) {
+    constexpr uint32_t BV = 16 * D;
+    uint32_t (*ring)[BV] = reinterpret_cast<uint32_t (*)[BV]>(colring_all + warp * kRing * 64);
+    auto prefetch_cols = [&](uint32_t sb, uint32_t slot) {
+        __syncwarp();  // every lane is done reading this slot
 #pragma unroll
-        for (int h = 0; h < CW; ++h) {
-            const uint32_t v = sb + 32 * h + lane;
-            cw[h] = v < vend ? __ldg(ci + v) : 0u;
+        for (uint32_t i = lane; i < BV; i += 32) {
+            const uint32_t v = min(sb + i, vend - 1);  // clamp: stays inside the item's columns
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             static_cast<uint32_t>(__cvta_generic_to_shared(&ring[slot][i]))),
+                         "l"(ci + v)
+                         : "memory");
         }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto issue = [&](uint32_t sb, const uint32_t (&cw)[CW], Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
+    auto issue = [&](uint32_t sb, uint32_t slot, Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             const uint32_t s = sb + 16 * d;
-            cg[d][0] = __shfl_sync(0xffffffffu, cw[d / 2], 16 * (d & 1) + g);
-            cg[d][1] = __shfl_sync(0xffffffffu, cw[d / 2], 16 * (d & 1) + g + 8);
+            cg[d][0] = ring[slot][16 * d + g];
+            cg[d][1] = ring[slot][16 * d + g + 8];
             if (s < vend) {
                 load(s, cg[d], 0, x[d]);
                 mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
@@ -265,24 +274,31 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
 
     Tile ta[D], tb[D];
     uint32_t ma[D][4], mb[D][4], ga[D][2], gb[D][2];
-    uint32_t c0[CW], c1[CW];
-    constexpr uint32_t BV = 16 * D;
     uint32_t s = it.vbeg;
     if (s < vend) {
-        batch_cols(s, c0);
-        batch_cols(s + BV, c1);
-        issue(s, c0, ta, ma, ga);
+        const uint32_t s0 = s;
+        uint32_t pb = 0, ib = 0;  // next batch to prefetch / to issue
+        for (int r = 0; r < kRing - 1; ++r, ++pb) prefetch_cols(s0 + pb * BV, pb % kRing);
+        auto next_issue = [&](Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
+            prefetch_cols(s0 + pb * BV, pb % kRing);
+            ++pb;
+            asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
+            __syncwarp();
+            issue(s0 + ib * BV, ib % kRing, x, mk, cg);
+            ++ib;
+        };
+        next_issue(ta, ma, ga);
         for (;;) {
-            if (s + BV < vend) issue(s + BV, c1, tb, mb, gb);
-            batch_cols(s + 2 * BV, c0);
+            if (s + BV < vend) next_issue(tb, mb, gb);
             consume(s, ta, ma, ga);
             if (s + BV >= vend) break;
-            if (s + 2 * BV < vend) issue(s + 2 * BV, c0, ta, ma, ga);
-            batch_cols(s + 3 * BV, c1);
+            if (s + 2 * BV < vend) next_issue(ta, ma, ga);
             consume(s + BV, tb, mb, gb);
             s += 2 * BV;
             if (s >= vend) break;
         }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // no ring write outlives the item
+        __syncwarp();
     }
     }  // work items
 }
