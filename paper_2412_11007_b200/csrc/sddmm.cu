@@ -78,8 +78,10 @@ __device__ __forceinline__ void mask_prefetch(const SddmmArgs& a, uint64_t vbase
         mk[q] = 0u;
         if (v < vend) {
             const uint64_t pos = acc_pos<K>(vbase, nvw, s, full, g, t, q);
-            if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos)) & 0x7FFFFFFFu;
-            else mk[q] = static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos)) & 0x7FFFu;
+            // raw bits only: the liveness test happens at store time, so the
+            // load stays in flight until then
+            if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos));
+            else mk[q] = static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos));
         }
     }
 }
@@ -91,7 +93,7 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
 }
 
 // Writes the 16x8 accumulator tile of the vector group starting at s.
-template <uint32_t K, bool OF32>
+template <uint32_t K, bool MF32, bool OF32>
 __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], const uint32_t (&mk)[4],
                                             uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g,
                                             uint32_t t) {
@@ -100,7 +102,8 @@ __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&ac
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
         if (v >= vend) continue;
-        out_store<OF32>(a.out, acc_pos<K>(vbase, nvw, s, full, g, t, q), mk[q] ? acc[q] : 0.f);
+        const bool live = (mk[q] & (MF32 ? 0x7FFFFFFFu : 0x7FFFu)) != 0u;
+        out_store<OF32>(a.out, acc_pos<K>(vbase, nvw, s, full, g, t, q), live ? acc[q] : 0.f);
     }
 }
 
@@ -231,7 +234,7 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
                 mma(x, arp, acc);
             }
         }
-        sddmm_store<TF32 ? 4u : 8u, OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
+        sddmm_store<TF32 ? 4u : 8u, MF32, OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
     };
 
     // Double-buffered batches of D groups (16*D vectors): the gathers and
