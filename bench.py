@@ -114,15 +114,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def shard_windows(row_ptr: torch.Tensor, rows: int, rank: int, world: int):
-    """Contiguous window range [w0, w1) of `rank`, cut at nnz quantiles."""
-    W = (rows + 7) // 8
-    starts = row_ptr[torch.clamp(torch.arange(W + 1, device=row_ptr.device) * 8, max=rows)].to(torch.int64)
-    total = int(starts[-1])
-    cuts = [0] + [int(torch.searchsorted(starts, total * r // world)) for r in range(1, world)] + [W]
-    return cuts[rank], cuts[rank + 1]
-
-
 def bytes_alg_spmm(W, nv, rows, N, vwA, vwB):
     """row pointers + column indices + sparse values (no padding)
     + one N-wide dense row per stored vector + the fp32 C write."""
@@ -145,17 +136,16 @@ def build_graph(args, device):
 # ---------------------------------------------------------------- ours
 def run_ours(args, rank, world, device):
     import paper_2412_11007_b200.tcsparse as T
-    from paper_2412_11007_b200 import _abi, graphs as G
+    from paper_2412_11007_b200 import _abi, distributed as D, graphs as G
 
     prec = T.Precision.fp16 if args.precision == "fp16" else T.Precision.tf32
     N = args.n
     rows, cols, rp, ci, v, desc = build_graph(args, device)
     nnz_total = int(ci.numel())
-    w0, w1 = shard_windows(rp, rows, rank, world)
-    r0, r1 = 8 * w0, min(8 * w1, rows)
-    lrp, lci, lv = G.row_slice(rp, ci, v, r0, r1)
-    l_rows = r1 - r0
-    local_csr = T.CsrMatrix(l_rows, cols, lrp.contiguous(), lci.contiguous(), lv.contiguous())
+    shard = D.shard_of(D.shard_windows(rp, rows, world), rank, rows)  # nnz-balanced window range
+    lrp, lci, lv = D.local_rows(rp, ci, v, shard)
+    l_rows = shard.rows
+    local_csr = T.CsrMatrix(l_rows, cols, lrp, lci, lv)
     del rp, ci, v
 
     # dense operand: generated on rank 0, broadcast over NCCL (timed separately)
@@ -167,7 +157,7 @@ def run_ours(args, rank, world, device):
         torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        torch.distributed.broadcast(B, src=0)
+        D.broadcast_dense(B, src=0)
         e1.record()
         torch.cuda.synchronize()
         bcast_ms = e0.elapsed_time(e1)

@@ -1,0 +1,118 @@
+"""Row-window sharding of the FlashSparse path over the GPUs of one box
+(one process per GPU, torch.distributed with NCCL; gloo works for the host
+logic and is what the CPU tests use).
+
+The unit of work is the 8-row window: windows own disjoint output rows
+(ref SPEC.md:364), so SpMM/SDDMM shard with no data-path collective.
+
+* ``shard_windows``: contiguous window ranges, cut at nnz quantiles (the
+  north star's balance criterion) -- or at nv quantiles if the ME-BCRS row
+  pointers are given (gather bytes scale with nv).
+* ``local_rows``: the CSR rows of one shard (row_ptr rebased; global column
+  indices kept, so every shard gathers from the full dense operand).
+* ``broadcast_dense``: dense B from one rank to all (NCCL broadcast over
+  NVLink/NVSwitch), done once per operand, outside the timed SpMM loop.
+* ``gather_rows``: optional all-gather of the per-shard outputs when layers
+  chain (GCN / AGNN): shards are padded to the largest one, all-gathered in
+  one collective, and trimmed.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    w0: int  # first window
+    w1: int  # one past the last window
+    r0: int  # first row
+    r1: int  # one past the last row
+
+    @property
+    def rows(self) -> int:
+        return self.r1 - self.r0
+
+
+def shard_windows(row_ptr: torch.Tensor, rows: int, world: int, weights: str = "nnz",
+                  mebcrs_row_pointers: torch.Tensor | None = None) -> list[int]:
+    """Window cut points [0 = c_0 <= c_1 <= ... <= c_world = W] such that
+    shard r = windows [c_r, c_{r+1}) carries ~1/world of the weight.
+    weights = "nnz" uses CSR row_ptr at window starts; "nv" uses the
+    ME-BCRS row pointers (stored 8x1 vectors per window)."""
+    W = (rows + 7) // 8
+    if weights == "nv":
+        if mebcrs_row_pointers is None:
+            raise ValueError("weights='nv' needs the ME-BCRS row pointers")
+        prefix = mebcrs_row_pointers.to(torch.int64).cpu()
+    else:
+        idx = torch.clamp(torch.arange(W + 1, dtype=torch.int64) * 8, max=rows)
+        prefix = row_ptr.to(torch.int64).cpu()[idx]
+    total = int(prefix[-1])
+    cuts = [0]
+    for r in range(1, world):
+        cuts.append(int(torch.searchsorted(prefix, total * r // world)))
+    cuts.append(W)
+    for i in range(1, len(cuts)):  # monotone even for degenerate inputs
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return cuts
+
+
+def shard_of(cuts: list[int], rank: int, rows: int) -> Shard:
+    w0, w1 = cuts[rank], cuts[rank + 1]
+    return Shard(rank, len(cuts) - 1, w0, w1, min(8 * w0, rows), min(8 * w1, rows))
+
+
+def local_rows(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, shard: Shard):
+    """CSR of rows [r0, r1) with row_ptr rebased to 0."""
+    b, e = int(row_ptr[shard.r0]), int(row_ptr[shard.r1])
+    return (row_ptr[shard.r0:shard.r1 + 1] - b).contiguous(), col_idx[b:e].contiguous(), values[b:e].contiguous()
+
+
+def broadcast_dense(B: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """In-place broadcast of the dense operand (NCCL: one ring/tree over NVLink)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.broadcast(B, src=src, group=group)
+    return B
+
+
+def gather_rows(C_local: torch.Tensor, shard_rows: list[int], group=None) -> torch.Tensor:
+    """All-gather row shards of different heights into the full matrix
+    (every rank receives it).  shard_rows[r] = rows owned by rank r."""
+    world = len(shard_rows)
+    if world == 1:
+        return C_local
+    hmax = max(shard_rows)
+    pad = torch.zeros((hmax,) + tuple(C_local.shape[1:]), dtype=C_local.dtype, device=C_local.device)
+    pad[: C_local.shape[0]] = C_local
+    out = torch.empty((world * hmax,) + tuple(C_local.shape[1:]), dtype=C_local.dtype, device=C_local.device)
+    dist.all_gather_into_tensor(out, pad, group=group)
+    return torch.cat([out[r * hmax: r * hmax + shard_rows[r]] for r in range(world)], dim=0)
+
+
+class ShardedSpmm:
+    """SpMM of one graph over all ranks: each rank converts and multiplies
+    its own window shard (tcs_mebcrs_encode + tcs_spmm on its GPU)."""
+
+    def __init__(self, rows, cols, row_ptr, col_idx, values, precision, group=None):
+        from . import tcsparse as T
+
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.cuts = shard_windows(row_ptr, rows, self.world)
+        self.shard = shard_of(self.cuts, self.rank, rows)
+        self.shard_rows = [shard_of(self.cuts, r, rows).rows for r in range(self.world)]
+        lrp, lci, lv = local_rows(row_ptr, col_idx, values, self.shard)
+        self.csr = T.CsrMatrix(self.shard.rows, cols, lrp, lci, lv)
+        self.me = T.encode_mebcrs(self.csr, precision)
+        self.cfg = T.KernelConfig(precision)
+        self._T = T
+
+    def __call__(self, B: torch.Tensor, gather: bool = False) -> torch.Tensor:
+        C = self._T.spmm(self.me, B, self.cfg).output
+        return gather_rows(C, self.shard_rows, self.group) if gather else C
