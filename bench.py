@@ -48,7 +48,7 @@ def parse():
     p.add_argument("--n", type=int, default=128)
     p.add_argument("--precision", default="fp16", choices=["fp16", "tf32"])
     p.add_argument("--workload", default="c3", choices=["c3", "c1"])
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU-baseline sample budget")
     p.add_argument("--quick", action="store_true", help="kernel timing only (for ncu runs)")
     return p.parse_args()
@@ -112,6 +112,74 @@ class ClockSampler:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def small_configs(device):
+    """BASELINE configs[0]/[1] (4096^2, 16 nnz/row): launch-latency-bound, so
+    timed as CUDA-graph replays of 200 back-to-back calls (us per call)."""
+    import paper_2412_11007_b200.tcsparse as T
+    from paper_2412_11007_b200 import graphs as G
+
+    rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real", device=device)
+    nnz = ci.numel()
+    csr = T.CsrMatrix(rows, cols, rp, ci, v)
+    out = {}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn, reps=200):
+        fn()
+        torch.cuda.synchronize()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        graph = None
+        try:
+            with torch.cuda.stream(s):
+                fn()
+            torch.cuda.synchronize()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=s):
+                for _ in range(reps):
+                    fn()
+        except Exception:
+            graph = None
+            torch.cuda.synchronize()
+        e0.record()
+        if graph is not None:
+            graph.replay()
+        else:
+            for _ in range(reps):
+                fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / reps, graph is not None
+
+    for pname, prec, dt in (("fp16", T.Precision.fp16, torch.float16), ("tf32", T.Precision.tf32, torch.float32)):
+        me = T.encode_mebcrs(csr, prec)
+        B = G.dense(cols, 128, 2, dtype=dt, device=device)
+        C = torch.empty(rows, 128, device=device)
+        us, g = timed(lambda: T.spmm(me, B, T.KernelConfig(prec), out=C))
+        out[f"c1_spmm_{pname}_n128_us"] = round(us, 2)
+        out[f"c1_spmm_{pname}_gflops"] = round(2.0 * nnz * 128 / (us * 1e-6) / 1e9, 1)
+        A = G.dense(rows, 32, 3, dtype=dt, device=device)
+        Bt = G.dense(cols, 32, 4, dtype=dt, device=device)
+        ov = torch.empty(8 * me.num_vectors, device=device)
+        ops = T.SddmmOperands(me, A, Bt)
+        us2, g2 = timed(lambda: T.sddmm(ops, T.KernelConfig(prec), out_values=ov))
+        out[f"c2_sddmm_{pname}_k32_us"] = round(us2, 2)
+        out[f"c2_sddmm_{pname}_gflops"] = round(2.0 * nnz * 32 / (us2 * 1e-6) / 1e9, 1)
+        out["graph_captured"] = bool(g and g2)
+        me.free()
+    t = []
+    for _ in range(5):  # conversion synchronises (data-dependent sizes): eager timing
+        e0.record()
+        m = T.encode_mebcrs(csr, T.Precision.fp16)
+        e1.record()
+        torch.cuda.synchronize()
+        t.append(e0.elapsed_time(e1) * 1e3)
+        m.free()
+    out["c2_encode_fp16_us"] = round(sorted(t)[len(t) // 2], 1)
+    out["nnz"] = int(nnz)
+    return out
 
 
 def bytes_alg_spmm(W, nv, rows, N, vwA, vwB):
@@ -472,6 +540,7 @@ def main():
     else:
         line = run_ours(args, rank, world, device)
         if line is not None and world == 1 and not args.quick:
+            line["small_configs"] = small_configs(device)
             line["cpu_baseline"] = cpu_baseline(args, device)
     if line is not None:
         print(json.dumps(line), flush=True)
