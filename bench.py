@@ -411,6 +411,15 @@ def run_e2e(args, T, _abi, local_csr, B, rows, cols, N, prec, device, world):
         assert rc == 0, lib.tcs_last_error()
         times.append(a.elapsed_time(b))
     ms = sum(times) / len(times)
+    # link check: plain pinned H2D of the same CSR bytes in this process state
+    d_ci = torch.empty_like(ci, device=device)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    d_ci.copy_(ci, non_blocking=True)
+    b.record(stream)
+    torch.cuda.synchronize()
+    h2d_gbs = ci.numel() * 4 / (a.elapsed_time(b) / 1e3) / 1e9
+    del d_ci
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     nnz = torch.tensor([local_csr.nnz], dtype=torch.float64, device=device)
     if world > 1:
@@ -420,6 +429,7 @@ def run_e2e(args, T, _abi, local_csr, B, rows, cols, N, prec, device, world):
     d2h = rows * N * 4
     return {"value": round(2.0 * float(nnz.item()) * N / (float(t.item()) / 1e3) / 1e9, 2), "unit": "GFLOP/s",
             "ms_per_step": round(float(t.item()), 3), "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "step_ms": [round(x, 2) for x in times], "pinned_h2d_gbs": round(h2d_gbs, 1),
             "call": "tcs_spmm_csr_host (host CSR + host f32 B -> host f32 C; GPU encode + SpMM)"}
 
 
