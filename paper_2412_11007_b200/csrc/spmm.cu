@@ -26,6 +26,7 @@
 // segment order by spmm_reduce_split (deterministic, no atomics).
 #include <algorithm>
 #include <type_traits>
+#include <vector>
 
 #include "tcs_internal.cuh"
 
@@ -601,28 +602,146 @@ extern "C" tcs_status tcs_spmm_host(uint64_t rows, uint64_t cols, tcs_precision 
     });
 }
 
+namespace tcs {
+namespace {
+__global__ void rebase_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t sub) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] -= sub;
+}
+
+struct Streams {
+    cudaStream_t copy = nullptr, compute = nullptr, drain = nullptr;
+    Streams() {
+        TCS_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
+        TCS_CUDA(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking));
+        TCS_CUDA(cudaStreamCreateWithFlags(&drain, cudaStreamNonBlocking));
+    }
+    ~Streams() {
+        cudaStreamDestroy(copy);
+        cudaStreamDestroy(compute);
+        cudaStreamDestroy(drain);
+    }
+};
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { TCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    ~Event() { cudaEventDestroy(e); }
+    void record(cudaStream_t s) { TCS_CUDA(cudaEventRecord(e, s)); }
+    void wait_on(cudaStream_t s) { TCS_CUDA(cudaStreamWaitEvent(s, e, 0)); }
+};
+}  // namespace
+}  // namespace tcs
+
+// The reference CLI pipeline (encode_mebcrs + spmm) from host buffers,
+// pipelined over window-range chunks: the copy stream uploads B then the
+// chunks' CSR slices back to back at link speed; the compute stream converts
+// and multiplies chunk i as soon as it has landed (conversion synchronises
+// the compute stream only, uploads keep flowing); the drain stream copies
+// each chunk's C rows back as soon as they are final.  Chunks are disjoint
+// row ranges, so the result is identical to a single encode + spmm.
 extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision precision, const float* b, int64_t n,
                                         float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
                                         tcs_stream_t stream) {
     return guard([&] {
-        if (!host_csr || !cfg) fail(TCS_ERR_ARGUMENT, "null argument");
+        if (!host_csr || !cfg || !host_csr->row_ptr) fail(TCS_ERR_ARGUMENT, "null argument");
+        if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
+        if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");
+        if (n < 0) fail(TCS_ERR_SHAPE, "negative dimension");
+        if (counters) *counters = tcs_counters{};
         cudaStream_t s = st(stream);
-        const uint64_t rows = host_csr->rows;
+        const uint64_t rows = host_csr->rows, nnz = host_csr->nnz, W = (rows + 7) / 8;
         const int64_t b_rows = static_cast<int64_t>(host_csr->cols);
-        tcs_mebcrs m{};
-        tcs_status rc = tcs_mebcrs_encode_host(host_csr, precision,
-                                               precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, stream);
-        if (rc != TCS_OK) fail(rc, tcs_last_error());
-        struct Free {
-            tcs_mebcrs* m;
-            tcs_stream_t s;
-            ~Free() { tcs_mebcrs_free(m, s); }
-        } fr{&m, stream};
-        DBuf db(std::max<int64_t>(1, b_rows * n) * 4, s), dc(std::max<uint64_t>(1, rows * n) * 4, s);
-        if (b_rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(db.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, s));
-        rc = tcs_spmm(&m, db.p, TCS_DTYPE_F32, n, b_rows, n, dc.as<float>(), n, cfg, counters, stream);
-        if (rc != TCS_OK) fail(rc, tcs_last_error());
-        if (rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(c, dc.p, rows * n * 4, cudaMemcpyDeviceToHost, s));
+        const uint32_t* hrp = host_csr->row_ptr;
+        if (hrp[0] != 0 || hrp[rows] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
+        if (rows == 0 || n == 0) return;
+
+        // chunk cut points: windows at nnz quantiles (host row_ptr)
+        const uint64_t nchunks = std::max<uint64_t>(1, std::min<uint64_t>({8, W, nnz / (1ull << 20) + 1}));
+        std::vector<uint64_t> wcut(nchunks + 1, 0);
+        for (uint64_t i = 1; i < nchunks; ++i) {
+            const uint64_t target = nnz * i / nchunks;
+            uint64_t lo = wcut[i - 1], hi = W;  // first window whose start >= target
+            while (lo < hi) {
+                const uint64_t mid = (lo + hi) / 2;
+                if (hrp[std::min(rows, 8 * mid)] < target) lo = mid + 1;
+                else hi = mid;
+            }
+            wcut[i] = lo;
+        }
+        wcut[nchunks] = W;
+
+        // device buffers, allocated in `stream` order before the fork
+        const bool f16 = precision == TCS_FP16;
+        DBuf d_rp((rows + nchunks) * 4, s), d_ci(std::max<uint64_t>(1, nnz) * 4, s),
+            d_v(std::max<uint64_t>(1, nnz) * 4, s), d_b32(std::max<int64_t>(1, b_rows * n) * 4, s),
+            d_c(rows * n * 4, s);
+        DBuf d_b16;
+        if (f16) d_b16 = DBuf(std::max<int64_t>(1, b_rows * n) * 2, s);
+        Streams ss;
+        Event forked;
+        forked.record(s);
+        forked.wait_on(ss.copy);
+        forked.wait_on(ss.compute);
+        forked.wait_on(ss.drain);
+
+        Event b_ready;
+        std::vector<Event> landed(nchunks), done(nchunks);
+        if (b_rows > 0) TCS_CUDA(cudaMemcpyAsync(d_b32.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, ss.copy));
+        b_ready.record(ss.copy);
+        for (uint64_t i = 0; i < nchunks; ++i) {
+            const uint64_t r0 = std::min(rows, 8 * wcut[i]), r1 = std::min(rows, 8 * wcut[i + 1]);
+            const uint64_t e0 = hrp[r0], e1 = hrp[r1];
+            TCS_CUDA(cudaMemcpyAsync(d_rp.as<uint32_t>() + r0 + i, hrp + r0, (r1 - r0 + 1) * 4, cudaMemcpyHostToDevice,
+                                     ss.copy));
+            if (e1 > e0) {
+                TCS_CUDA(cudaMemcpyAsync(d_ci.as<uint32_t>() + e0, host_csr->col_idx + e0, (e1 - e0) * 4,
+                                         cudaMemcpyHostToDevice, ss.copy));
+                TCS_CUDA(cudaMemcpyAsync(d_v.as<float>() + e0, host_csr->values + e0, (e1 - e0) * 4,
+                                         cudaMemcpyHostToDevice, ss.copy));
+            }
+            landed[i].record(ss.copy);
+        }
+        // dense operand in the kernel's storage type, once
+        b_ready.wait_on(ss.compute);
+        const void* bdev = d_b32.p;
+        tcs_dtype bdt = TCS_DTYPE_F32;
+        if (f16) {
+            pad_convert(d_b32.p, TCS_DTYPE_F32, n, d_b16.p, TCS_DTYPE_F16, n, b_rows, n, n, ss.compute);
+            bdev = d_b16.p;
+            bdt = TCS_DTYPE_F16;
+        }
+        tcs_stream_t ks = reinterpret_cast<tcs_stream_t>(ss.compute);
+        for (uint64_t i = 0; i < nchunks; ++i) {
+            const uint64_t r0 = std::min(rows, 8 * wcut[i]), r1 = std::min(rows, 8 * wcut[i + 1]);
+            const uint64_t e0 = hrp[r0], e1 = hrp[r1];
+            landed[i].wait_on(ss.compute);
+            uint32_t* rp_i = d_rp.as<uint32_t>() + r0 + i;
+            if (e0) {
+                rebase_u32<<<static_cast<unsigned>(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024)), 256, 0,
+                             ss.compute>>>(rp_i, r1 - r0 + 1, static_cast<uint32_t>(e0));
+                TCS_LAUNCHED("rebase_u32");
+            }
+            tcs_csr chunk{r1 - r0, host_csr->cols, e1 - e0, rp_i, d_ci.as<uint32_t>() + e0, d_v.as<float>() + e0};
+            tcs_mebcrs m{};
+            tcs_status rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
+            if (rc != TCS_OK) fail(rc, tcs_last_error());
+            tcs_counters cn{};
+            rc = tcs_spmm(&m, bdev, bdt, n, b_rows, n, d_c.as<float>() + r0 * n, n, cfg, counters ? &cn : nullptr, ks);
+            tcs_mebcrs_free(&m, ks);
+            if (rc != TCS_OK) fail(rc, tcs_last_error());
+            if (counters) counters->mma_invocations += cn.mma_invocations;
+            done[i].record(ss.compute);
+            done[i].wait_on(ss.drain);
+            TCS_CUDA(cudaMemcpyAsync(c + r0 * n, d_c.as<float>() + r0 * n, (r1 - r0) * n * 4, cudaMemcpyDeviceToHost,
+                                     ss.drain));
+        }
+        Event joined_copy, joined_compute, joined_drain;
+        joined_copy.record(ss.copy);
+        joined_compute.record(ss.compute);
+        joined_drain.record(ss.drain);
+        joined_copy.wait_on(s);
+        joined_compute.wait_on(s);
+        joined_drain.wait_on(s);
         TCS_CUDA(cudaStreamSynchronize(s));
     });
 }

@@ -101,7 +101,20 @@ def test_power_law_midsize_bit_exact(p):
     B = O.generate_random_dense(cols, 128, 9)
     Bd = torch.from_numpy(B).cuda()
     got = T.spmm(me, Bd.half() if p == 0 else Bd, T.KernelConfig(T.Precision(p))).output.cpu().numpy()
-    assert np.array_equal(got.view(np.uint32), O.spmm(ref, B).view(np.uint32))
+    want = O.spmm(ref, B)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    # the pipelined host-buffer call (3 window-range chunks at 3 M nnz)
+    import paper_2412_11007_b200._abi as abi
+
+    csr = abi.tcs_csr(rows, cols, m.nnz, m.row_ptr.ctypes.data, m.col_idx.ctypes.data, m.values.ctypes.data)
+    cfg = abi.tcs_kernel_config(p, 8, 1, 0)
+    cnt = abi.tcs_counters()
+    Ch = np.empty((rows, 128), np.float32)
+    rc = abi.load().tcs_spmm_csr_host(C.byref(csr), p, B.ctypes.data, 128, Ch.ctypes.data, C.byref(cfg),
+                                      C.byref(cnt), None)
+    assert rc == 0, abi.load().tcs_last_error()
+    assert np.array_equal(Ch.view(np.uint32), want.view(np.uint32))
+    assert cnt.mma_invocations == O.count_mma_spmm(ref, 128)
 
 
 def test_config3_full_size_properties():
