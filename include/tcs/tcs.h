@@ -92,6 +92,7 @@ typedef struct tcs_mebcrs {
 
 #define TCS_MEBCRS_OWN_STRUCTURE 0x1u /* row_pointers + column_indices */
 #define TCS_MEBCRS_OWN_VALUES 0x2u
+#define TCS_MEBCRS_BORROWED_PLAN 0x4u /* work list shared with the handle the structure came from */
 
 /* ref: spmm.hpp:17-21 (KernelConfig). */
 typedef struct tcs_kernel_config {
@@ -181,6 +182,18 @@ tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, i
                      int64_t f_a, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows,
                      int64_t f_b, tcs_mebcrs* out, tcs_dtype out_dtype, const tcs_kernel_config* cfg,
                      tcs_counters* counters, tcs_stream_t stream);
+
+/* ---------------------------------------------------- AGNN row softmax */
+/* Row-wise softmax over the ME-BCRS pattern, the middle stage of the AGNN
+ * attention layer (SDDMM -> row softmax -> SpMM).  Not a
+ * reference operator.  For every row r of every window:
+ *   out[pos] = exp(scale*scores[pos] - max_r) / sum_r  at live positions,
+ * live = mask value != 0 (the SDDMM sampling rule, ref sddmm.hpp:131); all
+ * other slots 0.  scores and mask share one structure (an SDDMM output and
+ * its mask).  `out` receives that structure (aliased) and values of
+ * out_dtype, library-allocated if out->values is NULL. */
+tcs_status tcs_mebcrs_row_softmax(const tcs_mebcrs* scores, const tcs_mebcrs* mask, float scale, tcs_mebcrs* out,
+                                  tcs_dtype out_dtype, tcs_stream_t stream);
 
 /* ------------------------------------------------- host-buffer entry points */
 /* Value semantics of the reference API: host arrays in, host arrays out.  */

@@ -315,8 +315,9 @@ tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream) {
     return guard([&] {
         check_mebcrs(m);
         cudaStream_t s = st(stream);
-        if (m->plan) free_plan(static_cast<Plan*>(m->plan), s);
+        if (m->plan && !(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
         m->plan = nullptr;
+        m->flags &= ~TCS_MEBCRS_BORROWED_PLAN;
         uint32_t mx = 0;
         uint64_t blocks = 0, groups = 0;
         m->plan = build_plan(m, s, &mx, &blocks, &groups);
@@ -335,7 +336,7 @@ tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream) {
             dfree(m->column_indices, s);
         }
         if (m->flags & TCS_MEBCRS_OWN_VALUES) dfree(m->values, s);
-        free_plan(static_cast<Plan*>(m->plan), s);
+        if (!(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
         std::memset(m, 0, sizeof(*m));
     });
 }

@@ -349,15 +349,14 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
         const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4;
         void* caller_values = out->values;
         tcs_mebcrs o = *mask;
-        o.flags = 0;
-        o.plan = nullptr;
+        o.flags = o.plan ? TCS_MEBCRS_BORROWED_PLAN : 0u;  // structure and work list shared
         o.value_dtype = out_dtype;
         if (tf32 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
         if (caller_values) {
             o.values = caller_values;
         } else {
             o.values = dalloc(std::max<uint64_t>(1, 8 * mask->num_vectors) * ow, s);
-            o.flags = TCS_MEBCRS_OWN_VALUES;
+            o.flags |= TCS_MEBCRS_OWN_VALUES;
         }
         if (counters) *counters = tcs_counters{};
         const uint64_t nv = mask->num_vectors;

@@ -1,0 +1,75 @@
+"""GNN layers on the B200 FlashSparse kernels -- the callers that BASELINE.json
+configs[3] and configs[4] name ("end-to-end GNN"):
+
+* ``GCNLayer``: H' = Â (H W) with Â = D^-1/2 (A + I) D^-1/2 (Kipf & Welling).
+  The dense transform H W is a plain library GEMM (cuBLAS through torch);
+  the aggregation Â · (HW) is tcs_spmm over the ME-BCRS encoding of Â.
+* ``AGNNLayer``: H' = softmax_row(beta * cos(h_i, h_j) on the edges) · H.
+  cos via tcs_sddmm over the row-normalised features, the row softmax via
+  tcs_mebcrs_row_softmax (binary16 probabilities), the aggregation via
+  tcs_spmm on the probability matrix -- no re-encoding between stages (the
+  pipeline closure of ref tests/test_kernels.cpp:313-327).
+
+Inputs are torch CUDA tensors; the graph is given once as CSR and encoded
+once on the GPU.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import _abi
+from . import tcsparse as T
+
+
+def normalized_adjacency(rows: int, row_ptr: torch.Tensor, col_idx: torch.Tensor, add_self_loops: bool = True):
+    """CSR of D^-1/2 (A + I) D^-1/2 (values f32) from a pattern CSR (int32)."""
+    dev = row_ptr.device
+    rp = row_ptr.to(torch.int64)
+    ci = col_idx.to(torch.int64)
+    r = torch.repeat_interleave(torch.arange(rows, device=dev), rp[1:] - rp[:-1])
+    if add_self_loops:
+        keys = torch.unique(torch.cat([r * rows + ci, torch.arange(rows, device=dev) * (rows + 1)]))
+        r, ci = keys // rows, keys % rows
+    deg = torch.bincount(r, minlength=rows).to(torch.float32)
+    dinv = deg.clamp(min=1).rsqrt()
+    vals = dinv[r] * dinv[ci]
+    new_rp = torch.zeros(rows + 1, dtype=torch.int64, device=dev)
+    new_rp[1:] = torch.cumsum(torch.bincount(r, minlength=rows), 0)
+    return new_rp.to(torch.int32), ci.to(torch.int32), vals
+
+
+class GCNLayer:
+    def __init__(self, rows: int, row_ptr: torch.Tensor, col_idx: torch.Tensor, weight: torch.Tensor,
+                 precision: T.Precision = T.Precision.fp16):
+        rp, ci, v = normalized_adjacency(rows, row_ptr, col_idx)
+        self.rows = rows
+        self.adj = T.encode_mebcrs(T.CsrMatrix(rows, rows, rp, ci, v), precision)
+        self.weight = weight
+        self.cfg = T.KernelConfig(precision)
+        self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
+
+    def __call__(self, H: torch.Tensor) -> torch.Tensor:
+        HW = (H.to(self.weight.dtype) @ self.weight).to(self.dtype)  # cuBLAS GEMM
+        return T.spmm(self.adj, HW, self.cfg).output
+
+
+class AGNNLayer:
+    def __init__(self, rows: int, row_ptr: torch.Tensor, col_idx: torch.Tensor, beta: float = 1.0,
+                 precision: T.Precision = T.Precision.fp16):
+        ones = torch.ones(col_idx.numel(), dtype=torch.float32, device=col_idx.device)
+        self.rows = rows
+        self.mask = T.encode_mebcrs(T.CsrMatrix(rows, rows, row_ptr, col_idx, ones), precision)
+        self.beta = float(beta)
+        self.cfg = T.KernelConfig(precision)
+        self.precision = precision
+        self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
+
+    def attention(self, H: torch.Tensor) -> T.MeBcrsMatrix:
+        Hn = torch.nn.functional.normalize(H.float(), dim=1).to(self.dtype)
+        scores = T.sddmm(T.SddmmOperands(self.mask, Hn, Hn), self.cfg).output  # cos(h_i, h_j) at the edges
+        pdt = _abi.TCS_DTYPE_F16 if self.precision == T.Precision.fp16 else _abi.TCS_DTYPE_F32
+        return T.row_softmax(scores, self.mask, self.beta, pdt)
+
+    def __call__(self, H: torch.Tensor) -> torch.Tensor:
+        P = self.attention(H)
+        return T.spmm(P, H.to(self.dtype), self.cfg).output

@@ -250,6 +250,20 @@ def sddmm(ops: SddmmOperands, cfg: KernelConfig = KernelConfig(), out_dtype: int
     return SddmmResult(MeBcrsMatrix(h, keepalive=keep), KernelCounters._from(cnt))
 
 
+def row_softmax(scores: MeBcrsMatrix, mask: MeBcrsMatrix, scale: float = 1.0,
+                out_dtype: int = _abi.TCS_DTYPE_F16, out_values: torch.Tensor | None = None) -> MeBcrsMatrix:
+    """Row-wise softmax over the pattern (tcs_mebcrs_row_softmax): the AGNN
+    attention normalisation between SDDMM and SpMM."""
+    h = _abi.tcs_mebcrs()
+    keep = [scores, mask]
+    if out_values is not None:
+        h.values = out_values.data_ptr()
+        keep.append(out_values)
+    _check(_abi.load().tcs_mebcrs_row_softmax(C.byref(scores._h), C.byref(mask._h), float(scale), C.byref(h),
+                                              int(out_dtype), _stream()))
+    return MeBcrsMatrix(h, keepalive=keep)
+
+
 def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
     """Device operand rounding used by the kernels (diagnostics)."""
     x = x.to(torch.float32).contiguous()

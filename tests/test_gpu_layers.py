@@ -1,0 +1,107 @@
+"""GPU: the GNN-layer glue (§8(f1)) -- row softmax over the ME-BCRS pattern,
+the AGNN attention layer (SDDMM -> row softmax -> SpMM) and the GCN layer
+(cuBLAS GEMM + SpMM), against plain PyTorch fp64 references of the same
+ops (the reference library has no GNN layers)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+T = L = None
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    global T, L
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2412_11007_b200.layers as layers
+    import paper_2412_11007_b200.tcsparse as tcs
+
+    T, L = tcs, layers
+
+
+def dense_pattern(m: O.Csr):
+    mask = np.zeros((m.rows, m.cols), bool)
+    r = np.repeat(np.arange(m.rows), np.diff(m.row_ptr.astype(np.int64)))
+    mask[r, m.col_idx] = m.values != 0
+    return mask
+
+
+def softmax_ref(S, mask, scale):
+    S = torch.as_tensor(S, dtype=torch.float64) * scale
+    M = torch.as_tensor(mask)
+    S = S.masked_fill(~M, float("-inf"))
+    P = torch.softmax(S, dim=1)
+    return torch.nan_to_num(P, nan=0.0).masked_fill(~M, 0.0)
+
+
+@pytest.mark.parametrize("p", [0, 1])
+@pytest.mark.parametrize("out_f16", [False, True])
+def test_row_softmax_matches_torch(p, out_f16):
+    if p == 1 and out_f16:
+        pytest.skip("TF32 stores f32")
+    m = O.generate_random_sparse(203, 150, 0.08, 17, real=True)
+    m.values[::7] = 0.0  # explicit zeros: stored vectors that are not live
+    me = T.encode_mebcrs(T.CsrMatrix(m.rows, m.cols, torch.from_numpy(m.row_ptr.view(np.int32)).cuda(),
+                                     torch.from_numpy(m.col_idx.view(np.int32)).cuda(),
+                                     torch.from_numpy(m.values).cuda()), T.Precision(p), 1)
+    A = torch.randn(m.rows, 24, device="cuda")
+    Bt = torch.randn(m.cols, 24, device="cuda")
+    scores = T.sddmm(T.SddmmOperands(me, A, Bt), T.KernelConfig(T.Precision(p))).output
+    P = T.row_softmax(scores, me, 0.7, 0 if out_f16 else 1)
+    rp, ci, sv = scores.to_host()
+    pv = P.to_host()[2]
+    S = O.mebcrs_to_dense(O.MeBcrs(m.rows, m.cols, p, rp, ci, sv))
+    # live-but-zero scores are dropped by mebcrs_to_dense; recompute them densely
+    mask = dense_pattern(m)
+    S_full = (A.double() @ Bt.double().T).cpu().numpy()
+    S = np.where(mask, S_full, 0.0)
+    want = softmax_ref(S, mask, 0.7).numpy()
+    got = O.mebcrs_to_dense(O.MeBcrs(m.rows, m.cols, p, rp, ci, pv))
+    tol = 2e-3 if out_f16 or p == 0 else 1e-4
+    assert np.abs(got - want).max() < tol
+    assert np.all(got[~mask] == 0)
+    # rows sum to 1 where the row has live entries
+    sums = got.sum(1)
+    live_rows = mask.any(1)
+    assert np.allclose(sums[live_rows], 1.0, atol=5e-3)
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_agnn_layer_matches_dense_reference(p):
+    n, F = 517, 32
+    m = O.generate_random_sparse(n, n, 0.02, 23)
+    rp = torch.from_numpy(m.row_ptr.view(np.int32)).cuda()
+    ci = torch.from_numpy(m.col_idx.view(np.int32)).cuda()
+    H = torch.randn(n, F, device="cuda")
+    layer = L.AGNNLayer(n, rp, ci, beta=1.5, precision=T.Precision(p))
+    got = layer(H).double().cpu()
+    Hn = torch.nn.functional.normalize(H.double(), dim=1).cpu()
+    mask = torch.as_tensor(dense_pattern(m) | (np.abs(O.Csr(n, n, m.row_ptr, m.col_idx, np.ones(m.nnz, np.float32))
+                                                       .to_dense()) > 0))
+    P = softmax_ref((Hn @ Hn.T).numpy(), mask.numpy(), 1.5)
+    want = P @ H.double().cpu()
+    err = (got - want).norm() / want.norm()
+    assert err < (1e-2 if p == 0 else 1e-3), float(err)
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_gcn_layer_matches_dense_reference(p):
+    n, Fi, Fo = 700, 64, 128
+    m = O.generate_random_sparse(n, n, 0.01, 29)
+    rp = torch.from_numpy(m.row_ptr.view(np.int32)).cuda()
+    ci = torch.from_numpy(m.col_idx.view(np.int32)).cuda()
+    W = torch.randn(Fi, Fo, device="cuda") / Fi ** 0.5
+    H = torch.randn(n, Fi, device="cuda")
+    layer = L.GCNLayer(n, rp, ci, W.half() if p == 0 else W, precision=T.Precision(p))
+    got = layer(H).double().cpu()
+    A = torch.as_tensor(dense_pattern(O.Csr(n, n, m.row_ptr, m.col_idx, np.ones(m.nnz, np.float32)))).double()
+    A = ((A + torch.eye(n, dtype=torch.float64)) > 0).double()
+    dinv = A.sum(1).rsqrt()
+    Ahat = dinv[:, None] * A * dinv[None, :]
+    want = Ahat @ (H.double().cpu() @ W.double().cpu())
+    err = (got - want).norm() / want.norm()
+    assert err < (1e-2 if p == 0 else 1e-3), float(err)
