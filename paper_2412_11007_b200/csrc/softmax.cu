@@ -8,10 +8,15 @@
 //   out[pos] = exp(scale*x[pos] - max_r) / sum_r   over the live positions
 //              of row r of the window; every other slot 0.
 //
-// One warp per window (grid-stride): lane handles vectors v = lane + 32i;
-// for each vector the 8 rows are visited in a static loop, so the per-row
-// running max / sum stay in registers; three passes (max, sum, write) over
-// the window's contiguous value region, warp-reduced per row.
+// Runs on the SpMM/SDDMM work list, so hub windows (R-MAT: 450 K vectors in
+// one window) are spread over many warps:
+//   K1 softmax_items   persistent warps; per item one online pass computes the
+//                      per-row (max, sum exp) over the item's vectors (lane v
+//                      = lane + 32i, the 8 rows in registers, warp-merged);
+//                      an unsplit window is normalised in place right away,
+//                      a split segment stores its 8 partials.
+//   K2 softmax_combine per split window: merges the segments' partials.
+//   K3 softmax_finish  writes the normalised values of split segments.
 #include <algorithm>
 #include <cfloat>
 
@@ -45,82 +50,182 @@ __device__ __forceinline__ void st_val<float>(float* p, uint64_t i, float x) { p
 template <>
 __device__ __forceinline__ void st_val<__half>(__half* p, uint64_t i, float x) { p[i] = __float2half_rn(x); }
 
+struct RowStat {
+    float m, s;  // running max, sum of exp(x - m)
+};
+
+__device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {
+    const float mm = fmaxf(m, m2);
+    s = (m == -FLT_MAX ? 0.f : s * __expf(m - mm)) + (m2 == -FLT_MAX ? 0.f : s2 * __expf(m2 - mm));
+    m = mm;
+}
+
+template <uint32_t K>
+__device__ __forceinline__ uint64_t vpos(uint64_t vb, uint32_t nvw, uint32_t v, uint32_t r) {
+    const uint32_t b = v / K, width = min(K, nvw - b * K);
+    return vb + 8ull * K * b + r * width + (v - b * K);
+}
+
 template <uint32_t K, typename VS, typename VM, typename VO>
-__global__ void __launch_bounds__(256) row_softmax_kernel(const uint32_t* __restrict__ rp, uint64_t W,
-                                                          const VS* __restrict__ scores, const VM* __restrict__ mask,
-                                                          VO* __restrict__ out, float scale) {
-    const uint32_t lane = threadIdx.x & 31;
-    const uint64_t warp0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
-    for (uint64_t w = warp0; w < W; w += nwarps) {
-        const uint32_t base = rp[w], nvw = rp[w + 1] - base;
-        if (nvw == 0) continue;
-        const uint64_t vb = 8ull * base;
-        auto pos = [&](uint32_t v, uint32_t r) -> uint64_t {
-            const uint32_t b = v / K, width = min(K, nvw - b * K);
-            return vb + 8ull * K * b + r * width + (v - b * K);
-        };
-        float mx[8], sm[8];
+__device__ __forceinline__ void write_range(const VS* scores, const VM* mask, VO* out, uint64_t vb, uint32_t nvw,
+                                            uint32_t v0, uint32_t v1, uint32_t lane, float scale, const float (&m)[8],
+                                            const float (&inv)[8]) {
+    for (uint32_t v = v0 + lane; v < v1; v += 32)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-            mx[r] = -FLT_MAX;
-            sm[r] = 0.f;
+            const uint64_t p = vpos<K>(vb, nvw, v, r);
+            const float y = live_at<VM>(mask, p) ? __expf(scale * ld_val<VS>(scores, p) - m[r]) * inv[r] : 0.f;
+            st_val<VO>(out, p, y);
         }
-        for (uint32_t v = lane; v < nvw; v += 32)
+}
+
+template <uint32_t K, typename VS, typename VM, typename VO>
+__global__ void __launch_bounds__(256) softmax_items(const WorkItem* __restrict__ items, uint64_t n_items,
+                                                     uint32_t* counter, const uint32_t* __restrict__ rp,
+                                                     const VS* __restrict__ scores, const VM* __restrict__ mask,
+                                                     VO* __restrict__ out, float scale, RowStat* __restrict__ part) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (;;) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(counter, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= n_items) break;
+        const WorkItem it = items[idx];
+        const uint32_t base = __ldg(rp + it.window), nvw = __ldg(rp + it.window + 1) - base;
+        const uint64_t vb = 8ull * base;
+        float m[8], s[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            m[r] = -FLT_MAX;
+            s[r] = 0.f;
+        }
+        for (uint32_t v = it.vbeg + lane; v < it.vend; v += 32)
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
-                const uint64_t p = pos(v, r);
-                if (live_at<VM>(mask, p)) mx[r] = fmaxf(mx[r], scale * ld_val<VS>(scores, p));
+                const uint64_t p = vpos<K>(vb, nvw, v, r);
+                if (live_at<VM>(mask, p)) {
+                    const float x = scale * ld_val<VS>(scores, p);
+                    if (x > m[r]) {
+                        s[r] = (m[r] == -FLT_MAX ? 0.f : s[r] * __expf(m[r] - x)) + 1.f;
+                        m[r] = x;
+                    } else {
+                        s[r] += __expf(x - m[r]);
+                    }
+                }
             }
 #pragma unroll
         for (int r = 0; r < 8; ++r)
 #pragma unroll
-            for (int o = 16; o; o >>= 1) mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], o));
-        for (uint32_t v = lane; v < nvw; v += 32)
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint64_t p = pos(v, r);
-                if (live_at<VM>(mask, p)) sm[r] += expf(scale * ld_val<VS>(scores, p) - mx[r]);
+            for (int o = 16; o; o >>= 1) {
+                const float m2 = __shfl_xor_sync(0xffffffffu, m[r], o), s2 = __shfl_xor_sync(0xffffffffu, s[r], o);
+                merge(m[r], s[r], m2, s2);
             }
+        if (it.slot != kNoSlot) {  // segment of a split window: publish partials
+            if (lane < 8) {
+                float mv = m[0], sv = s[0];
+#pragma unroll
+                for (int r = 1; r < 8; ++r)
+                    if (lane == (uint32_t)r) {
+                        mv = m[r];
+                        sv = s[r];
+                    }
+                part[8ull * it.slot + lane] = RowStat{mv, sv};
+            }
+            continue;
+        }
+        float inv[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) inv[r] = s[r] > 0.f ? 1.f / s[r] : 0.f;
+        write_range<K, VS, VM, VO>(scores, mask, out, vb, nvw, it.vbeg, it.vend, lane, scale, m, inv);
+    }
+}
+
+// one thread per (split window, row): merge the segments' partials in place
+// into the first segment's slot
+__global__ void softmax_combine(const SplitWindow* __restrict__ split, uint64_t n_split, RowStat* __restrict__ part) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 8 * n_split;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const SplitWindow sw = split[i / 8];
+        const uint32_t r = static_cast<uint32_t>(i % 8);
+        float m = -FLT_MAX, s = 0.f;
+        for (uint32_t q = 0; q < sw.nseg; ++q) {
+            const RowStat x = part[8ull * (sw.first_slot + q) + r];
+            merge(m, s, x.m, x.s);
+        }
+        part[8ull * sw.first_slot + r] = RowStat{m, s};
+    }
+}
+
+template <uint32_t K, typename VS, typename VM, typename VO>
+__global__ void __launch_bounds__(256) softmax_finish(const WorkItem* __restrict__ items, uint64_t n_slots,
+                                                      const SplitWindow* __restrict__ split, uint64_t n_split,
+                                                      const uint32_t* __restrict__ rp, const VS* __restrict__ scores,
+                                                      const VM* __restrict__ mask, VO* __restrict__ out, float scale,
+                                                      const RowStat* __restrict__ part) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    // split items occupy item indices [0, n_slots), slot == index
+    for (uint64_t idx = w0; idx < n_slots; idx += nw) {
+        const WorkItem it = items[idx];
+        // first slot of this item's window: binary search the split list
+        uint64_t lo = 0, hi = n_split;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (split[mid].first_slot <= it.slot) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t fs = split[lo].first_slot;
+        float m[8], inv[8];
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-#pragma unroll
-            for (int o = 16; o; o >>= 1) sm[r] += __shfl_xor_sync(0xffffffffu, sm[r], o);
-            sm[r] = sm[r] > 0.f ? 1.f / sm[r] : 0.f;
+            const RowStat x = part[8ull * fs + r];
+            m[r] = x.m;
+            inv[r] = x.s > 0.f ? 1.f / x.s : 0.f;
         }
-        for (uint32_t v = lane; v < nvw; v += 32)
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint64_t p = pos(v, r);
-                const float y = live_at<VM>(mask, p) ? expf(scale * ld_val<VS>(scores, p) - mx[r]) * sm[r] : 0.f;
-                st_val<VO>(out, p, y);
-            }
+        const uint32_t base = __ldg(rp + it.window), nvw = __ldg(rp + it.window + 1) - base;
+        write_range<K, VS, VM, VO>(scores, mask, out, 8ull * base, nvw, it.vbeg, it.vend, lane, scale, m, inv);
+    }
+}
+
+template <uint32_t K, typename VS, typename VM, typename VO>
+void run(const tcs_mebcrs* sc, const tcs_mebcrs* mk, VO* out, float scale, const Plan* plan, cudaStream_t s) {
+    const VS* sv = static_cast<const VS*>(sc->values);
+    const VM* mv = static_cast<const VM*>(mk->values);
+    DBuf ctr(sizeof(uint32_t), s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
+    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(uint32_t), s));
+    const int grid = static_cast<int>(std::min<uint64_t>((plan->n_items + 7) / 8, uint64_t(num_sms()) * 8));
+    softmax_items<K, VS, VM, VO><<<std::max(grid, 1), 256, 0, s>>>(plan->items, plan->n_items, ctr.as<uint32_t>(),
+                                                                   sc->row_pointers, sv, mv, out, scale,
+                                                                   part.as<RowStat>());
+    TCS_LAUNCHED("softmax_items");
+    if (plan->n_split) {
+        softmax_combine<<<static_cast<int>(std::min<uint64_t>((8 * plan->n_split + 255) / 256, 1024)), 256, 0, s>>>(
+            plan->split, plan->n_split, part.as<RowStat>());
+        TCS_LAUNCHED("softmax_combine");
+        const int g3 = static_cast<int>(std::min<uint64_t>((plan->n_slots + 7) / 8, uint64_t(num_sms()) * 8));
+        softmax_finish<K, VS, VM, VO><<<std::max(g3, 1), 256, 0, s>>>(plan->items, plan->n_slots, plan->split,
+                                                                      plan->n_split, sc->row_pointers, sv, mv, out,
+                                                                      scale, part.as<RowStat>());
+        TCS_LAUNCHED("softmax_finish");
     }
 }
 
 template <uint32_t K, typename VS, typename VM>
-void launch_out(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt, float scale, cudaStream_t s) {
-    const uint64_t W = sc->num_windows;
-    const int grid = static_cast<int>(std::min<uint64_t>((W + 7) / 8, uint64_t(num_sms()) * 8));
-    if (odt == TCS_DTYPE_F32)
-        row_softmax_kernel<K, VS, VM, float><<<grid, 256, 0, s>>>(sc->row_pointers, W, static_cast<const VS*>(sc->values),
-                                                                  static_cast<const VM*>(mk->values),
-                                                                  static_cast<float*>(out), scale);
-    else
-        row_softmax_kernel<K, VS, VM, __half><<<grid, 256, 0, s>>>(sc->row_pointers, W,
-                                                                   static_cast<const VS*>(sc->values),
-                                                                   static_cast<const VM*>(mk->values),
-                                                                   static_cast<__half*>(out), scale);
-    TCS_LAUNCHED("row_softmax");
+void run_o(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt, float scale, const Plan* plan,
+           cudaStream_t s) {
+    if (odt == TCS_DTYPE_F32) run<K, VS, VM, float>(sc, mk, static_cast<float*>(out), scale, plan, s);
+    else run<K, VS, VM, __half>(sc, mk, static_cast<__half*>(out), scale, plan, s);
 }
 
 template <uint32_t K>
-void launch_k(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt, float scale, cudaStream_t s) {
+void run_k(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt, float scale, const Plan* plan,
+           cudaStream_t s) {
     const bool s32 = sc->value_dtype == TCS_DTYPE_F32, m32 = mk->value_dtype == TCS_DTYPE_F32;
-    if (s32 && m32) launch_out<K, float, float>(sc, mk, out, odt, scale, s);
-    else if (s32) launch_out<K, float, __half>(sc, mk, out, odt, scale, s);
-    else if (m32) launch_out<K, __half, float>(sc, mk, out, odt, scale, s);
-    else launch_out<K, __half, __half>(sc, mk, out, odt, scale, s);
+    if (s32 && m32) run_o<K, float, float>(sc, mk, out, odt, scale, plan, s);
+    else if (s32) run_o<K, float, __half>(sc, mk, out, odt, scale, plan, s);
+    else if (m32) run_o<K, __half, float>(sc, mk, out, odt, scale, plan, s);
+    else run_o<K, __half, __half>(sc, mk, out, odt, scale, plan, s);
 }
 
 }  // namespace
@@ -153,8 +258,16 @@ extern "C" tcs_status tcs_mebcrs_row_softmax(const tcs_mebcrs* scores, const tcs
             o.flags |= TCS_MEBCRS_OWN_VALUES;
         }
         if (scores->num_vectors && scores->num_windows) {
-            if (scores->k == 8) launch_k<8>(scores, mask, o.values, out_dtype, scale, s);
-            else launch_k<4>(scores, mask, o.values, out_dtype, scale, s);
+            const Plan* plan = static_cast<const Plan*>(scores->plan ? scores->plan : mask->plan);
+            Plan* tmp = nullptr;
+            if (!plan) plan = tmp = build_plan(scores, s, nullptr, nullptr, nullptr);
+            struct G {
+                Plan* p;
+                cudaStream_t s;
+                ~G() { free_plan(p, s); }
+            } g{tmp, s};
+            if (scores->k == 8) run_k<8>(scores, mask, o.values, out_dtype, scale, plan, s);
+            else run_k<4>(scores, mask, o.values, out_dtype, scale, plan, s);
         }
         *out = o;
     });

@@ -69,6 +69,34 @@ def test_row_softmax_matches_torch(p, out_f16):
     assert np.allclose(sums[live_rows], 1.0, atol=5e-3)
 
 
+def test_row_softmax_split_hub_windows():
+    """Windows longer than the work-list segment: per-segment partials are
+    merged (online softmax) before normalisation."""
+    rng = np.random.default_rng(3)
+    rows, cols = 40, 30000
+    per_row = [25000] * 8 + [3] * 8 + [9000] * 8 + [0] * 8 + [100] * 8
+    rp = np.zeros(rows + 1, np.uint32)
+    cis = []
+    for r, d in enumerate(per_row):
+        cis.append(np.sort(rng.choice(cols, size=d, replace=False)).astype(np.uint32))
+        rp[r + 1] = rp[r] + d
+    ci = np.concatenate(cis)
+    m = O.Csr(rows, cols, rp, ci, np.ones(ci.size, np.float32))
+    me = T.encode_mebcrs(T.CsrMatrix(rows, cols, torch.from_numpy(rp.view(np.int32)).cuda(),
+                                     torch.from_numpy(ci.view(np.int32)).cuda(),
+                                     torch.from_numpy(m.values).cuda()), T.Precision.fp16, 1)
+    assert me.max_window_vectors > 8 * 256  # several segments
+    A = torch.randn(rows, 16, device="cuda")
+    Bt = torch.randn(cols, 16, device="cuda")
+    scores = T.sddmm(T.SddmmOperands(me, A, Bt), T.KernelConfig()).output
+    P = T.row_softmax(scores, me, 2.0, 1)
+    rph, cih, sv = scores.to_host()
+    got = O.mebcrs_to_dense(O.MeBcrs(rows, cols, 0, rph, cih, P.to_host()[2]))
+    S = O.mebcrs_to_dense(O.MeBcrs(rows, cols, 0, rph, cih, sv))
+    want = softmax_ref(S, dense_pattern(m), 2.0).numpy()
+    assert np.abs(got - want).max() < 1e-5 + 1e-4 * np.abs(want).max()
+
+
 @pytest.mark.parametrize("p", [0, 1])
 def test_agnn_layer_matches_dense_reference(p):
     n, F = 517, 32
