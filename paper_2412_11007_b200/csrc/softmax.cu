@@ -11,8 +11,10 @@
 // Runs on the SpMM/SDDMM work list, so hub windows (R-MAT: 450 K vectors in
 // one window) are spread over many warps:
 //   K1 softmax_items   persistent warps; per item one online pass computes the
-//                      per-row (max, sum exp) over the item's vectors (lane v
-//                      = lane + 32i, the 8 rows in registers, warp-merged);
+//                      per-row (max, sum exp) over the item's vectors: a full
+//                      block is row-major (8 rows x K), so lane l streams row
+//                      l%8 of block l/8 with one K-wide vector load and keeps
+//                      scalar statistics for that row (xor-8/16 merged);
 //                      an unsplit window is normalised in place right away,
 //                      a split segment stores its 8 partials.
 //   K2 softmax_combine per split window: merges the segments' partials.
@@ -60,23 +62,142 @@ __device__ __forceinline__ void merge(float& m, float& s, float m2, float s2) {
     m = mm;
 }
 
-template <uint32_t K>
-__device__ __forceinline__ uint64_t vpos(uint64_t vb, uint32_t nvw, uint32_t v, uint32_t r) {
-    const uint32_t b = v / K, width = min(K, nvw - b * K);
-    return vb + 8ull * K * b + r * width + (v - b * K);
+// ---- K-wide vector access to one block row (16-B / 8-B aligned: the block
+// row starts at element 8*base + 8K*b + r*K)
+template <int N>
+__device__ __forceinline__ void ldv(const float* p, float (&x)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(p + i));
+        x[i] = t.x; x[i + 1] = t.y; x[i + 2] = t.z; x[i + 3] = t.w;
+    }
+}
+template <int N>
+__device__ __forceinline__ void ldv(const __half* p, float (&x)[N]) {
+    if constexpr (N == 8) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {t.x, t.y, t.z, t.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+            x[2 * i] = f.x; x[2 * i + 1] = f.y;
+        }
+    } else {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        const uint32_t w[2] = {t.x, t.y};
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
+            x[2 * i] = f.x; x[2 * i + 1] = f.y;
+        }
+    }
+}
+template <int N>
+__device__ __forceinline__ void ldlive(const float* p, bool (&l)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p + i));
+        l[i] = (t.x & 0x7FFFFFFFu) != 0; l[i + 1] = (t.y & 0x7FFFFFFFu) != 0;
+        l[i + 2] = (t.z & 0x7FFFFFFFu) != 0; l[i + 3] = (t.w & 0x7FFFFFFFu) != 0;
+    }
+}
+template <int N>
+__device__ __forceinline__ void ldlive(const __half* p, bool (&l)[N]) {
+    uint32_t w[N / 2];
+    if constexpr (N == 8) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+        w[0] = t.x; w[1] = t.y; w[2] = t.z; w[3] = t.w;
+    } else {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        w[0] = t.x; w[1] = t.y;
+    }
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        l[2 * i] = (w[i] & 0x7FFFu) != 0;
+        l[2 * i + 1] = (w[i] & 0x7FFF0000u) != 0;
+    }
+}
+template <int N>
+__device__ __forceinline__ void stv(float* p, const float (&y)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+}
+template <int N>
+__device__ __forceinline__ void stv(__half* p, const float (&y)[N]) {
+    uint32_t w[N / 2];
+#pragma unroll
+    for (int i = 0; i < N / 2; ++i) {
+        const __half2 h = __floats2half2_rn(y[2 * i], y[2 * i + 1]);
+        w[i] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    if constexpr (N == 8) *reinterpret_cast<uint4*>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+}
+
+__device__ __forceinline__ void online(float& m, float& s, float x) {
+    if (x > m) {
+        s = (m == -FLT_MAX ? 0.f : s * __expf(m - x)) + 1.f;
+        m = x;
+    } else {
+        s += __expf(x - m);
+    }
+}
+
+// Lane l owns row r = l % 8 of block (l / 8) of every group of 4 full blocks
+// -- the K contiguous values of that block row -- so each lane's statistics
+// belong to one row.  A narrow last block (width w < K, only at the end of
+// a window) is taken by lanes 0..7, row = lane, values r*w .. r*w+w-1.
+template <uint32_t K, typename VS, typename VM>
+__device__ __forceinline__ void row_stats(const VS* scores, const VM* mask, uint64_t vb, uint32_t v0, uint32_t v1,
+                                          uint32_t lane, float scale, float& m, float& s) {
+    const uint32_t r = lane & 7, bl = lane >> 3;
+    const uint32_t b0 = v0 / K, nfull = (v1 - v0) / K, w = (v1 - v0) % K;
+    m = -FLT_MAX;
+    s = 0.f;
+    for (uint32_t b = b0 + bl; b < b0 + nfull; b += 4) {
+        const uint64_t p = vb + 8ull * K * b + r * K;
+        float x[K];
+        bool l[K];
+        ldv<K>(scores + p, x);
+        ldlive<K>(mask + p, l);
+#pragma unroll
+        for (uint32_t j = 0; j < K; ++j)
+            if (l[j]) online(m, s, scale * x[j]);
+    }
+    if (w && lane < 8) {
+        const uint64_t p = vb + 8ull * K * (b0 + nfull) + r * w;
+        for (uint32_t j = 0; j < w; ++j)
+            if (live_at<VM>(mask, p + j)) online(m, s, scale * ld_val<VS>(scores, p + j));
+    }
+    // merge the 4 lanes that own row r (lanes r, r+8, r+16, r+24)
+#pragma unroll
+    for (int o = 8; o <= 16; o <<= 1) {
+        const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+        merge(m, s, m2, s2);
+    }
 }
 
 template <uint32_t K, typename VS, typename VM, typename VO>
-__device__ __forceinline__ void write_range(const VS* scores, const VM* mask, VO* out, uint64_t vb, uint32_t nvw,
-                                            uint32_t v0, uint32_t v1, uint32_t lane, float scale, const float (&m)[8],
-                                            const float (&inv)[8]) {
-    for (uint32_t v = v0 + lane; v < v1; v += 32)
+__device__ __forceinline__ void row_write(const VS* scores, const VM* mask, VO* out, uint64_t vb, uint32_t v0,
+                                          uint32_t v1, uint32_t lane, float scale, float m, float inv) {
+    const uint32_t r = lane & 7, bl = lane >> 3;
+    const uint32_t b0 = v0 / K, nfull = (v1 - v0) / K, w = (v1 - v0) % K;
+    for (uint32_t b = b0 + bl; b < b0 + nfull; b += 4) {
+        const uint64_t p = vb + 8ull * K * b + r * K;
+        float x[K], y[K];
+        bool l[K];
+        ldv<K>(scores + p, x);
+        ldlive<K>(mask + p, l);
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const uint64_t p = vpos<K>(vb, nvw, v, r);
-            const float y = live_at<VM>(mask, p) ? __expf(scale * ld_val<VS>(scores, p) - m[r]) * inv[r] : 0.f;
-            st_val<VO>(out, p, y);
-        }
+        for (uint32_t j = 0; j < K; ++j) y[j] = l[j] ? __expf(scale * x[j] - m) * inv : 0.f;
+        stv<K>(out + p, y);
+    }
+    if (w && lane < 8) {
+        const uint64_t p = vb + 8ull * K * (b0 + nfull) + r * w;
+        for (uint32_t j = 0; j < w; ++j)
+            st_val<VO>(out, p + j,
+                       live_at<VM>(mask, p + j) ? __expf(scale * ld_val<VS>(scores, p + j) - m) * inv : 0.f);
+    }
 }
 
 template <uint32_t K, typename VS, typename VM, typename VO>
@@ -91,52 +212,14 @@ __global__ void __launch_bounds__(256) softmax_items(const WorkItem* __restrict_
         idx = __shfl_sync(0xffffffffu, idx, 0);
         if (idx >= n_items) break;
         const WorkItem it = items[idx];
-        const uint32_t base = __ldg(rp + it.window), nvw = __ldg(rp + it.window + 1) - base;
-        const uint64_t vb = 8ull * base;
-        float m[8], s[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            m[r] = -FLT_MAX;
-            s[r] = 0.f;
-        }
-        for (uint32_t v = it.vbeg + lane; v < it.vend; v += 32)
-#pragma unroll
-            for (int r = 0; r < 8; ++r) {
-                const uint64_t p = vpos<K>(vb, nvw, v, r);
-                if (live_at<VM>(mask, p)) {
-                    const float x = scale * ld_val<VS>(scores, p);
-                    if (x > m[r]) {
-                        s[r] = (m[r] == -FLT_MAX ? 0.f : s[r] * __expf(m[r] - x)) + 1.f;
-                        m[r] = x;
-                    } else {
-                        s[r] += __expf(x - m[r]);
-                    }
-                }
-            }
-#pragma unroll
-        for (int r = 0; r < 8; ++r)
-#pragma unroll
-            for (int o = 16; o; o >>= 1) {
-                const float m2 = __shfl_xor_sync(0xffffffffu, m[r], o), s2 = __shfl_xor_sync(0xffffffffu, s[r], o);
-                merge(m[r], s[r], m2, s2);
-            }
+        const uint64_t vb = 8ull * __ldg(rp + it.window);
+        float m, s;
+        row_stats<K, VS, VM>(scores, mask, vb, it.vbeg, it.vend, lane, scale, m, s);
         if (it.slot != kNoSlot) {  // segment of a split window: publish partials
-            if (lane < 8) {
-                float mv = m[0], sv = s[0];
-#pragma unroll
-                for (int r = 1; r < 8; ++r)
-                    if (lane == (uint32_t)r) {
-                        mv = m[r];
-                        sv = s[r];
-                    }
-                part[8ull * it.slot + lane] = RowStat{mv, sv};
-            }
+            if (lane < 8) part[8ull * it.slot + lane] = RowStat{m, s};
             continue;
         }
-        float inv[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) inv[r] = s[r] > 0.f ? 1.f / s[r] : 0.f;
-        write_range<K, VS, VM, VO>(scores, mask, out, vb, nvw, it.vbeg, it.vend, lane, scale, m, inv);
+        row_write<K, VS, VM, VO>(scores, mask, out, vb, it.vbeg, it.vend, lane, scale, m, s > 0.f ? 1.f / s : 0.f);
     }
 }
 
@@ -176,15 +259,9 @@ __global__ void __launch_bounds__(256) softmax_finish(const WorkItem* __restrict
             else hi = mid;
         }
         const uint32_t fs = split[lo].first_slot;
-        float m[8], inv[8];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-            const RowStat x = part[8ull * fs + r];
-            m[r] = x.m;
-            inv[r] = x.s > 0.f ? 1.f / x.s : 0.f;
-        }
-        const uint32_t base = __ldg(rp + it.window), nvw = __ldg(rp + it.window + 1) - base;
-        write_range<K, VS, VM, VO>(scores, mask, out, 8ull * base, nvw, it.vbeg, it.vend, lane, scale, m, inv);
+        const RowStat x = part[8ull * fs + (lane & 7)];
+        const uint64_t vb = 8ull * __ldg(rp + it.window);
+        row_write<K, VS, VM, VO>(scores, mask, out, vb, it.vbeg, it.vend, lane, scale, x.m, x.s > 0.f ? 1.f / x.s : 0.f);
     }
 }
 
