@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtcsparse_b200.so")
+# TCS_LIB_PATH: load an experimental build instead (tools/build_variant.sh)
+LIB_PATH = os.environ.get("TCS_LIB_PATH") or os.path.join(_HERE, "libtcsparse_b200.so")
 
 TCS_OK, TCS_ERR_ARGUMENT, TCS_ERR_SHAPE, TCS_ERR_FORMAT, TCS_ERR_CUDA, TCS_ERR_NCCL, TCS_ERR_OOM = range(7)
 TCS_FP16, TCS_TF32 = 0, 1

@@ -47,6 +47,10 @@ struct SddmmArgs {
 
 constexpr int kWarps = 4;
 constexpr int kRing = 4;  // column-index batches staged per warp
+// Resident CTAs per SM (sets the register budget): 4 (128 registers) for
+// single-pass inner dimensions, 3 when two super-chunks are double-buffered.
+template <int NSC>
+constexpr int kMinBlocks = NSC == 1 ? 4 : 3;
 
 // Storage position of accumulator element q (vector g or g+8, row 2t or
 // 2t+1) of the group at s.  K (storage block width) is a compile-time
@@ -68,20 +72,27 @@ __device__ __forceinline__ uint64_t acc_pos(uint64_t vbase, uint32_t nvw, uint32
 // Liveness bits of the mask values at the group's 4 accumulator positions
 // (nonzero magnitude == the reference's `mask.values[pos] != 0`; -0.0 is not
 // live, ref sddmm.hpp:131).  Issued one group ahead of use.
+// Mask words per group and lane: 4 f32 or 4 packed f16 values.
+template <bool MF32>
+constexpr int kMaskWords = MF32 ? 4 : 2;
+
 template <uint32_t K, bool MF32>
 __device__ __forceinline__ void mask_prefetch(const SddmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend,
-                                              uint32_t s, uint32_t g, uint32_t t, uint32_t (&mk)[4]) {
+                                              uint32_t s, uint32_t g, uint32_t t,
+                                              uint32_t (&mk)[kMaskWords<MF32>]) {
     const bool full = s + 16 <= vend;
+#pragma unroll
+    for (int w = 0; w < kMaskWords<MF32>; ++w) mk[w] = 0u;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
-        mk[q] = 0u;
         if (v < vend) {
             const uint64_t pos = acc_pos<K>(vbase, nvw, s, full, g, t, q);
             // raw bits only: the liveness test happens at store time, so the
             // load stays in flight until then
             if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos));
-            else mk[q] = static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos));
+            else mk[q >> 1] |= static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos))
+                               << (16 * (q & 1));
         }
     }
 }
@@ -94,7 +105,8 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
 
 // Writes the 16x8 accumulator tile of the vector group starting at s.
 template <uint32_t K, bool MF32, bool OF32>
-__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4], const uint32_t (&mk)[4],
+__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4],
+                                            const uint32_t (&mk)[kMaskWords<MF32>],
                                             uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g,
                                             uint32_t t) {
     const bool full = s + 16 <= vend;
@@ -102,9 +114,46 @@ __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&ac
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
         if (v >= vend) continue;
-        const bool live = (mk[q] & (MF32 ? 0x7FFFFFFFu : 0x7FFFu)) != 0u;
+        const bool live = MF32 ? (mk[q] & 0x7FFFFFFFu) != 0u : ((mk[q >> 1] >> (16 * (q & 1))) & 0x7FFFu) != 0u;
         out_store<OF32>(a.out, acc_pos<K>(vbase, nvw, s, full, g, t, q), live ? acc[q] : 0.f);
     }
+}
+
+// ---- full groups (all 16 vectors inside full-width blocks): the group's
+// 128 output/mask slots are contiguous; accumulator element q of lane (g,t)
+// sits at slot full_pos(g,t,q) of them.
+template <uint32_t K>
+__device__ __forceinline__ uint32_t full_pos(uint32_t g, uint32_t t, int q) {
+    if constexpr (K == 8) return 64u * (q >> 1) + 16u * t + 8u * (q & 1) + g;
+    else return 32u * (g >> 2) + 64u * (q >> 1) + 8u * t + 4u * (q & 1) + (g & 3);
+}
+
+// Liveness bits (bit q) of lane (g,t)'s accumulator elements, read from the
+// group's 128 mask values staged in shared memory.
+template <uint32_t K, bool MF32>
+__device__ __forceinline__ uint32_t ring_live(const unsigned char* m, uint32_t g, uint32_t t) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t p = full_pos<K>(g, t, q);
+        const bool live = MF32 ? (reinterpret_cast<const uint32_t*>(m)[p] & 0x7FFFFFFFu) != 0u
+                               : (reinterpret_cast<const unsigned short*>(m)[p] & 0x7FFFu) != 0u;
+        bits |= static_cast<uint32_t>(live) << q;
+    }
+    return bits;
+}
+
+template <uint32_t K, bool OF32>
+__device__ __forceinline__ void full_store(void* out, uint64_t slot0, const float (&acc)[4], uint32_t live,
+                                           uint32_t g, uint32_t t) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) out_store<OF32>(out, slot0 + full_pos<K>(g, t, q), (live >> q) & 1u ? acc[q] : 0.f);
+}
+
+// Bytes of one ring slot: BV column indices + BV*8 mask values.
+template <int NSC, bool MF32>
+constexpr uint32_t ring_slot_bytes() {
+    return 16u * (NSC == 1 ? 4u : 2u) * (4u + 8u * (MF32 ? 4u : 2u));
 }
 
 // ---------------------------------------------------------------- FP16
@@ -183,12 +232,12 @@ __device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, const uint
 
 // One kernel body for both precisions; Tile/loader/mma chosen by TF32.
 template <bool TF32, int NSC, bool MF32, bool OF32>
-__global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
     using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t g = lane >> 2, t = lane & 3;
-    __shared__ uint32_t colring_all[kWarps * kRing * 64];  // per-warp column-index ring
+    extern __shared__ __align__(16) unsigned char ring_all[];  // per-warp ring, see below
     // persistent warps pulling work items (cf. spmm.cu next_item)
     for (;;) {
     uint32_t idx = 0;
@@ -222,7 +271,8 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
         c[1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
     };
     // one group: prefetched pass 0 + (rare) extra passes loaded in place
-    auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0, const uint32_t (&mk)[4]) {
+    constexpr int MW = kMaskWords<MF32>;
+    auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0, const uint32_t (&mk)[MW]) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         mma(x0, ar0, acc);
         if constexpr (NSC > 1) {  // NSC == 1 <=> the inner dimension fits one pass
@@ -237,52 +287,96 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
         sddmm_store<TF32 ? 4u : 8u, MF32, OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
     };
 
-    // Double-buffered batches of D groups (16*D vectors): the gathers and
-    // mask bits of batch i+1 are in flight while batch i is consumed.  The
-    // column indices feeding the gathers are staged through a per-warp
-    // shared-memory ring by cp.async, RING-1 batches ahead, so no gather
-    // waits on a dependent global load.
+    // Double-buffered batches of D groups (16*D vectors): the gathers of
+    // batch i+1 are in flight while batch i is consumed.  A per-warp
+    // shared-memory ring, filled by cp.async RING-1 batches ahead, stages
+    // each batch's column indices (so no gather waits on a dependent global
+    // load) and, for a full batch, its 128*D contiguous mask values (the
+    // DRAM-streamed operand gets the deepest prefetch).  A batch whose
+    // vectors all lie in full-width blocks takes the predicate-free path
+    // (liveness bits read from the ring, fixed store offsets); only the last
+    // batch of a window takes the general one.
     constexpr int D = NSC == 1 ? 4 : 2;
     constexpr uint32_t BV = 16 * D;
-    uint32_t (*ring)[BV] = reinterpret_cast<uint32_t (*)[BV]>(colring_all + warp * kRing * 64);
+    constexpr uint32_t MSZ = MF32 ? 4 : 2;
+    constexpr uint32_t SLOT = ring_slot_bytes<NSC, MF32>();
+    unsigned char* wring = ring_all + warp * kRing * SLOT;
+    auto ring_cols = [&](uint32_t slot) { return reinterpret_cast<uint32_t*>(wring + slot * SLOT); };
+    auto ring_mask = [&](uint32_t slot) { return wring + slot * SLOT + BV * 4; };
     auto prefetch_cols = [&](uint32_t sb, uint32_t slot) {
         __syncwarp();  // every lane is done reading this slot
+        uint32_t* rc = ring_cols(slot);
 #pragma unroll
         for (uint32_t i = lane; i < BV; i += 32) {
             const uint32_t v = min(sb + i, vend - 1);  // clamp: stays inside the item's columns
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                             static_cast<uint32_t>(__cvta_generic_to_shared(&ring[slot][i]))),
+                             static_cast<uint32_t>(__cvta_generic_to_shared(rc + i))),
                          "l"(ci + v)
                          : "memory");
         }
+        if (sb + BV <= vend) {
+            const unsigned char* src = static_cast<const unsigned char*>(a.mask) + (vbase + 8ull * sb) * MSZ;
+            unsigned char* dst = ring_mask(slot);
+#pragma unroll
+            for (uint32_t c = lane; c < BV * 8 * MSZ / 16; c += 32)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 static_cast<uint32_t>(__cvta_generic_to_shared(dst + 16 * c))),
+                             "l"(src + 16 * c)
+                             : "memory");
+        }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto issue = [&](uint32_t sb, uint32_t slot, Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
+    auto issue = [&](uint32_t sb, uint32_t slot, Tile (&x)[D], uint32_t (&mk)[D][MW], uint32_t (&cg)[D][2]) {
+        const bool fullb = sb + BV <= vend;
+        const uint32_t* rc = ring_cols(slot);
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             const uint32_t s = sb + 16 * d;
-            cg[d][0] = ring[slot][16 * d + g];
-            cg[d][1] = ring[slot][16 * d + g + 8];
-            if (s < vend) {
+            cg[d][0] = rc[16 * d + g];
+            cg[d][1] = rc[16 * d + g + 8];
+            if (fullb) {
+                if constexpr (TF32) tf32_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
+                else f16_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
+                mk[d][0] = ring_live<TF32 ? 4u : 8u, MF32>(ring_mask(slot) + 128u * d * MSZ, g, t);
+            } else if (s < vend) {
                 load(s, cg[d], 0, x[d]);
                 mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
             }
         }
     };
-    auto consume = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&mk)[D][4], const uint32_t (&cg)[D][2]) {
+    auto consume = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&mk)[D][MW], const uint32_t (&cg)[D][2]) {
+        if (sb + BV <= vend) {
 #pragma unroll
-        for (int d = 0; d < D; ++d)
-            if (sb + 16 * d < vend) group(sb + 16 * d, cg[d], x[d], mk[d]);
+            for (int d = 0; d < D; ++d) {
+                const uint32_t s = sb + 16 * d;
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                mma(x[d], ar0, acc);
+                if constexpr (NSC > 1) {
+                    for (int p = 1; p < a.passes; ++p) {
+                        Tile xp;
+                        uint4 arp[NSC];
+                        load(s, cg[d], p, xp);
+                        arow_load<NSC>(arow, arow_ok, p, t, arp);
+                        mma(xp, arp, acc);
+                    }
+                }
+                full_store<TF32 ? 4u : 8u, OF32>(a.out, vbase + 8ull * s, acc, mk[d][0], g, t);
+            }
+        } else {
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                if (sb + 16 * d < vend) group(sb + 16 * d, cg[d], x[d], mk[d]);
+        }
     };
 
     Tile ta[D], tb[D];
-    uint32_t ma[D][4], mb[D][4], ga[D][2], gb[D][2];
+    uint32_t ma[D][MW], mb[D][MW], ga[D][2], gb[D][2];
     uint32_t s = it.vbeg;
     if (s < vend) {
         const uint32_t s0 = s;
         uint32_t pb = 0, ib = 0;  // next batch to prefetch / to issue
         for (int r = 0; r < kRing - 1; ++r, ++pb) prefetch_cols(s0 + pb * BV, pb % kRing);
-        auto next_issue = [&](Tile (&x)[D], uint32_t (&mk)[D][4], uint32_t (&cg)[D][2]) {
+        auto next_issue = [&](Tile (&x)[D], uint32_t (&mk)[D][MW], uint32_t (&cg)[D][2]) {
             prefetch_cols(s0 + pb * BV, pb % kRing);
             ++pb;
             asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
@@ -309,11 +403,13 @@ __global__ void __launch_bounds__(kWarps * 32, 3) sddmm_kernel(const SddmmArgs a
 template <bool TF32, int NSC>
 void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>(std::min<uint64_t>((a.n_items + kWarps - 1) / kWarps,
-                                                             uint64_t(num_sms()) * 3)));
-    if (mf32 && of32) sddmm_kernel<TF32, NSC, true, true><<<grid, kWarps * 32, 0, s>>>(a);
-    else if (mf32) sddmm_kernel<TF32, NSC, true, false><<<grid, kWarps * 32, 0, s>>>(a);
-    else if (of32) sddmm_kernel<TF32, NSC, false, true><<<grid, kWarps * 32, 0, s>>>(a);
-    else sddmm_kernel<TF32, NSC, false, false><<<grid, kWarps * 32, 0, s>>>(a);
+                                                             uint64_t(num_sms()) * kMinBlocks<NSC>)));
+    const size_t sm32 = kWarps * kRing * ring_slot_bytes<NSC, true>();
+    const size_t sm16 = kWarps * kRing * ring_slot_bytes<NSC, false>();
+    if (mf32 && of32) sddmm_kernel<TF32, NSC, true, true><<<grid, kWarps * 32, sm32, s>>>(a);
+    else if (mf32) sddmm_kernel<TF32, NSC, true, false><<<grid, kWarps * 32, sm32, s>>>(a);
+    else if (of32) sddmm_kernel<TF32, NSC, false, true><<<grid, kWarps * 32, sm16, s>>>(a);
+    else sddmm_kernel<TF32, NSC, false, false><<<grid, kWarps * 32, sm16, s>>>(a);
     TCS_LAUNCHED(TF32 ? "sddmm_tf32" : "sddmm_f16");
 }
 

@@ -185,6 +185,13 @@ __device__ __forceinline__ uint2 ld_stream_u64(const void* p) {
     asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
 }
+__device__ __forceinline__ uint4 ld_stream_u128(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
 // Dense-row gathers: read-only path, L1-allocating (hub rows are reused).
 __device__ __forceinline__ uint4 ld_gather_128(const void* p) {
     uint4 v;
