@@ -195,6 +195,19 @@ tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, i
 tcs_status tcs_mebcrs_row_softmax(const tcs_mebcrs* scores, const tcs_mebcrs* mask, float scale, tcs_mebcrs* out,
                                   tcs_dtype out_dtype, tcs_stream_t stream);
 
+/* Fused AGNN attention front half (no reference
+ * counterpart): out = row_softmax(S, mask, scale) with S = tcs_sddmm(mask,
+ * A, Bt) stored as score_dtype -- the result of tcs_sddmm followed by
+ * tcs_mebcrs_row_softmax up to the order of the per-row exp sums.  The
+ * SDDMM kernel publishes per-row softmax partials, so the scores are
+ * normalised in one streaming pass with no mask re-read.  Arguments and
+ * errors as tcs_sddmm; score_dtype as its out_dtype.  `out` as in
+ * tcs_mebcrs_row_softmax. */
+tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda,
+                                 int64_t a_rows, int64_t f_a, const void* bt, tcs_dtype bt_dtype, int64_t ldbt,
+                                 int64_t bt_rows, int64_t f_b, float scale, tcs_dtype score_dtype, tcs_mebcrs* out,
+                                 tcs_dtype out_dtype, const tcs_kernel_config* cfg, tcs_stream_t stream);
+
 /* ------------------------------------------------- host-buffer entry points */
 /* Value semantics of the reference API: host arrays in, host arrays out.  */
 

@@ -43,6 +43,7 @@ struct SddmmArgs {
     int passes;         // feature passes of NSC super-chunks
     uint32_t k;         // storage block width (8 / 4)
     uint32_t* counter;  // work-item counter (zeroed before launch)
+    float dead;         // value of stored slots whose mask value is 0: 0, or -inf for the fused softmax
 };
 
 constexpr int kWarps = 4;
@@ -103,10 +104,26 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
     else static_cast<__half*>(out)[pos] = __float2half_rn(v);
 }
 
-// Writes the 16x8 accumulator tile of the vector group starting at s.
-template <uint32_t K, bool MF32, bool OF32>
-__device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&acc)[4],
-                                            const uint32_t (&mk)[kMaskWords<MF32>],
+// Liveness bits (bit q) of lane (g,t)'s accumulator elements in a general
+// group; elements past the item's last vector are not live.
+template <bool MF32>
+__device__ __forceinline__ uint32_t slow_live(const uint32_t (&mk)[kMaskWords<MF32>], uint32_t s, uint32_t vend,
+                                              uint32_t g) {
+    uint32_t bits = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+        const bool live = v < vend && (MF32 ? (mk[q] & 0x7FFFFFFFu) != 0u
+                                            : ((mk[q >> 1] >> (16 * (q & 1))) & 0x7FFFu) != 0u);
+        bits |= static_cast<uint32_t>(live) << q;
+    }
+    return bits;
+}
+
+// Writes the 16x8 accumulator tile of the general group starting at s:
+// live elements get their value, the other stored slots `dead`.
+template <uint32_t K, bool OF32>
+__device__ __forceinline__ void sddmm_store(void* out, const float (&acc)[4], uint32_t live, float dead,
                                             uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g,
                                             uint32_t t) {
     const bool full = s + 16 <= vend;
@@ -114,8 +131,7 @@ __device__ __forceinline__ void sddmm_store(const SddmmArgs& a, const float (&ac
     for (int q = 0; q < 4; ++q) {
         const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
         if (v >= vend) continue;
-        const bool live = MF32 ? (mk[q] & 0x7FFFFFFFu) != 0u : ((mk[q >> 1] >> (16 * (q & 1))) & 0x7FFFu) != 0u;
-        out_store<OF32>(a.out, acc_pos<K>(vbase, nvw, s, full, g, t, q), live ? acc[q] : 0.f);
+        out_store<OF32>(out, acc_pos<K>(vbase, nvw, s, full, g, t, q), (live >> q) & 1u ? acc[q] : dead);
     }
 }
 
@@ -145,9 +161,10 @@ __device__ __forceinline__ uint32_t ring_live(const unsigned char* m, uint32_t g
 
 template <uint32_t K, bool OF32>
 __device__ __forceinline__ void full_store(void* out, uint64_t slot0, const float (&acc)[4], uint32_t live,
-                                           uint32_t g, uint32_t t) {
+                                           float dead, uint32_t g, uint32_t t) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) out_store<OF32>(out, slot0 + full_pos<K>(g, t, q), (live >> q) & 1u ? acc[q] : 0.f);
+    for (int q = 0; q < 4; ++q)
+        out_store<OF32>(out, slot0 + full_pos<K>(g, t, q), (live >> q) & 1u ? acc[q] : dead);
 }
 
 // Bytes of one ring slot: BV column indices + BV*8 mask values.
@@ -284,7 +301,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
                 mma(x, arp, acc);
             }
         }
-        sddmm_store<TF32 ? 4u : 8u, MF32, OF32>(a, acc, mk, vbase, nvw, vend, s, g, t);
+        const uint32_t live = slow_live<MF32>(mk, s, vend, g);
+        sddmm_store<TF32 ? 4u : 8u, OF32>(a.out, acc, live, a.dead, vbase, nvw, vend, s, g, t);
     };
 
     // Double-buffered batches of D groups (16*D vectors): the gathers of
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
         __syncwarp();  // every lane is done reading this slot
         uint32_t* rc = ring_cols(slot);
 #pragma unroll
-        for (uint32_t i = lane; i < BV; i += 32) {
+        for (uint32_t i = lane; i < BV && sb < vend; i += 32) {
             const uint32_t v = min(sb + i, vend - 1);  // clamp: stays inside the item's columns
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
                              static_cast<uint32_t>(__cvta_generic_to_shared(rc + i))),
@@ -326,73 +344,87 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto issue = [&](uint32_t sb, uint32_t slot, Tile (&x)[D], uint32_t (&mk)[D][MW], uint32_t (&cg)[D][2]) {
-        const bool fullb = sb + BV <= vend;
+    // Full batches: predicate-free loads, liveness from the ring.
+    auto issue_full = [&](uint32_t sb, uint32_t slot, Tile (&x)[D], uint32_t (&live)[D], uint32_t (&cg)[D][2]) {
         const uint32_t* rc = ring_cols(slot);
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            const uint32_t s = sb + 16 * d;
             cg[d][0] = rc[16 * d + g];
             cg[d][1] = rc[16 * d + g + 8];
-            if (fullb) {
-                if constexpr (TF32) tf32_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
-                else f16_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
-                mk[d][0] = ring_live<TF32 ? 4u : 8u, MF32>(ring_mask(slot) + 128u * d * MSZ, g, t);
-            } else if (s < vend) {
-                load(s, cg[d], 0, x[d]);
-                mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
-            }
+            if constexpr (TF32) tf32_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
+            else f16_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
+            live[d] = ring_live<TF32 ? 4u : 8u, MF32>(ring_mask(slot) + 128u * d * MSZ, g, t);
         }
     };
-    auto consume = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&mk)[D][MW], const uint32_t (&cg)[D][2]) {
-        if (sb + BV <= vend) {
+    auto consume_full = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&live)[D], const uint32_t (&cg)[D][2]) {
 #pragma unroll
-            for (int d = 0; d < D; ++d) {
-                const uint32_t s = sb + 16 * d;
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                mma(x[d], ar0, acc);
-                if constexpr (NSC > 1) {
-                    for (int p = 1; p < a.passes; ++p) {
-                        Tile xp;
-                        uint4 arp[NSC];
-                        load(s, cg[d], p, xp);
-                        arow_load<NSC>(arow, arow_ok, p, t, arp);
-                        mma(xp, arp, acc);
-                    }
+        for (int d = 0; d < D; ++d) {
+            const uint32_t s = sb + 16 * d;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            mma(x[d], ar0, acc);
+            if constexpr (NSC > 1) {
+                for (int p = 1; p < a.passes; ++p) {
+                    Tile xp;
+                    uint4 arp[NSC];
+                    load(s, cg[d], p, xp);
+                    arow_load<NSC>(arow, arow_ok, p, t, arp);
+                    mma(xp, arp, acc);
                 }
-                full_store<TF32 ? 4u : 8u, OF32>(a.out, vbase + 8ull * s, acc, mk[d][0], g, t);
             }
-        } else {
-#pragma unroll
-            for (int d = 0; d < D; ++d)
-                if (sb + 16 * d < vend) group(sb + 16 * d, cg[d], x[d], mk[d]);
+            full_store<TF32 ? 4u : 8u, OF32>(a.out, vbase + 8ull * s, acc, live[d], a.dead, g, t);
         }
     };
 
-    Tile ta[D], tb[D];
-    uint32_t ma[D][MW], mb[D][MW], ga[D][2], gb[D][2];
-    uint32_t s = it.vbeg;
-    if (s < vend) {
-        const uint32_t s0 = s;
-        uint32_t pb = 0, ib = 0;  // next batch to prefetch / to issue
+    const uint32_t s0 = it.vbeg;
+    if (s0 < vend) {
+        const uint32_t nf = (vend - s0) / BV;  // full batches; at most one partial batch follows
+        uint32_t pb = 0;                       // next batch to prefetch
         for (int r = 0; r < kRing - 1; ++r, ++pb) prefetch_cols(s0 + pb * BV, pb % kRing);
-        auto next_issue = [&](Tile (&x)[D], uint32_t (&mk)[D][MW], uint32_t (&cg)[D][2]) {
+        auto ring_next = [&]() {  // prefetch one more batch, wait for batch ib
             prefetch_cols(s0 + pb * BV, pb % kRing);
             ++pb;
             asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 1) : "memory");
             __syncwarp();
-            issue(s0 + ib * BV, ib % kRing, x, mk, cg);
-            ++ib;
         };
-        next_issue(ta, ma, ga);
-        for (;;) {
-            if (s + BV < vend) next_issue(tb, mb, gb);
-            consume(s, ta, ma, ga);
-            if (s + BV >= vend) break;
-            if (s + 2 * BV < vend) next_issue(ta, ma, ga);
-            consume(s + BV, tb, mb, gb);
-            s += 2 * BV;
-            if (s >= vend) break;
+        if (nf) {  // double-buffered full batches: batch i+1 in flight while i is consumed
+            Tile ta[D], tb[D];
+            uint32_t la[D], lb[D], ga[D][2], gb[D][2];
+            ring_next();
+            issue_full(s0, 0, ta, la, ga);
+            for (uint32_t i = 0;;) {
+                if (i + 1 < nf) {
+                    ring_next();
+                    issue_full(s0 + (i + 1) * BV, (i + 1) % kRing, tb, lb, gb);
+                }
+                consume_full(s0 + i * BV, ta, la, ga);
+                if (++i >= nf) break;
+                if (i + 1 < nf) {
+                    ring_next();
+                    issue_full(s0 + (i + 1) * BV, (i + 1) % kRing, ta, la, ga);
+                }
+                consume_full(s0 + i * BV, tb, lb, gb);
+                if (++i >= nf) break;
+            }
+        }
+        if (s0 + nf * BV < vend) {  // the window's last, partial batch: general path
+            ring_next();
+            const uint32_t sb = s0 + nf * BV;
+            const uint32_t* rc = ring_cols(nf % kRing);
+            Tile x[D];
+            uint32_t mk[D][MW], cg[D][2];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const uint32_t s = sb + 16 * d;
+                cg[d][0] = rc[16 * d + g];
+                cg[d][1] = rc[16 * d + g + 8];
+                if (s < vend) {
+                    load(s, cg[d], 0, x[d]);
+                    mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+                if (sb + 16 * d < vend) group(sb + 16 * d, cg[d], x[d], mk[d]);
         }
         asm volatile("cp.async.wait_group 0;" ::: "memory");  // no ring write outlives the item
         __syncwarp();
@@ -414,6 +446,85 @@ void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
 }
 
 }  // namespace
+
+// Validation shared by tcs_sddmm and tcs_sddmm_row_softmax (ref sddmm.hpp:86-90).
+void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda, int64_t a_rows, int64_t f_a,
+                 const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t f_b, tcs_dtype out_dtype,
+                 const tcs_kernel_config* cfg) {
+    if (!cfg) fail(TCS_ERR_ARGUMENT, "null argument");
+    check_mebcrs(mask);
+    if (cfg->precision != mask->precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded mask");
+    if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "SDDMM requires vector height 8");
+    if (a_rows != static_cast<int64_t>(mask->rows)) fail(TCS_ERR_SHAPE, "A rows must equal mask rows");
+    if (bt_rows != static_cast<int64_t>(mask->cols)) fail(TCS_ERR_SHAPE, "B cols must equal mask cols");
+    if (f_a != f_b) fail(TCS_ERR_SHAPE, "inner dimensions of A and B must agree");
+    if (f_a < 0) fail(TCS_ERR_SHAPE, "negative inner dimension");
+    if (out_dtype != TCS_DTYPE_F16 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown output dtype");
+    if ((a_rows && f_a && (!a || lda < f_a)) || (bt_rows && f_b && (!bt || ldbt < f_b)))
+        fail(TCS_ERR_ARGUMENT, "bad dense operand / leading dimension");
+    const bool tf32 = mask->precision == TCS_TF32;
+    if (tf32 && (a_dtype != TCS_DTYPE_F32 || bt_dtype != TCS_DTYPE_F32))
+        fail(TCS_ERR_ARGUMENT, "TF32 SDDMM needs f32 dense operands");
+    if (tf32 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
+}
+
+// Runs the SDDMM of `mask` into out_values (8*nv values of out_dtype).
+// `dead`: the value of stored slots whose mask value is 0 (0 for tcs_sddmm,
+// -inf for the fused softmax, which then needs no mask re-read).
+void sddmm_launch(const tcs_mebcrs* mask, const Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
+                  int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
+                  void* out_values, tcs_dtype out_dtype, float dead, cudaStream_t s) {
+    const uint64_t nv = mask->num_vectors;
+    const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4;
+    if (!nv) return;
+    if (F == 0 && dead == 0.f) {
+        TCS_CUDA(cudaMemsetAsync(out_values, 0, 8 * nv * ow, s));
+        return;
+    }
+    const bool tf32 = mask->precision == TCS_TF32;
+    // feature padding: super-chunk = 32 (FP16) / 16 (TF32) features
+    const int64_t sc = tf32 ? 16 : 32;
+    int64_t fpad = std::max<int64_t>(1, (F + sc - 1) / sc) * sc;
+    // NSC super-chunks per pass (double-buffered in registers); wider inner
+    // dimensions take several passes.
+    int nsc = 1;
+    if (fpad > sc) {
+        nsc = 2;
+        fpad = (F + 2 * sc - 1) / (2 * sc) * (2 * sc);
+    }
+    const tcs_dtype need = tf32 ? TCS_DTYPE_F32 : TCS_DTYPE_F16;
+    const int64_t al = tf32 ? 4 : 8;
+    auto prep = [&](const void* src, tcs_dtype dt, int64_t ld, int64_t nrows, DBuf& buf,
+                    int64_t& out_ld) -> const void* {
+        if (F > 0 && dt == need && ld >= fpad && ld % al == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+            out_ld = ld;
+            return src;
+        }
+        out_ld = fpad;
+        buf = DBuf(std::max<int64_t>(1, nrows) * fpad * (tf32 ? 4 : 2), s);
+        pad_convert(src, dt, ld, buf.p, need, fpad, nrows, F, fpad, s);
+        return buf.p;
+    };
+    DBuf abuf, bbuf;
+    int64_t alda = 0, bldb = 0;
+    const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
+    const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
+    DBuf item_ctr(sizeof(uint32_t), s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, sizeof(uint32_t), s));
+    SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
+                   ap, alda, bp, bldb, out_values, mask->rows,
+                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead};
+    const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
+    if (!plan->n_items) return;
+    if (tf32) {
+        if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
+        else launch_sddmm<true, 2>(args, mf32, of32, s);
+    } else {
+        if (nsc == 1) launch_sddmm<false, 1>(args, mf32, of32, s);
+        else launch_sddmm<false, 2>(args, mf32, of32, s);
+    }
+}
+
 }  // namespace tcs
 
 using namespace tcs;
@@ -423,31 +534,15 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
                                 int64_t bt_rows, int64_t f_b, tcs_mebcrs* out, tcs_dtype out_dtype,
                                 const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
-        if (!cfg || !out) fail(TCS_ERR_ARGUMENT, "null argument");
-        check_mebcrs(mask);
-        // ref sddmm.hpp:86-90
-        if (cfg->precision != mask->precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded mask");
-        if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "SDDMM requires vector height 8");
-        if (a_rows != static_cast<int64_t>(mask->rows)) fail(TCS_ERR_SHAPE, "A rows must equal mask rows");
-        if (bt_rows != static_cast<int64_t>(mask->cols)) fail(TCS_ERR_SHAPE, "B cols must equal mask cols");
-        if (f_a != f_b) fail(TCS_ERR_SHAPE, "inner dimensions of A and B must agree");
-        if (f_a < 0) fail(TCS_ERR_SHAPE, "negative inner dimension");
-        if (out_dtype != TCS_DTYPE_F16 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown output dtype");
-        if ((a_rows && f_a && (!a || lda < f_a)) || (bt_rows && f_b && (!bt || ldbt < f_b)))
-            fail(TCS_ERR_ARGUMENT, "bad dense operand / leading dimension");
+        if (!out) fail(TCS_ERR_ARGUMENT, "null argument");
+        sddmm_check(mask, a, a_dtype, lda, a_rows, f_a, bt, bt_dtype, ldbt, bt_rows, f_b, out_dtype, cfg);
         cudaStream_t s = st(stream);
-        const int64_t F = f_a;
-        const bool tf32 = mask->precision == TCS_TF32;
-        if (tf32 && (a_dtype != TCS_DTYPE_F32 || bt_dtype != TCS_DTYPE_F32))
-            fail(TCS_ERR_ARGUMENT, "TF32 SDDMM needs f32 dense operands");
-
         // output: the mask's structure, fresh values
         const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4;
         void* caller_values = out->values;
         tcs_mebcrs o = *mask;
         o.flags = o.plan ? TCS_MEBCRS_BORROWED_PLAN : 0u;  // structure and work list shared
         o.value_dtype = out_dtype;
-        if (tf32 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
         if (caller_values) {
             o.values = caller_values;
         } else {
@@ -455,65 +550,20 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
             o.flags |= TCS_MEBCRS_OWN_VALUES;
         }
         if (counters) *counters = tcs_counters{};
-        const uint64_t nv = mask->num_vectors;
-        if (nv) {
-            if (F == 0) {
-                TCS_CUDA(cudaMemsetAsync(o.values, 0, 8 * nv * ow, s));
-            } else {
-                Plan* plan = static_cast<Plan*>(mask->plan);
-                Plan* tmp_plan = nullptr;
-                if (!plan) plan = tmp_plan = build_plan(mask, s, nullptr, nullptr, nullptr);
-                struct PlanGuard {
-                    Plan* p;
-                    cudaStream_t s;
-                    ~PlanGuard() { free_plan(p, s); }
-                } pg{tmp_plan, s};
-                // feature padding: super-chunk = 32 (FP16) / 16 (TF32) features
-                const int64_t sc = tf32 ? 16 : 32;
-                int64_t fpad = (F + sc - 1) / sc * sc;
-                // NSC super-chunks per pass (double-buffered in registers);
-                // wider inner dimensions take several passes.
-                int nsc = 1;
-                if (fpad > sc) {
-                    nsc = 2;
-                    fpad = (F + 2 * sc - 1) / (2 * sc) * (2 * sc);
-                }
-                const tcs_dtype need = tf32 ? TCS_DTYPE_F32 : TCS_DTYPE_F16;
-                const int64_t al = tf32 ? 4 : 8;
-                auto prep = [&](const void* src, tcs_dtype dt, int64_t ld, int64_t nrows, DBuf& buf,
-                                int64_t& out_ld) -> const void* {
-                    if (dt == need && ld >= fpad && ld % al == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
-                        out_ld = ld;
-                        return src;
-                    }
-                    out_ld = fpad;
-                    buf = DBuf(std::max<int64_t>(1, nrows) * fpad * (tf32 ? 4 : 2), s);
-                    pad_convert(src, dt, ld, buf.p, need, fpad, nrows, F, fpad, s);
-                    return buf.p;
-                };
-                DBuf abuf, bbuf;
-                int64_t alda = 0, bldb = 0;
-                const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
-                const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
-                DBuf item_ctr(sizeof(uint32_t), s);
-                TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, sizeof(uint32_t), s));
-                SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
-                               ap, alda, bp, bldb, o.values, mask->rows,
-                               static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>()};
-                const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
-                if (plan->n_items) {
-                    if (tf32) {
-                        if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
-                        else launch_sddmm<true, 2>(args, mf32, of32, s);
-                    } else {
-                        if (nsc == 1) launch_sddmm<false, 1>(args, mf32, of32, s);
-                        else launch_sddmm<false, 2>(args, mf32, of32, s);
-                    }
-                }
-            }
+        if (mask->num_vectors) {
+            Plan* plan = static_cast<Plan*>(mask->plan);
+            Plan* tmp_plan = nullptr;
+            if (!plan && f_a > 0) plan = tmp_plan = build_plan(mask, s, nullptr, nullptr, nullptr);
+            struct PlanGuard {
+                Plan* p;
+                cudaStream_t s;
+                ~PlanGuard() { free_plan(p, s); }
+            } pg{tmp_plan, s};
+            sddmm_launch(mask, plan, a, a_dtype, lda, a_rows, bt, bt_dtype, ldbt, bt_rows, f_a, o.values, out_dtype,
+                         0.f, s);
         }
         // ref sddmm.hpp:121: one MMA per (16-vector group, k-step)
-        if (counters) counters->mma_invocations = mask->num_groups16 * ((F + mask->k - 1) / mask->k);
+        if (counters) counters->mma_invocations = mask->num_groups16 * ((f_a + mask->k - 1) / mask->k);
         *out = o;
     });
 }

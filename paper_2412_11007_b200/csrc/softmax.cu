@@ -21,6 +21,7 @@
 //   K3 softmax_finish  writes the normalised values of split segments.
 #include <algorithm>
 #include <cfloat>
+#include <type_traits>
 
 #include "tcs_internal.cuh"
 
@@ -147,6 +148,23 @@ __device__ __forceinline__ void online(float& m, float& s, float x) {
 // -- the K contiguous values of that block row -- so each lane's statistics
 // belong to one row.  A narrow last block (width w < K, only at the end of
 // a window) is taken by lanes 0..7, row = lane, values r*w .. r*w+w-1.
+// Liveness of a block row: from the mask values, or -- VM = void, the fused
+// SDDMM -> softmax whose dead slots hold -inf -- from the scores themselves.
+template <uint32_t K, typename VM>
+__device__ __forceinline__ void live_k(const VM* mask, uint64_t p, const float (&x)[K], bool (&l)[K]) {
+    if constexpr (std::is_void_v<VM>) {
+#pragma unroll
+        for (uint32_t j = 0; j < K; ++j) l[j] = x[j] != -INFINITY;
+    } else {
+        ldlive<K>(mask + p, l);
+    }
+}
+template <typename VM>
+__device__ __forceinline__ bool live_1(const VM* mask, uint64_t p, float x) {
+    if constexpr (std::is_void_v<VM>) return x != -INFINITY;
+    else return live_at<VM>(mask, p);
+}
+
 template <uint32_t K, typename VS, typename VM>
 __device__ __forceinline__ void row_stats(const VS* scores, const VM* mask, uint64_t vb, uint32_t v0, uint32_t v1,
                                           uint32_t lane, float scale, float& m, float& s) {
@@ -159,15 +177,17 @@ __device__ __forceinline__ void row_stats(const VS* scores, const VM* mask, uint
         float x[K];
         bool l[K];
         ldv<K>(scores + p, x);
-        ldlive<K>(mask + p, l);
+        live_k<K, VM>(mask, p, x, l);
 #pragma unroll
         for (uint32_t j = 0; j < K; ++j)
             if (l[j]) online(m, s, scale * x[j]);
     }
     if (w && lane < 8) {
         const uint64_t p = vb + 8ull * K * (b0 + nfull) + r * w;
-        for (uint32_t j = 0; j < w; ++j)
-            if (live_at<VM>(mask, p + j)) online(m, s, scale * ld_val<VS>(scores, p + j));
+        for (uint32_t j = 0; j < w; ++j) {
+            const float x = ld_val<VS>(scores, p + j);
+            if (live_1<VM>(mask, p + j, x)) online(m, s, scale * x);
+        }
     }
     // merge the 4 lanes that own row r (lanes r, r+8, r+16, r+24)
 #pragma unroll
@@ -187,24 +207,31 @@ __device__ __forceinline__ void row_write(const VS* scores, const VM* mask, VO* 
         float x[K], y[K];
         bool l[K];
         ldv<K>(scores + p, x);
-        ldlive<K>(mask + p, l);
+        live_k<K, VM>(mask, p, x, l);
 #pragma unroll
         for (uint32_t j = 0; j < K; ++j) y[j] = l[j] ? __expf(scale * x[j] - m) * inv : 0.f;
         stv<K>(out + p, y);
     }
-    if (w && lane < 8) {
+    if (w && lane < 8) {  // all loads before any store: no load-after-store round trips
         const uint64_t p = vb + 8ull * K * (b0 + nfull) + r * w;
-        for (uint32_t j = 0; j < w; ++j)
-            st_val<VO>(out, p + j,
-                       live_at<VM>(mask, p + j) ? __expf(scale * ld_val<VS>(scores, p + j) - m) * inv : 0.f);
+        float x[K];
+        bool l[K];
+#pragma unroll
+        for (uint32_t j = 0; j < K - 1; ++j) {
+            x[j] = j < w ? ld_val<VS>(scores, p + j) : 0.f;
+            l[j] = j < w && live_1<VM>(mask, p + j, x[j]);
+        }
+#pragma unroll
+        for (uint32_t j = 0; j < K - 1; ++j)
+            if (j < w) st_val<VO>(out, p + j, l[j] ? __expf(scale * x[j] - m) * inv : 0.f);
     }
 }
 
 template <uint32_t K, typename VS, typename VM, typename VO>
 __global__ void __launch_bounds__(256) softmax_items(const WorkItem* __restrict__ items, uint64_t n_items,
                                                      uint32_t* counter, const uint32_t* __restrict__ rp,
-                                                     const VS* __restrict__ scores, const VM* __restrict__ mask,
-                                                     VO* __restrict__ out, float scale, RowStat* __restrict__ part) {
+                                                     const VS* scores, const VM* __restrict__ mask, VO* out,
+                                                     float scale, RowStat* __restrict__ part) {
     const uint32_t lane = threadIdx.x & 31;
     for (;;) {
         uint32_t idx = 0;
@@ -242,8 +269,8 @@ __global__ void softmax_combine(const SplitWindow* __restrict__ split, uint64_t 
 template <uint32_t K, typename VS, typename VM, typename VO>
 __global__ void __launch_bounds__(256) softmax_finish(const WorkItem* __restrict__ items, uint64_t n_slots,
                                                       const SplitWindow* __restrict__ split, uint64_t n_split,
-                                                      const uint32_t* __restrict__ rp, const VS* __restrict__ scores,
-                                                      const VM* __restrict__ mask, VO* __restrict__ out, float scale,
+                                                      const uint32_t* __restrict__ rp, const VS* scores,
+                                                      const VM* __restrict__ mask, VO* out, float scale,
                                                       const RowStat* __restrict__ part) {
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
@@ -265,10 +292,10 @@ __global__ void __launch_bounds__(256) softmax_finish(const WorkItem* __restrict
     }
 }
 
+// scores sv (structure of sc), mask values mv (nullptr with VM = void), out
+// may alias sv.
 template <uint32_t K, typename VS, typename VM, typename VO>
-void run(const tcs_mebcrs* sc, const tcs_mebcrs* mk, VO* out, float scale, const Plan* plan, cudaStream_t s) {
-    const VS* sv = static_cast<const VS*>(sc->values);
-    const VM* mv = static_cast<const VM*>(mk->values);
+void run(const tcs_mebcrs* sc, const VS* sv, const VM* mv, VO* out, float scale, const Plan* plan, cudaStream_t s) {
     DBuf ctr(sizeof(uint32_t), s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
     TCS_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(uint32_t), s));
     const int grid = static_cast<int>(std::min<uint64_t>((plan->n_items + 7) / 8, uint64_t(num_sms()) * 8));
@@ -291,8 +318,10 @@ void run(const tcs_mebcrs* sc, const tcs_mebcrs* mk, VO* out, float scale, const
 template <uint32_t K, typename VS, typename VM>
 void run_o(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt, float scale, const Plan* plan,
            cudaStream_t s) {
-    if (odt == TCS_DTYPE_F32) run<K, VS, VM, float>(sc, mk, static_cast<float*>(out), scale, plan, s);
-    else run<K, VS, VM, __half>(sc, mk, static_cast<__half*>(out), scale, plan, s);
+    const VS* sv = static_cast<const VS*>(sc->values);
+    const VM* mv = static_cast<const VM*>(mk->values);
+    if (odt == TCS_DTYPE_F32) run<K, VS, VM, float>(sc, sv, mv, static_cast<float*>(out), scale, plan, s);
+    else run<K, VS, VM, __half>(sc, sv, mv, static_cast<__half*>(out), scale, plan, s);
 }
 
 template <uint32_t K>
@@ -303,6 +332,16 @@ void run_k(const tcs_mebcrs* sc, const tcs_mebcrs* mk, void* out, tcs_dtype odt,
     else if (s32) run_o<K, float, __half>(sc, mk, out, odt, scale, plan, s);
     else if (m32) run_o<K, __half, float>(sc, mk, out, odt, scale, plan, s);
     else run_o<K, __half, __half>(sc, mk, out, odt, scale, plan, s);
+}
+
+// Fused SDDMM -> row softmax: the scores come with dead slots = -inf, so
+// the softmax passes read no mask (VM = void).
+template <uint32_t K, typename VX>
+void run_fused(const tcs_mebcrs* m, const void* x, void* out, tcs_dtype odt, float scale, const Plan* plan,
+               cudaStream_t s) {
+    const VX* xv = static_cast<const VX*>(x);
+    if (odt == TCS_DTYPE_F32) run<K, VX, void, float>(m, xv, nullptr, static_cast<float*>(out), scale, plan, s);
+    else run<K, VX, void, __half>(m, xv, nullptr, static_cast<__half*>(out), scale, plan, s);
 }
 
 }  // namespace
@@ -345,6 +384,58 @@ extern "C" tcs_status tcs_mebcrs_row_softmax(const tcs_mebcrs* scores, const tcs
             } g{tmp, s};
             if (scores->k == 8) run_k<8>(scores, mask, o.values, out_dtype, scale, plan, s);
             else run_k<4>(scores, mask, o.values, out_dtype, scale, plan, s);
+        }
+        *out = o;
+    });
+}
+
+extern "C" tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda,
+                                            int64_t a_rows, int64_t f_a, const void* bt, tcs_dtype bt_dtype,
+                                            int64_t ldbt, int64_t bt_rows, int64_t f_b, float scale,
+                                            tcs_dtype score_dtype, tcs_mebcrs* out, tcs_dtype out_dtype,
+                                            const tcs_kernel_config* cfg, tcs_stream_t stream) {
+    return guard([&] {
+        if (!out) fail(TCS_ERR_ARGUMENT, "null output");
+        sddmm_check(mask, a, a_dtype, lda, a_rows, f_a, bt, bt_dtype, ldbt, bt_rows, f_b, score_dtype, cfg);
+        if (out_dtype != TCS_DTYPE_F16 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown output dtype");
+        if (mask->precision == TCS_TF32 && out_dtype != TCS_DTYPE_F32)
+            fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
+        cudaStream_t s = st(stream);
+        const uint64_t nv = mask->num_vectors;
+        void* caller_values = out->values;
+        tcs_mebcrs o = *mask;
+        o.flags = o.plan ? TCS_MEBCRS_BORROWED_PLAN : 0u;
+        o.value_dtype = out_dtype;
+        const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4, xw = score_dtype == TCS_DTYPE_F16 ? 2 : 4;
+        if (caller_values) {
+            o.values = caller_values;
+        } else {
+            o.values = dalloc(std::max<uint64_t>(1, 8 * nv) * ow, s);
+            o.flags |= TCS_MEBCRS_OWN_VALUES;
+        }
+        if (nv) {
+            Plan* plan = static_cast<Plan*>(mask->plan);
+            Plan* tmp_plan = nullptr;
+            if (!plan) plan = tmp_plan = build_plan(mask, s, nullptr, nullptr, nullptr);
+            struct PlanGuard {
+                Plan* p;
+                cudaStream_t s;
+                ~PlanGuard() { free_plan(p, s); }
+            } pg{tmp_plan, s};
+            // the scores go to the output buffer when the dtypes agree (normalised in place)
+            DBuf xbuf;
+            void* x = o.values;
+            if (score_dtype != out_dtype) {
+                xbuf = DBuf(8 * nv * xw, s);
+                x = xbuf.p;
+            }
+            sddmm_launch(mask, plan, a, a_dtype, lda, a_rows, bt, bt_dtype, ldbt, bt_rows, f_a, x, score_dtype,
+                         -INFINITY, s);
+            if (plan->n_items) {
+                if (mask->k == 4) run_fused<4, float>(mask, x, o.values, out_dtype, scale, plan, s);
+                else if (score_dtype == TCS_DTYPE_F32) run_fused<8, float>(mask, x, o.values, out_dtype, scale, plan, s);
+                else run_fused<8, __half>(mask, x, o.values, out_dtype, scale, plan, s);
+            }
         }
         *out = o;
     });

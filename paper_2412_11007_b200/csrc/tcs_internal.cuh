@@ -131,6 +131,14 @@ bool spmm_tc05(const tcs_mebcrs* A, const Plan* plan, const __half* B, int64_t l
                float* c, int64_t ldc, float* partial, int64_t ldp, cudaStream_t s);
 inline cudaStream_t st(tcs_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// SDDMM pieces shared with the fused SDDMM -> row-softmax (sddmm.cu).
+void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda, int64_t a_rows, int64_t f_a,
+                 const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t f_b, tcs_dtype out_dtype,
+                 const tcs_kernel_config* cfg);
+void sddmm_launch(const tcs_mebcrs* mask, const Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
+                  int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
+                  void* out_values, tcs_dtype out_dtype, float dead, cudaStream_t s);
+
 }  // namespace tcs
 
 // ============================================================ device helpers

@@ -64,10 +64,17 @@ class AGNNLayer:
         self.precision = precision
         self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
 
-    def attention(self, H: torch.Tensor) -> T.MeBcrsMatrix:
+    def attention(self, H: torch.Tensor, fused: bool = True) -> T.MeBcrsMatrix:
+        """P = row_softmax(beta * cos(h_i, h_j)) over the edges.  fused: one
+        SDDMM kernel that also emits the softmax row statistics, then one
+        normalisation pass (tcs_sddmm_row_softmax; FP16 keeps the scores in
+        f16, normalised in place); else SDDMM -> tcs_mebcrs_row_softmax."""
         Hn = torch.nn.functional.normalize(H.float(), dim=1).to(self.dtype)
-        scores = T.sddmm(T.SddmmOperands(self.mask, Hn, Hn), self.cfg).output  # cos(h_i, h_j) at the edges
+        ops = T.SddmmOperands(self.mask, Hn, Hn)
         pdt = _abi.TCS_DTYPE_F16 if self.precision == T.Precision.fp16 else _abi.TCS_DTYPE_F32
+        if fused:
+            return T.sddmm_row_softmax(ops, self.beta, self.cfg, score_dtype=pdt, out_dtype=pdt)
+        scores = T.sddmm(ops, self.cfg).output  # cos(h_i, h_j) at the edges
         return T.row_softmax(scores, self.mask, self.beta, pdt)
 
     def __call__(self, H: torch.Tensor) -> torch.Tensor:

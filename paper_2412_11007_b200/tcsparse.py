@@ -264,6 +264,29 @@ def row_softmax(scores: MeBcrsMatrix, mask: MeBcrsMatrix, scale: float = 1.0,
     return MeBcrsMatrix(h, keepalive=keep)
 
 
+def sddmm_row_softmax(ops: SddmmOperands, scale: float = 1.0, cfg: KernelConfig = KernelConfig(),
+                      score_dtype: int = _abi.TCS_DTYPE_F32, out_dtype: int = _abi.TCS_DTYPE_F16,
+                      out_values: torch.Tensor | None = None) -> MeBcrsMatrix:
+    """Fused ``row_softmax(sddmm(ops).output, ops.mask, scale)``
+    (tcs_sddmm_row_softmax): the scores (stored as score_dtype) carry the
+    per-row softmax partials out of the SDDMM kernel and are normalised in
+    one pass."""
+    a = ops.a if ops.a.stride(-1) == 1 else ops.a.contiguous()
+    b = ops.b_t if ops.b_t.stride(-1) == 1 else ops.b_t.contiguous()
+    h = _abi.tcs_mebcrs()
+    keep = [ops.mask]
+    if out_values is not None:
+        if out_values.numel() < 8 * ops.mask.num_vectors or not out_values.is_contiguous():
+            raise ArgumentError("out_values too small or not contiguous")
+        h.values = out_values.data_ptr()
+        keep.append(out_values)
+    _check(_abi.load().tcs_sddmm_row_softmax(C.byref(ops.mask._h), a.data_ptr(), _dtype_tag(a), a.stride(0),
+                                             a.shape[0], a.shape[1], b.data_ptr(), _dtype_tag(b), b.stride(0),
+                                             b.shape[0], b.shape[1], float(scale), int(score_dtype), C.byref(h),
+                                             int(out_dtype), C.byref(cfg._c()), _stream()))
+    return MeBcrsMatrix(h, keepalive=keep)
+
+
 def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
     """Device operand rounding used by the kernels (diagnostics)."""
     x = x.to(torch.float32).contiguous()

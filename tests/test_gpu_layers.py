@@ -132,3 +132,47 @@ def test_gcn_layer_matches_dense_reference(p):
     want = Ahat @ (H.double().cpu() @ W.double().cpu())
     err = (got - want).norm() / want.norm()
     assert err < (1e-2 if p == 0 else 1e-3), float(err)
+
+
+def _fused_case(m, p, score_dt, out_dt, scale, F=24):
+    me = T.encode_mebcrs(T.CsrMatrix(m.rows, m.cols, torch.from_numpy(m.row_ptr.view(np.int32)).cuda(),
+                                     torch.from_numpy(m.col_idx.view(np.int32)).cuda(),
+                                     torch.from_numpy(m.values).cuda()), T.Precision(p), 1)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn(m.rows, F, device="cuda", generator=g)
+    Bt = torch.randn(m.cols, F, device="cuda", generator=g)
+    ops = T.SddmmOperands(me, A, Bt)
+    cfg = T.KernelConfig(T.Precision(p))
+    fused = T.sddmm_row_softmax(ops, scale, cfg, score_dtype=score_dt, out_dtype=out_dt)
+    scores = T.sddmm(ops, cfg, out_dtype=score_dt).output
+    two = T.row_softmax(scores, me, scale, out_dt)
+    return fused.to_host()[2], two.to_host()[2]
+
+
+@pytest.mark.parametrize("p,score_dt,out_dt", [(0, 1, 0), (0, 0, 0), (0, 1, 1), (0, 0, 1), (1, 1, 1)])
+def test_fused_sddmm_softmax_equals_composition(p, score_dt, out_dt):
+    """tcs_sddmm_row_softmax == tcs_sddmm -> tcs_mebcrs_row_softmax up to the
+    order of the exp sums (max statistics are exact, dead slots exactly 0)."""
+    m = O.generate_random_sparse(203, 150, 0.08, 17, real=True)
+    m.values[::7] = 0.0  # stored but not live
+    got, want = _fused_case(m, p, score_dt, out_dt, 0.7)
+    tol = 2e-3 if out_dt == 0 else 1e-5
+    assert np.abs(got - want).max() < tol
+
+
+def test_fused_sddmm_softmax_split_windows():
+    rng = np.random.default_rng(4)
+    rows, cols = 40, 30000
+    per_row = [25000] * 8 + [3] * 8 + [9000] * 8 + [0] * 8 + [100] * 8
+    rp = np.zeros(rows + 1, np.uint32)
+    cis = []
+    for r, d in enumerate(per_row):
+        cis.append(np.sort(rng.choice(cols, size=d, replace=False)).astype(np.uint32))
+        rp[r + 1] = rp[r] + d
+    ci = np.concatenate(cis)
+    vals = np.ones(ci.size, np.float32)
+    vals[::11] = 0.0
+    m = O.Csr(rows, cols, rp, ci, vals)
+    for p in (0, 1):
+        got, want = _fused_case(m, p, 1, 1, 2.0, F=40)
+        assert np.abs(got - want).max() < 1e-5 + 1e-4 * np.abs(want).max()

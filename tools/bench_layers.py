@@ -73,10 +73,13 @@ if "c5" in which:
     softmax_ms = timed(lambda: T.row_softmax(scores, layer.mask, 1.0))
     P = T.row_softmax(scores, layer.mask, 1.0)
     spmm_ms = timed(lambda: T.spmm(P, H.half(), layer.cfg))
+    fused_ms = timed(lambda: T.sddmm_row_softmax(T.SddmmOperands(layer.mask, Hn, Hn), 1.0, layer.cfg,
+                                                 score_dtype=0, out_dtype=0))
     layer_ms = timed(lambda: layer(H))
     out["c5_agnn"] = {"nodes": rows, "nnz": nnz, "nv": layer.mask.num_vectors, "F": F,
                       "max_window_vectors": layer.mask.max_window_vectors,
-                      "sddmm_ms": round(sddmm_ms, 3), "softmax_ms": round(softmax_ms, 3), "spmm_ms": round(spmm_ms, 3),
+                      "sddmm_ms": round(sddmm_ms, 3), "softmax_ms": round(softmax_ms, 3),
+                      "fused_sddmm_softmax_ms": round(fused_ms, 3), "spmm_ms": round(spmm_ms, 3),
                       "layer_ms": round(layer_ms, 3), "sddmm_gflops": round(2 * nnz * F / sddmm_ms / 1e6, 1),
                       "spmm_gflops": round(2 * nnz * F / spmm_ms / 1e6, 1), "gen_s": round(gen_s, 1),
                       "build_s": round(build_s, 2)}
