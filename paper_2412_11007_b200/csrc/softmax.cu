@@ -135,14 +135,6 @@ __device__ __forceinline__ void stv(__half* p, const float (&y)[N]) {
     else *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
 }
 
-__device__ __forceinline__ void online(float& m, float& s, float x) {
-    if (x > m) {
-        s = (m == -FLT_MAX ? 0.f : s * __expf(m - x)) + 1.f;
-        m = x;
-    } else {
-        s += __expf(x - m);
-    }
-}
 
 // Lane l owns row r = l % 8 of block (l / 8) of every group of 4 full blocks
 // -- the K contiguous values of that block row -- so each lane's statistics
@@ -165,6 +157,33 @@ __device__ __forceinline__ bool live_1(const VM* mask, uint64_t p, float x) {
     else return live_at<VM>(mask, p);
 }
 
+// z = scale * x over a block row, -inf where not live.
+template <uint32_t K, typename VS, typename VM>
+__device__ __forceinline__ void block_z(const VS* scores, const VM* mask, uint64_t p, float scale, float (&z)[K]) {
+    float x[K];
+    bool l[K];
+    ldv<K>(scores + p, x);
+    live_k<K, VM>(mask, p, x, l);
+#pragma unroll
+    for (uint32_t j = 0; j < K; ++j) z[j] = l[j] ? scale * x[j] : -INFINITY;
+}
+
+// Adds n values (-inf = not live) to the running (m, s): one max over the
+// values, at most one rescale, then branch-free exps (exp(-inf) = 0; m
+// starts at -FLT_MAX, so no inf - inf arises).
+template <uint32_t N>
+__device__ __forceinline__ void add_values(float& m, float& s, const float (&z)[N]) {
+    float bm = z[0];
+#pragma unroll
+    for (uint32_t j = 1; j < N; ++j) bm = fmaxf(bm, z[j]);
+    if (bm > m) {
+        s *= __expf(m - bm);
+        m = bm;
+    }
+#pragma unroll
+    for (uint32_t j = 0; j < N; ++j) s += __expf(z[j] - m);
+}
+
 template <uint32_t K, typename VS, typename VM>
 __device__ __forceinline__ void row_stats(const VS* scores, const VM* mask, uint64_t vb, uint32_t v0, uint32_t v1,
                                           uint32_t lane, float scale, float& m, float& s) {
@@ -173,21 +192,22 @@ __device__ __forceinline__ void row_stats(const VS* scores, const VM* mask, uint
     m = -FLT_MAX;
     s = 0.f;
     for (uint32_t b = b0 + bl; b < b0 + nfull; b += 4) {
-        const uint64_t p = vb + 8ull * K * b + r * K;
-        float x[K];
-        bool l[K];
-        ldv<K>(scores + p, x);
-        live_k<K, VM>(mask, p, x, l);
-#pragma unroll
-        for (uint32_t j = 0; j < K; ++j)
-            if (l[j]) online(m, s, scale * x[j]);
+        float z[K];
+        block_z<K, VS, VM>(scores, mask, vb + 8ull * K * b + r * K, scale, z);
+        add_values<K>(m, s, z);
     }
     if (w && lane < 8) {
         const uint64_t p = vb + 8ull * K * (b0 + nfull) + r * w;
-        for (uint32_t j = 0; j < w; ++j) {
-            const float x = ld_val<VS>(scores, p + j);
-            if (live_1<VM>(mask, p + j, x)) online(m, s, scale * x);
+        float z[K - 1];
+#pragma unroll
+        for (uint32_t j = 0; j < K - 1; ++j) {
+            z[j] = -INFINITY;
+            if (j < w) {
+                const float x = ld_val<VS>(scores, p + j);
+                if (live_1<VM>(mask, p + j, x)) z[j] = scale * x;
+            }
         }
+        add_values<K - 1>(m, s, z);
     }
     // merge the 4 lanes that own row r (lanes r, r+8, r+16, r+24)
 #pragma unroll
@@ -204,12 +224,10 @@ __device__ __forceinline__ void row_write(const VS* scores, const VM* mask, VO* 
     const uint32_t b0 = v0 / K, nfull = (v1 - v0) / K, w = (v1 - v0) % K;
     for (uint32_t b = b0 + bl; b < b0 + nfull; b += 4) {
         const uint64_t p = vb + 8ull * K * b + r * K;
-        float x[K], y[K];
-        bool l[K];
-        ldv<K>(scores + p, x);
-        live_k<K, VM>(mask, p, x, l);
+        float z[K], y[K];
+        block_z<K, VS, VM>(scores, mask, p, scale, z);
 #pragma unroll
-        for (uint32_t j = 0; j < K; ++j) y[j] = l[j] ? __expf(scale * x[j] - m) * inv : 0.f;
+        for (uint32_t j = 0; j < K; ++j) y[j] = __expf(z[j] - m) * inv;  // not live: exp(-inf) = 0
         stv<K>(out + p, y);
     }
     if (w && lane < 8) {  // all loads before any store: no load-after-store round trips
