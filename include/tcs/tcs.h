@@ -208,6 +208,12 @@ tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtyp
                                  int64_t bt_rows, int64_t f_b, float scale, tcs_dtype score_dtype, tcs_mebcrs* out,
                                  tcs_dtype out_dtype, const tcs_kernel_config* cfg, tcs_stream_t stream);
 
+/* AGNN input transform (no reference counterpart): hn[i] = h[i] /
+ * max(||h[i]||_2, eps) and hc[i] = h[i], rounded to out_dtype (F16/F32),
+ * from one read of the f32 rows h [rows][ldh].  hn or hc may be NULL. */
+tcs_status tcs_rows_normalize(const float* h, int64_t rows, int64_t f, int64_t ldh, void* hn, void* hc, int64_t ldo,
+                              tcs_dtype out_dtype, float eps, tcs_stream_t stream);
+
 /* ------------------------------------------------- host-buffer entry points */
 /* Value semantics of the reference API: host arrays in, host arrays out.  */
 

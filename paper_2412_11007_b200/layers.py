@@ -64,12 +64,14 @@ class AGNNLayer:
         self.precision = precision
         self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
 
-    def attention(self, H: torch.Tensor, fused: bool = True) -> T.MeBcrsMatrix:
+    def attention(self, H: torch.Tensor, fused: bool = True, Hn: torch.Tensor | None = None) -> T.MeBcrsMatrix:
         """P = row_softmax(beta * cos(h_i, h_j)) over the edges.  fused: one
-        SDDMM kernel that also emits the softmax row statistics, then one
-        normalisation pass (tcs_sddmm_row_softmax; FP16 keeps the scores in
-        f16, normalised in place); else SDDMM -> tcs_mebcrs_row_softmax."""
-        Hn = torch.nn.functional.normalize(H.float(), dim=1).to(self.dtype)
+        SDDMM kernel writes the scores with -inf at non-edges, then the
+        softmax passes need no mask (tcs_sddmm_row_softmax; FP16 keeps the
+        scores in f16, normalised in place); else SDDMM ->
+        tcs_mebcrs_row_softmax."""
+        if Hn is None:
+            Hn, _ = T.rows_normalize(H.float().contiguous(), self.dtype, copy=False)
         ops = T.SddmmOperands(self.mask, Hn, Hn)
         pdt = _abi.TCS_DTYPE_F16 if self.precision == T.Precision.fp16 else _abi.TCS_DTYPE_F32
         if fused:
@@ -78,5 +80,8 @@ class AGNNLayer:
         return T.row_softmax(scores, self.mask, self.beta, pdt)
 
     def __call__(self, H: torch.Tensor) -> torch.Tensor:
-        P = self.attention(H)
-        return T.spmm(P, H.to(self.dtype), self.cfg).output
+        # one pass over H: the normalised rows (SDDMM operand) and H itself
+        # in the kernels' dtype (SpMM operand)
+        Hn, Hc = T.rows_normalize(H.float().contiguous(), self.dtype)
+        P = self.attention(H, Hn=Hn)
+        return T.spmm(P, Hc, self.cfg).output

@@ -287,6 +287,22 @@ def sddmm_row_softmax(ops: SddmmOperands, scale: float = 1.0, cfg: KernelConfig 
     return MeBcrsMatrix(h, keepalive=keep)
 
 
+def rows_normalize(h: torch.Tensor, dtype: torch.dtype = torch.float16, eps: float = 1e-12,
+                   normalized: bool = True, copy: bool = True):
+    """(h / max(||h_i||, eps), h) in `dtype` from one pass over the f32 rows
+    (tcs_rows_normalize; the AGNN layer's SDDMM / SpMM operands)."""
+    if h.dtype != torch.float32 or h.dim() != 2 or h.stride(-1) != 1:
+        raise ArgumentError("h must be a 2-D f32 tensor with unit column stride")
+    rows, f = h.shape
+    hn = torch.empty(rows, f, dtype=dtype, device=h.device) if normalized else None
+    hc = torch.empty(rows, f, dtype=dtype, device=h.device) if copy else None
+    tag = _abi.TCS_DTYPE_F16 if dtype == torch.float16 else _abi.TCS_DTYPE_F32
+    _check(_abi.load().tcs_rows_normalize(h.data_ptr(), rows, f, h.stride(0),
+                                          hn.data_ptr() if hn is not None else None,
+                                          hc.data_ptr() if hc is not None else None, f, tag, float(eps), _stream()))
+    return hn, hc
+
+
 def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
     """Device operand rounding used by the kernels (diagnostics)."""
     x = x.to(torch.float32).contiguous()

@@ -176,3 +176,15 @@ def test_fused_sddmm_softmax_split_windows():
     for p in (0, 1):
         got, want = _fused_case(m, p, 1, 1, 2.0, F=40)
         assert np.abs(got - want).max() < 1e-5 + 1e-4 * np.abs(want).max()
+
+
+@pytest.mark.parametrize("f", [1, 32, 45, 130])
+def test_rows_normalize_matches_torch(f):
+    g = torch.Generator(device="cuda").manual_seed(f)
+    h = torch.randn(1000, f, device="cuda", generator=g)
+    h[7] = 0.0  # zero row: eps guard, like torch.nn.functional.normalize
+    for dt in (torch.float16, torch.float32):
+        hn, hc = T.rows_normalize(h, dt)
+        want = torch.nn.functional.normalize(h, dim=1)
+        assert torch.equal(hc, h.to(dt))
+        assert (hn.float() - want).abs().max() < (1e-3 if dt == torch.float16 else 1e-6)
