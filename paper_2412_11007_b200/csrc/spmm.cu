@@ -53,6 +53,10 @@ struct SpmmArgs {
 };
 
 constexpr int kWarps = 4;
+// Resident CTAs per SM.  Narrow slabs (32 features: 64-byte gathers, few
+// registers) need more warps in flight to cover DRAM-latency gathers when
+// B does not fit in L2 (C5: 537 MB of B).
+constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : 4; }
 
 // ------------------------------------------------------------- scheduling
 // Persistent warps: each warp claims work items from a per-slab counter
@@ -202,7 +206,7 @@ __device__ __forceinline__ void store_row(float* __restrict__ dst, const float (
 }
 
 template <int NCHUNK, int FPL, bool VF32>
-__global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;             // fragment coordinates
@@ -450,11 +454,11 @@ __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __re
     }
 }
 
-// Persistent launch: up to 4 CTAs (16 warps) per SM per slab; warps pull
-// items from the slab's counter.
+// Persistent launch: `bps` CTAs (4 warps each) per SM, shared by the
+// slabs; warps pull items from their slab's counter.
 template <typename K>
-void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name) {
-    const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * 4 / std::max(1, slabs));
+void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name, int bps = 4) {
+    const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * bps / std::max(1, slabs));
     const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
     const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
@@ -557,8 +561,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                     vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>")
                          : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>");
                 else
-                    vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>")
-                         : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>");
+                    vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>", spmm_blocks(1, 4))
+                         : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));
             } else {
                 if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
                 else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>");
