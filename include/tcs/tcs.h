@@ -50,7 +50,11 @@ typedef enum tcs_precision { TCS_FP16 = 0, TCS_TF32 = 1 } tcs_precision;
 typedef enum tcs_dtype { TCS_DTYPE_F16 = 0, TCS_DTYPE_F32 = 1 } tcs_dtype;
 
 /* ref: access_pattern.hpp:15 (ThreadMapping). No numerical effect
- * (ref tests/acceptance.cpp:103-104); both run the coalesced kernel. */
+ * (ref tests/acceptance.cpp:103-104): both give bit-identical results.
+ * COALESCED (default) runs the memory-efficient mapping; DIRECT runs, for
+ * FP16 SpMM, the paper's direct mapping (each lane loads its own fragment
+ * elements as 2-byte gathers) as the ablation baseline.  TF32 mappings
+ * coincide (ref access_pattern.hpp:110-119). */
 typedef enum tcs_mapping { TCS_MAP_DIRECT = 0, TCS_MAP_COALESCED = 1 } tcs_mapping;
 
 /* ref: matrix.hpp:20-49 (CsrMatrix). u32 indices, f32 values; column
@@ -146,6 +150,17 @@ tcs_status tcs_round_values(tcs_precision precision, const float* in, float* out
 tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
                              tcs_mebcrs* out, tcs_stream_t stream);
 
+/* ref: partition_windows(m, vector_height, k) (partition.hpp:40-66) +
+ * the ME-BCRS layout of mebcrs.hpp:80-114 at either vector height.
+ * vector_height 8 is tcs_mebcrs_encode.  vector_height 16 builds the
+ * 16-row-window layout of the reference's 16x1 baseline (spmm.hpp:187-257:
+ * windows of 16 rows, blocks 16 x k, value (r, j) of block b of window w at
+ * 16 * (row_pointers[w] + b * k) + r * width_b + j); such a handle is accepted
+ * only by tcs_spmm_baseline16, download, validate, prepare and free.  Other
+ * heights -> ARGUMENT (ref partition.hpp:42-43). */
+tcs_status tcs_mebcrs_encode_v(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
+                               uint32_t vector_height, tcs_mebcrs* out, tcs_stream_t stream);
+
 /* Builds (or rebuilds) the work list and the block/group counts for an
  * ME-BCRS whose arrays were filled by the caller.  Synchronises. */
 tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream);
@@ -168,6 +183,18 @@ tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream);
 tcs_status tcs_spmm(const tcs_mebcrs* a, const void* b, tcs_dtype b_dtype, int64_t ldb, int64_t b_rows,
                     int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
                     tcs_counters* counters, tcs_stream_t stream);
+
+/* ref: spmm_baseline16(const CsrMatrix&, const DenseMatrix&, const KernelConfig&)
+ * (spmm.hpp:187-257) -- the paper's non-swapped 16x1 ablation: sparse
+ * 16 x k blocks as the m=16 left MMA operand, k x 8 dense tiles.  `a` is a
+ * vector_height-16 handle from tcs_mebcrs_encode_v.  Same numerical
+ * contract as tcs_spmm.  Errors: cfg->vector_height != 16 -> ARGUMENT (ref
+ * :190); precision mismatch -> ARGUMENT; a->cols != b_rows -> SHAPE.
+ * counters->mma_invocations = sum_w ceil(nv_w / k) * ceil(n / 8) (ref
+ * analysis.hpp:34-38, Strategy::baseline16). */
+tcs_status tcs_spmm_baseline16(const tcs_mebcrs* a, const void* b, tcs_dtype b_dtype, int64_t ldb, int64_t b_rows,
+                               int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
+                               tcs_counters* counters, tcs_stream_t stream);
 
 /* ------------------------------------------------------------------ SDDMM */
 /* ref: sddmm(const SddmmOperands&, const KernelConfig&)  (sddmm.hpp:84).

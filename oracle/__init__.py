@@ -60,6 +60,12 @@ def lib():
         _orc.orc_mebcrs_row_pointers.restype = C.c_int64
         _orc.orc_mebcrs_row_pointers.argtypes = [C.c_uint64, _u32p, _u32p, _u32p]
         _orc.orc_mebcrs_fill.argtypes = [C.c_uint64, _u32p, _u32p, _f32p, C.c_uint32, _u32p, _u32p, _f32p]
+        _orc.orc_mebcrs_row_pointers_v.restype = C.c_int64
+        _orc.orc_mebcrs_row_pointers_v.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _u32p]
+        _orc.orc_mebcrs_fill_v.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_uint32, _u32p, _u32p,
+                                           _f32p]
+        _orc.orc_spmm_v.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_int, _u32p, _u32p, _f32p, _f32p,
+                                    C.c_uint64, C.c_uint64, _f32p, C.c_uint64, C.c_int]
         _orc.orc_mebcrs_to_dense.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, _u32p, _u32p, _f32p, _f32p]
         _orc.orc_spmm.argtypes = [C.c_uint64, C.c_uint32, C.c_int, _u32p, _u32p, _f32p, _f32p,
                                   C.c_uint64, C.c_uint64, _f32p, C.c_uint64, C.c_int]
@@ -106,6 +112,12 @@ def ref():
         _ref.ref_sddmm.argtypes = [C.c_uint64, C.c_uint64, C.c_int, _u32p, _u32p, _f32p, _f32p,
                                    C.c_uint64, _f32p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
                                    _f32p, _u64p]
+        _ref.ref_partition_windows.restype = C.c_int64
+        _ref.ref_partition_windows.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_uint64, C.c_uint64,
+                                               C.POINTER(_u32p), C.POINTER(_u32p)]
+        _ref.ref_spmm_baseline16.restype = C.c_int
+        _ref.ref_spmm_baseline16.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, _f32p, C.c_uint64,
+                                             C.c_uint64, C.c_int, C.c_uint64, _f32p, _u64p]
         _ref.ref_sddmm_output_offsets.restype = C.c_uint64
         _ref.ref_sddmm_output_offsets.argtypes = [C.c_uint64, C.c_int]
         _ref.ref_free.argtypes = [C.c_void_p]
@@ -168,8 +180,9 @@ class Csr:
 class MeBcrs:
     """ME-BCRS (inc/mebcrs.hpp:23-78) with f32 values (reference storage)."""
 
-    def __init__(self, rows, cols, precision, row_pointers, column_indices, values):
+    def __init__(self, rows, cols, precision, row_pointers, column_indices, values, vector_height=8):
         self.rows, self.cols, self.precision = int(rows), int(cols), int(precision)
+        self.vector_height = int(vector_height)
         self.k = K_OF[self.precision]
         self.row_pointers = np.ascontiguousarray(row_pointers, dtype=np.uint32)
         self.column_indices = np.ascontiguousarray(column_indices, dtype=np.uint32)
@@ -202,15 +215,16 @@ def generate_random_dense(rows, cols, seed, real=False) -> np.ndarray:
     return out
 
 
-def encode_mebcrs(m: Csr, precision: int) -> MeBcrs:
-    W = (m.rows + 7) // 8
+def encode_mebcrs(m: Csr, precision: int, vector_height: int = 8) -> MeBcrs:
+    vh = vector_height
+    W = (m.rows + vh - 1) // vh
     rp = np.empty(W + 1, np.uint32)
-    nv = lib().orc_mebcrs_row_pointers(m.rows, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(rp, _u32p))
+    nv = lib().orc_mebcrs_row_pointers_v(m.rows, vh, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(rp, _u32p))
     ci = np.empty(max(nv, 1), np.uint32)
-    vals = np.empty(max(8 * nv, 1), np.float32)
-    lib().orc_mebcrs_fill(m.rows, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(m.values, _f32p),
-                          K_OF[precision], _p(rp, _u32p), _p(ci, _u32p), _p(vals, _f32p))
-    return MeBcrs(m.rows, m.cols, precision, rp, ci[:nv], vals[:8 * nv])
+    vals = np.empty(max(vh * nv, 1), np.float32)
+    lib().orc_mebcrs_fill_v(m.rows, vh, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(m.values, _f32p),
+                            K_OF[precision], _p(rp, _u32p), _p(ci, _u32p), _p(vals, _f32p))
+    return MeBcrs(m.rows, m.cols, precision, rp, ci[:nv], vals[:vh * nv], vector_height=vh)
 
 
 def mebcrs_to_dense(me: MeBcrs) -> np.ndarray:
@@ -224,8 +238,9 @@ def spmm(me: MeBcrs, B: np.ndarray, strict=False) -> np.ndarray:
     B = np.ascontiguousarray(B, np.float32)
     N = B.shape[1]
     Cm = np.zeros((me.rows, N), np.float32)
-    lib().orc_spmm(me.rows, me.k, me.precision, _p(me.row_pointers, _u32p), _p(me.column_indices, _u32p),
-                   _p(me.values, _f32p), _p(B, _f32p), N, N, _p(Cm, _f32p), N, int(strict))
+    lib().orc_spmm_v(me.rows, me.vector_height, me.k, me.precision, _p(me.row_pointers, _u32p),
+                     _p(me.column_indices, _u32p), _p(me.values, _f32p), _p(B, _f32p), N, N, _p(Cm, _f32p), N,
+                     int(strict))
     return Cm
 
 
@@ -357,6 +372,30 @@ class Ref:
         if rc:
             raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
         return out[:8 * mask.nv], int(cnt.value)
+
+    @staticmethod
+    def partition_windows(m: Csr, vector_height: int, k: int):
+        """(row_pointers, column_indices) of ref partition_windows (partition.hpp:40-66)."""
+        r = ref()
+        rp, ci = _u32p(), _u32p()
+        nv = r.ref_partition_windows(m.rows, m.cols, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p),
+                                     _p(m.values, _f32p), vector_height, k, C.byref(rp), C.byref(ci))
+        if nv < 0:
+            raise ValueError("ArgumentError")
+        W = (m.rows + vector_height - 1) // vector_height
+        return _take(r, rp, W + 1, np.uint32), _take(r, ci, nv, np.uint32)
+
+    @staticmethod
+    def spmm_baseline16(m: Csr, B, precision: int, vector_height: int = 16):
+        B = np.ascontiguousarray(B, np.float32)
+        Cm = np.zeros((m.rows, B.shape[1]), np.float32)
+        cnt = C.c_uint64(0)
+        rc = ref().ref_spmm_baseline16(m.rows, m.cols, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p),
+                                       _p(m.values, _f32p), _p(B, _f32p), B.shape[0], B.shape[1], precision,
+                                       vector_height, _p(Cm, _f32p), C.byref(cnt))
+        if rc:
+            raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
+        return Cm, int(cnt.value)
 
     @staticmethod
     def sddmm_output_offsets(lane, kind):

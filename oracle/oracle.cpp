@@ -139,9 +139,10 @@ void orc_generate_random_dense(uint64_t rows, uint64_t cols, uint64_t seed, int 
 // Computes row_pointers (num_windows+1 entries, inc/mebcrs.hpp:89-95) and
 // returns the stored vector count nv.  Windows are 8 rows; the union of the
 // rows' column sets, ascending, is the window's vector list.
-int64_t orc_mebcrs_row_pointers(uint64_t rows, const uint32_t* row_ptr, const uint32_t* col_idx,
-                                uint32_t* out_rp) {
-    const uint64_t W = (rows + 7) / 8;
+// vh = vector height (8; 16 for the baseline16 layout, partition.hpp:42).
+int64_t orc_mebcrs_row_pointers_v(uint64_t rows, uint64_t vh, const uint32_t* row_ptr, const uint32_t* col_idx,
+                                  uint32_t* out_rp) {
+    const uint64_t W = (rows + vh - 1) / vh;
     std::vector<uint32_t> counts(W, 0);
 #pragma omp parallel
     {
@@ -149,7 +150,7 @@ int64_t orc_mebcrs_row_pointers(uint64_t rows, const uint32_t* row_ptr, const ui
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < static_cast<int64_t>(W); ++w) {
             merged.clear();
-            const uint64_t r0 = 8 * w, r1 = std::min<uint64_t>(rows, r0 + 8);
+            const uint64_t r0 = vh * w, r1 = std::min<uint64_t>(rows, r0 + vh);
             merged.insert(merged.end(), col_idx + row_ptr[r0], col_idx + row_ptr[r1]);
             std::sort(merged.begin(), merged.end());
             counts[w] = static_cast<uint32_t>(std::unique(merged.begin(), merged.end()) - merged.begin());
@@ -163,24 +164,26 @@ int64_t orc_mebcrs_row_pointers(uint64_t rows, const uint32_t* row_ptr, const ui
     }
     return static_cast<int64_t>(acc);
 }
+int64_t orc_mebcrs_row_pointers(uint64_t rows, const uint32_t* row_ptr, const uint32_t* col_idx, uint32_t* out_rp) {
+    return orc_mebcrs_row_pointers_v(rows, 8, row_ptr, col_idx, out_rp);
+}
 
 // ---- ME-BCRS encode, phase 2: column_indices + values ----------------------
 // inc/mebcrs.hpp:86-112 without the O(rows*cols) to_dense (:97): each CSR
 // entry lands at values[8*(rp[w]+b*k) + r*width_b + j] where its column is
 // the (b*k+j)-th vector of window w and width_b = min(k, nv_w - b*k)
 // (block_width, inc/mebcrs.hpp:46-51).  Every other slot stays 0.
-void orc_mebcrs_fill(uint64_t rows, const uint32_t* row_ptr, const uint32_t* col_idx,
-                     const float* values, uint32_t k, const uint32_t* rp, uint32_t* out_ci,
-                     float* out_values) {
-    const uint64_t W = (rows + 7) / 8;
-    std::memset(out_values, 0, sizeof(float) * 8ull * rp[W]);
+void orc_mebcrs_fill_v(uint64_t rows, uint64_t vh, const uint32_t* row_ptr, const uint32_t* col_idx,
+                       const float* values, uint32_t k, const uint32_t* rp, uint32_t* out_ci, float* out_values) {
+    const uint64_t W = (rows + vh - 1) / vh;
+    std::memset(out_values, 0, sizeof(float) * vh * rp[W]);
 #pragma omp parallel
     {
         std::vector<uint32_t> merged;
 #pragma omp for schedule(dynamic, 64)
         for (int64_t w = 0; w < static_cast<int64_t>(W); ++w) {
             merged.clear();
-            const uint64_t r0 = 8 * w, r1 = std::min<uint64_t>(rows, r0 + 8);
+            const uint64_t r0 = vh * w, r1 = std::min<uint64_t>(rows, r0 + vh);
             merged.insert(merged.end(), col_idx + row_ptr[r0], col_idx + row_ptr[r1]);
             std::sort(merged.begin(), merged.end());
             merged.erase(std::unique(merged.begin(), merged.end()), merged.end());
@@ -191,11 +194,15 @@ void orc_mebcrs_fill(uint64_t rows, const uint32_t* row_ptr, const uint32_t* col
                     const uint64_t v = std::lower_bound(merged.begin(), merged.end(), col_idx[p]) - merged.begin();
                     const uint64_t b = v / k, j = v % k;
                     const uint64_t width = std::min<uint64_t>(k, nvw - b * k);
-                    out_values[8 * (base + b * k) + (r - r0) * width + j] = values[p];
+                    out_values[vh * (base + b * k) + (r - r0) * width + j] = values[p];
                 }
             }
         }
     }
+}
+void orc_mebcrs_fill(uint64_t rows, const uint32_t* row_ptr, const uint32_t* col_idx, const float* values,
+                     uint32_t k, const uint32_t* rp, uint32_t* out_ci, float* out_values) {
+    orc_mebcrs_fill_v(rows, 8, row_ptr, col_idx, values, k, rp, out_ci, out_values);
 }
 
 // ---- decode (inc/mebcrs.hpp:118-138): ME-BCRS -> dense, zeros dropped ------
@@ -224,30 +231,35 @@ void orc_mebcrs_to_dense(uint64_t rows, uint64_t cols, uint32_t k, const uint32_
 // (:59-74).  `strict` = 1 also visits stored zero fill (matters only for
 // non-finite B, 0*inf = NaN); strict = 0 visits the stored vector values
 // only.  Empty windows leave rows at 0 (:128).  C is rows x N row-major.
-void orc_spmm(uint64_t rows, uint32_t k, int precision, const uint32_t* rp, const uint32_t* ci,
-              const float* vals, const float* B, uint64_t ldb, uint64_t N, float* C, uint64_t ldc,
-              int strict) {
-    const int64_t W = static_cast<int64_t>((rows + 7) / 8);
+// vh 16: spmm_baseline16 (inc/spmm.hpp:187-257) -- the same sequential
+// ascending-vector sum over 16-row windows ("same numerical contract").
+void orc_spmm_v(uint64_t rows, uint64_t vh, uint32_t k, int precision, const uint32_t* rp, const uint32_t* ci,
+                const float* vals, const float* B, uint64_t ldb, uint64_t N, float* C, uint64_t ldc, int strict) {
+    const int64_t W = static_cast<int64_t>((rows + vh - 1) / vh);
 #pragma omp parallel
     {
         std::vector<float> acc(N), brow(N);
 #pragma omp for schedule(dynamic, 16)
         for (int64_t w = 0; w < W; ++w) {
             const uint64_t nvw = rp[w + 1] - rp[w];
-            for (uint64_t r = 0; r < 8 && 8 * w + r < rows; ++r) {
+            for (uint64_t r = 0; r < vh && vh * w + r < rows; ++r) {
                 std::fill(acc.begin(), acc.end(), 0.0f);
                 for (uint64_t v = 0; v < nvw; ++v) {
                     const uint64_t b = v / k, j = v % k, width = std::min<uint64_t>(k, nvw - b * k);
-                    const float a = vals[8 * (rp[w] + b * k) + r * width + j];
+                    const float a = vals[vh * (rp[w] + b * k) + r * width + j];
                     if (a == 0.0f && !strict) continue;
                     const float ar = rnd(a, precision);
                     const float* brp = B + static_cast<uint64_t>(ci[rp[w] + v]) * ldb;
                     for (uint64_t n = 0; n < N; ++n) acc[n] += ar * rnd(brp[n], precision);
                 }
-                std::copy(acc.begin(), acc.end(), C + (8 * w + r) * ldc);
+                std::copy(acc.begin(), acc.end(), C + (vh * w + r) * ldc);
             }
         }
     }
+}
+void orc_spmm(uint64_t rows, uint32_t k, int precision, const uint32_t* rp, const uint32_t* ci, const float* vals,
+              const float* B, uint64_t ldb, uint64_t N, float* C, uint64_t ldc, int strict) {
+    orc_spmm_v(rows, 8, k, precision, rp, ci, vals, B, ldb, N, C, ldc, strict);
 }
 
 // ---- SDDMM (inc/sddmm.hpp:84-136) ------------------------------------------

@@ -165,6 +165,48 @@ int ref_sddmm(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp, c
     }
 }
 
+// partition_windows (inc/partition.hpp:40-66) at any vector height, as
+// CSR-style row pointers + concatenated window column lists.  Returns nv.
+int64_t ref_partition_windows(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci,
+                              const float* vals, uint64_t vector_height, uint64_t k, uint32_t** out_rp,
+                              uint32_t** out_ci) {
+    try {
+        const WindowPartition part = partition_windows(make_csr(rows, cols, rp, ci, vals), vector_height, k);
+        std::vector<uint32_t> prp(1, 0), pci;
+        for (const auto& w : part.windows) {
+            pci.insert(pci.end(), w.begin(), w.end());
+            prp.push_back(static_cast<uint32_t>(pci.size()));
+        }
+        *out_rp = dup(prp);
+        *out_ci = dup(pci);
+        return static_cast<int64_t>(pci.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// spmm_baseline16 (inc/spmm.hpp:187-257).  Returns 0 / 1 ArgumentError /
+// 2 ShapeError / 3 other.
+int ref_spmm_baseline16(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci, const float* vals,
+                        const float* B, uint64_t b_rows, uint64_t N, int precision, uint64_t vector_height,
+                        float* C, uint64_t* mma_invocations) {
+    try {
+        DenseMatrix b(b_rows, N);
+        std::memcpy(b.data.data(), B, sizeof(float) * b_rows * N);
+        const KernelConfig cfg{static_cast<Precision>(precision), vector_height, ThreadMapping::coalesced};
+        const SpmmResult res = spmm_baseline16(make_csr(rows, cols, rp, ci, vals), b, cfg);
+        std::memcpy(C, res.output.data.data(), sizeof(float) * rows * N);
+        if (mma_invocations) *mma_invocations = res.counters.mma_invocations;
+        return 0;
+    } catch (const ArgumentError&) {
+        return 1;
+    } catch (const ShapeError&) {
+        return 2;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
 uint64_t ref_sddmm_output_offsets(uint64_t lane, int kind) {
     return sddmm_output_offsets(lane, kind == 0 ? SubBlockKind::b8x8 : SubBlockKind::b8x4);
 }

@@ -53,6 +53,11 @@ EXPORTS = {
     "tcs_launch_count": (C.c_uint64, []),
     "tcs_round_values": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]),
     "tcs_mebcrs_encode": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_int, C.POINTER(tcs_mebcrs), C.c_void_p]),
+    "tcs_mebcrs_encode_v": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_int, C.c_uint32, C.POINTER(tcs_mebcrs),
+                                      C.c_void_p]),
+    "tcs_spmm_baseline16": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                      C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
+                                      C.c_void_p]),
     "tcs_mebcrs_prepare": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_validate": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_free": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),

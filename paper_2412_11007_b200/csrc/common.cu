@@ -276,14 +276,15 @@ __global__ void round_values_kernel(int precision, const float* __restrict__ in,
 }
 }  // namespace
 
-void check_mebcrs(const tcs_mebcrs* m) {
+void check_mebcrs(const tcs_mebcrs* m, bool any_height) {
     if (!m) fail(TCS_ERR_ARGUMENT, "null ME-BCRS handle");
-    if (m->vector_height != 8) fail(TCS_ERR_ARGUMENT, "ME-BCRS vector height must be 8");
+    if (m->vector_height != 8 && !(any_height && m->vector_height == 16))
+        fail(TCS_ERR_ARGUMENT, "ME-BCRS vector height must be 8");
     if (m->precision != TCS_FP16 && m->precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
     if (m->k != (m->precision == TCS_FP16 ? 8u : 4u)) fail(TCS_ERR_FORMAT, "block width k does not match precision");
     if (m->precision == TCS_TF32 && m->value_dtype != TCS_DTYPE_F32)
         fail(TCS_ERR_ARGUMENT, "TF32 ME-BCRS values must be stored as f32");
-    if (m->num_windows != (m->rows + 7) / 8) fail(TCS_ERR_FORMAT, "row_pointers length must be numWindows+1");
+    if (m->num_windows != (m->rows + m->vector_height - 1) / m->vector_height) fail(TCS_ERR_FORMAT, "row_pointers length must be numWindows+1");
     if (m->num_vectors >= (1ull << 32)) fail(TCS_ERR_FORMAT, "vector count exceeds u32 row pointers");
     if (!m->row_pointers) fail(TCS_ERR_ARGUMENT, "null row_pointers");
     if (m->num_vectors && (!m->column_indices || !m->values)) fail(TCS_ERR_ARGUMENT, "null ME-BCRS arrays");
@@ -313,7 +314,7 @@ tcs_status tcs_round_values(tcs_precision precision, const float* in, float* out
 
 tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream) {
     return guard([&] {
-        check_mebcrs(m);
+        check_mebcrs(m, true);
         cudaStream_t s = st(stream);
         if (m->plan && !(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
         m->plan = nullptr;
@@ -344,14 +345,14 @@ tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream) {
 tcs_status tcs_mebcrs_download(const tcs_mebcrs* m, uint32_t* row_pointers, uint32_t* column_indices,
                                float* values, tcs_stream_t stream) {
     return guard([&] {
-        check_mebcrs(m);
+        check_mebcrs(m, true);
         cudaStream_t s = st(stream);
         if (row_pointers)
             TCS_CUDA(cudaMemcpyAsync(row_pointers, m->row_pointers, (m->num_windows + 1) * 4, cudaMemcpyDeviceToHost, s));
         if (column_indices && m->num_vectors)
             TCS_CUDA(cudaMemcpyAsync(column_indices, m->column_indices, m->num_vectors * 4, cudaMemcpyDeviceToHost, s));
         if (values && m->num_vectors) {
-            const uint64_t n = 8 * m->num_vectors;
+            const uint64_t n = uint64_t(m->vector_height) * m->num_vectors;
             if (m->value_dtype == TCS_DTYPE_F32) {
                 TCS_CUDA(cudaMemcpyAsync(values, m->values, n * 4, cudaMemcpyDeviceToHost, s));
             } else {
@@ -403,7 +404,7 @@ tcs_status tcs_mebcrs_upload(uint64_t rows, uint64_t cols, tcs_precision precisi
 
 tcs_status tcs_mebcrs_validate(const tcs_mebcrs* m, tcs_stream_t stream) {
     return guard([&] {
-        check_mebcrs(m);
+        check_mebcrs(m, true);
         std::vector<uint32_t> rp(m->num_windows + 1), ci(m->num_vectors);
         cudaStream_t s = st(stream);
         TCS_CUDA(cudaMemcpyAsync(rp.data(), m->row_pointers, rp.size() * 4, cudaMemcpyDeviceToHost, s));

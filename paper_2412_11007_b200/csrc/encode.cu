@@ -48,11 +48,12 @@ struct CheckOut {
     uint32_t bad;  // nonzero = violated invariant code (see kBadMsg)
 };
 
+template <int VH>
 __global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uint64_t W, uint64_t nnz,
                              CheckOut* out) {
     uint32_t mx = 0, bad = 0;
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r0 = 8 * w, r1 = min(r0 + 8, rows);
+        const uint64_t r0 = VH * w, r1 = min(r0 + VH, rows);
         uint32_t prev = rp[r0];
         for (uint64_t r = r0 + 1; r <= r1; ++r) {
             const uint32_t x = rp[r];
@@ -73,14 +74,15 @@ __global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uin
     }
 }
 
-// Column index i (window-local) of the window whose row boundaries are rb[0..8]:
+// Column index i (window-local) of the window whose row boundaries are rb[0..VH]:
 // in range and strictly greater than its predecessor in the same row.
+template <int VH>
 __device__ __forceinline__ uint32_t check_col(const uint32_t* __restrict__ ci, uint32_t e0, uint32_t i, uint32_t c,
                                               const uint32_t* rb, uint64_t cols) {
     uint32_t bad = c >= cols ? 3u : 0u;
     bool row_start = false;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) row_start |= (i == rb[r]);
+    for (int r = 0; r < VH; ++r) row_start |= (i == rb[r]);
     if (!row_start && __ldg(ci + e0 + i - 1) >= c) bad = 4u;
     return bad;
 }
@@ -124,36 +126,47 @@ __device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restric
     }
 }
 
-// One window's merge + unique + rank, executed by the whole CTA.
+// One window's merge + unique + rank, executed by the whole CTA: the VH
+// rows are VH sorted runs, merged pairwise in log2(VH) passes.
 // bufA/bufB hold >= n keys each (shared or global).
+template <int VH>
 __device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint32_t* __restrict__ ci,
                                  uint64_t rows, uint64_t cols, uint64_t w, uint64_t* bufA, uint64_t* bufB,
                                  uint32_t* __restrict__ tmp_cols, uint32_t* __restrict__ rank,
                                  uint32_t* __restrict__ nv_out, CheckOut* chk) {
-    __shared__ uint32_t bnd[9];
-    __shared__ uint32_t bnd2[5];
-    __shared__ uint32_t bnd3[3];
-    const uint64_t r0 = 8 * w;
+    __shared__ uint32_t bnd[2 * VH + 8];  // run boundaries of every pass: VH+1, VH/2+1, ..., 2 entries
+    const uint64_t r0 = VH * w;
     const uint32_t e0 = csr_rp[r0];
-    if (threadIdx.x < 9) bnd[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
+    if (threadIdx.x <= VH) bnd[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
     __syncthreads();
-    const uint32_t n = bnd[8];
-    if (threadIdx.x < 5) bnd2[threadIdx.x] = bnd[2 * threadIdx.x];
-    if (threadIdx.x < 3) bnd3[threadIdx.x] = bnd[4 * threadIdx.x];
+    const uint32_t n = bnd[VH];
+    {
+        int off = VH + 1;
+        for (int runs = VH / 2; runs >= 1; runs /= 2) {  // boundaries of the pass producing `runs` runs
+            if (threadIdx.x <= runs) bnd[off + threadIdx.x] = bnd[threadIdx.x * (VH / runs)];
+            off += runs + 1;
+        }
+    }
     uint32_t bad = 0;
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t c = ci[e0 + i];
-        bad = max(bad, check_col(ci, e0, i, c, bnd, cols));
+        bad = max(bad, check_col<VH>(ci, e0, i, c, bnd, cols));
         bufA[i] = (static_cast<uint64_t>(c) << 32) | i;
     }
     if (bad) atomicMax(&chk->bad, bad);
     __syncthreads();
-    merge_pass(bufA, bufB, bnd, 8, n);
-    __syncthreads();
-    merge_pass(bufB, bufA, bnd2, 4, n);
-    __syncthreads();
-    merge_pass(bufA, bufB, bnd3, 2, n);
-    __syncthreads();
+    {
+        int off = 0;
+        for (int runs = VH; runs > 1; runs /= 2) {
+            merge_pass(bufA, bufB, bnd + off, runs, n);
+            __syncthreads();
+            uint64_t* t = bufA;
+            bufA = bufB;
+            bufB = t;
+            off += runs + 1;
+        }
+    }
+    bufB = bufA;  // the merged keys
     // bufB: entries sorted by (column, entry) -- the first entry of each
     // column run is the column's representative (ref partition.hpp:60-62:
     // sort + unique).
@@ -177,6 +190,7 @@ __device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint
     __syncthreads();  // bnd / buffers are reused by the next window
 }
 
+template <int VH>
 __global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_t* __restrict__ csr_rp,
                                                                    const uint32_t* __restrict__ ci, uint64_t rows,
                                                                    uint64_t cols, uint64_t W,
@@ -186,12 +200,13 @@ __global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_
     __shared__ uint64_t bufA[kSmallCap];
     __shared__ uint64_t bufB[kSmallCap];
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const uint32_t n = csr_rp[min(8 * w + 8, rows)] - csr_rp[8 * w];
+        const uint32_t n = csr_rp[min(VH * w + VH, rows)] - csr_rp[VH * w];
         if (n > kSmallCap) continue;  // block-uniform
-        window_sort_rank(csr_rp, ci, rows, cols, w, bufA, bufB, tmp_cols, rank, nv_out, chk);
+        window_sort_rank<VH>(csr_rp, ci, rows, cols, w, bufA, bufB, tmp_cols, rank, nv_out, chk);
     }
 }
 
+template <int VH>
 __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* __restrict__ csr_rp,
                                                                const uint32_t* __restrict__ ci, uint64_t rows,
                                                                uint64_t cols, uint64_t W,
@@ -201,8 +216,8 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                                                uint32_t* __restrict__ nv_out, CheckOut* chk) {
     extern __shared__ uint64_t smem_keys[];
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const uint32_t e0 = csr_rp[8 * w];
-        const uint32_t n = csr_rp[min(8 * w + 8, rows)] - e0;
+        const uint32_t e0 = csr_rp[VH * w];
+        const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
         if (n <= kSmallCap) continue;
         uint64_t *a, *b;
         if (n <= kBigCap) {
@@ -212,11 +227,12 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
             a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
             b = a + n;
         }
-        window_sort_rank(csr_rp, ci, rows, cols, w, a, b, tmp_cols, rank, nv_out, chk);
+        window_sort_rank<VH>(csr_rp, ci, rows, cols, w, a, b, tmp_cols, rank, nv_out, chk);
     }
 }
 
 // Bitmap ranking for windows with more than kSmallCap entries.
+template <int VH>
 __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* __restrict__ csr_rp,
                                                                 const uint32_t* __restrict__ ci, uint64_t rows,
                                                                 uint64_t cols, uint64_t W,
@@ -227,20 +243,20 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
     const uint32_t words = static_cast<uint32_t>((cols + 31) / 32);
     uint32_t* bm = bm_smem;
     uint32_t* pre = bm_smem + words;
-    __shared__ uint32_t rb[9];
+    __shared__ uint32_t rb[VH + 1];
     const uint32_t nt = blockDim.x, wpt = (words + nt - 1) / nt;
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const uint64_t r0 = 8 * w;
+        const uint64_t r0 = VH * w;
         const uint32_t e0 = csr_rp[r0];
-        const uint32_t n = csr_rp[min(r0 + 8, rows)] - e0;
+        const uint32_t n = csr_rp[min(r0 + VH, rows)] - e0;
         if (n <= kSmallCap) continue;  // block-uniform
-        if (threadIdx.x < 9) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
+        if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
         for (uint32_t i = threadIdx.x; i < words; i += nt) bm[i] = 0u;
         __syncthreads();
         uint32_t bad = 0;
         for (uint32_t i = threadIdx.x; i < n; i += nt) {
             const uint32_t c = ci[e0 + i];
-            const uint32_t b = check_col(ci, e0, i, c, rb, cols);
+            const uint32_t b = check_col<VH>(ci, e0, i, c, rb, cols);
             bad = max(bad, b);
             if (!b || b == 4u) atomicOr(&bm[c >> 5], 1u << (c & 31));
         }
@@ -284,7 +300,7 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 // coalesced stores -- every value byte hits global memory exactly once.
 constexpr uint32_t kScatterTile = 4096;  // vectors per smem tile (multiple of k)
 
-template <typename V>
+template <int VH, typename V>
 __global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
                                                       uint32_t k, const uint32_t* __restrict__ rp,
@@ -293,18 +309,19 @@ __global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals) {
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
-    __shared__ uint32_t rb[9];
+    __shared__ uint32_t rb[VH + 1];
+    constexpr uint32_t kTile = kScatterTile * 8 / VH;  // vectors per smem tile
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const uint64_t r0 = 8 * w;
-        if (threadIdx.x < 9) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
+        const uint64_t r0 = VH * w;
+        if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
         const uint32_t base = rp[w], nvw = rp[w + 1] - base;
         __syncthreads();
-        const uint32_t e0 = rb[0], e1 = rb[8];
+        const uint32_t e0 = rb[0], e1 = rb[VH];
         for (uint32_t i = threadIdx.x; i < nvw; i += blockDim.x) out_ci[base + i] = tmp_cols[e0 + i];
-        V* vals = out_vals + 8ull * base;
-        for (uint32_t t0 = 0; t0 < nvw; t0 += kScatterTile) {
-            const uint32_t tn = min(kScatterTile, nvw - t0);  // vectors in this tile
-            const uint32_t n16 = (8 * tn * sizeof(V) + 15) / 16;
+        V* vals = out_vals + static_cast<uint64_t>(VH) * base;
+        for (uint32_t t0 = 0; t0 < nvw; t0 += kTile) {
+            const uint32_t tn = min(kTile, nvw - t0);  // vectors in this tile
+            const uint32_t n16 = (VH * tn * sizeof(V) + 15) / 16;
             for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) tile_raw[i] = make_uint4(0, 0, 0, 0);
             __syncthreads();
             // 4 entries in flight per thread (coalesced per sub-step)
@@ -323,15 +340,15 @@ __global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict
                     if (v[u] < t0 || v[u] >= t0 + tn) continue;
                     uint32_t r = 0;
 #pragma unroll
-                    for (int q = 1; q < 8; ++q) r += (e >= rb[q]) ? 1u : 0u;
+                    for (int q = 1; q < VH; ++q) r += (e >= rb[q]) ? 1u : 0u;
                     const uint32_t b = v[u] / k, j = v[u] - b * k;
                     const uint32_t width = min(k, nvw - b * k);
-                    tile[(b * k - t0) * 8 + r * width + j] = store_cvt<V>(x[u]);
+                    tile[(b * k - t0) * VH + r * width + j] = store_cvt<V>(x[u]);
                 }
             }
             __syncthreads();
-            uint4* dst = reinterpret_cast<uint4*>(vals + 8ull * t0);  // 16-B aligned: 8*(base+t0)*sizeof(V)
-            const uint32_t full16 = (8 * tn * sizeof(V)) / 16;
+            uint4* dst = reinterpret_cast<uint4*>(vals + static_cast<uint64_t>(VH) * t0);  // 16-B aligned
+            const uint32_t full16 = (VH * tn * sizeof(V)) / 16;
             for (uint32_t i = threadIdx.x; i < full16; i += blockDim.x) dst[i] = tile_raw[i];
             __syncthreads();
         }
@@ -346,9 +363,13 @@ const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds n
 
 using namespace tcs;
 
-extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
-                                        tcs_mebcrs* out, tcs_stream_t stream) {
-    return guard([&] {
+namespace tcs {
+namespace {
+
+template <int VH>
+void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
+                 tcs_stream_t stream) {
+    {
         if (!csr || !out) fail(TCS_ERR_ARGUMENT, "null argument");
         if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
         if (precision == TCS_TF32 && value_dtype != TCS_DTYPE_F32)
@@ -357,14 +378,14 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
         if (!csr->row_ptr || (csr->nnz && (!csr->col_idx || !csr->values))) fail(TCS_ERR_ARGUMENT, "null CSR array");
         if (csr->nnz >= (1ull << 32)) fail(TCS_ERR_FORMAT, "nnz exceeds u32 row_ptr");
         cudaStream_t s = st(stream);
-        const uint64_t rows = csr->rows, W = (rows + 7) / 8, nnz = csr->nnz, cols = csr->cols;
+        const uint64_t rows = csr->rows, W = (rows + VH - 1) / VH, nnz = csr->nnz, cols = csr->cols;
         const uint32_t k = precision == TCS_FP16 ? 8 : 4;
         const int sms = num_sms();
 
         tcs_mebcrs m{};
         m.rows = rows;
         m.cols = cols;
-        m.vector_height = 8;
+        m.vector_height = VH;
         m.k = k;
         m.precision = precision;
         m.value_dtype = value_dtype;
@@ -390,7 +411,7 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
             DBuf chk(sizeof(CheckOut), s);
             TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
             const int g0 = static_cast<int>(std::min<uint64_t>((W + 255) / 256, uint64_t(sms) * 8));
-            window_stats<<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>());
+            window_stats<VH><<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>());
             TCS_LAUNCHED("window_stats");
             CheckOut h{};
             uint32_t ends[2] = {0, 0};
@@ -405,7 +426,7 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
             DBuf nvw(W * 4, s);
             CheckOut* dchk = chk.as<CheckOut>();
             const int g1 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * 16));
-            window_sort_small<<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+            window_sort_small<VH><<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                            tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
                                                            nvw.as<uint32_t>(), dchk);
             TCS_LAUNCHED("window_sort_small");
@@ -413,11 +434,11 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
                 const uint64_t words = (cols + 31) / 32;
                 if (words <= kBitmapMaxWords) {
                     const size_t smem = 2 * words * sizeof(uint32_t);
-                    TCS_CUDA(cudaFuncSetAttribute(window_bitmap, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    TCS_CUDA(cudaFuncSetAttribute(window_bitmap<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(std::max<size_t>(smem, 1))));
                     const int per_sm = std::max<int>(1, std::min<int>(4, int(200 * 1024 / std::max<size_t>(smem, 1))));
                     const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
-                    window_bitmap<<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                    window_bitmap<VH><<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
                                                                    nvw.as<uint32_t>(), dchk);
                     TCS_LAUNCHED("window_bitmap");
@@ -425,10 +446,10 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
                     DBuf scratch;
                     if (h.max_window_entries > kBigCap) scratch = DBuf(2 * nnz * 8, s);
                     const size_t smem = 2 * kBigCap * sizeof(uint64_t);
-                    TCS_CUDA(cudaFuncSetAttribute(window_sort_big, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                    TCS_CUDA(cudaFuncSetAttribute(window_sort_big<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(smem)));
                     const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms)));
-                    window_sort_big<<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                    window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
                                                                    rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk);
                     TCS_LAUNCHED("window_sort_big");
@@ -442,21 +463,21 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
             m.num_vectors = nv;
             const size_t vw = value_dtype == TCS_DTYPE_F16 ? 2 : 4;
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
-            m.values = dalloc(std::max<uint64_t>(1, 8ull * nv) * vw, s);
+            m.values = dalloc(std::max<uint64_t>(1, uint64_t(VH) * nv) * vw, s);
             const size_t tile_smem = size_t(kScatterTile) * 8 * vw;
             const int per_sm = static_cast<int>(std::max<size_t>(1, (200 * 1024) / tile_smem));
             const int g3 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
             if (value_dtype == TCS_DTYPE_F16) {
-                TCS_CUDA(cudaFuncSetAttribute(window_scatter<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<__half><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<VH, __half><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                   m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                   rank.as<uint32_t>(), m.column_indices,
                                                                   static_cast<__half*>(m.values));
             } else {
-                TCS_CUDA(cudaFuncSetAttribute(window_scatter<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<float><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<VH, float><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                  m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                  rank.as<uint32_t>(), m.column_indices,
                                                                  static_cast<float*>(m.values));
@@ -475,6 +496,24 @@ extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precis
             tcs_mebcrs_free(out, stream);
             fail(rc, msg);
         }
+    }
+}
+
+}  // namespace
+}  // namespace tcs
+
+extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
+                                        tcs_mebcrs* out, tcs_stream_t stream) {
+    return guard([&] { encode_impl<8>(csr, precision, value_dtype, out, stream); });
+}
+
+extern "C" tcs_status tcs_mebcrs_encode_v(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
+                                          uint32_t vector_height, tcs_mebcrs* out, tcs_stream_t stream) {
+    return guard([&] {
+        // ref partition.hpp:42-43
+        if (vector_height == 8) encode_impl<8>(csr, precision, value_dtype, out, stream);
+        else if (vector_height == 16) encode_impl<16>(csr, precision, value_dtype, out, stream);
+        else fail(TCS_ERR_ARGUMENT, "vector height must be 8 or 16");
     });
 }
 

@@ -283,6 +283,106 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     }
 }
 
+// ------------------------------------------------- FP16, direct mapping
+//
+// The paper's "direct" thread mapping (ref access_pattern.hpp:79-95,
+// ThreadMapping::direct), kept as the ablation of the memory-efficient
+// mapping above: lane (g, t) loads exactly its own A-fragment elements,
+// i.e. B[col(2t+dr)][16j + g + dc] for dr in {0,1}, dc in {0,8}, as single
+// 2-byte loads -- 8 lanes of a quarter touch 16 bytes of a row per load and
+// every B row is requested 2x as often (4 steps instead of 2 in the
+// reference's transaction model).  Same MMA operands and k order as the
+// coalesced kernel, hence bit-identical results (ref acceptance.cpp:103-104).
+template <int NMMA, bool VF32>
+__global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const SpmmArgs a) {
+    constexpr int SLAB = 16 * NMMA;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const unsigned short* Bl = static_cast<const unsigned short*>(a.B) + feat0 + g;
+    uint32_t* counter = a.counter + blockIdx.y;
+
+    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
+
+        float acc[NMMA][4];
+#pragma unroll
+        for (int j = 0; j < NMMA; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
+
+        for (uint32_t s = it.vbeg; s < vend; s += 16) {
+            const uint32_t colv = load_colpair(ci, s, vend, lane);
+            uint32_t col[4];
+            bool ok[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {  // k slots 2t, 2t+1, 2t+8, 2t+9
+                const uint32_t v = 2 * t + (u & 1) + 8 * (u >> 1);
+                col[u] = __shfl_sync(0xffffffffu, colv, v);
+                ok[u] = s + v < vend;
+            }
+            uint32_t b0, b1;  // sparse fragment: rows g, vectors {2t, 2t+1}, {2t+8, 2t+9}
+            if (s + 16 <= vend) {
+                const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;
+                if constexpr (VF32) {
+                    const float* fv = static_cast<const float*>(a.vals);
+                    const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
+                    b0 = f2_to_h2(__uint_as_float(x.x), __uint_as_float(x.y));
+                    b1 = f2_to_h2(__uint_as_float(y.x), __uint_as_float(y.y));
+                } else {
+                    const __half* hv = static_cast<const __half*>(a.vals);
+                    b0 = ld_stream_u32(hv + off);
+                    b1 = ld_stream_u32(hv + off + 64);
+                }
+            } else {
+                const uint32_t v0 = s + 2 * t;
+                b0 = (v0 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0, g) : 0u) |
+                     ((v0 + 1 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 1, g) : 0u) << 16);
+                b1 = (v0 + 8 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 8, g) : 0u) |
+                     ((v0 + 9 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 9, g) : 0u) << 16);
+            }
+#pragma unroll
+            for (int j = 0; j < NMMA; ++j) {
+                uint32_t e[4][2];  // [k slot][feature g / g + 8]
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        e[u][h] = ok[u] ? __ldg(Bl + static_cast<uint64_t>(col[u]) * a.ldb + 16 * j + 8 * h) : 0u;
+                mma_f16_16816(acc[j], e[0][0] | (e[1][0] << 16), e[0][1] | (e[1][1] << 16),
+                              e[2][0] | (e[3][0] << 16), e[2][1] | (e[3][1] << 16), b0, b1);
+            }
+        }
+
+        // accumulator (m = feature, n = window row): d0 (g, 2t), d1 (g, 2t+1), d2 (g+8, 2t), d3 (g+8, 2t+1)
+        const bool split = it.slot != kNoSlot;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const uint32_t r = 2 * t + rr;
+            const uint64_t row = 8ull * it.window + r;
+            float* dst;
+            int64_t lim;
+            if (split) {
+                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+                lim = a.ldp;
+            } else {
+                if (row >= a.rows) continue;
+                dst = a.C + row * a.ldc;
+                lim = a.N;
+            }
+#pragma unroll
+            for (int j = 0; j < NMMA; ++j) {
+                const int64_t f = feat0 + 16 * j + g;
+                if (f < lim) dst[f] = acc[j][rr];
+                if (f + 8 < lim) dst[f + 8] = acc[j][2 + rr];
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------- TF32 path
 //
 // Same scheme with m16n8k8.tf32: an 8-vector step; loader slot u (0, 1) of
@@ -551,7 +651,19 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         }
         SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
                    c, ldc, A->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>()};
-        if (plan->n_items && !launched) {
+        const bool direct_map = cfg->mapping == TCS_MAP_DIRECT && A->precision == TCS_FP16;
+        if (plan->n_items && !launched && direct_map) {  // ablation: the paper's direct thread mapping
+            const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
+            if (slab == 128)
+                vf32 ? launch(spmm_f16_direct_kernel<8, true>, a, slabs, s, "spmm_f16_direct<128,f32v>")
+                     : launch(spmm_f16_direct_kernel<8, false>, a, slabs, s, "spmm_f16_direct<128>");
+            else if (slab == 64)
+                vf32 ? launch(spmm_f16_direct_kernel<4, true>, a, slabs, s, "spmm_f16_direct<64,f32v>")
+                     : launch(spmm_f16_direct_kernel<4, false>, a, slabs, s, "spmm_f16_direct<64>");
+            else
+                vf32 ? launch(spmm_f16_direct_kernel<2, true>, a, slabs, s, "spmm_f16_direct<32,f32v>")
+                     : launch(spmm_f16_direct_kernel<2, false>, a, slabs, s, "spmm_f16_direct<32>");
+        } else if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
                 if (slab == 128)

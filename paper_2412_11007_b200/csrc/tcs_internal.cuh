@@ -124,7 +124,8 @@ void free_plan(Plan* p, cudaStream_t s);
 void pad_convert(const void* src, tcs_dtype sdt, int64_t lds, void* dst, tcs_dtype ddt, int64_t ldd,
                  int64_t rows, int64_t cols, int64_t cols_pad, cudaStream_t s);
 
-void check_mebcrs(const tcs_mebcrs* m);
+// vector height 8 only unless any_height (8 or 16: the 16x1 baseline layout).
+void check_mebcrs(const tcs_mebcrs* m, bool any_height = false);
 
 // TMA-gather + tcgen05 SpMM (spmm_tc05.cu); false = not applicable, nothing launched.
 bool spmm_tc05(const tcs_mebcrs* A, const Plan* plan, const __half* B, int64_t ldb, int64_t b_rows, int64_t n,

@@ -142,10 +142,10 @@ class MeBcrsMatrix:
 
         rp = np.empty(self.num_windows + 1, np.uint32)
         ci = np.empty(max(1, self.num_vectors), np.uint32)
-        v = np.empty(max(1, 8 * self.num_vectors), np.float32)
+        v = np.empty(max(1, self.vector_height * self.num_vectors), np.float32)
         _check(_abi.load().tcs_mebcrs_download(C.byref(self._h), rp.ctypes.data, ci.ctypes.data, v.ctypes.data,
                                                _stream()))
-        return rp, ci[: self.num_vectors], v[: 8 * self.num_vectors]
+        return rp, ci[: self.num_vectors], v[: self.vector_height * self.num_vectors]
 
     def validate(self):
         _check(_abi.load().tcs_mebcrs_validate(C.byref(self._h), _stream()))
@@ -174,13 +174,21 @@ class MeBcrsMatrix:
         return MeBcrsMatrix(h)
 
 
-def encode_mebcrs(csr: CsrMatrix, precision: Precision, value_dtype: int | None = None) -> MeBcrsMatrix:
-    """ref mebcrs.hpp:80.  value_dtype: TCS_DTYPE_F16 (default for fp16) or TCS_DTYPE_F32."""
+def encode_mebcrs(csr: CsrMatrix, precision: Precision, value_dtype: int | None = None,
+                  vector_height: int = 8) -> MeBcrsMatrix:
+    """ref mebcrs.hpp:80.  value_dtype: TCS_DTYPE_F16 (default for fp16) or TCS_DTYPE_F32.
+    vector_height 16 builds the 16-row-window layout of the 16x1 baseline
+    (ref partition.hpp:40-66 with vector_height 16; for spmm_baseline16)."""
     if value_dtype is None:
         value_dtype = _abi.TCS_DTYPE_F16 if int(precision) == 0 else _abi.TCS_DTYPE_F32
     c = csr._c()
     h = _abi.tcs_mebcrs()
-    _check(_abi.load().tcs_mebcrs_encode(C.byref(c), int(precision), int(value_dtype), C.byref(h), _stream()))
+    lib = _abi.load()
+    if vector_height == 8:
+        _check(lib.tcs_mebcrs_encode(C.byref(c), int(precision), int(value_dtype), C.byref(h), _stream()))
+    else:
+        _check(lib.tcs_mebcrs_encode_v(C.byref(c), int(precision), int(value_dtype), int(vector_height), C.byref(h),
+                                       _stream()))
     return MeBcrsMatrix(h)
 
 
@@ -211,6 +219,25 @@ def spmm(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = KernelCo
     _check(_abi.load().tcs_spmm(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
                                 dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()), C.byref(cnt),
                                 _stream()))
+    return SpmmResult(out, KernelCounters._from(cnt))
+
+
+def spmm_baseline16(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig | None = None,
+                    out: torch.Tensor | None = None) -> SpmmResult:
+    """ref spmm.hpp:187-257 (the non-swapped 16x1 ablation).  ``sparse`` is a
+    vector_height-16 encoding (encode_mebcrs(..., vector_height=16)); cfg
+    defaults to the matrix precision with vector_height 16."""
+    if cfg is None:
+        cfg = KernelConfig(sparse.precision, vector_height=16)
+    if dense.dim() != 2 or dense.stride(1) != 1:
+        dense = dense.contiguous()
+    m, n = sparse.rows, dense.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    cnt = _abi.tcs_counters()
+    _check(_abi.load().tcs_spmm_baseline16(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
+                                           dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
+                                           C.byref(cnt), _stream()))
     return SpmmResult(out, KernelCounters._from(cnt))
 
 

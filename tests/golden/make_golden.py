@@ -44,6 +44,11 @@ def record(case: cases.Case) -> dict:
         if case.B is not None:
             Cm, cnt = R.spmm(me, case.B)
             rec[f"spmm_{tag}"] = {"sha": cases.sha(Cm), "mma": cnt}
+            # 16x1 ablation (inc/spmm.hpp:187-257) on the 16-row partition (inc/partition.hpp:40-66)
+            prp, pci = R.partition_windows(m, 16, O.K_OF[p])
+            C16, cnt16 = R.spmm_baseline16(m, case.B, p)
+            rec[f"b16_{tag}"] = {"nv": int(pci.shape[0]), "part_sha": cases.sha(prp, pci), "sha": cases.sha(C16),
+                                 "mma": cnt16}
         if case.A is not None:
             out, cnt = R.sddmm(me, case.A, case.Bt)
             rec[f"sddmm_{tag}"] = {"sha": cases.sha(out), "mma": cnt}

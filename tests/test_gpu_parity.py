@@ -39,7 +39,7 @@ def rel_l2(got, want):
     return np.linalg.norm(got - want) / (den if den else 1.0)
 
 
-def check_case(case, rec, value_dtype, path="auto"):
+def check_case(case, rec, value_dtype, path="auto", mapping=None):
     for p in case.precisions:
         if p == 1 and value_dtype == F16:
             continue
@@ -55,6 +55,8 @@ def check_case(case, rec, value_dtype, path="auto"):
             assert np.array_equal(v.view(np.uint32), O.round_array(ref_me.values, 0).view(np.uint32)), case.name
         cfg = T.KernelConfig(T.Precision(p))
         scfg = T.KernelConfig(T.Precision(p), path=path if (p == 0 and value_dtype == F16) else "auto")
+        if mapping is not None:
+            scfg.mapping = mapping
         if case.B is not None:
             for dense in ([torch.from_numpy(case.B).cuda()] +
                           ([torch.from_numpy(case.B).cuda().half()] if p == 0 else [])):
@@ -98,6 +100,18 @@ def test_spmm_instruction_paths_bit_exact(golden, path):
     for case in cases.kat_cases():
         check_case(case, golden["cases"][case.name], F16, path)
     check_case(cases.c1_case(False), golden["cases"]["c1"], F16, path)
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_direct_mapping_replay(golden, value_dtype):
+    """ThreadMapping::direct runs the direct-mapping ablation kernel (FP16);
+    results must equal the reference's, exactly as for coalesced
+    (ref tests/acceptance.cpp:103-104)."""
+    params = cases.acceptance2_params()
+    for i in range(1, 200, 3):
+        check_case(cases.acceptance2_case(i, params), golden["cases"][f"acc2_{i:03d}"], value_dtype,
+                   mapping=T.ThreadMapping.direct)
+    check_case(cases.c1_case(False), golden["cases"]["c1"], value_dtype, mapping=T.ThreadMapping.direct)
 
 
 def test_acceptance6_replay(golden):
@@ -192,3 +206,54 @@ def test_reference_error_taxonomy():
                       torch.tensor([3, 1], dtype=torch.int32, device="cuda"), torch.ones(2, device="cuda"))
     with pytest.raises(T.FormatError):
         T.encode_mebcrs(bad, T.Precision.fp16)
+
+
+def check_baseline16(case, rec, value_dtype):
+    """16x1 non-swapped ablation (ref spmm.hpp:187-257) on the 16-row-window
+    layout: partition bit-exact with ref partition_windows(m, 16, k), values
+    laid out like the 8-row format, output and counters == the reference's
+    spmm_baseline16 (golden hashes)."""
+    for p in case.precisions:
+        if p == 1 and value_dtype == F16:
+            continue
+        tag = "fp16" if p == 0 else "tf32"
+        r16 = rec[f"b16_{tag}"]
+        m16 = T.encode_mebcrs(dev_csr(case.csr), T.Precision(p), value_dtype, vector_height=16)
+        rp, ci, v = m16.to_host()
+        assert cases.sha(rp, ci) == r16["part_sha"], case.name
+        ref16 = O.encode_mebcrs(case.csr, p, vector_height=16)  # pinned by test_oracle.py
+        want_v = ref16.values if value_dtype == F32 else O.round_array(ref16.values, 0)
+        assert np.array_equal(v.view(np.uint32), want_v.view(np.uint32)), case.name
+        for dense in ([torch.from_numpy(case.B).cuda()] + ([torch.from_numpy(case.B).cuda().half()] if p == 0 else [])):
+            res = T.spmm_baseline16(m16, dense)
+            assert cases.sha(res.output.cpu().numpy()) == r16["sha"], (case.name, dense.dtype)
+            assert res.counters.mma_invocations == r16["mma"]
+        m16.free()
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_baseline16_matches_reference(golden, value_dtype):
+    params = cases.acceptance2_params()
+    todo = [c for c in cases.kat_cases() if c.B is not None]
+    todo += [cases.acceptance2_case(i, params) for i in range(0, 200, 2)]
+    todo += [cases.c1_case(False)]
+    for c in todo:
+        check_baseline16(c, golden["cases"][c.name], value_dtype)
+
+
+def test_baseline16_errors():
+    """ref spmm.hpp:190-191: the baseline needs vector height 16."""
+    m = O.generate_random_sparse(40, 24, 0.2, 3)
+    m16 = T.encode_mebcrs(dev_csr(m), T.Precision.fp16, vector_height=16)
+    m8 = T.encode_mebcrs(dev_csr(m), T.Precision.fp16)
+    B = torch.ones(24, 16, device="cuda")
+    with pytest.raises(T.ArgumentError):
+        T.spmm_baseline16(m16, B, T.KernelConfig(T.Precision.fp16, vector_height=8))
+    with pytest.raises(T.ArgumentError):
+        T.spmm_baseline16(m8, B, T.KernelConfig(T.Precision.fp16, vector_height=16))
+    with pytest.raises(T.ArgumentError):  # a 16-high handle is not a swap8 operand
+        T.spmm(m16, B, T.KernelConfig(T.Precision.fp16))
+    with pytest.raises(T.ShapeError):
+        T.spmm_baseline16(m16, torch.ones(23, 16, device="cuda"))
+    with pytest.raises(T.ArgumentError):
+        T.encode_mebcrs(dev_csr(m), T.Precision.fp16, vector_height=4)

@@ -197,3 +197,39 @@ def test_host_entry_points_match_device_path():
                                 ref.values.ctypes.data, A.ctypes.data, 300, 20, Bt.ctypes.data, 200, 20,
                                 out.ctypes.data, C.byref(cfg), None, None)
         assert rc == 0 and np.array_equal(out.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32))
+
+
+@pytest.mark.parametrize("p", [0, 1])
+@pytest.mark.parametrize("n", [128, 64, 32, 200])
+def test_hub_windows_baseline16_bit_exact(p, n):
+    """16x1 ablation on hub windows (split segments + ordered reduction)."""
+    m = hub_matrix()
+    ref = O.encode_mebcrs(m, p, vector_height=16)
+    m16 = T.encode_mebcrs(dev(m), T.Precision(p), 1, vector_height=16)
+    rp, ci, v = m16.to_host()
+    assert np.array_equal(rp, ref.row_pointers) and np.array_equal(ci, ref.column_indices)
+    assert np.array_equal(v.view(np.uint32), ref.values.view(np.uint32))
+    B = O.generate_random_dense(m.cols, n, 5)
+    want = O.spmm(ref, B)
+    got = T.spmm_baseline16(m16, torch.from_numpy(B).cuda()).output.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if p == 0:
+        m16h = T.encode_mebcrs(dev(m), T.Precision(p), 0, vector_height=16)
+        got = T.spmm_baseline16(m16h, torch.from_numpy(B).cuda().half()).output.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [128, 64, 32, 200])
+@pytest.mark.parametrize("vdt", [0, 1])
+def test_direct_mapping_bit_identical(n, vdt):
+    """ThreadMapping::direct (the paper's ablation kernel) == coalesced, bit
+    for bit (ref tests/acceptance.cpp:103-104), incl. split hub windows."""
+    m = hub_matrix()
+    ref = O.encode_mebcrs(m, 0)
+    me = T.encode_mebcrs(dev(m), T.Precision.fp16, vdt)
+    B = O.generate_random_dense(m.cols, n, 9)
+    want = O.spmm(ref, B)
+    for dense in (torch.from_numpy(B).cuda(), torch.from_numpy(B).cuda().half()):
+        cfg = T.KernelConfig(T.Precision.fp16, mapping=T.ThreadMapping.direct)
+        got = T.spmm(me, dense, cfg).output.cpu().numpy()
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))

@@ -61,6 +61,13 @@ def check_case(case, rec):
         if case.B is not None:
             assert cases.sha(O.spmm(me, case.B)) == rec[f"spmm_{tag}"]["sha"]
             assert O.count_mma_spmm(me, case.B.shape[1]) == rec[f"spmm_{tag}"]["mma"]
+            m16 = O.encode_mebcrs(m, p, vector_height=16)
+            assert m16.nv == rec[f"b16_{tag}"]["nv"]
+            assert cases.sha(m16.row_pointers, m16.column_indices) == rec[f"b16_{tag}"]["part_sha"]
+            assert cases.sha(O.spmm(m16, case.B)) == rec[f"b16_{tag}"]["sha"]
+            blocks = int(sum((int(m16.row_pointers[w + 1] - m16.row_pointers[w]) + m16.k - 1) // m16.k
+                             for w in range(m16.num_windows)))
+            assert blocks * ((case.B.shape[1] + 7) // 8) == rec[f"b16_{tag}"]["mma"]
         if case.A is not None:
             out = O.sddmm(me, case.A, case.Bt)
             assert cases.sha(out) == rec[f"sddmm_{tag}"]["sha"]
