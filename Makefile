@@ -9,10 +9,18 @@ PKG     := paper_2412_11007_b200
 SRCS    := $(wildcard $(PKG)/csrc/*.cu)
 OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 LIB     := $(PKG)/libtcsparse_b200.so
+CLI     := $(PKG)/tcsparse-b200
 
-all: lib oracle
+all: lib cli oracle
 
 lib: $(LIB)
+
+# The reference CLI (ref tools/tcsparse.cpp) on the B200 library.
+cli: $(CLI)
+
+$(CLI): $(PKG)/cli/tcsparse_b200.cpp include/tcs/tcs.h $(LIB)
+	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -ltcsparse_b200 \
+	    -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -lpthread -Wl,-rpath,'$$ORIGIN'
 
 build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/tcs_internal.cuh include/tcs/tcs.h
 	@mkdir -p build
@@ -25,7 +33,7 @@ oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib cli oracle clean

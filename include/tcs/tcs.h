@@ -40,7 +40,10 @@ typedef enum tcs_status {
     TCS_ERR_FORMAT = 3,   /* ref FormatError: ME-BCRS / CSR invariants violated         */
     TCS_ERR_CUDA = 4,     /* CUDA runtime error (no device, launch failure, ...)        */
     TCS_ERR_NCCL = 5,     /* reserved for the multi-GPU layer                           */
-    TCS_ERR_OOM = 6       /* device allocation failed                                   */
+    TCS_ERR_OOM = 6,      /* device allocation failed                                   */
+    TCS_ERR_PARSE = 7,    /* ref ParseError (errors.hpp:11-22): malformed MatrixMarket;
+                             the message carries "line N: " as the reference's          */
+    TCS_ERR_IO = 8        /* a container / output file cannot be opened or written      */
 } tcs_status;
 
 /* ref: precision.hpp:13 (Precision{fp16=0, tf32=1}). */
@@ -113,11 +116,15 @@ typedef struct tcs_kernel_config {
  * values, N <= 256; ARGUMENT error otherwise). */
 #define TCS_CFG_PATH_MMA_SYNC 0x1u
 #define TCS_CFG_PATH_TCGEN05 0x2u
+/* Also fill counters->transactions / transaction_bytes / useful_bytes with
+ * the reference's access model (tcs_mebcrs_cost, one extra kernel). */
+#define TCS_CFG_COUNT_ACCESS 0x4u
 
 /* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
  * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);
- * the transaction fields belong to the reference's analytic cost model and
- * are left 0 (coalescing is measured with ncu instead). */
+ * the transaction fields belong to the reference's analytic cost model:
+ * 0 unless cfg->flags has TCS_CFG_COUNT_ACCESS (real coalescing is measured
+ * with ncu). */
 typedef struct tcs_counters {
     uint64_t mma_invocations;
     uint64_t transactions;
@@ -196,6 +203,28 @@ tcs_status tcs_spmm_baseline16(const tcs_mebcrs* a, const void* b, tcs_dtype b_d
                                int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
                                tcs_counters* counters, tcs_stream_t stream);
 
+/* ------------------------------------------------------------ cost model */
+/* ref analysis.hpp:34-131 + footprint.hpp:13-25: the structural cost of one
+ * SpMM over `m` with n_cols dense columns -- swapped 8x1 strategy for a
+ * vector-height-8 handle, the 16x1 baseline for a vector-height-16 one --
+ * evaluated on the GPU (the dense-operand gather of the reference's warp
+ * model replayed per block and tile, 32-byte segments merged into aligned
+ * 64/128-byte transactions).  nnz = the source CSR's entry count. */
+typedef struct tcs_cost {
+    uint64_t mma_count;              /* ref count_mma                                  */
+    uint64_t zero_fill;              /* ref count_zero_fill: vh * nv - nnz             */
+    uint64_t access_bytes;           /* ref data_access_cost(...).total()              */
+    uint64_t transactions;           /* ref count_spmm_transactions (tiles 0,1 extrapolated) */
+    uint64_t exec_transactions;      /* summed over all tiles == the executing kernel's */
+    uint64_t exec_transaction_bytes; /*   KernelCounters (ref spmm.hpp:146-151, :236-240) */
+    uint64_t exec_useful_bytes;
+    uint64_t footprint_me;           /* ref footprint_me_bytes                          */
+    uint64_t footprint_sr;           /* ref footprint_sr_bytes                          */
+    uint64_t padded_vectors;         /* ref WindowPartition::padded_vectors             */
+} tcs_cost;
+tcs_status tcs_mebcrs_cost(const tcs_mebcrs* m, uint64_t nnz, int64_t n_cols, tcs_mapping mapping, tcs_cost* out,
+                           tcs_stream_t stream);
+
 /* ------------------------------------------------------------------ SDDMM */
 /* ref: sddmm(const SddmmOperands&, const KernelConfig&)  (sddmm.hpp:84).
  * out.values[pos] = sum_l A[i][l] * Bt[j][l] at every mask position whose
@@ -240,6 +269,38 @@ tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtyp
  * from one read of the f32 rows h [rows][ldh].  hn or hc may be NULL. */
 tcs_status tcs_rows_normalize(const float* h, int64_t rows, int64_t f, int64_t ldh, void* hn, void* hc, int64_t ldo,
                               tcs_dtype out_dtype, float eps, tcs_stream_t stream);
+
+/* ------------------------------------------------------ ingest / containers */
+/* ref: parse_matrix_market (matrix_market.hpp:28-94) -- coordinate
+ * real/integer/pattern, general/symmetric (expanded), pattern -> 1.0,
+ * duplicates summed (csr_from_coords, matrix.hpp:96-128).  The text is
+ * tokenised by all host cores; the coordinate -> CSR assembly (sort, run
+ * sums, row pointers) runs on the GPU.  `out` receives library-allocated
+ * HOST arrays (release with tcs_csr_free_host).  Malformed input ->
+ * TCS_ERR_PARSE with the reference's message and line number. */
+tcs_status tcs_matrix_market_parse(const char* text, uint64_t len, tcs_csr* out, tcs_stream_t stream);
+/* As above from a file; an unreadable file -> TCS_ERR_PARSE "cannot open '<path>'"
+ * (ref cli.hpp:34-38). */
+tcs_status tcs_matrix_market_read(const char* path, tcs_csr* out, tcs_stream_t stream);
+/* ref write_matrix_market (matrix_market.hpp:97-104), host CSR. */
+tcs_status tcs_matrix_market_write(const char* path, const tcs_csr* host_csr);
+tcs_status tcs_csr_free_host(tcs_csr* m);
+/* ref csr_from_coords (matrix.hpp:96-128) on the device: n DEVICE
+ * coordinates (0-based, in range) -> device CSR with library-allocated
+ * arrays (release with tcs_csr_free).  Duplicates are summed in input order. */
+tcs_status tcs_coo_to_csr(uint64_t rows, uint64_t cols, uint64_t n, const uint32_t* row, const uint32_t* col,
+                          const float* values, tcs_csr* out, tcs_stream_t stream);
+tcs_status tcs_csr_free(tcs_csr* m, tcs_stream_t stream);
+/* ref write_mebcrs / read_mebcrs (container_io.hpp:56-91): the MEBC v1
+ * container ("MEBC", u32 version, u64 rows, u64 cols, u32 vector_height,
+ * u32 k, u8 precision, then u32-length-prefixed row_pointers, column_indices
+ * and f32 values; little endian).  Write downloads the handle (binary16
+ * values are widened, so a file is byte-identical to the reference's only
+ * for F32-valued handles or fp16-representable values).  Read validates like
+ * the reference (FORMAT errors with its messages) and returns a device handle
+ * with F32 values, prepared.  Unopenable files -> TCS_ERR_IO. */
+tcs_status tcs_mebcrs_write(const char* path, const tcs_mebcrs* m, tcs_stream_t stream);
+tcs_status tcs_mebcrs_read(const char* path, tcs_mebcrs* out, tcs_stream_t stream);
 
 /* ------------------------------------------------- host-buffer entry points */
 /* Value semantics of the reference API: host arrays in, host arrays out.  */

@@ -118,6 +118,16 @@ def ref():
         _ref.ref_spmm_baseline16.restype = C.c_int
         _ref.ref_spmm_baseline16.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, _f32p, C.c_uint64,
                                              C.c_uint64, C.c_int, C.c_uint64, _f32p, _u64p]
+        _ref.ref_cli.restype = C.c_int
+        _ref.ref_cli.argtypes = [C.c_int, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int, C.c_int, _u64p, C.c_int,
+                                 C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p),
+                                 C.POINTER(C.c_void_p)]
+        _ref.ref_parse_matrix_market.restype = C.c_int64
+        _ref.ref_parse_matrix_market.argtypes = [C.c_char_p, C.c_uint64, _u64p, _u64p, C.POINTER(_u32p),
+                                                 C.POINTER(_u32p), C.POINTER(_f32p), C.POINTER(C.c_void_p)]
+        _ref.ref_read_mebcrs.restype = C.c_int64
+        _ref.ref_read_mebcrs.argtypes = [C.c_char_p, _u64p, _u64p, C.POINTER(C.c_int), C.POINTER(_u32p),
+                                         C.POINTER(_u32p), C.POINTER(_f32p), C.POINTER(C.c_void_p)]
         _ref.ref_sddmm_output_offsets.restype = C.c_uint64
         _ref.ref_sddmm_output_offsets.argtypes = [C.c_uint64, C.c_int]
         _ref.ref_free.argtypes = [C.c_void_p]
@@ -396,6 +406,54 @@ class Ref:
         if rc:
             raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
         return Cm, int(cnt.value)
+
+    @staticmethod
+    def _str(ptr):
+        if not ptr:
+            return None
+        out = C.cast(ptr, C.c_char_p).value.decode()
+        ref().ref_free(ptr)
+        return out
+
+    @staticmethod
+    def cli(cmd, input="", dir="", output="", precision=0, mapping=1, n=(), vector_height=8, seed=1,
+            verify=False, real=False, json=False):
+        """The reference CLI (inc/cli.hpp run_convert/spmm/sddmm/stats/bench):
+        returns (exit code, stdout text, stderr text)."""
+        code = {"convert": 0, "spmm": 1, "sddmm": 2, "stats": 3, "bench": 4}[cmd]
+        ns = np.ascontiguousarray(list(n) or [0], np.uint64)
+        o, e = C.c_void_p(), C.c_void_p()
+        rc = ref().ref_cli(code, str(input).encode(), str(dir).encode(), str(output).encode(), precision, mapping,
+                           _p(ns, _u64p), len(n), vector_height, seed, int(verify), int(real), int(json),
+                           C.byref(o), C.byref(e))
+        return rc, Ref._str(o.value), Ref._str(e.value)
+
+    @staticmethod
+    def parse_matrix_market(text):
+        """Csr, or raises ValueError(ParseError message)."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        r = ref()
+        rows, cols = C.c_uint64(), C.c_uint64()
+        rp, ci, v, err = _u32p(), _u32p(), _f32p(), C.c_void_p()
+        nnz = r.ref_parse_matrix_market(b, len(b), C.byref(rows), C.byref(cols), C.byref(rp), C.byref(ci),
+                                        C.byref(v), C.byref(err))
+        if nnz < 0:
+            raise ValueError(Ref._str(err.value))
+        return Csr(rows.value, cols.value, _take(r, rp, rows.value + 1, np.uint32), _take(r, ci, nnz, np.uint32),
+                   _take(r, v, nnz, np.float32))
+
+    @staticmethod
+    def read_mebcrs(path):
+        r = ref()
+        rows, cols, prec = C.c_uint64(), C.c_uint64(), C.c_int()
+        rp, ci, v, err = _u32p(), _u32p(), _f32p(), C.c_void_p()
+        nv = r.ref_read_mebcrs(str(path).encode(), C.byref(rows), C.byref(cols), C.byref(prec), C.byref(rp),
+                               C.byref(ci), C.byref(v), C.byref(err))
+        if nv < 0:
+            raise ValueError(Ref._str(err.value))
+        W = (rows.value + 7) // 8
+        return MeBcrs(rows.value, cols.value, prec.value, _take(r, rp, W + 1, np.uint32), _take(r, ci, nv, np.uint32),
+                      _take(r, v, 8 * nv, np.float32))
 
     @staticmethod
     def sddmm_output_offsets(lane, kind):

@@ -14,6 +14,10 @@
 #include <exception>
 #include <vector>
 
+#include <sstream>
+#include <string>
+
+#include "tcsparse/cli.hpp"
 #include "tcsparse/tcsparse.hpp"
 
 using namespace tcsparse;
@@ -204,6 +208,131 @@ int ref_spmm_baseline16(uint64_t rows, uint64_t cols, const uint32_t* rp, const 
         return 2;
     } catch (const std::exception&) {
         return 3;
+    }
+}
+
+// ---- the reference CLI (inc/cli.hpp:104-358), stdout/stderr captured ----
+static char* dup_str(const std::string& x) {
+    char* p = static_cast<char*>(std::malloc(x.size() + 1));
+    std::memcpy(p, x.c_str(), x.size() + 1);
+    return p;
+}
+
+// cmd: 0 convert, 1 spmm, 2 sddmm, 3 stats, 4 bench.  n_list has n_count
+// entries (spmm/sddmm/bench use the last).  Returns the exit code.
+int ref_cli(int cmd, const char* input, const char* dir, const char* output, int precision, int mapping,
+            const uint64_t* n_list, int n_count, uint64_t vector_height, uint64_t seed, int verify, int real,
+            int json, char** out_text, char** err_text) {
+    std::ostringstream out, err;
+    int rc = -1;
+    try {
+        const Precision p = static_cast<Precision>(precision);
+        const ThreadMapping m = mapping == 0 ? ThreadMapping::direct : ThreadMapping::coalesced;
+        std::vector<std::size_t> ns(n_list, n_list + n_count);
+        switch (cmd) {
+            case 0: {
+                cli::ConvertOptions o;
+                o.input = input;
+                o.output = output;
+                o.precision = p;
+                rc = cli::run_convert(o, out, err);
+                break;
+            }
+            case 1: {
+                cli::SpmmOptions o;
+                o.input = input;
+                if (!ns.empty()) o.n = ns.back();
+                o.precision = p;
+                o.vector_height = vector_height;
+                o.mapping = m;
+                o.seed = seed;
+                o.verify = verify;
+                o.real_values = real;
+                rc = cli::run_spmm(o, out, err);
+                break;
+            }
+            case 2: {
+                cli::SddmmOptions o;
+                o.input = input;
+                if (!ns.empty()) o.n = ns.back();
+                o.precision = p;
+                o.seed = seed;
+                o.verify = verify;
+                o.real_values = real;
+                o.output = output;
+                rc = cli::run_sddmm(o, out, err);
+                break;
+            }
+            case 3: {
+                cli::StatsOptions o;
+                o.input = input;
+                o.dir = dir;
+                if (!ns.empty()) o.n_list = ns;
+                o.mapping = m;
+                o.format = json ? ReportFormat::json : ReportFormat::csv;
+                o.output = output;
+                rc = cli::run_stats(o, out, err);
+                break;
+            }
+            case 4: {
+                cli::BenchOptions o;
+                o.input = input;
+                o.dir = dir;
+                if (!ns.empty()) o.n = ns.back();
+                o.seed = seed;
+                o.mapping = m;
+                o.output = output;
+                rc = cli::run_bench(o, out, err);
+                break;
+            }
+        }
+    } catch (const std::exception& e) {
+        err << "exception: " << e.what() << "\n";
+        rc = -2;
+    }
+    *out_text = dup_str(out.str());
+    *err_text = dup_str(err.str());
+    return rc;
+}
+
+// parse_matrix_market (inc/matrix_market.hpp:28-94) of an in-memory text.
+// Returns nnz, or -1 with *err_text = the ParseError message.
+int64_t ref_parse_matrix_market(const char* text, uint64_t len, uint64_t* rows, uint64_t* cols, uint32_t** rp,
+                                uint32_t** ci, float** vals, char** err_text) {
+    *err_text = nullptr;
+    try {
+        std::istringstream in(std::string(text, len));
+        const CsrMatrix m = parse_matrix_market(in);
+        *rows = m.rows;
+        *cols = m.cols;
+        *rp = dup(m.row_ptr);
+        *ci = dup(m.col_idx);
+        *vals = dup(m.values);
+        return static_cast<int64_t>(m.nnz());
+    } catch (const std::exception& e) {
+        *err_text = dup_str(e.what());
+        return -1;
+    }
+}
+
+// read_mebcrs (inc/container_io.hpp:70-91) of a file; returns nv or -1 with
+// the FormatError message.
+int64_t ref_read_mebcrs(const char* path, uint64_t* rows, uint64_t* cols, int* precision, uint32_t** rp,
+                        uint32_t** ci, float** vals, char** err_text) {
+    *err_text = nullptr;
+    try {
+        std::ifstream in(path, std::ios::binary);
+        const MeBcrsMatrix m = read_mebcrs(in);
+        *rows = m.rows;
+        *cols = m.cols;
+        *precision = static_cast<int>(m.precision);
+        *rp = dup(m.row_pointers);
+        *ci = dup(m.column_indices);
+        *vals = dup(m.values);
+        return static_cast<int64_t>(m.column_indices.size());
+    } catch (const std::exception& e) {
+        *err_text = dup_str(e.what());
+        return -1;
     }
 }
 

@@ -13,7 +13,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # TCS_LIB_PATH: load an experimental build instead (tools/build_variant.sh)
 LIB_PATH = os.environ.get("TCS_LIB_PATH") or os.path.join(_HERE, "libtcsparse_b200.so")
 
-TCS_OK, TCS_ERR_ARGUMENT, TCS_ERR_SHAPE, TCS_ERR_FORMAT, TCS_ERR_CUDA, TCS_ERR_NCCL, TCS_ERR_OOM = range(7)
+(TCS_OK, TCS_ERR_ARGUMENT, TCS_ERR_SHAPE, TCS_ERR_FORMAT, TCS_ERR_CUDA, TCS_ERR_NCCL, TCS_ERR_OOM, TCS_ERR_PARSE,
+ TCS_ERR_IO) = range(9)
+TCS_MAP_DIRECT, TCS_MAP_COALESCED = 0, 1
+TCS_CFG_COUNT_ACCESS = 0x4
 TCS_FP16, TCS_TF32 = 0, 1
 TCS_DTYPE_F16, TCS_DTYPE_F32 = 0, 1
 TCS_MEBCRS_OWN_STRUCTURE, TCS_MEBCRS_OWN_VALUES = 1, 2
@@ -46,6 +49,12 @@ class tcs_counters(C.Structure):
                 ("transaction_bytes", C.c_uint64), ("useful_bytes", C.c_uint64)]
 
 
+class tcs_cost(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("mma_count", "zero_fill", "access_bytes", "transactions",
+                                          "exec_transactions", "exec_transaction_bytes", "exec_useful_bytes",
+                                          "footprint_me", "footprint_sr", "padded_vectors")]
+
+
 EXPORTS = {
     # name: (restype, argtypes)
     "tcs_version": (C.c_char_p, []),
@@ -58,6 +67,17 @@ EXPORTS = {
     "tcs_spmm_baseline16": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                       C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
                                       C.c_void_p]),
+    "tcs_mebcrs_cost": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_uint64, C.c_int64, C.c_int, C.POINTER(tcs_cost),
+                                  C.c_void_p]),
+    "tcs_matrix_market_parse": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(tcs_csr), C.c_void_p]),
+    "tcs_matrix_market_read": (C.c_int, [C.c_char_p, C.POINTER(tcs_csr), C.c_void_p]),
+    "tcs_matrix_market_write": (C.c_int, [C.c_char_p, C.POINTER(tcs_csr)]),
+    "tcs_csr_free_host": (C.c_int, [C.POINTER(tcs_csr)]),
+    "tcs_coo_to_csr": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.POINTER(tcs_csr), C.c_void_p]),
+    "tcs_csr_free": (C.c_int, [C.POINTER(tcs_csr), C.c_void_p]),
+    "tcs_mebcrs_write": (C.c_int, [C.c_char_p, C.POINTER(tcs_mebcrs), C.c_void_p]),
+    "tcs_mebcrs_read": (C.c_int, [C.c_char_p, C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_prepare": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_validate": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_free": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),

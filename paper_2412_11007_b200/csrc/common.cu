@@ -290,6 +290,39 @@ void check_mebcrs(const tcs_mebcrs* m, bool any_height) {
     if (m->num_vectors && (!m->column_indices || !m->values)) fail(TCS_ERR_ARGUMENT, "null ME-BCRS arrays");
 }
 
+void upload_mebcrs(uint64_t rows, uint64_t cols, tcs_precision precision, uint32_t vh, const uint32_t* row_pointers,
+                   const uint32_t* column_indices, const float* values, tcs_mebcrs* out, cudaStream_t s) {
+    if (!out || !row_pointers) fail(TCS_ERR_ARGUMENT, "null argument");
+    if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
+    if (vh != 8 && vh != 16) fail(TCS_ERR_ARGUMENT, "vector height must be 8 or 16");
+    tcs_mebcrs m{};
+    m.rows = rows;
+    m.cols = cols;
+    m.vector_height = vh;
+    m.k = precision == TCS_FP16 ? 8 : 4;
+    m.precision = precision;
+    m.value_dtype = TCS_DTYPE_F32;
+    m.num_windows = (rows + vh - 1) / vh;
+    m.num_vectors = row_pointers[m.num_windows];
+    m.row_pointers = static_cast<uint32_t*>(dalloc((m.num_windows + 1) * 4, s));
+    m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, m.num_vectors) * 4, s));
+    m.values = dalloc(std::max<uint64_t>(1, uint64_t(vh) * m.num_vectors) * 4, s);
+    m.flags = TCS_MEBCRS_OWN_STRUCTURE | TCS_MEBCRS_OWN_VALUES;
+    TCS_CUDA(cudaMemcpyAsync(m.row_pointers, row_pointers, (m.num_windows + 1) * 4, cudaMemcpyHostToDevice, s));
+    if (m.num_vectors) {
+        TCS_CUDA(cudaMemcpyAsync(m.column_indices, column_indices, m.num_vectors * 4, cudaMemcpyHostToDevice, s));
+        TCS_CUDA(cudaMemcpyAsync(m.values, values, uint64_t(vh) * m.num_vectors * 4, cudaMemcpyHostToDevice, s));
+    }
+    *out = m;
+    const tcs_stream_t ts = reinterpret_cast<tcs_stream_t>(s);
+    tcs_status rc = tcs_mebcrs_prepare(out, ts);
+    if (rc != TCS_OK) {
+        std::string msg = tcs_last_error();
+        tcs_mebcrs_free(out, ts);
+        fail(rc, msg);
+    }
+}
+
 }  // namespace tcs
 
 // ===================================================================== ABI
@@ -371,34 +404,7 @@ tcs_status tcs_mebcrs_upload(uint64_t rows, uint64_t cols, tcs_precision precisi
                              const uint32_t* column_indices, const float* values, tcs_mebcrs* out,
                              tcs_stream_t stream) {
     return guard([&] {
-        if (!out || !row_pointers) fail(TCS_ERR_ARGUMENT, "null argument");
-        if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
-        cudaStream_t s = st(stream);
-        tcs_mebcrs m{};
-        m.rows = rows;
-        m.cols = cols;
-        m.vector_height = 8;
-        m.k = precision == TCS_FP16 ? 8 : 4;
-        m.precision = precision;
-        m.value_dtype = TCS_DTYPE_F32;
-        m.num_windows = (rows + 7) / 8;
-        m.num_vectors = row_pointers[m.num_windows];
-        m.row_pointers = static_cast<uint32_t*>(dalloc((m.num_windows + 1) * 4, s));
-        m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, m.num_vectors) * 4, s));
-        m.values = dalloc(std::max<uint64_t>(1, 8 * m.num_vectors) * 4, s);
-        m.flags = TCS_MEBCRS_OWN_STRUCTURE | TCS_MEBCRS_OWN_VALUES;
-        TCS_CUDA(cudaMemcpyAsync(m.row_pointers, row_pointers, (m.num_windows + 1) * 4, cudaMemcpyHostToDevice, s));
-        if (m.num_vectors) {
-            TCS_CUDA(cudaMemcpyAsync(m.column_indices, column_indices, m.num_vectors * 4, cudaMemcpyHostToDevice, s));
-            TCS_CUDA(cudaMemcpyAsync(m.values, values, 8 * m.num_vectors * 4, cudaMemcpyHostToDevice, s));
-        }
-        *out = m;
-        tcs_status rc = tcs_mebcrs_prepare(out, stream);
-        if (rc != TCS_OK) {
-            std::string msg = tcs_last_error();
-            tcs_mebcrs_free(out, stream);
-            fail(rc, msg);
-        }
+        upload_mebcrs(rows, cols, precision, 8, row_pointers, column_indices, values, out, st(stream));
     });
 }
 

@@ -688,6 +688,13 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
             TCS_LAUNCHED("spmm_reduce_split");
         }
         if (counters) counters->mma_invocations = A->num_blocks * ((n + 15) / 16);  // ref analysis.hpp:34-38
+        if (counters && (cfg->flags & TCS_CFG_COUNT_ACCESS)) {
+            tcs_cost cost{};
+            mebcrs_cost(A, 0, n, cfg->mapping, &cost, s);
+            counters->transactions = cost.exec_transactions;
+            counters->transaction_bytes = cost.exec_transaction_bytes;
+            counters->useful_bytes = cost.exec_useful_bytes;
+        }
     });
 }
 

@@ -435,5 +435,12 @@ extern "C" tcs_status tcs_spmm_baseline16(const tcs_mebcrs* A, const void* b, tc
         }
         // ref analysis.hpp:34-38 with Strategy::baseline16: blocks x ceil(N / 8)
         if (counters) counters->mma_invocations = A->num_blocks * ((n + 7) / 8);
+        if (counters && (cfg->flags & TCS_CFG_COUNT_ACCESS)) {
+            tcs_cost cost{};
+            mebcrs_cost(A, 0, n, cfg->mapping, &cost, s);
+            counters->transactions = cost.exec_transactions;
+            counters->transaction_bytes = cost.exec_transaction_bytes;
+            counters->useful_bytes = cost.exec_useful_bytes;
+        }
     });
 }

@@ -126,6 +126,11 @@ void pad_convert(const void* src, tcs_dtype sdt, int64_t lds, void* dst, tcs_dty
 
 // vector height 8 only unless any_height (8 or 16: the 16x1 baseline layout).
 void check_mebcrs(const tcs_mebcrs* m, bool any_height = false);
+// Reference cost model (cost.cu).
+void mebcrs_cost(const tcs_mebcrs* m, uint64_t nnz, int64_t n_cols, tcs_mapping mapping, tcs_cost* out, cudaStream_t s);
+// Host arrays -> device handle (F32 values, vector height 8 or 16), prepared.
+void upload_mebcrs(uint64_t rows, uint64_t cols, tcs_precision precision, uint32_t vh, const uint32_t* row_pointers,
+                   const uint32_t* column_indices, const float* values, tcs_mebcrs* out, cudaStream_t s);
 
 // TMA-gather + tcgen05 SpMM (spmm_tc05.cu); false = not applicable, nothing launched.
 bool spmm_tc05(const tcs_mebcrs* A, const Plan* plan, const __half* B, int64_t ldb, int64_t b_rows, int64_t n,

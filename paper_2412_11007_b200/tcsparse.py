@@ -35,12 +35,21 @@ class FormatError(TcsError):
     """ref errors.hpp:24."""
 
 
+class ParseError(TcsError):
+    """ref errors.hpp:11-22 (malformed MatrixMarket; message carries "line N: ")."""
+
+
+class FileError(TcsError, OSError):
+    """A container / output file cannot be opened or written."""
+
+
 class CudaError(TcsError):
     pass
 
 
 _ERR = {_abi.TCS_ERR_ARGUMENT: ArgumentError, _abi.TCS_ERR_SHAPE: ShapeError, _abi.TCS_ERR_FORMAT: FormatError,
-        _abi.TCS_ERR_CUDA: CudaError, _abi.TCS_ERR_OOM: CudaError, _abi.TCS_ERR_NCCL: CudaError}
+        _abi.TCS_ERR_CUDA: CudaError, _abi.TCS_ERR_OOM: CudaError, _abi.TCS_ERR_NCCL: CudaError,
+        _abi.TCS_ERR_PARSE: ParseError, _abi.TCS_ERR_IO: FileError}
 
 
 def _check(rc: int):
@@ -336,6 +345,68 @@ def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
     out = torch.empty_like(x)
     _check(_abi.load().tcs_round_values(int(precision), x.data_ptr(), out.data_ptr(), x.numel(), _stream()))
     return out
+
+
+# ------------------------------------------------------ ingest / containers
+def _host_csr_to_device(h: _abi.tcs_csr) -> CsrMatrix:
+    import numpy as np
+
+    try:
+        rows, cols, nnz = int(h.rows), int(h.cols), int(h.nnz)
+        rp = np.ctypeslib.as_array(C.cast(h.row_ptr, C.POINTER(C.c_uint32)), shape=(rows + 1,)).copy()
+        ci = np.ctypeslib.as_array(C.cast(h.col_idx, C.POINTER(C.c_uint32)), shape=(max(nnz, 1),))[:nnz].copy()
+        v = np.ctypeslib.as_array(C.cast(h.values, C.POINTER(C.c_float)), shape=(max(nnz, 1),))[:nnz].copy()
+    finally:
+        _abi.load().tcs_csr_free_host(C.byref(h))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    return CsrMatrix(rows, cols, torch.from_numpy(rp.view(np.int32)).to(dev), torch.from_numpy(ci.view(np.int32)).to(dev),
+                     torch.from_numpy(v).to(dev))
+
+
+def parse_matrix_market(text: str | bytes) -> CsrMatrix:
+    """ref parse_matrix_market (matrix_market.hpp:28-94); CSR assembled on the GPU."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    h = _abi.tcs_csr()
+    _check(_abi.load().tcs_matrix_market_parse(b, len(b), C.byref(h), _stream()))
+    return _host_csr_to_device(h)
+
+
+def read_matrix_market(path: str) -> CsrMatrix:
+    h = _abi.tcs_csr()
+    _check(_abi.load().tcs_matrix_market_read(str(path).encode(), C.byref(h), _stream()))
+    return _host_csr_to_device(h)
+
+
+def write_matrix_market(path: str, csr: CsrMatrix) -> None:
+    """ref write_matrix_market (matrix_market.hpp:97-104)."""
+    import numpy as np
+
+    rp = csr.row_ptr.cpu().numpy().astype(np.uint32)
+    ci = csr.col_idx.cpu().numpy().astype(np.uint32)
+    v = csr.values.cpu().numpy().astype(np.float32)
+    h = _abi.tcs_csr(csr.rows, csr.cols, ci.size, rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+    _check(_abi.load().tcs_matrix_market_write(str(path).encode(), C.byref(h)))
+
+
+def write_mebcrs(path: str, m: MeBcrsMatrix) -> None:
+    """ref write_mebcrs (container_io.hpp:56-68), MEBC v1."""
+    _check(_abi.load().tcs_mebcrs_write(str(path).encode(), C.byref(m._h), _stream()))
+
+
+def read_mebcrs(path: str) -> MeBcrsMatrix:
+    """ref read_mebcrs (container_io.hpp:70-91): validated, F32 values on the device."""
+    h = _abi.tcs_mebcrs()
+    _check(_abi.load().tcs_mebcrs_read(str(path).encode(), C.byref(h), _stream()))
+    return MeBcrsMatrix(h)
+
+
+def mebcrs_cost(m: MeBcrsMatrix, nnz: int, n_cols: int,
+                mapping: ThreadMapping = ThreadMapping.coalesced) -> dict:
+    """ref analysis.hpp:34-131 / footprint.hpp (tcs_mebcrs_cost): swap8 for a
+    vector-height-8 matrix, the 16x1 baseline for a vector-height-16 one."""
+    c = _abi.tcs_cost()
+    _check(_abi.load().tcs_mebcrs_cost(C.byref(m._h), int(nnz), int(n_cols), int(mapping), C.byref(c), _stream()))
+    return {name: int(getattr(c, name)) for name, _ in _abi.tcs_cost._fields_}
 
 
 def launch_count() -> int:
