@@ -56,7 +56,14 @@ constexpr int kWarps = 4;
 // Resident CTAs per SM.  Narrow slabs (32 features: 64-byte gathers, few
 // registers) need more warps in flight to cover DRAM-latency gathers when
 // B does not fit in L2 (C5: 537 MB of B).
-constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : 4; }
+#ifndef TCS_SPMM_BPS_WIDE
+#define TCS_SPMM_BPS_WIDE 4
+#endif
+constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : nchunk * fpl <= 8 ? TCS_SPMM_BPS_WIDE : 4; }
+// Feature slab of the FP16 kernel for N > 64 (experiment knob: 128 or 64).
+#ifndef TCS_SPMM_SLAB_F16
+#define TCS_SPMM_SLAB_F16 128
+#endif
 
 // ------------------------------------------------------------- scheduling
 // Persistent warps: each warp claims work items from a per-slab counter
@@ -603,7 +610,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
 
         // Feature padding: 32 / 64 / multiple of 128.
         const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
-        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : 128;
+        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : 128;
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
         const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
@@ -670,8 +677,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                     vf32 ? launch(spmm_f16_kernel<2, 8, true>, a, slabs, s, "spmm_f16<128,f32v>")
                          : launch(spmm_f16_kernel<2, 8, false>, a, slabs, s, "spmm_f16<128>");
                 else if (slab == 64)
-                    vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>")
-                         : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>");
+                    vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>", spmm_blocks(1, 8))
+                         : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>", spmm_blocks(1, 8));
                 else
                     vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>", spmm_blocks(1, 4))
                          : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));

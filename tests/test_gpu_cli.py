@@ -195,13 +195,20 @@ TOL_LINE = re.compile(r"max_abs_diff=([0-9.e+-]+)")
 
 
 def _same_up_to_diff(got, want, tol):
-    """Real-valued runs: identical text except the max_abs_diff figure (the
-    tensor core sums in another order), which must be within tolerance."""
+    """Real-valued runs: identical text and verdict except the max_abs_diff
+    figure (the tensor core sums in another order).  That figure is the
+    error against the CLI's double-precision check of the UNROUNDED inputs,
+    dominated by operand rounding, so it must track the reference's own
+    figure; the reference itself exceeds the per-element TF32 threshold on
+    some inputs (SURVEY §8(c) caveat, ref cli.hpp:67), and so must we then."""
     assert got[0] == want[0]
     assert TOL_LINE.sub("X", got[1]) == TOL_LINE.sub("X", want[1])
     assert TOL_LINE.sub("X", got[2]) == TOL_LINE.sub("X", want[2])
-    for x in TOL_LINE.findall(got[1] + got[2]):
-        assert float(x) <= tol
+    mine = [float(x) for x in TOL_LINE.findall(got[1] + got[2])]
+    theirs = [float(x) for x in TOL_LINE.findall(want[1] + want[2])]
+    assert len(mine) == len(theirs)
+    for x, y in zip(mine, theirs):
+        assert abs(x - y) <= 0.05 * y + 0.05 * tol, (x, y)
 
 
 @pytest.mark.parametrize("prec", [0, 1])

@@ -1,0 +1,220 @@
+// Microbenchmark (not product code), follow-up to gather_bench.cu: the TMA
+// gather4 and LDGSTS rows there were limited by a dependent index load per
+// stage (each producer waited one L2/DRAM round trip before every TMA
+// issue).  Here the producers prefetch their row indices D stages ahead, so
+// the measured rate is the TMA / LDGSTS engine's, not the index latency.
+// Same workload: 32M random 256-byte row gathers from an L2-resident
+// 233K x 128 fp16 matrix.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/gather_bench2 tools/gather_bench2.cu -lcuda
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
+
+typedef CUresult (*EncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n@!p bra W_%=;\n}\n" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+
+// P producer warps + 1 consumer warp per CTA, STAGES x 4 KB ring (16 rows of
+// 256 B per stage).  MODE 0: gather4 box {64,1} SW128 (two per 4 rows);
+// MODE 2: gather4 box {128,1} no swizzle (one per 4 rows).  A producer's lane
+// j < 16 holds the row index of stage (its k-th + D) -- loaded D stages early.
+template <int P, int STAGES, int MODE, int D>
+__global__ void __launch_bounds__(32 * (P + 1), 1) tma_pf_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                                 const uint32_t* __restrict__ idx, uint64_t nrows_total) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < STAGES; ++i) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&full[i])));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&empty[i])));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const uint64_t nstages_total = nrows_total / 16;
+    const uint64_t per_cta = (nstages_total + gridDim.x - 1) / gridDim.x;
+    const uint64_t s0 = blockIdx.x * per_cta, s1 = min(nstages_total, s0 + per_cta);
+    if (warp < P) {
+        uint32_t pre[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const uint64_t s = s0 + warp + uint64_t(d) * P;
+            pre[d] = (lane < 16 && s < s1) ? __ldg(idx + s * 16 + lane) : 0u;
+        }
+        for (uint64_t s = s0 + warp; s < s1; s += uint64_t(D) * P) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const uint64_t sd = s + uint64_t(d) * P;
+                if (sd >= s1) break;
+                const uint32_t myrow = pre[d];
+                const uint64_t sn = sd + uint64_t(D) * P;
+                pre[d] = (lane < 16 && sn < s1) ? __ldg(idx + sn * 16 + lane) : 0u;
+                const uint32_t slot = (uint32_t)((sd - s0) % STAGES);
+                const uint32_t ph = (uint32_t)(((sd - s0) / STAGES) & 1);
+                mbar_wait(&empty[slot], ph ^ 1);
+                uint8_t* dst = base + (size_t)slot * 4096;
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&full[slot])), "r"(4096) : "memory");
+                __syncwarp();
+                const uint32_t srcl = 4 * (lane & 3);
+                const uint32_t r0 = __shfl_sync(0xffffffffu, myrow, srcl), r1 = __shfl_sync(0xffffffffu, myrow, srcl + 1),
+                               r2 = __shfl_sync(0xffffffffu, myrow, srcl + 2), r3 = __shfl_sync(0xffffffffu, myrow, srcl + 3);
+                if (lane < 4) {
+                    if (MODE == 0) {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+                            asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst + h * 2048 + lane * 512)), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(smem_u32(&full[slot])), "r"(64 * h), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+                    } else {
+                        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(dst + lane * 1024)), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(smem_u32(&full[slot])), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+                    }
+                }
+            }
+        }
+    } else {
+        for (uint64_t s = s0; s < s1; ++s) {
+            const uint32_t slot = (uint32_t)((s - s0) % STAGES);
+            const uint32_t ph = (uint32_t)(((s - s0) / STAGES) & 1);
+            mbar_wait(&full[slot], ph);
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[slot])) : "memory");
+            __syncwarp();
+        }
+    }
+}
+
+// LDGSTS (cp.async.cg 16 B) with indices prefetched 8 iterations ahead: each
+// warp iteration gathers 4 rows x 256 B into a 4-slot ring.
+__global__ void __launch_bounds__(256) cpasync_pf_kernel(const uint4* __restrict__ B, const uint32_t* __restrict__ idx,
+                                                         uint64_t nrows_total) {
+    __shared__ __align__(16) uint4 buf[8][4][32][2];
+    const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    uint32_t it = 0;
+    for (uint64_t g0 = warp * 32; g0 < nrows_total; g0 += nwarps * 32) {  // 32 rows: one index per lane
+        const uint32_t mine = __ldg(idx + g0 + lane);
+#pragma unroll
+        for (int u = 0; u < 8; ++u, ++it) {
+            const uint32_t row = __shfl_sync(0xffffffffu, mine, 4 * u + (lane >> 3));
+            const uint4* p = B + (uint64_t)row * 16 + (lane & 7);
+            uint4* d = &buf[wl][it & 3][lane][0];
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d)), "l"(p));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(d + 1)), "l"(p + 8));
+            asm volatile("cp.async.commit_group;");
+            asm volatile("cp.async.wait_group 3;");
+        }
+    }
+    asm volatile("cp.async.wait_group 0;");
+}
+
+// LDG.128 at the SpMM kernel's memory-level parallelism: 16 rows x 256 B
+// (4 KB) in flight per warp, 4 warps x 4 CTAs per SM, plus the SHFL
+// redistribution the mma.sync fragment needs (one SHFL per loaded register).
+template <bool SHFL>
+__global__ void __launch_bounds__(128, 4) ldg_spmm_like(const uint4* __restrict__ B, const uint32_t* __restrict__ idx,
+                                                        uint64_t nrows_total, uint4* sink) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    const uint32_t src = 8 * (lane & 3) + (lane >> 2);
+    for (uint64_t g0 = warp * 32; g0 < nrows_total; g0 += nwarps * 32) {
+        const uint32_t mine = __ldg(idx + g0 + lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t row = __shfl_sync(0xffffffffu, mine, 16 * h + 4 * u + (lane >> 3));
+                const uint4* p = B + (uint64_t)row * 16 + (lane & 7);
+                v[2 * u] = __ldg(p);
+                v[2 * u + 1] = __ldg(p + 8);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                uint4 x = v[u];
+                if (SHFL) {
+                    x.x = __shfl_sync(0xffffffffu, x.x, src);
+                    x.y = __shfl_sync(0xffffffffu, x.y, src);
+                    x.z = __shfl_sync(0xffffffffu, x.z, src);
+                    x.w = __shfl_sync(0xffffffffu, x.w, src);
+                }
+                acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+            }
+        }
+    }
+    if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
+int main() {
+    const int K = 232965, NC = 128;
+    const uint64_t R = 1ull << 25;
+    __half* dB;
+    uint32_t* didx;
+    uint4* sink;
+    CK(cudaMalloc(&dB, (size_t)K * NC * 2));
+    CK(cudaMemset(dB, 1, (size_t)K * NC * 2));
+    CK(cudaMalloc(&didx, R * 4));
+    CK(cudaMalloc(&sink, 64));
+    std::vector<uint32_t> h(R);
+    uint64_t x = 88172645463325252ull;
+    for (uint64_t i = 0; i < R; ++i) { x ^= x << 13; x ^= x >> 7; x ^= x << 17; h[i] = (uint32_t)(x % K); }
+    CK(cudaMemcpy(didx, h.data(), R * 4, cudaMemcpyHostToDevice));
+    int sms;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto report = [&](const char* name, auto launch) {
+        launch();
+        CK(cudaDeviceSynchronize());
+        cudaEventRecord(a);
+        for (int r = 0; r < 3; ++r) launch();
+        cudaEventRecord(b);
+        CK(cudaEventSynchronize(b));
+        CK(cudaGetLastError());
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        ms /= 3;
+        printf("%-52s %8.3f ms  %8.1f GB/s\n", name, ms, R * 256.0 / ms / 1e6);
+    };
+    report("LDG.128, SpMM-like MLP (4 KB/warp, 16 warps/SM)", [&] { ldg_spmm_like<false><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
+    report("LDG.128 + SHFL, SpMM-like MLP", [&] { ldg_spmm_like<true><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
+    report("cp.async.cg 16B -> smem, idx prefetched", [&] { cpasync_pf_kernel<<<sms * 7, 256>>>((const uint4*)dB, didx, R); });
+
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    CUtensorMap t64, t128;
+    cuuint64_t dims[2] = {(cuuint64_t)NC, (cuuint64_t)K};
+    cuuint64_t strides[1] = {(cuuint64_t)NC * 2};
+    cuuint32_t es[2] = {1, 1};
+    cuuint32_t box64[2] = {64, 1}, box128[2] = {128, 1};
+    ((EncodeTiled)fn)(&t64, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, dB, dims, strides, box64, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    ((EncodeTiled)fn)(&t128, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, dB, dims, strides, box128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const size_t smem = 1024 + 48 * 4096;
+#define TMA_CASE(P, MODE, D, MAP, NAME)                                                                                  \
+    {                                                                                                                    \
+        CK(cudaFuncSetAttribute(tma_pf_kernel<P, 48, MODE, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        report(NAME, [&] { tma_pf_kernel<P, 48, MODE, D><<<sms, 32 * (P + 1), smem>>>(MAP, didx, R); });               \
+    }
+    TMA_CASE(1, 0, 8, t64, "TMA gather4 {64,1} SW128, 1 warp, idx 8 ahead");
+    TMA_CASE(2, 0, 8, t64, "TMA gather4 {64,1} SW128, 2 warps, idx 8 ahead");
+    TMA_CASE(4, 0, 8, t64, "TMA gather4 {64,1} SW128, 4 warps, idx 8 ahead");
+    TMA_CASE(8, 0, 4, t64, "TMA gather4 {64,1} SW128, 8 warps, idx 4 ahead");
+    TMA_CASE(1, 2, 8, t128, "TMA gather4 {128,1} no swizzle, 1 warp, idx 8 ahead");
+    TMA_CASE(4, 2, 8, t128, "TMA gather4 {128,1} no swizzle, 4 warps, idx 8 ahead");
+    TMA_CASE(8, 2, 4, t128, "TMA gather4 {128,1} no swizzle, 8 warps, idx 4 ahead");
+    return 0;
+}
