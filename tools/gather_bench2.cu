@@ -216,5 +216,8 @@ int main() {
     TMA_CASE(1, 2, 8, t128, "TMA gather4 {128,1} no swizzle, 1 warp, idx 8 ahead");
     TMA_CASE(4, 2, 8, t128, "TMA gather4 {128,1} no swizzle, 4 warps, idx 8 ahead");
     TMA_CASE(8, 2, 4, t128, "TMA gather4 {128,1} no swizzle, 8 warps, idx 4 ahead");
+    TMA_CASE(16, 2, 2, t128, "TMA gather4 {128,1} no swizzle, 16 warps, idx 2 ahead");
+    TMA_CASE(24, 2, 2, t128, "TMA gather4 {128,1} no swizzle, 24 warps, idx 2 ahead");
+    TMA_CASE(16, 0, 2, t64, "TMA gather4 {64,1} SW128, 16 warps, idx 2 ahead");
     return 0;
 }
