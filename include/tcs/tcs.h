@@ -203,6 +203,69 @@ tcs_status tcs_spmm_baseline16(const tcs_mebcrs* a, const void* b, tcs_dtype b_d
                                int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
                                tcs_counters* counters, tcs_stream_t stream);
 
+/* -------------------------------------------- SR-BCRS (padded ablation) */
+/* ref: srbcrs.hpp:11-38 (SrBcrsMatrix) -- the zero-vector padded baseline
+ * format of the paper's footprint ablation: every window is widened to a
+ * multiple of k vectors, so every block is a full 8 x k tile; padded
+ * vectors carry TCS_SR_PADDING as column index and zero values.  The
+ * pointer array holds a (begin, end) pair per window.  Value (r, j) of block
+ * b of window w sits at 8 * (row_pointer_pairs[2w] + b * k) + r * k + j. */
+#define TCS_SR_PADDING 0xFFFFFFFFu /* ref kPaddingSentinel (srbcrs.hpp:12) */
+typedef struct tcs_srbcrs {
+    uint64_t rows;
+    uint64_t cols;
+    uint32_t vector_height; /* 8 */
+    uint32_t k;             /* 8 (FP16), 4 (TF32) */
+    tcs_precision precision;
+    tcs_dtype value_dtype;
+    uint64_t num_windows;
+    uint64_t num_padded;         /* stored (padded) vectors = column_indices length */
+    uint32_t* row_pointer_pairs; /* device, 2 * num_windows */
+    uint32_t* column_indices;    /* device, num_padded      */
+    void* values;                /* device, 8 * num_padded  */
+    void* impl;                  /* library-private gather view + work list */
+} tcs_srbcrs;
+
+/* ref: encode_srbcrs(const CsrMatrix&, Precision) (srbcrs.hpp:40-72), on the
+ * GPU: CSR -> ME-BCRS -> padded.  All arrays bit-identical to the
+ * reference's (values as F32, or their binary16 rounding as F16). */
+tcs_status tcs_srbcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_srbcrs* out,
+                             tcs_stream_t stream);
+/* The padding step alone (ref srbcrs.hpp:49-70), from a device ME-BCRS. */
+tcs_status tcs_srbcrs_from_mebcrs(const tcs_mebcrs* me, tcs_srbcrs* out, tcs_stream_t stream);
+/* Host arrays (2W pairs, padded column indices, 8 * padded f32 values) ->
+ * device handle.  Windows must be stored back to back (pairs[2w+1] ==
+ * pairs[2w+2], as encode_srbcrs produces them) and each a multiple of k
+ * vectors; FORMAT error otherwise. */
+tcs_status tcs_srbcrs_upload(uint64_t rows, uint64_t cols, tcs_precision precision,
+                             const uint32_t* row_pointer_pairs, const uint32_t* column_indices, const float* values,
+                             tcs_srbcrs* out, tcs_stream_t stream);
+/* Device handle -> caller-sized host arrays (values widened to f32); any
+ * pointer may be NULL.  Synchronises. */
+tcs_status tcs_srbcrs_download(const tcs_srbcrs* m, uint32_t* row_pointer_pairs, uint32_t* column_indices,
+                               float* values, tcs_stream_t stream);
+tcs_status tcs_srbcrs_free(tcs_srbcrs* m, tcs_stream_t stream);
+/* ref: spmm(const SrBcrsMatrix&, const DenseMatrix&, const KernelConfig&)
+ * (spmm.hpp:181-185): the swapped 8x1 kernel over the padded format;
+ * padded vectors gather a zero row (the reference's kAbsentRow) and are
+ * numerically inert.  The result equals tcs_spmm on the compact format bit
+ * for bit wherever the sums are exact (the reference's small-integer
+ * inputs); with real values, windows long enough to be split across work
+ * items may associate their partial sums differently.  Arguments,
+ * errors and counters as tcs_spmm (mma_invocations = sum_w padded_w / k *
+ * ceil(n / 16)). */
+tcs_status tcs_spmm_srbcrs(const tcs_srbcrs* a, const void* b, tcs_dtype b_dtype, int64_t ldb, int64_t b_rows,
+                           int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg, tcs_counters* counters,
+                           tcs_stream_t stream);
+/* tcs_spmm_srbcrs with host operands (the reference's value semantics): A
+ * given by host SR-BCRS arrays (f32 values), B host f32 [b_rows x n], C host
+ * f32 [rows x n]. */
+tcs_status tcs_spmm_srbcrs_host(uint64_t rows, uint64_t cols, tcs_precision precision,
+                                const uint32_t* row_pointer_pairs, const uint32_t* column_indices,
+                                const float* values, const float* b, int64_t b_rows, int64_t n, float* c,
+                                const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream);
+
+
 /* ------------------------------------------------------------ cost model */
 /* ref analysis.hpp:34-131 + footprint.hpp:13-25: the structural cost of one
  * SpMM over `m` with n_cols dense columns -- swapped 8x1 strategy for a

@@ -115,6 +115,51 @@ inline SpmmResult spmm(const MeBcrsMatrix& sparse, const DenseMatrix& dense, con
     return res;
 }
 
+/// ref srbcrs.hpp:40 -- CSR -> SR-BCRS (the zero-vector padded baseline
+/// format of the footprint ablation), converted on the GPU.
+inline SrBcrsMatrix encode_srbcrs(const CsrMatrix& m, Precision p) {
+    const tcs_csr c{m.rows, m.cols, m.nnz(), m.row_ptr.data(), m.col_idx.data(), m.values.data()};
+    tcs_mebcrs d{};
+    detail::check(tcs_mebcrs_encode_host(&c, static_cast<tcs_precision>(p), TCS_DTYPE_F32, &d, nullptr));
+    tcs_srbcrs sr{};
+    const tcs_status rc = tcs_srbcrs_from_mebcrs(&d, &sr, nullptr);
+    tcs_mebcrs_free(&d, nullptr);
+    detail::check(rc);
+    SrBcrsMatrix out;
+    out.rows = m.rows;
+    out.cols = m.cols;
+    out.vector_height = sr.vector_height;
+    out.k = sr.k;
+    out.precision = p;
+    out.row_pointer_pairs.resize(2 * sr.num_windows);
+    out.column_indices.resize(sr.num_padded);
+    out.values.resize(8 * sr.num_padded);
+    const tcs_status s = tcs_srbcrs_download(&sr, out.row_pointer_pairs.data(), out.column_indices.data(),
+                                             out.values.data(), nullptr);
+    tcs_srbcrs_free(&sr, nullptr);
+    detail::check(s);
+    return out;
+}
+
+/// ref spmm.hpp:181 -- the same swapped kernel over the padded format.
+inline SpmmResult spmm(const SrBcrsMatrix& sparse, const DenseMatrix& dense, const KernelConfig& cfg) {
+    const tcs_kernel_config kc = detail::config(cfg);
+    if (cfg.vector_height != 8) throw ArgumentError("swap-and-transpose path requires vector height 8");
+    if (cfg.precision != sparse.precision) throw ArgumentError("config precision must match the encoded matrix");
+    if (sparse.cols != dense.rows) throw ShapeError("sparse cols must equal dense rows");
+    if (sparse.row_pointer_pairs.size() != 2 * ((sparse.rows + 7) / 8))
+        throw FormatError("row_pointer_pairs length must be 2 * numWindows");
+    SpmmResult res;
+    res.output = DenseMatrix(sparse.rows, dense.cols);
+    tcs_counters cn{};
+    detail::check(tcs_spmm_srbcrs_host(sparse.rows, sparse.cols, static_cast<tcs_precision>(sparse.precision),
+                                       sparse.row_pointer_pairs.data(), sparse.column_indices.data(),
+                                       sparse.values.data(), dense.data.data(), static_cast<int64_t>(dense.rows),
+                                       static_cast<int64_t>(dense.cols), res.output.data.data(), &kc, &cn, nullptr));
+    res.counters = detail::counters(cn);
+    return res;
+}
+
 /// ref sddmm.hpp:84 -- sampled dense-dense product over the mask pattern.
 inline SddmmResult sddmm(const SddmmOperands& ops, const KernelConfig& cfg) {
     const tcs_kernel_config kc = detail::config(cfg);

@@ -128,6 +128,12 @@ def ref():
         _ref.ref_read_mebcrs.restype = C.c_int64
         _ref.ref_read_mebcrs.argtypes = [C.c_char_p, _u64p, _u64p, C.POINTER(C.c_int), C.POINTER(_u32p),
                                          C.POINTER(_u32p), C.POINTER(_f32p), C.POINTER(C.c_void_p)]
+        _ref.ref_encode_srbcrs.restype = C.c_int64
+        _ref.ref_encode_srbcrs.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_int,
+                                           C.POINTER(_u32p), C.POINTER(_u32p), C.POINTER(_f32p)]
+        _ref.ref_spmm_srbcrs.restype = C.c_int
+        _ref.ref_spmm_srbcrs.argtypes = [C.c_uint64, C.c_uint64, C.c_int, _u32p, _u32p, _f32p, _f32p, C.c_uint64,
+                                         C.c_uint64, C.c_int, _f32p, _u64p]
         _ref.ref_sddmm_output_offsets.restype = C.c_uint64
         _ref.ref_sddmm_output_offsets.argtypes = [C.c_uint64, C.c_int]
         _ref.ref_free.argtypes = [C.c_void_p]
@@ -235,6 +241,46 @@ def encode_mebcrs(m: Csr, precision: int, vector_height: int = 8) -> MeBcrs:
     lib().orc_mebcrs_fill_v(m.rows, vh, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(m.values, _f32p),
                             K_OF[precision], _p(rp, _u32p), _p(ci, _u32p), _p(vals, _f32p))
     return MeBcrs(m.rows, m.cols, precision, rp, ci[:nv], vals[:vh * nv], vector_height=vh)
+
+
+class SrBcrs:
+    """ref srbcrs.hpp:17-38 (host arrays)."""
+
+    def __init__(self, rows, cols, precision, row_pointer_pairs, column_indices, values):
+        self.rows, self.cols, self.precision = rows, cols, precision
+        self.k = K_OF[precision]
+        self.row_pointer_pairs = np.ascontiguousarray(row_pointer_pairs, np.uint32)
+        self.column_indices = np.ascontiguousarray(column_indices, np.uint32)
+        self.values = np.ascontiguousarray(values, np.float32)
+
+
+SR_PADDING = 0xFFFFFFFF  # ref kPaddingSentinel (srbcrs.hpp:12)
+
+
+def encode_srbcrs(me: MeBcrs) -> SrBcrs:
+    """Restatement of ref encode_srbcrs's padding loop (srbcrs.hpp:49-70),
+    vectorised: window w keeps its nv_w columns and gains ceil(nv_w/k)*k -
+    nv_w sentinel columns; block b is re-laid from width_b to k columns,
+    zeros past width_b."""
+    k, rp = me.k, me.row_pointers.astype(np.int64)
+    W = len(rp) - 1
+    nvw = np.diff(rp)
+    padded = (nvw + k - 1) // k * k
+    start = np.zeros(W + 1, np.int64)
+    np.cumsum(padded, out=start[1:])
+    P = int(start[-1])
+    pairs = np.empty(2 * W, np.uint32)
+    pairs[0::2], pairs[1::2] = start[:-1], start[1:]
+    ci = np.full(P, SR_PADDING, np.uint32)
+    vals = np.zeros(8 * P, np.float32)
+    w_of = np.repeat(np.arange(W), nvw)                       # window of every stored vector
+    j = np.arange(len(me.column_indices)) - rp[w_of]         # slot within its window
+    ci[start[w_of] + j] = me.column_indices
+    b, jj = j // k, j % k
+    width = np.minimum(k, nvw[w_of] - b * k)
+    for r in range(8):
+        vals[8 * (start[w_of] + b * k) + r * k + jj] = me.values[8 * (rp[w_of] + b * k) + r * width + jj]
+    return SrBcrs(me.rows, me.cols, me.precision, pairs, ci, vals)
 
 
 def mebcrs_to_dense(me: MeBcrs) -> np.ndarray:
@@ -382,6 +428,31 @@ class Ref:
         if rc:
             raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
         return out[:8 * mask.nv], int(cnt.value)
+
+    @staticmethod
+    def encode_srbcrs(m: Csr, precision: int) -> "SrBcrs":
+        r = ref()
+        pp, ci, v = _u32p(), _u32p(), _f32p()
+        n = r.ref_encode_srbcrs(m.rows, m.cols, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p), _p(m.values, _f32p),
+                                precision, C.byref(pp), C.byref(ci), C.byref(v))
+        if n < 0:
+            raise ValueError("encode failed")
+        W = (m.rows + 7) // 8
+        return SrBcrs(m.rows, m.cols, precision, _take(r, pp, 2 * W, np.uint32), _take(r, ci, n, np.uint32),
+                      _take(r, v, 8 * n, np.float32))
+
+    @staticmethod
+    def spmm_srbcrs(sr: "SrBcrs", B, cfg_precision=None):
+        B = np.ascontiguousarray(B, np.float32)
+        Cm = np.zeros((sr.rows, B.shape[1]), np.float32)
+        cnt = C.c_uint64(0)
+        rc = ref().ref_spmm_srbcrs(sr.rows, sr.cols, sr.precision, _p(sr.row_pointer_pairs, _u32p),
+                                   _p(sr.column_indices, _u32p), _p(sr.values, _f32p), _p(B, _f32p), B.shape[0],
+                                   B.shape[1], sr.precision if cfg_precision is None else cfg_precision,
+                                   _p(Cm, _f32p), C.byref(cnt))
+        if rc:
+            raise ValueError({1: "ArgumentError", 2: "ShapeError"}.get(rc, "error"))
+        return Cm, int(cnt.value)
 
     @staticmethod
     def partition_windows(m: Csr, vector_height: int, k: int):

@@ -112,7 +112,18 @@ bool criterion7() {  // tests/acceptance.cpp:240-273 (its value draws; reference
         for (Precision p : {Precision::fp16, Precision::tf32}) {
             const MeBcrsMatrix me = gpu::encode_mebcrs(m, p);
             if (!same_me(me, encode_mebcrs(m, p))) return false;
-            if (gpu::spmm(me, dense, {p, 8, ThreadMapping::coalesced}).output != want) return false;
+            const auto me_out = gpu::spmm(me, dense, {p, 8, ThreadMapping::coalesced});
+            if (me_out.output != want) return false;
+            // padded baseline format (tests/acceptance.cpp:264-267)
+            const SrBcrsMatrix sr = gpu::encode_srbcrs(m, p);
+            const SrBcrsMatrix sr_ref = encode_srbcrs(m, p);
+            if (sr.row_pointer_pairs != sr_ref.row_pointer_pairs || sr.column_indices != sr_ref.column_indices ||
+                sr.values != sr_ref.values)
+                return false;
+            const auto sr_out = gpu::spmm(sr, dense, {p, 8, ThreadMapping::coalesced});
+            if (sr_out.output != me_out.output) return false;
+            if (sr_out.counters.mma_invocations != spmm(sr_ref, dense, {p, 8, ThreadMapping::coalesced}).counters.mma_invocations)
+                return false;
             if (decode_mebcrs(me) != m) return false;
         }
     }
@@ -152,7 +163,7 @@ int main() {
     report(2, "gpu spmm == reference spmm == dense oracle (200 matrices, both precisions/mappings)", criterion2());
     report(3, "scenario matrix: 2 MMAs on the swapped path", criterion3());
     report(6, "gpu sddmm == reference sddmm, and feeds spmm", criterion6());
-    report(7, "residue blocks: gpu encode/spmm == reference, decode round-trips", criterion7());
+    report(7, "residue blocks: gpu encode/spmm (ME-BCRS and SR-BCRS) == reference, decode round-trips", criterion7());
     report(0, "reference exception taxonomy through the C-ABI", errors());
     std::printf(failures ? "%d drop-in criteria FAILED\n" : "all drop-in criteria passed\n", failures);
     return failures ? 1 : 0;

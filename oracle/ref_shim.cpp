@@ -143,6 +143,53 @@ int ref_spmm(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp, co
     }
 }
 
+// encode_srbcrs (inc/srbcrs.hpp:40-72). Returns the padded vector count, or -1.
+int64_t ref_encode_srbcrs(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci, const float* vals,
+                          int precision, uint32_t** out_pairs, uint32_t** out_ci, float** out_vals) {
+    try {
+        const SrBcrsMatrix sr = encode_srbcrs(make_csr(rows, cols, rp, ci, vals), static_cast<Precision>(precision));
+        *out_pairs = dup(sr.row_pointer_pairs);
+        *out_ci = dup(sr.column_indices);
+        *out_vals = dup(sr.values);
+        return static_cast<int64_t>(sr.column_indices.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// spmm(SrBcrsMatrix) (inc/spmm.hpp:181-185) on arrays from ref_encode_srbcrs.
+int ref_spmm_srbcrs(uint64_t rows, uint64_t cols, int precision, const uint32_t* pairs, const uint32_t* ci,
+                    const float* vals, const float* B, uint64_t b_rows, uint64_t N, int cfg_precision, float* C,
+                    uint64_t* mma_invocations) {
+    try {
+        SrBcrsMatrix sr;
+        const Precision p = static_cast<Precision>(precision);
+        sr.rows = rows;
+        sr.cols = cols;
+        sr.vector_height = 8;
+        sr.k = shape_for(p).k;
+        sr.precision = p;
+        const uint64_t W = (rows + 7) / 8;
+        sr.row_pointer_pairs.assign(pairs, pairs + 2 * W);
+        const uint64_t P = W ? pairs[2 * W - 1] : 0;
+        sr.column_indices.assign(ci, ci + P);
+        sr.values.assign(vals, vals + 8 * P);
+        DenseMatrix b(b_rows, N);
+        std::memcpy(b.data.data(), B, sizeof(float) * b_rows * N);
+        const SpmmResult res = spmm(sr, b, KernelConfig{static_cast<Precision>(cfg_precision), 8,
+                                                        ThreadMapping::coalesced});
+        std::memcpy(C, res.output.data.data(), sizeof(float) * rows * N);
+        if (mma_invocations) *mma_invocations = res.counters.mma_invocations;
+        return 0;
+    } catch (const ArgumentError&) {
+        return 1;
+    } catch (const ShapeError&) {
+        return 2;
+    } catch (const std::exception&) {
+        return 3;
+    }
+}
+
 // sddmm (inc/sddmm.hpp:84). out_vals has 8*nv floats.
 int ref_sddmm(uint64_t rows, uint64_t cols, int precision, const uint32_t* rp, const uint32_t* ci,
               const float* mask_vals, const float* A, uint64_t a_rows, const float* Bt,

@@ -39,6 +39,17 @@ class tcs_mebcrs(C.Structure):
                 ("num_blocks", C.c_uint64), ("num_groups16", C.c_uint64), ("plan", C.c_void_p)]
 
 
+class tcs_srbcrs(C.Structure):
+    _fields_ = [("rows", C.c_uint64), ("cols", C.c_uint64), ("vector_height", C.c_uint32),
+                ("k", C.c_uint32), ("precision", C.c_int), ("value_dtype", C.c_int),
+                ("num_windows", C.c_uint64), ("num_padded", C.c_uint64),
+                ("row_pointer_pairs", C.c_void_p), ("column_indices", C.c_void_p), ("values", C.c_void_p),
+                ("impl", C.c_void_p)]
+
+
+TCS_SR_PADDING = 0xFFFFFFFF
+
+
 class tcs_kernel_config(C.Structure):
     _fields_ = [("precision", C.c_int), ("vector_height", C.c_uint32), ("mapping", C.c_int),
                 ("flags", C.c_uint32)]
@@ -67,6 +78,18 @@ EXPORTS = {
     "tcs_spmm_baseline16": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                       C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
                                       C.c_void_p]),
+    "tcs_srbcrs_encode": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_int, C.POINTER(tcs_srbcrs), C.c_void_p]),
+    "tcs_srbcrs_from_mebcrs": (C.c_int, [C.POINTER(tcs_mebcrs), C.POINTER(tcs_srbcrs), C.c_void_p]),
+    "tcs_srbcrs_upload": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.POINTER(tcs_srbcrs), C.c_void_p]),
+    "tcs_srbcrs_download": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "tcs_srbcrs_free": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p]),
+    "tcs_spmm_srbcrs": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                  C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
+                                  C.c_void_p]),
+    "tcs_spmm_srbcrs_host": (C.c_int, [C.c_uint64, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.POINTER(tcs_kernel_config),
+                                       C.POINTER(tcs_counters), C.c_void_p]),
     "tcs_mebcrs_cost": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_uint64, C.c_int64, C.c_int, C.POINTER(tcs_cost),
                                   C.c_void_p]),
     "tcs_matrix_market_parse": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(tcs_csr), C.c_void_p]),

@@ -218,7 +218,10 @@ def _dtype_tag(t: torch.Tensor) -> int:
 def spmm(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = KernelConfig(),
          out: torch.Tensor | None = None) -> SpmmResult:
     """ref spmm.hpp:173.  dense: [K, N] f16 (FP16) or f32 CUDA tensor, row-major
-    (any row stride).  Returns C [M, N] f32."""
+    (any row stride).  Returns C [M, N] f32.  An SrBcrsMatrix runs the
+    reference's spmm(SrBcrsMatrix) overload (spmm.hpp:181)."""
+    if isinstance(sparse, SrBcrsMatrix):
+        return spmm_srbcrs(sparse, dense, cfg, out)
     if dense.dim() != 2 or dense.stride(1) != 1:
         dense = dense.contiguous()
     m, n = sparse.rows, dense.shape[1]
@@ -247,6 +250,87 @@ def spmm_baseline16(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig
     _check(_abi.load().tcs_spmm_baseline16(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
                                            dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
                                            C.byref(cnt), _stream()))
+    return SpmmResult(out, KernelCounters._from(cnt))
+
+
+class SrBcrsMatrix:
+    """Device SR-BCRS (ref srbcrs.hpp:11-38), the zero-vector padded baseline
+    format, owned by the C library."""
+
+    def __init__(self, handle: _abi.tcs_srbcrs):
+        self._h = handle
+
+    rows = property(lambda self: self._h.rows)
+    cols = property(lambda self: self._h.cols)
+    k = property(lambda self: self._h.k)
+    vector_height = property(lambda self: self._h.vector_height)
+    precision = property(lambda self: Precision(self._h.precision))
+    num_windows = property(lambda self: self._h.num_windows)
+    num_padded = property(lambda self: self._h.num_padded)
+
+    def to_host(self):
+        """(row_pointer_pairs, column_indices, values[f32]) as numpy arrays."""
+        import numpy as np
+
+        rpp = np.empty(max(1, 2 * self.num_windows), np.uint32)
+        ci = np.empty(max(1, self.num_padded), np.uint32)
+        v = np.empty(max(1, 8 * self.num_padded), np.float32)
+        _check(_abi.load().tcs_srbcrs_download(C.byref(self._h), rpp.ctypes.data, ci.ctypes.data, v.ctypes.data,
+                                               _stream()))
+        return rpp[: 2 * self.num_windows], ci[: self.num_padded], v[: 8 * self.num_padded]
+
+    def free(self):
+        if getattr(self, "_h", None) is not None and self._h.impl:
+            _abi.load().tcs_srbcrs_free(C.byref(self._h), _stream())
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_host(rows, cols, precision, row_pointer_pairs, column_indices, values) -> "SrBcrsMatrix":
+        import numpy as np
+
+        rpp = np.ascontiguousarray(row_pointer_pairs, np.uint32)
+        ci = np.ascontiguousarray(column_indices, np.uint32)
+        v = np.ascontiguousarray(values, np.float32)
+        h = _abi.tcs_srbcrs()
+        _check(_abi.load().tcs_srbcrs_upload(rows, cols, int(precision), rpp.ctypes.data, ci.ctypes.data,
+                                             v.ctypes.data, C.byref(h), _stream()))
+        return SrBcrsMatrix(h)
+
+
+def encode_srbcrs(csr: CsrMatrix | MeBcrsMatrix, precision: Precision | None = None,
+                  value_dtype: int | None = None) -> SrBcrsMatrix:
+    """ref encode_srbcrs (srbcrs.hpp:40-72) on the GPU, from a CSR (encoded
+    to ME-BCRS first) or directly from a device ME-BCRS."""
+    h = _abi.tcs_srbcrs()
+    lib = _abi.load()
+    if isinstance(csr, MeBcrsMatrix):
+        _check(lib.tcs_srbcrs_from_mebcrs(C.byref(csr._h), C.byref(h), _stream()))
+    else:
+        if value_dtype is None:
+            value_dtype = _abi.TCS_DTYPE_F16 if int(precision) == 0 else _abi.TCS_DTYPE_F32
+        c = csr._c()
+        _check(lib.tcs_srbcrs_encode(C.byref(c), int(precision), int(value_dtype), C.byref(h), _stream()))
+    return SrBcrsMatrix(h)
+
+
+def spmm_srbcrs(sparse: SrBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = KernelConfig(),
+                out: torch.Tensor | None = None) -> SpmmResult:
+    """ref spmm(const SrBcrsMatrix&, ...) (spmm.hpp:181-185): same kernel and
+    result as spmm() on the compact format."""
+    if dense.dim() != 2 or dense.stride(1) != 1:
+        dense = dense.contiguous()
+    m, n = sparse.rows, dense.shape[1]
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    cnt = _abi.tcs_counters()
+    _check(_abi.load().tcs_spmm_srbcrs(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
+                                       dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
+                                       C.byref(cnt), _stream()))
     return SpmmResult(out, KernelCounters._from(cnt))
 
 

@@ -49,6 +49,13 @@ def record(case: cases.Case) -> dict:
             C16, cnt16 = R.spmm_baseline16(m, case.B, p)
             rec[f"b16_{tag}"] = {"nv": int(pci.shape[0]), "part_sha": cases.sha(prp, pci), "sha": cases.sha(C16),
                                  "mma": cnt16}
+        # SR-BCRS padded ablation format (inc/srbcrs.hpp:40-72) and its SpMM (inc/spmm.hpp:181)
+        sr = R.encode_srbcrs(m, p)
+        rec[f"sr_{tag}"] = {"np": int(sr.column_indices.shape[0]),
+                            "sha": cases.sha(sr.row_pointer_pairs, sr.column_indices, sr.values)}
+        if case.B is not None:
+            Csr_, cnt_sr = R.spmm_srbcrs(sr, case.B)
+            rec[f"sr_{tag}"].update({"spmm_sha": cases.sha(Csr_), "mma": cnt_sr})
         if case.A is not None:
             out, cnt = R.sddmm(me, case.A, case.Bt)
             rec[f"sddmm_{tag}"] = {"sha": cases.sha(out), "mma": cnt}

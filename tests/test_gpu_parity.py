@@ -257,3 +257,68 @@ def test_baseline16_errors():
         T.spmm_baseline16(m16, torch.ones(23, 16, device="cuda"))
     with pytest.raises(T.ArgumentError):
         T.encode_mebcrs(dev_csr(m), T.Precision.fp16, vector_height=4)
+
+
+def check_srbcrs(case, rec, value_dtype):
+    """SR-BCRS padded ablation format (ref srbcrs.hpp:40-72): arrays
+    bit-exact with ref encode_srbcrs, and spmm over it (ref spmm.hpp:181)
+    == the compact-format result == the reference's (golden hashes)."""
+    for p in case.precisions:
+        if p == 1 and value_dtype == F16:
+            continue
+        tag = "fp16" if p == 0 else "tf32"
+        r_sr = rec[f"sr_{tag}"]
+        me = T.encode_mebcrs(dev_csr(case.csr), T.Precision(p), value_dtype)
+        for sr in (T.encode_srbcrs(dev_csr(case.csr), T.Precision(p), value_dtype), T.encode_srbcrs(me)):
+            assert sr.num_padded == r_sr["np"], case.name
+            pairs, ci, v = sr.to_host()
+            want = O.encode_srbcrs(O.encode_mebcrs(case.csr, p))  # pinned by test_oracle.py
+            assert np.array_equal(pairs, want.row_pointer_pairs) and np.array_equal(ci, want.column_indices)
+            want_v = want.values if value_dtype == F32 else O.round_array(want.values, 0)
+            assert np.array_equal(v.view(np.uint32), want_v.view(np.uint32)), case.name
+            if value_dtype == F32:
+                assert cases.sha(pairs, ci, v) == r_sr["sha"], case.name
+            if case.B is not None:
+                res = T.spmm(sr, torch.from_numpy(case.B).cuda(), T.KernelConfig(T.Precision(p)))
+                assert cases.sha(res.output.cpu().numpy()) == r_sr["spmm_sha"], case.name
+                assert res.counters.mma_invocations == r_sr["mma"]
+            sr.free()
+        me.free()
+
+
+@pytest.mark.parametrize("value_dtype", [F32, F16])
+def test_srbcrs_matches_reference(golden, value_dtype):
+    params = cases.acceptance2_params()
+    todo = list(cases.kat_cases())
+    todo += [cases.acceptance2_case(i, params) for i in range(0, 200, 3)]
+    todo += [cases.c1_case(False)]
+    for c in todo:
+        check_srbcrs(c, golden["cases"][c.name], value_dtype)
+
+
+def test_srbcrs_padding_inert_and_upload():
+    """Padded vectors gather the reference's absent (zero) row: non-finite B
+    rows cannot leak into the result; host upload of the reference's own
+    arrays runs the same kernel; malformed pairs -> FormatError."""
+    m = O.generate_random_sparse(300, 200, 0.03, 11, real=True)
+    B = O.generate_random_dense(200, 48, 12, real=True)
+    B[0, :] = np.nan  # column 0 may be gathered by real vectors only
+    for p in (0, 1):
+        me = T.encode_mebcrs(dev_csr(m), T.Precision(p), F32)
+        cfg = T.KernelConfig(T.Precision(p))
+        want = T.spmm(me, torch.from_numpy(B).cuda(), cfg).output.cpu().numpy()
+        ref = O.Ref.encode_srbcrs(m, p)
+        sr = T.SrBcrsMatrix.from_host(m.rows, m.cols, p, ref.row_pointer_pairs, ref.column_indices, ref.values)
+        got = T.spmm(sr, torch.from_numpy(B).cuda(), cfg).output.cpu().numpy()
+        assert np.array_equal(got, want, equal_nan=True)
+        ref_c, _ = O.Ref.spmm_srbcrs(ref, np.nan_to_num(B, nan=0.0))
+        got0 = T.spmm(sr, torch.from_numpy(np.nan_to_num(B, nan=0.0)).cuda(), cfg).output.cpu().numpy()
+        assert rel_l2(got0, ref_c) < 1e-5
+        bad = ref.row_pointer_pairs.copy()
+        bad[1] += 1  # window 0 no longer a multiple of k
+        with pytest.raises(T.FormatError):
+            T.SrBcrsMatrix.from_host(m.rows, m.cols, p, bad, ref.column_indices, ref.values)
+        with pytest.raises(T.ShapeError):
+            T.spmm(sr, torch.ones(199, 16, device="cuda"), cfg)
+        with pytest.raises(T.ArgumentError):
+            T.spmm(sr, torch.ones(200, 16, device="cuda"), T.KernelConfig(T.Precision(1 - p)))

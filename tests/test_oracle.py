@@ -68,6 +68,12 @@ def check_case(case, rec):
             blocks = int(sum((int(m16.row_pointers[w + 1] - m16.row_pointers[w]) + m16.k - 1) // m16.k
                              for w in range(m16.num_windows)))
             assert blocks * ((case.B.shape[1] + 7) // 8) == rec[f"b16_{tag}"]["mma"]
+        sr = O.encode_srbcrs(me)
+        r_sr = rec[f"sr_{tag}"]
+        assert sr.column_indices.shape[0] == r_sr["np"]
+        assert cases.sha(sr.row_pointer_pairs, sr.column_indices, sr.values) == r_sr["sha"]
+        if case.B is not None:  # ref spmm(SrBcrs) == spmm(MeBcrs) bit for bit (spmm.hpp:179-180)
+            assert r_sr["spmm_sha"] == rec[f"spmm_{tag}"]["sha"] and r_sr["mma"] == rec[f"spmm_{tag}"]["mma"]
         if case.A is not None:
             out = O.sddmm(me, case.A, case.Bt)
             assert cases.sha(out) == rec[f"sddmm_{tag}"]["sha"]

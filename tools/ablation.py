@@ -65,6 +65,23 @@ for pname in ("fp16", "tf32"):
         out["runs"].append({"kernel": f"swap8/{mname}", "precision": pname, "ms": round(ms, 4),
                             "gflops": round(2 * nnz * N / ms / 1e6, 1), "nv": me.num_vectors,
                             "mma": me.num_blocks * ((N + 15) // 16), "encode_ms": round(enc8, 3)})
+    # SR-BCRS: the zero-vector padded format (ref srbcrs.hpp) on the same kernel
+    sr = T.encode_srbcrs(me)
+    enc_sr = timed(lambda: T.encode_srbcrs(me).free())
+    ms = timed(lambda: T.spmm(sr, B, T.KernelConfig(prec), out=C))
+    # long windows may be split at other points than on the compact format
+    # (the work-list segment size follows the vector count), so real-valued
+    # sums can associate differently: compare in rel-L2
+    rel_sr = float((C - base_out).norm() / base_out.norm())
+    assert rel_sr < 1e-5, rel_sr
+    vb = 2 if pname == "fp16" else 4
+    W = me.num_windows
+    out["runs"].append({"kernel": "swap8/srbcrs", "precision": pname, "ms": round(ms, 4),
+                        "gflops": round(2 * nnz * N / ms / 1e6, 1), "nv_padded": sr.num_padded,
+                        "footprint_me_bytes": 4 * (W + 1) + me.num_vectors * (4 + 8 * vb),
+                        "footprint_sr_bytes": 8 * W + sr.num_padded * (4 + 8 * vb),
+                        "pad_ms": round(enc_sr, 3), "rel_l2_vs_swap8": rel_sr})
+    sr.free()
     me.free()
     m16 = T.encode_mebcrs(csr, prec, vector_height=16)
     enc16 = timed(lambda: T.encode_mebcrs(csr, prec, vector_height=16).free())
