@@ -212,6 +212,42 @@ __device__ __forceinline__ void store_row(float* __restrict__ dst, const float (
     }
 }
 
+// Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
+// of every chunk (accumulator layout, ref fragment.hpp:60-66).
+template <int NCHUNK, int FPL>
+__device__ __forceinline__ void f16_epilogue(const SpmmArgs& a, const WorkItem& it,
+                                             const float (&acc)[NCHUNK][FPL / 2][4], int64_t feat0, uint32_t g,
+                                             uint32_t t) {
+    constexpr int NJ = FPL / 2, CHUNK = 8 * FPL;
+    const bool split = it.slot != kNoSlot;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t r = 2 * t + rr;
+        const uint64_t row = 8ull * it.window + r;
+        float* dst;
+        bool vec_ok;
+        if (split) {
+            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+            vec_ok = true;
+        } else {
+            if (row >= a.rows) continue;
+            dst = a.C + row * a.ldc;
+            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            float v[FPL];
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                v[2 * j] = acc[c][j][rr];
+                v[2 * j + 1] = acc[c][j][2 + rr];
+            }
+            const int64_t feat = feat0 + c * CHUNK + FPL * g;
+            store_row<FPL>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        }
+    }
+}
+
 template <int NCHUNK, int FPL, bool VF32>
 __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
@@ -258,35 +294,7 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
             }
         }
 
-        // Epilogue: lane holds window rows 2t, 2t+1 x features FPL*g + [0, FPL)
-        // of every chunk (accumulator layout, ref fragment.hpp:60-66).
-        const bool split = it.slot != kNoSlot;
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const uint32_t r = 2 * t + rr;
-            const uint64_t row = 8ull * it.window + r;
-            float* dst;
-            bool vec_ok;
-            if (split) {
-                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
-                vec_ok = true;
-            } else {
-                if (row >= a.rows) continue;
-                dst = a.C + row * a.ldc;
-                vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
-            }
-#pragma unroll
-            for (int c = 0; c < NCHUNK; ++c) {
-                float v[FPL];
-#pragma unroll
-                for (int j = 0; j < NJ; ++j) {
-                    v[2 * j] = acc[c][j][rr];
-                    v[2 * j + 1] = acc[c][j][2 + rr];
-                }
-                const int64_t feat = feat0 + c * CHUNK + FPL * g;
-                store_row<FPL>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
-            }
-        }
+        f16_epilogue<NCHUNK, FPL>(a, it, acc, feat0, g, t);
     }
 }
 
