@@ -148,19 +148,27 @@ def test_config3_full_size_properties():
     Bt = G.dense(cols, 32, 5, values="int", dtype=torch.float32)
     out_vals = torch.empty(8 * nv, dtype=torch.float32, device="cuda")
     T.sddmm(T.SddmmOperands(me, Af, Bt), T.KernelConfig(), out_values=out_vals)
-    rng = np.random.default_rng(3)
-    vid = np.sort(rng.choice(nv, 20000, replace=False))
+    vid = np.sort(np.random.default_rng(3).choice(nv, 20000, replace=False))
+    check_sddmm_samples(rows, cols, rp, ci, rp_host, ci_host, Af, Bt, out_vals, vid, k=8)
+    me.free()
+
+
+def check_sddmm_samples(rows, cols, rp, ci, rp_host, ci_host, Af, Bt, out_vals, vid, k):
+    """SDDMM output at the stored vectors `vid` == direct dot products of
+    A's rows and Bt's rows where the CSR has an entry, 0 elsewhere."""
+    r_of = torch.repeat_interleave(torch.arange(rows, device="cuda"), (rp[1:] - rp[:-1]).long())
+    entry_keys = r_of * cols + ci.long()  # CSR order == sorted
+    del r_of
     w = np.searchsorted(rp_host, vid, side="right") - 1
     vl = vid - rp_host[w]
     nvw = rp_host[w + 1] - rp_host[w]
-    b, j = vl // 8, vl % 8
-    width = np.minimum(8, nvw - 8 * b)
+    b, j = vl // k, vl % k
+    width = np.minimum(k, nvw - k * b)
     col = ci_host[vid].astype(np.int64)
-    entry_keys = (r_of * cols + ci.long())  # CSR order == sorted
     for r in range(8):
-        row = 8 * w + r
+        row = 8 * w.astype(np.int64) + r
         ok = row < rows
-        pos = 8 * (rp_host[w].astype(np.int64) + 8 * b) + r * width + j
+        pos = 8 * (rp_host[w].astype(np.int64) + k * b) + r * width + j
         got_r = out_vals[torch.from_numpy(pos).cuda()].cpu().numpy()
         q = torch.from_numpy(np.where(ok, row, 0) * cols + col).cuda()
         idx = torch.searchsorted(entry_keys, q).clamp(max=entry_keys.numel() - 1)
@@ -168,7 +176,47 @@ def test_config3_full_size_properties():
         dots = (Af[torch.from_numpy(np.where(ok, row, 0)).cuda()] * Bt[torch.from_numpy(col).cuda()]).sum(1)
         want_r = np.where(present, dots.cpu().numpy(), 0.0).astype(np.float32)
         assert np.array_equal(got_r, want_r), r
-    me.free()
+
+
+def test_config5_full_size_64bit_offsets():
+    """BASELINE config 5 at full size (R-MAT scale 23, ~250 M nnz): the
+    FP16 value array holds 1.9e9 elements (3.9 GB, byte offsets past 2^31)
+    and the TF32 one 7.8 GB (past 2^32).  Integer-valued SpMM (both
+    precisions, N = 32) == an independent exact fp32 product; SDDMM at
+    vectors sampled from the top end of the value array == direct dots."""
+    rows, cols, rp, ci, v = G.rmat_csr(G.C5_RMAT, values="int")
+    nnz = ci.numel()
+    assert 230e6 < nnz < 280e6
+    csr = T.CsrMatrix(rows, cols, rp, ci, v)
+    A = torch.sparse_csr_tensor(rp.long(), ci.long(), v, size=(rows, cols))
+    B = G.dense(cols, 32, 3, values="int", dtype=torch.float32)
+    want = A @ B
+    del A
+    import paper_2412_11007_b200._abi as abi
+
+    for p in (T.Precision.fp16, T.Precision.tf32):
+        me = T.encode_mebcrs(csr, p)
+        # FP16: 3.9 GB of values (byte offsets past 2^31); TF32: 7.8 GB (past 2^32)
+        assert 8 * me.num_vectors * (2 if p == T.Precision.fp16 else 4) > (1 << (31 if p == T.Precision.fp16 else 32))
+        got = T.spmm(me, B.half() if p == T.Precision.fp16 else B, T.KernelConfig(p)).output
+        assert torch.equal(got, want), p
+        del got
+        if p == T.Precision.tf32:
+            nv = me.num_vectors
+            rp_host = np.empty(me.num_windows + 1, np.uint32)
+            ci_host = np.empty(nv, np.uint32)
+            assert abi.load().tcs_mebcrs_download(C.byref(me._h), rp_host.ctypes.data, ci_host.ctypes.data, None,
+                                                  C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+            Af = G.dense(rows, 32, 4, values="int", dtype=torch.float32)
+            Bt = G.dense(cols, 32, 5, values="int", dtype=torch.float32)
+            out_vals = torch.empty(8 * nv, dtype=torch.float32, device="cuda")
+            T.sddmm(T.SddmmOperands(me, Af, Bt), T.KernelConfig(p), out_values=out_vals)
+            rng = np.random.default_rng(5)
+            vid = np.sort(rng.choice(np.arange(nv - nv // 10, nv), 20000, replace=False))
+            check_sddmm_samples(rows, cols, rp, ci, rp_host, ci_host, Af, Bt, out_vals, vid, k=4)
+            del out_vals, Af, Bt
+        me.free()
+        torch.cuda.empty_cache()
 
 
 def test_host_entry_points_match_device_path():
