@@ -50,6 +50,7 @@ struct SpmmArgs {
     float* partial;  // [slot][8][ldp]
     int64_t ldp;
     uint32_t* counter;  // per-slab work-item counters (zeroed before launch)
+    uint32_t slab0;     // first feature slab of this launch (slab = slab0 + blockIdx.y)
 };
 
 constexpr int kWarps = 4;
@@ -80,7 +81,7 @@ __device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) 
 // loaded coalesced; slots pick theirs with a shuffle.
 __device__ __forceinline__ uint32_t load_colpair(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
                                                  uint32_t lane) {
-    return s + lane < vend ? __ldg(ci + s + lane) : 0u;
+    return s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
 }
 
 // ------------------------------------------------------------- FP16 path
@@ -255,9 +256,9 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     const uint32_t g = lane >> 2, t = lane & 3;             // fragment coordinates
     const uint32_t q = lane >> 3, p = lane & 7;             // loader coordinates (quarter, lane in quarter)
     const uint32_t src_lane = 8 * t + g;                    // where this lane's fragment data was loaded
-    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    uint32_t* counter = a.counter + blockIdx.y;
+    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
 
     for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
@@ -313,9 +314,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
     constexpr int SLAB = 16 * NMMA;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
-    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const unsigned short* Bl = static_cast<const unsigned short*>(a.B) + feat0 + g;
-    uint32_t* counter = a.counter + blockIdx.y;
+    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
 
     for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
@@ -477,9 +478,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArg
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
     const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
-    const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * SLAB;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
-    uint32_t* counter = a.counter + blockIdx.y;
+    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
 
     for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
@@ -573,8 +574,8 @@ __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __re
 // slabs; warps pull items from their slab's counter.
 template <typename K>
 void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name, int bps = 4) {
-    const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * bps / std::max(1, slabs));
     const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
+    const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * bps / std::max(1, slabs));
     const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
     TCS_LAUNCHED(name);
