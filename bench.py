@@ -541,9 +541,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # TCS_DIST_BACKEND=gloo runs the multi-rank path with every rank on the
+    # GPUs there are (ranks share a device round-robin): a functional check
+    # of the sharded bench on a 1-GPU box; its timings mean nothing.
+    backend = os.environ.get("TCS_DIST_BACKEND", "nccl")
+    if torch.cuda.is_available():
+        local = local % torch.cuda.device_count() if backend != "nccl" else local
     if world > 1:
         torch.cuda.set_device(local)
-        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            torch.distributed.init_process_group(backend)
     device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
     if args.impl == "reference":
         line = run_reference(args, rank, world, device)
