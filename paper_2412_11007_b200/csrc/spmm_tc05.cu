@@ -19,8 +19,9 @@
 //      (N = 8 needs M = 64), H instructions per step for 64*H features;
 //      fp32 accumulators in TMEM, double buffered across work items.
 //
-// Warp roles (persistent CTA, one per SM): warp 0 = TMA producer, warp 1 =
-// MMA issuer (one elected lane) + TMEM owner, warps 2-5 = epilogue
+// Warp roles (persistent CTA, one per SM): warps 0-7 = TMA producers
+// (steps dealt round-robin), warp 8 = MMA issuer (one elected lane) + TMEM
+// owner, warps 9-12 = epilogue
 // (tcgen05.ld 32x32b, one TMEM sub-partition each).  smem ring of STAGES
 // {A, S} stages with full/empty mbarriers; TMEM ring of 2 accumulators with
 // full/empty mbarriers.  Layouts were validated on a B200 by
@@ -112,16 +113,83 @@ __device__ __forceinline__ uint64_t desc_b_k_interleave(uint32_t addr) {
 // B K-major, N = 8, M = 64.
 constexpr uint32_t kIdesc = (1u << 4) | (1u << 15) | ((8u >> 3) << 17) | ((64u >> 4) << 24);
 
+// One accumulator tile (8H columns) of this warp's TMEM sub-partition.
+template <int H>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, uint32_t (&r)[8 * H]) {
+    if constexpr (H == 1) {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    } else {
+#pragma unroll
+        for (int g = 0; g < H / 2; ++g)
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, "
+                "[%16];"
+                : "=r"(r[16 * g + 0]), "=r"(r[16 * g + 1]), "=r"(r[16 * g + 2]), "=r"(r[16 * g + 3]),
+                  "=r"(r[16 * g + 4]), "=r"(r[16 * g + 5]), "=r"(r[16 * g + 6]), "=r"(r[16 * g + 7]),
+                  "=r"(r[16 * g + 8]), "=r"(r[16 * g + 9]), "=r"(r[16 * g + 10]), "=r"(r[16 * g + 11]),
+                  "=r"(r[16 * g + 12]), "=r"(r[16 * g + 13]), "=r"(r[16 * g + 14]), "=r"(r[16 * g + 15])
+                : "r"(taddr + 16 * g));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Position in a CTA's step sequence: its work items blockIdx.x + i*gridDim.x
+// in order, 16-vector steps each (items without vectors have no steps).
+struct StepCursor {
+    uint64_t idx;
+    WorkItem it;
+    uint32_t s, base_v, nvw;
+    __device__ __forceinline__ bool load_item(const Tc05Args& a) {
+        for (; idx < a.n_items; idx += gridDim.x) {
+            it = a.items[idx];
+            if (it.vend > it.vbeg) {
+                base_v = __ldg(a.rp + it.window);
+                nvw = __ldg(a.rp + it.window + 1) - base_v;
+                s = it.vbeg;
+                return true;
+            }
+        }
+        return false;
+    }
+    __device__ __forceinline__ bool start(const Tc05Args& a) {
+        idx = blockIdx.x;
+        return load_item(a);
+    }
+    __device__ __forceinline__ bool advance(const Tc05Args& a) {
+        s += 16;
+        if (s < it.vend) return true;
+        idx += gridDim.x;
+        return load_item(a);
+    }
+    // lane j < 16: column index of vector s + j (row k_rows -> TMA zero fill past the item)
+    __device__ __forceinline__ uint32_t cols(const Tc05Args& a, uint32_t lane) const {
+        return lane < 16 && s + lane < it.vend ? __ldg(a.ci + base_v + s + lane) : a.k_rows;
+    }
+};
+
+// Independent TMEM accumulators per work item: consecutive steps rotate
+// over them.  One M=64, N=8, K=16 MMA into the same accumulator as its
+// predecessor waits for it (~190 cycles per step measured with a single
+// accumulator, which bound the kernel at one step per ~380 cycles per SM);
+// kAcc chains overlap, and the epilogue adds the partial tiles in a fixed
+// order (acc0 + acc1 + acc2 + acc3: deterministic).
+constexpr int kAcc = 4;
+
 template <int H>
 struct Tc05Cfg {
     static constexpr int STAGES = H == 1 ? 48 : H == 2 ? 32 : 16;
     static constexpr int A_STAGE = H * 2048;  // H halves x 16 rows x 128 B
     static constexpr int S_STAGE = 256;
-    static constexpr int TMEM_COLS = 16 * H <= 32 ? 32 : 64;  // 2 accumulators x 8H columns
+    // 2 items in flight x kAcc accumulators x 8H columns
+    static constexpr int TMEM_COLS = 2 * kAcc * 8 * H <= 32 ? 32 : 2 * kAcc * 8 * H <= 64 ? 64
+                                   : 2 * kAcc * 8 * H <= 128 ? 128 : 256;
     static constexpr size_t SMEM = 1024 + (size_t)STAGES * (A_STAGE + S_STAGE) + 1024;
 };
 
-constexpr int kThreads = 192;
+constexpr int kProducers = 8;                 // TMA producer warps
+constexpr int kThreads = 32 * (kProducers + 5);  // + MMA issuer + 4 epilogue warps
 
 template <int H>
 __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_constant__ CUtensorMap tmap,
@@ -148,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_con
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap)) : "memory");
-    if (warp == 1) {
+    if (warp == kProducers) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base_sh)),
                      "n"(Cfg::TMEM_COLS));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -158,81 +226,81 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_con
     tc_fence_after();
     const uint32_t tbase = tmem_base_sh;
 
-    if (warp == 0) {
-        // ------------------------------------------------ TMA producer warp
-        uint32_t stage = 0, phase = 0;
-        for (uint64_t idx = blockIdx.x; idx < a.n_items; idx += gridDim.x) {
-            const WorkItem it = a.items[idx];
-            const uint32_t base_v = __ldg(a.rp + it.window);
-            const uint32_t nvw = __ldg(a.rp + it.window + 1) - base_v;
-            const uint32_t* ci = a.ci + base_v;
-            const __half* vals = a.vals + 8ull * base_v;
-            const uint32_t vend = it.vend;
-            // residue tile of the item's last step (narrow block or < 16 vectors)
-            const uint32_t last = it.vbeg + ((vend - it.vbeg + 15) / 16 - 1) * 16;
-            const bool partial_last = vend > it.vbeg && last + 16 > vend;
-            __half res[4];
-            if (partial_last) {
+    if (warp < kProducers) {
+        // ----------------------------------------------- TMA producer warps
+        // The CTA's step sequence (its items blockIdx.x + i*gridDim.x in
+        // order, 16-vector steps each) is dealt round-robin: producer p
+        // issues global steps g = p, p + P, ...  into ring stage g % STAGES.
+        // One producer warp is bound by its TMA issue latency at ~1.3 TB/s
+        // (tools/gather_bench2.cu); eight saturate the TMA unit.  Each
+        // producer's column indices are loaded three own steps ahead.
+        StepCursor cur, pre;  // issue position; prefetch position (3 own steps ahead)
+        bool ok = cur.start(a), ok_pre = pre.start(a);
+        for (uint32_t k = 0; ok && k < warp; ++k) ok = cur.advance(a);
+        for (uint32_t k = 0; ok_pre && k < warp; ++k) ok_pre = pre.advance(a);
+        uint32_t c1 = 0, c2 = 0, c3 = 0;  // column indices of the next three own steps
+        if (ok_pre) c1 = pre.cols(a, lane);
+        for (int k = 0; ok_pre && k < kProducers; ++k) ok_pre = pre.advance(a);
+        if (ok_pre) c2 = pre.cols(a, lane);
+        for (int k = 0; ok_pre && k < kProducers; ++k) ok_pre = pre.advance(a);
+        if (ok_pre) c3 = pre.cols(a, lane);
+        uint32_t stage = warp, phase = 0;
+        while (ok) {
+            const uint32_t cs = cur.s, cvend = cur.it.vend, cbase = cur.base_v, cnvw = cur.nvw, ccol = c1;
+            for (int k = 0; ok && k < kProducers; ++k) ok = cur.advance(a);
+            c1 = c2;
+            c2 = c3;
+            for (int k = 0; ok_pre && k < kProducers; ++k) ok_pre = pre.advance(a);
+            if (ok_pre) c3 = pre.cols(a, lane);  // in flight for three iterations
+            const __half* vals = a.vals + 8ull * cbase;
+            const bool full_step = cs + 16 <= cvend;
+            mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* dA = sA + (size_t)stage * Cfg::A_STAGE;
+            uint8_t* dS = sS + (size_t)stage * Cfg::S_STAGE;
+            if (!full_step) {  // residue tile: zero fill past the window's last vector
+                uint32_t w2[2];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint32_t e = 4 * lane + q;  // tile element: kb*64 + r*8 + j
-                    const uint32_t kb = e >> 6, r = (e >> 3) & 7, j = e & 7;
-                    const uint32_t v = last + 8 * kb + j;
-                    __half x = __float2half(0.f);
-                    if (v < vend) {
-                        const uint32_t b = v >> 3, width = min(8u, nvw - 8 * b);
-                        x = vals[64ull * b + r * width + j];
+                for (int q2 = 0; q2 < 2; ++q2) {
+                    uint32_t packed = 0;
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const uint32_t e = 4 * lane + 2 * q2 + h2;  // tile element: kb*64 + r*8 + j
+                        const uint32_t kb = e >> 6, r = (e >> 3) & 7, j = e & 7;
+                        const uint32_t v = cs + 8 * kb + j;
+                        uint32_t x = 0;
+                        if (v < cvend) {
+                            const uint32_t b = v >> 3, width = min(8u, cnvw - 8 * b);
+                            x = __half_as_ushort(vals[64ull * b + r * width + j]);
+                        }
+                        packed |= x << (16 * h2);
                     }
-                    res[q] = x;
+                    w2[q2] = packed;
                 }
+                *reinterpret_cast<uint2*>(dS + 8 * lane) = make_uint2(w2[0], w2[1]);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             }
-            for (uint32_t c0 = it.vbeg; c0 < vend; c0 += 256) {
-                uint32_t col[8];  // lane l: vectors c0 + l + 32 j
+            __syncwarp();
+            const uint32_t srcl = 4 * (lane & 3);
+            const uint32_t r0 = __shfl_sync(0xffffffffu, ccol, srcl + 0);
+            const uint32_t r1 = __shfl_sync(0xffffffffu, ccol, srcl + 1);
+            const uint32_t r2 = __shfl_sync(0xffffffffu, ccol, srcl + 2);
+            const uint32_t r3 = __shfl_sync(0xffffffffu, ccol, srcl + 3);
+            if (lane == 0) mbar_expect_tx(&full[stage], H * 2048 + (full_step ? 256 : 0));
+            __syncwarp();
+            if (lane < 4) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t v = c0 + lane + 32 * j;
-                    col[j] = v < vend ? __ldg(ci + v) : a.k_rows;
-                }
-#pragma unroll
-                for (int st = 0; st < 16; ++st) {
-                    const uint32_t s = c0 + 16 * st;
-                    if (s >= vend) break;
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* dA = sA + (size_t)stage * Cfg::A_STAGE;
-                    uint8_t* dS = sS + (size_t)stage * Cfg::S_STAGE;
-                    const bool full_step = s + 16 <= vend;
-                    if (!full_step) {
-                        uint2 w;
-                        w.x = (uint32_t)__half_as_ushort(res[0]) | ((uint32_t)__half_as_ushort(res[1]) << 16);
-                        w.y = (uint32_t)__half_as_ushort(res[2]) | ((uint32_t)__half_as_ushort(res[3]) << 16);
-                        *reinterpret_cast<uint2*>(dS + 8 * lane) = w;
-                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    }
-                    __syncwarp();
-                    // columns of this step: lanes (st&1)*16 + u, register st/2
-                    const uint32_t mine = col[st >> 1];
-                    const uint32_t srcl = ((st & 1) << 4) + 4 * (lane & 3);
-                    const uint32_t r0 = __shfl_sync(0xffffffffu, mine, srcl + 0);
-                    const uint32_t r1 = __shfl_sync(0xffffffffu, mine, srcl + 1);
-                    const uint32_t r2 = __shfl_sync(0xffffffffu, mine, srcl + 2);
-                    const uint32_t r3 = __shfl_sync(0xffffffffu, mine, srcl + 3);
-                    if (lane == 0) mbar_expect_tx(&full[stage], H * 2048 + (full_step ? 256 : 0));
-                    __syncwarp();
-                    if (lane < 4) {
-#pragma unroll
-                        for (int h = 0; h < H; ++h)
-                            tma_gather4(dA + h * 2048 + lane * 512, &tmap, &full[stage], 64 * h, (int32_t)r0,
-                                        (int32_t)r1, (int32_t)r2, (int32_t)r3);
-                    }
-                    if (full_step && lane == 4) bulk_copy(dS, vals + 8ull * s, 256, &full[stage]);
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
+                for (int h = 0; h < H; ++h)
+                    tma_gather4(dA + h * 2048 + lane * 512, &tmap, &full[stage], 64 * h, (int32_t)r0, (int32_t)r1,
+                                (int32_t)r2, (int32_t)r3);
+            }
+            if (full_step && lane == 4) bulk_copy(dS, vals + 8ull * cs, 256, &full[stage]);
+            stage += kProducers;
+            if (stage >= STAGES) {
+                stage -= STAGES;
+                phase ^= 1;
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kProducers) {
         // ------------------------------------------------- MMA issuer warp
         uint32_t stage = 0, phase = 0, ab = 0, aphase = 0;
         for (uint64_t idx = blockIdx.x; idx < a.n_items; idx += gridDim.x) {
@@ -240,16 +308,18 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_con
             const uint32_t nsteps = (it.vend - it.vbeg + 15) / 16;
             mbar_wait(&acc_empty[ab], aphase ^ 1);
             tc_fence_after();
-            const uint32_t d0 = tbase + ab * (8 * H);
+            const uint32_t d0 = tbase + ab * (kAcc * 8 * H);
             for (uint32_t stp = 0; stp < nsteps; ++stp) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t aaddr = smem_u32(sA + (size_t)stage * Cfg::A_STAGE);
                     const uint64_t bdesc = desc_b_k_interleave(smem_u32(sS + (size_t)stage * Cfg::S_STAGE));
+                    const uint32_t d = d0 + (stp % kAcc) * (8 * H);
 #pragma unroll
                     for (int h = 0; h < H; ++h)
-                        tc_mma_f16(d0 + 8 * h, desc_a_mn_sw128(aaddr + h * 2048), bdesc, kIdesc, stp > 0 ? 1u : 0u);
+                        tc_mma_f16(d + 8 * h, desc_a_mn_sw128(aaddr + h * 2048), bdesc, kIdesc,
+                                   stp >= kAcc ? 1u : 0u);
                     tc_commit(&empty[stage]);
                 }
                 __syncwarp();
@@ -278,29 +348,18 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_con
             mbar_wait(&acc_full[ab], aphase);
             tc_fence_after();
             uint32_t r[8 * H];
+#pragma unroll
+            for (int i = 0; i < 8 * H; ++i) r[i] = 0u;
             if (any) {
-                const uint32_t taddr = tbase + ((32 * q) << 16) + ab * (8 * H);
-                if constexpr (H == 1) {
-                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                                   "=r"(r[7])
-                                 : "r"(taddr));
-                } else {
+                const uint32_t used = min(static_cast<uint32_t>(kAcc), (it.vend - it.vbeg + 15) / 16);
+                for (uint32_t j = 0; j < used; ++j) {
+                    const uint32_t taddr = tbase + ((32 * q) << 16) + (ab * kAcc + j) * (8 * H);
+                    uint32_t x[8 * H];
+                    tmem_ld<H>(taddr, x);
 #pragma unroll
-                    for (int g = 0; g < H / 2; ++g)
-                        asm volatile(
-                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%"
-                            "14,%15}, [%16];"
-                            : "=r"(r[16 * g + 0]), "=r"(r[16 * g + 1]), "=r"(r[16 * g + 2]), "=r"(r[16 * g + 3]),
-                              "=r"(r[16 * g + 4]), "=r"(r[16 * g + 5]), "=r"(r[16 * g + 6]), "=r"(r[16 * g + 7]),
-                              "=r"(r[16 * g + 8]), "=r"(r[16 * g + 9]), "=r"(r[16 * g + 10]), "=r"(r[16 * g + 11]),
-                              "=r"(r[16 * g + 12]), "=r"(r[16 * g + 13]), "=r"(r[16 * g + 14]), "=r"(r[16 * g + 15])
-                            : "r"(taddr + 16 * g));
+                    for (int i = 0; i < 8 * H; ++i)
+                        r[i] = j ? __float_as_uint(__uint_as_float(r[i]) + __uint_as_float(x[i])) : x[i];
                 }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8 * H; ++i) r[i] = 0u;
             }
             tc_fence_before();
             __syncwarp();
@@ -337,7 +396,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_tc05_kernel(const __grid_con
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == kProducers) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(Cfg::TMEM_COLS));
     }
