@@ -155,6 +155,124 @@ __global__ void __launch_bounds__(128, 4) ldg_spmm_like(const uint4* __restrict_
     if (acc.x == 0x12345678u) sink[0] = acc;
 }
 
+// Alternative fragment exchange: lane 4v + r loads 16 B (features 8r..8r+7)
+// of vector v (a quarter-warp reads 2 rows x 64 B), then one movmatrix.trans
+// per register yields the mma.sync A fragment (feature, vector pair).  Same
+// bytes and the same 4 KB per warp in flight as ldg_spmm_like.
+__global__ void __launch_bounds__(128, 4) ldg_movmatrix(const uint4* __restrict__ B, const uint32_t* __restrict__ idx,
+                                                        uint64_t nrows_total, uint4* sink) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint64_t g0 = warp * 32; g0 < nrows_total; g0 += nwarps * 32) {
+        const uint32_t mine = __ldg(idx + g0 + lane);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {  // 8 vectors per u; 16 per h
+                const uint32_t row = __shfl_sync(0xffffffffu, mine, 16 * h + 8 * u + (lane >> 2));
+#pragma unroll
+                for (int c = 0; c < 4; ++c)  // 4 x 32 features: lane r covers features 32c + 8r .. +7
+                    v[4 * u + c] = __ldg(B + (uint64_t)row * 16 + 4 * c + (lane & 3));
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                uint4 x = v[u];
+                asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(x.x));
+                asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(x.y));
+                asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(x.z));
+                asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %0;" : "+r"(x.w));
+                acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+            }
+        }
+    }
+    if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
+// Hybrid: per 32-row iteration a warp gathers 16 rows with LDG.128 + SHFL
+// and the other 16 with TMA gather4 (box {64,1}, 128-B swizzle) into its
+// own shared-memory slot, read back with ldmatrix.x4.trans (conflict-free
+// under the swizzle).  TMA for iteration i+1 is issued before the LDG part
+// of iteration i.  Tests whether moving half of the bytes off the LDG+SHFL
+// path (2 L1 wavefronts per 128 B) onto TMA + ldmatrix (1 wavefront) lifts
+// the per-SM ceiling.
+__global__ void __launch_bounds__(128, 4) hybrid_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                        const uint4* __restrict__ B, const uint32_t* __restrict__ idx,
+                                                        uint64_t nrows_total, uint4* sink) {
+    __shared__ __align__(1024) uint8_t slots[4][2][4096];
+    __shared__ __align__(8) uint64_t bar[4][2];
+    const uint32_t lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    if (lane == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[wl][0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[wl][1])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncwarp();
+    const uint32_t src = 8 * (lane & 3) + (lane >> 2);
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    auto issue = [&](uint64_t g, uint32_t slot, uint32_t rows_idx) {
+        // rows_idx: lane j < 16 holds row index of TMA row j
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (lane == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[wl][slot])), "r"(4096) : "memory");
+        __syncwarp();
+        const uint32_t srcl = 4 * (lane & 3);
+        const uint32_t r0 = __shfl_sync(0xffffffffu, rows_idx, srcl), r1 = __shfl_sync(0xffffffffu, rows_idx, srcl + 1),
+                       r2 = __shfl_sync(0xffffffffu, rows_idx, srcl + 2), r3 = __shfl_sync(0xffffffffu, rows_idx, srcl + 3);
+        if (lane < 4) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+                asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(&slots[wl][slot][h * 2048 + lane * 512])), "l"(reinterpret_cast<uint64_t>(&tmap)), "r"(smem_u32(&bar[wl][slot])), "r"(64 * h), "r"(r0), "r"(r1), "r"(r2), "r"(r3) : "memory");
+        }
+    };
+    uint64_t g0 = warp * 32;
+    if (g0 >= nrows_total) return;
+    uint32_t mine = __ldg(idx + g0 + lane);
+    issue(g0, 0, __shfl_sync(0xffffffffu, mine, 16 + (lane & 15)));
+    uint32_t it = 0;
+    for (; g0 < nrows_total; g0 += nwarps * 32, ++it) {
+        const uint64_t gn = g0 + nwarps * 32;
+        const uint32_t next = gn < nrows_total ? __ldg(idx + gn + lane) : 0u;
+        if (gn < nrows_total) issue(gn, (it + 1) & 1, __shfl_sync(0xffffffffu, next, 16 + (lane & 15)));
+        // LDG + SHFL half: rows 0..15 of this iteration
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t row = __shfl_sync(0xffffffffu, mine, 4 * u + (lane >> 3));
+            const uint4* p = B + (uint64_t)row * 16 + (lane & 7);
+            v[2 * u] = __ldg(p);
+            v[2 * u + 1] = __ldg(p + 8);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            uint4 x = v[u];
+            x.x = __shfl_sync(0xffffffffu, x.x, src);
+            x.y = __shfl_sync(0xffffffffu, x.y, src);
+            x.z = __shfl_sync(0xffffffffu, x.z, src);
+            x.w = __shfl_sync(0xffffffffu, x.w, src);
+            acc.x ^= x.x; acc.y ^= x.y; acc.z ^= x.z; acc.w ^= x.w;
+        }
+        // TMA half: wait, then 8 x ldmatrix.x4.trans over the 4 KB slot
+        const uint32_t slot = it & 1;
+        mbar_wait(&bar[wl][slot], (it >> 1) & 1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            // instruction i: half h = i/4, 16-B logical chunk pair; lane -> row (lane & 15), chunk 2*(i%4) + (lane >> 4)
+            const uint32_t h = i >> 2, r = lane & 15, c = 2 * (i & 3) + (lane >> 4);
+            const uint32_t addr = smem_u32(&slots[wl][slot][h * 2048 + r * 128 + ((c ^ (r & 7)) * 16)]);
+            uint32_t a0, a1, a2, a3;
+            asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(addr));
+            acc.x ^= a0; acc.y ^= a1; acc.z ^= a2; acc.w ^= a3;
+        }
+        __syncwarp();
+        mine = next;
+    }
+    if (acc.x == 0x12345678u) sink[0] = acc;
+}
+
 int main() {
     const int K = 232965, NC = 128;
     const uint64_t R = 1ull << 25;
@@ -189,6 +307,7 @@ int main() {
     };
     report("LDG.128, SpMM-like MLP (4 KB/warp, 16 warps/SM)", [&] { ldg_spmm_like<false><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
     report("LDG.128 + SHFL, SpMM-like MLP", [&] { ldg_spmm_like<true><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
+    report("LDG.128 2 rows/quarter + movmatrix.trans", [&] { ldg_movmatrix<<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
     report("cp.async.cg 16B -> smem, idx prefetched", [&] { cpasync_pf_kernel<<<sms * 7, 256>>>((const uint4*)dB, didx, R); });
 
     void* fn = nullptr;
@@ -203,6 +322,7 @@ int main() {
                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     ((EncodeTiled)fn)(&t128, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, dB, dims, strides, box128, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    report("hybrid: 16 rows LDG+SHFL + 16 rows TMA->ldmatrix per warp", [&] { hybrid_kernel<<<sms * 4, 128>>>(t64, (const uint4*)dB, didx, R, sink); });
     const size_t smem = 1024 + 48 * 4096;
 #define TMA_CASE(P, MODE, D, MAP, NAME)                                                                                  \
     {                                                                                                                    \
