@@ -155,6 +155,83 @@ __global__ void __launch_bounds__(128, 4) ldg_spmm_like(const uint4* __restrict_
     if (acc.x == 0x12345678u) sink[0] = acc;
 }
 
+// ldg_spmm_like + the SpMM kernel's arithmetic: PRMT pairs + HMMA m16n8k16
+// per shuffled register quad (MMA), and the sparse-operand stream: VALS = 0
+// none, 1 = 16 B of values per gathered row loaded right before use (read
+// once with L1::no_allocate, as the ME-BCRS values are), 2 = the same loaded
+// one 32-row iteration ahead.
+template <bool MMA, int VALS>
+__global__ void __launch_bounds__(128, 4) ldg_spmm_math(const uint4* __restrict__ B, const uint32_t* __restrict__ idx,
+                                                        const uint2* __restrict__ vals, uint64_t nrows_total,
+                                                        float* sink) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * (uint64_t)blockDim.x) >> 5;
+    float acc[8][4] = {};
+    const uint32_t src = 8 * (lane & 3) + (lane >> 2);
+    uint2 pre[2] = {make_uint2(0, 0), make_uint2(0, 0)};
+    if (VALS == 2 && warp * 32 < nrows_total) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const uint2* pv = vals + (warp * 32 + 16 * h) * 2 + lane;
+            asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];" : "=r"(pre[h].x), "=r"(pre[h].y) : "l"(pv));
+        }
+    }
+    for (uint64_t g0 = warp * 32; g0 < nrows_total; g0 += nwarps * 32) {
+        const uint32_t mine = __ldg(idx + g0 + lane);
+        uint2 cur[2] = {pre[0], pre[1]};
+        if (VALS == 2 && g0 + nwarps * 32 < nrows_total) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint2* pv = vals + (g0 + nwarps * 32 + 16 * h) * 2 + lane;
+                asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];" : "=r"(pre[h].x), "=r"(pre[h].y) : "l"(pv));
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 v[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t row = __shfl_sync(0xffffffffu, mine, 16 * h + 4 * u + (lane >> 3));
+                const uint4* p = B + (uint64_t)row * 16 + (lane & 7);
+                v[2 * u] = __ldg(p);
+                v[2 * u + 1] = __ldg(p + 8);
+            }
+            uint2 b = make_uint2(0x3c003c00u, 0x3c003c00u);
+            if (VALS == 2) b = cur[h];
+            if (VALS == 1) {
+                const uint2* pv = vals + (g0 + 16 * h) * 2 + lane;
+                asm volatile("ld.global.nc.L1::no_allocate.v2.b32 {%0,%1}, [%2];" : "=r"(b.x), "=r"(b.y) : "l"(pv));
+            }
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t x[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint4 w = v[2 * u + c];
+                        const uint32_t r = j == 0 ? w.x : j == 1 ? w.y : j == 2 ? w.z : w.w;
+                        x[u] = __shfl_sync(0xffffffffu, r, src);
+                    }
+                    if (MMA) {
+                        const uint32_t a0 = __byte_perm(x[0], x[1], 0x5410), a1 = __byte_perm(x[0], x[1], 0x7632);
+                        const uint32_t a2 = __byte_perm(x[2], x[3], 0x5410), a3 = __byte_perm(x[2], x[3], 0x7632);
+                        float* d = acc[4 * c + j];
+                        asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                                     : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+                                     : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b.x), "r"(b.y));
+                    } else {
+                        acc[4 * c + j][0] += __uint_as_float(x[0] ^ x[1] ^ x[2] ^ x[3] ^ b.x);
+                    }
+                }
+        }
+    }
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += acc[i][0] + acc[i][1] + acc[i][2] + acc[i][3];
+    if (t == 1234.5f) sink[0] = t;
+}
+
 // Alternative fragment exchange: lane 4v + r loads 16 B (features 8r..8r+7)
 // of vector v (a quarter-warp reads 2 rows x 64 B), then one movmatrix.trans
 // per register yields the mma.sync A fragment (feature, vector pair).  Same
@@ -307,6 +384,13 @@ int main() {
     };
     report("LDG.128, SpMM-like MLP (4 KB/warp, 16 warps/SM)", [&] { ldg_spmm_like<false><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
     report("LDG.128 + SHFL, SpMM-like MLP", [&] { ldg_spmm_like<true><<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
+    uint2* dvals;
+    CK(cudaMalloc(&dvals, R * 16));
+    CK(cudaMemset(dvals, 0, R * 16));
+    report("LDG+SHFL (no MMA), same code shape", [&] { ldg_spmm_math<false, 0><<<sms * 4, 128>>>((const uint4*)dB, didx, dvals, R, (float*)sink); });
+    report("LDG+SHFL + PRMT + HMMA", [&] { ldg_spmm_math<true, 0><<<sms * 4, 128>>>((const uint4*)dB, didx, dvals, R, (float*)sink); });
+    report("LDG+SHFL + PRMT + HMMA + 16 B/row values, loaded at use", [&] { ldg_spmm_math<true, 1><<<sms * 4, 128>>>((const uint4*)dB, didx, dvals, R, (float*)sink); });
+    report("LDG+SHFL + PRMT + HMMA + values one iteration ahead", [&] { ldg_spmm_math<true, 2><<<sms * 4, 128>>>((const uint4*)dB, didx, dvals, R, (float*)sink); });
     report("LDG.128 2 rows/quarter + movmatrix.trans", [&] { ldg_movmatrix<<<sms * 4, 128>>>((const uint4*)dB, didx, R, sink); });
     report("cp.async.cg 16B -> smem, idx prefetched", [&] { cpasync_pf_kernel<<<sms * 7, 256>>>((const uint4*)dB, didx, R); });
 
