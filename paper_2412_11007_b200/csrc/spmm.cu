@@ -103,7 +103,29 @@ struct F16Step {
     uint32_t b[2];                      // sparse fragment: rows g, vectors {2t,2t+1}, {2t+8,2t+9}
 };
 
-__device__ __forceinline__ uint32_t loader_vec(uint32_t u, uint32_t q) { return 2 * q + (u & 1) + 8 * (u >> 1); }
+// Vector held by MMA k slot u (0..3 = k 2t, 2t+1, 2t+8, 2t+9) of lane (g, t).
+// Any bijection works if both operands use it; this one makes the sparse
+// fragment the natural ME-BCRS pair at 8g + 2t of each k=8 block (placing
+// vectors 4t..4t+3 instead, one 8-byte load per lane, measured 1.5% slower).
+__device__ __forceinline__ uint32_t kslot_vec(uint32_t u, uint32_t t) { return 2 * t + (u & 1) + 8 * (u >> 1); }
+__device__ __forceinline__ uint32_t loader_vec(uint32_t u, uint32_t q) { return kslot_vec(u, q); }
+
+// Sparse fragment of a full 16-vector step: rows g, k slots of lane (g, t).
+template <bool VF32>
+__device__ __forceinline__ void load_sparse_full(const void* vals, uint64_t vbase, uint32_t s, uint32_t g, uint32_t t,
+                                                 uint32_t& b0, uint32_t& b1) {
+    const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;  // rows g, slots 2t..2t+1 of blocks s/8, s/8+1
+    if constexpr (VF32) {
+        const float* fv = static_cast<const float*>(vals);
+        const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
+        b0 = f2_to_h2(__uint_as_float(x.x), __uint_as_float(x.y));
+        b1 = f2_to_h2(__uint_as_float(y.x), __uint_as_float(y.y));
+    } else {
+        const __half* hv = static_cast<const __half*>(vals);
+        b0 = ld_stream_u32(hv + off);
+        b1 = ld_stream_u32(hv + off + 64);
+    }
+}
 
 template <bool VF32>
 __device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t vbase, uint32_t nvw, uint32_t v,
@@ -144,17 +166,7 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
                 }
             }
         }
-        const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;  // rows g, slots 2t..2t+1 of blocks s/8, s/8+1
-        if constexpr (VF32) {
-            const float* fv = static_cast<const float*>(a.vals);
-            const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
-            st.b[0] = f2_to_h2(__uint_as_float(x.x), __uint_as_float(x.y));
-            st.b[1] = f2_to_h2(__uint_as_float(y.x), __uint_as_float(y.y));
-        } else {
-            const __half* hv = static_cast<const __half*>(a.vals);
-            st.b[0] = ld_stream_u32(hv + off);
-            st.b[1] = ld_stream_u32(hv + off + 64);
-        }
+        load_sparse_full<VF32>(a.vals, vbase, s, g, t, st.b[0], st.b[1]);
     } else {
         // residue step: vectors at or past vend contribute zero registers
 #pragma unroll
@@ -172,13 +184,14 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
                 }
             }
         }
-        const uint32_t v0 = s + 2 * t;
-        const uint32_t e0 = v0 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0, g) : 0u;
-        const uint32_t e1 = v0 + 1 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 1, g) : 0u;
-        const uint32_t e2 = v0 + 8 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 8, g) : 0u;
-        const uint32_t e3 = v0 + 9 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 9, g) : 0u;
-        st.b[0] = e0 | (e1 << 16);
-        st.b[1] = e2 | (e3 << 16);
+        uint32_t e[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t v = s + kslot_vec(u, t);
+            e[u] = v < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v, g) : 0u;
+        }
+        st.b[0] = e[0] | (e[1] << 16);
+        st.b[1] = e[2] | (e[3] << 16);
     }
 }
 
@@ -335,30 +348,23 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
             uint32_t col[4];
             bool ok[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {  // k slots 2t, 2t+1, 2t+8, 2t+9
-                const uint32_t v = 2 * t + (u & 1) + 8 * (u >> 1);
+            for (int u = 0; u < 4; ++u) {  // k slots 2t, 2t+1, 2t+8, 2t+9 (vector order: kslot_vec)
+                const uint32_t v = kslot_vec(u, t);
                 col[u] = __shfl_sync(0xffffffffu, colv, v);
                 ok[u] = s + v < vend;
             }
             uint32_t b0, b1;  // sparse fragment: rows g, vectors {2t, 2t+1}, {2t+8, 2t+9}
             if (s + 16 <= vend) {
-                const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;
-                if constexpr (VF32) {
-                    const float* fv = static_cast<const float*>(a.vals);
-                    const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
-                    b0 = f2_to_h2(__uint_as_float(x.x), __uint_as_float(x.y));
-                    b1 = f2_to_h2(__uint_as_float(y.x), __uint_as_float(y.y));
-                } else {
-                    const __half* hv = static_cast<const __half*>(a.vals);
-                    b0 = ld_stream_u32(hv + off);
-                    b1 = ld_stream_u32(hv + off + 64);
-                }
+                load_sparse_full<VF32>(a.vals, vbase, s, g, t, b0, b1);
             } else {
-                const uint32_t v0 = s + 2 * t;
-                b0 = (v0 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0, g) : 0u) |
-                     ((v0 + 1 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 1, g) : 0u) << 16);
-                b1 = (v0 + 8 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 8, g) : 0u) |
-                     ((v0 + 9 < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v0 + 9, g) : 0u) << 16);
+                uint32_t e[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const uint32_t v = s + kslot_vec(u, t);
+                    e[u] = v < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v, g) : 0u;
+                }
+                b0 = e[0] | (e[1] << 16);
+                b1 = e[2] | (e[3] << 16);
             }
 #pragma unroll
             for (int j = 0; j < NMMA; ++j) {
