@@ -478,6 +478,34 @@ __device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (
     }
 }
 
+// TF32 epilogue: lane holds rows 2t, 2t+1 x features 32c + 4g .. +3.
+template <int NCHUNK>
+__device__ __forceinline__ void tf32_epilogue(const SpmmArgs& a, const WorkItem& it, const float (&acc)[NCHUNK][2][4],
+                                              int64_t feat0, uint32_t g, uint32_t t) {
+    const bool split = it.slot != kNoSlot;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+        const uint32_t r = 2 * t + rr;
+        const uint64_t row = 8ull * it.window + r;
+        float* dst;
+        bool vec_ok;
+        if (split) {
+            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
+            vec_ok = true;
+        } else {
+            if (row >= a.rows) continue;
+            dst = a.C + row * a.ldc;
+            vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
+        }
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            const float v[4] = {acc[c][0][rr], acc[c][0][2 + rr], acc[c][1][rr], acc[c][1][2 + rr]};
+            const int64_t feat = feat0 + c * 32 + 4 * g;
+            store_row<4>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
+        }
+    }
+}
+
 template <int NCHUNK>
 __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArgs a) {
     constexpr int SLAB = NCHUNK * 32;
@@ -534,28 +562,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArg
             }
         }
 
-        const bool split = it.slot != kNoSlot;
-#pragma unroll
-        for (int rr = 0; rr < 2; ++rr) {
-            const uint32_t r = 2 * t + rr;
-            const uint64_t row = 8ull * it.window + r;
-            float* dst;
-            bool vec_ok;
-            if (split) {
-                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + r) * a.ldp;
-                vec_ok = true;
-            } else {
-                if (row >= a.rows) continue;
-                dst = a.C + row * a.ldc;
-                vec_ok = (a.ldc & 3) == 0 && (reinterpret_cast<uintptr_t>(a.C) & 15) == 0;
-            }
-#pragma unroll
-            for (int c = 0; c < NCHUNK; ++c) {
-                const float v[4] = {acc[c][0][rr], acc[c][0][2 + rr], acc[c][1][rr], acc[c][1][2 + rr]};
-                const int64_t feat = feat0 + c * 32 + 4 * g;
-                store_row<4>(dst + feat, v, feat, split ? a.ldp : a.N, vec_ok);
-            }
-        }
+        tf32_epilogue<NCHUNK>(a, it, acc, feat0, g, t);
     }
 }
 
