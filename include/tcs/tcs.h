@@ -119,6 +119,14 @@ typedef struct tcs_kernel_config {
 /* Also fill counters->transactions / transaction_bytes / useful_bytes with
  * the reference's access model (tcs_mebcrs_cost, one extra kernel). */
 #define TCS_CFG_COUNT_ACCESS 0x4u
+/* SDDMM (and the fused SDDMM -> softmax): the mask's values do not change
+ * between calls.  The sampling rule (value != 0) is then read from one
+ * liveness byte per stored vector, built from the values on first use and
+ * cached in the handle's work list, instead of from the 8 stored values
+ * (16 or 32 bytes per vector).  Results are identical; a caller that edits
+ * the values in place must call tcs_mebcrs_prepare (fresh work list) before
+ * relying on this flag again. */
+#define TCS_CFG_STATIC_MASK 0x8u
 
 /* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
  * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);

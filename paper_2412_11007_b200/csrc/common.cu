@@ -230,6 +230,7 @@ void free_plan(Plan* p, cudaStream_t s) {
     if (!p) return;
     dfree(p->items, s);
     dfree(p->split, s);
+    dfree(p->live, s);
     delete p;
 }
 

@@ -44,7 +44,13 @@ struct SddmmArgs {
     uint32_t k;         // storage block width (8 / 4)
     uint32_t* counter;  // work-item counter (zeroed before launch)
     float dead;         // value of stored slots whose mask value is 0: 0, or -inf for the fused softmax
+    const uint8_t* live;  // per-vector liveness bytes (bit r: row r's mask value != 0), mask mode kLive
 };
+
+// Mask modes (template parameter MM): how a slot's liveness is read.
+constexpr int kMaskF16 = 0;   // the mask's binary16 values
+constexpr int kMaskF32 = 1;   // the mask's binary32 values
+constexpr int kLive = 2;      // one liveness byte per stored vector (TCS_CFG_STATIC_MASK)
 
 constexpr int kWarps = 4;
 constexpr int kRing = 4;  // column-index batches staged per warp
@@ -74,28 +80,40 @@ __device__ __forceinline__ uint64_t acc_pos(uint64_t vbase, uint32_t nvw, uint32
 // (nonzero magnitude == the reference's `mask.values[pos] != 0`; -0.0 is not
 // live, ref sddmm.hpp:131).  Issued one group ahead of use.
 // Mask words per group and lane: 4 f32 or 4 packed f16 values.
-template <bool MF32>
-constexpr int kMaskWords = MF32 ? 4 : 2;
+template <int MM>
+constexpr int kMaskWords = MM == kMaskF32 ? 4 : MM == kMaskF16 ? 2 : 1;
 
-template <uint32_t K, bool MF32>
+template <uint32_t K, int MM>
 __device__ __forceinline__ void mask_prefetch(const SddmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend,
                                               uint32_t s, uint32_t g, uint32_t t,
-                                              uint32_t (&mk)[kMaskWords<MF32>]) {
+                                              uint32_t (&mk)[kMaskWords<MM>]) {
     const bool full = s + 16 <= vend;
 #pragma unroll
-    for (int w = 0; w < kMaskWords<MF32>; ++w) mk[w] = 0u;
+    for (int w = 0; w < kMaskWords<MM>; ++w) mk[w] = 0u;
+    if constexpr (MM == kLive) {  // bytes of vectors g (bits 0-7) and g + 8 (bits 8-15)
+        const uint8_t* lv = a.live + vbase / 8;
+        if (s + g < vend) mk[0] = __ldg(lv + s + g);
+        if (s + g + 8 < vend) mk[0] |= static_cast<uint32_t>(__ldg(lv + s + g + 8)) << 8;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
-        if (v < vend) {
-            const uint64_t pos = acc_pos<K>(vbase, nvw, s, full, g, t, q);
-            // raw bits only: the liveness test happens at store time, so the
-            // load stays in flight until then
-            if constexpr (MF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos));
-            else mk[q >> 1] |= static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos))
-                               << (16 * (q & 1));
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+            if (v < vend) {
+                const uint64_t pos = acc_pos<K>(vbase, nvw, s, full, g, t, q);
+                // raw bits only: the liveness test happens at store time, so the
+                // load stays in flight until then
+                if constexpr (MM == kMaskF32) mk[q] = __float_as_uint(__ldg(static_cast<const float*>(a.mask) + pos));
+                else mk[q >> 1] |= static_cast<uint32_t>(__ldg(static_cast<const unsigned short*>(a.mask) + pos))
+                                   << (16 * (q & 1));
+            }
         }
     }
+}
+
+// Liveness bits (bit q) of lane (g,t)'s accumulator elements from the two
+// liveness bytes of vectors g (b0) and g + 8 (b1): rows 2t, 2t+1.
+__device__ __forceinline__ uint32_t live_bits(uint32_t b0, uint32_t b1, uint32_t t) {
+    return ((b0 >> (2 * t)) & 3u) | (((b1 >> (2 * t)) & 3u) << 2);
 }
 
 template <bool OF32>
@@ -106,16 +124,20 @@ __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
 
 // Liveness bits (bit q) of lane (g,t)'s accumulator elements in a general
 // group; elements past the item's last vector are not live.
-template <bool MF32>
-__device__ __forceinline__ uint32_t slow_live(const uint32_t (&mk)[kMaskWords<MF32>], uint32_t s, uint32_t vend,
-                                              uint32_t g) {
+template <int MM>
+__device__ __forceinline__ uint32_t slow_live(const uint32_t (&mk)[kMaskWords<MM>], uint32_t s, uint32_t vend,
+                                              uint32_t g, uint32_t t) {
     uint32_t bits = 0;
+    if constexpr (MM == kLive) {
+        bits = live_bits(mk[0] & 0xFFu, mk[0] >> 8, t);  // bytes past vend were left 0
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
-        const bool live = v < vend && (MF32 ? (mk[q] & 0x7FFFFFFFu) != 0u
-                                            : ((mk[q >> 1] >> (16 * (q & 1))) & 0x7FFFu) != 0u);
-        bits |= static_cast<uint32_t>(live) << q;
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t v = s + g + (q >= 2 ? 8u : 0u);
+            const bool live = v < vend && (MM == kMaskF32 ? (mk[q] & 0x7FFFFFFFu) != 0u
+                                                          : ((mk[q >> 1] >> (16 * (q & 1))) & 0x7FFFu) != 0u);
+            bits |= static_cast<uint32_t>(live) << q;
+        }
     }
     return bits;
 }
@@ -146,15 +168,19 @@ __device__ __forceinline__ uint32_t full_pos(uint32_t g, uint32_t t, int q) {
 
 // Liveness bits (bit q) of lane (g,t)'s accumulator elements, read from the
 // group's 128 mask values staged in shared memory.
-template <uint32_t K, bool MF32>
+template <uint32_t K, int MM>
 __device__ __forceinline__ uint32_t ring_live(const unsigned char* m, uint32_t g, uint32_t t) {
     uint32_t bits = 0;
+    if constexpr (MM == kLive) {
+        bits = live_bits(m[g], m[g + 8], t);  // m: the group's 16 liveness bytes
+    } else {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const uint32_t p = full_pos<K>(g, t, q);
-        const bool live = MF32 ? (reinterpret_cast<const uint32_t*>(m)[p] & 0x7FFFFFFFu) != 0u
-                               : (reinterpret_cast<const unsigned short*>(m)[p] & 0x7FFFu) != 0u;
-        bits |= static_cast<uint32_t>(live) << q;
+        for (int q = 0; q < 4; ++q) {
+            const uint32_t p = full_pos<K>(g, t, q);
+            const bool live = MM == kMaskF32 ? (reinterpret_cast<const uint32_t*>(m)[p] & 0x7FFFFFFFu) != 0u
+                                             : (reinterpret_cast<const unsigned short*>(m)[p] & 0x7FFFu) != 0u;
+            bits |= static_cast<uint32_t>(live) << q;
+        }
     }
     return bits;
 }
@@ -167,10 +193,12 @@ __device__ __forceinline__ void full_store(void* out, uint64_t slot0, const floa
         out_store<OF32>(out, slot0 + full_pos<K>(g, t, q), (live >> q) & 1u ? acc[q] : dead);
 }
 
-// Bytes of one ring slot: BV column indices + BV*8 mask values.
-template <int NSC, bool MF32>
+// Bytes of one ring slot: BV column indices + BV*8 mask values, or BV
+// liveness bytes + one spare word (they are copied as aligned 4-byte words).
+template <int NSC, int MM>
 constexpr uint32_t ring_slot_bytes() {
-    return 16u * (NSC == 1 ? 4u : 2u) * (4u + 8u * (MF32 ? 4u : 2u));
+    constexpr uint32_t BV = 16u * (NSC == 1 ? 4u : 2u);
+    return MM == kLive ? (BV * 4u + BV + 4u + 15u) / 16u * 16u : BV * (4u + 8u * (MM == kMaskF32 ? 4u : 2u));
 }
 
 // ---------------------------------------------------------------- FP16
@@ -248,7 +276,7 @@ __device__ __forceinline__ void tf32_tile_mma(const Tf32Tile<NSC>& x, const uint
 }
 
 // One kernel body for both precisions; Tile/loader/mma chosen by TF32.
-template <bool TF32, int NSC, bool MF32, bool OF32>
+template <bool TF32, int NSC, int MM, bool OF32>
 __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
     using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
@@ -288,7 +316,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
         c[1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
     };
     // one group: prefetched pass 0 + (rare) extra passes loaded in place
-    constexpr int MW = kMaskWords<MF32>;
+    constexpr int MW = kMaskWords<MM>;
     auto group = [&](uint32_t s, const uint32_t (&c)[2], const Tile& x0, const uint32_t (&mk)[MW]) {
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
         mma(x0, ar0, acc);
@@ -301,7 +329,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
                 mma(x, arp, acc);
             }
         }
-        const uint32_t live = slow_live<MF32>(mk, s, vend, g);
+        const uint32_t live = slow_live<MM>(mk, s, vend, g, t);
         sddmm_store<TF32 ? 4u : 8u, OF32>(a.out, acc, live, a.dead, vbase, nvw, vend, s, g, t);
     };
 
@@ -316,8 +344,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     // batch of a window takes the general one.
     constexpr int D = NSC == 1 ? 4 : 2;
     constexpr uint32_t BV = 16 * D;
-    constexpr uint32_t MSZ = MF32 ? 4 : 2;
-    constexpr uint32_t SLOT = ring_slot_bytes<NSC, MF32>();
+    constexpr uint32_t MSZ = MM == kMaskF32 ? 4 : 2;
+    constexpr uint32_t SLOT = ring_slot_bytes<NSC, MM>();
     unsigned char* wring = ring_all + warp * kRing * SLOT;
     auto ring_cols = [&](uint32_t slot) { return reinterpret_cast<uint32_t*>(wring + slot * SLOT); };
     auto ring_mask = [&](uint32_t slot) { return wring + slot * SLOT + BV * 4; };
@@ -333,14 +361,26 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
                          : "memory");
         }
         if (sb + BV <= vend) {
-            const unsigned char* src = static_cast<const unsigned char*>(a.mask) + (vbase + 8ull * sb) * MSZ;
-            unsigned char* dst = ring_mask(slot);
+            if constexpr (MM == kLive) {
+                // the batch's BV liveness bytes, as the aligned words covering them
+                const uint8_t* src = a.live + vbase / 8 + sb;
+                const uint32_t* w0 = reinterpret_cast<const uint32_t*>(reinterpret_cast<uintptr_t>(src) & ~uintptr_t(3));
+                unsigned char* dst = ring_mask(slot);
+                if (lane <= BV / 4)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + 4 * lane))),
+                                 "l"(w0 + lane)
+                                 : "memory");
+            } else {
+                const unsigned char* src = static_cast<const unsigned char*>(a.mask) + (vbase + 8ull * sb) * MSZ;
+                unsigned char* dst = ring_mask(slot);
 #pragma unroll
-            for (uint32_t c = lane; c < BV * 8 * MSZ / 16; c += 32)
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                                 static_cast<uint32_t>(__cvta_generic_to_shared(dst + 16 * c))),
-                             "l"(src + 16 * c)
-                             : "memory");
+                for (uint32_t c = lane; c < BV * 8 * MSZ / 16; c += 32)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                     static_cast<uint32_t>(__cvta_generic_to_shared(dst + 16 * c))),
+                                 "l"(src + 16 * c)
+                                 : "memory");
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -353,7 +393,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
             cg[d][1] = rc[16 * d + g + 8];
             if constexpr (TF32) tf32_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
             else f16_tile_load<NSC>(a, cg[d][0], true, cg[d][1], true, 0, t, x[d]);
-            live[d] = ring_live<TF32 ? 4u : 8u, MF32>(ring_mask(slot) + 128u * d * MSZ, g, t);
+            if constexpr (MM == kLive)
+                live[d] = ring_live<TF32 ? 4u : 8u, MM>(ring_mask(slot) + ((vbase / 8 + sb) & 3u) + 16u * d, g, t);
+            else
+                live[d] = ring_live<TF32 ? 4u : 8u, MM>(ring_mask(slot) + 128u * d * MSZ, g, t);
         }
     };
     auto consume_full = [&](uint32_t sb, const Tile (&x)[D], const uint32_t (&live)[D], const uint32_t (&cg)[D][2]) {
@@ -419,7 +462,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
                 cg[d][1] = rc[16 * d + g + 8];
                 if (s < vend) {
                     load(s, cg[d], 0, x[d]);
-                    mask_prefetch<TF32 ? 4u : 8u, MF32>(a, vbase, nvw, vend, s, g, t, mk[d]);
+                    mask_prefetch<TF32 ? 4u : 8u, MM>(a, vbase, nvw, vend, s, g, t, mk[d]);
                 }
             }
 #pragma unroll
@@ -436,13 +479,43 @@ template <bool TF32, int NSC>
 void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>(std::min<uint64_t>((a.n_items + kWarps - 1) / kWarps,
                                                              uint64_t(num_sms()) * kMinBlocks<NSC>)));
-    const size_t sm32 = kWarps * kRing * ring_slot_bytes<NSC, true>();
-    const size_t sm16 = kWarps * kRing * ring_slot_bytes<NSC, false>();
-    if (mf32 && of32) sddmm_kernel<TF32, NSC, true, true><<<grid, kWarps * 32, sm32, s>>>(a);
-    else if (mf32) sddmm_kernel<TF32, NSC, true, false><<<grid, kWarps * 32, sm32, s>>>(a);
-    else if (of32) sddmm_kernel<TF32, NSC, false, true><<<grid, kWarps * 32, sm16, s>>>(a);
-    else sddmm_kernel<TF32, NSC, false, false><<<grid, kWarps * 32, sm16, s>>>(a);
+    const size_t sm32 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF32>();
+    const size_t sm16 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF16>();
+    const size_t sml = kWarps * kRing * ring_slot_bytes<NSC, kLive>();
+    if (a.live) {
+        if (of32) sddmm_kernel<TF32, NSC, kLive, true><<<grid, kWarps * 32, sml, s>>>(a);
+        else sddmm_kernel<TF32, NSC, kLive, false><<<grid, kWarps * 32, sml, s>>>(a);
+    } else if (mf32 && of32) sddmm_kernel<TF32, NSC, kMaskF32, true><<<grid, kWarps * 32, sm32, s>>>(a);
+    else if (mf32) sddmm_kernel<TF32, NSC, kMaskF32, false><<<grid, kWarps * 32, sm32, s>>>(a);
+    else if (of32) sddmm_kernel<TF32, NSC, kMaskF16, true><<<grid, kWarps * 32, sm16, s>>>(a);
+    else sddmm_kernel<TF32, NSC, kMaskF16, false><<<grid, kWarps * 32, sm16, s>>>(a);
     TCS_LAUNCHED(TF32 ? "sddmm_tf32" : "sddmm_f16");
+}
+
+// Liveness byte of every stored vector (bit r = row r's stored value is
+// nonzero; -0.0 is not live, ref sddmm.hpp:131), one thread per vector.
+template <typename V>
+__global__ void live_build(const uint32_t* __restrict__ rp, uint64_t W, const V* __restrict__ vals, uint64_t nv,
+                           uint32_t k, uint8_t* __restrict__ live) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = W;  // window: rp[lo] <= p < rp[lo + 1]
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) / 2;
+            if (rp[mid] <= p) lo = mid; else hi = mid;
+        }
+        const uint32_t base = rp[lo], j = static_cast<uint32_t>(p - base), nvw = rp[lo + 1] - base;
+        const uint32_t b = j / k, jj = j % k, width = min(k, nvw - b * k);
+        const uint64_t off = 8ull * (base + b * k) + jj;
+        uint32_t bits = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const V x = vals[off + r * width];
+            const bool nz = sizeof(V) == 2 ? (static_cast<uint32_t>(x) & 0x7FFFu) != 0u
+                                           : (static_cast<uint32_t>(x) & 0x7FFFFFFFu) != 0u;
+            bits |= static_cast<uint32_t>(nz) << r;
+        }
+        live[p] = static_cast<uint8_t>(bits);
+    }
 }
 
 }  // namespace
@@ -471,9 +544,30 @@ void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64
 // Runs the SDDMM of `mask` into out_values (8*nv values of out_dtype).
 // `dead`: the value of stored slots whose mask value is 0 (0 for tcs_sddmm,
 // -inf for the fused softmax, which then needs no mask re-read).
-void sddmm_launch(const tcs_mebcrs* mask, const Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
+// Liveness bytes of the mask's current values, cached in its work list
+// (TCS_CFG_STATIC_MASK: the caller guarantees the values do not change
+// between calls that reuse the cache).
+const uint8_t* mask_liveness(const tcs_mebcrs* mask, Plan* plan, cudaStream_t s) {
+    if (plan->live && plan->live_src == mask->values) return plan->live;
+    const uint64_t nv = mask->num_vectors;
+    if (!plan->live) plan->live = static_cast<uint8_t*>(dalloc(nv + 16, s));
+    TCS_CUDA(cudaMemsetAsync(plan->live + nv, 0, 16, s));
+    const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((nv + 255) / 256, uint64_t(num_sms()) * 16)));
+    if (mask->value_dtype == TCS_DTYPE_F16)
+        live_build<unsigned short><<<grid, 256, 0, s>>>(mask->row_pointers, mask->num_windows,
+                                                        static_cast<const unsigned short*>(mask->values), nv, mask->k,
+                                                        plan->live);
+    else
+        live_build<uint32_t><<<grid, 256, 0, s>>>(mask->row_pointers, mask->num_windows,
+                                                  static_cast<const uint32_t*>(mask->values), nv, mask->k, plan->live);
+    TCS_LAUNCHED("sddmm_live_build");
+    plan->live_src = mask->values;
+    return plan->live;
+}
+
+void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
                   int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
-                  void* out_values, tcs_dtype out_dtype, float dead, cudaStream_t s) {
+                  void* out_values, tcs_dtype out_dtype, float dead, bool static_mask, cudaStream_t s) {
     const uint64_t nv = mask->num_vectors;
     const size_t ow = out_dtype == TCS_DTYPE_F16 ? 2 : 4;
     if (!nv) return;
@@ -513,9 +607,10 @@ void sddmm_launch(const tcs_mebcrs* mask, const Plan* plan, const void* a, tcs_d
     TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, sizeof(uint32_t), s));
     SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
                    ap, alda, bp, bldb, out_values, mask->rows,
-                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead};
+                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr};
     const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
     if (!plan->n_items) return;
+    if (static_mask) args.live = mask_liveness(mask, plan, s);
     if (tf32) {
         if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
         else launch_sddmm<true, 2>(args, mf32, of32, s);
@@ -559,8 +654,10 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
                 cudaStream_t s;
                 ~PlanGuard() { free_plan(p, s); }
             } pg{tmp_plan, s};
+            // a temporary plan cannot keep a liveness cache
+            const bool static_mask = (cfg->flags & TCS_CFG_STATIC_MASK) && !tmp_plan;
             sddmm_launch(mask, plan, a, a_dtype, lda, a_rows, bt, bt_dtype, ldbt, bt_rows, f_a, o.values, out_dtype,
-                         0.f, s);
+                         0.f, static_mask, s);
         }
         // ref sddmm.hpp:121: one MMA per (16-vector group, k-step)
         if (counters) counters->mma_invocations = mask->num_groups16 * ((f_a + mask->k - 1) / mask->k);

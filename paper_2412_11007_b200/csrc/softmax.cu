@@ -448,7 +448,7 @@ extern "C" tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* 
                 x = xbuf.p;
             }
             sddmm_launch(mask, plan, a, a_dtype, lda, a_rows, bt, bt_dtype, ldbt, bt_rows, f_a, x, score_dtype,
-                         -INFINITY, s);
+                         -INFINITY, (cfg->flags & TCS_CFG_STATIC_MASK) && !tmp_plan, s);
             if (plan->n_items) {
                 if (mask->k == 4) run_fused<4, float>(mask, x, o.values, out_dtype, scale, plan, s);
                 else if (score_dtype == TCS_DTYPE_F32) run_fused<8, float>(mask, x, o.values, out_dtype, scale, plan, s);

@@ -114,6 +114,11 @@ struct Plan {
     uint64_t n_split = 0;
     WorkItem* items = nullptr;      // device
     SplitWindow* split = nullptr;   // device
+    // SDDMM liveness bytes of the values at `live_src` (TCS_CFG_STATIC_MASK),
+    // built on first use; rebuilt when a handle sharing this plan brings
+    // other values.
+    uint8_t* live = nullptr;        // device, num_vectors + 16
+    const void* live_src = nullptr;
 };
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16);
@@ -141,9 +146,9 @@ inline cudaStream_t st(tcs_stream_t s) { return reinterpret_cast<cudaStream_t>(s
 void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda, int64_t a_rows, int64_t f_a,
                  const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t f_b, tcs_dtype out_dtype,
                  const tcs_kernel_config* cfg);
-void sddmm_launch(const tcs_mebcrs* mask, const Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
+void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
                   int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
-                  void* out_values, tcs_dtype out_dtype, float dead, cudaStream_t s);
+                  void* out_values, tcs_dtype out_dtype, float dead, bool static_mask, cudaStream_t s);
 
 }  // namespace tcs
 

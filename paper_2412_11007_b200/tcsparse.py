@@ -77,9 +77,10 @@ class KernelConfig:
     vector_height: int = 8
     mapping: ThreadMapping = ThreadMapping.coalesced
     path: str = "auto"  # SpMM instruction path: auto | mma_sync | tcgen05 (tcs.h TCS_CFG_PATH_*)
+    static_mask: bool = False  # SDDMM: mask values fixed across calls -> cached liveness bytes (TCS_CFG_STATIC_MASK)
 
     def _c(self):
-        flags = {"auto": 0, "mma_sync": 1, "tcgen05": 2}[self.path]
+        flags = {"auto": 0, "mma_sync": 1, "tcgen05": 2}[self.path] | (8 if self.static_mask else 0)
         return _abi.tcs_kernel_config(int(self.precision), int(self.vector_height), int(self.mapping), flags)
 
 

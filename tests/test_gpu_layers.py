@@ -144,6 +144,9 @@ def _fused_case(m, p, score_dt, out_dt, scale, F=24):
     ops = T.SddmmOperands(me, A, Bt)
     cfg = T.KernelConfig(T.Precision(p))
     fused = T.sddmm_row_softmax(ops, scale, cfg, score_dtype=score_dt, out_dtype=out_dt)
+    static = T.sddmm_row_softmax(ops, scale, T.KernelConfig(T.Precision(p), static_mask=True),
+                                 score_dtype=score_dt, out_dtype=out_dt)
+    assert np.array_equal(static.to_host()[2].view(np.uint32), fused.to_host()[2].view(np.uint32))
     scores = T.sddmm(ops, cfg, out_dtype=score_dt).output
     two = T.row_softmax(scores, me, scale, out_dt)
     return fused.to_host()[2], two.to_host()[2]

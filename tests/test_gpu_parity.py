@@ -322,3 +322,32 @@ def test_srbcrs_padding_inert_and_upload():
             T.spmm(sr, torch.ones(199, 16, device="cuda"), cfg)
         with pytest.raises(T.ArgumentError):
             T.spmm(sr, torch.ones(200, 16, device="cuda"), T.KernelConfig(T.Precision(1 - p)))
+
+
+def test_sddmm_static_mask_matches_reference(golden):
+    """TCS_CFG_STATIC_MASK (liveness bytes cached in the work list) gives the
+    reference's SDDMM bit for bit, incl. explicit 0.0 / -0.0 mask entries
+    (kat_zero_mask) and both value storages; the cache follows the values
+    (an SDDMM output used as the next mask gets its own liveness)."""
+    params = cases.acceptance6_params()
+    todo = [c for c in cases.kat_cases() if c.A is not None]
+    todo += [cases.acceptance6_case(i, params) for i in range(0, 100, 4)]
+    for case in todo:
+        rec = golden["cases"][case.name]
+        for p in case.precisions:
+            tag = "fp16" if p == 0 else "tf32"
+            for vdt in ((F32, F16) if p == 0 else (F32,)):
+                me = T.encode_mebcrs(dev_csr(case.csr), T.Precision(p), vdt)
+                ops = T.SddmmOperands(me, torch.from_numpy(case.A).cuda(), torch.from_numpy(case.Bt).cuda())
+                cfg = T.KernelConfig(T.Precision(p), static_mask=True)
+                for _ in range(2):
+                    res = T.sddmm(ops, cfg)
+                    assert cases.sha(res.output.to_host()[2]) == rec[f"sddmm_{tag}"]["sha"], (case.name, vdt)
+                # the output (same structure and work list, other values) as the next mask
+                ops2 = T.SddmmOperands(res.output, ops.a, ops.b_t)
+                want = T.sddmm(ops2, T.KernelConfig(T.Precision(p))).output.to_host()[2]
+                got = T.sddmm(ops2, cfg).output.to_host()[2]
+                assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), case.name
+                again = T.sddmm(ops, cfg).output.to_host()[2]
+                assert cases.sha(again) == rec[f"sddmm_{tag}"]["sha"], case.name
+                me.free()

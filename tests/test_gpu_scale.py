@@ -84,9 +84,14 @@ def test_hub_windows_bit_exact(p, n):
                 assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (path, dense.dtype)
     A = O.generate_random_dense(m.rows, 32, 6)
     Bt = O.generate_random_dense(m.cols, 32, 7)
-    out = T.sddmm(T.SddmmOperands(me, torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda()),
-                  T.KernelConfig(T.Precision(p))).output.to_host()[2]
-    assert np.array_equal(out.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32))
+    want_s = O.sddmm(ref, A, Bt)
+    ops = T.SddmmOperands(me, torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda())
+    out = T.sddmm(ops, T.KernelConfig(T.Precision(p))).output.to_host()[2]
+    assert np.array_equal(out.view(np.uint32), want_s.view(np.uint32))
+    # TCS_CFG_STATIC_MASK: liveness bytes built on the first call, cached after
+    for _ in range(2):
+        out = T.sddmm(ops, T.KernelConfig(T.Precision(p), static_mask=True)).output.to_host()[2]
+        assert np.array_equal(out.view(np.uint32), want_s.view(np.uint32))
 
 
 @pytest.mark.parametrize("p", [0, 1])

@@ -49,6 +49,8 @@ if "c3" in which:
             Bt = G.dense(cols, 32, 5)
             ov = torch.empty(8 * me.num_vectors, device="cuda")
             out["c3_sddmm_fp16_f32"] = timed(lambda: T.sddmm(T.SddmmOperands(me, A, Bt), T.KernelConfig(), out_values=ov))
+            sm = T.KernelConfig(static_mask=True)
+            out["c3_sddmm_fp16_f32_static"] = timed(lambda: T.sddmm(T.SddmmOperands(me, A, Bt), sm, out_values=ov))
             del A, Bt, ov
         me.free()
         del B, C
