@@ -335,6 +335,19 @@ tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtyp
                                  int64_t bt_rows, int64_t f_b, float scale, tcs_dtype score_dtype, tcs_mebcrs* out,
                                  tcs_dtype out_dtype, const tcs_kernel_config* cfg, tcs_stream_t stream);
 
+/* AGNN aggregation (no reference counterpart):
+ *   C[rows x n] (f32, stride ldc) = row_softmax(scale * S) . Hc,
+ *   S = Hn Hn^T sampled at the mask's live slots (tcs_sddmm's rule),
+ * bit for bit the result of tcs_sddmm_row_softmax(mask, Hn, Hn, scale,
+ * binary16 scores, binary16 P) followed by tcs_spmm(P, Hc), without
+ * writing P: the softmax is applied to each sparse value inside the SpMM.
+ * FP16 masks only (ARGUMENT otherwise); the mask must be square (SHAPE).
+ * Hn [rows x f] (stride ldhn), Hc [rows x n] (stride ldhc), F16 or F32
+ * (rounded RNE to binary16).  cfg->flags may carry TCS_CFG_STATIC_MASK. */
+tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype hn_dtype, int64_t ldhn, int64_t rows,
+                              int64_t f, float scale, const void* hc, tcs_dtype hc_dtype, int64_t ldhc, int64_t n,
+                              float* c, int64_t ldc, const tcs_kernel_config* cfg, tcs_stream_t stream);
+
 /* AGNN input transform (no reference counterpart): hn[i] = h[i] /
  * max(||h[i]||_2, eps) and hc[i] = h[i], rounded to out_dtype (F16/F32),
  * from one read of the f32 rows h [rows][ldh].  hn or hc may be NULL. */

@@ -310,6 +310,46 @@ __global__ void __launch_bounds__(256) softmax_finish(const WorkItem* __restrict
     }
 }
 
+// ---- statistics only (the AGNN aggregation applies the softmax inside the
+// SpMM, spmm_f16_softmax): per row (m, 1/sum), exactly the values
+// softmax_items / softmax_finish normalise with.
+template <uint32_t K, typename VS>
+__global__ void __launch_bounds__(256) softmax_stats_items(const WorkItem* __restrict__ items, uint64_t n_items,
+                                                           uint32_t* counter, const uint32_t* __restrict__ rp,
+                                                           const VS* scores, float scale, float2* __restrict__ rowstat,
+                                                           RowStat* __restrict__ part) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (;;) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(counter, 1u);
+        idx = __shfl_sync(0xffffffffu, idx, 0);
+        if (idx >= n_items) break;
+        const WorkItem it = items[idx];
+        const uint64_t vb = 8ull * __ldg(rp + it.window);
+        float m, s;
+        row_stats<K, VS, void>(scores, nullptr, vb, it.vbeg, it.vend, lane, scale, m, s);
+        if (lane < 8) {
+            if (it.slot != kNoSlot) part[8ull * it.slot + lane] = RowStat{m, s};
+            else rowstat[8ull * it.window + lane] = make_float2(m, s > 0.f ? 1.f / s : 0.f);
+        }
+    }
+}
+
+__global__ void softmax_stats_combine(const SplitWindow* __restrict__ split, uint64_t n_split,
+                                      const RowStat* __restrict__ part, float2* __restrict__ rowstat) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < 8 * n_split;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const SplitWindow sw = split[i / 8];
+        const uint32_t r = static_cast<uint32_t>(i % 8);
+        float m = -FLT_MAX, s = 0.f;
+        for (uint32_t q = 0; q < sw.nseg; ++q) {
+            const RowStat x = part[8ull * (sw.first_slot + q) + r];
+            merge(m, s, x.m, x.s);
+        }
+        rowstat[8ull * sw.window + r] = make_float2(m, s > 0.f ? 1.f / s : 0.f);
+    }
+}
+
 // scores sv (structure of sc), mask values mv (nullptr with VM = void), out
 // may alias sv.
 template <uint32_t K, typename VS, typename VM, typename VO>
@@ -363,6 +403,24 @@ void run_fused(const tcs_mebcrs* m, const void* x, void* out, tcs_dtype odt, flo
 }
 
 }  // namespace
+
+void softmax_rowstats(const tcs_mebcrs* S, const Plan* plan, float scale, float2* rowstat, cudaStream_t s) {
+    if (!plan->n_items) return;
+    DBuf ctr(sizeof(uint32_t), s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
+    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(uint32_t), s));
+    const int grid = static_cast<int>(std::min<uint64_t>((plan->n_items + 7) / 8, uint64_t(num_sms()) * 8));
+    const __half* sv = static_cast<const __half*>(S->values);
+    softmax_stats_items<8, __half><<<std::max(grid, 1), 256, 0, s>>>(plan->items, plan->n_items, ctr.as<uint32_t>(),
+                                                                      S->row_pointers, sv, scale, rowstat,
+                                                                      part.as<RowStat>());
+    TCS_LAUNCHED("softmax_stats_items");
+    if (plan->n_split) {
+        softmax_stats_combine<<<static_cast<int>(std::min<uint64_t>((8 * plan->n_split + 255) / 256, 1024)), 256, 0,
+                                s>>>(plan->split, plan->n_split, part.as<RowStat>(), rowstat);
+        TCS_LAUNCHED("softmax_stats_combine");
+    }
+}
+
 }  // namespace tcs
 
 using namespace tcs;
@@ -456,5 +514,50 @@ extern "C" tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* 
             }
         }
         *out = o;
+    });
+}
+
+// AGNN aggregation (no reference counterpart):
+//   C = row_softmax(scale * (Hn Hn^T) restricted to the mask's live slots) . Hc
+// = tcs_sddmm_row_softmax(mask, Hn, Hn, scale, binary16 scores and P) then
+// tcs_spmm(P, Hc), bit for bit, without materialising P: the SDDMM writes
+// binary16 scores with dead slots -inf, a statistics pass computes each row's
+// (max, 1/sum), and the SpMM applies the softmax to each sparse value in
+// registers.
+extern "C" tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype hn_dtype, int64_t ldhn,
+                                         int64_t rows, int64_t f, float scale, const void* hc, tcs_dtype hc_dtype,
+                                         int64_t ldhc, int64_t n, float* c, int64_t ldc,
+                                         const tcs_kernel_config* cfg, tcs_stream_t stream) {
+    return guard([&] {
+        sddmm_check(mask, hn, hn_dtype, ldhn, rows, f, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
+                    TCS_DTYPE_F16, cfg);
+        if (mask->precision != TCS_FP16) fail(TCS_ERR_ARGUMENT, "the fused AGNN aggregation runs in FP16");
+        if (mask->rows != mask->cols) fail(TCS_ERR_SHAPE, "AGNN attention needs a square adjacency");
+        if (n < 0) fail(TCS_ERR_SHAPE, "negative dimension");
+        if (hc_dtype != TCS_DTYPE_F16 && hc_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown dtype");
+        if (n > 0 && rows > 0 && (!hc || ldhc < n || !c || ldc < n)) fail(TCS_ERR_ARGUMENT, "bad dense buffer");
+        cudaStream_t s = st(stream);
+        const uint64_t nv = mask->num_vectors;
+        if (n == 0 || rows == 0) return;
+        if (!nv) {
+            TCS_CUDA(cudaMemset2DAsync(c, ldc * 4, 0, n * 4, rows, s));
+            return;
+        }
+        Plan* plan = static_cast<Plan*>(mask->plan);
+        Plan* tmp_plan = nullptr;
+        if (!plan) plan = tmp_plan = build_plan(mask, s, nullptr, nullptr, nullptr);
+        struct PlanGuard {
+            Plan* p;
+            cudaStream_t s;
+            ~PlanGuard() { free_plan(p, s); }
+        } pg{tmp_plan, s};
+        DBuf scores(8 * nv * 2, s), rowstat(8 * mask->num_windows * sizeof(float2), s);
+        sddmm_launch(mask, plan, hn, hn_dtype, ldhn, rows, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
+                     scores.p, TCS_DTYPE_F16, -INFINITY, (cfg->flags & TCS_CFG_STATIC_MASK) && !tmp_plan, s);
+        tcs_mebcrs S = *mask;
+        S.values = scores.p;
+        S.value_dtype = TCS_DTYPE_F16;
+        softmax_rowstats(&S, plan, scale, rowstat.as<float2>(), s);
+        spmm_f16_softmax(&S, plan, rowstat.as<float2>(), scale, hc, hc_dtype, ldhc, rows, n, c, ldc, s);
     });
 }

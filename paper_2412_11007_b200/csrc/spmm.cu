@@ -51,7 +51,25 @@ struct SpmmArgs {
     int64_t ldp;
     uint32_t* counter;  // per-slab work-item counters (zeroed before launch)
     uint32_t slab0;     // first feature slab of this launch (slab = slab0 + blockIdx.y)
+    // Softmax operand (SMX kernels, the AGNN aggregation): the sparse values
+    // are binary16 scores x with dead slots -inf, and each is replaced by
+    // exp(scale*x - m_r) * inv_r of its row r before the MMA -- the row
+    // softmax of softmax.cu applied in registers instead of in memory.
+    const float2* rowstat;  // per row (m, 1/sum), 8 * num_windows entries
+    float scale;
 };
+
+// One binary16 score -> its softmax value, rounded as softmax.cu stores it
+// (row_write: z = live ? scale*x : -inf; __expf(z - m) * inv; RNE to f16).
+__device__ __forceinline__ uint32_t smx_h(uint32_t h, float scale, float m, float inv) {
+    const float x = __half2float(__ushort_as_half(static_cast<unsigned short>(h)));
+    const float z = x != -INFINITY ? scale * x : -INFINITY;
+    return static_cast<uint32_t>(__half_as_ushort(__float2half_rn(__expf(z - m) * inv)));
+}
+__device__ __forceinline__ uint32_t smx_h2(uint32_t w, float scale, float m, float inv) {
+    return smx_h(w & 0xFFFFu, scale, m, inv) | (smx_h(w >> 16, scale, m, inv) << 16);
+}
+constexpr uint32_t kHalfNegInf = 0xFC00u;
 
 constexpr int kWarps = 4;
 // Resident CTAs per SM.  Narrow slabs (32 features: 64-byte gathers, few
@@ -142,7 +160,7 @@ __device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t v
 
 // Issues the gathers + sparse-value loads of the 16-vector step at s.
 // colpair holds the column indices of vectors [s - 16*half, +32).
-template <int NCHUNK, int FPL, bool VF32>
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
 __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __restrict__ Bl, uint64_t vbase,
                                           uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t, uint32_t q,
                                           uint32_t colpair, uint32_t half, F16Step<NCHUNK, FPL, VF32>& st) {
@@ -188,16 +206,22 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint32_t v = s + kslot_vec(u, t);
-            e[u] = v < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v, g) : 0u;
+            // past the item: 0, or -inf for a softmax operand (exp(-inf) = 0)
+            e[u] = v < vend ? f16_val_general<VF32>(a.vals, vbase, nvw, v, g) : (SMX ? kHalfNegInf : 0u);
         }
         st.b[0] = e[0] | (e[1] << 16);
         st.b[1] = e[2] | (e[3] << 16);
     }
 }
 
-template <int NCHUNK, int FPL, bool VF32>
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
 __device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st, float (&acc)[NCHUNK][FPL / 2][4],
-                                            uint32_t src_lane) {
+                                            uint32_t src_lane, float scale = 0.f, float sm = 0.f, float sinv = 0.f) {
+    uint32_t b0 = st.b[0], b1 = st.b[1];
+    if constexpr (SMX) {  // applied here, when the values have landed
+        b0 = smx_h2(b0, scale, sm, sinv);
+        b1 = smx_h2(b1, scale, sm, sinv);
+    }
 #pragma unroll
     for (int c = 0; c < NCHUNK; ++c)
 #pragma unroll
@@ -207,8 +231,7 @@ __device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st
             const uint32_t x1 = __shfl_sync(0xffffffffu, st.L[1][c][j], src_lane);
             const uint32_t x2 = __shfl_sync(0xffffffffu, st.L[2][c][j], src_lane);
             const uint32_t x3 = __shfl_sync(0xffffffffu, st.L[3][c][j], src_lane);
-            mma_f16_16816(acc[c][j], pack_lo(x0, x1), pack_hi(x0, x1), pack_lo(x2, x3), pack_hi(x2, x3), st.b[0],
-                          st.b[1]);
+            mma_f16_16816(acc[c][j], pack_lo(x0, x1), pack_hi(x0, x1), pack_lo(x2, x3), pack_hi(x2, x3), b0, b1);
         }
 }
 
@@ -262,7 +285,7 @@ __device__ __forceinline__ void f16_epilogue(const SpmmArgs& a, const WorkItem& 
     }
 }
 
-template <int NCHUNK, int FPL, bool VF32>
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
 __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
@@ -280,6 +303,12 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
         const uint32_t* ci = a.ci + base;
         const uint64_t vbase = 8ull * base;
         const uint32_t vend = it.vend;
+        float sm = 0.f, sinv = 0.f;  // softmax statistics of this lane's row g
+        if constexpr (SMX) {
+            const float2 st2 = a.rowstat[8ull * it.window + g];
+            sm = st2.x;
+            sinv = st2.y;
+        }
 
         float acc[NCHUNK][NJ][4];
 #pragma unroll
@@ -294,15 +323,15 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
         if (s < vend) {
             uint32_t cp0 = load_colpair(ci, s, vend, lane);       // steps s, s+16
             uint32_t cp1 = load_colpair(ci, s + 32, vend, lane);  // steps s+32, s+48
-            f16_issue(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa);
+            f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa);
             for (;;) {
-                if (s + 16 < vend) f16_issue(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb);
-                f16_compute(sa, acc, src_lane);
+                if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(sa, acc, src_lane, a.scale, sm, sinv);
                 if (s + 16 >= vend) break;
-                if (s + 32 < vend) f16_issue(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa);
+                if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa);
                 cp0 = cp1;
                 cp1 = load_colpair(ci, s + 64, vend, lane);
-                f16_compute(sb, acc, src_lane);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(sb, acc, src_lane, a.scale, sm, sinv);
                 s += 32;
                 if (s >= vend) break;
             }
@@ -595,6 +624,47 @@ void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* 
 }
 
 }  // namespace
+
+// C = softmax_rows(scale * S) . B for binary16 scores S whose dead slots are
+// -inf (an SDDMM output with dead = -inf) and per-row statistics (m, 1/sum)
+// from softmax_rowstats: the SpMM kernel applies the softmax to each sparse
+// value in registers (SMX).  Same result, bit for bit, as normalising S into
+// P with tcs_sddmm_row_softmax (binary16 P) and running tcs_spmm on P.
+void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowstat, float scale, const void* b,
+                      tcs_dtype b_dtype, int64_t ldb, int64_t b_rows, int64_t n, float* c, int64_t ldc,
+                      cudaStream_t s) {
+    if (n == 0 || S->rows == 0 || !plan->n_items) return;
+    const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
+    const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : 128;
+    const bool direct = b_dtype == TCS_DTYPE_F16 && ldb % 8 == 0 && ldb >= npad &&
+                        (reinterpret_cast<uintptr_t>(b) & 15) == 0;
+    DBuf bpad;
+    const void* bp = b;
+    int64_t bld = ldb;
+    if (!direct) {
+        bld = npad;
+        bpad = DBuf(static_cast<size_t>(std::max<int64_t>(1, b_rows)) * npad * 2, s);
+        pad_convert(b, b_dtype, ldb, bpad.p, TCS_DTYPE_F16, npad, b_rows, n, npad, s);
+        bp = bpad.p;
+    }
+    DBuf partial;
+    if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
+    const int slabs = static_cast<int>(npad / slab);
+    DBuf item_ctr(slabs * sizeof(uint32_t), s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * sizeof(uint32_t), s));
+    SpmmArgs a{plan->items, plan->n_items, S->row_pointers, S->column_indices, S->values, bp, bld,
+               c, ldc, S->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>(), 0, rowstat, scale};
+    if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
+    else if (slab == 64) launch(spmm_f16_kernel<1, 8, false, true>, a, slabs, s, "spmm_f16_softmax<64>", spmm_blocks(1, 8));
+    else launch(spmm_f16_kernel<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax<32>", spmm_blocks(1, 4));
+    if (plan->n_split) {
+        const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
+        spmm_reduce_split<<<grid, 256, 0, s>>>(plan->split, plan->n_split, partial.as<float>(), npad, c, ldc, S->rows,
+                                              n);
+        TCS_LAUNCHED("spmm_reduce_split");
+    }
+}
+
 }  // namespace tcs
 
 using namespace tcs;

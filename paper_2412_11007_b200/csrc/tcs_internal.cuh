@@ -150,6 +150,14 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
                   int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
                   void* out_values, tcs_dtype out_dtype, float dead, bool static_mask, cudaStream_t s);
 
+// AGNN aggregation pieces (softmax.cu / spmm.cu): per-row softmax
+// statistics (m, 1/sum) of binary16 scores with dead slots -inf, and the
+// SpMM that applies the softmax to its sparse operand in registers.
+void softmax_rowstats(const tcs_mebcrs* S, const Plan* plan, float scale, float2* rowstat, cudaStream_t s);
+void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowstat, float scale, const void* b,
+                      tcs_dtype b_dtype, int64_t ldb, int64_t b_rows, int64_t n, float* c, int64_t ldc,
+                      cudaStream_t s);
+
 }  // namespace tcs
 
 // ============================================================ device helpers

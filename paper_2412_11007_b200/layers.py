@@ -61,6 +61,9 @@ class AGNNLayer:
         self.mask = T.encode_mebcrs(T.CsrMatrix(rows, rows, row_ptr, col_idx, ones), precision)
         self.beta = float(beta)
         self.cfg = T.KernelConfig(precision)
+        # the adjacency mask never changes: its sampling rule is read from
+        # cached liveness bytes (TCS_CFG_STATIC_MASK)
+        self.mask_cfg = T.KernelConfig(precision, static_mask=True)
         self.precision = precision
         self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
 
@@ -75,13 +78,16 @@ class AGNNLayer:
         ops = T.SddmmOperands(self.mask, Hn, Hn)
         pdt = _abi.TCS_DTYPE_F16 if self.precision == T.Precision.fp16 else _abi.TCS_DTYPE_F32
         if fused:
-            return T.sddmm_row_softmax(ops, self.beta, self.cfg, score_dtype=pdt, out_dtype=pdt)
-        scores = T.sddmm(ops, self.cfg).output  # cos(h_i, h_j) at the edges
+            return T.sddmm_row_softmax(ops, self.beta, self.mask_cfg, score_dtype=pdt, out_dtype=pdt)
+        scores = T.sddmm(ops, self.mask_cfg).output  # cos(h_i, h_j) at the edges
         return T.row_softmax(scores, self.mask, self.beta, pdt)
 
     def __call__(self, H: torch.Tensor) -> torch.Tensor:
         # one pass over H: the normalised rows (SDDMM operand) and H itself
         # in the kernels' dtype (SpMM operand)
         Hn, Hc = T.rows_normalize(H.float().contiguous(), self.dtype)
+        if self.precision == T.Precision.fp16:
+            # SDDMM -> softmax -> SpMM without materialising P (tcs_agnn_aggregate)
+            return T.agnn_aggregate(self.mask, Hn, Hc, self.beta, self.mask_cfg)
         P = self.attention(H, Hn=Hn)
         return T.spmm(P, Hc, self.cfg).output

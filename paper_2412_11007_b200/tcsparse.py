@@ -408,6 +408,24 @@ def sddmm_row_softmax(ops: SddmmOperands, scale: float = 1.0, cfg: KernelConfig 
     return MeBcrsMatrix(h, keepalive=keep)
 
 
+def agnn_aggregate(mask: MeBcrsMatrix, hn: torch.Tensor, hc: torch.Tensor, scale: float = 1.0,
+                   cfg: KernelConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """C = row_softmax(scale * (hn hn^T) at the mask's live slots) @ hc
+    (tcs_agnn_aggregate): == spmm(sddmm_row_softmax(..., binary16 scores and
+    P), hc) bit for bit, with the softmax applied inside the SpMM."""
+    if cfg is None:
+        cfg = KernelConfig(mask.precision)
+    hn = hn if hn.stride(-1) == 1 else hn.contiguous()
+    hc = hc if hc.stride(-1) == 1 else hc.contiguous()
+    rows, n = hn.shape[0], hc.shape[1]
+    if out is None:
+        out = torch.empty((rows, n), dtype=torch.float32, device=hc.device)
+    _check(_abi.load().tcs_agnn_aggregate(C.byref(mask._h), hn.data_ptr(), _dtype_tag(hn), hn.stride(0), rows,
+                                          hn.shape[1], float(scale), hc.data_ptr(), _dtype_tag(hc), hc.stride(0), n,
+                                          out.data_ptr(), out.stride(0), C.byref(cfg._c()), _stream()))
+    return out
+
+
 def rows_normalize(h: torch.Tensor, dtype: torch.dtype = torch.float16, eps: float = 1e-12,
                    normalized: bool = True, copy: bool = True):
     """(h / max(||h_i||, eps), h) in `dtype` from one pass over the f32 rows

@@ -191,3 +191,38 @@ def test_rows_normalize_matches_torch(f):
         want = torch.nn.functional.normalize(h, dim=1)
         assert torch.equal(hc, h.to(dt))
         assert (hn.float() - want).abs().max() < (1e-3 if dt == torch.float16 else 1e-6)
+
+
+@pytest.mark.parametrize("n", [32, 20, 64, 128])
+def test_agnn_aggregate_equals_materialised_softmax(n):
+    """tcs_agnn_aggregate == spmm(sddmm_row_softmax(binary16 scores/P), Hc)
+    bit for bit: the softmax applied in the SpMM's registers rounds exactly
+    like the stored P.  Split hub windows, empty rows, dead (explicit-zero)
+    mask entries, f32 and f16 operands, static and per-call mask."""
+    rng = np.random.default_rng(n)
+    rows = 3000
+    per_row = rng.integers(0, 12, rows)
+    per_row[8:16] = 2500   # a hub window longer than the work-list segment
+    per_row[40:48] = 0     # an empty window
+    rp = np.zeros(rows + 1, np.uint32)
+    rp[1:] = np.cumsum(per_row)
+    ci = np.concatenate([np.sort(rng.choice(rows, size=d, replace=False)) for d in per_row]).astype(np.uint32)
+    vals = np.ones(ci.size, np.float32)
+    vals[::13] = 0.0  # stored, not sampled
+    m = O.Csr(rows, rows, rp, ci, vals)
+    me = T.encode_mebcrs(T.CsrMatrix(rows, rows, torch.from_numpy(rp.view(np.int32)).cuda(),
+                                     torch.from_numpy(ci.view(np.int32)).cuda(), torch.from_numpy(vals).cuda()),
+                         T.Precision.fp16)
+    g = torch.Generator(device="cuda").manual_seed(n)
+    hn = torch.nn.functional.normalize(torch.randn(rows, 24, device="cuda", generator=g), dim=1)
+    hc = torch.randn(rows, n, device="cuda", generator=g)
+    for static in (False, True):
+        cfg = T.KernelConfig(T.Precision.fp16, static_mask=static)
+        for a_dt in (torch.float32, torch.float16):
+            P = T.sddmm_row_softmax(T.SddmmOperands(me, hn.to(a_dt), hn.to(a_dt)), 0.9, cfg, score_dtype=0,
+                                    out_dtype=0)
+            want = T.spmm(P, hc.half(), T.KernelConfig()).output
+            for h_dt in (torch.float32, torch.float16):
+                got = T.agnn_aggregate(me, hn.to(a_dt), hc.to(h_dt), 0.9, cfg)
+                assert torch.equal(got, want), (static, a_dt, h_dt)
+    assert m.nnz == ci.size
