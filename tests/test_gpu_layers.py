@@ -181,7 +181,7 @@ def test_fused_sddmm_softmax_split_windows():
         assert np.abs(got - want).max() < 1e-5 + 1e-4 * np.abs(want).max()
 
 
-@pytest.mark.parametrize("f", [1, 32, 45, 130])
+@pytest.mark.parametrize("f", [1, 12, 32, 45, 128, 130])
 def test_rows_normalize_matches_torch(f):
     g = torch.Generator(device="cuda").manual_seed(f)
     h = torch.randn(1000, f, device="cuda", generator=g)
