@@ -184,6 +184,18 @@ tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream);
  * (copies them back; test/debug use).  Returns TCS_ERR_FORMAT on violation. */
 tcs_status tcs_mebcrs_validate(const tcs_mebcrs* m, tcs_stream_t stream);
 
+/* ref: decode_mebcrs(const MeBcrsMatrix&) (mebcrs.hpp:116-138): device
+ * ME-BCRS -> device CSR (library-allocated arrays, release with
+ * tcs_csr_free).  Every stored value != 0 becomes an entry (+-0.0 fill is
+ * dropped), rows sorted by column, f32 values (binary16 storage widened).
+ * The arrays are assumed valid (the reference validates first:
+ * tcs_mebcrs_validate). */
+tcs_status tcs_mebcrs_decode(const tcs_mebcrs* m, tcs_csr* out, tcs_stream_t stream);
+/* Copies a device CSR into caller-sized host arrays (rows+1, nnz, nnz); any
+ * pointer may be NULL.  Synchronises. */
+tcs_status tcs_csr_download(const tcs_csr* m, uint32_t* row_ptr, uint32_t* col_idx, float* values,
+                            tcs_stream_t stream);
+
 /* Releases the arrays flagged as owned and the work list; zeroes *m. */
 tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream);
 

@@ -96,6 +96,28 @@ inline MeBcrsMatrix encode_mebcrs(const CsrMatrix& m, Precision p) {
     return out;
 }
 
+/// ref mebcrs.hpp:117 -- ME-BCRS -> CSR on the GPU (stored zeros dropped).
+inline CsrMatrix decode_mebcrs(const MeBcrsMatrix& m) {
+    m.validate();  // the reference's FormatError checks, in its order
+    tcs_mebcrs d{};
+    detail::check(tcs_mebcrs_upload(m.rows, m.cols, static_cast<tcs_precision>(m.precision), m.row_pointers.data(),
+                                    m.column_indices.data(), m.values.data(), &d, nullptr));
+    tcs_csr c{};
+    tcs_status s = tcs_mebcrs_decode(&d, &c, nullptr);
+    tcs_mebcrs_free(&d, nullptr);
+    detail::check(s);
+    CsrMatrix out;
+    out.rows = m.rows;
+    out.cols = m.cols;
+    out.row_ptr.resize(m.rows + 1);
+    out.col_idx.resize(c.nnz);
+    out.values.resize(c.nnz);
+    s = tcs_csr_download(&c, out.row_ptr.data(), out.col_idx.data(), out.values.data(), nullptr);
+    tcs_csr_free(&c, nullptr);
+    detail::check(s);
+    return out;
+}
+
 /// ref spmm.hpp:173 -- C = A * B with the 8x1 swap-and-transpose kernel.
 inline SpmmResult spmm(const MeBcrsMatrix& sparse, const DenseMatrix& dense, const KernelConfig& cfg) {
     const tcs_kernel_config kc = detail::config(cfg);

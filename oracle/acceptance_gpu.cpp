@@ -125,6 +125,7 @@ bool criterion7() {  // tests/acceptance.cpp:240-273 (its value draws; reference
             if (sr_out.counters.mma_invocations != spmm(sr_ref, dense, {p, 8, ThreadMapping::coalesced}).counters.mma_invocations)
                 return false;
             if (decode_mebcrs(me) != m) return false;
+            if (gpu::decode_mebcrs(me) != m) return false;  // GPU decode round trip
         }
     }
     return true;

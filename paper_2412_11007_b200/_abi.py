@@ -104,6 +104,8 @@ EXPORTS = {
     "tcs_mebcrs_prepare": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_validate": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
     "tcs_mebcrs_free": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p]),
+    "tcs_mebcrs_decode": (C.c_int, [C.POINTER(tcs_mebcrs), C.POINTER(tcs_csr), C.c_void_p]),
+    "tcs_csr_download": (C.c_int, [C.POINTER(tcs_csr), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tcs_spmm": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                            C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
                            C.c_void_p]),

@@ -160,6 +160,25 @@ class MeBcrsMatrix:
     def validate(self):
         _check(_abi.load().tcs_mebcrs_validate(C.byref(self._h), _stream()))
 
+    def decode(self):
+        """ref decode_mebcrs (mebcrs.hpp:116-138) on the GPU: the stored
+        values != 0 as CSR, returned as host numpy arrays (row_ptr, col_idx,
+        values) -- the reference's test-side round trip."""
+        import numpy as np
+
+        lib = _abi.load()
+        h = _abi.tcs_csr()
+        _check(lib.tcs_mebcrs_decode(C.byref(self._h), C.byref(h), _stream()))
+        try:
+            rows, nnz = int(h.rows), int(h.nnz)
+            rp = np.empty(rows + 1, np.uint32)
+            ci = np.empty(max(1, nnz), np.uint32)
+            v = np.empty(max(1, nnz), np.float32)
+            _check(lib.tcs_csr_download(C.byref(h), rp.ctypes.data, ci.ctypes.data, v.ctypes.data, _stream()))
+        finally:
+            lib.tcs_csr_free(C.byref(h), _stream())
+        return rp, ci[:nnz], v[:nnz]
+
     def free(self):
         if getattr(self, "_h", None) is not None and (self._h.flags or self._h.plan):
             _abi.load().tcs_mebcrs_free(C.byref(self._h), _stream())

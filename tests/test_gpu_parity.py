@@ -351,3 +351,24 @@ def test_sddmm_static_mask_matches_reference(golden):
                 again = T.sddmm(ops, cfg).output.to_host()[2]
                 assert cases.sha(again) == rec[f"sddmm_{tag}"]["sha"], case.name
                 me.free()
+
+
+def test_decode_matches_reference(golden):
+    """GPU decode_mebcrs (ref mebcrs.hpp:116-138) == the reference's decode
+    of the same ME-BCRS: stored zeros (fill, explicit 0.0 / -0.0 entries)
+    dropped, rows sorted; binary16 storage decodes its rounded values."""
+    params = cases.acceptance2_params()
+    todo = list(cases.kat_cases()) + [cases.acceptance2_case(i, params) for i in range(0, 200, 5)]
+    for case in todo:
+        for p in case.precisions:
+            for vdt in ((F32, F16) if p == 0 else (F32,)):
+                me = T.encode_mebcrs(dev_csr(case.csr), T.Precision(p), vdt)
+                rp, ci, v = me.decode()
+                ref_me = O.encode_mebcrs(case.csr, p)  # pinned == reference
+                if vdt == F16:
+                    ref_me = O.MeBcrs(ref_me.rows, ref_me.cols, p, ref_me.row_pointers, ref_me.column_indices,
+                                      O.round_array(ref_me.values, 0))
+                want = O.Ref.decode_mebcrs(ref_me)
+                assert np.array_equal(rp, want.row_ptr) and np.array_equal(ci, want.col_idx), (case.name, p, vdt)
+                assert np.array_equal(v.view(np.uint32), want.values.view(np.uint32)), (case.name, p, vdt)
+                me.free()

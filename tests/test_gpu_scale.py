@@ -141,6 +141,12 @@ def test_config3_full_size_properties():
                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
     want_rp = np.concatenate([[0], np.cumsum(counts.cpu().numpy())]).astype(np.uint32)
     assert np.array_equal(rp_host, want_rp)
+    # (1b) decode(encode(A)) == A (no value is 0, so nothing is dropped)
+    drp, dci, dv = me.decode()
+    assert np.array_equal(drp, rp.cpu().numpy().view(np.uint32))
+    assert np.array_equal(dci, ci.cpu().numpy().view(np.uint32))
+    assert np.array_equal(dv, v.cpu().numpy())
+    del drp, dci, dv
     # (2) integer SpMM == exact independent product
     B = G.dense(cols, 128, 3, values="int", dtype=torch.float32)
     got = T.spmm(me, B.half(), T.KernelConfig()).output
