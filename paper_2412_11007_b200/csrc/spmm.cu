@@ -80,6 +80,15 @@ constexpr int kWarps = 4;
 #endif
 constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : nchunk * fpl <= 8 ? TCS_SPMM_BPS_WIDE : 4; }
 // Feature slab of the FP16 kernel for N > 64 (experiment knob: 128 or 64).
+// Host pipeline of tcs_spmm_csr_host: at most this many window-range chunks,
+// each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
+// tail after the last upload (the last chunk's encode + SpMM + download).
+#ifndef TCS_E2E_MAX_CHUNKS
+#define TCS_E2E_MAX_CHUNKS 8
+#endif
+#ifndef TCS_E2E_CHUNK_NNZ
+#define TCS_E2E_CHUNK_NNZ (1ull << 20)
+#endif
 #ifndef TCS_SPMM_SLAB_F16
 #define TCS_SPMM_SLAB_F16 128
 #endif
@@ -878,7 +887,8 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         if (rows == 0 || n == 0) return;
 
         // chunk cut points: windows at nnz quantiles (host row_ptr)
-        const uint64_t nchunks = std::max<uint64_t>(1, std::min<uint64_t>({8, W, nnz / (1ull << 20) + 1}));
+        const uint64_t nchunks = std::max<uint64_t>(
+            1, std::min<uint64_t>({TCS_E2E_MAX_CHUNKS, W, nnz / (TCS_E2E_CHUNK_NNZ) + 1}));
         std::vector<uint64_t> wcut(nchunks + 1, 0);
         for (uint64_t i = 1; i < nchunks; ++i) {
             const uint64_t target = nnz * i / nchunks;
