@@ -25,6 +25,8 @@
 // Windows longer than plan.seg are split; partial sums are reduced in
 // segment order by spmm_reduce_split (deterministic, no atomics).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 #include <vector>
 
@@ -853,9 +855,18 @@ struct Streams {
         cudaStreamDestroy(drain);
     }
 };
+// TCS_E2E_TRACE=1 (environment): the host pipeline below prints when each
+// chunk landed / was multiplied / was drained (diagnostics).
+bool e2e_trace() {
+    static const bool on = [] {
+        const char* v = std::getenv("TCS_E2E_TRACE");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
 struct Event {
     cudaEvent_t e = nullptr;
-    Event() { TCS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    Event() { TCS_CUDA(cudaEventCreateWithFlags(&e, e2e_trace() ? cudaEventDefault : cudaEventDisableTiming)); }
     ~Event() { cudaEventDestroy(e); }
     void record(cudaStream_t s) { TCS_CUDA(cudaEventRecord(e, s)); }
     void wait_on(cudaStream_t s) { TCS_CUDA(cudaStreamWaitEvent(s, e, 0)); }
@@ -968,6 +979,22 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
                                      ss.drain));
         }
         Event joined_copy, joined_compute, joined_drain;
+        if (e2e_trace()) {
+            std::vector<Event> drained(1);
+            drained[0].record(ss.drain);
+            TCS_CUDA(cudaStreamSynchronize(ss.drain));
+            TCS_CUDA(cudaStreamSynchronize(ss.compute));
+            auto ms = [&](const Event& x) {
+                float t = 0.f;
+                cudaEventElapsedTime(&t, forked.e, x.e);
+                return t;
+            };
+            std::fprintf(stderr, "[tcs e2e] %llu chunks, B landed %.3f ms\n", (unsigned long long)nchunks, ms(b_ready));
+            for (uint64_t i = 0; i < nchunks; ++i)
+                std::fprintf(stderr, "[tcs e2e] chunk %llu: landed %.3f  computed %.3f\n", (unsigned long long)i,
+                             ms(landed[i]), ms(done[i]));
+            std::fprintf(stderr, "[tcs e2e] drained %.3f ms\n", ms(drained[0]));
+        }
         joined_copy.record(ss.copy);
         joined_compute.record(ss.compute);
         joined_drain.record(ss.drain);
