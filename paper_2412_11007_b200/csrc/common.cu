@@ -370,6 +370,9 @@ tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream) {
             dfree(m->row_pointers, s);
             dfree(m->column_indices, s);
         }
+        // a liveness cache built from these values must not outlive them
+        // (the allocator may hand the address to another handle of this plan)
+        if (auto* p = static_cast<Plan*>(m->plan); p && p->live_src == m->values) p->live_src = nullptr;
         if (m->flags & TCS_MEBCRS_OWN_VALUES) dfree(m->values, s);
         if (!(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
         std::memset(m, 0, sizeof(*m));
