@@ -46,22 +46,60 @@ constexpr uint64_t kSentinel = ~0ull;
 struct CheckOut {
     uint32_t max_window_entries;
     uint32_t bad;  // nonzero = violated invariant code (see kBadMsg)
+    // window lists by size class (K0): small (<= kSmallCap entries) in
+    // `small`, huge (> kBigCap) from the front and medium from the back of
+    // `big` -- so the big-window kernels start the longest windows first and
+    // no kernel walks (and skips) the windows of another class
+    uint32_t n_small, n_medium, n_huge;
 };
+
+// i-th window of the big list: huge ones first (front), then medium (back).
+__device__ __forceinline__ uint32_t big_window(const uint32_t* big, uint64_t W, uint32_t n_huge, uint32_t i) {
+    return i < n_huge ? big[i] : big[W - 1 - (i - n_huge)];
+}
+
+// Appends w to a list with one atomic per warp and class.
+__device__ __forceinline__ void list_push(bool mine, uint32_t w, uint32_t* counter, uint32_t* list, bool from_back,
+                                          uint64_t W) {
+    const uint32_t m = __ballot_sync(0xffffffffu, mine);
+    if (!m) return;
+    const uint32_t lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (mine) {
+        const uint32_t idx = base + __popc(m & ((1u << lane) - 1u));
+        list[from_back ? W - 1 - idx : idx] = w;
+    }
+}
 
 template <int VH>
 __global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uint64_t W, uint64_t nnz,
-                             CheckOut* out) {
+                             CheckOut* out, uint32_t* __restrict__ small, uint32_t* __restrict__ big) {
     uint32_t mx = 0, bad = 0;
-    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W; w += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r0 = VH * w, r1 = min(r0 + VH, rows);
-        uint32_t prev = rp[r0];
-        for (uint64_t r = r0 + 1; r <= r1; ++r) {
-            const uint32_t x = rp[r];
-            if (x < prev) bad = max(bad, 1u);
-            prev = x;
+    const uint64_t W32 = (W + 31) / 32 * 32;  // whole warps iterate (ballots below)
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W32; w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t n = 0;
+        bool ok = false;
+        if (w < W) {
+            const uint64_t r0 = VH * w, r1 = min(r0 + VH, rows);
+            uint32_t prev = rp[r0];
+            bool wbad = false;
+            for (uint64_t r = r0 + 1; r <= r1; ++r) {
+                const uint32_t x = rp[r];
+                if (x < prev) bad = max(bad, 1u), wbad = true;
+                prev = x;
+            }
+            if (prev > nnz) bad = max(bad, 2u), wbad = true;
+            if (!wbad) {
+                n = prev - rp[r0];
+                mx = max(mx, n);
+                ok = true;
+            }
         }
-        if (prev > nnz) bad = max(bad, 2u);
-        if (!bad) mx = max(mx, prev - rp[r0]);
+        list_push(ok && n <= kSmallCap, static_cast<uint32_t>(w), &out->n_small, small, false, W);
+        list_push(ok && n > kBigCap, static_cast<uint32_t>(w), &out->n_huge, big, false, W);
+        list_push(ok && n > kSmallCap && n <= kBigCap, static_cast<uint32_t>(w), &out->n_medium, big, true, W);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
@@ -196,14 +234,12 @@ __global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_
                                                                    uint64_t cols, uint64_t W,
                                                                    uint32_t* __restrict__ tmp_cols,
                                                                    uint32_t* __restrict__ rank,
-                                                                   uint32_t* __restrict__ nv_out, CheckOut* chk) {
+                                                                   uint32_t* __restrict__ nv_out, CheckOut* chk,
+                                                                   const uint32_t* __restrict__ small, uint32_t n_small) {
     __shared__ uint64_t bufA[kSmallCap];
     __shared__ uint64_t bufB[kSmallCap];
-    for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
-        const uint32_t n = csr_rp[min(VH * w + VH, rows)] - csr_rp[VH * w];
-        if (n > kSmallCap) continue;  // block-uniform
-        window_sort_rank<VH>(csr_rp, ci, rows, cols, w, bufA, bufB, tmp_cols, rank, nv_out, chk);
-    }
+    for (uint32_t i = blockIdx.x; i < n_small; i += gridDim.x)
+        window_sort_rank<VH>(csr_rp, ci, rows, cols, small[i], bufA, bufB, tmp_cols, rank, nv_out, chk);
 }
 
 template <int VH>
@@ -213,12 +249,14 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                                                uint64_t* __restrict__ scratch,
                                                                uint32_t* __restrict__ tmp_cols,
                                                                uint32_t* __restrict__ rank,
-                                                               uint32_t* __restrict__ nv_out, CheckOut* chk) {
+                                                               uint32_t* __restrict__ nv_out, CheckOut* chk,
+                                                               const uint32_t* __restrict__ big, uint32_t n_huge,
+                                                               uint32_t n_big) {
     extern __shared__ uint64_t smem_keys[];
-    for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    for (uint32_t i = blockIdx.x; i < n_big; i += gridDim.x) {
+        const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
-        if (n <= kSmallCap) continue;
         uint64_t *a, *b;
         if (n <= kBigCap) {
             a = smem_keys;
@@ -238,18 +276,20 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
                                                                 uint64_t cols, uint64_t W,
                                                                 uint32_t* __restrict__ tmp_cols,
                                                                 uint32_t* __restrict__ rank,
-                                                                uint32_t* __restrict__ nv_out, CheckOut* chk) {
+                                                                uint32_t* __restrict__ nv_out, CheckOut* chk,
+                                                                const uint32_t* __restrict__ big, uint32_t n_huge,
+                                                                uint32_t n_big) {
     extern __shared__ uint32_t bm_smem[];
     const uint32_t words = static_cast<uint32_t>((cols + 31) / 32);
     uint32_t* bm = bm_smem;
     uint32_t* pre = bm_smem + words;
     __shared__ uint32_t rb[VH + 1];
     const uint32_t nt = blockDim.x, wpt = (words + nt - 1) / nt;
-    for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    for (uint32_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+        const uint64_t w = big_window(big, W, n_huge, bi);
         const uint64_t r0 = VH * w;
         const uint32_t e0 = csr_rp[r0];
         const uint32_t n = csr_rp[min(r0 + VH, rows)] - e0;
-        if (n <= kSmallCap) continue;  // block-uniform
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
         for (uint32_t i = threadIdx.x; i < words; i += nt) bm[i] = 0u;
         __syncthreads();
@@ -298,10 +338,18 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 // are assembled in shared memory a tile of kScatterTile vectors at a time
 // (zero fill + scatter of the tile's entries) and written out with 16-byte
 // coalesced stores -- every value byte hits global memory exactly once.
-constexpr uint32_t kScatterTile = 4096;  // vectors per smem tile (multiple of k)
+#ifndef TCS_SCATTER_TILE
+#define TCS_SCATTER_TILE 4096
+#endif
+#ifndef TCS_SCATTER_THREADS
+#define TCS_SCATTER_THREADS 512
+#endif
+constexpr uint32_t kScatterTile = TCS_SCATTER_TILE;  // vectors per smem tile (multiple of k)
+constexpr int kScatterThreads = TCS_SCATTER_THREADS;
+constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
 
 template <int VH, typename V>
-__global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict__ csr_rp,
+__global__ void __launch_bounds__(kScatterThreads) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
                                                       uint32_t k, const uint32_t* __restrict__ rp,
                                                       const uint32_t* __restrict__ tmp_cols,
@@ -310,6 +358,7 @@ __global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
+    __shared__ uint32_t rlo[VH + 1], rhi[VH], roff[VH + 1];  // this tile's entry range per row
     constexpr uint32_t kTile = kScatterTile * 8 / VH;  // vectors per smem tile
     for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
         const uint64_t r0 = VH * w;
@@ -323,24 +372,68 @@ __global__ void __launch_bounds__(512) window_scatter(const uint32_t* __restrict
             const uint32_t tn = min(kTile, nvw - t0);  // vectors in this tile
             const uint32_t n16 = (VH * tn * sizeof(V) + 15) / 16;
             for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) tile_raw[i] = make_uint4(0, 0, 0, 0);
+            // The entries whose vector falls in this tile: within a row the
+            // rank ascends with the column, so per row they are one contiguous
+            // range (binary search) -- each entry is visited by one tile only,
+            // instead of every tile scanning the whole window (quadratic on
+            // hub windows of 10^5 vectors).
+            // block-uniform: a window of at most kRangedTiles tiles scans all of
+            // its entries per tile and keeps those of the tile (cheap for few
+            // tiles); longer (hub) windows locate the tile's range per row
+            const bool ranged = nvw > kRangedTiles * kTile;
+            if (ranged && threadIdx.x < VH) {
+                const uint32_t a = rb[threadIdx.x], z = rb[threadIdx.x + 1];
+                auto first_geq = [&](uint32_t key) {  // first entry of the row with rank >= key
+                    uint32_t lo = a, hi = z;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) / 2;
+                        if (__ldg(rank + mid) < key) lo = mid + 1; else hi = mid;
+                    }
+                    return lo;
+                };
+                rlo[threadIdx.x] = first_geq(t0);
+                rhi[threadIdx.x] = first_geq(t0 + tn);
+            }
             __syncthreads();
+            if (ranged) {
+                if (threadIdx.x == 0) {  // prefix of the per-row range lengths
+                    uint32_t acc = 0;
+                    for (int q = 0; q < VH; ++q) {
+                        roff[q] = acc;
+                        acc += rhi[q] - rlo[q];
+                    }
+                    roff[VH] = acc;
+                }
+                __syncthreads();
+            }
+            const uint32_t total = ranged ? roff[VH] : e1 - e0;
             // 4 entries in flight per thread (coalesced per sub-step)
-            for (uint32_t e4 = e0; e4 < e1; e4 += 4 * blockDim.x) {
-                uint32_t v[4];
+            for (uint32_t i4 = 0; i4 < total; i4 += 4 * blockDim.x) {
+                uint32_t v[4], e[4];
                 float x[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t e = e4 + u * blockDim.x + threadIdx.x;
-                    v[u] = e < e1 ? __ldg(rank + e) : 0xFFFFFFFFu;
-                    x[u] = e < e1 ? __ldg(csr_vals + e) : 0.f;
+                    const uint32_t i = i4 + u * blockDim.x + threadIdx.x;
+                    e[u] = 0xFFFFFFFFu;
+                    if (i < total) {
+                        if (!ranged) {
+                            e[u] = e0 + i;
+                        } else {
+                            uint32_t q = 0;
+#pragma unroll
+                            for (int qq = 1; qq < VH; ++qq) q += (i >= roff[qq]) ? 1u : 0u;
+                            e[u] = rlo[q] + (i - roff[q]);
+                        }
+                    }
+                    v[u] = e[u] != 0xFFFFFFFFu ? __ldg(rank + e[u]) : 0u;
+                    x[u] = e[u] != 0xFFFFFFFFu ? __ldg(csr_vals + e[u]) : 0.f;
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const uint32_t e = e4 + u * blockDim.x + threadIdx.x;
-                    if (v[u] < t0 || v[u] >= t0 + tn) continue;
+                    if (e[u] == 0xFFFFFFFFu || v[u] < t0 || v[u] >= t0 + tn) continue;
                     uint32_t r = 0;
 #pragma unroll
-                    for (int q = 1; q < VH; ++q) r += (e >= rb[q]) ? 1u : 0u;
+                    for (int q = 1; q < VH; ++q) r += (e[u] >= rb[q]) ? 1u : 0u;
                     const uint32_t b = v[u] / k, j = v[u] - b * k;
                     const uint32_t width = min(k, nvw - b * k);
                     tile[(b * k - t0) * VH + r * width + j] = store_cvt<V>(x[u]);
@@ -408,10 +501,11 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         uint32_t nv = 0;
         if (W) {
             // K0: row_ptr invariants + longest window
-            DBuf chk(sizeof(CheckOut), s);
+            DBuf chk(sizeof(CheckOut), s), small_list(W * 4, s), big_list(W * 4, s);
             TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
             const int g0 = static_cast<int>(std::min<uint64_t>((W + 255) / 256, uint64_t(sms) * 8));
-            window_stats<VH><<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>());
+            window_stats<VH><<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>(),
+                                                small_list.as<uint32_t>(), big_list.as<uint32_t>());
             TCS_LAUNCHED("window_stats");
             CheckOut h{};
             uint32_t ends[2] = {0, 0};
@@ -425,22 +519,27 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             DBuf tmp_cols(std::max<uint64_t>(1, nnz) * 4, s), rank(std::max<uint64_t>(1, nnz) * 4, s);
             DBuf nvw(W * 4, s);
             CheckOut* dchk = chk.as<CheckOut>();
-            const int g1 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * 16));
-            window_sort_small<VH><<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
-                                                           tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                           nvw.as<uint32_t>(), dchk);
-            TCS_LAUNCHED("window_sort_small");
-            if (h.max_window_entries > kSmallCap) {
+            const uint32_t n_big = h.n_medium + h.n_huge;
+            if (h.n_small) {
+                const int g1 = static_cast<int>(std::min<uint64_t>(h.n_small, uint64_t(sms) * 16));
+                window_sort_small<VH><<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                                                               tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
+                                                               nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>(),
+                                                               h.n_small);
+                TCS_LAUNCHED("window_sort_small");
+            }
+            if (n_big) {
                 const uint64_t words = (cols + 31) / 32;
                 if (words <= kBitmapMaxWords) {
                     const size_t smem = 2 * words * sizeof(uint32_t);
                     TCS_CUDA(cudaFuncSetAttribute(window_bitmap<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(std::max<size_t>(smem, 1))));
                     const int per_sm = std::max<int>(1, std::min<int>(4, int(200 * 1024 / std::max<size_t>(smem, 1))));
-                    const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
+                    const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
                     window_bitmap<VH><<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                                   nvw.as<uint32_t>(), dchk);
+                                                                   nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>(),
+                                                                   h.n_huge, n_big);
                     TCS_LAUNCHED("window_bitmap");
                 } else {
                     DBuf scratch;
@@ -448,10 +547,11 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                     const size_t smem = 2 * kBigCap * sizeof(uint64_t);
                     TCS_CUDA(cudaFuncSetAttribute(window_sort_big<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(smem)));
-                    const int g2 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms)));
+                    const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms)));
                     window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
-                                                                   rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk);
+                                                                   rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk,
+                                                                   big_list.as<uint32_t>(), h.n_huge, n_big);
                     TCS_LAUNCHED("window_sort_big");
                 }
             }
@@ -465,19 +565,20 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
             m.values = dalloc(std::max<uint64_t>(1, uint64_t(VH) * nv) * vw, s);
             const size_t tile_smem = size_t(kScatterTile) * 8 * vw;
-            const int per_sm = static_cast<int>(std::max<size_t>(1, (200 * 1024) / tile_smem));
+            const int per_sm = static_cast<int>(std::max<size_t>(
+                1, std::min<size_t>((200 * 1024) / tile_smem, 2048 / kScatterThreads)));
             const int g3 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
             if (value_dtype == TCS_DTYPE_F16) {
                 TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<VH, __half><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<VH, __half><<<g3, kScatterThreads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                   m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                   rank.as<uint32_t>(), m.column_indices,
                                                                   static_cast<__half*>(m.values));
             } else {
                 TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                window_scatter<VH, float><<<g3, 512, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
+                window_scatter<VH, float><<<g3, kScatterThreads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
                                                                  m.row_pointers, tmp_cols.as<uint32_t>(),
                                                                  rank.as<uint32_t>(), m.column_indices,
                                                                  static_cast<float*>(m.values));
