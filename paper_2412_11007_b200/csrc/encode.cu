@@ -338,29 +338,33 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 // are assembled in shared memory a tile of kScatterTile vectors at a time
 // (zero fill + scatter of the tile's entries) and written out with 16-byte
 // coalesced stores -- every value byte hits global memory exactly once.
-#ifndef TCS_SCATTER_TILE
-#define TCS_SCATTER_TILE 4096
-#endif
-#ifndef TCS_SCATTER_THREADS
-#define TCS_SCATTER_THREADS 512
-#endif
-constexpr uint32_t kScatterTile = TCS_SCATTER_TILE;  // vectors per smem tile (multiple of k)
-constexpr int kScatterThreads = TCS_SCATTER_THREADS;
+// Two launch shapes over the K0 size-class lists: small windows (at most
+// kSmallCap entries, so at most kSmallCap vectors) get 128-thread CTAs with a
+// kSmallCap-vector tile, many per SM -- a 512-thread CTA's barriers dominate
+// on windows of a few hundred vectors (R-MAT: 10^6 windows of ~240); big
+// windows get 512 threads and 4096-vector tiles.
+constexpr uint32_t kScatterTileBig = 4096;  // vectors per smem tile (multiple of k)
+constexpr int kScatterThreadsBig = 512;
+constexpr uint32_t kScatterTileSmall = kSmallCap;
+constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
 
-template <int VH, typename V>
-__global__ void __launch_bounds__(kScatterThreads) window_scatter(const uint32_t* __restrict__ csr_rp,
+template <int VH, typename V, int THREADS, uint32_t TILE>
+__global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
                                                       uint32_t k, const uint32_t* __restrict__ rp,
                                                       const uint32_t* __restrict__ tmp_cols,
                                                       const uint32_t* __restrict__ rank,
-                                                      uint32_t* __restrict__ out_ci, V* __restrict__ out_vals) {
+                                                      uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
+                                                      const uint32_t* __restrict__ list, bool big_list,
+                                                      uint32_t n_huge, uint32_t n_list) {
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
     __shared__ uint32_t rlo[VH + 1], rhi[VH], roff[VH + 1];  // this tile's entry range per row
-    constexpr uint32_t kTile = kScatterTile * 8 / VH;  // vectors per smem tile
-    for (uint64_t w = blockIdx.x; w < W; w += gridDim.x) {
+    constexpr uint32_t kTile = TILE * 8 / VH;  // vectors per smem tile
+    for (uint32_t li = blockIdx.x; li < n_list; li += gridDim.x) {
+        const uint64_t w = big_list ? big_window(list, W, n_huge, li) : list[li];
         const uint64_t r0 = VH * w;
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
         const uint32_t base = rp[w], nvw = rp[w + 1] - base;
@@ -447,6 +451,12 @@ __global__ void __launch_bounds__(kScatterThreads) window_scatter(const uint32_t
         }
     }
 }
+
+// Value type V of a window_scatter instantiation (for the launch helper).
+template <typename V>
+V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
+                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, uint32_t,
+                           uint32_t));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
                          "column indices must be strictly ascending within a row"};
@@ -564,24 +574,29 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             const size_t vw = value_dtype == TCS_DTYPE_F16 ? 2 : 4;
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
             m.values = dalloc(std::max<uint64_t>(1, uint64_t(VH) * nv) * vw, s);
-            const size_t tile_smem = size_t(kScatterTile) * 8 * vw;
-            const int per_sm = static_cast<int>(std::max<size_t>(
-                1, std::min<size_t>((200 * 1024) / tile_smem, 2048 / kScatterThreads)));
-            const int g3 = static_cast<int>(std::min<uint64_t>(W, uint64_t(sms) * per_sm));
+            auto scatter = [&](auto kern, int threads, uint32_t tile, const uint32_t* list, bool big, uint32_t n) {
+                if (!n) return;
+                const size_t tile_smem = size_t(tile) * 8 * vw;
+                const int per_sm = static_cast<int>(
+                    std::max<size_t>(1, std::min<size_t>((200 * 1024) / tile_smem, 2048 / threads)));
+                const int g3 = static_cast<int>(std::min<uint64_t>(n, uint64_t(sms) * per_sm));
+                TCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(tile_smem)));
+                kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
+                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
+                                                    static_cast<decltype(kern_value_type(kern))*>(m.values), list, big,
+                                                    h.n_huge, n);
+            };
             if (value_dtype == TCS_DTYPE_F16) {
-                TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, __half>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(tile_smem)));
-                window_scatter<VH, __half><<<g3, kScatterThreads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
-                                                                  m.row_pointers, tmp_cols.as<uint32_t>(),
-                                                                  rank.as<uint32_t>(), m.column_indices,
-                                                                  static_cast<__half*>(m.values));
+                scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
+                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
+                scatter(window_scatter<VH, __half, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_small);
             } else {
-                TCS_CUDA(cudaFuncSetAttribute(window_scatter<VH, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(tile_smem)));
-                window_scatter<VH, float><<<g3, kScatterThreads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k,
-                                                                 m.row_pointers, tmp_cols.as<uint32_t>(),
-                                                                 rank.as<uint32_t>(), m.column_indices,
-                                                                 static_cast<float*>(m.values));
+                scatter(window_scatter<VH, float, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
+                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
+                scatter(window_scatter<VH, float, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_small);
             }
             TCS_LAUNCHED("window_scatter");
         } else {
