@@ -129,7 +129,7 @@ __device__ __forceinline__ uint32_t check_col(const uint32_t* __restrict__ ci, u
 // src[bnd[2q+1] .. bnd[2q+2]) into dst (same span).  Every thread produces a
 // contiguous slice of the output: a merge-path binary search locates its
 // start, then a sequential two-pointer merge.  Keys are unique.
-__device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint32_t* bnd,
+__device__ __forceinline__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restrict__ dst, const uint32_t* bnd,
                            int nruns, uint32_t n) {
     const uint32_t nt = blockDim.x;
     const uint32_t ipt = (n + nt - 1) / nt;
@@ -168,7 +168,7 @@ __device__ void merge_pass(const uint64_t* __restrict__ src, uint64_t* __restric
 // rows are VH sorted runs, merged pairwise in log2(VH) passes.
 // bufA/bufB hold >= n keys each (shared or global).
 template <int VH>
-__device__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint32_t* __restrict__ ci,
+__device__ __forceinline__ void window_sort_rank(const uint32_t* __restrict__ csr_rp, const uint32_t* __restrict__ ci,
                                  uint64_t rows, uint64_t cols, uint64_t w, uint64_t* bufA, uint64_t* bufB,
                                  uint32_t* __restrict__ tmp_cols, uint32_t* __restrict__ rank,
                                  uint32_t* __restrict__ nv_out, CheckOut* chk) {
@@ -257,15 +257,15 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
         const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
-        uint64_t *a, *b;
+        // two inlined call sites, so that the shared-memory one compiles to
+        // LDS/STS instead of generic loads and stores
         if (n <= kBigCap) {
-            a = smem_keys;
-            b = smem_keys + kBigCap;
+            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + kBigCap, tmp_cols, rank, nv_out,
+                                 chk);
         } else {
-            a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
-            b = a + n;
+            uint64_t* a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
+            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, a, a + n, tmp_cols, rank, nv_out, chk);
         }
-        window_sort_rank<VH>(csr_rp, ci, rows, cols, w, a, b, tmp_cols, rank, nv_out, chk);
     }
 }
 

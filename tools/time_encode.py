@@ -11,7 +11,7 @@ import paper_2412_11007_b200.tcsparse as T  # noqa: E402
 from paper_2412_11007_b200 import graphs as G  # noqa: E402
 
 out = {}
-for name, gen in (("c3", lambda: G.power_law_csr(G.C3_REDDIT, values="real")), ("c5", lambda: G.rmat_csr(G.C5_RMAT, values="real"))):
+for name, gen in [x for x in (("c3", lambda: G.power_law_csr(G.C3_REDDIT, values="real")), ("c5", lambda: G.rmat_csr(G.C5_RMAT, values="real"))) if x[0] in (sys.argv[1:] or ["c3", "c5"])]:
     rows, cols, rp, ci, v = gen()
     csr = T.CsrMatrix(rows, cols, rp, ci, v)
     ts = []
