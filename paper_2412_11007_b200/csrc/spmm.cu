@@ -88,6 +88,9 @@ constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : 
 #ifndef TCS_E2E_MAX_CHUNKS
 #define TCS_E2E_MAX_CHUNKS 8
 #endif
+#ifndef TCS_E2E_TAIL_CUT
+#define TCS_E2E_TAIL_CUT 0
+#endif
 #ifndef TCS_E2E_CHUNK_NNZ
 #define TCS_E2E_CHUNK_NNZ (1ull << 20)
 #endif
@@ -842,16 +845,24 @@ __global__ void rebase_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t sub) {
         p[i] -= sub;
 }
 
+// Compute streams the chunks alternate over.  Two (chunk i's SpMM running
+// while the host waits in chunk i+1's encode) measured no faster than one on
+// C3: each chunk's encode + SpMM starts when it lands and the tail is the
+// last chunk's work either way.
+#ifndef TCS_E2E_STREAMS
+#define TCS_E2E_STREAMS 1
+#endif
 struct Streams {
-    cudaStream_t copy = nullptr, compute = nullptr, drain = nullptr;
+    cudaStream_t copy = nullptr, drain = nullptr;
+    cudaStream_t compute[TCS_E2E_STREAMS] = {};
     Streams() {
         TCS_CUDA(cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking));
-        TCS_CUDA(cudaStreamCreateWithFlags(&compute, cudaStreamNonBlocking));
+        for (auto& c : compute) TCS_CUDA(cudaStreamCreateWithFlags(&c, cudaStreamNonBlocking));
         TCS_CUDA(cudaStreamCreateWithFlags(&drain, cudaStreamNonBlocking));
     }
     ~Streams() {
         cudaStreamDestroy(copy);
-        cudaStreamDestroy(compute);
+        for (auto& c : compute) cudaStreamDestroy(c);
         cudaStreamDestroy(drain);
     }
 };
@@ -898,11 +909,15 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         if (rows == 0 || n == 0) return;
 
         // chunk cut points: windows at nnz quantiles (host row_ptr)
-        const uint64_t nchunks = std::max<uint64_t>(
+        // Equal chunks; with TCS_E2E_TAIL_CUT the last one is cut again at
+        // 3/4 (only the work after the last upload is exposed).
+        const uint64_t neq = std::max<uint64_t>(
             1, std::min<uint64_t>({TCS_E2E_MAX_CHUNKS, W, nnz / (TCS_E2E_CHUNK_NNZ) + 1}));
+        const bool tail_cut = TCS_E2E_TAIL_CUT && neq > 1 && W > neq;
+        const uint64_t nchunks = neq + (tail_cut ? 1 : 0);
         std::vector<uint64_t> wcut(nchunks + 1, 0);
         for (uint64_t i = 1; i < nchunks; ++i) {
-            const uint64_t target = nnz * i / nchunks;
+            const uint64_t target = i < neq ? nnz * i / neq : nnz - nnz / (4 * neq);
             uint64_t lo = wcut[i - 1], hi = W;  // first window whose start >= target
             while (lo < hi) {
                 const uint64_t mid = (lo + hi) / 2;
@@ -924,7 +939,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         Event forked;
         forked.record(s);
         forked.wait_on(ss.copy);
-        forked.wait_on(ss.compute);
+        for (auto c : ss.compute) forked.wait_on(c);
         forked.wait_on(ss.drain);
 
         Event b_ready;
@@ -945,23 +960,27 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             landed[i].record(ss.copy);
         }
         // dense operand in the kernel's storage type, once
-        b_ready.wait_on(ss.compute);
+        b_ready.wait_on(ss.compute[0]);
         const void* bdev = d_b32.p;
         tcs_dtype bdt = TCS_DTYPE_F32;
         if (f16) {
-            pad_convert(d_b32.p, TCS_DTYPE_F32, n, d_b16.p, TCS_DTYPE_F16, n, b_rows, n, n, ss.compute);
+            pad_convert(d_b32.p, TCS_DTYPE_F32, n, d_b16.p, TCS_DTYPE_F16, n, b_rows, n, n, ss.compute[0]);
             bdev = d_b16.p;
             bdt = TCS_DTYPE_F16;
         }
-        tcs_stream_t ks = reinterpret_cast<tcs_stream_t>(ss.compute);
+        Event b_conv;
+        b_conv.record(ss.compute[0]);
+        for (int q = 1; q < TCS_E2E_STREAMS; ++q) b_conv.wait_on(ss.compute[q]);
         for (uint64_t i = 0; i < nchunks; ++i) {
             const uint64_t r0 = std::min(rows, 8 * wcut[i]), r1 = std::min(rows, 8 * wcut[i + 1]);
             const uint64_t e0 = hrp[r0], e1 = hrp[r1];
-            landed[i].wait_on(ss.compute);
+            cudaStream_t cs = ss.compute[i % TCS_E2E_STREAMS];
+            tcs_stream_t ks = reinterpret_cast<tcs_stream_t>(cs);
+            landed[i].wait_on(cs);
             uint32_t* rp_i = d_rp.as<uint32_t>() + r0 + i;
             if (e0) {
                 rebase_u32<<<static_cast<unsigned>(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024)), 256, 0,
-                             ss.compute>>>(rp_i, r1 - r0 + 1, static_cast<uint32_t>(e0));
+                             cs>>>(rp_i, r1 - r0 + 1, static_cast<uint32_t>(e0));
                 TCS_LAUNCHED("rebase_u32");
             }
             tcs_csr chunk{r1 - r0, host_csr->cols, e1 - e0, rp_i, d_ci.as<uint32_t>() + e0, d_v.as<float>() + e0};
@@ -973,17 +992,18 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             tcs_mebcrs_free(&m, ks);
             if (rc != TCS_OK) fail(rc, tcs_last_error());
             if (counters) counters->mma_invocations += cn.mma_invocations;
-            done[i].record(ss.compute);
+            done[i].record(cs);
             done[i].wait_on(ss.drain);
             TCS_CUDA(cudaMemcpyAsync(c + r0 * n, d_c.as<float>() + r0 * n, (r1 - r0) * n * 4, cudaMemcpyDeviceToHost,
                                      ss.drain));
         }
-        Event joined_copy, joined_compute, joined_drain;
+        Event joined_copy, joined_drain;
+        Event joined_compute[TCS_E2E_STREAMS];
         if (e2e_trace()) {
             std::vector<Event> drained(1);
             drained[0].record(ss.drain);
             TCS_CUDA(cudaStreamSynchronize(ss.drain));
-            TCS_CUDA(cudaStreamSynchronize(ss.compute));
+            for (auto c : ss.compute) TCS_CUDA(cudaStreamSynchronize(c));
             auto ms = [&](const Event& x) {
                 float t = 0.f;
                 cudaEventElapsedTime(&t, forked.e, x.e);
@@ -996,10 +1016,10 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             std::fprintf(stderr, "[tcs e2e] drained %.3f ms\n", ms(drained[0]));
         }
         joined_copy.record(ss.copy);
-        joined_compute.record(ss.compute);
+        for (int q = 0; q < TCS_E2E_STREAMS; ++q) joined_compute[q].record(ss.compute[q]);
         joined_drain.record(ss.drain);
         joined_copy.wait_on(s);
-        joined_compute.wait_on(s);
+        for (auto& e : joined_compute) e.wait_on(s);
         joined_drain.wait_on(s);
         TCS_CUDA(cudaStreamSynchronize(s));
     });
