@@ -181,6 +181,15 @@ __global__ void plan_fill(const uint32_t* __restrict__ rp, uint64_t W, uint32_t 
 }
 }  // namespace
 
+// Shortest work item (vectors; a multiple of 16).  Small matrices split
+// their windows down to this so that enough warps share the work.  32 or 64
+// make C1 (4096^2, 65 k nnz) slower, 11.8 -> 22.6 / 17.7 us per graph-
+// replayed SpMM: the split partials and their reduction cost more than the
+// extra warps gain.
+#ifndef TCS_PLAN_MIN_SEG
+#define TCS_PLAN_MIN_SEG 256
+#endif
+
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16) {
     const uint64_t W = m->num_windows;
@@ -188,7 +197,8 @@ Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t
     // Segment length: enough items for ~64 per SM, bounded to [256, 16384]
     // vectors and a multiple of 16 (SpMM/SDDMM step granularity).
     const uint64_t target = std::max<uint64_t>(1, nv / (uint64_t(num_sms()) * 64));
-    const uint32_t seg = static_cast<uint32_t>(std::min<uint64_t>(16384, std::max<uint64_t>(256, (target + 15) / 16 * 16)));
+    const uint32_t seg = static_cast<uint32_t>(
+        std::min<uint64_t>(16384, std::max<uint64_t>(TCS_PLAN_MIN_SEG, (target + 15) / 16 * 16)));
 
     DBuf nslot((W + 1) * 4, s), nsplit((W + 1) * 4, s), slot_off((W + 1) * 4, s), split_off((W + 1) * 4, s);
     DBuf tot(sizeof(PlanTotals), s);
