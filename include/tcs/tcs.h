@@ -349,16 +349,19 @@ tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* a, tcs_dtyp
 
 /* AGNN aggregation (no reference counterpart):
  *   C[rows x n] (f32, stride ldc) = row_softmax(scale * S) . Hc,
- *   S = Hn Hn^T sampled at the mask's live slots (tcs_sddmm's rule),
- * bit for bit the result of tcs_sddmm_row_softmax(mask, Hn, Hn, scale,
- * binary16 scores, binary16 P) followed by tcs_spmm(P, Hc), without
+ *   S[i][j] = Hn[row0 + i] . Hn[j] sampled at the mask's live slots
+ *   (tcs_sddmm's rule),
+ * bit for bit the result of tcs_sddmm_row_softmax(mask, Hn[row0..], Hn,
+ * scale, binary16 scores, binary16 P) followed by tcs_spmm(P, Hc), without
  * writing P: the softmax is applied to each sparse value inside the SpMM.
- * FP16 masks only (ARGUMENT otherwise); the mask must be square (SHAPE).
- * Hn [rows x f] (stride ldhn), Hc [rows x n] (stride ldhc), F16 or F32
- * (rounded RNE to binary16).  cfg->flags may carry TCS_CFG_STATIC_MASK. */
-tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype hn_dtype, int64_t ldhn, int64_t rows,
-                              int64_t f, float scale, const void* hc, tcs_dtype hc_dtype, int64_t ldhc, int64_t n,
-                              float* c, int64_t ldc, const tcs_kernel_config* cfg, tcs_stream_t stream);
+ * The mask is the adjacency rows [row0, row0 + rows) of a graph with
+ * mask->cols nodes (row0 = 0 and rows = cols for the whole graph; a row
+ * shard otherwise).  Hn [cols x f] (stride ldhn), Hc [cols x n] (stride
+ * ldhc), F16 or F32 (rounded RNE to binary16).  FP16 masks only
+ * (ARGUMENT otherwise).  cfg->flags may carry TCS_CFG_STATIC_MASK. */
+tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype hn_dtype, int64_t ldhn, int64_t row0,
+                              int64_t rows, int64_t f, float scale, const void* hc, tcs_dtype hc_dtype, int64_t ldhc,
+                              int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg, tcs_stream_t stream);
 
 /* AGNN input transform (no reference counterpart): hn[i] = h[i] /
  * max(||h[i]||_2, eps) and hc[i] = h[i], rounded to out_dtype (F16/F32),

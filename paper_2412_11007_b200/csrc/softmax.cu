@@ -525,14 +525,18 @@ extern "C" tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* 
 // (max, 1/sum), and the SpMM applies the softmax to each sparse value in
 // registers.
 extern "C" tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype hn_dtype, int64_t ldhn,
-                                         int64_t rows, int64_t f, float scale, const void* hc, tcs_dtype hc_dtype,
-                                         int64_t ldhc, int64_t n, float* c, int64_t ldc,
+                                         int64_t row0, int64_t rows, int64_t f, float scale, const void* hc,
+                                         tcs_dtype hc_dtype, int64_t ldhc, int64_t n, float* c, int64_t ldc,
                                          const tcs_kernel_config* cfg, tcs_stream_t stream) {
     return guard([&] {
-        sddmm_check(mask, hn, hn_dtype, ldhn, rows, f, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
+        if (row0 < 0 || !mask || row0 + static_cast<int64_t>(mask->rows) > static_cast<int64_t>(mask->cols))
+            fail(TCS_ERR_SHAPE, "AGNN attention: mask rows [row0, row0 + rows) must be nodes of its columns");
+        // the mask's row i is node row0 + i: A = Hn[row0 .. row0 + rows), Bt = Hn (all nodes)
+        const size_t hw = hn_dtype == TCS_DTYPE_F16 ? 2 : 4;
+        const void* hrows = static_cast<const char*>(hn) + static_cast<size_t>(row0) * ldhn * hw;
+        sddmm_check(mask, hrows, hn_dtype, ldhn, rows, f, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
                     TCS_DTYPE_F16, cfg);
         if (mask->precision != TCS_FP16) fail(TCS_ERR_ARGUMENT, "the fused AGNN aggregation runs in FP16");
-        if (mask->rows != mask->cols) fail(TCS_ERR_SHAPE, "AGNN attention needs a square adjacency");
         if (n < 0) fail(TCS_ERR_SHAPE, "negative dimension");
         if (hc_dtype != TCS_DTYPE_F16 && hc_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown dtype");
         if (n > 0 && rows > 0 && (!hc || ldhc < n || !c || ldc < n)) fail(TCS_ERR_ARGUMENT, "bad dense buffer");
@@ -552,12 +556,13 @@ extern "C" tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn,
             ~PlanGuard() { free_plan(p, s); }
         } pg{tmp_plan, s};
         DBuf scores(8 * nv * 2, s), rowstat(8 * mask->num_windows * sizeof(float2), s);
-        sddmm_launch(mask, plan, hn, hn_dtype, ldhn, rows, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
+        sddmm_launch(mask, plan, hrows, hn_dtype, ldhn, rows, hn, hn_dtype, ldhn, static_cast<int64_t>(mask->cols), f,
                      scores.p, TCS_DTYPE_F16, -INFINITY, (cfg->flags & TCS_CFG_STATIC_MASK) && !tmp_plan, s);
         tcs_mebcrs S = *mask;
         S.values = scores.p;
         S.value_dtype = TCS_DTYPE_F16;
         softmax_rowstats(&S, plan, scale, rowstat.as<float2>(), s);
-        spmm_f16_softmax(&S, plan, rowstat.as<float2>(), scale, hc, hc_dtype, ldhc, rows, n, c, ldc, s);
+        spmm_f16_softmax(&S, plan, rowstat.as<float2>(), scale, hc, hc_dtype, ldhc, static_cast<int64_t>(mask->cols),
+                         n, c, ldc, s);
     });
 }

@@ -116,3 +116,56 @@ class ShardedSpmm:
     def __call__(self, B: torch.Tensor, gather: bool = False) -> torch.Tensor:
         C = self._T.spmm(self.me, B, self.cfg).output
         return gather_rows(C, self.shard_rows, self.group) if gather else C
+
+
+class ShardedGCNLayer:
+    """GCN layer H' = Â (H W) over all ranks (BASELINE configs[3]): every
+    rank holds the full features H (the previous layer's all-gather), does
+    the dense transform on the rows it needs (all of them: the SpMM gathers
+    arbitrary columns), aggregates its window shard of Â, and all-gathers
+    the rows for the next layer (``gather=False`` keeps them local)."""
+
+    def __init__(self, rows, row_ptr, col_idx, weight, precision=None, group=None):
+        from . import layers as L
+        from . import tcsparse as T
+
+        precision = T.Precision.fp16 if precision is None else precision
+        rp, ci, v = L.normalized_adjacency(rows, row_ptr, col_idx)
+        self.spmm = ShardedSpmm(rows, rows, rp, ci, v, precision, group)
+        self.weight = weight
+        self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
+
+    def __call__(self, H: torch.Tensor, gather: bool = True) -> torch.Tensor:
+        HW = (H.to(self.weight.dtype) @ self.weight).to(self.dtype)  # cuBLAS GEMM
+        return self.spmm(HW, gather=gather)
+
+
+class ShardedAGNNLayer:
+    """AGNN layer (BASELINE configs[4]) over all ranks: the attention rows of
+    a window shard need that shard's normalised rows against every node's,
+    so every rank holds the full H; each computes its rows with
+    tcs_agnn_aggregate (row offset = its first row) and the rows are
+    all-gathered for the next layer."""
+
+    def __init__(self, rows, row_ptr, col_idx, beta=1.0, group=None):
+        from . import tcsparse as T
+
+        self.rows = rows
+        self.group = group
+        world = dist.get_world_size(group) if dist.is_initialized() else 1
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.cuts = shard_windows(row_ptr, rows, world)
+        self.shard = shard_of(self.cuts, rank, rows)
+        self.shard_rows = [shard_of(self.cuts, r, rows).rows for r in range(world)]
+        ones = torch.ones(col_idx.numel(), dtype=torch.float32, device=col_idx.device)
+        lrp, lci, lv = local_rows(row_ptr, col_idx, ones, self.shard)
+        self.mask = T.encode_mebcrs(T.CsrMatrix(self.shard.rows, rows, lrp, lci, lv), T.Precision.fp16)
+        self.beta = float(beta)
+        self.cfg = T.KernelConfig(T.Precision.fp16, static_mask=True)
+        self._T = T
+
+    def __call__(self, H: torch.Tensor, gather: bool = True) -> torch.Tensor:
+        T = self._T
+        Hn, Hc = T.rows_normalize(H.float().contiguous(), torch.float16)
+        C = T.agnn_aggregate(self.mask, Hn, Hc, self.beta, self.cfg, row0=self.shard.r0)
+        return gather_rows(C, self.shard_rows, self.group) if gather else C

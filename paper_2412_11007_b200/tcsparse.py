@@ -428,20 +428,23 @@ def sddmm_row_softmax(ops: SddmmOperands, scale: float = 1.0, cfg: KernelConfig 
 
 
 def agnn_aggregate(mask: MeBcrsMatrix, hn: torch.Tensor, hc: torch.Tensor, scale: float = 1.0,
-                   cfg: KernelConfig | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
-    """C = row_softmax(scale * (hn hn^T) at the mask's live slots) @ hc
-    (tcs_agnn_aggregate): == spmm(sddmm_row_softmax(..., binary16 scores and
-    P), hc) bit for bit, with the softmax applied inside the SpMM."""
+                   cfg: KernelConfig | None = None, out: torch.Tensor | None = None, row0: int = 0) -> torch.Tensor:
+    """C = row_softmax(scale * (hn[row0 + i] . hn[j]) at the mask's live
+    slots) @ hc (tcs_agnn_aggregate): == spmm(sddmm_row_softmax(..., binary16
+    scores and P), hc) bit for bit, with the softmax applied inside the SpMM.
+    hn, hc hold every node; the mask holds the adjacency rows
+    [row0, row0 + mask.rows) (a row shard, or the whole graph)."""
     if cfg is None:
         cfg = KernelConfig(mask.precision)
     hn = hn if hn.stride(-1) == 1 else hn.contiguous()
     hc = hc if hc.stride(-1) == 1 else hc.contiguous()
-    rows, n = hn.shape[0], hc.shape[1]
+    rows, n = mask.rows, hc.shape[1]
     if out is None:
         out = torch.empty((rows, n), dtype=torch.float32, device=hc.device)
-    _check(_abi.load().tcs_agnn_aggregate(C.byref(mask._h), hn.data_ptr(), _dtype_tag(hn), hn.stride(0), rows,
-                                          hn.shape[1], float(scale), hc.data_ptr(), _dtype_tag(hc), hc.stride(0), n,
-                                          out.data_ptr(), out.stride(0), C.byref(cfg._c()), _stream()))
+    _check(_abi.load().tcs_agnn_aggregate(C.byref(mask._h), hn.data_ptr(), _dtype_tag(hn), hn.stride(0), int(row0),
+                                          rows, hn.shape[1], float(scale), hc.data_ptr(), _dtype_tag(hc),
+                                          hc.stride(0), n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
+                                          _stream()))
     return out
 
 
