@@ -372,3 +372,42 @@ def test_decode_matches_reference(golden):
                 assert np.array_equal(rp, want.row_ptr) and np.array_equal(ci, want.col_idx), (case.name, p, vdt)
                 assert np.array_equal(v.view(np.uint32), want.values.view(np.uint32)), (case.name, p, vdt)
                 me.free()
+
+
+@pytest.mark.parametrize("p", [0, 1])
+def test_shapes_strides_and_alignment(p):
+    """Dense widths across the slab boundaries (N = 1 .. 300: 32/64/128-
+    feature slabs, 3 slabs past 256), strided and misaligned dense operands
+    (the padding/conversion path), strided outputs, and SDDMM inner
+    dimensions across the pass boundaries (F = 1 .. 100) -- all bit-exact
+    against the oracle on small-integer inputs."""
+    m = O.generate_random_sparse(203, 157, 0.06, 41)
+    ref = O.encode_mebcrs(m, p)
+    for vdt in ((F32, F16) if p == 0 else (F32,)):
+        me = T.encode_mebcrs(dev_csr(m), T.Precision(p), vdt)
+        cfg = T.KernelConfig(T.Precision(p))
+        for n in (1, 7, 33, 64, 100, 130, 256, 300):
+            B = O.generate_random_dense(m.cols, n, 40 + n)
+            want = O.spmm(ref, B)
+            Bd = torch.from_numpy(B).cuda()
+            variants = [Bd]
+            wide = torch.zeros(m.cols, n + 5, device="cuda")
+            wide[:, :n] = Bd
+            variants.append(wide[:, :n])  # row stride n + 5
+            flat = torch.zeros(m.cols * n + 1, device="cuda")
+            flat[1:] = Bd.flatten()
+            variants.append(flat[1:].view(m.cols, n))  # misaligned by 4 bytes
+            if p == 0:
+                variants.append(Bd.half())
+            for dense in variants:
+                out = torch.full((m.rows, n + 3), 7.0, device="cuda")
+                got = T.spmm(me, dense, cfg, out=out[:, :n]).output
+                assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32)), (n, dense.stride())
+                assert torch.all(out[:, n:] == 7.0), "wrote past the output columns"
+        for f in (1, 8, 13, 33, 64, 65, 100):
+            A = O.generate_random_dense(m.rows, f, 70 + f)
+            Bt = O.generate_random_dense(m.cols, f, 80 + f)
+            got = T.sddmm(T.SddmmOperands(me, torch.from_numpy(A).cuda(), torch.from_numpy(Bt).cuda()),
+                          cfg).output.to_host()[2]
+            assert np.array_equal(got.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32)), f
+        me.free()
