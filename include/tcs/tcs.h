@@ -265,6 +265,10 @@ tcs_status tcs_srbcrs_upload(uint64_t rows, uint64_t cols, tcs_precision precisi
 tcs_status tcs_srbcrs_download(const tcs_srbcrs* m, uint32_t* row_pointer_pairs, uint32_t* column_indices,
                                float* values, tcs_stream_t stream);
 tcs_status tcs_srbcrs_free(tcs_srbcrs* m, tcs_stream_t stream);
+/* ref: decode_srbcrs (srbcrs.hpp:74-90): device CSR (library-allocated,
+ * release with tcs_csr_free) of the stored values != 0; padded vectors
+ * decode to nothing. */
+tcs_status tcs_srbcrs_decode(const tcs_srbcrs* m, tcs_csr* out, tcs_stream_t stream);
 /* ref: spmm(const SrBcrsMatrix&, const DenseMatrix&, const KernelConfig&)
  * (spmm.hpp:181-185): the swapped 8x1 kernel over the padded format;
  * padded vectors gather a zero row (the reference's kAbsentRow) and are

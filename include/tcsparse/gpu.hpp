@@ -163,6 +163,28 @@ inline SrBcrsMatrix encode_srbcrs(const CsrMatrix& m, Precision p) {
     return out;
 }
 
+/// ref srbcrs.hpp:74 -- SR-BCRS -> CSR on the GPU (padding decodes to nothing).
+inline CsrMatrix decode_srbcrs(const SrBcrsMatrix& m) {
+    tcs_srbcrs d{};
+    detail::check(tcs_srbcrs_upload(m.rows, m.cols, static_cast<tcs_precision>(m.precision),
+                                    m.row_pointer_pairs.data(), m.column_indices.data(), m.values.data(), &d,
+                                    nullptr));
+    tcs_csr c{};
+    tcs_status s = tcs_srbcrs_decode(&d, &c, nullptr);
+    tcs_srbcrs_free(&d, nullptr);
+    detail::check(s);
+    CsrMatrix out;
+    out.rows = m.rows;
+    out.cols = m.cols;
+    out.row_ptr.resize(m.rows + 1);
+    out.col_idx.resize(c.nnz);
+    out.values.resize(c.nnz);
+    s = tcs_csr_download(&c, out.row_ptr.data(), out.col_idx.data(), out.values.data(), nullptr);
+    tcs_csr_free(&c, nullptr);
+    detail::check(s);
+    return out;
+}
+
 /// ref spmm.hpp:181 -- the same swapped kernel over the padded format.
 inline SpmmResult spmm(const SrBcrsMatrix& sparse, const DenseMatrix& dense, const KernelConfig& cfg) {
     const tcs_kernel_config kc = detail::config(cfg);

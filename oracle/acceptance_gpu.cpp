@@ -120,6 +120,7 @@ bool criterion7() {  // tests/acceptance.cpp:240-273 (its value draws; reference
             if (sr.row_pointer_pairs != sr_ref.row_pointer_pairs || sr.column_indices != sr_ref.column_indices ||
                 sr.values != sr_ref.values)
                 return false;
+            if (gpu::decode_srbcrs(sr) != decode_srbcrs(sr_ref)) return false;
             const auto sr_out = gpu::spmm(sr, dense, {p, 8, ThreadMapping::coalesced});
             if (sr_out.output != me_out.output) return false;
             if (sr_out.counters.mma_invocations != spmm(sr_ref, dense, {p, 8, ThreadMapping::coalesced}).counters.mma_invocations)

@@ -84,6 +84,7 @@ EXPORTS = {
                                     C.POINTER(tcs_srbcrs), C.c_void_p]),
     "tcs_srbcrs_download": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "tcs_srbcrs_free": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p]),
+    "tcs_srbcrs_decode": (C.c_int, [C.POINTER(tcs_srbcrs), C.POINTER(tcs_csr), C.c_void_p]),
     "tcs_spmm_srbcrs": (C.c_int, [C.POINTER(tcs_srbcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                   C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
                                   C.c_void_p]),

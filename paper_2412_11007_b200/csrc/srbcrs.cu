@@ -353,3 +353,16 @@ extern "C" tcs_status tcs_spmm_srbcrs_host(uint64_t rows, uint64_t cols, tcs_pre
         TCS_CUDA(cudaStreamSynchronize(s));
     });
 }
+
+// ref decode_srbcrs (srbcrs.hpp:74-90): padded vectors hold zero values, so
+// decoding the gather view (padding -> the extra zero row `cols`) drops them
+// like every other stored zero.
+extern "C" tcs_status tcs_srbcrs_decode(const tcs_srbcrs* m, tcs_csr* out, tcs_stream_t stream) {
+    return guard([&] {
+        check_sr(m);
+        if (!out) fail(TCS_ERR_ARGUMENT, "null output");
+        tcs_status rc = tcs_mebcrs_decode(&static_cast<SrImpl*>(m->impl)->view, out, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        out->cols = m->cols;
+    });
+}

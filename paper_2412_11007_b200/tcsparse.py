@@ -164,20 +164,7 @@ class MeBcrsMatrix:
         """ref decode_mebcrs (mebcrs.hpp:116-138) on the GPU: the stored
         values != 0 as CSR, returned as host numpy arrays (row_ptr, col_idx,
         values) -- the reference's test-side round trip."""
-        import numpy as np
-
-        lib = _abi.load()
-        h = _abi.tcs_csr()
-        _check(lib.tcs_mebcrs_decode(C.byref(self._h), C.byref(h), _stream()))
-        try:
-            rows, nnz = int(h.rows), int(h.nnz)
-            rp = np.empty(rows + 1, np.uint32)
-            ci = np.empty(max(1, nnz), np.uint32)
-            v = np.empty(max(1, nnz), np.float32)
-            _check(lib.tcs_csr_download(C.byref(h), rp.ctypes.data, ci.ctypes.data, v.ctypes.data, _stream()))
-        finally:
-            lib.tcs_csr_free(C.byref(h), _stream())
-        return rp, ci[:nnz], v[:nnz]
+        return _decode_to_host(lambda h: _abi.load().tcs_mebcrs_decode(C.byref(self._h), C.byref(h), _stream()))
 
     def free(self):
         if getattr(self, "_h", None) is not None and (self._h.flags or self._h.plan):
@@ -201,6 +188,25 @@ class MeBcrsMatrix:
         _check(_abi.load().tcs_mebcrs_upload(rows, cols, int(precision), rp.ctypes.data, ci.ctypes.data,
                                              v.ctypes.data, C.byref(h), _stream()))
         return MeBcrsMatrix(h)
+
+
+def _decode_to_host(run):
+    """Runs a tcs_*_decode call into a device CSR and returns it as host
+    numpy arrays (row_ptr, col_idx, values); the device CSR is freed."""
+    import numpy as np
+
+    lib = _abi.load()
+    h = _abi.tcs_csr()
+    _check(run(h))
+    try:
+        rows, nnz = int(h.rows), int(h.nnz)
+        rp = np.empty(rows + 1, np.uint32)
+        ci = np.empty(max(1, nnz), np.uint32)
+        v = np.empty(max(1, nnz), np.float32)
+        _check(lib.tcs_csr_download(C.byref(h), rp.ctypes.data, ci.ctypes.data, v.ctypes.data, _stream()))
+    finally:
+        lib.tcs_csr_free(C.byref(h), _stream())
+    return rp, ci[:nnz], v[:nnz]
 
 
 def encode_mebcrs(csr: CsrMatrix, precision: Precision, value_dtype: int | None = None,
@@ -298,6 +304,11 @@ class SrBcrsMatrix:
         _check(_abi.load().tcs_srbcrs_download(C.byref(self._h), rpp.ctypes.data, ci.ctypes.data, v.ctypes.data,
                                                _stream()))
         return rpp[: 2 * self.num_windows], ci[: self.num_padded], v[: 8 * self.num_padded]
+
+    def decode(self):
+        """ref decode_srbcrs (srbcrs.hpp:74-90) on the GPU: host numpy
+        (row_ptr, col_idx, values) of the stored values != 0."""
+        return _decode_to_host(lambda h: _abi.load().tcs_srbcrs_decode(C.byref(self._h), C.byref(h), _stream()))
 
     def free(self):
         if getattr(self, "_h", None) is not None and self._h.impl:

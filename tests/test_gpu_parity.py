@@ -278,6 +278,11 @@ def check_srbcrs(case, rec, value_dtype):
             assert np.array_equal(v.view(np.uint32), want_v.view(np.uint32)), case.name
             if value_dtype == F32:
                 assert cases.sha(pairs, ci, v) == r_sr["sha"], case.name
+            # ref decode_srbcrs (srbcrs.hpp:74-90) == decode of the compact format
+            drp, dci, dv = sr.decode()
+            want_rp, want_ci, want_v = me.decode()
+            assert np.array_equal(drp, want_rp) and np.array_equal(dci, want_ci), case.name
+            assert np.array_equal(dv.view(np.uint32), want_v.view(np.uint32)), case.name
             if case.B is not None:
                 res = T.spmm(sr, torch.from_numpy(case.B).cuda(), T.KernelConfig(T.Precision(p)))
                 assert cases.sha(res.output.cpu().numpy()) == r_sr["spmm_sha"], case.name
