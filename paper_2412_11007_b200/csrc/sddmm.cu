@@ -28,6 +28,10 @@ namespace {
 
 using namespace dev;
 
+#ifndef TCS_SDDMM_NSC4
+#define TCS_SDDMM_NSC4 1
+#endif
+
 struct SddmmArgs {
     const WorkItem* items;
     uint64_t n_items;
@@ -58,6 +62,10 @@ constexpr int kRing = 4;  // column-index batches staged per warp
 // single-pass inner dimensions, 3 when two super-chunks are double-buffered.
 template <int NSC>
 constexpr int kMinBlocks = NSC == 1 ? 4 : 3;
+// Groups per double-buffered batch: the register budget of a batch is about
+// constant (NSC * D super-chunk tiles).
+template <int NSC>
+constexpr int kBatchGroups = NSC == 1 ? 4 : NSC == 2 ? 2 : 1;
 
 // Storage position of accumulator element q (vector g or g+8, row 2t or
 // 2t+1) of the group at s.  K (storage block width) is a compile-time
@@ -197,7 +205,7 @@ __device__ __forceinline__ void full_store(void* out, uint64_t slot0, const floa
 // liveness bytes + one spare word (they are copied as aligned 4-byte words).
 template <int NSC, int MM>
 constexpr uint32_t ring_slot_bytes() {
-    constexpr uint32_t BV = 16u * (NSC == 1 ? 4u : 2u);
+    constexpr uint32_t BV = 16u * kBatchGroups<NSC>;
     return MM == kLive ? (BV * 4u + BV + 4u + 15u) / 16u * 16u : BV * (4u + 8u * (MM == kMaskF32 ? 4u : 2u));
 }
 
@@ -342,7 +350,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     // vectors all lie in full-width blocks takes the predicate-free path
     // (liveness bits read from the ring, fixed store offsets); only the last
     // batch of a window takes the general one.
-    constexpr int D = NSC == 1 ? 4 : 2;
+    constexpr int D = kBatchGroups<NSC>;
     constexpr uint32_t BV = 16 * D;
     constexpr uint32_t MSZ = MM == kMaskF32 ? 4 : 2;
     constexpr uint32_t SLOT = ring_slot_bytes<NSC, MM>();
@@ -581,8 +589,14 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     int64_t fpad = std::max<int64_t>(1, (F + sc - 1) / sc) * sc;
     // NSC super-chunks per pass (double-buffered in registers); wider inner
     // dimensions take several passes.
+    // (Every pass after the first loads and multiplies without prefetch, so
+    // wide inner dimensions use 4 super-chunks per pass: FP16 F <= 128 and
+    // TF32 F <= 64 in one pass.)
     int nsc = 1;
-    if (fpad > sc) {
+    if (fpad > 2 * sc && TCS_SDDMM_NSC4) {
+        nsc = 4;
+        fpad = (F + 4 * sc - 1) / (4 * sc) * (4 * sc);
+    } else if (fpad > sc) {
         nsc = 2;
         fpad = (F + 2 * sc - 1) / (2 * sc) * (2 * sc);
     }
@@ -613,10 +627,12 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     if (static_mask) args.live = mask_liveness(mask, plan, s);
     if (tf32) {
         if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
-        else launch_sddmm<true, 2>(args, mf32, of32, s);
+        else if (nsc == 2) launch_sddmm<true, 2>(args, mf32, of32, s);
+        else launch_sddmm<true, 4>(args, mf32, of32, s);
     } else {
         if (nsc == 1) launch_sddmm<false, 1>(args, mf32, of32, s);
-        else launch_sddmm<false, 2>(args, mf32, of32, s);
+        else if (nsc == 2) launch_sddmm<false, 2>(args, mf32, of32, s);
+        else launch_sddmm<false, 4>(args, mf32, of32, s);
     }
 }
 
