@@ -78,9 +78,13 @@ constexpr int kWarps = 4;
 // registers) need more warps in flight to cover DRAM-latency gathers when
 // B does not fit in L2 (C5: 537 MB of B).
 #ifndef TCS_SPMM_BPS_WIDE
-#define TCS_SPMM_BPS_WIDE 4
+#define TCS_SPMM_BPS_WIDE 8
 #endif
 constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : nchunk * fpl <= 8 ? TCS_SPMM_BPS_WIDE : 4; }
+#ifndef TCS_SPMM_TF32_BPS_NARROW
+#define TCS_SPMM_TF32_BPS_NARROW 8
+#endif
+constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_NARROW : 4; }
 // Feature slab of the FP16 kernel for N > 64 (experiment knob: 128 or 64).
 // Host pipeline of tcs_spmm_csr_host: at most this many window-range chunks,
 // each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
@@ -565,7 +569,7 @@ __device__ __forceinline__ void tf32_epilogue(const SpmmArgs& a, const WorkItem&
 }
 
 template <int NCHUNK>
-__global__ void __launch_bounds__(kWarps * 32, 4) spmm_tf32_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_kernel(const SpmmArgs a) {
     constexpr int SLAB = NCHUNK * 32;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
@@ -805,8 +809,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                          : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));
             } else {
                 if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
-                else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>");
-                else launch(spmm_tf32_kernel<1>, a, slabs, s, "spmm_tf32<32>");
+                else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>", tf32_blocks(2));
+                else launch(spmm_tf32_kernel<1>, a, slabs, s, "spmm_tf32<32>", tf32_blocks(1));
             }
         }
         if (plan->n_split) {
