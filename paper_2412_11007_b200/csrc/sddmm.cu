@@ -28,6 +28,9 @@ namespace {
 
 using namespace dev;
 
+#ifndef TCS_SDDMM_BPS1
+#define TCS_SDDMM_BPS1 4
+#endif
 #ifndef TCS_SDDMM_NSC4
 #define TCS_SDDMM_NSC4 1
 #endif
@@ -61,7 +64,7 @@ constexpr int kRing = 4;  // column-index batches staged per warp
 // Resident CTAs per SM (sets the register budget): 4 (128 registers) for
 // single-pass inner dimensions, 3 when two super-chunks are double-buffered.
 template <int NSC>
-constexpr int kMinBlocks = NSC == 1 ? 4 : 3;
+constexpr int kMinBlocks = NSC == 1 ? TCS_SDDMM_BPS1 : 3;
 // Groups per double-buffered batch: the register budget of a batch is about
 // constant (NSC * D super-chunk tiles).
 template <int NSC>
