@@ -98,6 +98,9 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_E2E_CHUNK_NNZ
 #define TCS_E2E_CHUNK_NNZ (1ull << 20)
 #endif
+#ifndef TCS_SPMM_DEEP32
+#define TCS_SPMM_DEEP32 1
+#endif
 #ifndef TCS_SPMM_SLAB_F16
 #define TCS_SPMM_SLAB_F16 128
 #endif
@@ -370,6 +373,85 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
             }
         }
 
+        f16_epilogue<NCHUNK, FPL>(a, it, acc, feat0, g, t);
+    }
+}
+
+// Four-stage variant for narrow slabs (32 features: 64-byte rows, few
+// registers per stage): three gather steps in flight while a fourth is
+// multiplied, column indices four steps ahead -- for graphs whose dense
+// operand misses L2 (C5: 537 MB of B), where the gathers wait on DRAM.
+#ifndef TCS_SPMM_DEEP_BPS
+#define TCS_SPMM_DEEP_BPS 6
+#endif
+__device__ __forceinline__ uint32_t load_col16(const uint32_t* __restrict__ ci, uint32_t s, uint32_t vend,
+                                               uint32_t lane) {
+    return lane < 16 && s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
+}
+
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
+__global__ void __launch_bounds__(kWarps * 32, TCS_SPMM_DEEP_BPS) spmm_f16_kernel_deep(const SpmmArgs a) {
+    constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t q = lane >> 3, p = lane & 7;
+    const uint32_t src_lane = 8 * t + g;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
+    const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
+    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
+
+    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
+        float sm = 0.f, sinv = 0.f;
+        if constexpr (SMX) {
+            const float2 st2 = a.rowstat[8ull * it.window + g];
+            sm = st2.x;
+            sinv = st2.y;
+        }
+        float acc[NCHUNK][NJ][4];
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+
+        F16Step<NCHUNK, FPL, VF32> s0, s1, s2, s3;
+        uint32_t s = it.vbeg;
+        if (s < vend) {
+            // loop-top invariant: s0/s1/s2 hold steps s, s+16, s+32 (issued);
+            // c3 = columns of s+48, c0 of s+64, c1 of s+80, c2 of s+96
+            uint32_t c0 = load_col16(ci, s, vend, lane), c1 = load_col16(ci, s + 16, vend, lane);
+            uint32_t c2 = load_col16(ci, s + 32, vend, lane), c3 = load_col16(ci, s + 48, vend, lane);
+            f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s, g, t, q, c0, 0, s0);
+            c0 = load_col16(ci, s + 64, vend, lane);
+            if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, c1, 0, s1);
+            c1 = load_col16(ci, s + 80, vend, lane);
+            if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, c2, 0, s2);
+            c2 = load_col16(ci, s + 96, vend, lane);
+            for (;;) {
+                if (s + 48 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 48, g, t, q, c3, 0, s3);
+                c3 = load_col16(ci, s + 112, vend, lane);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(s0, acc, src_lane, a.scale, sm, sinv);
+                if (s + 16 >= vend) break;
+                if (s + 64 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 64, g, t, q, c0, 0, s0);
+                c0 = load_col16(ci, s + 128, vend, lane);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(s1, acc, src_lane, a.scale, sm, sinv);
+                if (s + 32 >= vend) break;
+                if (s + 80 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 80, g, t, q, c1, 0, s1);
+                c1 = load_col16(ci, s + 144, vend, lane);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(s2, acc, src_lane, a.scale, sm, sinv);
+                if (s + 48 >= vend) break;
+                if (s + 96 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 96, g, t, q, c2, 0, s2);
+                c2 = load_col16(ci, s + 160, vend, lane);
+                f16_compute<NCHUNK, FPL, VF32, SMX>(s3, acc, src_lane, a.scale, sm, sinv);
+                s += 64;
+                if (s >= vend) break;
+            }
+        }
         f16_epilogue<NCHUNK, FPL>(a, it, acc, feat0, g, t);
     }
 }
@@ -689,6 +771,8 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
                c, ldc, S->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>(), 0, rowstat, scale};
     if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
     else if (slab == 64) launch(spmm_f16_kernel<1, 8, false, true>, a, slabs, s, "spmm_f16_softmax<64>", spmm_blocks(1, 8));
+    else if (TCS_SPMM_DEEP32)
+        launch(spmm_f16_kernel_deep<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax_deep<32>", TCS_SPMM_DEEP_BPS);
     else launch(spmm_f16_kernel<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax<32>", spmm_blocks(1, 4));
     if (plan->n_split) {
         const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
@@ -804,6 +888,9 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 else if (slab == 64)
                     vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>", spmm_blocks(1, 8))
                          : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>", spmm_blocks(1, 8));
+                else if (TCS_SPMM_DEEP32)
+                    vf32 ? launch(spmm_f16_kernel_deep<1, 4, true>, a, slabs, s, "spmm_f16_deep<32,f32v>", TCS_SPMM_DEEP_BPS)
+                         : launch(spmm_f16_kernel_deep<1, 4, false>, a, slabs, s, "spmm_f16_deep<32>", TCS_SPMM_DEEP_BPS);
                 else
                     vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>", spmm_blocks(1, 4))
                          : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));
