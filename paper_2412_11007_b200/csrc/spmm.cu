@@ -379,8 +379,9 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
 
 // Four-stage variant for narrow slabs (32 features: 64-byte rows, few
 // registers per stage): three gather steps in flight while a fourth is
-// multiplied, column indices four steps ahead -- for graphs whose dense
-// operand misses L2 (C5: 537 MB of B), where the gathers wait on DRAM.
+// multiplied, column indices four steps ahead.  (For 64-feature slabs, at 4
+// CTAs/SM and 123 registers, it measured only 1% faster than the two-stage
+// kernel at 8 CTAs/SM, so those keep the latter.)
 #ifndef TCS_SPMM_DEEP_BPS
 #define TCS_SPMM_DEEP_BPS 6
 #endif
@@ -389,8 +390,8 @@ __device__ __forceinline__ uint32_t load_col16(const uint32_t* __restrict__ ci, 
     return lane < 16 && s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
 }
 
-template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
-__global__ void __launch_bounds__(kWarps * 32, TCS_SPMM_DEEP_BPS) spmm_f16_kernel_deep(const SpmmArgs a) {
+template <int NCHUNK, int FPL, bool VF32, bool SMX, int BPS>
+__global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
@@ -772,7 +773,8 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
     if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
     else if (slab == 64) launch(spmm_f16_kernel<1, 8, false, true>, a, slabs, s, "spmm_f16_softmax<64>", spmm_blocks(1, 8));
     else if (TCS_SPMM_DEEP32)
-        launch(spmm_f16_kernel_deep<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax_deep<32>", TCS_SPMM_DEEP_BPS);
+        launch(spmm_f16_kernel_deep<1, 4, false, true, TCS_SPMM_DEEP_BPS>, a, slabs, s, "spmm_f16_softmax_deep<32>",
+               TCS_SPMM_DEEP_BPS);
     else launch(spmm_f16_kernel<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax<32>", spmm_blocks(1, 4));
     if (plan->n_split) {
         const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
@@ -889,8 +891,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                     vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>", spmm_blocks(1, 8))
                          : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>", spmm_blocks(1, 8));
                 else if (TCS_SPMM_DEEP32)
-                    vf32 ? launch(spmm_f16_kernel_deep<1, 4, true>, a, slabs, s, "spmm_f16_deep<32,f32v>", TCS_SPMM_DEEP_BPS)
-                         : launch(spmm_f16_kernel_deep<1, 4, false>, a, slabs, s, "spmm_f16_deep<32>", TCS_SPMM_DEEP_BPS);
+                    vf32 ? launch(spmm_f16_kernel_deep<1, 4, true, false, TCS_SPMM_DEEP_BPS>, a, slabs, s, "spmm_f16_deep<32,f32v>", TCS_SPMM_DEEP_BPS)
+                         : launch(spmm_f16_kernel_deep<1, 4, false, false, TCS_SPMM_DEEP_BPS>, a, slabs, s, "spmm_f16_deep<32>", TCS_SPMM_DEEP_BPS);
                 else
                     vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>", spmm_blocks(1, 4))
                          : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));
