@@ -101,6 +101,10 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_SPMM_DEEP32
 #define TCS_SPMM_DEEP32 1
 #endif
+// Feature slab of the TF32 kernel for N > 64 (experiment knob: 128 or 64).
+#ifndef TCS_SPMM_SLAB_TF32
+#define TCS_SPMM_SLAB_TF32 128
+#endif
 #ifndef TCS_SPMM_SLAB_F16
 #define TCS_SPMM_SLAB_F16 128
 #endif
@@ -821,7 +825,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
 
         // Feature padding: 32 / 64 / multiple of 128.
         const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
-        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : 128;
+        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : TCS_SPMM_SLAB_TF32;
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
         const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
