@@ -182,6 +182,49 @@ def small_configs(device):
     return out
 
 
+def layer_configs(device):
+    """BASELINE configs[3]/[4] on this GPU (reported beside the headline, not
+    the metric): the GCN layer on the ogbn-products-shaped graph (F = 128)
+    and the AGNN layer on R-MAT scale 23 (F = 32).  CUDA events, L2 flushed
+    before every timed call, median of 5."""
+    import paper_2412_11007_b200.layers as L
+    from paper_2412_11007_b200 import graphs as G
+
+    flush = torch.empty(64 << 20, dtype=torch.int32, device=device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def timed(fn, reps=5):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        return round(sorted(ts)[len(ts) // 2], 3)
+
+    out = {}
+    rows, _, rp, ci, _ = G.power_law_csr(G.C4_PRODUCTS, values="real", device=device)
+    W = torch.randn(128, 128, device=device).half() / 128 ** 0.5
+    H = torch.randn(rows, 128, device=device).half()
+    gcn = L.GCNLayer(rows, rp, ci, W)
+    out["c4_gcn"] = {"nodes": rows, "nnz": int(ci.numel()), "adjacency": "D^-1/2 (A + I) D^-1/2", "F": 128,
+                     "layer_ms": timed(lambda: gcn(H)), "precision": "fp16", "path": "cuBLAS GEMM + tcs_spmm"}
+    del gcn, H, rp, ci
+    torch.cuda.empty_cache()
+    rows, _, rp, ci, _ = G.rmat_csr(G.C5_RMAT, values="real", device=device)
+    H = torch.randn(rows, 32, device=device)
+    agnn = L.AGNNLayer(rows, rp, ci, beta=1.0)
+    out["c5_agnn"] = {"nodes": rows, "nnz": int(ci.numel()), "F": 32, "layer_ms": timed(lambda: agnn(H)),
+                      "precision": "fp16", "path": "rows_normalize + tcs_agnn_aggregate (static mask)"}
+    del agnn, H, rp, ci
+    torch.cuda.empty_cache()
+    return out
+
+
 def bytes_alg_spmm(W, nv, rows, N, vwA, vwB):
     """row pointers + column indices + sparse values (no padding)
     + one N-wide dense row per stored vector + the fp32 C write."""
@@ -567,6 +610,7 @@ def main():
         line = run_ours(args, rank, world, device)
         if line is not None and world == 1 and not args.quick:
             line["small_configs"] = small_configs(device)
+            line["layer_configs"] = layer_configs(device)
             line["cpu_baseline"] = cpu_baseline(args, device)
     if line is not None:
         print(json.dumps(line), flush=True)
