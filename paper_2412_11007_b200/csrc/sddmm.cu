@@ -49,7 +49,7 @@ struct SddmmArgs {
     uint64_t rows;
     int passes;         // feature passes of NSC super-chunks
     uint32_t k;         // storage block width (8 / 4)
-    uint32_t* counter;  // work-item counter (zeroed before launch)
+    uint32_t* counter;  // claim counters, dev::kClaimBytes (zeroed before launch)
     float dead;         // value of stored slots whose mask value is 0: 0, or -inf for the fused softmax
     const uint8_t* live;  // per-vector liveness bytes (bit r: row r's mask value != 0), mask mode kLive
 };
@@ -294,12 +294,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t g = lane >> 2, t = lane & 3;
     extern __shared__ __align__(16) unsigned char ring_all[];  // per-warp ring, see below
-    // persistent warps pulling work items (cf. spmm.cu next_item)
-    for (;;) {
-    uint32_t idx = 0;
-    if (lane == 0) idx = atomicAdd(a.counter, 1u);
-    idx = __shfl_sync(0xffffffffu, idx, 0);
-    if (idx >= a.n_items) break;
+    // persistent warps pulling work items (dev::StripedClaim)
+    dev::StripedClaim<4> claim;
+    for (uint32_t idx; claim.get(a.counter, a.n_items, idx);) {
     const WorkItem it = a.items[idx];
     const uint32_t base = __ldg(a.rp + it.window);
     const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -620,8 +617,8 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     int64_t alda = 0, bldb = 0;
     const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
     const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
-    DBuf item_ctr(sizeof(uint32_t), s);
-    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, sizeof(uint32_t), s));
+    DBuf item_ctr(dev::kClaimBytes, s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, dev::kClaimBytes, s));
     SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
                    ap, alda, bp, bldb, out_values, mask->rows,
                    static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr};

@@ -254,11 +254,8 @@ __global__ void __launch_bounds__(256) softmax_items(const WorkItem* __restrict_
                                                      const VS* scores, const VM* __restrict__ mask, VO* out,
                                                      float scale, RowStat* __restrict__ part) {
     const uint32_t lane = threadIdx.x & 31;
-    for (;;) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(counter, 1u);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= n_items) break;
+    dev::StripedClaim<8> claim;
+    for (uint32_t idx; claim.get(counter, n_items, idx);) {
         const WorkItem it = items[idx];
         const uint64_t vb = 8ull * __ldg(rp + it.window);
         float m, s;
@@ -322,11 +319,8 @@ __global__ void __launch_bounds__(256) softmax_stats_items(const WorkItem* __res
                                                            const VS* scores, float scale, float2* __restrict__ rowstat,
                                                            RowStat* __restrict__ part) {
     const uint32_t lane = threadIdx.x & 31;
-    for (;;) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(counter, 1u);
-        idx = __shfl_sync(0xffffffffu, idx, 0);
-        if (idx >= n_items) break;
+    dev::StripedClaim<8> claim;
+    for (uint32_t idx; claim.get(counter, n_items, idx);) {
         const WorkItem it = items[idx];
         const uint64_t vb = 8ull * __ldg(rp + it.window);
         float m, s;
@@ -357,8 +351,8 @@ __global__ void softmax_stats_combine(const SplitWindow* __restrict__ split, uin
 // may alias sv.
 template <uint32_t K, typename VS, typename VM, typename VO>
 void run(const tcs_mebcrs* sc, const VS* sv, const VM* mv, VO* out, float scale, const Plan* plan, cudaStream_t s) {
-    DBuf ctr(sizeof(uint32_t), s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
-    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(uint32_t), s));
+    DBuf ctr(dev::kClaimBytes, s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
+    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, dev::kClaimBytes, s));
     const int grid = static_cast<int>(std::min<uint64_t>((plan->n_items + 7) / 8, uint64_t(num_sms()) * 8));
     softmax_items<K, VS, VM, VO><<<std::max(grid, 1), 256, 0, s>>>(plan->items, plan->n_items, ctr.as<uint32_t>(),
                                                                    sc->row_pointers, sv, mv, out, scale,
@@ -409,8 +403,8 @@ void run_fused(const tcs_mebcrs* m, const void* x, void* out, tcs_dtype odt, flo
 
 void softmax_rowstats(const tcs_mebcrs* S, const Plan* plan, float scale, float2* rowstat, cudaStream_t s) {
     if (!plan->n_items) return;
-    DBuf ctr(sizeof(uint32_t), s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
-    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, sizeof(uint32_t), s));
+    DBuf ctr(dev::kClaimBytes, s), part(std::max<uint64_t>(1, plan->n_slots) * 8 * sizeof(RowStat), s);
+    TCS_CUDA(cudaMemsetAsync(ctr.p, 0, dev::kClaimBytes, s));
     const int grid = static_cast<int>(std::min<uint64_t>((plan->n_items + 7) / 8, uint64_t(num_sms()) * 8));
     const __half* sv = static_cast<const __half*>(S->values);
     softmax_stats_items<8, __half><<<std::max(grid, 1), 256, 0, s>>>(plan->items, plan->n_items, ctr.as<uint32_t>(),

@@ -51,7 +51,7 @@ struct SpmmArgs {
     int64_t N;
     float* partial;  // [slot][8][ldp]
     int64_t ldp;
-    uint32_t* counter;  // per-slab work-item counters (zeroed before launch)
+    uint32_t* counter;  // per-slab claim counters, dev::kClaimBytes each (zeroed before launch)
     uint32_t slab0;     // first feature slab of this launch (slab = slab0 + blockIdx.y)
     // Softmax operand (SMX kernels, the AGNN aggregation): the sparse values
     // are binary16 scores x with dead slots -inf, and each is replaced by
@@ -110,15 +110,11 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #endif
 
 // ------------------------------------------------------------- scheduling
-// Persistent warps: each warp claims work items from a per-slab counter
-// (atomicAdd by lane 0, broadcast by shuffle) until the list is exhausted,
-// so no warp slot idles behind a long item of a sibling warp.  Items are
-// ordered longest-first by the planner (split-window segments lead).
-__device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1u);
-    return __shfl_sync(0xffffffffu, i, 0);
-}
+// Persistent warps: each warp claims work items from its slab's striped
+// counters (dev::StripedClaim: atomicAdd by lane 0, broadcast by shuffle)
+// until the list is exhausted, so no warp slot idles behind a long item of a
+// sibling warp.  Items are ordered longest-first by the planner (split-window
+// segments lead); every stripe is a longest-first subsequence.
 
 // Column indices of a 2-step (32-vector) window of the item, one per lane,
 // loaded coalesced; slots pick theirs with a shuffle.
@@ -334,9 +330,9 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     const uint32_t src_lane = 8 * t + g;                    // where this lane's fragment data was loaded
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
+    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
 
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -403,9 +399,9 @@ __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const S
     const uint32_t src_lane = 8 * t + g;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
-
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
+    dev::StripedClaim<1> claim;  // this loop form measured 7% faster than next_item here (C5 N=32)
+    for (uint32_t idx; claim.get(counter, a.n_items, idx);) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -478,9 +474,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
     const uint32_t g = lane >> 2, t = lane & 3;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const unsigned short* Bl = static_cast<const unsigned short*>(a.B) + feat0 + g;
-    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
+    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
 
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -663,9 +659,9 @@ __global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_ke
     const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
-    uint32_t* counter = a.counter + a.slab0 + blockIdx.y;
+    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
 
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -770,8 +766,8 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
     DBuf partial;
     if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
     const int slabs = static_cast<int>(npad / slab);
-    DBuf item_ctr(slabs * sizeof(uint32_t), s);
-    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * sizeof(uint32_t), s));
+    DBuf item_ctr(slabs * dev::kClaimBytes, s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
     SpmmArgs a{plan->items, plan->n_items, S->row_pointers, S->column_indices, S->values, bp, bld,
                c, ldc, S->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>(), 0, rowstat, scale};
     if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
@@ -868,8 +864,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         const int slabs = static_cast<int>(npad / slab);
         DBuf item_ctr;
         if (!launched && plan->n_items) {
-            item_ctr = DBuf(slabs * sizeof(uint32_t), s);
-            TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * sizeof(uint32_t), s));
+            item_ctr = DBuf(slabs * dev::kClaimBytes, s);
+            TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
         }
         SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
                    c, ldc, A->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>()};

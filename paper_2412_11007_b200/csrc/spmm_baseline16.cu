@@ -64,12 +64,6 @@ __device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint3
                  : "r"(addr));
 }
 
-__device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(counter, 1u);
-    return __shfl_sync(0xffffffffu, i, 0);
-}
-
 // Sparse element (row r, window-relative vector v) of a 16-high window
 // (ref mebcrs.hpp:46-56 with vector_height 16), 0 past the residue.
 template <typename V>
@@ -134,11 +128,11 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_b16_f16_kernel(const B16A
     unsigned char* tile = smem + warp * 2 * T::BYTES;
     const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * 8 * NT;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0;
-    uint32_t* counter = a.counter + blockIdx.y;
+    uint32_t* counter = a.counter + static_cast<uint64_t>(blockIdx.y) * (dev::kClaimBytes / 4);
     // ldmatrix row addresses: matrix m = lane/8 -> k rows (m&1)*8 + lane%8, features +8*(m>>1)
     const uint32_t ld_k = ((lane >> 3) & 1) * 8 + (lane & 7), ld_n = (lane >> 4) * 8;
 
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -247,9 +241,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_b16_tf32_kernel(const B16
     const int64_t feat0 = static_cast<int64_t>(blockIdx.y) * 8 * NT;
     const float* Bl = static_cast<const float*>(a.B) + feat0;
     const float* fv = static_cast<const float*>(a.vals);
-    uint32_t* counter = a.counter + blockIdx.y;
+    uint32_t* counter = a.counter + static_cast<uint64_t>(blockIdx.y) * (dev::kClaimBytes / 4);
 
-    for (uint32_t idx = next_item(counter, lane); idx < a.n_items; idx = next_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -395,8 +389,8 @@ extern "C" tcs_status tcs_spmm_baseline16(const tcs_mebcrs* A, const void* b, tc
         DBuf partial;
         if (plan->n_slots) partial = DBuf(plan->n_slots * 16 * npad * sizeof(float), s);
         const int slabs = static_cast<int>(npad / slab);
-        DBuf ctr(slabs * sizeof(uint32_t), s);
-        TCS_CUDA(cudaMemsetAsync(ctr.p, 0, slabs * sizeof(uint32_t), s));
+        DBuf ctr(slabs * dev::kClaimBytes, s);
+        TCS_CUDA(cudaMemsetAsync(ctr.p, 0, slabs * dev::kClaimBytes, s));
         B16Args a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
                   c, ldc, A->rows, n, partial.as<float>(), npad, ctr.as<uint32_t>()};
         if (plan->n_items) {

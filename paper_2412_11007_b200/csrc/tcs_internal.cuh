@@ -165,6 +165,47 @@ namespace tcs::dev {
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
+// Work-item claiming for the persistent kernels.  Items are dealt
+// round-robin to NS counters on separate 128-byte lines (item i to stripe
+// i % NS); a warp starts on its block's stripe and moves on when that stripe
+// runs dry.  Still one item per atomic -- the balance of a single counter --
+// but the same-address atomics of ~1200 resident warps are spread over the
+// stripes.  Every claimed list owns kClaimBytes of zeroed counters (room for
+// kMaxClaimStripes).  Measured per kernel (profiles/r1s4_claim_stripes.txt):
+// the C5 softmax statistics pass drops 1.55 -> 1.14 ms at NS = 8, the SDDMM
+// gains ~1-2% at NS = 4, the C3 SpMM prefers the plain counter.
+constexpr uint32_t kMaxClaimStripes = 8;
+constexpr uint32_t kClaimStride = 32;  // u32 per stripe counter (128 B)
+constexpr size_t kClaimBytes = size_t(kMaxClaimStripes) * kClaimStride * sizeof(uint32_t);
+template <uint32_t NS>
+struct StripedClaim {
+    static_assert(NS >= 1 && NS <= kMaxClaimStripes, "stripe count");
+    uint32_t stripe, tried = 0;
+    __device__ __forceinline__ StripedClaim() : stripe(blockIdx.x % NS) {}
+    __device__ __forceinline__ bool get(uint32_t* counters, uint64_t n_items, uint32_t& idx) {
+        while (tried < NS) {
+            uint32_t k = 0;
+            if ((threadIdx.x & 31u) == 0) k = atomicAdd(counters + stripe * kClaimStride, 1u);
+            k = __shfl_sync(0xffffffffu, k, 0);
+            const uint64_t i = uint64_t(k) * NS + stripe;
+            if (i < n_items) {
+                idx = static_cast<uint32_t>(i);
+                return true;
+            }
+            stripe = (stripe + 1) % NS;
+            ++tried;
+        }
+        return false;
+    }
+};
+
+// Plain single-counter claim (stripe 0 of a kClaimBytes block).
+__device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(counter, 1u);
+    return __shfl_sync(0xffffffffu, i, 0);
+}
+
 // RNE fp32 -> tf32 (cvt.rn.tf32.f32, sm_90+); matches the reference's
 // round_to_tf32 (ref precision.hpp:42-46; inf/NaN pass through).
 __device__ __forceinline__ uint32_t to_tf32(float x) {

@@ -1,5 +1,5 @@
 """Timing aid for A/B builds (TCS_LIB_PATH): SpMM on C3 (FP16 / TF32,
-N=128), C4 (FP16, N=128), C5 (FP16, N=32) and SDDMM on C3 (FP16, F=32).
+N=128), C4 (FP16, N=128), C5 (FP16, N=32) and SDDMM on C3 and C5 (FP16, F=32).
 CUDA events, L2 flushed before every timed call; prints one JSON object."""
 import json
 import os
@@ -71,5 +71,11 @@ if "c5" in which:
     B = G.dense(cols, 32, 2)
     C = torch.empty(rows, 32, device="cuda")
     out["c5_spmm_fp16_n32"] = timed(lambda: T.spmm(me, B, T.KernelConfig(), out=C))
+    del B, C
+    A = G.dense(rows, 32, 4)
+    Bt = G.dense(cols, 32, 5)
+    ov = torch.empty(8 * me.num_vectors, device="cuda")
+    out["c5_sddmm_fp16_f32"] = timed(lambda: T.sddmm(T.SddmmOperands(me, A, Bt), T.KernelConfig(), out_values=ov))
+    del A, Bt, ov
     me.free()
 print(json.dumps(out))
