@@ -36,6 +36,8 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Measured ceiling of the SpMM gather pattern on B200 (FP16, 256-byte B rows).
+GATHER_CEILING_GBS = 11757.2
 METRIC = "SpMM/SDDMM effective GFLOP/s (2·nnz·N) and % HBM roofline at 1/2/4/8 B200"
 
 
@@ -420,7 +422,15 @@ def run_ours(args, rank, world, device):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
-                     "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>"},
+                     "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>",
+                     # bytes_alg/t above the HBM peak = B-row gathers served by L2.
+                     # The binding resource is the L1 data pipe: the same gather
+                     # shape (LDG.128 + SHFL + HMMA + values one step ahead, no
+                     # sparse structure) peaks at this rate in tools/gather_bench2.cu.
+                     "gather_ceiling": {"achieved_over_ceiling": round(achieved / GATHER_CEILING_GBS, 4),
+                                        "ceiling_gbs": GATHER_CEILING_GBS,
+                                        "source": "profiles/r1s3_gather_bench2.txt (LDG+SHFL+PRMT+HMMA+values ahead)"}
+                     if prec == 0 else None},
         "gpu_launches": launches,
         "clocks": clocks,
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
