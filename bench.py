@@ -221,7 +221,7 @@ def layer_configs(device):
     H = torch.randn(rows, 32, device=device)
     agnn = L.AGNNLayer(rows, rp, ci, beta=1.0)
     out["c5_agnn"] = {"nodes": rows, "nnz": int(ci.numel()), "F": 32, "layer_ms": timed(lambda: agnn(H)),
-                      "precision": "fp16", "path": "rows_normalize + tcs_agnn_aggregate (static mask)"}
+                      "precision": "fp16", "path": "rows_normalize (f16 copy) + tcs_agnn_attend (one pass, static mask)"}
     del agnn, H, rp, ci
     torch.cuda.empty_cache()
     return out

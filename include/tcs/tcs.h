@@ -367,6 +367,21 @@ tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn, tcs_dtype 
                               int64_t rows, int64_t f, float scale, const void* hc, tcs_dtype hc_dtype, int64_t ldhc,
                               int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg, tcs_stream_t stream);
 
+/* Fused AGNN attention (no reference counterpart):
+ *   C[i] (f32, rows x f, stride ldc) = sum_j softmax_j(scale * cos(h[row0 + i], h[j])) h[j]
+ * over the mask's live slots (tcs_sddmm's rule: mask value != 0), in ONE
+ * pass: every neighbour row is gathered once and feeds both the score MMA
+ * and the aggregation MMA (online softmax, flash-attention style).  h
+ * [cols x f] f16 (stride ldh, 16-byte aligned rows), f = 32 or 64; the cosine
+ * uses 1 / max(||h_j||, eps).  Tolerance-level agreement with
+ * tcs_agnn_aggregate (scores are not rounded to binary16 here, P is
+ * rounded to binary16 before the aggregation MMA).  Any mask precision
+ * (only its pattern and liveness are read); cfg->flags may carry
+ * TCS_CFG_STATIC_MASK.  SHAPE for other f, ARGUMENT for misaligned buffers. */
+tcs_status tcs_agnn_attend(const tcs_mebcrs* mask, const void* h, tcs_dtype h_dtype, int64_t ldh, int64_t row0,
+                           int64_t f, float scale, float eps, float* c, int64_t ldc, const tcs_kernel_config* cfg,
+                           tcs_stream_t stream);
+
 /* AGNN input transform (no reference counterpart): hn[i] = h[i] /
  * max(||h[i]||_2, eps) and hc[i] = h[i], rounded to out_dtype (F16/F32),
  * from one read of the f32 rows h [rows][ldh].  hn or hc may be NULL. */

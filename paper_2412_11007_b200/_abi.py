@@ -121,6 +121,9 @@ EXPORTS = {
     "tcs_agnn_aggregate": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, C.c_float, C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_void_p,
                                      C.c_int64, C.POINTER(tcs_kernel_config), C.c_void_p]),
+    "tcs_agnn_attend": (C.c_int, [C.POINTER(tcs_mebcrs), C.c_void_p, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                  C.c_float, C.c_float, C.c_void_p, C.c_int64, C.POINTER(tcs_kernel_config),
+                                  C.c_void_p]),
     "tcs_rows_normalize": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_int64, C.c_int, C.c_float, C.c_void_p]),
     "tcs_mebcrs_encode_host": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_int, C.POINTER(tcs_mebcrs), C.c_void_p]),

@@ -557,20 +557,26 @@ void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64
 // between calls that reuse the cache).
 const uint8_t* mask_liveness(const tcs_mebcrs* mask, Plan* plan, cudaStream_t s) {
     if (plan->live && plan->live_src == mask->values) return plan->live;
+    if (!plan->live) plan->live = static_cast<uint8_t*>(dalloc(mask->num_vectors + 16, s));
+    build_liveness(mask, plan->live, s);
+    plan->live_src = mask->values;
+    return plan->live;
+}
+
+// live[p] for every stored vector p (nv + 16 bytes; the 16 past nv zeroed).
+void build_liveness(const tcs_mebcrs* mask, uint8_t* live, cudaStream_t s) {
     const uint64_t nv = mask->num_vectors;
-    if (!plan->live) plan->live = static_cast<uint8_t*>(dalloc(nv + 16, s));
-    TCS_CUDA(cudaMemsetAsync(plan->live + nv, 0, 16, s));
+    TCS_CUDA(cudaMemsetAsync(live + nv, 0, 16, s));
+    if (!nv) return;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((nv + 255) / 256, uint64_t(num_sms()) * 16)));
     if (mask->value_dtype == TCS_DTYPE_F16)
         live_build<unsigned short><<<grid, 256, 0, s>>>(mask->row_pointers, mask->num_windows,
                                                         static_cast<const unsigned short*>(mask->values), nv, mask->k,
-                                                        plan->live);
+                                                        live);
     else
         live_build<uint32_t><<<grid, 256, 0, s>>>(mask->row_pointers, mask->num_windows,
-                                                  static_cast<const uint32_t*>(mask->values), nv, mask->k, plan->live);
+                                                  static_cast<const uint32_t*>(mask->values), nv, mask->k, live);
     TCS_LAUNCHED("sddmm_live_build");
-    plan->live_src = mask->values;
-    return plan->live;
 }
 
 void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,

@@ -1051,7 +1051,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         forked.wait_on(ss.drain);
 
         Event b_ready;
-        std::vector<Event> landed(nchunks), done(nchunks);
+        std::vector<Event> landed(nchunks), done(nchunks), encoded(e2e_trace() ? nchunks : 0);
         if (b_rows > 0) TCS_CUDA(cudaMemcpyAsync(d_b32.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, ss.copy));
         b_ready.record(ss.copy);
         for (uint64_t i = 0; i < nchunks; ++i) {
@@ -1095,6 +1095,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             tcs_mebcrs m{};
             tcs_status rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
             if (rc != TCS_OK) fail(rc, tcs_last_error());
+            if (e2e_trace()) encoded[i].record(cs);
             tcs_counters cn{};
             rc = tcs_spmm(&m, bdev, bdt, n, b_rows, n, d_c.as<float>() + r0 * n, n, cfg, counters ? &cn : nullptr, ks);
             tcs_mebcrs_free(&m, ks);
@@ -1119,8 +1120,8 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             };
             std::fprintf(stderr, "[tcs e2e] %llu chunks, B landed %.3f ms\n", (unsigned long long)nchunks, ms(b_ready));
             for (uint64_t i = 0; i < nchunks; ++i)
-                std::fprintf(stderr, "[tcs e2e] chunk %llu: landed %.3f  computed %.3f\n", (unsigned long long)i,
-                             ms(landed[i]), ms(done[i]));
+                std::fprintf(stderr, "[tcs e2e] chunk %llu: landed %.3f  encoded %.3f  computed %.3f\n",
+                             (unsigned long long)i, ms(landed[i]), ms(encoded[i]), ms(done[i]));
             std::fprintf(stderr, "[tcs e2e] drained %.3f ms\n", ms(drained[0]));
         }
         joined_copy.record(ss.copy);

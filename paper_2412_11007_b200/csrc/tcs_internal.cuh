@@ -146,6 +146,11 @@ inline cudaStream_t st(tcs_stream_t s) { return reinterpret_cast<cudaStream_t>(s
 void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64_t lda, int64_t a_rows, int64_t f_a,
                  const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t f_b, tcs_dtype out_dtype,
                  const tcs_kernel_config* cfg);
+// Per-vector liveness bytes of a mask (bit r: row r's mask value != 0).
+// mask_liveness caches them in the work list (TCS_CFG_STATIC_MASK);
+// build_liveness writes nv + 16 bytes into caller memory.
+const uint8_t* mask_liveness(const tcs_mebcrs* mask, Plan* plan, cudaStream_t s);
+void build_liveness(const tcs_mebcrs* mask, uint8_t* live, cudaStream_t s);
 void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a_dtype, int64_t lda,
                   int64_t a_rows, const void* bt, tcs_dtype bt_dtype, int64_t ldbt, int64_t bt_rows, int64_t F,
                   void* out_values, tcs_dtype out_dtype, float dead, bool static_mask, cudaStream_t s);

@@ -164,8 +164,12 @@ class ShardedAGNNLayer:
         self.cfg = T.KernelConfig(T.Precision.fp16, static_mask=True)
         self._T = T
 
-    def __call__(self, H: torch.Tensor, gather: bool = True) -> torch.Tensor:
+    def __call__(self, H: torch.Tensor, gather: bool = True, one_pass: bool = True) -> torch.Tensor:
         T = self._T
-        Hn, Hc = T.rows_normalize(H.float().contiguous(), torch.float16)
-        C = T.agnn_aggregate(self.mask, Hn, Hc, self.beta, self.cfg, row0=self.shard.r0)
+        if one_pass and H.shape[1] in (32, 64):  # as AGNNLayer: tcs_agnn_attend
+            _, Hc = T.rows_normalize(H.float().contiguous(), torch.float16, normalized=False)
+            C = T.agnn_attend(self.mask, Hc, self.beta, self.cfg, row0=self.shard.r0)
+        else:
+            Hn, Hc = T.rows_normalize(H.float().contiguous(), torch.float16)
+            C = T.agnn_aggregate(self.mask, Hn, Hc, self.beta, self.cfg, row0=self.shard.r0)
         return gather_rows(C, self.shard_rows, self.group) if gather else C

@@ -5,10 +5,12 @@ configs[3] and configs[4] name (PAPER.md:685-712, "end-to-end GNN"):
   The dense transform H W is a plain library GEMM (cuBLAS through torch);
   the aggregation Â · (HW) is tcs_spmm over the ME-BCRS encoding of Â.
 * ``AGNNLayer``: H' = softmax_row(beta * cos(h_i, h_j) on the edges) · H.
-  cos via tcs_sddmm over the row-normalised features, the row softmax via
-  tcs_mebcrs_row_softmax (binary16 probabilities), the aggregation via
-  tcs_spmm on the probability matrix -- no re-encoding between stages (the
-  pipeline closure of ref tests/test_kernels.cpp:313-327).
+  FP16 with F = 32 or 64: tcs_agnn_attend, one kernel (scores, online
+  softmax and aggregation from a single gather of each neighbour row).
+  Otherwise cos via tcs_sddmm over the row-normalised features, the row
+  softmax and the aggregation via tcs_agnn_aggregate (FP16) or
+  tcs_sddmm_row_softmax + tcs_spmm (TF32) -- no re-encoding between stages
+  (the pipeline closure of ref tests/test_kernels.cpp:313-327).
 
 Inputs are torch CUDA tensors; the graph is given once as CSR and encoded
 once on the GPU.
@@ -82,7 +84,12 @@ class AGNNLayer:
         scores = T.sddmm(ops, self.mask_cfg).output  # cos(h_i, h_j) at the edges
         return T.row_softmax(scores, self.mask, self.beta, pdt)
 
-    def __call__(self, H: torch.Tensor) -> torch.Tensor:
+    def __call__(self, H: torch.Tensor, one_pass: bool = True) -> torch.Tensor:
+        if one_pass and self.precision == T.Precision.fp16 and H.shape[1] in (32, 64):
+            # tcs_agnn_attend: scores, online softmax and aggregation in one
+            # kernel, each neighbour row gathered once
+            _, Hc = T.rows_normalize(H.float().contiguous(), torch.float16, normalized=False)
+            return T.agnn_attend(self.mask, Hc, self.beta, self.mask_cfg)
         # one pass over H: the normalised rows (SDDMM operand) and H itself
         # in the kernels' dtype (SpMM operand)
         Hn, Hc = T.rows_normalize(H.float().contiguous(), self.dtype)

@@ -459,6 +459,26 @@ def agnn_aggregate(mask: MeBcrsMatrix, hn: torch.Tensor, hc: torch.Tensor, scale
     return out
 
 
+def agnn_attend(mask: MeBcrsMatrix, h: torch.Tensor, scale: float = 1.0, cfg: KernelConfig | None = None,
+                out: torch.Tensor | None = None, row0: int = 0, eps: float = 1e-12) -> torch.Tensor:
+    """C[i] = sum_j softmax_j(scale * cos(h[row0 + i], h[j])) h[j] over the
+    mask's live slots, fused in one pass (tcs_agnn_attend): h is the f16
+    feature matrix of every node (F = 32 or 64), gathered once per stored
+    vector for both the scores and the aggregation."""
+    if cfg is None:
+        cfg = KernelConfig(mask.precision)
+    if h.dtype != torch.float16 or h.dim() != 2:
+        raise ArgumentError("h must be a 2-D float16 tensor")
+    h = h if h.stride(-1) == 1 else h.contiguous()
+    rows, f = mask.rows, h.shape[1]
+    if out is None:
+        out = torch.empty((rows, f), dtype=torch.float32, device=h.device)
+    _check(_abi.load().tcs_agnn_attend(C.byref(mask._h), h.data_ptr(), _abi.TCS_DTYPE_F16, h.stride(0), int(row0),
+                                       f, float(scale), float(eps), out.data_ptr(), out.stride(0),
+                                       C.byref(cfg._c()), _stream()))
+    return out
+
+
 def rows_normalize(h: torch.Tensor, dtype: torch.dtype = torch.float16, eps: float = 1e-12,
                    normalized: bool = True, copy: bool = True):
     """(h / max(||h_i||, eps), h) in `dtype` from one pass over the f32 rows

@@ -226,3 +226,93 @@ def test_agnn_aggregate_equals_materialised_softmax(n):
                 got = T.agnn_aggregate(me, hn.to(a_dt), hc.to(h_dt), 0.9, cfg)
                 assert torch.equal(got, want), (static, a_dt, h_dt)
     assert m.nnz == ci.size
+
+
+def _attend_case(seed, rows, cols, hub=True):
+    rng = np.random.default_rng(seed)
+    per_row = rng.integers(0, 12, rows)
+    if hub:
+        per_row[8:16] = min(cols, 2500)  # a hub window longer than the work-list segment
+    per_row[40:48] = 0                   # an empty window
+    per_row[-1] = 0                      # an empty last row
+    rp = np.zeros(rows + 1, np.uint32)
+    rp[1:] = np.cumsum(per_row)
+    ci = np.concatenate([np.sort(rng.choice(cols, size=d, replace=False)) for d in per_row]).astype(np.uint32)
+    vals = np.ones(ci.size, np.float32)
+    vals[::13] = 0.0  # stored, not sampled
+    m = O.Csr(rows, cols, rp, ci, vals)
+    me = T.encode_mebcrs(T.CsrMatrix(rows, cols, torch.from_numpy(rp.view(np.int32)).cuda(),
+                                     torch.from_numpy(ci.view(np.int32)).cuda(), torch.from_numpy(vals).cuda()),
+                         T.Precision.fp16)
+    return m, me
+
+
+def _attend_ref(m, h16, row0, scale, eps=1e-12):
+    hf = h16.double().cpu()
+    rn = 1.0 / hf.norm(dim=1).clamp_min(eps)
+    hi = hf[row0:row0 + m.rows]
+    S = (hi @ hf.T) * rn[row0:row0 + m.rows, None] * rn[None, :]
+    P = softmax_ref(S, dense_pattern(m), scale)
+    return (P @ hf).to(h16.device)
+
+
+def _rel_l2(a, b):
+    return float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("f", [32, 64])
+def test_agnn_attend_matches_fp64(f):
+    """Fused one-pass AGNN attention vs an fp64 dense PyTorch reference on
+    the same f16 features: split hub windows, empty windows and rows, dead
+    (explicit-zero) mask entries, static and per-call mask.  P is rounded to
+    binary16 before the aggregation MMA, so the bound is FP16-level."""
+    rows = 3000
+    m, me = _attend_case(f, rows, rows)
+    g = torch.Generator(device="cuda").manual_seed(f)
+    h = torch.randn(rows, f, device="cuda", generator=g).half()
+    want = _attend_ref(m, h, 0, 0.9)
+    for static in (False, True):
+        got = T.agnn_attend(me, h, 0.9, T.KernelConfig(T.Precision.fp16, static_mask=static))
+        assert got.shape == (rows, f)
+        assert _rel_l2(got, want) < 2e-3, (static, _rel_l2(got, want))
+        assert torch.all(got[40:48] == 0) and torch.all(got[-1] == 0)
+
+
+def test_agnn_attend_agrees_with_three_pass_aggregate():
+    """The fused kernel and tcs_agnn_aggregate (SDDMM -> statistics ->
+    softmax-applying SpMM, binary16 scores) compute the same layer."""
+    rows, f = 3000, 32
+    m, me = _attend_case(7, rows, rows)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    h = torch.randn(rows, f, device="cuda", generator=g)
+    hn, hc = T.rows_normalize(h, torch.float16)
+    three = T.agnn_aggregate(me, hn, hc, 1.3)
+    fused = T.agnn_attend(me, hc, 1.3)
+    assert _rel_l2(fused, three) < 5e-3
+
+
+def test_agnn_attend_row_shard_and_large_scores():
+    """A row shard (row0 > 0, mask rows < nodes, rows not a multiple of 8)
+    and a large scale (scores up to +-40 in log2 units: the online
+    max-rescaling must keep the sums finite)."""
+    nodes, row0, rows, f = 4000, 1203, 1501, 32
+    m, me = _attend_case(11, rows, nodes)
+    g = torch.Generator(device="cuda").manual_seed(11)
+    h = torch.randn(nodes, f, device="cuda", generator=g).half()
+    for scale in (0.5, 30.0):
+        want = _attend_ref(m, h, row0, scale)
+        got = T.agnn_attend(me, h, scale, row0=row0)
+        assert torch.isfinite(got).all()
+        assert _rel_l2(got, want) < 4e-3, (scale, _rel_l2(got, want))
+
+
+def test_agnn_attend_rejects_bad_arguments():
+    rows = 64
+    _, me = _attend_case(3, rows, rows, hub=False)
+    h = torch.randn(rows, 48, device="cuda").half()
+    with pytest.raises(T.ShapeError):
+        T.agnn_attend(me, h)
+    with pytest.raises(T.ArgumentError):
+        T.agnn_attend(me, torch.randn(rows, 32, device="cuda"))
+    with pytest.raises(T.ShapeError):
+        T.agnn_attend(me, torch.randn(rows, 32, device="cuda").half(), row0=1)
