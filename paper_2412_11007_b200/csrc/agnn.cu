@@ -79,8 +79,8 @@ __device__ __forceinline__ float fast_exp2(float x) {
 template <int NC>
 struct AttStep {
     uint4 h[2][NC];  // vectors g (half 0) and g + 8 (half 1), features 32c + 8t .. +7
-    float rnj;       // lanes 0..15: inverse norm of vector `lane` of the step
-    uint32_t live;   // lanes 0..15: liveness byte of vector `lane`
+    float rn[2];     // inverse norms of those two vectors
+    uint32_t live[2];  // their liveness bytes
 };
 
 // cols: column indices of vectors [s0, s0 + 32) of the window, one per lane.
@@ -88,82 +88,94 @@ template <int NC>
 __device__ __forceinline__ void att_issue(const AttendArgs& a, uint32_t base, uint32_t vend, uint32_t s, uint32_t s0,
                                           uint32_t cols, uint32_t lane, AttStep<NC>& st) {
     const uint32_t g = lane >> 2, t = lane & 3, off = s - s0;
-    const uint32_t c0 = __shfl_sync(0xffffffffu, cols, off + g);
-    const uint32_t c1 = __shfl_sync(0xffffffffu, cols, off + 8 + g);
-    const uint32_t cl = __shfl_sync(0xffffffffu, cols, off + (lane & 15));
-    const bool ok0 = s + g < vend, ok1 = s + 8 + g < vend;
-    const __half* r0 = a.h + static_cast<uint64_t>(c0) * a.ldh + 8 * t;
-    const __half* r1 = a.h + static_cast<uint64_t>(c1) * a.ldh + 8 * t;
 #pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        st.h[0][c] = ok0 ? ld_gather_128(r0 + 32 * c) : make_uint4(0, 0, 0, 0);
-        st.h[1][c] = ok1 ? ld_gather_128(r1 + 32 * c) : make_uint4(0, 0, 0, 0);
+    for (int hf = 0; hf < 2; ++hf) {
+        const uint32_t v = s + 8 * hf + g;
+        const uint32_t col = __shfl_sync(0xffffffffu, cols, off + 8 * hf + g);
+        const bool ok = v < vend;
+        const __half* r = a.h + static_cast<uint64_t>(col) * a.ldh + 8 * t;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) st.h[hf][c] = ok ? ld_gather_128(r + 32 * c) : make_uint4(0, 0, 0, 0);
+        st.rn[hf] = ok ? __ldg(a.rn + col) : 0.f;
+        st.live[hf] = ok ? static_cast<uint32_t>(__ldg(a.live + base + v)) : 0u;
     }
-    const bool okl = lane < 16 && s + lane < vend;
-    st.rnj = okl ? __ldg(a.rn + cl) : 0.f;
-    st.live = okl ? static_cast<uint32_t>(__ldg(a.live + base + s + lane)) : 0u;
 }
 
 __device__ __forceinline__ uint32_t comp(const uint4& v, int k) {
     return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
 }
 
+// Scores of one step, zero C (no accumulator materialisation).
+__device__ __forceinline__ void mma_f16_16816_z(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                               uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%10,%10,%10,%10};"
+        : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1), "f"(0.f));
+}
+
+// Swap form (vectors on M): lane (g, t) owns vectors g, g + 8 and rows
+// 2t, 2t + 1 of the window.
+//   S^T (16 vec x 8 rows) = Hj (16 x F) . Hi^T      A = gathered rows, B = Hi
+//   O^T (F x 8 rows)     += Hj^T (F x 16) . P^T     A = movmatrix(Hj), B = movmatrix(P^T)
+// m, l: running max (log2 units) and lane-partial sum of rows 2t, 2t + 1.
+// o[c][q]: features phi(c, 2q + j, g) = 32c + 8(g >> 1) + 2(2q + j) + (g & 1),
+// j = 0 (o[0], o[1]) and 1 (o[2], o[3]); o[.][.][e & 1] is row 2t + (e & 1).
 template <int NC>
-__device__ __forceinline__ void att_compute(const AttStep<NC>& st, const uint4 (&hi)[NC], float qscale, uint32_t lane,
-                                            float& m, float& l, float (&o)[NC][4][4]) {
-    const uint32_t g = lane >> 2, t = lane & 3;
-    // S = Hi . Hj^T: acc[hf][e] = S[row g][vector 8hf + 2t + e] (e < 2; 2, 3 padding rows)
-    float acc[2][4];
+__device__ __forceinline__ void att_compute(const AttStep<NC>& st, const uint4 (&hi)[NC], const float (&qs)[2],
+                                            uint32_t lane, float (&m)[2], float (&l)[2], float (&o)[NC][2][4]) {
+    const uint32_t t = lane & 3;
+    float acc[4];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf) {
-        acc[hf][0] = acc[hf][1] = acc[hf][2] = acc[hf][3] = 0.f;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            mma_f16_16816(acc[hf], hi[c].x, 0u, hi[c].y, 0u, st.h[hf][c].x, st.h[hf][c].y);
-            mma_f16_16816(acc[hf], hi[c].z, 0u, hi[c].w, 0u, st.h[hf][c].z, st.h[hf][c].w);
-        }
+    for (int c = 0; c < NC; ++c) {
+        const uint4 &x = st.h[0][c], &y = st.h[1][c];
+        if (c == 0) mma_f16_16816_z(acc, x.x, y.x, x.y, y.y, hi[c].x, hi[c].y);
+        else mma_f16_16816(acc, x.x, y.x, x.y, y.y, hi[c].x, hi[c].y);
+        mma_f16_16816(acc, x.z, y.z, x.w, y.w, hi[c].z, hi[c].w);
     }
-    float z[2][2];
-    float mx = -INFINITY;
+    // acc: (vector g, row 2t), (g, 2t+1), (g+8, 2t), (g+8, 2t+1)
+    float z[4];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf)
+    for (int e = 0; e < 4; ++e) {
+        const int hf = e >> 1, r = e & 1;
+        const bool live = (st.live[hf] >> (2 * t + r)) & 1u;
+        z[e] = live ? acc[e] * qs[r] * st.rn[hf] : -INFINITY;
+    }
+    float mx[2] = {fmaxf(z[0], z[2]), fmaxf(z[1], z[3])};
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const uint32_t v = 8 * hf + 2 * t + e;
-            const float rj = __shfl_sync(0xffffffffu, st.rnj, v);
-            const uint32_t lv = __shfl_sync(0xffffffffu, st.live, v);
-            z[hf][e] = (lv >> g) & 1u ? acc[hf][e] * qscale * rj : -INFINITY;
-            mx = fmaxf(mx, z[hf][e]);
-        }
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-    const float mn = fmaxf(m, mx);
-    // No early exit: the MMAs below are warp-collective.  A row with no live
-    // slot yet keeps m = -inf and gets p = 0 (exp2(-inf - 0)).
-    const float mref = mn == -INFINITY ? 0.f : mn;
-    const float alpha = fast_exp2(m - mref);  // m = -inf -> 0
-    m = mn;
-    float p[2][2];
-    float ps = 0.f;
+    for (int o2 = 4; o2 <= 16; o2 <<= 1) {
+        mx[0] = fmaxf(mx[0], __shfl_xor_sync(0xffffffffu, mx[0], o2));
+        mx[1] = fmaxf(mx[1], __shfl_xor_sync(0xffffffffu, mx[1], o2));
+    }
+    float alpha[2], mref[2];
 #pragma unroll
-    for (int hf = 0; hf < 2; ++hf)
+    for (int r = 0; r < 2; ++r) {
+        const float mn = fmaxf(m[r], mx[r]);
+        // no early exit (the MMAs are warp-collective): a row with no live
+        // slot yet keeps m = -inf and gets p = 0
+        mref[r] = mn == -INFINITY ? 0.f : mn;
+        alpha[r] = fast_exp2(m[r] - mref[r]);  // m = -inf -> 0
+        m[r] = mn;
+    }
+    float p[4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            p[hf][e] = fast_exp2(z[hf][e] - mref);
-            ps += p[hf][e];
-        }
-    l = l * alpha + ps;
-    // P as the A operand: k = vectors 2t, 2t+1 (half 0) and 2t+8, 2t+9 (half 1)
-    const uint32_t pa0 = f2_to_h2(p[0][0], p[0][1]), pa2 = f2_to_h2(p[1][0], p[1][1]);
+    for (int e = 0; e < 4; ++e) p[e] = fast_exp2(z[e] - mref[e & 1]);
+    l[0] = l[0] * alpha[0] + (p[0] + p[2]);
+    l[1] = l[1] * alpha[1] + (p[1] + p[3]);
+    // P^T as the B operand: k = vectors 2t, 2t+1 (b0) and 2t+8, 2t+9 (b1), n = row g
+    const uint32_t b0 = movtrans(f2_to_h2(p[0], p[1])), b1 = movtrans(f2_to_h2(p[2], p[3]));
 #pragma unroll
     for (int c = 0; c < NC; ++c)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            float (&d)[4] = o[c][k];
-            d[0] *= alpha;
-            d[1] *= alpha;
-            const uint32_t b0 = movtrans(comp(st.h[0][c], k)), b1 = movtrans(comp(st.h[1][c], k));
-            mma_f16_16816(d, pa0, 0u, pa2, 0u, b0, b1);
+        for (int q = 0; q < 2; ++q) {
+            float (&d)[4] = o[c][q];
+            d[0] *= alpha[0];
+            d[1] *= alpha[1];
+            d[2] *= alpha[0];
+            d[3] *= alpha[1];
+            mma_f16_16816(d, movtrans(comp(st.h[0][c], 2 * q)), movtrans(comp(st.h[0][c], 2 * q + 1)),
+                          movtrans(comp(st.h[1][c], 2 * q)), movtrans(comp(st.h[1][c], 2 * q + 1)), b0, b1);
         }
 }
 
@@ -177,21 +189,26 @@ __global__ void __launch_bounds__(kAgnnWarps * 32, agnn_bps(NC)) agnn_attend_ker
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t* ci = a.ci + base;
         const uint32_t vend = it.vend;
-        const uint64_t row = 8ull * it.window + g;
-        const bool row_ok = row < a.rows;
-        const int64_t node = a.row0 + static_cast<int64_t>(row_ok ? row : 0);
+        const uint64_t row_g = 8ull * it.window + g;  // Hi operand row
+        const bool g_ok = row_g < a.rows;
+        const int64_t node_g = a.row0 + static_cast<int64_t>(g_ok ? row_g : 0);
         uint4 hi[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
-            hi[c] = row_ok ? ld_gather_128(a.h + node * a.ldh + 32 * c + 8 * t) : make_uint4(0, 0, 0, 0);
-        const float qscale = row_ok ? a.scale2 * __ldg(a.rn + node) : 0.f;
+            hi[c] = g_ok ? ld_gather_128(a.h + node_g * a.ldh + 32 * c + 8 * t) : make_uint4(0, 0, 0, 0);
+        float qs[2];  // scale * log2(e) / |h_i| of rows 2t, 2t + 1
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint64_t row = 8ull * it.window + 2 * t + r;
+            qs[r] = row < a.rows ? a.scale2 * __ldg(a.rn + a.row0 + static_cast<int64_t>(row)) : 0.f;
+        }
 
-        float m = -INFINITY, l = 0.f;
-        float o[NC][4][4];
+        float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+        float o[NC][2][4];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
 #pragma unroll
-            for (int k = 0; k < 4; ++k) o[c][k][0] = o[c][k][1] = o[c][k][2] = o[c][k][3] = 0.f;
+            for (int q = 0; q < 2; ++q) o[c][q][0] = o[c][q][1] = o[c][q][2] = o[c][q][3] = 0.f;
 
         uint32_t s = it.vbeg;
         if (s < vend) {
@@ -202,7 +219,7 @@ __global__ void __launch_bounds__(kAgnnWarps * 32, agnn_bps(NC)) agnn_attend_ker
             att_issue<NC>(a, base, vend, s, s0, cur, lane, sa);
             for (;;) {  // invariant: s == s0, cur = columns of steps s and s + 16
                 if (s + 16 < vend) att_issue<NC>(a, base, vend, s + 16, s0, cur, lane, sb);
-                att_compute<NC>(sa, hi, qscale, lane, m, l, o);
+                att_compute<NC>(sa, hi, qs, lane, m, l, o);
                 if (s + 16 >= vend) break;
                 if (s + 32 < vend) {  // advance the column window by 32
                     s0 += 32;
@@ -210,32 +227,50 @@ __global__ void __launch_bounds__(kAgnnWarps * 32, agnn_bps(NC)) agnn_attend_ker
                     nxt = s0 + 32 + lane < vend ? ld_stream_u32(ci + s0 + 32 + lane) : 0u;
                     att_issue<NC>(a, base, vend, s + 32, s0, cur, lane, sa);
                 }
-                att_compute<NC>(sb, hi, qscale, lane, m, l, o);
+                att_compute<NC>(sb, hi, qs, lane, m, l, o);
                 s += 32;
                 if (s >= vend) break;
             }
         }
-        l += __shfl_xor_sync(0xffffffffu, l, 1);
-        l += __shfl_xor_sync(0xffffffffu, l, 2);
-        const bool split = it.slot != kNoSlot;
-        float* dst;
-        float inv = 1.f;
-        if (split) {
-            dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + g) * F;
-            if (t == 0) a.pstat[static_cast<uint64_t>(it.slot) * 8 + g] = make_float2(m, l);
-        } else {
-            dst = a.out + row * a.ldo;
-            inv = l > 0.f ? 1.f / l : 0.f;
-        }
-        // lane (g, t): features 32c + 8t + 2k + e of row g in o[c][k][e]
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            if (!split && !row_ok) break;
-            float* p = dst + 32 * c + 8 * t;
-            *reinterpret_cast<float4*>(p) =
-                make_float4(o[c][0][0] * inv, o[c][0][1] * inv, o[c][1][0] * inv, o[c][1][1] * inv);
-            *reinterpret_cast<float4*>(p + 4) =
-                make_float4(o[c][2][0] * inv, o[c][2][1] * inv, o[c][3][0] * inv, o[c][3][1] * inv);
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int o2 = 4; o2 <= 16; o2 <<= 1) l[r] += __shfl_xor_sync(0xffffffffu, l[r], o2);
+        const bool split = it.slot != kNoSlot;
+        if (split && g == 0) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r)
+                a.pstat[static_cast<uint64_t>(it.slot) * 8 + 2 * t + r] = make_float2(m[r], l[r]);
+        }
+        // Lanes g and g ^ 1 hold the even / odd features of the same 8-feature
+        // group: swap halves so that each writes 4 contiguous features of its
+        // rows (even g: group + 0..3, odd g: group + 4..7).
+        const bool odd = g & 1;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint64_t row = 8ull * it.window + 2 * t + r;
+            float* dst;
+            float inv = 1.f;
+            if (split) {
+                dst = a.partial + (static_cast<uint64_t>(it.slot) * 8 + 2 * t + r) * F;
+            } else {
+                dst = a.out + row * a.ldo;
+                inv = l[r] > 0.f ? 1.f / l[r] : 0.f;
+            }
+            const bool ok = split || row < a.rows;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                // own values at features 2k + (g & 1), k = 0..3: o[c][k >> 1][2 (k & 1) + r]
+                const float v0 = o[c][0][r], v1 = o[c][0][2 + r], v2 = o[c][1][r], v3 = o[c][1][2 + r];
+                // even lane keeps k = 0, 1 and receives the odd lane's k = 0, 1
+                const float s0v = odd ? v0 : v2, s1v = odd ? v1 : v3;
+                const float r0v = __shfl_xor_sync(0xffffffffu, s0v, 4);
+                const float r1v = __shfl_xor_sync(0xffffffffu, s1v, 4);
+                float4 out;
+                if (!odd) out = make_float4(v0 * inv, r0v * inv, v1 * inv, r1v * inv);
+                else out = make_float4(r0v * inv, v2 * inv, r1v * inv, v3 * inv);
+                if (ok) *reinterpret_cast<float4*>(dst + 32 * c + 8 * (g >> 1) + 4 * odd) = out;
+            }
         }
     }
 }
