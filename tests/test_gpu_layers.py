@@ -289,6 +289,12 @@ def test_agnn_attend_agrees_with_three_pass_aggregate():
     three = T.agnn_aggregate(me, hn, hc, 1.3)
     fused = T.agnn_attend(me, hc, 1.3)
     assert _rel_l2(fused, three) < 5e-3
+    # only the pattern and liveness are read: a TF32-encoded mask (block
+    # width 4) gives the same result
+    me32 = T.encode_mebcrs(T.CsrMatrix(rows, rows, torch.from_numpy(m.row_ptr.view(np.int32)).cuda(),
+                                       torch.from_numpy(m.col_idx.view(np.int32)).cuda(),
+                                       torch.from_numpy(m.values).cuda()), T.Precision.tf32)
+    assert _rel_l2(T.agnn_attend(me32, hc, 1.3), fused) < 1e-6
 
 
 def test_agnn_attend_row_shard_and_large_scores():
