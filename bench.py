@@ -66,9 +66,63 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+class NvmlClockSampler:
+    """SM clock and throttle reasons sampled every 10 ms through NVML during
+    the timed region (the nvidia-smi loop needs longer to start than a
+    sub-second timed region lasts)."""
+
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+    lead_s = 0.0
+
+    def __init__(self, device):
+        import pynvml
+
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(device)
+        try:
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        self.sm, self.reasons, self.run, self.t = [], 0, False, None
+
+    def _loop(self):
+        nv = self.nv
+        while self.run:
+            self.sm.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            try:
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            time.sleep(0.01)
+
+    def start(self):
+        self.run = True
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
+
+    def stop(self):
+        self.run = False
+        self.t.join(1)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max,
+                "reasons": sorted(k for k, b in self.BITS.items() if self.reasons & b), "samples": len(self.sm),
+                "sampler": "nvml 10 ms"}
+
+
+def clock_sampler(device):
+    try:
+        return NvmlClockSampler(device)
+    except Exception:
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
+    lead_s = 0.15
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
@@ -297,9 +351,9 @@ def run_ours(args, rank, world, device):
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
-    sampler = ClockSampler(device.index if device.index is not None else 0)
+    sampler = clock_sampler(device.index if device.index is not None else 0)
     sampler.start()
-    time.sleep(0.15)
+    time.sleep(sampler.lead_s)  # nvidia-smi loop start-up; NVML samples at once
     l0 = T.launch_count()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
