@@ -1,7 +1,8 @@
 #!/bin/bash
 # compute-sanitizer memcheck/racecheck over the small GPU tests (run on the GPU box):
 #   gpurun --timeout 6000 -- bash tools/sanitize.sh
-OUT=gpurun_out/r1s3s; mkdir -p $OUT
+OUT=gpurun_out/${1:-sanitize}; mkdir -p $OUT
 timeout 2400 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "known or acceptance6 or baseline16_errors or srbcrs_padding or static_mask or decode or taxonomy" > $OUT/memcheck_parity.log 2>&1; echo "rc=$?" >> $OUT/memcheck_parity.log
 timeout 1800 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_layers.py tests/test_gpu_scale.py -m gpu -q -x -k "not config3 and not config5 and not midsize" > $OUT/memcheck_layers.log 2>&1; echo "rc=$?" >> $OUT/memcheck_layers.log
 timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "known_answer" > $OUT/racecheck.log 2>&1; echo "rc=$?" >> $OUT/racecheck.log
+timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_layers.py -m gpu -q -x -k "attend or aggregate" > $OUT/racecheck_layers.log 2>&1; echo "rc=$?" >> $OUT/racecheck_layers.log
