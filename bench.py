@@ -36,6 +36,8 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# mma.sync (HMMA) peak measured on B200 by tools/mma_peak.cu, TFLOP/s.
+MMA_SYNC_PEAK_TFLOPS = {"fp16": 554.6, "tf32": 277.7}
 # Measured ceiling of the SpMM gather pattern on B200 (FP16, 256-byte B rows).
 GATHER_CEILING_GBS = 11757.2
 METRIC = "SpMM/SDDMM effective GFLOP/s (2·nnz·N) and % HBM roofline at 1/2/4/8 B200"
@@ -341,6 +343,14 @@ def run_ours(args, rank, world, device):
     encode_ms = e0.elapsed_time(e1)
     nv, W = me.num_vectors, me.num_windows
     nnz_local = local_csr.nnz
+    # tensor work the kernel issues: one MMA k-step per kin vectors of a
+    # window (16 FP16 / 8 TF32, residue steps padded), 8 rows x N features
+    rp_host = np.empty(W + 1, np.uint32)
+    rc = _abi.load().tcs_mebcrs_download(C.byref(me._h), rp_host.ctypes.data, None, None,
+                                         C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0, _abi.load().tcs_last_error()
+    kin = 16 if prec == T.Precision.fp16 else 8
+    tensor_flops = 2.0 * 8 * kin * N * float(((np.diff(rp_host.astype(np.int64)) + kin - 1) // kin).sum())
 
     out = torch.empty(l_rows, N, dtype=torch.float32, device=device)
     cfg = T.KernelConfig(prec)
@@ -448,7 +458,7 @@ def run_ours(args, rank, world, device):
         e2e = run_e2e(args, T, _abi, local_csr, B, l_rows, cols, N, prec, device, world)
 
     res = {"rank": rank, "nnz": nnz_local, "nv": nv, "W": W, "step_ms": step_ms, "encode_ms": encode_ms,
-           "bytes_alg": balg, "bytes_min": bmin, "achieved": achieved}
+           "bytes_alg": balg, "bytes_min": bmin, "achieved": achieved, "tensor_flops": tensor_flops}
     gathered = [res]
     if world > 1:
         gathered = [None] * world
@@ -484,7 +494,17 @@ def run_ours(args, rank, world, device):
                      "gather_ceiling": {"achieved_over_ceiling": round(achieved / GATHER_CEILING_GBS, 4),
                                         "ceiling_gbs": GATHER_CEILING_GBS,
                                         "source": "profiles/r1s3_gather_bench2.txt (LDG+SHFL+PRMT+HMMA+values ahead)"}
-                     if prec == 0 else None},
+                     if prec == 0 else None,
+                     # the legacy tensor path this kernel uses (HMMA), against its
+                     # measured peak; the tcgen05 bf16 peak for scale
+                     "tensor_pipe": {"issued_tflop_per_launch": round(tensor_flops / 1e12, 4),
+                                     "achieved_tflops": round(tensor_flops / (step_ms / 1e3) / 1e12, 2),
+                                     "peak_mma_sync_tflops": MMA_SYNC_PEAK_TFLOPS[args.precision],
+                                     "frac": round(tensor_flops / (step_ms / 1e3) / 1e12
+                                                   / MMA_SYNC_PEAK_TFLOPS[args.precision], 4),
+                                     "frac_of_tcgen05_bf16_peak": round(tensor_flops / (step_ms / 1e3) / 1e12
+                                                                        / 1693.0, 4),
+                                     "peak_source": "tools/mma_peak.cu (profiles/r1s4_mma_sync_peak.txt)"}},
         "gpu_launches": launches,
         "clocks": clocks,
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
