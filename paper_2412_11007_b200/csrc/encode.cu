@@ -51,7 +51,19 @@ struct CheckOut {
     // `big` -- so the big-window kernels start the longest windows first and
     // no kernel walks (and skips) the windows of another class
     uint32_t n_small, n_medium, n_huge;
+    // dynamic window queues of the big-window kernels (a hub window of 10^5+
+    // entries must not delay the windows behind it on a fixed CTA stride)
+    uint32_t next_sort_big, next_bitmap, next_scatter_big;
 };
+
+// CTA-wide queue claim: thread 0 takes the next index, every thread gets it.
+__device__ __forceinline__ uint32_t cta_next(uint32_t* counter) {
+    __shared__ uint32_t s_next;
+    __syncthreads();  // the previous claim has been read by every thread
+    if (threadIdx.x == 0) s_next = atomicAdd(counter, 1u);
+    __syncthreads();
+    return s_next;
+}
 
 // i-th window of the big list: huge ones first (front), then medium (back).
 __device__ __forceinline__ uint32_t big_window(const uint32_t* big, uint64_t W, uint32_t n_huge, uint32_t i) {
@@ -253,7 +265,7 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                                                const uint32_t* __restrict__ big, uint32_t n_huge,
                                                                uint32_t n_big) {
     extern __shared__ uint64_t smem_keys[];
-    for (uint32_t i = blockIdx.x; i < n_big; i += gridDim.x) {
+    for (uint32_t i = cta_next(&chk->next_sort_big); i < n_big; i = cta_next(&chk->next_sort_big)) {
         const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
@@ -285,7 +297,7 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
     uint32_t* pre = bm_smem + words;
     __shared__ uint32_t rb[VH + 1];
     const uint32_t nt = blockDim.x, wpt = (words + nt - 1) / nt;
-    for (uint32_t bi = blockIdx.x; bi < n_big; bi += gridDim.x) {
+    for (uint32_t bi = cta_next(&chk->next_bitmap); bi < n_big; bi = cta_next(&chk->next_bitmap)) {
         const uint64_t w = big_window(big, W, n_huge, bi);
         const uint64_t r0 = VH * w;
         const uint32_t e0 = csr_rp[r0];
@@ -357,13 +369,15 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
                                                       const uint32_t* __restrict__ list, bool big_list,
-                                                      uint32_t n_huge, uint32_t n_list) {
+                                                      uint32_t n_huge, uint32_t n_list, uint32_t* next) {
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
     __shared__ uint32_t rlo[VH + 1], rhi[VH], roff[VH + 1];  // this tile's entry range per row
     constexpr uint32_t kTile = TILE * 8 / VH;  // vectors per smem tile
-    for (uint32_t li = blockIdx.x; li < n_list; li += gridDim.x) {
+    // big list: dynamic queue (next != nullptr); small list: fixed stride
+    for (uint32_t li = next ? cta_next(next) : blockIdx.x; li < n_list;
+         li = next ? cta_next(next) : li + gridDim.x) {
         const uint64_t w = big_list ? big_window(list, W, n_huge, li) : list[li];
         const uint64_t r0 = VH * w;
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
@@ -456,7 +470,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
 template <typename V>
 V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
                            const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, uint32_t,
-                           uint32_t));
+                           uint32_t, uint32_t*));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
                          "column indices must be strictly ascending within a row"};
@@ -585,7 +599,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                 kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
                                                     static_cast<decltype(kern_value_type(kern))*>(m.values), list, big,
-                                                    h.n_huge, n);
+                                                    h.n_huge, n, big ? &dchk->next_scatter_big : nullptr);
             };
             if (value_dtype == TCS_DTYPE_F16) {
                 scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
