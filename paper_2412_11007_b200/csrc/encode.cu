@@ -35,6 +35,8 @@
 namespace tcs {
 namespace {
 
+constexpr uint32_t kTinyCap = 256;      // entries per window, one warp (window_sort_warp)
+constexpr int kTinyWarps = 8;           // warps per CTA of window_sort_warp
 constexpr uint32_t kSmallCap = 2048;    // entries per window, 128-thread CTA, 32 KB smem
 constexpr uint32_t kSmallThreads = 128;
 constexpr uint32_t kBigCap = 12288;     // 512-thread CTA, 192 KB smem
@@ -51,6 +53,7 @@ struct CheckOut {
     // `big` -- so the big-window kernels start the longest windows first and
     // no kernel walks (and skips) the windows of another class
     uint32_t n_small, n_medium, n_huge;
+    uint32_t n_tiny;  // tiny (<= kTinyCap entries) from the front of `small`, small from its back
     // dynamic window queues of the big-window kernels (a hub window of 10^5+
     // entries must not delay the windows behind it on a fixed CTA stride)
     uint32_t next_sort_big, next_bitmap, next_scatter_big;
@@ -109,7 +112,8 @@ __global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uin
                 ok = true;
             }
         }
-        list_push(ok && n <= kSmallCap, static_cast<uint32_t>(w), &out->n_small, small, false, W);
+        list_push(ok && n <= kTinyCap, static_cast<uint32_t>(w), &out->n_tiny, small, false, W);
+        list_push(ok && n > kTinyCap && n <= kSmallCap, static_cast<uint32_t>(w), &out->n_small, small, true, W);
         list_push(ok && n > kBigCap, static_cast<uint32_t>(w), &out->n_huge, big, false, W);
         list_push(ok && n > kSmallCap && n <= kBigCap, static_cast<uint32_t>(w), &out->n_medium, big, true, W);
     }
@@ -250,8 +254,102 @@ __global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_
                                                                    const uint32_t* __restrict__ small, uint32_t n_small) {
     __shared__ uint64_t bufA[kSmallCap];
     __shared__ uint64_t bufB[kSmallCap];
-    for (uint32_t i = blockIdx.x; i < n_small; i += gridDim.x)
-        window_sort_rank<VH>(csr_rp, ci, rows, cols, small[i], bufA, bufB, tmp_cols, rank, nv_out, chk);
+    for (uint32_t i = blockIdx.x; i < n_small; i += gridDim.x)  // small windows sit at the back of the list
+        window_sort_rank<VH>(csr_rp, ci, rows, cols, small[W - 1 - i], bufA, bufB, tmp_cols, rank, nv_out, chk);
+}
+
+// Tiny windows (<= kTinyCap entries, most of an R-MAT graph's 10^6 windows):
+// one warp per window, no CTA barriers.  The VH rows are sorted runs staged
+// in shared memory; an entry's position in the stable (column, row) merge is
+// its offset in its own row plus, per other row, the number of entries with
+// a smaller column (a larger-or-equal one for rows above it) -- binary
+// searches.  The merged columns then give the first-occurrence flags, whose
+// warp prefix is the rank (ref partition.hpp:55-64: sort + unique).
+template <int VH>
+__global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32_t* __restrict__ csr_rp,
+                                                                    const uint32_t* __restrict__ ci, uint64_t rows,
+                                                                    uint64_t cols, uint32_t* __restrict__ tmp_cols,
+                                                                    uint32_t* __restrict__ rank,
+                                                                    uint32_t* __restrict__ nv_out, CheckOut* chk,
+                                                                    const uint32_t* __restrict__ tiny,
+                                                                    uint32_t n_tiny) {
+    constexpr uint32_t kPer = kTinyCap / 32;  // entries per lane
+    __shared__ uint32_t s_col[kTinyWarps][kTinyCap];
+    __shared__ uint32_t s_mrg[kTinyWarps][kTinyCap];
+    __shared__ uint32_t s_rb[kTinyWarps][VH + 1];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t* col = s_col[wid];
+    uint32_t* mrg = s_mrg[wid];
+    uint32_t* rb = s_rb[wid];
+    uint32_t bad = 0;
+    for (uint32_t i = blockIdx.x * kTinyWarps + wid; i < n_tiny; i += gridDim.x * kTinyWarps) {
+        const uint64_t w = tiny[i], r0 = VH * w;
+        uint32_t b = 0;
+        if (lane <= VH) b = __ldg(csr_rp + min(r0 + lane, rows));
+        const uint32_t e0 = __shfl_sync(0xffffffffu, b, 0);
+        if (lane <= VH) rb[lane] = b - e0;
+        const uint32_t n = __shfl_sync(0xffffffffu, b, VH) - e0;
+        for (uint32_t j = lane; j < n; j += 32) col[j] = __ldg(ci + e0 + j);
+        __syncwarp();
+        uint32_t pos[kPer];
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            const uint32_t j = lane + 32 * k;
+            pos[k] = 0;
+            if (j >= n) continue;
+            const uint32_t c = col[j];
+            uint32_t r = 0;  // row of entry j: the last r with rb[r] <= j (empty rows share boundaries)
+            bool row_start = false;
+#pragma unroll
+            for (int q = 0; q < VH; ++q) {
+                r = rb[q] <= j ? q : r;
+                row_start |= rb[q] == j;
+            }
+            if (c >= cols) bad = max(bad, 3u);
+            if (!row_start && col[j - 1] >= c) bad = max(bad, 4u);
+            uint32_t p = j - rb[r];
+#pragma unroll
+            for (int q = 0; q < VH; ++q) {
+                if (q == static_cast<int>(r)) continue;
+                // rows above: entries with column <= c precede; rows below: < c
+                uint32_t lo = rb[q], hi = rb[q + 1];
+                const uint32_t base = lo;
+                while (lo < hi) {
+                    const uint32_t mid = (lo + hi) >> 1;
+                    const uint32_t x = col[mid];
+                    if (q < static_cast<int>(r) ? x <= c : x < c) lo = mid + 1;
+                    else hi = mid;
+                }
+                p += lo - base;
+            }
+            pos[k] = min(p, n - 1);  // invalid input (flagged above) must not write out of range
+            mrg[pos[k]] = c;
+        }
+        __syncwarp();
+        // first-occurrence flags of the merged columns -> inclusive prefix U
+        // (stored over `col`, no longer needed); U - 1 is the rank
+        uint32_t nv = 0;
+        for (uint32_t p0 = 0; p0 < n; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            const bool valid = p < n;
+            const uint32_t x = valid ? mrg[p] : 0u;
+            const bool first = valid && (p == 0 || mrg[p - 1] != x);
+            const uint32_t m = __ballot_sync(0xffffffffu, first);
+            const uint32_t u = nv + __popc(m & (0xffffffffu >> (31 - lane)));
+            if (valid) col[p] = u;
+            if (first) tmp_cols[e0 + u - 1] = x;
+            nv += __popc(m);
+        }
+        __syncwarp();
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            const uint32_t j = lane + 32 * k;
+            if (j < n) rank[e0 + j] = col[pos[k]] - 1;
+        }
+        if (lane == 0) nv_out[w] = nv;
+        __syncwarp();  // shared buffers are reused by the next window
+    }
+    if (bad) atomicMax(&chk->bad, bad);
 }
 
 template <int VH>
@@ -368,8 +466,8 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ tmp_cols,
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
-                                                      const uint32_t* __restrict__ list, bool big_list,
-                                                      uint32_t n_huge, uint32_t n_list, uint32_t* next) {
+                                                      const uint32_t* __restrict__ list, uint32_t n_front,
+                                                      uint32_t n_list, uint32_t* next) {
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
@@ -378,7 +476,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
     // big list: dynamic queue (next != nullptr); small list: fixed stride
     for (uint32_t li = next ? cta_next(next) : blockIdx.x; li < n_list;
          li = next ? cta_next(next) : li + gridDim.x) {
-        const uint64_t w = big_list ? big_window(list, W, n_huge, li) : list[li];
+        const uint64_t w = big_window(list, W, n_front, li);  // n_front from the front, the rest from the back
         const uint64_t r0 = VH * w;
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
         const uint32_t base = rp[w], nvw = rp[w + 1] - base;
@@ -469,7 +567,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
 // Value type V of a window_scatter instantiation (for the launch helper).
 template <typename V>
 V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
-                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, uint32_t,
+                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, uint32_t,
                            uint32_t, uint32_t*));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
@@ -544,6 +642,15 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             DBuf nvw(W * 4, s);
             CheckOut* dchk = chk.as<CheckOut>();
             const uint32_t n_big = h.n_medium + h.n_huge;
+            if (h.n_tiny) {
+                const int gt = static_cast<int>(
+                    std::min<uint64_t>((h.n_tiny + kTinyWarps - 1) / kTinyWarps, uint64_t(sms) * 8));
+                window_sort_warp<VH><<<gt, kTinyWarps * 32, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols,
+                                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
+                                                                    nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>(),
+                                                                    h.n_tiny);
+                TCS_LAUNCHED("window_sort_warp");
+            }
             if (h.n_small) {
                 const int g1 = static_cast<int>(std::min<uint64_t>(h.n_small, uint64_t(sms) * 16));
                 window_sort_small<VH><<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
@@ -598,19 +705,20 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                                               static_cast<int>(tile_smem)));
                 kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
-                                                    static_cast<decltype(kern_value_type(kern))*>(m.values), list, big,
-                                                    h.n_huge, n, big ? &dchk->next_scatter_big : nullptr);
+                                                    static_cast<decltype(kern_value_type(kern))*>(m.values), list,
+                                                    big ? h.n_huge : h.n_tiny, n,
+                                                    big ? &dchk->next_scatter_big : nullptr);
             };
             if (value_dtype == TCS_DTYPE_F16) {
                 scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
                         kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
                 scatter(window_scatter<VH, __half, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
-                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_small);
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_tiny + h.n_small);
             } else {
                 scatter(window_scatter<VH, float, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
                         kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
                 scatter(window_scatter<VH, float, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
-                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_small);
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_tiny + h.n_small);
             }
             TCS_LAUNCHED("window_scatter");
         } else {
