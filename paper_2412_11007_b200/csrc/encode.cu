@@ -35,7 +35,10 @@
 namespace tcs {
 namespace {
 
-constexpr uint32_t kTinyCap = 256;      // entries per window, one warp (window_sort_warp)
+#ifndef TCS_ENC_TINY_CAP
+#define TCS_ENC_TINY_CAP 256
+#endif
+constexpr uint32_t kTinyCap = TCS_ENC_TINY_CAP;  // entries per window, one warp (window_sort_warp)
 constexpr int kTinyWarps = 8;           // warps per CTA of window_sort_warp
 constexpr uint32_t kSmallCap = 2048;    // entries per window, 128-thread CTA, 32 KB smem
 constexpr uint32_t kSmallThreads = 128;
