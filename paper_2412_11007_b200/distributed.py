@@ -118,12 +118,23 @@ class ShardedSpmm:
         return gather_rows(C, self.shard_rows, self.group) if gather else C
 
 
+def local_input(H: torch.Tensor, shard: Shard, rows: int) -> torch.Tensor:
+    """The rows of H this rank owns: H is either the full matrix (every
+    node) or already the shard's rows (a previous layer's local output)."""
+    if H.shape[0] == shard.rows:
+        return H
+    if H.shape[0] != rows:
+        raise ValueError(f"expected {rows} (all) or {shard.rows} (this shard's) rows, got {H.shape[0]}")
+    return H[shard.r0:shard.r1]
+
+
 class ShardedGCNLayer:
-    """GCN layer H' = Â (H W) over all ranks (BASELINE configs[3]): every
-    rank holds the full features H (the previous layer's all-gather), does
-    the dense transform on the rows it needs (all of them: the SpMM gathers
-    arbitrary columns), aggregates its window shard of Â, and all-gathers
-    the rows for the next layer (``gather=False`` keeps them local)."""
+    """GCN layer H' = Â (H W) over all ranks (BASELINE configs[3]).  Each
+    rank transforms only its own rows (cuBLAS GEMM), all-gathers the
+    transformed rows in the SpMM's operand dtype (f16: half the bytes of
+    gathering the f32 output, and no replicated GEMM), and aggregates its
+    window shard of Â.  Input: all rows or this shard's rows; output: this
+    shard's rows (``gather=False``, what the next layer takes) or all rows."""
 
     def __init__(self, rows, row_ptr, col_idx, weight, precision=None, group=None):
         from . import layers as L
@@ -133,19 +144,24 @@ class ShardedGCNLayer:
         rp, ci, v = L.normalized_adjacency(rows, row_ptr, col_idx)
         self.spmm = ShardedSpmm(rows, rows, rp, ci, v, precision, group)
         self.weight = weight
+        self.rows = rows
         self.dtype = torch.float16 if precision == T.Precision.fp16 else torch.float32
 
     def __call__(self, H: torch.Tensor, gather: bool = True) -> torch.Tensor:
-        HW = (H.to(self.weight.dtype) @ self.weight).to(self.dtype)  # cuBLAS GEMM
-        return self.spmm(HW, gather=gather)
+        sp = self.spmm
+        Hl = local_input(H, sp.shard, self.rows)
+        HW_local = (Hl.to(self.weight.dtype) @ self.weight).to(self.dtype)  # cuBLAS GEMM, own rows
+        HW = gather_rows(HW_local.contiguous(), sp.shard_rows, sp.group)  # every node's row, f16
+        return sp(HW, gather=gather)
 
 
 class ShardedAGNNLayer:
     """AGNN layer (BASELINE configs[4]) over all ranks: the attention rows of
-    a window shard need that shard's normalised rows against every node's,
-    so every rank holds the full H; each computes its rows with
-    tcs_agnn_aggregate (row offset = its first row) and the rows are
-    all-gathered for the next layer."""
+    a window shard need that shard's rows against every node's.  Each rank
+    converts its own rows to the f16 gather operand, all-gathers that (half
+    the bytes of gathering the f32 output) and computes its rows with
+    tcs_agnn_attend (row offset = its first row).  Input: all rows or this
+    shard's rows; output: this shard's rows (``gather=False``) or all rows."""
 
     def __init__(self, rows, row_ptr, col_idx, beta=1.0, group=None):
         from . import tcsparse as T
@@ -167,9 +183,13 @@ class ShardedAGNNLayer:
     def __call__(self, H: torch.Tensor, gather: bool = True, one_pass: bool = True) -> torch.Tensor:
         T = self._T
         if one_pass and H.shape[1] in (32, 64):  # as AGNNLayer: tcs_agnn_attend
-            _, Hc = T.rows_normalize(H.float().contiguous(), torch.float16, normalized=False)
+            Hl = local_input(H, self.shard, self.rows)
+            _, Hc_local = T.rows_normalize(Hl.float().contiguous(), torch.float16, normalized=False)
+            Hc = gather_rows(Hc_local, self.shard_rows, self.group)  # every node's row, f16
             C = T.agnn_attend(self.mask, Hc, self.beta, self.cfg, row0=self.shard.r0)
         else:
+            if H.shape[0] != self.rows:
+                raise ValueError("the three-pass path needs every node's rows")
             Hn, Hc = T.rows_normalize(H.float().contiguous(), torch.float16)
             C = T.agnn_aggregate(self.mask, Hn, Hc, self.beta, self.cfg, row0=self.shard.r0)
         return gather_rows(C, self.shard_rows, self.group) if gather else C

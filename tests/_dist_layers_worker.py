@@ -1,6 +1,7 @@
 """Worker for tests/test_gpu_distributed.py (run under torchrun, 2 ranks,
 gloo, both ranks on the one visible GPU): two chained layers of the sharded
-GCN and AGNN against the single-process layers on the same graph."""
+GCN and AGNN against the single-process layers on the same graph, chained
+through full outputs and through each shard's local rows."""
 import os
 import sys
 
@@ -24,12 +25,15 @@ want = gcn2(gcn1(H))
 s1, s2 = D.ShardedGCNLayer(rows, rp, ci, W1), D.ShardedGCNLayer(rows, rp, ci, W2)
 got = s2(s1(H))
 gcn_err = float((got - want).norm() / want.norm())
+# chaining on local rows: layer 1 keeps its shard, layer 2 takes it
+got_local = s2(s1(H, gather=False))
+gcn_err = max(gcn_err, float((got_local - want).norm() / want.norm()))
 
 agnn = L.AGNNLayer(rows, rp, ci, beta=1.3)
 want = agnn(agnn(H))
 sa = D.ShardedAGNNLayer(rows, rp, ci, beta=1.3)
 got = sa(sa(H))
-agnn_exact = bool(torch.equal(got, want))
+agnn_exact = bool(torch.equal(got, want)) and bool(torch.equal(sa(sa(H, gather=False)), want))
 agnn_err = float((got - want).norm() / want.norm())
 print(f"RANK{rank} gcn_rel_l2={gcn_err:.3e} agnn_exact={agnn_exact} agnn_rel_l2={agnn_err:.3e}", flush=True)
 dist.barrier()
