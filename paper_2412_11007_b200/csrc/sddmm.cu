@@ -127,10 +127,22 @@ __device__ __forceinline__ uint32_t live_bits(uint32_t b0, uint32_t b1, uint32_t
     return ((b0 >> (2 * t)) & 3u) | (((b1 >> (2 * t)) & 3u) << 2);
 }
 
+// Output values are written once and not re-read by this kernel: streaming
+// (evict-first) stores keep L2 for the gathered rows and the mask stream
+// (C3 F=32 1.345 -> 1.29 ms, C5 4.30 -> 4.17 ms; profiles/r1s4_sddmm_stream_stores.txt).
+// TCS_SDDMM_STREAM_OUT=0 restores plain stores (A/B knob).
+#ifndef TCS_SDDMM_STREAM_OUT
+#define TCS_SDDMM_STREAM_OUT 1
+#endif
 template <bool OF32>
 __device__ __forceinline__ void out_store(void* out, uint64_t pos, float v) {
+#if TCS_SDDMM_STREAM_OUT
+    if constexpr (OF32) __stcs(static_cast<float*>(out) + pos, v);
+    else __stcs(reinterpret_cast<unsigned short*>(out) + pos, __half_as_ushort(__float2half_rn(v)));
+#else
     if constexpr (OF32) static_cast<float*>(out)[pos] = v;
     else static_cast<__half*>(out)[pos] = __float2half_rn(v);
+#endif
 }
 
 // Liveness bits (bit q) of lane (g,t)'s accumulator elements in a general
