@@ -84,7 +84,10 @@ constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : 
 #ifndef TCS_SPMM_TF32_BPS_NARROW
 #define TCS_SPMM_TF32_BPS_NARROW 8
 #endif
-constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_NARROW : 4; }
+#ifndef TCS_SPMM_TF32_BPS_WIDE
+#define TCS_SPMM_TF32_BPS_WIDE 4
+#endif
+constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_NARROW : TCS_SPMM_TF32_BPS_WIDE; }
 // Feature slab of the FP16 kernel for N > 64 (experiment knob: 128 or 64).
 // Host pipeline of tcs_spmm_csr_host: at most this many window-range chunks,
 // each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
