@@ -29,7 +29,7 @@ build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/tcs_internal.cuh include/tcs/tcs.h
 $(LIB): $(OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
 
-oracle:
+oracle: lib
 	$(MAKE) -s -C oracle
 
 clean:

@@ -456,6 +456,17 @@ tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision precision, c
                              float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
                              tcs_stream_t stream);
 
+/* ref spmm_baseline16(const CsrMatrix&, const DenseMatrix&, const
+ * KernelConfig&) (spmm.hpp:187-257) with host operands: host CSR + host f32
+ * B [b_rows x n] -> host f32 C [rows x n].  The CSR is partitioned into
+ * 16-row windows on the GPU (ref partition_windows(sparse, 16, k), :195) and
+ * multiplied by tcs_spmm_baseline16.  Errors in the reference's order:
+ * cfg->vector_height != 16 -> ARGUMENT (:190), host_csr->cols != b_rows ->
+ * SHAPE (:191). */
+tcs_status tcs_spmm_baseline16_csr_host(const tcs_csr* host_csr, const float* b, int64_t b_rows, int64_t n,
+                                        float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
+                                        tcs_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

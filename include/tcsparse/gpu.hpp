@@ -4,6 +4,7 @@
 //   tcsparse::encode_mebcrs(m, p)   ->  tcsparse::gpu::encode_mebcrs(m, p)
 //   tcsparse::spmm(a, b, cfg)       ->  tcsparse::gpu::spmm(a, b, cfg)
 //   tcsparse::sddmm(ops, cfg)       ->  tcsparse::gpu::sddmm(ops, cfg)
+//   tcsparse::spmm_baseline16(m, b, cfg) -> tcsparse::gpu::spmm_baseline16(m, b, cfg)
 //
 // Same parameter and return types as the reference (ref mebcrs.hpp:80,
 // spmm.hpp:173, sddmm.hpp:84) -- this header includes the reference's own
@@ -47,10 +48,13 @@ inline void check(tcs_status s) {
     }
 }
 
+// TCS_CFG_COUNT_ACCESS: the transaction counters are filled in the
+// reference's units (its warp gather model, ref spmm.hpp:146-151, replayed
+// on the GPU by the cost model) so every KernelCounters field matches.
 inline tcs_kernel_config config(const KernelConfig& cfg) {
     return tcs_kernel_config{static_cast<tcs_precision>(cfg.precision),
                              static_cast<uint32_t>(cfg.vector_height),
-                             static_cast<tcs_mapping>(cfg.mapping), 0u};
+                             static_cast<tcs_mapping>(cfg.mapping), TCS_CFG_COUNT_ACCESS};
 }
 
 inline KernelCounters counters(const tcs_counters& c) {
@@ -133,6 +137,25 @@ inline SpmmResult spmm(const MeBcrsMatrix& sparse, const DenseMatrix& dense, con
                                 sparse.row_pointers.data(), sparse.column_indices.data(), sparse.values.data(),
                                 dense.data.data(), static_cast<int64_t>(dense.rows),
                                 static_cast<int64_t>(dense.cols), res.output.data.data(), &kc, &cn, nullptr));
+    res.counters = detail::counters(cn);
+    return res;
+}
+
+/// ref spmm.hpp:187-257 -- the non-swapped 16x1 baseline over 16-row
+/// windows of the CSR (the paper's ablation), on the GPU.
+inline SpmmResult spmm_baseline16(const CsrMatrix& sparse, const DenseMatrix& dense, const KernelConfig& cfg) {
+    // the reference's checks, in its order (ref spmm.hpp:190-191)
+    if (cfg.vector_height != 16) throw ArgumentError("baseline path requires vector height 16");
+    if (sparse.cols != dense.rows) throw ShapeError("sparse cols must equal dense rows");
+    const tcs_kernel_config kc = detail::config(cfg);
+    const tcs_csr c{sparse.rows, sparse.cols, sparse.nnz(), sparse.row_ptr.data(), sparse.col_idx.data(),
+                    sparse.values.data()};
+    SpmmResult res;
+    res.output = DenseMatrix(sparse.rows, dense.cols);
+    tcs_counters cn{};
+    detail::check(tcs_spmm_baseline16_csr_host(&c, dense.data.data(), static_cast<int64_t>(dense.rows),
+                                               static_cast<int64_t>(dense.cols), res.output.data.data(), &kc, &cn,
+                                               nullptr));
     res.counters = detail::counters(cn);
     return res;
 }

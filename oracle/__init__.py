@@ -537,3 +537,42 @@ class Ref:
     @staticmethod
     def round_tf32(x):
         return ref().ref_round_tf32(x)
+
+
+def spmm_csr_rows(m: Csr, B: np.ndarray, precision: int, rows=None) -> np.ndarray:
+    """Reference SpMM result (inc/spmm.hpp:126-163) computed from the CSR
+    (orc_spmm_csr_rows): all rows, or the rows listed in ``rows``."""
+    B = np.ascontiguousarray(B, np.float32)
+    N = B.shape[1]
+    sel = None if rows is None else np.ascontiguousarray(rows, np.uint64)
+    n = m.rows if sel is None else sel.size
+    Cm = np.zeros((n, N), np.float32)
+    lib().orc_spmm_csr_rows(C.c_uint64(m.rows), precision, _p(m.row_ptr, _u32p), _p(m.col_idx, _u32p),
+                            _p(m.values, _f32p), _p(B, _f32p), C.c_uint64(B.shape[0]), C.c_uint64(N),
+                            C.c_uint64(N), None if sel is None else _p(sel, _u64p), C.c_uint64(n),
+                            _p(Cm, _f32p), C.c_uint64(N))
+    return Cm
+
+
+def sddmm_csr_rows(m: Csr, precision: int, rp: np.ndarray, ci: np.ndarray, A: np.ndarray, Bt: np.ndarray,
+                   rows=None):
+    """Reference SDDMM values (inc/sddmm.hpp:102-132) of the CSR entries of
+    ``rows`` (all rows if None), in CSR order, with each entry's slot in the
+    ME-BCRS value array of (rp, ci) (orc_sddmm_csr_rows).  Returns
+    (dot[f32], pos[u64]); pos = 2^64-1 marks an entry missing from (rp, ci)."""
+    A = np.ascontiguousarray(A, np.float32)
+    Bt = np.ascontiguousarray(Bt, np.float32)
+    rp = np.ascontiguousarray(rp, np.uint32)
+    ci = np.ascontiguousarray(ci, np.uint32)
+    sel = np.arange(m.rows, dtype=np.uint64) if rows is None else np.ascontiguousarray(rows, np.uint64)
+    lens = (m.row_ptr[sel.astype(np.int64) + 1].astype(np.uint64) - m.row_ptr[sel.astype(np.int64)].astype(np.uint64))
+    eoff = np.zeros(sel.size + 1, np.uint64)
+    np.cumsum(lens, out=eoff[1:])
+    dot = np.zeros(max(int(eoff[-1]), 1), np.float32)
+    pos = np.zeros(max(int(eoff[-1]), 1), np.uint64)
+    lib().orc_sddmm_csr_rows(C.c_uint64(m.rows), precision, K_OF[precision], _p(m.row_ptr, _u32p),
+                             _p(m.col_idx, _u32p), _p(m.values, _f32p), _p(rp, _u32p), _p(ci, _u32p), _p(A, _f32p),
+                             C.c_uint64(A.shape[1]), _p(Bt, _f32p), C.c_uint64(Bt.shape[1]), C.c_uint64(A.shape[1]),
+                             _p(sel, _u64p), C.c_uint64(sel.size), _p(eoff, _u64p), _p(dot, _f32p), _p(pos, _u64p))
+    n = int(eoff[-1])
+    return dot[:n], pos[:n]

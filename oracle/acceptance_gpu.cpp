@@ -53,9 +53,19 @@ bool criterion2() {  // tests/acceptance.cpp:89-110
             for (ThreadMapping mode : {ThreadMapping::direct, ThreadMapping::coalesced}) {
                 const SpmmResult r = gpu::spmm(me, dense, {p, 8, mode});
                 if (r.output != want) return false;
-                if (r.counters.mma_invocations != spmm(me, dense, {p, 8, mode}).counters.mma_invocations)
+                // every counter in the reference's units (ref spmm.hpp:144-151)
+                const KernelCounters rc = spmm(me, dense, {p, 8, mode}).counters;
+                if (r.counters.mma_invocations != rc.mma_invocations || r.counters.transactions != rc.transactions ||
+                    r.counters.transaction_bytes != rc.transaction_bytes || r.counters.useful_bytes != rc.useful_bytes)
                     return false;
             }
+            // tests/acceptance.cpp:105 -- the 16x1 baseline on the CSR
+            const SpmmResult b16 = gpu::spmm_baseline16(m, dense, {p, 16, ThreadMapping::coalesced});
+            if (b16.output != want) return false;
+            const KernelCounters rb = spmm_baseline16(m, dense, {p, 16, ThreadMapping::coalesced}).counters;
+            if (b16.counters.mma_invocations != rb.mma_invocations || b16.counters.transactions != rb.transactions ||
+                b16.counters.transaction_bytes != rb.transaction_bytes || b16.counters.useful_bytes != rb.useful_bytes)
+                return false;
         }
     }
     return true;

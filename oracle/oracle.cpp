@@ -290,6 +290,82 @@ void orc_sddmm(uint64_t rows, uint32_t k, int precision, const uint32_t* rp, con
     }
 }
 
+// ---- CSR-form restatements for full-size parity (BASELINE configs 3-5) ----
+// The reference needs an O(M*K) dense copy to encode (inc/mebcrs.hpp:97),
+// so at C3-C5 sizes the oracle computes the same sums straight from the CSR:
+//
+// SpMM (inc/spmm.hpp:126-163): C[r][n] = sum over the row's stored vectors
+// in ascending column order of rnd(a)*rnd(B[c][n]), accumulated sequentially
+// in fp32 (mma.hpp:55-57, block after block).  The zero fill and residue
+// slots of a window add +-0 and change nothing (orc_spmm_v with strict = 0
+// skips them the same way), so the ascending CSR row loop is the same
+// sequence of additions.  B is rounded once up front (rnd is a pure function
+// of the element).  Rows `sel[i]` (all rows if sel is null) -> C row i.
+void orc_spmm_csr_rows(uint64_t rows, int precision, const uint32_t* row_ptr, const uint32_t* col_idx,
+                       const float* vals, const float* B, uint64_t b_rows, uint64_t ldb, uint64_t N,
+                       const uint64_t* sel, uint64_t n_sel, float* C, uint64_t ldc) {
+    std::vector<float> Br(b_rows * N);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < static_cast<int64_t>(b_rows); ++i)
+        for (uint64_t n = 0; n < N; ++n) Br[i * N + n] = rnd(B[i * ldb + n], precision);
+    const int64_t cnt = static_cast<int64_t>(sel ? n_sel : rows);
+#pragma omp parallel
+    {
+        std::vector<float> acc(N);
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < cnt; ++i) {
+            const uint64_t r = sel ? sel[i] : static_cast<uint64_t>(i);
+            std::fill(acc.begin(), acc.end(), 0.0f);
+            for (uint32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+                if (vals[e] == 0.0f) continue;
+                const float a = rnd(vals[e], precision);
+                const float* brp = Br.data() + static_cast<uint64_t>(col_idx[e]) * N;
+                for (uint64_t n = 0; n < N; ++n) acc[n] += a * brp[n];
+            }
+            std::copy(acc.begin(), acc.end(), C + i * ldc);
+        }
+    }
+}
+
+// SDDMM (inc/sddmm.hpp:102-132) per CSR entry of the selected rows, in CSR
+// order: dot[e] = sum_l rnd(A[r][l]) * rnd(Bt[c][l]) (l ascending) where the
+// f32 value is nonzero (:131), else 0; pos[e] = the entry's slot in the
+// ME-BCRS value array 8*(rp[w]+b*k) + (r%8)*width_b + j (inc/mebcrs.hpp:46-56)
+// for the window's vector list (rp, ci) -- the vector index j of column c is
+// found by a merge of the ascending row and window lists.  Entries are
+// written at offsets eoff[i] + (e - row_ptr[r]) (eoff: prefix of the
+// selected rows' lengths).
+void orc_sddmm_csr_rows(uint64_t rows, int precision, uint32_t k, const uint32_t* row_ptr, const uint32_t* col_idx,
+                        const float* vals, const uint32_t* rp, const uint32_t* ci, const float* A, uint64_t lda,
+                        const float* Bt, uint64_t ldbt, uint64_t F, const uint64_t* sel, uint64_t n_sel,
+                        const uint64_t* eoff, float* dot, uint64_t* pos) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t i = 0; i < static_cast<int64_t>(n_sel); ++i) {
+        const uint64_t r = sel[i], w = r / 8;
+        const uint32_t base = rp[w], nvw = rp[w + 1] - base;
+        uint32_t j = 0;
+        for (uint32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
+            const uint32_t c = col_idx[e];
+            while (j < nvw && ci[base + j] < c) ++j;
+            const uint64_t o = eoff[i] + (e - row_ptr[r]);
+            if (j >= nvw || ci[base + j] != c) {  // not a vector of the window: an encoding error
+                pos[o] = ~0ull;
+                dot[o] = 0.0f;
+                continue;
+            }
+            const uint32_t b = j / k, jj = j % k, width = std::min(k, nvw - b * k);
+            pos[o] = 8ull * (base + b * k) + (r % 8) * width + jj;
+            float acc = 0.0f;
+            if (vals[e] != 0.0f) {
+                const float* a = A + r * lda;
+                const float* bt = Bt + static_cast<uint64_t>(c) * ldbt;
+                for (uint64_t l = 0; l < F; ++l) acc += rnd(a[l], precision) * rnd(bt[l], precision);
+            }
+            dot[o] = acc;
+        }
+    }
+}
+
 // count_mma (inc/analysis.hpp:34-38) for the swap8 strategy:
 //   sum_w ceil(nv_w / k) * ceil(N / 16).
 uint64_t orc_count_mma_spmm(uint64_t W, const uint32_t* rp, uint32_t k, uint64_t N) {

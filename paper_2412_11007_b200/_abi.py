@@ -138,6 +138,9 @@ EXPORTS = {
                                  C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters), C.c_void_p]),
     "tcs_spmm_csr_host": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_void_p, C.c_int64, C.c_void_p,
                                     C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters), C.c_void_p]),
+    "tcs_spmm_baseline16_csr_host": (C.c_int, [C.POINTER(tcs_csr), C.c_void_p, C.c_int64, C.c_int64, C.c_void_p,
+                                               C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters),
+                                               C.c_void_p]),
 }
 
 _lib = None

@@ -241,6 +241,7 @@ void free_plan(Plan* p, cudaStream_t s) {
     dfree(p->items, s);
     dfree(p->split, s);
     dfree(p->live, s);
+    dfree(p->exact_live, s);
     delete p;
 }
 
@@ -360,12 +361,21 @@ tcs_status tcs_mebcrs_prepare(tcs_mebcrs* m, tcs_stream_t stream) {
     return guard([&] {
         check_mebcrs(m, true);
         cudaStream_t s = st(stream);
-        if (m->plan && !(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
+        uint8_t* exact = nullptr;  // exact liveness of these values survives a re-prepare
+        if (m->plan && !(m->flags & TCS_MEBCRS_BORROWED_PLAN)) {
+            Plan* old = static_cast<Plan*>(m->plan);
+            if (old->exact_for(m->values)) std::swap(exact, old->exact_live);
+            free_plan(old, s);
+        }
         m->plan = nullptr;
         m->flags &= ~TCS_MEBCRS_BORROWED_PLAN;
         uint32_t mx = 0;
         uint64_t blocks = 0, groups = 0;
         m->plan = build_plan(m, s, &mx, &blocks, &groups);
+        if (exact) {
+            static_cast<Plan*>(m->plan)->exact_live = exact;
+            static_cast<Plan*>(m->plan)->exact_live_src = m->values;
+        }
         m->max_window_vectors = mx;
         m->num_blocks = blocks;
         m->num_groups16 = groups;
@@ -383,6 +393,7 @@ tcs_status tcs_mebcrs_free(tcs_mebcrs* m, tcs_stream_t stream) {
         // a liveness cache built from these values must not outlive them
         // (the allocator may hand the address to another handle of this plan)
         if (auto* p = static_cast<Plan*>(m->plan); p && p->live_src == m->values) p->live_src = nullptr;
+        if (auto* p = static_cast<Plan*>(m->plan); p && p->exact_live_src == m->values) p->exact_live_src = nullptr;
         if (m->flags & TCS_MEBCRS_OWN_VALUES) dfree(m->values, s);
         if (!(m->flags & TCS_MEBCRS_BORROWED_PLAN)) free_plan(static_cast<Plan*>(m->plan), s);
         std::memset(m, 0, sizeof(*m));

@@ -60,6 +60,11 @@ struct CheckOut {
     // dynamic window queues of the big-window kernels (a hub window of 10^5+
     // entries must not delay the windows behind it on a fixed CTA stride)
     uint32_t next_sort_big, next_bitmap, next_scatter_big;
+    // set by the F16 scatter when a nonzero f32 value rounds to a binary16
+    // zero (0 < |v| <= 2^-25): the reference still samples it in SDDMM
+    // (ref sddmm.hpp:131 tests the f32 value), so the handle gets exact
+    // liveness bytes built from the f32 CSR values
+    uint32_t tiny;
 };
 
 // CTA-wide queue claim: thread 0 takes the next index, every thread gets it.
@@ -470,7 +475,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
                                                       const uint32_t* __restrict__ list, uint32_t n_front,
-                                                      uint32_t n_list, uint32_t* next) {
+                                                      uint32_t n_list, uint32_t* next, uint32_t* tiny) {
     extern __shared__ uint4 tile_raw[];
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
@@ -555,7 +560,11 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                     for (int q = 1; q < VH; ++q) r += (e[u] >= rb[q]) ? 1u : 0u;
                     const uint32_t b = v[u] / k, j = v[u] - b * k;
                     const uint32_t width = min(k, nvw - b * k);
-                    tile[(b * k - t0) * VH + r * width + j] = store_cvt<V>(x[u]);
+                    const V y = store_cvt<V>(x[u]);
+                    tile[(b * k - t0) * VH + r * width + j] = y;
+                    if constexpr (sizeof(V) == 2) {  // nonzero f32 that rounds to a binary16 zero
+                        if ((__float_as_uint(x[u]) & 0x7FFFFFFFu) && !(__half_as_ushort(y) & 0x7FFFu)) atomicOr(tiny, 1u);
+                    }
                 }
             }
             __syncthreads();
@@ -567,11 +576,28 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
     }
 }
 
+// Exact SDDMM liveness bytes (bit r of byte p: row r of stored vector p has
+// a nonzero f32 CSR value, ref sddmm.hpp:131) for an F16 handle whose
+// binary16 values lost a tiny nonzero (CheckOut::tiny).  One thread per CSR
+// row; rare path, so bits are set with word atomics.
+__global__ void exact_live_build(const uint32_t* __restrict__ csr_rp, const float* __restrict__ csr_vals,
+                                 uint64_t rows, const uint32_t* __restrict__ rp, const uint32_t* __restrict__ rank,
+                                 uint8_t* live) {
+    for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < rows; r += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t base = rp[r / 8], bit = 1u << (r % 8);
+        for (uint32_t e = csr_rp[r]; e < csr_rp[r + 1]; ++e) {
+            if (!(__float_as_uint(csr_vals[e]) & 0x7FFFFFFFu)) continue;
+            const uint64_t p = uint64_t(base) + rank[e];
+            atomicOr(reinterpret_cast<uint32_t*>(live + (p & ~uint64_t(3))), bit << (8 * (p & 3)));
+        }
+    }
+}
+
 // Value type V of a window_scatter instantiation (for the launch helper).
 template <typename V>
 V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
                            const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, uint32_t,
-                           uint32_t, uint32_t*));
+                           uint32_t, uint32_t*, uint32_t*));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
                          "column indices must be strictly ascending within a row"};
@@ -624,6 +650,12 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         } cleanup{&m, s};
 
         uint32_t nv = 0;
+        uint8_t* exact_live = nullptr;  // see CheckOut::tiny
+        struct LiveCleanup {
+            uint8_t*& p;
+            cudaStream_t s;
+            ~LiveCleanup() { dfree(p, s); }
+        } live_cleanup{exact_live, s};
         if (W) {
             // K0: row_ptr invariants + longest window
             DBuf chk(sizeof(CheckOut), s), small_list(W * 4, s), big_list(W * 4, s);
@@ -710,7 +742,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
                                                     static_cast<decltype(kern_value_type(kern))*>(m.values), list,
                                                     big ? h.n_huge : h.n_tiny, n,
-                                                    big ? &dchk->next_scatter_big : nullptr);
+                                                    big ? &dchk->next_scatter_big : nullptr, &dchk->tiny);
             };
             if (value_dtype == TCS_DTYPE_F16) {
                 scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
@@ -724,6 +756,19 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                         kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_tiny + h.n_small);
             }
             TCS_LAUNCHED("window_scatter");
+            if (value_dtype == TCS_DTYPE_F16 && VH == 8) {
+                uint32_t tiny = 0;
+                TCS_CUDA(cudaMemcpyAsync(&tiny, &dchk->tiny, 4, cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaStreamSynchronize(s));
+                if (tiny) {
+                    exact_live = static_cast<uint8_t*>(dalloc(uint64_t(nv) + 16, s));
+                    TCS_CUDA(cudaMemsetAsync(exact_live, 0, uint64_t(nv) + 16, s));
+                    const int gl = static_cast<int>(std::min<uint64_t>((rows + 255) / 256, uint64_t(sms) * 8));
+                    exact_live_build<<<gl, 256, 0, s>>>(csr->row_ptr, csr->values, rows, m.row_pointers,
+                                                        rank.as<uint32_t>(), exact_live);
+                    TCS_LAUNCHED("exact_live_build");
+                }
+            }
         } else {
             TCS_CUDA(cudaMemsetAsync(m.row_pointers, 0, 4, s));
             m.column_indices = static_cast<uint32_t*>(dalloc(4, s));
@@ -736,6 +781,12 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             const std::string msg = tcs_last_error();
             tcs_mebcrs_free(out, stream);
             fail(rc, msg);
+        }
+        if (exact_live) {  // the work list owns them from here
+            Plan* plan = static_cast<Plan*>(out->plan);
+            plan->exact_live = exact_live;
+            plan->exact_live_src = out->values;
+            exact_live = nullptr;
         }
     }
 }

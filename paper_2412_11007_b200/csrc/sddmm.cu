@@ -568,6 +568,7 @@ void sddmm_check(const tcs_mebcrs* mask, const void* a, tcs_dtype a_dtype, int64
 // (TCS_CFG_STATIC_MASK: the caller guarantees the values do not change
 // between calls that reuse the cache).
 const uint8_t* mask_liveness(const tcs_mebcrs* mask, Plan* plan, cudaStream_t s) {
+    if (const uint8_t* ex = plan->exact_for(mask->values)) return ex;
     if (plan->live && plan->live_src == mask->values) return plan->live;
     if (!plan->live) plan->live = static_cast<uint8_t*>(dalloc(mask->num_vectors + 16, s));
     build_liveness(mask, plan->live, s);
@@ -578,6 +579,10 @@ const uint8_t* mask_liveness(const tcs_mebcrs* mask, Plan* plan, cudaStream_t s)
 // live[p] for every stored vector p (nv + 16 bytes; the 16 past nv zeroed).
 void build_liveness(const tcs_mebcrs* mask, uint8_t* live, cudaStream_t s) {
     const uint64_t nv = mask->num_vectors;
+    if (const Plan* plan = static_cast<const Plan*>(mask->plan); plan && plan->exact_for(mask->values)) {
+        TCS_CUDA(cudaMemcpyAsync(live, plan->exact_live, nv + 16, cudaMemcpyDeviceToDevice, s));
+        return;
+    }
     TCS_CUDA(cudaMemsetAsync(live + nv, 0, 16, s));
     if (!nv) return;
     const int grid = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((nv + 255) / 256, uint64_t(num_sms()) * 16)));
@@ -643,6 +648,8 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
     if (!plan->n_items) return;
     if (static_mask) args.live = mask_liveness(mask, plan, s);
+    // binary16 values that lost a tiny nonzero: the exact bytes decide (ref :131)
+    else if (const uint8_t* ex = plan->exact_for(mask->values)) args.live = ex;
     if (tf32) {
         if (nsc == 1) launch_sddmm<true, 1>(args, mf32, of32, s);
         else if (nsc == 2) launch_sddmm<true, 2>(args, mf32, of32, s);

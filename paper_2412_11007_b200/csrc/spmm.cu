@@ -1047,6 +1047,20 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         DBuf d_b16;
         if (f16) d_b16 = DBuf(std::max<int64_t>(1, b_rows * n) * 2, s);
         Streams ss;
+        // On any exit (an error in a later chunk included) the side streams'
+        // queued copies and kernels finish before the buffers above are
+        // released in `stream` order and before control returns to the
+        // caller (the drain stream writes into the caller's host C).
+        struct Join {
+            Streams& ss;
+            bool joined = false;
+            ~Join() {
+                if (joined) return;
+                cudaStreamSynchronize(ss.copy);
+                for (auto c : ss.compute) cudaStreamSynchronize(c);
+                cudaStreamSynchronize(ss.drain);
+            }
+        } join{ss};
         Event forked;
         forked.record(s);
         forked.wait_on(ss.copy);
@@ -1133,6 +1147,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         joined_copy.wait_on(s);
         for (auto& e : joined_compute) e.wait_on(s);
         joined_drain.wait_on(s);
+        join.joined = true;
         TCS_CUDA(cudaStreamSynchronize(s));
     });
 }

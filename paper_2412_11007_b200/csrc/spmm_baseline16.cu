@@ -438,3 +438,39 @@ extern "C" tcs_status tcs_spmm_baseline16(const tcs_mebcrs* A, const void* b, tc
         }
     });
 }
+
+extern "C" tcs_status tcs_spmm_baseline16_csr_host(const tcs_csr* host_csr, const float* b, int64_t b_rows,
+                                                   int64_t n, float* c, const tcs_kernel_config* cfg,
+                                                   tcs_counters* counters, tcs_stream_t stream) {
+    return guard([&] {
+        if (!host_csr || !cfg || !host_csr->row_ptr) fail(TCS_ERR_ARGUMENT, "null argument");
+        // ref spmm.hpp:190-191, in its order
+        if (cfg->vector_height != 16) fail(TCS_ERR_ARGUMENT, "baseline path requires vector height 16");
+        if (static_cast<int64_t>(host_csr->cols) != b_rows) fail(TCS_ERR_SHAPE, "sparse cols must equal dense rows");
+        if (n < 0) fail(TCS_ERR_SHAPE, "negative dimension");
+        cudaStream_t s = st(stream);
+        const uint64_t rows = host_csr->rows, nnz = host_csr->nnz;
+        DBuf rp((rows + 1) * 4, s), ci(std::max<uint64_t>(1, nnz) * 4, s), v(std::max<uint64_t>(1, nnz) * 4, s);
+        TCS_CUDA(cudaMemcpyAsync(rp.p, host_csr->row_ptr, (rows + 1) * 4, cudaMemcpyHostToDevice, s));
+        if (nnz) {
+            TCS_CUDA(cudaMemcpyAsync(ci.p, host_csr->col_idx, nnz * 4, cudaMemcpyHostToDevice, s));
+            TCS_CUDA(cudaMemcpyAsync(v.p, host_csr->values, nnz * 4, cudaMemcpyHostToDevice, s));
+        }
+        const tcs_csr d{rows, host_csr->cols, nnz, rp.as<uint32_t>(), ci.as<uint32_t>(), v.as<float>()};
+        tcs_mebcrs m{};
+        tcs_status rc = tcs_mebcrs_encode_v(&d, cfg->precision, TCS_DTYPE_F32, 16, &m, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        struct Free {
+            tcs_mebcrs* m;
+            tcs_stream_t s;
+            ~Free() { tcs_mebcrs_free(m, s); }
+        } fr{&m, stream};
+        DBuf db(std::max<int64_t>(1, b_rows * n) * 4, s), dc(std::max<uint64_t>(1, rows * n) * 4, s);
+        if (b_rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(db.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, s));
+        rc = tcs_spmm_baseline16(&m, db.p, TCS_DTYPE_F32, std::max<int64_t>(1, n), b_rows, n, dc.as<float>(),
+                                 std::max<int64_t>(1, n), cfg, counters, stream);
+        if (rc != TCS_OK) fail(rc, tcs_last_error());
+        if (rows > 0 && n > 0) TCS_CUDA(cudaMemcpyAsync(c, dc.p, rows * n * 4, cudaMemcpyDeviceToHost, s));
+        TCS_CUDA(cudaStreamSynchronize(s));
+    });
+}

@@ -119,6 +119,14 @@ struct Plan {
     // other values.
     uint8_t* live = nullptr;        // device, num_vectors + 16
     const void* live_src = nullptr;
+    // Exact liveness bytes of an F16 encode whose binary16 values lost a tiny
+    // nonzero f32 value (encode.cu, CheckOut::tiny); valid for the values at
+    // `exact_live_src` only.  Every liveness consumer prefers them.
+    uint8_t* exact_live = nullptr;  // device, num_vectors + 16
+    const void* exact_live_src = nullptr;
+    const uint8_t* exact_for(const void* values) const {
+        return exact_live && exact_live_src == values ? exact_live : nullptr;
+    }
 };
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16);

@@ -101,6 +101,40 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def _dev(t: torch.Tensor, name: str) -> torch.Tensor:
+    """Device operands go to the kernels as raw pointers on the current
+    device's stream: anything else would fault (host memory) or run against
+    another device's memory pool."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ArgumentError(f"{name} must be a CUDA tensor")
+    if t.device.index != torch.cuda.current_device():
+        raise ArgumentError(f"{name} is on {t.device}, the current device is cuda:{torch.cuda.current_device()}")
+    return t
+
+
+_TORCH_OF_TAG = {_abi.TCS_DTYPE_F16: torch.float16, _abi.TCS_DTYPE_F32: torch.float32}
+
+
+def _out_rows(out: torch.Tensor, rows: int, n: int, name: str = "out") -> torch.Tensor:
+    """Caller-supplied f32 output [>= rows, >= n] with unit column stride."""
+    _dev(out, name)
+    if out.dtype != torch.float32 or out.dim() != 2 or out.stride(1) != 1 or out.shape[0] < rows \
+            or out.shape[1] < n:
+        raise ArgumentError(f"{name} must be a float32 [>= {rows}, >= {n}] tensor with unit column stride")
+    return out
+
+
+def _out_values(v: torch.Tensor, nv: int, tag: int, name: str = "out_values") -> torch.Tensor:
+    """Caller-supplied ME-BCRS value array: 8 * nv contiguous elements of the
+    output dtype (the kernels write 8 * nv * width bytes)."""
+    _dev(v, name)
+    if v.dtype != _TORCH_OF_TAG[int(tag)]:
+        raise ArgumentError(f"{name} must be {_TORCH_OF_TAG[int(tag)]} for this output dtype, not {v.dtype}")
+    if v.numel() < 8 * nv or not v.is_contiguous():
+        raise ArgumentError(f"{name} too small or not contiguous (needs {8 * nv} elements)")
+    return v
+
+
 def _u32(t: torch.Tensor) -> torch.Tensor:
     if t.dtype == torch.uint32:
         return t.contiguous()
@@ -121,6 +155,8 @@ class CsrMatrix:
         return int(self.col_idx.numel())
 
     def _c(self):
+        for name in ("row_ptr", "col_idx", "values"):
+            _dev(getattr(self, name), name)
         self.row_ptr, self.col_idx = _u32(self.row_ptr), _u32(self.col_idx)
         self.values = self.values.to(torch.float32).contiguous()
         return _abi.tcs_csr(self.rows, self.cols, self.nnz, self.row_ptr.data_ptr(), self.col_idx.data_ptr(),
@@ -248,11 +284,13 @@ def spmm(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = KernelCo
     reference's spmm(SrBcrsMatrix) overload (spmm.hpp:181)."""
     if isinstance(sparse, SrBcrsMatrix):
         return spmm_srbcrs(sparse, dense, cfg, out)
+    _dev(dense, "dense")
     if dense.dim() != 2 or dense.stride(1) != 1:
         dense = dense.contiguous()
     m, n = sparse.rows, dense.shape[1]
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    _out_rows(out, m, n)
     cnt = _abi.tcs_counters()
     _check(_abi.load().tcs_spmm(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
                                 dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()), C.byref(cnt),
@@ -267,11 +305,13 @@ def spmm_baseline16(sparse: MeBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig
     defaults to the matrix precision with vector_height 16."""
     if cfg is None:
         cfg = KernelConfig(sparse.precision, vector_height=16)
+    _dev(dense, "dense")
     if dense.dim() != 2 or dense.stride(1) != 1:
         dense = dense.contiguous()
     m, n = sparse.rows, dense.shape[1]
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    _out_rows(out, m, n)
     cnt = _abi.tcs_counters()
     _check(_abi.load().tcs_spmm_baseline16(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
                                            dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
@@ -353,11 +393,13 @@ def spmm_srbcrs(sparse: SrBcrsMatrix, dense: torch.Tensor, cfg: KernelConfig = K
                 out: torch.Tensor | None = None) -> SpmmResult:
     """ref spmm(const SrBcrsMatrix&, ...) (spmm.hpp:181-185): same kernel and
     result as spmm() on the compact format."""
+    _dev(dense, "dense")
     if dense.dim() != 2 or dense.stride(1) != 1:
         dense = dense.contiguous()
     m, n = sparse.rows, dense.shape[1]
     if out is None:
         out = torch.empty((m, n), dtype=torch.float32, device=dense.device)
+    _out_rows(out, m, n)
     cnt = _abi.tcs_counters()
     _check(_abi.load().tcs_spmm_srbcrs(C.byref(sparse._h), dense.data_ptr(), _dtype_tag(dense), dense.stride(0),
                                        dense.shape[0], n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
@@ -384,15 +426,12 @@ def sddmm(ops: SddmmOperands, cfg: KernelConfig = KernelConfig(), out_dtype: int
     """ref sddmm.hpp:84.  The output shares the mask's structure (kept alive).
     ``out_values`` (optional): caller-owned device tensor of 8 * nv elements
     of out_dtype receiving the values (else the library allocates them)."""
-    a = ops.a if ops.a.stride(-1) == 1 else ops.a.contiguous()
-    b = ops.b_t if ops.b_t.stride(-1) == 1 else ops.b_t.contiguous()
+    a = _dev(ops.a, "a") if ops.a.stride(-1) == 1 else _dev(ops.a, "a").contiguous()
+    b = _dev(ops.b_t, "b_t") if ops.b_t.stride(-1) == 1 else _dev(ops.b_t, "b_t").contiguous()
     h = _abi.tcs_mebcrs()
     keep = [ops.mask]
     if out_values is not None:
-        need = 8 * ops.mask.num_vectors
-        if out_values.numel() < need or not out_values.is_contiguous():
-            raise ArgumentError("out_values too small or not contiguous")
-        h.values = out_values.data_ptr()
+        h.values = _out_values(out_values, ops.mask.num_vectors, out_dtype).data_ptr()
         keep.append(out_values)
     cnt = _abi.tcs_counters()
     _check(_abi.load().tcs_sddmm(C.byref(ops.mask._h), a.data_ptr(), _dtype_tag(a), a.stride(0), a.shape[0],
@@ -408,7 +447,7 @@ def row_softmax(scores: MeBcrsMatrix, mask: MeBcrsMatrix, scale: float = 1.0,
     h = _abi.tcs_mebcrs()
     keep = [scores, mask]
     if out_values is not None:
-        h.values = out_values.data_ptr()
+        h.values = _out_values(out_values, scores.num_vectors, out_dtype).data_ptr()
         keep.append(out_values)
     _check(_abi.load().tcs_mebcrs_row_softmax(C.byref(scores._h), C.byref(mask._h), float(scale), C.byref(h),
                                               int(out_dtype), _stream()))
@@ -422,14 +461,12 @@ def sddmm_row_softmax(ops: SddmmOperands, scale: float = 1.0, cfg: KernelConfig 
     (tcs_sddmm_row_softmax): the scores (stored as score_dtype) carry the
     per-row softmax partials out of the SDDMM kernel and are normalised in
     one pass."""
-    a = ops.a if ops.a.stride(-1) == 1 else ops.a.contiguous()
-    b = ops.b_t if ops.b_t.stride(-1) == 1 else ops.b_t.contiguous()
+    a = _dev(ops.a, "a") if ops.a.stride(-1) == 1 else _dev(ops.a, "a").contiguous()
+    b = _dev(ops.b_t, "b_t") if ops.b_t.stride(-1) == 1 else _dev(ops.b_t, "b_t").contiguous()
     h = _abi.tcs_mebcrs()
     keep = [ops.mask]
     if out_values is not None:
-        if out_values.numel() < 8 * ops.mask.num_vectors or not out_values.is_contiguous():
-            raise ArgumentError("out_values too small or not contiguous")
-        h.values = out_values.data_ptr()
+        h.values = _out_values(out_values, ops.mask.num_vectors, out_dtype).data_ptr()
         keep.append(out_values)
     _check(_abi.load().tcs_sddmm_row_softmax(C.byref(ops.mask._h), a.data_ptr(), _dtype_tag(a), a.stride(0),
                                              a.shape[0], a.shape[1], b.data_ptr(), _dtype_tag(b), b.stride(0),
@@ -447,11 +484,16 @@ def agnn_aggregate(mask: MeBcrsMatrix, hn: torch.Tensor, hc: torch.Tensor, scale
     [row0, row0 + mask.rows) (a row shard, or the whole graph)."""
     if cfg is None:
         cfg = KernelConfig(mask.precision)
-    hn = hn if hn.stride(-1) == 1 else hn.contiguous()
-    hc = hc if hc.stride(-1) == 1 else hc.contiguous()
+    hn = _dev(hn, "hn") if hn.stride(-1) == 1 else _dev(hn, "hn").contiguous()
+    hc = _dev(hc, "hc") if hc.stride(-1) == 1 else _dev(hc, "hc").contiguous()
     rows, n = mask.rows, hc.shape[1]
+    # the kernels read feature rows of every node (mask.cols of them) and
+    # the score rows [row0, row0 + rows)
+    if hn.dim() != 2 or hc.dim() != 2 or hn.shape[0] < max(mask.cols, row0 + rows) or hc.shape[0] < mask.cols:
+        raise ShapeError(f"hn / hc must hold every node's row ({mask.cols}; row0 + rows = {row0 + rows})")
     if out is None:
         out = torch.empty((rows, n), dtype=torch.float32, device=hc.device)
+    _out_rows(out, rows, n)
     _check(_abi.load().tcs_agnn_aggregate(C.byref(mask._h), hn.data_ptr(), _dtype_tag(hn), hn.stride(0), int(row0),
                                           rows, hn.shape[1], float(scale), hc.data_ptr(), _dtype_tag(hc),
                                           hc.stride(0), n, out.data_ptr(), out.stride(0), C.byref(cfg._c()),
@@ -469,10 +511,13 @@ def agnn_attend(mask: MeBcrsMatrix, h: torch.Tensor, scale: float = 1.0, cfg: Ke
         cfg = KernelConfig(mask.precision)
     if h.dtype != torch.float16 or h.dim() != 2:
         raise ArgumentError("h must be a 2-D float16 tensor")
-    h = h if h.stride(-1) == 1 else h.contiguous()
+    h = _dev(h, "h") if h.stride(-1) == 1 else _dev(h, "h").contiguous()
     rows, f = mask.rows, h.shape[1]
+    if h.shape[0] < max(mask.cols, row0 + rows):  # every node's row (agnn.cu reads mask.cols rows)
+        raise ShapeError(f"h must hold every node's row ({mask.cols}; row0 + rows = {row0 + rows})")
     if out is None:
         out = torch.empty((rows, f), dtype=torch.float32, device=h.device)
+    _out_rows(out, rows, f)
     _check(_abi.load().tcs_agnn_attend(C.byref(mask._h), h.data_ptr(), _abi.TCS_DTYPE_F16, h.stride(0), int(row0),
                                        f, float(scale), float(eps), out.data_ptr(), out.stride(0),
                                        C.byref(cfg._c()), _stream()))
@@ -485,6 +530,7 @@ def rows_normalize(h: torch.Tensor, dtype: torch.dtype = torch.float16, eps: flo
     (tcs_rows_normalize; the AGNN layer's SDDMM / SpMM operands)."""
     if h.dtype != torch.float32 or h.dim() != 2 or h.stride(-1) != 1:
         raise ArgumentError("h must be a 2-D f32 tensor with unit column stride")
+    _dev(h, "h")
     rows, f = h.shape
     hn = torch.empty(rows, f, dtype=dtype, device=h.device) if normalized else None
     hc = torch.empty(rows, f, dtype=dtype, device=h.device) if copy else None
@@ -497,7 +543,7 @@ def rows_normalize(h: torch.Tensor, dtype: torch.dtype = torch.float16, eps: flo
 
 def round_values(x: torch.Tensor, precision: Precision) -> torch.Tensor:
     """Device operand rounding used by the kernels (diagnostics)."""
-    x = x.to(torch.float32).contiguous()
+    x = _dev(x, "x").to(torch.float32).contiguous()
     out = torch.empty_like(x)
     _check(_abi.load().tcs_round_values(int(precision), x.data_ptr(), out.data_ptr(), x.numel(), _stream()))
     return out

@@ -75,6 +75,14 @@ def kat_cases():
     mz = O.Csr(8, 8, [0, 1, 1, 2, 2, 3, 3, 3, 3], [1, 3, 5], np.array([1.0, 0.0, -0.0], np.float32))
     cases.append(Case("kat_zero_mask", mz, B=np.ones((8, 16), np.float32),
                       A=np.ones((8, 4), np.float32), Bt=np.ones((8, 4), np.float32)))
+    # tiny mask values: nonzero in f32 (so sampled, inc/sddmm.hpp:131) but
+    # zero once rounded to binary16 (1e-10, -3e-9, 2^-25 ties to 0); 2^-24
+    # is the smallest binary16 subnormal.  Every precision and storage must
+    # sample all five.
+    mt = O.Csr.from_coords(16, 12, [(0, 1, 1e-10), (1, 2, 2.0 ** -24), (2, 3, -3e-9), (4, 5, 1.0),
+                                    (6, 6, 2.0 ** -25), (9, 6, -1e-12), (9, 7, 0.0)])
+    cases.append(Case("kat_tiny_mask", mt, B=GEN.generate_random_dense(12, 16, 31),
+                      A=GEN.generate_random_dense(16, 4, 32), Bt=GEN.generate_random_dense(12, 4, 33)))
     # residue-heavy windows: counts 1, 9, 17, 3 (cf. tests/test_kernels.cpp:24-35;
     # our own deterministic values since that helper draws two mt19937 values
     # inside one expression)

@@ -416,3 +416,31 @@ def test_shapes_strides_and_alignment(p):
                           cfg).output.to_host()[2]
             assert np.array_equal(got.view(np.uint32), O.sddmm(ref, A, Bt).view(np.uint32)), f
         me.free()
+
+
+def test_tiny_mask_values_sampled_with_binary16_storage(golden):
+    """Mask values that are nonzero in f32 but round to a binary16 zero
+    (1e-10, -3e-9, 2^-25, -1e-12) are sampled by the reference SDDMM, which
+    tests the f32 value (ref sddmm.hpp:131).  With binary16 value storage the
+    encoder keeps exact liveness bytes for them: the SDDMM (default and
+    static-mask), the fused SDDMM -> row softmax and a re-prepared handle
+    all sample them; an SDDMM output used as the next mask does not inherit
+    them (its own values decide)."""
+    case = next(c for c in cases.kat_cases() if c.name == "kat_tiny_mask")
+    rec = golden["cases"][case.name]
+    me = T.encode_mebcrs(dev_csr(case.csr), T.Precision.fp16, F16)
+    ops = T.SddmmOperands(me, torch.from_numpy(case.A).cuda(), torch.from_numpy(case.Bt).cuda())
+    for static in (False, True, False):
+        out = T.sddmm(ops, T.KernelConfig(T.Precision.fp16, static_mask=static)).output.to_host()[2]
+        assert cases.sha(out) == rec["sddmm_fp16"]["sha"], static
+    # 6 live slots (the explicit 0.0 is stored but not sampled)
+    assert int(np.count_nonzero(out)) == 6
+    sm = T.sddmm_row_softmax(ops, 1.0, T.KernelConfig(T.Precision.fp16)).to_host()[2]
+    assert int(np.count_nonzero(sm)) == 6 and np.all(np.isfinite(sm))
+    import ctypes
+    from paper_2412_11007_b200 import _abi
+    assert _abi.load().tcs_mebcrs_prepare(ctypes.byref(me._h),
+                                          ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    out = T.sddmm(ops, T.KernelConfig(T.Precision.fp16)).output.to_host()[2]
+    assert cases.sha(out) == rec["sddmm_fp16"]["sha"]
+    me.free()

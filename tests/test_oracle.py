@@ -145,3 +145,35 @@ def test_live_differential_against_reference():
             a, b = O.encode_mebcrs(m, p), O.Ref.encode_mebcrs(m, p)
             assert np.array_equal(a.values.view(np.uint32), b.values.view(np.uint32))
             assert np.array_equal(O.spmm(a, B).view(np.uint32), O.Ref.spmm(b, B)[0].view(np.uint32))
+
+
+def _csr_form_matches(case, rec):
+    m = case.csr
+    for p in case.precisions:
+        tag = "fp16" if p == 0 else "tf32"
+        if case.B is not None:
+            assert cases.sha(O.spmm_csr_rows(m, case.B, p)) == rec[f"spmm_{tag}"]["sha"], (case.name, p)
+            rows = np.arange(m.rows)[::3]
+            assert np.array_equal(O.spmm_csr_rows(m, case.B, p, rows).view(np.uint32),
+                                  O.spmm_csr_rows(m, case.B, p)[rows].view(np.uint32))
+        if case.A is not None:
+            me = O.encode_mebcrs(m, p)
+            dot, pos = O.sddmm_csr_rows(m, p, me.row_pointers, me.column_indices, case.A, case.Bt)
+            assert not np.any(pos == np.iinfo(np.uint64).max)
+            out = np.zeros(8 * me.nv, np.float32)
+            out[pos.astype(np.int64)] = dot
+            assert cases.sha(out) == rec[f"sddmm_{tag}"]["sha"], (case.name, p)
+
+
+def test_csr_form_oracle_matches_golden(golden):
+    """The CSR-form restatements used for the full-size (C3-C5) parity gates
+    (orc_spmm_csr_rows / orc_sddmm_csr_rows) give the reference's bits on
+    every golden case: KATs, the acceptance replays and C1 in both value
+    modes."""
+    todo = list(cases.kat_cases())
+    p2, p6 = cases.acceptance2_params(), cases.acceptance6_params()
+    todo += [cases.acceptance2_case(i, p2) for i in range(0, 200, 2)]
+    todo += [cases.acceptance6_case(i, p6) for i in range(0, 100, 2)]
+    todo += [cases.c1_case(False), cases.c1_case(True)]
+    for case in todo:
+        _csr_form_matches(case, golden["cases"][case.name])
