@@ -11,7 +11,7 @@ OBJS    := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRCS))
 LIB     := $(PKG)/libtcsparse_b200.so
 CLI     := $(PKG)/tcsparse-b200
 
-all: lib cli oracle
+all: lib cli probe oracle
 
 lib: $(LIB)
 
@@ -36,4 +36,10 @@ clean:
 	rm -rf build $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all lib cli oracle clean
+# Hardware L2 -> SM gather ceiling, run by bench.py (roofline.l2_gather).
+probe: tools/l2_gather_peak
+
+tools/l2_gather_peak: tools/l2_gather_peak.cu
+	$(NVCC) $(ARCH) -O3 -o $@ $<
+
+.PHONY: all lib cli probe oracle clean

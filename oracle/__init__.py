@@ -137,6 +137,15 @@ def ref():
         _ref.ref_sddmm_output_offsets.restype = C.c_uint64
         _ref.ref_sddmm_output_offsets.argtypes = [C.c_uint64, C.c_int]
         _ref.ref_free.argtypes = [C.c_void_p]
+        _ref.ref_dense_new.restype = C.c_void_p
+        _ref.ref_dense_new.argtypes = [C.c_uint64, C.c_uint64, _f32p]
+        _ref.ref_dense_free.argtypes = [C.c_void_p]
+        _ref.ref_time_encode_spmm.restype = C.c_double
+        _ref.ref_time_encode_spmm.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_int, C.c_void_p,
+                                              _f32p]
+        _ref.ref_time_encode_sddmm.restype = C.c_double
+        _ref.ref_time_encode_sddmm.argtypes = [C.c_uint64, C.c_uint64, _u32p, _u32p, _f32p, C.c_int, _f32p,
+                                               C.c_uint64, C.c_void_p, _f32p, C.c_uint64]
     return _ref
 
 

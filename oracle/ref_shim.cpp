@@ -8,6 +8,8 @@
 // the reference's own CPU path in bench.py (--impl reference / cpu_baseline).
 // No reference source is copied into this repository.
 // ============================================================================
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -385,6 +387,58 @@ int64_t ref_read_mebcrs(const char* path, uint64_t* rows, uint64_t* cols, int* p
 
 uint64_t ref_sddmm_output_offsets(uint64_t lane, int kind) {
     return sddmm_output_offsets(lane, kind == 0 ? SubBlockKind::b8x8 : SubBlockKind::b8x4);
+}
+
+// ---- timed reference pipelines for bench.py's CPU baseline -----------------
+// The reference CLI's pipelines (inc/cli.hpp:162-200 spmm, :205-240 sddmm):
+// encode_mebcrs then spmm / sddmm on a CSR row slice, against a dense
+// operand built once (ref_dense_new) so that the shim's own copies stay out
+// of the measurement.  Returns the seconds spent inside the reference calls,
+// or a negative value on error.
+void* ref_dense_new(uint64_t rows, uint64_t cols, const float* data) {
+    auto* d = new DenseMatrix(rows, cols);
+    std::memcpy(d->data.data(), data, sizeof(float) * rows * cols);
+    return d;
+}
+void ref_dense_free(void* d) { delete static_cast<DenseMatrix*>(d); }
+
+double ref_time_encode_spmm(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci,
+                            const float* vals, int precision, const void* dense, float* C) {
+    try {
+        const CsrMatrix m = make_csr(rows, cols, rp, ci, vals);
+        const DenseMatrix& b = *static_cast<const DenseMatrix*>(dense);
+        const Precision p = static_cast<Precision>(precision);
+        const auto t0 = std::chrono::steady_clock::now();
+        const MeBcrsMatrix me = encode_mebcrs(m, p);
+        const SpmmResult res = spmm(me, b, KernelConfig{p, 8, ThreadMapping::coalesced});
+        const auto t1 = std::chrono::steady_clock::now();
+        std::memcpy(C, res.output.data.data(), sizeof(float) * rows * b.cols);
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (const std::exception&) {
+        return -1.0;
+    }
+}
+
+double ref_time_encode_sddmm(uint64_t rows, uint64_t cols, const uint32_t* rp, const uint32_t* ci,
+                             const float* vals, int precision, const float* A, uint64_t F, const void* bt_dense,
+                             float* out_vals, uint64_t out_cap) {
+    try {
+        const CsrMatrix m = make_csr(rows, cols, rp, ci, vals);
+        const Precision p = static_cast<Precision>(precision);
+        SddmmOperands ops;
+        ops.a = DenseMatrix(rows, F);
+        std::memcpy(ops.a.data.data(), A, sizeof(float) * rows * F);
+        ops.b_t = *static_cast<const DenseMatrix*>(bt_dense);
+        const auto t0 = std::chrono::steady_clock::now();
+        ops.mask = encode_mebcrs(m, p);
+        const SddmmResult res = sddmm(ops, KernelConfig{p, 8, ThreadMapping::coalesced});
+        const auto t1 = std::chrono::steady_clock::now();
+        const uint64_t n = std::min<uint64_t>(out_cap, res.output.values.size());
+        std::memcpy(out_vals, res.output.values.data(), sizeof(float) * n);
+        return std::chrono::duration<double>(t1 - t0).count();
+    } catch (const std::exception&) {
+        return -1.0;
+    }
 }
 
 }  // extern "C"
