@@ -22,12 +22,12 @@ $(CLI): $(PKG)/cli/tcsparse_b200.cpp include/tcs/tcs.h $(LIB)
 	g++ -std=c++17 -O2 -Wall -Iinclude -I/usr/local/cuda/include -o $@ $< -L$(PKG) -ltcsparse_b200 \
 	    -L/usr/local/cuda/lib64 -lcudart_static -ldl -lrt -lpthread -Wl,-rpath,'$$ORIGIN'
 
-build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/tcs_internal.cuh include/tcs/tcs.h
+build/%.o: $(PKG)/csrc/%.cu $(PKG)/csrc/tcs_internal.cuh $(wildcard include/tcs/*.h)
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@
 
 $(LIB): $(OBJS)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl
 
 oracle: lib
 	$(MAKE) -s -C oracle

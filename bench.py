@@ -38,8 +38,10 @@ sys.path.insert(0, ROOT)
 
 # mma.sync (HMMA) peak measured on B200 by tools/mma_peak.cu, TFLOP/s.
 MMA_SYNC_PEAK_TFLOPS = {"fp16": 554.6, "tf32": 277.7}
-# Measured ceiling of the SpMM gather pattern on B200 (FP16, 256-byte B rows).
-GATHER_CEILING_GBS = 11757.2
+# Hardware L2 -> SM gather peak (random 256-byte rows, LDG.128 only), as last
+# measured by tools/l2_gather_peak on a B200 (profiles/r2_l2_gather_peak.json);
+# bench.py re-measures it in the run and uses this only when the probe is missing.
+L2_GATHER_PEAK_GBS = 18953.9
 METRIC = "SpMM/SDDMM effective GFLOP/s (2·nnz·N) and % HBM roofline at 1/2/4/8 B200"
 
 
@@ -176,7 +178,7 @@ def small_configs(device):
     """BASELINE configs[0]/[1] (4096^2, 16 nnz/row): launch-latency-bound, so
     timed as CUDA-graph replays of 200 back-to-back calls (us per call)."""
     import paper_2412_11007_b200.tcsparse as T
-    from paper_2412_11007_b200 import graphs as G
+    from paper_2412_11007_b200 import _abi, graphs as G
 
     rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real", device=device)
     nnz = ci.numel()
@@ -211,20 +213,30 @@ def small_configs(device):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) * 1e3 / reps, graph is not None
 
+    peak, _ = peaks()
     for pname, prec, dt in (("fp16", T.Precision.fp16, torch.float16), ("tf32", T.Precision.tf32, torch.float32)):
         me = T.encode_mebcrs(csr, prec)
+        W, nv = me.num_windows, me.num_vectors
+        vw = 2 if dt == torch.float16 else 4
+        vwA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
         B = G.dense(cols, 128, 2, dtype=dt, device=device)
         C = torch.empty(rows, 128, device=device)
         us, g = timed(lambda: T.spmm(me, B, T.KernelConfig(prec), out=C))
+        balg = bytes_alg_spmm(W, nv, rows, 128, vwA, vw)
         out[f"c1_spmm_{pname}_n128_us"] = round(us, 2)
         out[f"c1_spmm_{pname}_gflops"] = round(2.0 * nnz * 128 / (us * 1e-6) / 1e9, 1)
+        out[f"c1_spmm_{pname}_roofline"] = {"bytes_alg": balg, "frac": round(balg / (us * 1e-6) / 1e9 / peak, 4),
+                                            "us_at_peak": round(balg / (peak * 1e9) * 1e6, 2)}
         A = G.dense(rows, 32, 3, dtype=dt, device=device)
         Bt = G.dense(cols, 32, 4, dtype=dt, device=device)
         ov = torch.empty(8 * me.num_vectors, device=device)
         ops = T.SddmmOperands(me, A, Bt)
         us2, g2 = timed(lambda: T.sddmm(ops, T.KernelConfig(prec), out_values=ov))
+        sbalg = bytes_alg_sddmm(W, nv, rows, 32, vwA, vw)
         out[f"c2_sddmm_{pname}_k32_us"] = round(us2, 2)
         out[f"c2_sddmm_{pname}_gflops"] = round(2.0 * nnz * 32 / (us2 * 1e-6) / 1e9, 1)
+        out[f"c2_sddmm_{pname}_roofline"] = {"bytes_alg": sbalg, "frac": round(sbalg / (us2 * 1e-6) / 1e9 / peak, 4),
+                                             "us_at_peak": round(sbalg / (peak * 1e9) * 1e6, 2)}
         out["graph_captured"] = bool(g and g2)
         me.free()
     t = []
@@ -246,6 +258,7 @@ def layer_configs(device):
     and the AGNN layer on R-MAT scale 23 (F = 32).  CUDA events, L2 flushed
     before every timed call, median of 5."""
     import paper_2412_11007_b200.layers as L
+    import paper_2412_11007_b200.tcsparse as T
     from paper_2412_11007_b200 import graphs as G
 
     flush = torch.empty(64 << 20, dtype=torch.int32, device=device)
@@ -265,28 +278,115 @@ def layer_configs(device):
         return round(sorted(ts)[len(ts) // 2], 3)
 
     out = {}
+    peak, _ = peaks()
+
+    def roof(bytes_alg, bytes_min, ms, key):
+        d = {"bytes_alg": bytes_alg, "frac": round(bytes_alg / (ms / 1e3) / 1e9 / peak, 4)}
+        if bytes_min is not None:
+            d["bytes_min"] = bytes_min
+            d["frac_bytes_min"] = round(bytes_min / (ms / 1e3) / 1e9 / peak, 4)
+        dram = dram_traffic(key)
+        if dram:
+            d["dram"] = dict(dram, frac_dram=round(dram["bytes_per_launch"] / (ms / 1e3) / 1e9 / peak, 4))
+        return d
+
     rows, _, rp, ci, _ = G.power_law_csr(G.C4_PRODUCTS, values="real", device=device)
     W = torch.randn(128, 128, device=device).half() / 128 ** 0.5
     H = torch.randn(rows, 128, device=device).half()
     gcn = L.GCNLayer(rows, rp, ci, W)
+    adj = gcn.adj
+    HW = (H @ W).contiguous()
+    Cf = torch.empty(rows, 128, device=device)
+    spmm_ms = timed(lambda: T.spmm(adj, HW, gcn.cfg, out=Cf))
+    nv, Wn = adj.num_vectors, adj.num_windows
     out["c4_gcn"] = {"nodes": rows, "nnz": int(ci.numel()), "adjacency": "D^-1/2 (A + I) D^-1/2", "F": 128,
-                     "layer_ms": timed(lambda: gcn(H)), "precision": "fp16", "path": "cuBLAS GEMM + tcs_spmm"}
-    del gcn, H, rp, ci
+                     "degree_cap": f"Chung-Lu hub weight cap {G.C4_PRODUCTS.cap:g}x mean weight (SURVEY 8(d))",
+                     "layer_ms": timed(lambda: gcn(H)), "precision": "fp16", "path": "cuBLAS GEMM + tcs_spmm",
+                     "spmm_ms": spmm_ms,
+                     "spmm_roofline": roof(bytes_alg_spmm(Wn, nv, rows, 128, 2, 2),
+                                           bytes_alg_spmm(Wn, nv, rows, 128, 2, 2) - nv * 128 * 2 + rows * 128 * 2,
+                                           spmm_ms, "c4_fp16_n128_g1")}
+    del gcn, H, HW, Cf, adj, rp, ci
     torch.cuda.empty_cache()
     rows, _, rp, ci, _ = G.rmat_csr(G.C5_RMAT, values="real", device=device)
     H = torch.randn(rows, 32, device=device)
     agnn = L.AGNNLayer(rows, rp, ci, beta=1.0)
+    mask = agnn.mask
+    nv, Wn = mask.num_vectors, mask.num_windows
+    Hh = H.half().contiguous()
+    Cf = torch.empty(rows, 32, device=device)
+    sp_ms = timed(lambda: T.spmm(mask, Hh, agnn.cfg, out=Cf))
+    ov = torch.empty(8 * nv, device=device)
+    ops = T.SddmmOperands(mask, Hh, Hh)
+    sd_ms = timed(lambda: T.sddmm(ops, agnn.mask_cfg, out_values=ov))
     out["c5_agnn"] = {"nodes": rows, "nnz": int(ci.numel()), "F": 32, "layer_ms": timed(lambda: agnn(H)),
-                      "precision": "fp16", "path": "rows_normalize (f16 copy) + tcs_agnn_attend (one pass, static mask)"}
-    del agnn, H, rp, ci
+                      "precision": "fp16", "path": "rows_normalize (f16 copy) + tcs_agnn_attend (one pass, static mask)",
+                      "spmm_n32_ms": sp_ms,
+                      "spmm_n32_roofline": roof(bytes_alg_spmm(Wn, nv, rows, 32, 2, 2),
+                                                bytes_alg_spmm(Wn, nv, rows, 32, 2, 2) - nv * 32 * 2 + rows * 32 * 2,
+                                                sp_ms, "c5_fp16_n32_g1"),
+                      "sddmm_f32_static_mask_ms": sd_ms,
+                      "sddmm_f32_roofline": roof(bytes_alg_sddmm(Wn, nv, rows, 32, 2, 2, pattern_bytes=nv), None,
+                                                 sd_ms, "c5_sddmm_fp16_f32_g1")}
+    del agnn, H, Hh, Cf, ov, ops, mask, rp, ci
     torch.cuda.empty_cache()
     return out
+
+
+def dram_traffic(key):
+    """ncu-measured DRAM bytes per launch of the dominant kernel for this
+    config (profiles/traffic.json, written by tools/traffic_from_ncu.py from
+    a `ncu --set full` capture).  `current` says whether the kernel sources
+    the capture was taken on are the ones in this tree."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+    except Exception:
+        return None
+    e = tj.get(key)
+    if not isinstance(e, dict):
+        return None
+    out = {k: e[k] for k in ("bytes_per_launch", "l2_hit_pct", "source") if k in e}
+    out["current"] = e.get("csrc_sha") == csrc_sha()
+    return out
+
+
+def csrc_sha():
+    import hashlib
+
+    h = hashlib.sha256()
+    d = os.path.join(ROOT, "paper_2412_11007_b200", "csrc")
+    for name in sorted(os.listdir(d)):
+        with open(os.path.join(d, name), "rb") as f:
+            h.update(name.encode() + f.read())
+    return h.hexdigest()[:16]
+
+
+def l2_gather_peak():
+    """Hardware L2 -> SM gather peak measured now by tools/l2_gather_peak
+    (random 256-B rows of a 60 MB table, LDG.128 only, best over memory-level
+    parallelism and occupancy)."""
+    exe = os.path.join(ROOT, "tools", "l2_gather_peak")
+    try:
+        r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+        return {"peak_gbs": float(d["l2_gather_peak_gbs"]), "source": "measured in this run (tools/l2_gather_peak)"}
+    except Exception:
+        return {"peak_gbs": L2_GATHER_PEAK_GBS, "source": "profiles/r2_l2_gather_peak.json (probe unavailable)"}
 
 
 def bytes_alg_spmm(W, nv, rows, N, vwA, vwB):
     """row pointers + column indices + sparse values (no padding)
     + one N-wide dense row per stored vector + the fp32 C write."""
     return 4 * (W + 1) + 4 * nv + 8 * nv * vwA + nv * N * vwB + 4 * rows * N
+
+
+def bytes_alg_sddmm(W, nv, rows, F, vwA, vwB, pattern_bytes=None, vo=4):
+    """row pointers + column indices + the mask pattern (its
+    stored values, or 1 liveness byte per vector) + the A rows once + one
+    F-wide Bt row per stored vector + the 8 output values per vector."""
+    P = 8 * nv * vwA if pattern_bytes is None else pattern_bytes
+    return 4 * (W + 1) + 4 * nv + P + rows * F * vwB + nv * F * vwB + 8 * nv * vo
 
 
 # --------------------------------------------------------------- workloads
@@ -466,14 +566,10 @@ def run_ours(args, rank, world, device):
     if rank != 0:
         return None
     value = 2.0 * nnz_total * N / (step_ms_max / 1e3) / 1e9
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tj = json.load(f)
-        key = f"{args.workload}_{args.precision}_n{N}_g{world}"
-        traffic = tj.get(key)
-    except Exception:
-        pass
+    dram = dram_traffic(f"{args.workload}_{args.precision}_n{N}_g{world}")
+    gather_bytes = nv * N * vwB  # the B-row gathers alone: what the L2 probe measures
+    l2 = l2_gather_peak() if rank == 0 and not args.quick else {"peak_gbs": L2_GATHER_PEAK_GBS,
+                                                                 "source": "profiles/r2_l2_gather_peak.json"}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(step_ms_max, 4), "higher_is_better": True,
@@ -481,20 +577,26 @@ def run_ours(args, rank, world, device):
         "config": {"workload": desc + f", {args.precision.upper()} N={N}", "nodes": rows, "nnz": nnz_total,
                    "nv_8x1": sum(g["nv"] for g in gathered), "N": N, "precision": args.precision,
                    "values": "uniform [-1,1) (seeded)", "l2": "flushed before every timed step (256 MB write)",
-                   "parallelism": f"row-window shards x{world} (nnz-balanced), B broadcast over NCCL"},
+                   "parallelism": f"row-window shards x{world} (nnz-balanced), B broadcast over NCCL",
+                   "backend": os.environ.get("TCS_BENCH_BACKEND", "none")},
+        # Contract fields: achieved = ALGORITHMIC bytes / kernel
+        # time, against the measured HBM copy peak.  frac > 1 because B (60 MB
+        # in f16) is L2-resident: the B-row gathers are served by L2, not HBM.
+        # The resource that binds is the L2 -> SM gather path (l2_gather);
+        # measured DRAM traffic (dram) is close to bytes_min.
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
+                     "frac": round(achieved / peak, 4),
+                     "traffic": dram["bytes_per_launch"] if dram else None, "peak_source": peak_src,
                      "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
                      "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>",
-                     # bytes_alg/t above the HBM peak = B-row gathers served by L2.
-                     # The binding resource is the L1 data pipe: the same gather
-                     # shape (LDG.128 + SHFL + HMMA + values one step ahead, no
-                     # sparse structure) peaks at this rate in tools/gather_bench2.cu.
-                     "gather_ceiling": {"achieved_over_ceiling": round(achieved / GATHER_CEILING_GBS, 4),
-                                        "ceiling_gbs": GATHER_CEILING_GBS,
-                                        "source": "profiles/r1s3_gather_bench2.txt (LDG+SHFL+PRMT+HMMA+values ahead)"}
-                     if prec == 0 else None,
+                     "binding_resource": "l2_gather" if prec == 0 else "dram latency (31% of gather sectors miss L2)",
+                     "dram": None if not dram else dict(dram, achieved_gbs=round(dram["bytes_per_launch"] / (step_ms / 1e3) / 1e9, 1),
+                                                        frac_dram=round(dram["bytes_per_launch"] / (step_ms / 1e3) / 1e9 / peak, 4)),
+                     "l2_gather": {"gather_bytes_per_launch": gather_bytes,
+                                   "achieved_gbs": round(gather_bytes / (step_ms / 1e3) / 1e9, 1),
+                                   "peak_gbs": l2["peak_gbs"], "peak_source": l2["source"],
+                                   "frac": round(gather_bytes / (step_ms / 1e3) / 1e9 / l2["peak_gbs"], 4)},
                      # the legacy tensor path this kernel uses (HMMA), against its
                      # measured peak; the tcgen05 bf16 peak for scale
                      "tensor_pipe": {"issued_tflop_per_launch": round(tensor_flops / 1e12, 4),
@@ -570,25 +672,47 @@ def run_e2e(args, T, _abi, local_csr, B, rows, cols, N, prec, device, world):
 
 
 # ----------------------------------------------------------- reference arm
-def reference_sample_runner(args, device):
-    """Returns (run_step(budget_s) -> (flops, seconds, nnz), description,
-    threads).  Each step: the reference's encode_mebcrs + spmm
-    (oracle/_ref = the unmodified reference headers) over disjoint 64-row
-    slices (8 windows) of the workload, one slice per host thread."""
-    import oracle as O
+_HOST_GRAPH = {}
+
+
+def host_graph(args, device):
+    """The workload's CSR and dense operands on the host (built once)."""
     from paper_2412_11007_b200 import graphs as G
 
-    rows, cols, rp, ci, v, _ = build_graph(args, device)
-    N = args.n
-    rp_h = rp.cpu().numpy().view(np.uint32)
-    ci_h = ci.cpu().numpy().view(np.uint32)
-    v_h = v.cpu().numpy()
-    dt = torch.float16 if args.precision == "fp16" else torch.float32
-    Bh = np.ascontiguousarray(G.dense(cols, N, 3, values="real", dtype=dt, device=device).float().cpu().numpy())
-    del rp, ci, v
-    threads = max(1, min(os.cpu_count() or 1, 32))
+    key = (args.workload, args.precision, args.n)
+    if key not in _HOST_GRAPH:
+        rows, cols, rp, ci, v, _ = build_graph(args, device)
+        dt = torch.float16 if args.precision == "fp16" else torch.float32
+        g = {"rows": rows, "cols": cols, "rp": rp.cpu().numpy().view(np.uint32),
+             "ci": ci.cpu().numpy().view(np.uint32), "v": v.cpu().numpy(),
+             # the same operands run_ours uses (seeded), as f32 host arrays
+             "B": np.ascontiguousarray(G.dense(cols, args.n, 3, values="real", dtype=dt, device=device)
+                                       .float().cpu().numpy()),
+             "A": np.ascontiguousarray(G.dense(rows, 32, 4, values="real", dtype=dt, device=device)
+                                       .float().cpu().numpy()),
+             "Bt": np.ascontiguousarray(G.dense(cols, 32, 5, values="real", dtype=dt, device=device)
+                                        .float().cpu().numpy())}
+        del rp, ci, v
+        _HOST_GRAPH.clear()
+        _HOST_GRAPH[key] = g
+    return _HOST_GRAPH[key]
+
+
+def reference_sample_runner(args, device, op="spmm"):
+    """Returns (run_step(budget_s) -> (flops, seconds, nnz), description,
+    threads).  Each step: the reference's encode_mebcrs + spmm (or + sddmm,
+    F = 32) -- oracle/_ref, the unmodified reference headers, timed inside
+    the shim around the reference calls only -- over disjoint 64-row slices
+    (8 windows) spread over the workload, one slice per host thread."""
+    import oracle as O
+
+    g = host_graph(args, device)
+    rows, cols, rp_h, ci_h, v_h = g["rows"], g["cols"], g["rp"], g["ci"], g["v"]
+    N = args.n if op == "spmm" else 32
+    threads = max(1, min(os.cpu_count() or 1, 64))
     prec = 0 if args.precision == "fp16" else 1
     lib = O.ref()
+    dense = lib.ref_dense_new(cols, N, (g["B"] if op == "spmm" else g["Bt"]).ctypes.data_as(O._f32p))
     nslices = (rows + 63) // 64
     stride = max(1, nslices // 997)  # spread slices over the whole graph
     state = {"next": 0}
@@ -602,17 +726,19 @@ def reference_sample_runner(args, device):
         sci = np.ascontiguousarray(ci_h[b:e])
         sv = np.ascontiguousarray(v_h[b:e])
         up = O._u32p
-        orp, oci, ov = up(), up(), O._f32p()
-        nv = lib.ref_encode_mebcrs(r1 - r0, cols, srp.ctypes.data_as(up), sci.ctypes.data_as(up),
-                                   sv.ctypes.data_as(O._f32p), prec, C.byref(orp), C.byref(oci), C.byref(ov))
-        Cm = np.empty((r1 - r0, N), np.float32)
-        cnt = C.c_uint64(0)
-        rc = lib.ref_spmm(r1 - r0, cols, prec, orp, oci, ov, Bh.ctypes.data_as(O._f32p), cols, N, prec, 8, 1,
-                          Cm.ctypes.data_as(O._f32p), C.byref(cnt))
-        for p in (orp, oci, ov):
-            lib.ref_free(C.cast(p, C.c_void_p))
-        assert nv >= 0 and rc == 0
-        return e - b
+        if op == "spmm":
+            Cm = np.empty((r1 - r0, N), np.float32)
+            secs = lib.ref_time_encode_spmm(r1 - r0, cols, srp.ctypes.data_as(up), sci.ctypes.data_as(up),
+                                            sv.ctypes.data_as(O._f32p), prec, dense, Cm.ctypes.data_as(O._f32p))
+        else:
+            As = np.ascontiguousarray(g["A"][r0:r1])
+            cap = 8 * (e - b) + 64
+            out = np.empty(cap, np.float32)
+            secs = lib.ref_time_encode_sddmm(r1 - r0, cols, srp.ctypes.data_as(up), sci.ctypes.data_as(up),
+                                             sv.ctypes.data_as(O._f32p), prec, As.ctypes.data_as(O._f32p), N,
+                                             dense, out.ctypes.data_as(O._f32p), cap)
+        assert secs >= 0
+        return e - b, secs
 
     def run_step(budget_s):
         done = {"nnz": 0}
@@ -623,7 +749,7 @@ def reference_sample_runner(args, device):
                 with lock:
                     idx = state["next"]
                     state["next"] += 1
-                n = one_slice(idx)
+                n, _ = one_slice(idx)
                 with lock:
                     done["nnz"] += n
 
@@ -635,7 +761,8 @@ def reference_sample_runner(args, device):
         secs = time.perf_counter() - t0
         return 2.0 * done["nnz"] * N, secs, done["nnz"]
 
-    desc = (f"reference encode_mebcrs+spmm (oracle/_ref, -O3, unmodified headers) on 64-row slices "
+    what = "spmm" if op == "spmm" else "sddmm (F=32, f32 output)"
+    desc = (f"reference encode_mebcrs+{what} (oracle/_ref, -O3, unmodified headers) on 64-row slices "
             f"(8 windows) spread over the graph, {threads} threads")
     return run_step, desc, threads
 
@@ -664,40 +791,125 @@ def run_reference(args, rank, world, device):
             "e2e": {"value": round(value, 5), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+def restatement_baseline(args, device, budget_s):
+    """BASELINE.md / SURVEY §8(d) item 2: the CPU restatement of the reference
+    semantics (oracle/oracle.cpp: ordered CSR loop with RNE operands, OpenMP
+    over rows) on all host cores -- SpMM at N and SDDMM at F = 32 -- over a
+    row sample sized to ~budget_s each.  Returns GFLOP/s per op."""
+    import oracle as O
+
+    g = host_graph(args, device)
+    lib = O.lib()
+    cores = os.cpu_count() or 1
+    lib.orc_set_num_threads(cores)  # torchrun exports OMP_NUM_THREADS=1
+    m = O.Csr(g["rows"], g["cols"], g["rp"], g["ci"], g["v"])
+    prec = 0 if args.precision == "fp16" else 1
+    rng = np.random.default_rng(7)
+    out = {"cores": int(lib.orc_num_threads()), "kind": "port",
+           "what": "oracle/oracle.cpp CSR-form restatement (bit-exact with the reference), OpenMP"}
+    for op in ("spmm", "sddmm"):
+        frac = 0.002
+        while True:
+            sel = np.sort(rng.choice(g["rows"], max(1, int(g["rows"] * frac)), replace=False)).astype(np.uint64)
+            nnz = int((g["rp"][sel.astype(np.int64) + 1].astype(np.int64) - g["rp"][sel.astype(np.int64)]).sum())
+            t0 = time.perf_counter()
+            if op == "spmm":
+                O.spmm_csr_rows(m, g["B"], prec, rows=sel)
+                flops = 2.0 * nnz * g["B"].shape[1]
+            else:
+                # dot products only: the ME-BCRS output slots are a parity
+                # concern, not part of the timed work
+                O.sddmm_csr_rows(m, prec, None, None, g["A"], g["Bt"], rows=sel)
+                flops = 2.0 * nnz * 32
+            secs = time.perf_counter() - t0
+            if secs > budget_s / 4 or frac >= 1.0:
+                break
+            frac = min(1.0, frac * max(2.0, budget_s / max(secs, 1e-3) / 2))
+        out[op] = {"value": round(flops / secs / 1e9, 4), "unit": "GFLOP/s", "rows": int(sel.size), "nnz": nnz,
+                   "seconds": round(secs, 3)}
+    return out
+
+
 def cpu_baseline(args, device):
     run_step, desc, threads = reference_sample_runner(args, device)
     run_step(1.0)
     f, s, nnz = run_step(args.cpu_seconds)
-    return {"value": round(f / s / 1e9, 5), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
-            "sample": desc + f", {s:.1f}s wall, {nnz} nnz"}
+    out = {"value": round(f / s / 1e9, 5), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+           "sample": desc + f", {s:.1f}s wall, {nnz} nnz"}
+    # the reference's SDDMM (sddmm.hpp:84) on the same pattern, F = 32
+    run_sd, desc_sd, _ = reference_sample_runner(args, device, op="sddmm")
+    run_sd(0.5)
+    f, s, nnz = run_sd(max(2.0, args.cpu_seconds / 3))
+    out["sddmm"] = {"value": round(f / s / 1e9, 5), "unit": "GFLOP/s", "cores": threads, "kind": "reference",
+                    "sample": desc_sd + f", {s:.1f}s wall, {nnz} nnz"}
+    out["restatement"] = restatement_baseline(args, device, max(2.0, args.cpu_seconds / 3))
+    return out
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args) -> int:
+    """`bench.py --gpus N` without torchrun: start N ranks (one per GPU)
+    under torch.distributed.run on this node and forward their output.  The
+    rank count is visible to the driver through NCCL_DEBUG=INFO (stderr)."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    ngpu = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if ngpu < args.gpus and "TCS_DIST_BACKEND" not in env:
+        # NCCL refuses two ranks on one device: with fewer GPUs than ranks the
+        # sharded path still runs (gloo, ranks share devices round-robin) as a
+        # functional check; the line says so in config.backend.
+        env["TCS_DIST_BACKEND"] = "gloo"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
 
 
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; using WORLD_SIZE", file=sys.stderr)
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # TCS_DIST_BACKEND=gloo runs the multi-rank path with every rank on the
     # GPUs there are (ranks share a device round-robin): a functional check
     # of the sharded bench on a 1-GPU box; its timings mean nothing.
     backend = os.environ.get("TCS_DIST_BACKEND", "nccl")
+    os.environ["TCS_BENCH_BACKEND"] = backend if world > 1 else "none"
+    if args.impl == "reference":
+        # the reference arm is host-only: rank 0 runs it, the other ranks exit
+        # 0 without work (no process group needed)
+        if rank == 0:
+            dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+            print(json.dumps(run_reference(args, rank, world, dev)), flush=True)
+        return
+    if not torch.cuda.is_available():
+        backend = "gloo"
     if torch.cuda.is_available():
         local = local % torch.cuda.device_count() if backend != "nccl" else local
     if world > 1:
-        torch.cuda.set_device(local)
+        if torch.cuda.is_available():
+            torch.cuda.set_device(local)
         if backend == "nccl":
             torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             torch.distributed.init_process_group(backend)
     device = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
-    if args.impl == "reference":
-        line = run_reference(args, rank, world, device)
-    else:
-        line = run_ours(args, rank, world, device)
-        if line is not None and world == 1 and not args.quick:
-            line["small_configs"] = small_configs(device)
-            line["layer_configs"] = layer_configs(device)
-            line["cpu_baseline"] = cpu_baseline(args, device)
+    line = run_ours(args, rank, world, device)
+    if line is not None and world == 1 and not args.quick:
+        line["small_configs"] = small_configs(device)
+        line["layer_configs"] = layer_configs(device)
+        line["cpu_baseline"] = cpu_baseline(args, device)
     if line is not None:
         print(json.dumps(line), flush=True)
     if world > 1:

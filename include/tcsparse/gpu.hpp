@@ -5,6 +5,8 @@
 //   tcsparse::spmm(a, b, cfg)       ->  tcsparse::gpu::spmm(a, b, cfg)
 //   tcsparse::sddmm(ops, cfg)       ->  tcsparse::gpu::sddmm(ops, cfg)
 //   tcsparse::spmm_baseline16(m, b, cfg) -> tcsparse::gpu::spmm_baseline16(m, b, cfg)
+//   (multi-GPU extension, no reference counterpart)
+//                                   tcsparse::gpu::spmm_sharded(m, b, cfg, comm)
 //
 // Same parameter and return types as the reference (ref mebcrs.hpp:80,
 // spmm.hpp:173, sddmm.hpp:84) -- this header includes the reference's own
@@ -29,6 +31,7 @@
 #include <vector>
 
 #include "tcs/tcs.h"
+#include "tcs/tcs_dist.h"
 #include "tcsparse/mebcrs.hpp"
 #include "tcsparse/sddmm.hpp"
 #include "tcsparse/spmm.hpp"
@@ -44,6 +47,7 @@ inline void check(tcs_status s) {
         case TCS_ERR_ARGUMENT: throw ArgumentError(msg);
         case TCS_ERR_SHAPE: throw ShapeError(msg);
         case TCS_ERR_FORMAT: throw FormatError(msg);
+        case TCS_ERR_NCCL: throw std::runtime_error("tcsparse-b200 (NCCL): " + msg);
         default: throw std::runtime_error("tcsparse-b200: " + msg);
     }
 }
@@ -137,6 +141,35 @@ inline SpmmResult spmm(const MeBcrsMatrix& sparse, const DenseMatrix& dense, con
                                 sparse.row_pointers.data(), sparse.column_indices.data(), sparse.values.data(),
                                 dense.data.data(), static_cast<int64_t>(dense.rows),
                                 static_cast<int64_t>(dense.cols), res.output.data.data(), &kc, &cn, nullptr));
+    res.counters = detail::counters(cn);
+    return res;
+}
+
+/// Multi-GPU extension of the CLI's encode + spmm pipeline (ref
+/// cli.hpp:162-200; the reference itself has no communication layer, its
+/// rows are independent per 8-row window): every rank of the
+/// NCCL communicator `nccl_comm` (an ncclComm_t) calls this with the same
+/// CSR; rank `root`'s dense operand is broadcast (the others' content is
+/// ignored, only its shape is checked).  The row windows are cut by nnz,
+/// each rank converts and multiplies its own rows, and every rank returns
+/// the whole C.  An NCCL error, or no completion within timeout_ms, aborts
+/// the communicator and throws std::runtime_error.  counters are this
+/// rank's shard's.
+inline SpmmResult spmm_sharded(const CsrMatrix& sparse, const DenseMatrix& dense, const KernelConfig& cfg,
+                               void* nccl_comm, int root = 0, int64_t timeout_ms = 60000) {
+    if (cfg.vector_height != 8) throw ArgumentError("swap-and-transpose path requires vector height 8");
+    if (sparse.cols != dense.rows) throw ShapeError("sparse cols must equal dense rows");
+    tcs_dist d{};
+    detail::check(tcs_dist_init(&d, nccl_comm, timeout_ms));
+    const tcs_kernel_config kc = detail::config(cfg);
+    const tcs_csr c{sparse.rows, sparse.cols, sparse.nnz(), sparse.row_ptr.data(), sparse.col_idx.data(),
+                    sparse.values.data()};
+    SpmmResult res;
+    res.output = DenseMatrix(sparse.rows, dense.cols);
+    tcs_counters cn{};
+    detail::check(tcs_spmm_sharded_csr_host(&d, &c, static_cast<tcs_precision>(cfg.precision), dense.data.data(),
+                                            static_cast<int64_t>(dense.cols), root, res.output.data.data(), &kc,
+                                            &cn, nullptr));
     res.counters = detail::counters(cn);
     return res;
 }

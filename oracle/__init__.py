@@ -76,6 +76,7 @@ def lib():
         _orc.orc_count_mma_sddmm.restype = C.c_uint64
         _orc.orc_count_mma_sddmm.argtypes = [C.c_uint64, _u32p, C.c_uint32, C.c_uint64]
         _orc.orc_num_threads.restype = C.c_int
+        _orc.orc_set_num_threads.argtypes = [C.c_int]
         _orc.orc_mt19937.argtypes = [C.c_uint32, C.c_uint64, _u32p]
         _orc.orc_round_array.argtypes = [C.c_int, _f32p, _f32p, C.c_uint64]
         _orc.orc_free.argtypes = [C.c_void_p]
@@ -571,8 +572,9 @@ def sddmm_csr_rows(m: Csr, precision: int, rp: np.ndarray, ci: np.ndarray, A: np
     (dot[f32], pos[u64]); pos = 2^64-1 marks an entry missing from (rp, ci)."""
     A = np.ascontiguousarray(A, np.float32)
     Bt = np.ascontiguousarray(Bt, np.float32)
-    rp = np.ascontiguousarray(rp, np.uint32)
-    ci = np.ascontiguousarray(ci, np.uint32)
+    # rp = ci = None: dot products only, no ME-BCRS positions (pos stays 0)
+    rp = None if rp is None else np.ascontiguousarray(rp, np.uint32)
+    ci = None if ci is None else np.ascontiguousarray(ci, np.uint32)
     sel = np.arange(m.rows, dtype=np.uint64) if rows is None else np.ascontiguousarray(rows, np.uint64)
     lens = (m.row_ptr[sel.astype(np.int64) + 1].astype(np.uint64) - m.row_ptr[sel.astype(np.int64)].astype(np.uint64))
     eoff = np.zeros(sel.size + 1, np.uint64)
@@ -580,7 +582,8 @@ def sddmm_csr_rows(m: Csr, precision: int, rp: np.ndarray, ci: np.ndarray, A: np
     dot = np.zeros(max(int(eoff[-1]), 1), np.float32)
     pos = np.zeros(max(int(eoff[-1]), 1), np.uint64)
     lib().orc_sddmm_csr_rows(C.c_uint64(m.rows), precision, K_OF[precision], _p(m.row_ptr, _u32p),
-                             _p(m.col_idx, _u32p), _p(m.values, _f32p), _p(rp, _u32p), _p(ci, _u32p), _p(A, _f32p),
+                             _p(m.col_idx, _u32p), _p(m.values, _f32p), None if rp is None else _p(rp, _u32p),
+                             None if ci is None else _p(ci, _u32p), _p(A, _f32p),
                              C.c_uint64(A.shape[1]), _p(Bt, _f32p), C.c_uint64(Bt.shape[1]), C.c_uint64(A.shape[1]),
                              _p(sel, _u64p), C.c_uint64(sel.size), _p(eoff, _u64p), _p(dot, _f32p), _p(pos, _u64p))
     n = int(eoff[-1])

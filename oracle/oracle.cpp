@@ -342,19 +342,21 @@ void orc_sddmm_csr_rows(uint64_t rows, int precision, uint32_t k, const uint32_t
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t i = 0; i < static_cast<int64_t>(n_sel); ++i) {
         const uint64_t r = sel[i], w = r / 8;
-        const uint32_t base = rp[w], nvw = rp[w + 1] - base;
+        const uint32_t base = rp ? rp[w] : 0, nvw = rp ? rp[w + 1] - base : 0;
         uint32_t j = 0;
         for (uint32_t e = row_ptr[r]; e < row_ptr[r + 1]; ++e) {
             const uint32_t c = col_idx[e];
-            while (j < nvw && ci[base + j] < c) ++j;
             const uint64_t o = eoff[i] + (e - row_ptr[r]);
-            if (j >= nvw || ci[base + j] != c) {  // not a vector of the window: an encoding error
-                pos[o] = ~0ull;
-                dot[o] = 0.0f;
-                continue;
+            if (rp) {  // rp == null: dot products only (the CPU-baseline timing)
+                while (j < nvw && ci[base + j] < c) ++j;
+                if (j >= nvw || ci[base + j] != c) {  // not a vector of the window: an encoding error
+                    pos[o] = ~0ull;
+                    dot[o] = 0.0f;
+                    continue;
+                }
+                const uint32_t b = j / k, jj = j % k, width = std::min(k, nvw - b * k);
+                pos[o] = 8ull * (base + b * k) + (r % 8) * width + jj;
             }
-            const uint32_t b = j / k, jj = j % k, width = std::min(k, nvw - b * k);
-            pos[o] = 8ull * (base + b * k) + (r % 8) * width + jj;
             float acc = 0.0f;
             if (vals[e] != 0.0f) {
                 const float* a = A + r * lda;
@@ -386,6 +388,14 @@ uint64_t orc_count_mma_sddmm(uint64_t W, const uint32_t* rp, uint32_t k, uint64_
 void orc_mt19937(uint32_t seed, uint64_t n, uint32_t* out) {
     std::mt19937 g(seed);
     for (uint64_t i = 0; i < n; ++i) out[i] = g();
+}
+
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
 }
 
 int orc_num_threads(void) {

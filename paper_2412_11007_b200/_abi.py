@@ -66,7 +66,27 @@ class tcs_cost(C.Structure):
                                           "footprint_me", "footprint_sr", "padded_vectors")]
 
 
+class tcs_dist(C.Structure):
+    _fields_ = [("comm", C.c_void_p), ("rank", C.c_int), ("world", C.c_int), ("timeout_ms", C.c_int64)]
+
+
+TCS_DIST_BROADCAST_B, TCS_DIST_ALLGATHER_C = 0x1, 0x2
+
 EXPORTS = {
+    # include/tcs/tcs_dist.h
+    "tcs_dist_init": (C.c_int, [C.POINTER(tcs_dist), C.c_void_p, C.c_int64]),
+    "tcs_shard_windows": (C.c_int, [C.POINTER(tcs_csr), C.c_int, C.c_void_p, C.c_void_p]),
+    "tcs_mebcrs_encode_shard": (C.c_int, [C.POINTER(tcs_csr), C.c_uint64, C.c_uint64, C.c_int, C.c_int,
+                                          C.POINTER(tcs_mebcrs), C.c_void_p]),
+    "tcs_dist_broadcast": (C.c_int, [C.POINTER(tcs_dist), C.c_void_p, C.c_uint64, C.c_int, C.c_void_p]),
+    "tcs_spmm_sharded": (C.c_int, [C.POINTER(tcs_dist), C.c_void_p, C.c_uint64, C.POINTER(tcs_mebcrs), C.c_void_p,
+                                   C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int, C.c_uint32, C.c_void_p,
+                                   C.c_int64, C.POINTER(tcs_kernel_config), C.POINTER(tcs_counters), C.c_void_p]),
+    "tcs_dist_wait": (C.c_int, [C.POINTER(tcs_dist), C.c_void_p, C.c_int64]),
+    "tcs_spmm_sharded_csr_host": (C.c_int, [C.POINTER(tcs_dist), C.POINTER(tcs_csr), C.c_int, C.c_void_p, C.c_int64,
+                                            C.c_int, C.c_void_p, C.POINTER(tcs_kernel_config),
+                                            C.POINTER(tcs_counters), C.c_void_p]),
+    # include/tcs/tcs.h
     # name: (restype, argtypes)
     "tcs_version": (C.c_char_p, []),
     "tcs_last_error": (C.c_char_p, []),

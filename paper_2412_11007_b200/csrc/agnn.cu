@@ -337,6 +337,7 @@ extern "C" tcs_status tcs_agnn_attend(const tcs_mebcrs* mask, const void* h, tcs
                                       int64_t row0, int64_t f, float scale, float eps, float* c, int64_t ldc,
                                       const tcs_kernel_config* cfg, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_agnn_attend");
         if (!mask || !cfg) fail(TCS_ERR_ARGUMENT, "null argument");
         check_mebcrs(mask);
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");

@@ -796,12 +796,14 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
 
 extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
                                         tcs_mebcrs* out, tcs_stream_t stream) {
-    return guard([&] { encode_impl<8>(csr, precision, value_dtype, out, stream); });
+    return guard([&] {
+        NvtxRange nvtx_range("tcs_mebcrs_encode"); encode_impl<8>(csr, precision, value_dtype, out, stream); });
 }
 
 extern "C" tcs_status tcs_mebcrs_encode_v(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
                                           uint32_t vector_height, tcs_mebcrs* out, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_mebcrs_encode_v");
         // ref partition.hpp:42-43
         if (vector_height == 8) encode_impl<8>(csr, precision, value_dtype, out, stream);
         else if (vector_height == 16) encode_impl<16>(csr, precision, value_dtype, out, stream);
@@ -812,6 +814,7 @@ extern "C" tcs_status tcs_mebcrs_encode_v(const tcs_csr* csr, tcs_precision prec
 extern "C" tcs_status tcs_mebcrs_encode_host(const tcs_csr* host_csr, tcs_precision precision,
                                              tcs_dtype value_dtype, tcs_mebcrs* out, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_mebcrs_encode_host");
         if (!host_csr || !out || !host_csr->row_ptr) fail(TCS_ERR_ARGUMENT, "null argument");
         cudaStream_t s = st(stream);
         const uint64_t rows = host_csr->rows, nnz = host_csr->nnz;

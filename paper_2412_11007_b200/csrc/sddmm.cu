@@ -670,6 +670,7 @@ extern "C" tcs_status tcs_sddmm(const tcs_mebcrs* mask, const void* a, tcs_dtype
                                 int64_t bt_rows, int64_t f_b, tcs_mebcrs* out, tcs_dtype out_dtype,
                                 const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_sddmm");
         if (!out) fail(TCS_ERR_ARGUMENT, "null argument");
         sddmm_check(mask, a, a_dtype, lda, a_rows, f_a, bt, bt_dtype, ldbt, bt_rows, f_b, out_dtype, cfg);
         cudaStream_t s = st(stream);
@@ -712,6 +713,7 @@ extern "C" tcs_status tcs_sddmm_host(uint64_t rows, uint64_t cols, tcs_precision
                                      const float* bt, int64_t bt_rows, int64_t f_b, float* out_values,
                                      const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_sddmm_host");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded mask");
         if (a_rows != static_cast<int64_t>(rows)) fail(TCS_ERR_SHAPE, "A rows must equal mask rows");

@@ -425,6 +425,7 @@ using namespace tcs;
 extern "C" tcs_status tcs_mebcrs_row_softmax(const tcs_mebcrs* scores, const tcs_mebcrs* mask, float scale,
                                              tcs_mebcrs* out, tcs_dtype out_dtype, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_mebcrs_row_softmax");
         if (!out) fail(TCS_ERR_ARGUMENT, "null output");
         check_mebcrs(scores);
         check_mebcrs(mask);
@@ -468,6 +469,7 @@ extern "C" tcs_status tcs_sddmm_row_softmax(const tcs_mebcrs* mask, const void* 
                                             tcs_dtype score_dtype, tcs_mebcrs* out, tcs_dtype out_dtype,
                                             const tcs_kernel_config* cfg, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_sddmm_row_softmax");
         if (!out) fail(TCS_ERR_ARGUMENT, "null output");
         sddmm_check(mask, a, a_dtype, lda, a_rows, f_a, bt, bt_dtype, ldbt, bt_rows, f_b, score_dtype, cfg);
         if (out_dtype != TCS_DTYPE_F16 && out_dtype != TCS_DTYPE_F32) fail(TCS_ERR_ARGUMENT, "unknown output dtype");
@@ -526,6 +528,7 @@ extern "C" tcs_status tcs_agnn_aggregate(const tcs_mebcrs* mask, const void* hn,
                                          tcs_dtype hc_dtype, int64_t ldhc, int64_t n, float* c, int64_t ldc,
                                          const tcs_kernel_config* cfg, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_agnn_aggregate");
         if (row0 < 0 || !mask || row0 + static_cast<int64_t>(mask->rows) > static_cast<int64_t>(mask->cols))
             fail(TCS_ERR_SHAPE, "AGNN attention: mask rows [row0, row0 + rows) must be nodes of its columns");
         // the mask's row i is node row0 + i: A = Hn[row0 .. row0 + rows), Bt = Hn (all nodes)

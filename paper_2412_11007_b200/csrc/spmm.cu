@@ -795,6 +795,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                                int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
                                tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         // ref spmm.hpp:106-109
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
@@ -927,6 +928,7 @@ extern "C" tcs_status tcs_spmm_host(uint64_t rows, uint64_t cols, tcs_precision 
                                     const float* b, int64_t b_rows, int64_t n, float* c,
                                     const tcs_kernel_config* cfg, tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_host");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
         if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");
@@ -1007,6 +1009,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
                                         float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
                                         tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_csr_host");
         if (!host_csr || !cfg || !host_csr->row_ptr) fail(TCS_ERR_ARGUMENT, "null argument");
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
         if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");

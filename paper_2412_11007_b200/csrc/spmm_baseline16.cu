@@ -345,6 +345,7 @@ extern "C" tcs_status tcs_spmm_baseline16(const tcs_mebcrs* A, const void* b, tc
                                           const tcs_kernel_config* cfg, tcs_counters* counters,
                                           tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_baseline16");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         // ref spmm.hpp:190-191
         if (cfg->vector_height != 16) fail(TCS_ERR_ARGUMENT, "baseline path requires vector height 16");
@@ -443,6 +444,7 @@ extern "C" tcs_status tcs_spmm_baseline16_csr_host(const tcs_csr* host_csr, cons
                                                    int64_t n, float* c, const tcs_kernel_config* cfg,
                                                    tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_baseline16_csr_host");
         if (!host_csr || !cfg || !host_csr->row_ptr) fail(TCS_ERR_ARGUMENT, "null argument");
         // ref spmm.hpp:190-191, in its order
         if (cfg->vector_height != 16) fail(TCS_ERR_ARGUMENT, "baseline path requires vector height 16");

@@ -204,12 +204,14 @@ void from_mebcrs(const tcs_mebcrs* me, tcs_srbcrs* out, cudaStream_t s) {
 using namespace tcs;
 
 extern "C" tcs_status tcs_srbcrs_from_mebcrs(const tcs_mebcrs* me, tcs_srbcrs* out, tcs_stream_t stream) {
-    return guard([&] { from_mebcrs(me, out, st(stream)); });
+    return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_from_mebcrs"); from_mebcrs(me, out, st(stream)); });
 }
 
 extern "C" tcs_status tcs_srbcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,
                                         tcs_srbcrs* out, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_encode");
         tcs_mebcrs me{};
         tcs_status rc = tcs_mebcrs_encode(csr, precision, value_dtype, &me, stream);
         if (rc != TCS_OK) fail(rc, tcs_last_error());
@@ -226,6 +228,7 @@ extern "C" tcs_status tcs_srbcrs_upload(uint64_t rows, uint64_t cols, tcs_precis
                                         const uint32_t* row_pointer_pairs, const uint32_t* column_indices,
                                         const float* values, tcs_srbcrs* out, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_upload");
         if (!out || (rows && !row_pointer_pairs)) fail(TCS_ERR_ARGUMENT, "null argument");
         if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
         cudaStream_t s = st(stream);
@@ -270,6 +273,7 @@ extern "C" tcs_status tcs_srbcrs_upload(uint64_t rows, uint64_t cols, tcs_precis
 extern "C" tcs_status tcs_srbcrs_download(const tcs_srbcrs* m, uint32_t* row_pointer_pairs, uint32_t* column_indices,
                                           float* values, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_download");
         check_sr(m);
         cudaStream_t s = st(stream);
         if (row_pointer_pairs && m->num_windows)
@@ -293,13 +297,15 @@ extern "C" tcs_status tcs_srbcrs_download(const tcs_srbcrs* m, uint32_t* row_poi
 }
 
 extern "C" tcs_status tcs_srbcrs_free(tcs_srbcrs* m, tcs_stream_t stream) {
-    return guard([&] { sr_release(m, st(stream)); });
+    return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_free"); sr_release(m, st(stream)); });
 }
 
 extern "C" tcs_status tcs_spmm_srbcrs(const tcs_srbcrs* A, const void* b, tcs_dtype b_dtype, int64_t ldb,
                                       int64_t b_rows, int64_t n, float* c, int64_t ldc, const tcs_kernel_config* cfg,
                                       tcs_counters* counters, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_srbcrs");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         // ref spmm.hpp:106-109 (spmm_swapped's checks, shared by both formats)
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
@@ -332,6 +338,7 @@ extern "C" tcs_status tcs_spmm_srbcrs_host(uint64_t rows, uint64_t cols, tcs_pre
                                            const tcs_kernel_config* cfg, tcs_counters* counters,
                                            tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_spmm_srbcrs_host");
         if (!cfg) fail(TCS_ERR_ARGUMENT, "null kernel config");
         if (cfg->vector_height != 8) fail(TCS_ERR_ARGUMENT, "swap-and-transpose path requires vector height 8");
         if (cfg->precision != precision) fail(TCS_ERR_ARGUMENT, "config precision must match the encoded matrix");
@@ -359,6 +366,7 @@ extern "C" tcs_status tcs_spmm_srbcrs_host(uint64_t rows, uint64_t cols, tcs_pre
 // like every other stored zero.
 extern "C" tcs_status tcs_srbcrs_decode(const tcs_srbcrs* m, tcs_csr* out, tcs_stream_t stream) {
     return guard([&] {
+        NvtxRange nvtx_range("tcs_srbcrs_decode");
         check_sr(m);
         if (!out) fail(TCS_ERR_ARGUMENT, "null output");
         tcs_status rc = tcs_mebcrs_decode(&static_cast<SrImpl*>(m->impl)->view, out, stream);

@@ -9,13 +9,15 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HEADER = os.path.join(ROOT, "include", "tcs", "tcs.h")
+HEADERS = [os.path.join(ROOT, "include", "tcs", h) for h in ("tcs.h", "tcs_dist.h")]
 
 
 def declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tcs_\w+)\s*\(", src, flags=re.M)))
+    names = set()
+    for header in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(header).read(), flags=re.S)
+        names |= set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(tcs_\w+)\s*\(", src, flags=re.M))
+    return sorted(names)
 
 
 @pytest.fixture(scope="module")
@@ -49,6 +51,7 @@ def test_struct_layouts_match_header(lib):
     assert C.sizeof(_abi.tcs_mebcrs) == 104
     assert C.sizeof(_abi.tcs_kernel_config) == 16
     assert C.sizeof(_abi.tcs_counters) == 32
+    assert C.sizeof(_abi.tcs_dist) == 24
 
 
 def test_version_and_no_silent_fallback(lib):
@@ -80,3 +83,14 @@ def test_argument_errors_precede_device_work(lib):
     cfg = _abi.tcs_kernel_config(0, 8, 1, 0)
     rc = lib.tcs_spmm_host(8, 8, 0, None, None, None, None, 9, 16, None, C.byref(cfg), None, None)
     assert rc == _abi.TCS_ERR_SHAPE  # sparse cols != dense rows (ref spmm.hpp:109)
+
+
+def test_dist_argument_errors_without_device(lib):
+    """tcs_dist_* reject bad arguments before touching NCCL or the device."""
+    from paper_2412_11007_b200 import _abi
+
+    d = _abi.tcs_dist()
+    assert lib.tcs_dist_init(C.byref(d), None, 0) == _abi.TCS_ERR_ARGUMENT
+    assert lib.tcs_dist_broadcast(C.byref(d), None, 0, 0, None) == _abi.TCS_ERR_NCCL  # never bound
+    assert b"communicator" in lib.tcs_last_error()
+    assert lib.tcs_shard_windows(None, 2, None, None) == _abi.TCS_ERR_ARGUMENT

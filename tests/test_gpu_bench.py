@@ -44,3 +44,19 @@ def test_bench_two_ranks_sharded():
     assert sum(s["nnz"] for s in two["shards"]) == one["config"]["nnz"]
     # windows never straddle shards, so the vector count is the same
     assert two["config"]["nv_8x1"] == one["config"]["nv_8x1"]
+
+
+def test_bench_gpus_flag_launches_ranks_itself():
+    """`bench.py --gpus 2` with no torchrun: bench.py starts the ranks itself
+    (gloo when the box has fewer GPUs than ranks, NCCL otherwise)."""
+    one = _run([sys.executable, "bench.py", "--workload", "c1", "--quick", "--steps", "3", "--warmup", "3"])
+    two = _run([sys.executable, "bench.py", "--gpus", "2", "--workload", "c1", "--quick", "--steps", "3",
+                "--warmup", "3"])
+    assert two["n_gpus"] == 2 and len(two["shards"]) == 2
+    assert two["config"]["backend"] in ("nccl", "gloo")
+    if torch.cuda.device_count() >= 2:
+        assert two["config"]["backend"] == "nccl"
+    assert sum(s["nnz"] for s in two["shards"]) == one["config"]["nnz"]
+    ref = _run([sys.executable, "bench.py", "--impl", "reference", "--gpus", "2", "--workload", "c1", "--steps", "3",
+                "--warmup", "3"])
+    assert ref["impl"] == "reference" and ref["n_gpus"] == 2 and ref["value"] > 0
