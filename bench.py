@@ -226,7 +226,8 @@ def small_configs(device):
         out[f"c1_spmm_{pname}_n128_us"] = round(us, 2)
         out[f"c1_spmm_{pname}_gflops"] = round(2.0 * nnz * 128 / (us * 1e-6) / 1e9, 1)
         out[f"c1_spmm_{pname}_roofline"] = {"bytes_alg": balg, "frac": round(balg / (us * 1e-6) / 1e9 / peak, 4),
-                                            "us_at_peak": round(balg / (peak * 1e9) * 1e6, 2)}
+                                            "us_at_peak": round(balg / (peak * 1e9) * 1e6, 2),
+                                            "dram": _with_frac(dram_traffic(f"c1_{pname}_n128_g1"), us / 1e3)}
         A = G.dense(rows, 32, 3, dtype=dt, device=device)
         Bt = G.dense(cols, 32, 4, dtype=dt, device=device)
         ov = torch.empty(8 * me.num_vectors, device=device)
@@ -236,7 +237,8 @@ def small_configs(device):
         out[f"c2_sddmm_{pname}_k32_us"] = round(us2, 2)
         out[f"c2_sddmm_{pname}_gflops"] = round(2.0 * nnz * 32 / (us2 * 1e-6) / 1e9, 1)
         out[f"c2_sddmm_{pname}_roofline"] = {"bytes_alg": sbalg, "frac": round(sbalg / (us2 * 1e-6) / 1e9 / peak, 4),
-                                             "us_at_peak": round(sbalg / (peak * 1e9) * 1e6, 2)}
+                                             "us_at_peak": round(sbalg / (peak * 1e9) * 1e6, 2),
+                                             "dram": _with_frac(dram_traffic(f"c2_sddmm_{pname}_f32_g1"), us2 / 1e3)}
         out["graph_captured"] = bool(g and g2)
         me.free()
     t = []
@@ -285,9 +287,7 @@ def layer_configs(device):
         if bytes_min is not None:
             d["bytes_min"] = bytes_min
             d["frac_bytes_min"] = round(bytes_min / (ms / 1e3) / 1e9 / peak, 4)
-        dram = dram_traffic(key)
-        if dram:
-            d["dram"] = dict(dram, frac_dram=round(dram["bytes_per_launch"] / (ms / 1e3) / 1e9 / peak, 4))
+        d["dram"] = _with_frac(dram_traffic(key), ms)
         return d
 
     rows, _, rp, ci, _ = G.power_law_csr(G.C4_PRODUCTS, values="real", device=device)
@@ -349,6 +349,13 @@ def dram_traffic(key):
     out = {k: e[k] for k in ("bytes_per_launch", "l2_hit_pct", "source") if k in e}
     out["current"] = e.get("csrc_sha") == csrc_sha()
     return out
+
+
+def _with_frac(dram, ms):
+    """dram_traffic() plus the measured DRAM bytes / time against the HBM peak."""
+    if not dram:
+        return None
+    return dict(dram, frac_dram=round(dram["bytes_per_launch"] / (ms / 1e3) / 1e9 / peaks()[0], 4))
 
 
 def csrc_sha():
@@ -542,6 +549,7 @@ def run_ours(args, rank, world, device):
         sddmm = {"F": F, "ms": round(sd_ms, 4), "gflops": round(2.0 * nnz_local * F / (sd_ms / 1e3) / 1e9, 1),
                  "bytes_alg_per_launch": sd_bytes, "achieved_gbs": round(sd_bytes / (sd_ms / 1e3) / 1e9, 1),
                  "frac": round(sd_bytes / (sd_ms / 1e3) / 1e9 / peak_, 4), "out": "f32 ME-BCRS values",
+                 "dram": _with_frac(dram_traffic(f"{args.workload}_sddmm_{args.precision}_f{F}_g{world}"), sd_ms),
                  "ms_static_mask": round(sd_static_ms, 4),
                  "gflops_static_mask": round(2.0 * nnz_local * F / (sd_static_ms / 1e3) / 1e9, 1)}
         del Ad, Btd, ov
@@ -591,8 +599,7 @@ def run_ours(args, rank, world, device):
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
                      "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>",
                      "binding_resource": "l2_gather" if prec == 0 else "dram latency (31% of gather sectors miss L2)",
-                     "dram": None if not dram else dict(dram, achieved_gbs=round(dram["bytes_per_launch"] / (step_ms / 1e3) / 1e9, 1),
-                                                        frac_dram=round(dram["bytes_per_launch"] / (step_ms / 1e3) / 1e9 / peak, 4)),
+                     "dram": _with_frac(dram, step_ms),
                      "l2_gather": {"gather_bytes_per_launch": gather_bytes,
                                    "achieved_gbs": round(gather_bytes / (step_ms / 1e3) / 1e9, 1),
                                    "peak_gbs": l2["peak_gbs"], "peak_source": l2["source"],

@@ -127,6 +127,10 @@ typedef struct tcs_kernel_config {
  * the values in place must call tcs_mebcrs_prepare (fresh work list) before
  * relying on this flag again. */
 #define TCS_CFG_STATIC_MASK 0x8u
+/* TF32 SpMM, N > 32: gather the f32 dense operand as given instead of its
+ * per-call repack into 2.5 bytes per feature (the top 19 bits the TF32 MMA
+ * reads).  Same results bit for bit; kept as the ablation. */
+#define TCS_CFG_TF32_F32_GATHER 0x10u
 
 /* ref: spmm.hpp:23-28 (KernelCounters).  mma_invocations is reported in the
  * reference's units (storage-k blocks x 16-wide tiles, ref analysis.hpp:34);

@@ -52,6 +52,7 @@ struct SddmmArgs {
     uint32_t* counter;  // claim counters, dev::kClaimBytes (zeroed before launch)
     float dead;         // value of stored slots whose mask value is 0: 0, or -inf for the fused softmax
     const uint8_t* live;  // per-vector liveness bytes (bit r: row r's mask value != 0), mask mode kLive
+    uint32_t sub;         // warps per work item (direct dispatch only; 1 otherwise)
 };
 
 // Mask modes (template parameter MM): how a slot's liveness is read.
@@ -308,13 +309,19 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     extern __shared__ __align__(16) unsigned char ring_all[];  // per-warp ring, see below
     // persistent warps pulling work items (dev::StripedClaim)
     dev::StripedClaim<4> claim;
-    for (uint32_t idx; claim.get(a.counter, a.n_items, idx);) {
-    const WorkItem it = a.items[idx];
+    for (uint32_t idx; claim.get(a.counter, a.n_items * a.sub, idx);) {
+    // Direct dispatch of a small list may give an item `sub` warps: warp
+    // `part` takes the part-th run of 16-vector groups (each vector's output
+    // is independent, so the runs need no reduction).
+    const uint32_t part = idx % a.sub;
+    const WorkItem it = a.items[idx / a.sub];
     const uint32_t base = __ldg(a.rp + it.window);
     const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
     const uint32_t* ci = a.ci + base;
     const uint64_t vbase = 8ull * base;
-    const uint32_t vend = it.vend;
+    const uint32_t run = ((it.vend - it.vbeg + a.sub - 1) / a.sub + 15u) & ~15u;
+    const uint32_t vbeg = min(it.vend, it.vbeg + part * run);
+    const uint32_t vend = min(it.vend, vbeg + run);
     const uint64_t arow_i = 8ull * it.window + g;
     const bool arow_ok = arow_i < a.rows;
     const Elem* arow = static_cast<const Elem*>(a.A) + (arow_ok ? arow_i : 0) * a.lda;
@@ -438,7 +445,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
         }
     };
 
-    const uint32_t s0 = it.vbeg;
+    const uint32_t s0 = vbeg;
     if (s0 < vend) {
         const uint32_t nf = (vend - s0) / BV;  // full batches; at most one partial batch follows
         uint32_t pb = 0;                       // next batch to prefetch
@@ -497,8 +504,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
 
 template <bool TF32, int NSC>
 void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
-    const dim3 grid(static_cast<unsigned>(std::min<uint64_t>((a.n_items + kWarps - 1) / kWarps,
-                                                             uint64_t(num_sms()) * kMinBlocks<NSC>)));
+    const uint64_t need = (a.n_items * a.sub + kWarps - 1) / kWarps;
+    const dim3 grid(static_cast<unsigned>(a.counter ? std::min<uint64_t>(need, uint64_t(num_sms()) * kMinBlocks<NSC>)
+                                                    : need));
     const size_t sm32 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF32>();
     const size_t sm16 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF16>();
     const size_t sml = kWarps * kRing * ring_slot_bytes<NSC, kLive>();
@@ -640,11 +648,26 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     int64_t alda = 0, bldb = 0;
     const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
     const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
-    DBuf item_ctr(dev::kClaimBytes, s);
-    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, dev::kClaimBytes, s));
+    // direct dispatch (one warp per item, no claim counter) when the items
+    // fit in one wave at the lowest residency of the SDDMM kernels
+    DBuf item_ctr;
+#ifndef TCS_NO_DIRECT_DISPATCH
+    const bool direct = (plan->n_items + kWarps - 1) / kWarps <= uint64_t(num_sms()) * 3;
+#else
+    const bool direct = false;
+#endif
+    if (!direct) {
+        item_ctr = DBuf(dev::kClaimBytes, s);
+        TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, dev::kClaimBytes, s));
+    }
+    // direct dispatch: as many warps per item as one wave holds (<= 8)
+    const uint32_t sub = direct ? static_cast<uint32_t>(std::max<uint64_t>(
+                                      1, std::min<uint64_t>(8, uint64_t(num_sms()) * 3 * kWarps /
+                                                                   std::max<uint64_t>(1, plan->n_items))))
+                                : 1u;
     SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
                    ap, alda, bp, bldb, out_values, mask->rows,
-                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr};
+                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr, sub};
     const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
     if (!plan->n_items) return;
     if (static_mask) args.live = mask_liveness(mask, plan, s);

@@ -104,6 +104,14 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_SPMM_DEEP32
 #define TCS_SPMM_DEEP32 1
 #endif
+// TF32 SpMM on the 2.5-byte packed dense operand (spmm_tf32p_kernel) for
+// feature slabs of 64 / 128; 0 = the f32-gather kernel everywhere.
+#ifndef TCS_TF32_PACKED
+#define TCS_TF32_PACKED 1
+#endif
+#ifndef TCS_SMALL_SLAB32
+#define TCS_SMALL_SLAB32 1
+#endif
 // Feature slab of the TF32 kernel for N > 64 (experiment knob: 128 or 64).
 #ifndef TCS_SPMM_SLAB_TF32
 #define TCS_SPMM_SLAB_TF32 128
@@ -333,9 +341,9 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     const uint32_t src_lane = 8 * t + g;                    // where this lane's fragment data was loaded
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
+    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -402,7 +410,7 @@ __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const S
     const uint32_t src_lane = 8 * t + g;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
-    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
     dev::StripedClaim<1> claim;  // this loop form measured 7% faster than next_item here (C5 N=32)
     for (uint32_t idx; claim.get(counter, a.n_items, idx);) {
         const WorkItem it = a.items[idx];
@@ -477,9 +485,9 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
     const uint32_t g = lane >> 2, t = lane & 3;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const unsigned short* Bl = static_cast<const unsigned short*>(a.B) + feat0 + g;
-    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
+    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -662,9 +670,9 @@ __global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_ke
     const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
-    uint32_t* counter = a.counter + static_cast<uint64_t>(a.slab0 + blockIdx.y) * (dev::kClaimBytes / 4);
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
+    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -714,6 +722,185 @@ __global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_ke
     }
 }
 
+// ------------------------------------------------- TF32, packed operand
+//
+// The TF32 MMA reads only the top 19 bits of an operand (sign, exponent, 10
+// mantissa bits), so the RNE-rounded dense operand is repacked once per call
+// into 2.5 bytes per feature: the top 16 bits ("hi", one u16) and mantissa
+// bits 10..12 below them ("lo", one nibble, stored as e << 1).  Per B row:
+// [hi: 2*npad bytes][lo: npad/2 bytes] -- 320 B instead of 512 B at N = 128,
+// so C3's 119 MB f32 operand becomes 75 MB and stays L2-resident, and each
+// gathered row costs 2 + 1 loads and 10 shuffles per 128 features instead
+// of 4 and 16.  Rebuilding an operand is one PRMT: the hi pair supplies the
+// top two bytes, the nibble's byte the third (bits 13..15 = e; the low 13
+// bits the MMA ignores are don't-care).  Bit-identical to the f32 path.
+//
+// Mapping: as the f32 TF32 kernel (loader slot u of quarter q reads vector
+// q + 4u) but with 64-feature chunks, 8 features per lane: lane (g, t) gets,
+// after the shuffle from lane 8t+g, features 8g..8g+7 of vectors t and t+4.
+// M-tile j of a chunk holds feature 8g+2j in row g and 8g+2j+1 in row g+8,
+// so the accumulator layout is the FP16 kernel's (f16_epilogue<., 8>).
+__global__ void __launch_bounds__(256) tf32_pack_kernel(const float* __restrict__ b, int64_t ldb, int64_t rows,
+                                                        int64_t n, int64_t npad, unsigned char* __restrict__ out,
+                                                        int64_t lds) {
+    const int64_t groups = npad / 8, total = rows * groups;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / groups, f0 = (i - r * groups) * 8;
+        uint32_t w[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) w[k] = f0 + k < n ? to_tf32(b[r * ldb + f0 + k]) : 0u;
+        uint4 hi;
+        hi.x = (w[0] >> 16) | (w[1] & 0xFFFF0000u);
+        hi.y = (w[2] >> 16) | (w[3] & 0xFFFF0000u);
+        hi.z = (w[4] >> 16) | (w[5] & 0xFFFF0000u);
+        hi.w = (w[6] >> 16) | (w[7] & 0xFFFF0000u);
+        uint32_t lo = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) lo |= ((w[k] >> 13) & 7u) << (4 * k + 1);  // nibble k = e << 1
+        unsigned char* row = out + r * lds;
+        *reinterpret_cast<uint4*>(row + 2 * f0) = hi;
+        *reinterpret_cast<uint32_t*>(row + 2 * npad + f0 / 2) = lo;
+    }
+}
+
+// Operands of features 2j, 2j+1 from hi word h (pair j) and the nibble word
+// L (S = L << 4): the odd feature's nibble is the high nibble of L's byte j,
+// the even one's the high nibble of S's byte j.
+template <int J>
+__device__ __forceinline__ uint32_t tf32p_even(uint32_t h, uint32_t S) {
+    return __byte_perm(h, S, 0x1000 | ((4 + J) << 4));
+}
+template <int J>
+__device__ __forceinline__ uint32_t tf32p_odd(uint32_t h, uint32_t L) {
+    return __byte_perm(h, L, 0x3200 | ((4 + J) << 4));
+}
+
+template <int NCHUNK>
+struct Tf32PStep {
+    uint4 H[2][NCHUNK];     // loader slots: vector q + 4u, hi of features 64c + 8p .. +7
+    uint32_t L[2][NCHUNK];  // their nibbles
+    uint32_t b[2];          // sparse fragment: row g, vectors t, t+4
+};
+
+template <int NCHUNK>
+__device__ __forceinline__ void tf32p_issue(const SpmmArgs& a, const unsigned char* __restrict__ Bl,
+                                            const unsigned char* __restrict__ Ll, uint64_t vbase, uint32_t nvw,
+                                            uint32_t vend, uint32_t s, uint32_t g, uint32_t t, uint32_t q,
+                                            uint32_t colquad, uint32_t sub, Tf32PStep<NCHUNK>& st) {
+    const uint32_t c0 = __shfl_sync(0xffffffffu, colquad, 8 * sub + q);
+    const uint32_t c1 = __shfl_sync(0xffffffffu, colquad, 8 * sub + q + 4);
+    const float* fv = static_cast<const float*>(a.vals);
+    const uint64_t o0 = static_cast<uint64_t>(c0) * a.ldb, o1 = static_cast<uint64_t>(c1) * a.ldb;
+    float x0, x1;
+    if (s + 8 <= vend) {
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            st.H[0][c] = ld_gather_128(Bl + o0 + c * 128);
+            st.H[1][c] = ld_gather_128(Bl + o1 + c * 128);
+            st.L[0][c] = ld_gather_32(Ll + o0 + c * 32);
+            st.L[1][c] = ld_gather_32(Ll + o1 + c * 32);
+        }
+        const uint64_t off = vbase + 8ull * s + 4 * g + t;
+        x0 = __uint_as_float(ld_stream_u32(fv + off));
+        x1 = __uint_as_float(ld_stream_u32(fv + off + 32));
+    } else {
+        const bool ok0 = s + q < vend, ok1 = s + q + 4 < vend;
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c) {
+            st.H[0][c] = ok0 ? ld_gather_128(Bl + o0 + c * 128) : make_uint4(0, 0, 0, 0);
+            st.H[1][c] = ok1 ? ld_gather_128(Bl + o1 + c * 128) : make_uint4(0, 0, 0, 0);
+            st.L[0][c] = ok0 ? ld_gather_32(Ll + o0 + c * 32) : 0u;
+            st.L[1][c] = ok1 ? ld_gather_32(Ll + o1 + c * 32) : 0u;
+        }
+        x0 = s + t < vend ? tf32_val_general(fv, vbase, nvw, s + t, g) : 0.f;
+        x1 = s + t + 4 < vend ? tf32_val_general(fv, vbase, nvw, s + t + 4, g) : 0.f;
+    }
+    st.b[0] = to_tf32(x0);
+    st.b[1] = to_tf32(x1);
+}
+
+template <int NCHUNK>
+__device__ __forceinline__ void tf32p_compute(const Tf32PStep<NCHUNK>& st, float (&acc)[NCHUNK][4][4],
+                                              uint32_t src_lane) {
+#pragma unroll
+    for (int c = 0; c < NCHUNK; ++c) {
+        const uint4 x = shfl4(st.H[0][c], src_lane), y = shfl4(st.H[1][c], src_lane);
+        const uint32_t lx = __shfl_sync(0xffffffffu, st.L[0][c], src_lane);
+        const uint32_t ly = __shfl_sync(0xffffffffu, st.L[1][c], src_lane);
+        const uint32_t sx = lx << 4, sy = ly << 4;
+        mma_tf32_1688(acc[c][0], tf32p_even<0>(x.x, sx), tf32p_odd<0>(x.x, lx), tf32p_even<0>(y.x, sy),
+                      tf32p_odd<0>(y.x, ly), st.b[0], st.b[1]);
+        mma_tf32_1688(acc[c][1], tf32p_even<1>(x.y, sx), tf32p_odd<1>(x.y, lx), tf32p_even<1>(y.y, sy),
+                      tf32p_odd<1>(y.y, ly), st.b[0], st.b[1]);
+        mma_tf32_1688(acc[c][2], tf32p_even<2>(x.z, sx), tf32p_odd<2>(x.z, lx), tf32p_even<2>(y.z, sy),
+                      tf32p_odd<2>(y.z, ly), st.b[0], st.b[1]);
+        mma_tf32_1688(acc[c][3], tf32p_even<3>(x.w, sx), tf32p_odd<3>(x.w, lx), tf32p_even<3>(y.w, sy),
+                      tf32p_odd<3>(y.w, ly), st.b[0], st.b[1]);
+    }
+}
+
+#ifndef TCS_TF32P_BPS
+#define TCS_TF32P_BPS 4
+#endif
+// a.B = packed rows (tf32_pack_kernel), a.ldb = their stride in BYTES.
+template <int NCHUNK>
+__global__ void __launch_bounds__(kWarps * 32, TCS_TF32P_BPS) spmm_tf32p_kernel(const SpmmArgs a) {
+    constexpr int SLAB = NCHUNK * 64;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
+    const unsigned char* Bl = static_cast<const unsigned char*>(a.B) + 2 * feat0 + 16 * p;
+    const unsigned char* Ll = static_cast<const unsigned char*>(a.B) + 2 * a.ldp + feat0 / 2 + 4 * p;
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
+
+    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
+
+        float acc[NCHUNK][4][4];
+#pragma unroll
+        for (int c = 0; c < NCHUNK; ++c)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[c][j][0] = acc[c][j][1] = acc[c][j][2] = acc[c][j][3] = 0.f;
+
+        Tf32PStep<NCHUNK> sa, sb;
+        uint32_t s = it.vbeg;
+        if (s < vend) {
+            uint32_t s0 = s;
+            uint32_t cur = load_colpair(ci, s0, vend, lane);
+            uint32_t nxt = load_colpair(ci, s0 + 32, vend, lane);
+            tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s, g, t, q, cur, 0, sa);
+            for (;;) {
+                if (s + 8 < vend) {
+                    const uint32_t sub = (s + 8 - s0) >> 3;
+                    tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 8, g, t, q, sub < 4 ? cur : nxt, sub & 3, sb);
+                }
+                tf32p_compute(sa, acc, src_lane);
+                if (s + 8 >= vend) break;
+                if (s + 16 < vend) {
+                    uint32_t sub = (s + 16 - s0) >> 3;
+                    if (sub >= 4) {
+                        s0 += 32;
+                        cur = nxt;
+                        nxt = load_colpair(ci, s0 + 32, vend, lane);
+                        sub -= 4;
+                    }
+                    tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 16, g, t, q, cur, sub, sa);
+                }
+                tf32p_compute(sb, acc, src_lane);
+                s += 16;
+                if (s >= vend) break;
+            }
+        }
+        f16_epilogue<NCHUNK, 8>(a, it, acc, feat0, g, t);
+    }
+}
+
 // Sums the segments of split windows in segment order (deterministic).
 __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __restrict__ split, uint64_t n_split,
                                                          const float* __restrict__ partial, int64_t ldp, float* C,
@@ -732,14 +919,27 @@ __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __re
 }
 
 // Persistent launch: `bps` CTAs (4 warps each) per SM, shared by the
-// slabs; warps pull items from their slab's counter.
+// slabs; warps pull items from their slab's counter.  With a.counter ==
+// nullptr (direct dispatch, see direct_dispatch) one warp per item.
 template <typename K>
 void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name, int bps = 4) {
     const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
     const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * bps / std::max(1, slabs));
-    const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
+    const dim3 grid(static_cast<unsigned>(a.counter ? std::min(need, per_slab) : need), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
     TCS_LAUNCHED(name);
+}
+
+// Direct dispatch when every slab's item list fits in one wave of resident
+// warps at the smallest residency any SpMM kernel runs with (4 CTAs/SM):
+// then a persistent claim loop buys no balance and costs a counter
+// allocation, a memset and an atomic round trip per item.
+bool direct_dispatch(uint64_t n_items, int slabs) {
+#ifdef TCS_NO_DIRECT_DISPATCH
+    return false;
+#else
+    return (n_items + kWarps - 1) / kWarps <= std::max<uint64_t>(1, uint64_t(num_sms()) * 4 / std::max(1, slabs));
+#endif
 }
 
 }  // namespace
@@ -769,8 +969,11 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
     DBuf partial;
     if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
     const int slabs = static_cast<int>(npad / slab);
-    DBuf item_ctr(slabs * dev::kClaimBytes, s);
-    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
+    DBuf item_ctr;
+    if (!direct_dispatch(plan->n_items, slabs)) {
+        item_ctr = DBuf(slabs * dev::kClaimBytes, s);
+        TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
+    }
     SpmmArgs a{plan->items, plan->n_items, S->row_pointers, S->column_indices, S->values, bp, bld,
                c, ldc, S->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>(), 0, rowstat, scale};
     if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
@@ -825,7 +1028,15 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
 
         // Feature padding: 32 / 64 / multiple of 128.
         const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
-        const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : TCS_SPMM_SLAB_TF32;
+        int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : TCS_SPMM_SLAB_TF32;
+        // Small item lists (BASELINE C1: 512 windows) leave most warp slots
+        // idle and each warp walks its window serially: 32-feature slabs
+        // give every window npad/32 warps (the FP16 one with three gather
+        // steps in flight) while the whole launch still fits one wave.
+        if (npad > 32 && cfg->mapping != TCS_MAP_DIRECT && TCS_SMALL_SLAB32 &&
+            plan->n_items * uint64_t(npad / 32) <=
+                uint64_t(num_sms()) * kWarps * (A->precision == TCS_FP16 ? TCS_SPMM_DEEP_BPS : tf32_blocks(1)))
+            slab = 32;
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
         const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
@@ -867,7 +1078,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         }
         const int slabs = static_cast<int>(npad / slab);
         DBuf item_ctr;
-        if (!launched && plan->n_items) {
+        if (!launched && plan->n_items && !direct_dispatch(plan->n_items, slabs)) {
             item_ctr = DBuf(slabs * dev::kClaimBytes, s);
             TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
         }
@@ -900,6 +1111,22 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 else
                     vf32 ? launch(spmm_f16_kernel<1, 4, true>, a, slabs, s, "spmm_f16<32,f32v>", spmm_blocks(1, 4))
                          : launch(spmm_f16_kernel<1, 4, false>, a, slabs, s, "spmm_f16<32>", spmm_blocks(1, 4));
+            } else if (TCS_TF32_PACKED && slab >= 64 && !(cfg->flags & TCS_CFG_TF32_F32_GATHER)) {
+                // dense operand repacked to 2.5 B per feature (see tf32_pack_kernel)
+                const int64_t lds = npad * 5 / 2;
+                DBuf packed(static_cast<size_t>(std::max<int64_t>(1, b_rows)) * lds, s);
+                if (b_rows > 0) {
+                    const int64_t total = b_rows * (npad / 8);
+                    const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms()) * 16));
+                    tf32_pack_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(bp), bld, b_rows, n, npad,
+                                                          packed.as<unsigned char>(), lds);
+                    TCS_LAUNCHED("tf32_pack");
+                }
+                SpmmArgs ap = a;
+                ap.B = packed.p;
+                ap.ldb = lds;  // bytes
+                if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", TCS_TF32P_BPS);
+                else launch(spmm_tf32p_kernel<1>, ap, slabs, s, "spmm_tf32p<64>", TCS_TF32P_BPS);
             } else {
                 if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
                 else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>", tf32_blocks(2));

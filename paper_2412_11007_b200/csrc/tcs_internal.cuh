@@ -208,6 +208,12 @@ struct StripedClaim {
     uint32_t stripe, tried = 0;
     __device__ __forceinline__ StripedClaim() : stripe(blockIdx.x % NS) {}
     __device__ __forceinline__ bool get(uint32_t* counters, uint64_t n_items, uint32_t& idx) {
+        if (!counters) {  // direct dispatch: one item per warp, in warp order
+            if (tried) return false;
+            tried = NS;
+            idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+            return idx < n_items;
+        }
         while (tried < NS) {
             uint32_t k = 0;
             if ((threadIdx.x & 31u) == 0) k = atomicAdd(counters + stripe * kClaimStride, 1u);
@@ -229,6 +235,21 @@ __device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) 
     uint32_t i = 0;
     if (lane == 0) i = atomicAdd(counter, 1u);
     return __shfl_sync(0xffffffffu, i, 0);
+}
+// Direct dispatch (counter == nullptr): the launch holds one warp per work
+// item, so a warp's item is its global warp index along x and there is no
+// second one -- no counter to allocate and zero, and no atomic round trip
+// ahead of the first load.  Chosen by the host when the item list fits in
+// one wave of resident warps (the small configs, e.g. BASELINE C1/C2).
+__device__ __forceinline__ uint32_t first_item(uint32_t* counter, uint32_t lane) {
+    return counter ? next_item(counter, lane) : blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+}
+__device__ __forceinline__ uint32_t following_item(uint32_t* counter, uint32_t lane) {
+    return counter ? next_item(counter, lane) : 0xFFFFFFFFu;
+}
+// The claim counter of slab `slab` (nullptr stays nullptr: direct dispatch).
+__device__ __forceinline__ uint32_t* slab_counter(uint32_t* counters, uint32_t slab) {
+    return counters ? counters + static_cast<uint64_t>(slab) * (kClaimBytes / 4) : nullptr;
 }
 
 // RNE fp32 -> tf32 (cvt.rn.tf32.f32, sm_90+); matches the reference's
@@ -291,6 +312,11 @@ __device__ __forceinline__ uint4 ld_gather_128(const void* p) {
     asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
                  : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_gather_32(const void* p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
 __device__ __forceinline__ uint2 ld_gather_64(const void* p) {

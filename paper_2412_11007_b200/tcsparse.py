@@ -78,9 +78,11 @@ class KernelConfig:
     mapping: ThreadMapping = ThreadMapping.coalesced
     path: str = "auto"  # SpMM instruction path: auto | mma_sync | tcgen05 (tcs.h TCS_CFG_PATH_*)
     static_mask: bool = False  # SDDMM: mask values fixed across calls -> cached liveness bytes (TCS_CFG_STATIC_MASK)
+    tf32_f32_gather: bool = False  # TF32 SpMM ablation: gather f32 B, no 2.5-byte repack (TCS_CFG_TF32_F32_GATHER)
 
     def _c(self):
-        flags = {"auto": 0, "mma_sync": 1, "tcgen05": 2}[self.path] | (8 if self.static_mask else 0)
+        flags = ({"auto": 0, "mma_sync": 1, "tcgen05": 2}[self.path] | (8 if self.static_mask else 0)
+                 | (0x10 if self.tf32_f32_gather else 0))
         return _abi.tcs_kernel_config(int(self.precision), int(self.vector_height), int(self.mapping), flags)
 
 

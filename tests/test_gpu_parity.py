@@ -444,3 +444,30 @@ def test_tiny_mask_values_sampled_with_binary16_storage(golden):
     out = T.sddmm(ops, T.KernelConfig(T.Precision.fp16)).output.to_host()[2]
     assert cases.sha(out) == rec["sddmm_fp16"]["sha"]
     me.free()
+
+
+@pytest.mark.parametrize("n", [64, 96, 128, 200, 256])
+def test_tf32_packed_operand_equals_f32_gather(n):
+    """TF32 SpMM on the 2.5-byte repacked dense operand (hi 16 bits + a
+    nibble of the next mantissa bits) == the f32-gather kernel bit for bit,
+    on real values with full 10-bit TF32 mantissas, signed zeros, subnormals,
+    inf and large magnitudes; both within the north-star tolerance of the
+    oracle (the reference's sequential binary32 sums)."""
+    rng = np.random.default_rng(n)
+    m = O.generate_random_sparse(1203, 997, 0.05, 90 + n, real=True)
+    B = rng.standard_normal((m.cols, n)).astype(np.float32) * np.float32(3.7)
+    B[::97, ::5] = np.float32(1e-39)   # subnormal
+    B[::89, 1::7] = -0.0
+    B[::83, 2::11] = np.float32(3e30)
+    me = T.encode_mebcrs(dev_csr(m), T.Precision.tf32)
+    Bd = torch.from_numpy(B).cuda()
+    packed = T.spmm(me, Bd, T.KernelConfig(T.Precision.tf32)).output.cpu().numpy()
+    plain = T.spmm(me, Bd, T.KernelConfig(T.Precision.tf32, tf32_f32_gather=True)).output.cpu().numpy()
+    assert np.array_equal(packed.view(np.uint32), plain.view(np.uint32))
+    want = O.spmm_csr_rows(m, B, 1)
+    assert rel_l2(packed, want) < 1e-3
+    Bd[5, 3] = float("inf")
+    packed = T.spmm(me, Bd, T.KernelConfig(T.Precision.tf32)).output.cpu().numpy()
+    plain = T.spmm(me, Bd, T.KernelConfig(T.Precision.tf32, tf32_f32_gather=True)).output.cpu().numpy()
+    assert np.array_equal(packed.view(np.uint32), plain.view(np.uint32))
+    me.free()
