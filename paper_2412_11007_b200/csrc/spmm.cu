@@ -839,12 +839,20 @@ __device__ __forceinline__ void tf32p_compute(const Tf32PStep<NCHUNK>& st, float
     }
 }
 
-#ifndef TCS_TF32P_BPS
-#define TCS_TF32P_BPS 4
+// Resident CTAs per SM: 64-feature slabs (79 registers at 6, no spill)
+// need the warps to cover DRAM latency (C3 N=64: 4.53 ms at 4, 3.60 at 6);
+// 128-feature slabs keep their 126 registers (5 CTAs/SM spill: N=128 5.45
+// -> 5.98 ms).  profiles/r2_tf32_packed.txt
+#ifndef TCS_TF32P_BPS_WIDE
+#define TCS_TF32P_BPS_WIDE 4
 #endif
+#ifndef TCS_TF32P_BPS_NARROW
+#define TCS_TF32P_BPS_NARROW 6
+#endif
+constexpr int tf32p_blocks(int nchunk) { return nchunk == 1 ? TCS_TF32P_BPS_NARROW : TCS_TF32P_BPS_WIDE; }
 // a.B = packed rows (tf32_pack_kernel), a.ldb = their stride in BYTES.
 template <int NCHUNK>
-__global__ void __launch_bounds__(kWarps * 32, TCS_TF32P_BPS) spmm_tf32p_kernel(const SpmmArgs a) {
+__global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_kernel(const SpmmArgs a) {
     constexpr int SLAB = NCHUNK * 64;
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t g = lane >> 2, t = lane & 3;
@@ -1125,8 +1133,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 SpmmArgs ap = a;
                 ap.B = packed.p;
                 ap.ldb = lds;  // bytes
-                if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", TCS_TF32P_BPS);
-                else launch(spmm_tf32p_kernel<1>, ap, slabs, s, "spmm_tf32p<64>", TCS_TF32P_BPS);
+                if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", tf32p_blocks(2));
+                else launch(spmm_tf32p_kernel<1>, ap, slabs, s, "spmm_tf32p<64>", tf32p_blocks(1));
             } else {
                 if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
                 else if (slab == 64) launch(spmm_tf32_kernel<2>, a, slabs, s, "spmm_tf32<64>", tf32_blocks(2));

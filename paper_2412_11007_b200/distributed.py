@@ -73,10 +73,52 @@ def local_rows(row_ptr: torch.Tensor, col_idx: torch.Tensor, values: torch.Tenso
     return (row_ptr[shard.r0:shard.r1 + 1] - b).contiguous(), col_idx[b:e].contiguous(), values[b:e].contiguous()
 
 
+_DISTS: dict = {}
+
+
+def tcs_dist(group=None):
+    """The library's tcs_dist (include/tcs/tcs_dist.h) bound to torch's own
+    NCCL communicator of `group` (ProcessGroupNCCL._comm_ptr), or None when
+    the process group is not NCCL (gloo: the CPU tests).  Cached per group."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_backend(group) != "nccl":
+        return None
+    key = id(group)
+    if key not in _DISTS:
+        import ctypes as C
+
+        from . import _abi
+
+        pg = group if group is not None else dist.distributed_c10d._get_default_group()
+        ptr = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))._comm_ptr()
+        d = _abi.tcs_dist()
+        rc = _abi.load().tcs_dist_init(C.byref(d), C.c_void_p(ptr), 0)
+        if rc != 0:
+            raise RuntimeError(f"tcs_dist_init: {_abi.load().tcs_last_error().decode()}")
+        _DISTS[key] = d
+    return _DISTS[key]
+
+
 def broadcast_dense(B: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
-    """In-place broadcast of the dense operand (NCCL: one ring/tree over NVLink)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+    """In-place broadcast of the dense operand.  NCCL process groups: the
+    library's tcs_dist_broadcast on torch's communicator (one NCCL broadcast
+    over NVLink/NVSwitch, stream-ordered on the current stream); other
+    backends: torch.distributed.broadcast."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return B
+    d = tcs_dist(group) if B.is_cuda else None
+    if d is None:
         dist.broadcast(B, src=src, group=group)
+        return B
+    import ctypes as C
+
+    from . import _abi
+
+    root = dist.get_group_rank(group, src) if group is not None else src
+    lib = _abi.load()
+    rc = lib.tcs_dist_broadcast(C.byref(d), C.c_void_p(B.data_ptr()), B.numel() * B.element_size(), root,
+                                C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    if rc != 0:
+        raise RuntimeError(f"tcs_dist_broadcast: {lib.tcs_last_error().decode()}")
     return B
 
 
