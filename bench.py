@@ -180,7 +180,11 @@ def small_configs(device):
     import paper_2412_11007_b200.tcsparse as T
     from paper_2412_11007_b200 import _abi, graphs as G
 
-    rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real", device=device)
+    # the reference's own C1 inputs (generate.hpp restated in graphs.py;
+    # tests/test_graphs.py pins them to the golden hashes): seed 1, real mode
+    rows = cols = 4096
+    rp, ci, v = (torch.from_numpy(x.view("int32") if x.dtype.kind == "u" else x).to(device)
+                 for x in G.reference_random_csr(rows, cols, 16.0 / 4096, 1, "real"))
     nnz = ci.numel()
     csr = T.CsrMatrix(rows, cols, rp, ci, v)
     out = {}
@@ -219,7 +223,7 @@ def small_configs(device):
         W, nv = me.num_windows, me.num_vectors
         vw = 2 if dt == torch.float16 else 4
         vwA = 2 if me.value_dtype == _abi.TCS_DTYPE_F16 else 4
-        B = G.dense(cols, 128, 2, dtype=dt, device=device)
+        B = torch.from_numpy(G.reference_random_dense(cols, 128, 2, "real")).to(device=device, dtype=dt)
         C = torch.empty(rows, 128, device=device)
         us, g = timed(lambda: T.spmm(me, B, T.KernelConfig(prec), out=C))
         balg = bytes_alg_spmm(W, nv, rows, 128, vwA, vw)
@@ -228,8 +232,8 @@ def small_configs(device):
         out[f"c1_spmm_{pname}_roofline"] = {"bytes_alg": balg, "frac": round(balg / (us * 1e-6) / 1e9 / peak, 4),
                                             "us_at_peak": round(balg / (peak * 1e9) * 1e6, 2),
                                             "dram": _with_frac(dram_traffic(f"c1_{pname}_n128_g1"), us / 1e3)}
-        A = G.dense(rows, 32, 3, dtype=dt, device=device)
-        Bt = G.dense(cols, 32, 4, dtype=dt, device=device)
+        A = torch.from_numpy(G.reference_random_dense(rows, 32, 3, "real")).to(device=device, dtype=dt)
+        Bt = torch.from_numpy(G.reference_random_dense(cols, 32, 4, "real")).to(device=device, dtype=dt)
         ov = torch.empty(8 * me.num_vectors, device=device)
         ops = T.SddmmOperands(me, A, Bt)
         us2, g2 = timed(lambda: T.sddmm(ops, T.KernelConfig(prec), out_values=ov))
@@ -404,8 +408,10 @@ def build_graph(args, device):
         rows, cols, rp, ci, v = G.power_law_csr(G.C3_REDDIT, values="real", device=device)
         desc = "C3 SpMM on Reddit-shaped synthetic power-law graph (Chung-Lu alpha=1.2, hub cap 60x mean)"
     else:
-        rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real", device=device)
-        desc = "C1 SpMM on uniform-random 4096x4096 (16 nnz/row)"
+        rows = cols = 4096
+        rp, ci, v = (torch.from_numpy(x.view("int32") if x.dtype.kind == "u" else x).to(device)
+                     for x in G.reference_random_csr(rows, cols, 16.0 / 4096, 1, "real"))
+        desc = "C1 SpMM on the reference's generate_random_sparse_real(4096, 4096, 16/4096, seed 1)"
     return rows, cols, rp, ci, v, desc
 
 

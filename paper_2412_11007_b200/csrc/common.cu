@@ -162,9 +162,19 @@ __global__ void plan_count(const uint32_t* __restrict__ rp, uint64_t W, uint32_t
 // Split windows' segments first (they are the longest items and should be
 // dispatched first), then one item per remaining window (empty windows too:
 // their item writes the zero rows).
+// dcounts == nullptr: items from index 0 (the host read the counts).
+// Otherwise the pipelined plan: items end at `cap`, and dcounts receives the
+// claim start (cap - items) and the split-window count.
 __global__ void plan_fill(const uint32_t* __restrict__ rp, uint64_t W, uint32_t seg,
                           const uint32_t* __restrict__ slot_off, const uint32_t* __restrict__ split_off,
-                          uint32_t n_slots, WorkItem* __restrict__ items, SplitWindow* __restrict__ split) {
+                          WorkItem* __restrict__ items, SplitWindow* __restrict__ split, uint64_t cap,
+                          uint32_t* __restrict__ dcounts) {
+    const uint32_t n_slots = slot_off[W], n_split = split_off[W];
+    const uint64_t off = dcounts ? cap - (n_slots + (W - n_split)) : 0;
+    if (dcounts && blockIdx.x == 0 && threadIdx.x == 0) {
+        dcounts[0] = static_cast<uint32_t>(off);
+        dcounts[1] = n_split;
+    }
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W;
          w += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t nv = rp[w + 1] - rp[w];
@@ -172,12 +182,16 @@ __global__ void plan_fill(const uint32_t* __restrict__ rp, uint64_t W, uint32_t 
         if (nv > seg) {
             const uint32_t nseg = (nv + seg - 1) / seg;
             for (uint32_t i = 0; i < nseg; ++i)
-                items[so + i] = WorkItem{(uint32_t)w, i * seg, min(nv, (i + 1) * seg), so + i};
+                items[off + so + i] = WorkItem{(uint32_t)w, i * seg, min(nv, (i + 1) * seg), so + i};
             split[sp] = SplitWindow{(uint32_t)w, so, nseg, 0};
         } else {
-            items[n_slots + (w - sp)] = WorkItem{(uint32_t)w, 0, nv, kNoSlot};
+            items[off + n_slots + (w - sp)] = WorkItem{(uint32_t)w, 0, nv, kNoSlot};
         }
     }
+}
+
+__global__ void plan_blocks_out(const PlanTotals* __restrict__ tot, uint32_t* __restrict__ dcounts) {
+    *reinterpret_cast<unsigned long long*>(dcounts + 2) = tot->blocks_k;
 }
 }  // namespace
 
@@ -190,15 +204,19 @@ __global__ void plan_fill(const uint32_t* __restrict__ rp, uint64_t W, uint32_t 
 #define TCS_PLAN_MIN_SEG 256
 #endif
 
+// Segment length: enough items for ~64 per SM, bounded to [256, 16384]
+// vectors and a multiple of 16 (SpMM/SDDMM step granularity).
+static uint32_t plan_seg(uint64_t nv) {
+    const uint64_t target = std::max<uint64_t>(1, nv / (uint64_t(num_sms()) * 64));
+    return static_cast<uint32_t>(
+        std::min<uint64_t>(16384, std::max<uint64_t>(TCS_PLAN_MIN_SEG, (target + 15) / 16 * 16)));
+}
+
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16) {
     const uint64_t W = m->num_windows;
     const uint64_t nv = m->num_vectors;
-    // Segment length: enough items for ~64 per SM, bounded to [256, 16384]
-    // vectors and a multiple of 16 (SpMM/SDDMM step granularity).
-    const uint64_t target = std::max<uint64_t>(1, nv / (uint64_t(num_sms()) * 64));
-    const uint32_t seg = static_cast<uint32_t>(
-        std::min<uint64_t>(16384, std::max<uint64_t>(TCS_PLAN_MIN_SEG, (target + 15) / 16 * 16)));
+    const uint32_t seg = plan_seg(nv);
 
     DBuf nslot((W + 1) * 4, s), nsplit((W + 1) * 4, s), slot_off((W + 1) * 4, s), split_off((W + 1) * 4, s);
     DBuf tot(sizeof(PlanTotals), s);
@@ -227,7 +245,7 @@ Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t
     p->split = static_cast<SplitWindow*>(dalloc(std::max<uint64_t>(1, n_split) * sizeof(SplitWindow), s));
     if (W) {
         plan_fill<<<grid, 256, 0, s>>>(m->row_pointers, W, seg, slot_off.as<uint32_t>(), split_off.as<uint32_t>(),
-                                       n_slots, p->items, p->split);
+                                       p->items, p->split, 0, nullptr);
         TCS_LAUNCHED("plan_fill");
     }
     if (max_nv) *max_nv = h.max_nv;
@@ -236,8 +254,46 @@ Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t
     return p;
 }
 
+// The same work list without a host round trip (tcs_spmm_csr_host's
+// chunks): the segment length comes from the vector capacity nv_cap, the
+// arrays are sized for the worst case (a split window has more than seg
+// vectors, so split windows <= nv/seg and segments <= 2 nv/seg), and the
+// real counts stay on the device (Plan::dcounts).
+Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, cudaStream_t s) {
+    const uint64_t W = m->num_windows;
+    const uint32_t seg = plan_seg(nv_cap);
+    const uint64_t split_cap = std::min<uint64_t>(W, nv_cap / seg);
+    Plan* p = new Plan;
+    p->seg = seg;
+    p->n_split = split_cap;
+    p->n_slots = nv_cap / seg + split_cap;
+    p->n_items = p->n_slots + W;
+    p->items = static_cast<WorkItem*>(dalloc(std::max<uint64_t>(1, p->n_items) * sizeof(WorkItem), s));
+    p->split = static_cast<SplitWindow*>(dalloc(std::max<uint64_t>(1, split_cap) * sizeof(SplitWindow), s));
+    p->dcounts = static_cast<uint32_t*>(dalloc(16, s));
+    TCS_CUDA(cudaMemsetAsync(p->dcounts, 0, 16, s));
+    if (W) {
+        DBuf nslot((W + 1) * 4, s), nsplit((W + 1) * 4, s), slot_off((W + 1) * 4, s), split_off((W + 1) * 4, s);
+        DBuf tot(sizeof(PlanTotals), s);
+        TCS_CUDA(cudaMemsetAsync(tot.p, 0, sizeof(PlanTotals), s));
+        const int grid = static_cast<int>(std::min<uint64_t>((W + 255) / 256 + 1, 4096));
+        plan_count<<<grid, 256, 0, s>>>(m->row_pointers, W, seg, m->k, nslot.as<uint32_t>(), nsplit.as<uint32_t>(),
+                                        tot.as<PlanTotals>());
+        TCS_LAUNCHED("plan_count");
+        exclusive_scan_u32(nslot.as<uint32_t>(), slot_off.as<uint32_t>(), W, s);
+        exclusive_scan_u32(nsplit.as<uint32_t>(), split_off.as<uint32_t>(), W, s);
+        plan_fill<<<grid, 256, 0, s>>>(m->row_pointers, W, seg, slot_off.as<uint32_t>(), split_off.as<uint32_t>(),
+                                       p->items, p->split, p->n_items, p->dcounts);
+        TCS_LAUNCHED("plan_fill");
+        plan_blocks_out<<<1, 1, 0, s>>>(tot.as<PlanTotals>(), p->dcounts);
+        TCS_LAUNCHED("plan_blocks_out");
+    }
+    return p;
+}
+
 void free_plan(Plan* p, cudaStream_t s) {
     if (!p) return;
+    dfree(p->dcounts, s);
     dfree(p->items, s);
     dfree(p->split, s);
     dfree(p->live, s);

@@ -213,7 +213,9 @@ __device__ __forceinline__ void window_sort_rank(const uint32_t* __restrict__ cs
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint32_t c = ci[e0 + i];
         bad = max(bad, check_col<VH>(ci, e0, i, c, bnd, cols));
-        bufA[i] = (static_cast<uint64_t>(c) << 32) | i;
+        // an out-of-range column (reported via chk->bad) must not reach the
+        // output: the pipelined encode multiplies before the host sees the flag
+        bufA[i] = (static_cast<uint64_t>(c < cols ? c : 0u) << 32) | i;
     }
     if (bad) atomicMax(&chk->bad, bad);
     __syncthreads();
@@ -259,9 +261,10 @@ __global__ void __launch_bounds__(kSmallThreads) window_sort_small(const uint32_
                                                                    uint32_t* __restrict__ tmp_cols,
                                                                    uint32_t* __restrict__ rank,
                                                                    uint32_t* __restrict__ nv_out, CheckOut* chk,
-                                                                   const uint32_t* __restrict__ small, uint32_t n_small) {
+                                                                   const uint32_t* __restrict__ small) {
     __shared__ uint64_t bufA[kSmallCap];
     __shared__ uint64_t bufB[kSmallCap];
+    const uint32_t n_small = chk->n_small;  // class counts come from window_stats on the device
     for (uint32_t i = blockIdx.x; i < n_small; i += gridDim.x)  // small windows sit at the back of the list
         window_sort_rank<VH>(csr_rp, ci, rows, cols, small[W - 1 - i], bufA, bufB, tmp_cols, rank, nv_out, chk);
 }
@@ -279,9 +282,9 @@ __global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32
                                                                     uint64_t cols, uint32_t* __restrict__ tmp_cols,
                                                                     uint32_t* __restrict__ rank,
                                                                     uint32_t* __restrict__ nv_out, CheckOut* chk,
-                                                                    const uint32_t* __restrict__ tiny,
-                                                                    uint32_t n_tiny) {
+                                                                    const uint32_t* __restrict__ tiny) {
     constexpr uint32_t kPer = kTinyCap / 32;  // entries per lane
+    const uint32_t n_tiny = chk->n_tiny;
     __shared__ uint32_t s_col[kTinyWarps][kTinyCap];
     __shared__ uint32_t s_mrg[kTinyWarps][kTinyCap];
     __shared__ uint32_t s_rb[kTinyWarps][VH + 1];
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32
             const uint32_t j = lane + 32 * k;
             pos[k] = 0;
             if (j >= n) continue;
-            const uint32_t c = col[j];
+            const uint32_t c = col[j] < cols ? col[j] : 0u;  // out of range: flagged below, never output
             uint32_t r = 0;  // row of entry j: the last r with rb[r] <= j (empty rows share boundaries)
             bool row_start = false;
 #pragma unroll
@@ -313,8 +316,8 @@ __global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32
                 r = rb[q] <= j ? q : r;
                 row_start |= rb[q] == j;
             }
-            if (c >= cols) bad = max(bad, 3u);
-            if (!row_start && col[j - 1] >= c) bad = max(bad, 4u);
+            if (col[j] >= cols) bad = max(bad, 3u);
+            if (!row_start && col[j - 1] >= col[j]) bad = max(bad, 4u);
             uint32_t p = j - rb[r];
 #pragma unroll
             for (int q = 0; q < VH; ++q) {
@@ -368,9 +371,9 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                                                uint32_t* __restrict__ tmp_cols,
                                                                uint32_t* __restrict__ rank,
                                                                uint32_t* __restrict__ nv_out, CheckOut* chk,
-                                                               const uint32_t* __restrict__ big, uint32_t n_huge,
-                                                               uint32_t n_big) {
+                                                               const uint32_t* __restrict__ big) {
     extern __shared__ uint64_t smem_keys[];
+    const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
     for (uint32_t i = cta_next(&chk->next_sort_big); i < n_big; i = cta_next(&chk->next_sort_big)) {
         const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
@@ -395,9 +398,9 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
                                                                 uint32_t* __restrict__ tmp_cols,
                                                                 uint32_t* __restrict__ rank,
                                                                 uint32_t* __restrict__ nv_out, CheckOut* chk,
-                                                                const uint32_t* __restrict__ big, uint32_t n_huge,
-                                                                uint32_t n_big) {
+                                                                const uint32_t* __restrict__ big) {
     extern __shared__ uint32_t bm_smem[];
+    const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
     const uint32_t words = static_cast<uint32_t>((cols + 31) / 32);
     uint32_t* bm = bm_smem;
     uint32_t* pre = bm_smem + words;
@@ -474,9 +477,14 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ tmp_cols,
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
-                                                      const uint32_t* __restrict__ list, uint32_t n_front,
-                                                      uint32_t n_list, uint32_t* next, uint32_t* tiny) {
+                                                      const uint32_t* __restrict__ list, bool big, CheckOut* chk) {
     extern __shared__ uint4 tile_raw[];
+    // big list: huge windows from the front, medium from the back, dynamic
+    // queue; small list: tiny from the front, small from the back, fixed stride
+    const uint32_t n_front = big ? chk->n_huge : chk->n_tiny;
+    const uint32_t n_list = n_front + (big ? chk->n_medium : chk->n_small);
+    uint32_t* next = big ? &chk->next_scatter_big : nullptr;
+    uint32_t* tiny = &chk->tiny;
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
     __shared__ uint32_t rlo[VH + 1], rhi[VH], roff[VH + 1];  // this tile's entry range per row
@@ -596,8 +604,7 @@ __global__ void exact_live_build(const uint32_t* __restrict__ csr_rp, const floa
 // Value type V of a window_scatter instantiation (for the launch helper).
 template <typename V>
 V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
-                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, uint32_t,
-                           uint32_t, uint32_t*, uint32_t*));
+                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, CheckOut*));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
                          "column indices must be strictly ascending within a row"};
@@ -610,9 +617,18 @@ using namespace tcs;
 namespace tcs {
 namespace {
 
+// async_bad == nullptr: the API encode (exact sizes; validation errors are
+// thrown before it returns; three host round trips).  Otherwise the
+// pipelined encode of tcs_spmm_csr_host: no host round trip at all -- the
+// size-class kernels run on capacity grids and read their counts on the
+// device, the ME-BCRS arrays are allocated for nv <= nnz, the work list is
+// built with device-side counts (build_plan_async), and the validation code
+// lands in *async_bad (device) for the caller to check once at the end.
+// The handle's num_vectors is then a capacity, and SDDMM liveness extras
+// are not built (the pipeline only multiplies).
 template <int VH>
 void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                 tcs_stream_t stream) {
+                 tcs_stream_t stream, uint32_t* async_bad = nullptr) {
     {
         if (!csr || !out) fail(TCS_ERR_ARGUMENT, "null argument");
         if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
@@ -622,6 +638,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         if (!csr->row_ptr || (csr->nnz && (!csr->col_idx || !csr->values))) fail(TCS_ERR_ARGUMENT, "null CSR array");
         if (csr->nnz >= (1ull << 32)) fail(TCS_ERR_FORMAT, "nnz exceeds u32 row_ptr");
         cudaStream_t s = st(stream);
+        const bool async = async_bad != nullptr;
         const uint64_t rows = csr->rows, W = (rows + VH - 1) / VH, nnz = csr->nnz, cols = csr->cols;
         const uint32_t k = precision == TCS_FP16 ? 8 : 4;
         const int sms = num_sms();
@@ -657,7 +674,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             ~LiveCleanup() { dfree(p, s); }
         } live_cleanup{exact_live, s};
         if (W) {
-            // K0: row_ptr invariants + longest window
+            // K0: row_ptr invariants + size-class window lists
             DBuf chk(sizeof(CheckOut), s), small_list(W * 4, s), big_list(W * 4, s);
             TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
             const int g0 = static_cast<int>(std::min<uint64_t>((W + 255) / 256, uint64_t(sms) * 8));
@@ -665,33 +682,41 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                                                 small_list.as<uint32_t>(), big_list.as<uint32_t>());
             TCS_LAUNCHED("window_stats");
             CheckOut h{};
-            uint32_t ends[2] = {0, 0};
-            TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaMemcpyAsync(&ends[0], csr->row_ptr, 4, cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaMemcpyAsync(&ends[1], csr->row_ptr + rows, 4, cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaStreamSynchronize(s));
-            if (ends[0] != 0 || ends[1] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
-            if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
+            if (!async) {
+                uint32_t ends[2] = {0, 0};
+                TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaMemcpyAsync(&ends[0], csr->row_ptr, 4, cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaMemcpyAsync(&ends[1], csr->row_ptr + rows, 4, cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaStreamSynchronize(s));
+                if (ends[0] != 0 || ends[1] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
+                if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
+            } else {  // unknown: every class may hold every window
+                const uint32_t w32 = static_cast<uint32_t>(std::min<uint64_t>(W, 0xFFFFFFFFu));
+                h.n_tiny = h.n_small = h.n_medium = w32;
+                h.n_huge = 0;
+                h.max_window_entries = 0xFFFFFFFFu;
+            }
 
             DBuf tmp_cols(std::max<uint64_t>(1, nnz) * 4, s), rank(std::max<uint64_t>(1, nnz) * 4, s);
             DBuf nvw(W * 4, s);
+            // windows that fail validation are in no list: 0 vectors (the
+            // pipelined encode scans before anyone looks at the flag)
+            if (async) TCS_CUDA(cudaMemsetAsync(nvw.p, 0, W * 4, s));
             CheckOut* dchk = chk.as<CheckOut>();
-            const uint32_t n_big = h.n_medium + h.n_huge;
+            const uint64_t n_big = uint64_t(h.n_medium) + h.n_huge;
             if (h.n_tiny) {
                 const int gt = static_cast<int>(
                     std::min<uint64_t>((h.n_tiny + kTinyWarps - 1) / kTinyWarps, uint64_t(sms) * 8));
                 window_sort_warp<VH><<<gt, kTinyWarps * 32, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols,
                                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                                    nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>(),
-                                                                    h.n_tiny);
+                                                                    nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>());
                 TCS_LAUNCHED("window_sort_warp");
             }
             if (h.n_small) {
                 const int g1 = static_cast<int>(std::min<uint64_t>(h.n_small, uint64_t(sms) * 16));
                 window_sort_small<VH><<<g1, kSmallThreads, 0, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                               nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>(),
-                                                               h.n_small);
+                                                               nvw.as<uint32_t>(), dchk, small_list.as<uint32_t>());
                 TCS_LAUNCHED("window_sort_small");
             }
             if (n_big) {
@@ -704,8 +729,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                     const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
                     window_bitmap<VH><<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
-                                                                   nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>(),
-                                                                   h.n_huge, n_big);
+                                                                   nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_bitmap");
                 } else {
                     DBuf scratch;
@@ -717,20 +741,24 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                     window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
                                                                    rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk,
-                                                                   big_list.as<uint32_t>(), h.n_huge, n_big);
+                                                                   big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_sort_big");
                 }
             }
             exclusive_scan_u32(nvw.as<uint32_t>(), m.row_pointers, W, s);
-            TCS_CUDA(cudaMemcpyAsync(&nv, m.row_pointers + W, 4, cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-            TCS_CUDA(cudaStreamSynchronize(s));
-            if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
+            if (!async) {
+                TCS_CUDA(cudaMemcpyAsync(&nv, m.row_pointers + W, 4, cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaStreamSynchronize(s));
+                if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
+            } else {
+                nv = static_cast<uint32_t>(nnz);  // capacity: nv <= nnz
+            }
             m.num_vectors = nv;
             const size_t vw = value_dtype == TCS_DTYPE_F16 ? 2 : 4;
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
             m.values = dalloc(std::max<uint64_t>(1, uint64_t(VH) * nv) * vw, s);
-            auto scatter = [&](auto kern, int threads, uint32_t tile, const uint32_t* list, bool big, uint32_t n) {
+            auto scatter = [&](auto kern, int threads, uint32_t tile, const uint32_t* list, bool big, uint64_t n) {
                 if (!n) return;
                 const size_t tile_smem = size_t(tile) * 8 * vw;
                 const int per_sm = static_cast<int>(
@@ -741,22 +769,24 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                 kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
                                                     static_cast<decltype(kern_value_type(kern))*>(m.values), list,
-                                                    big ? h.n_huge : h.n_tiny, n,
-                                                    big ? &dchk->next_scatter_big : nullptr, &dchk->tiny);
+                                                    big, dchk);
             };
+            const uint64_t n_smalls = async ? W : uint64_t(h.n_tiny) + h.n_small;
             if (value_dtype == TCS_DTYPE_F16) {
                 scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
                         kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
                 scatter(window_scatter<VH, __half, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
-                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_tiny + h.n_small);
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, n_smalls);
             } else {
                 scatter(window_scatter<VH, float, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
                         kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
                 scatter(window_scatter<VH, float, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
-                        kScatterTileSmall, small_list.as<uint32_t>(), false, h.n_tiny + h.n_small);
+                        kScatterTileSmall, small_list.as<uint32_t>(), false, n_smalls);
             }
             TCS_LAUNCHED("window_scatter");
-            if (value_dtype == TCS_DTYPE_F16 && VH == 8) {
+            if (async) {
+                TCS_CUDA(cudaMemcpyAsync(async_bad, &dchk->bad, 4, cudaMemcpyDeviceToDevice, s));
+            } else if (value_dtype == TCS_DTYPE_F16 && VH == 8) {
                 uint32_t tiny = 0;
                 TCS_CUDA(cudaMemcpyAsync(&tiny, &dchk->tiny, 4, cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaStreamSynchronize(s));
@@ -773,9 +803,14 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             TCS_CUDA(cudaMemsetAsync(m.row_pointers, 0, 4, s));
             m.column_indices = static_cast<uint32_t*>(dalloc(4, s));
             m.values = dalloc(4, s);
+            if (async) TCS_CUDA(cudaMemsetAsync(async_bad, 0, 4, s));
         }
         cleanup.armed = false;
         *out = m;
+        if (async) {
+            out->plan = build_plan_async(out, nnz, s);
+            return;
+        }
         const tcs_status rc = tcs_mebcrs_prepare(out, stream);
         if (rc != TCS_OK) {
             const std::string msg = tcs_last_error();
@@ -792,6 +827,15 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
 }
 
 }  // namespace
+
+const char* encode_bad_msg(uint32_t code) { return kBadMsg[code < 5 ? code : 0]; }
+
+// The pipelined encode (see encode_impl): tcs_spmm_csr_host's chunks.
+void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
+                         cudaStream_t s, uint32_t* bad_dev) {
+    encode_impl<8>(csr, precision, value_dtype, out, reinterpret_cast<tcs_stream_t>(s), bad_dev);
+}
+
 }  // namespace tcs
 
 extern "C" tcs_status tcs_mebcrs_encode(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype,

@@ -52,7 +52,7 @@ struct SddmmArgs {
     uint32_t* counter;  // claim counters, dev::kClaimBytes (zeroed before launch)
     float dead;         // value of stored slots whose mask value is 0: 0, or -inf for the fused softmax
     const uint8_t* live;  // per-vector liveness bytes (bit r: row r's mask value != 0), mask mode kLive
-    uint32_t sub;         // warps per work item (direct dispatch only; 1 otherwise)
+    uint32_t sub;         // warps per work item (burst kernel only; 1 otherwise)
 };
 
 // Mask modes (template parameter MM): how a slot's liveness is read.
@@ -309,19 +309,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     extern __shared__ __align__(16) unsigned char ring_all[];  // per-warp ring, see below
     // persistent warps pulling work items (dev::StripedClaim)
     dev::StripedClaim<4> claim;
-    for (uint32_t idx; claim.get(a.counter, a.n_items * a.sub, idx);) {
-    // Direct dispatch of a small list may give an item `sub` warps: warp
-    // `part` takes the part-th run of 16-vector groups (each vector's output
-    // is independent, so the runs need no reduction).
-    const uint32_t part = idx % a.sub;
-    const WorkItem it = a.items[idx / a.sub];
+    for (uint32_t idx; claim.get(a.counter, a.n_items, idx);) {
+    const WorkItem it = a.items[idx];
     const uint32_t base = __ldg(a.rp + it.window);
     const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
     const uint32_t* ci = a.ci + base;
     const uint64_t vbase = 8ull * base;
-    const uint32_t run = ((it.vend - it.vbeg + a.sub - 1) / a.sub + 15u) & ~15u;
-    const uint32_t vbeg = min(it.vend, it.vbeg + part * run);
-    const uint32_t vend = min(it.vend, vbeg + run);
+    const uint32_t vbeg = it.vbeg, vend = it.vend;
     const uint64_t arow_i = 8ull * it.window + g;
     const bool arow_ok = arow_i < a.rows;
     const Elem* arow = static_cast<const Elem*>(a.A) + (arow_ok ? arow_i : 0) * a.lda;
@@ -502,11 +496,97 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
     }  // work items
 }
 
+// Small lists (BASELINE configs[1]: 512 windows of ~123 vectors) are
+// latency-bound: one wave, and the ring pipeline above never reaches steady
+// state.  Here `sub` warps share an item, each taking a run of its 16-vector
+// groups and issuing all loads of up to G groups at once, so the chain is
+// row pointers -> column indices (+ mask values) -> gathers -> MMA -> store.
+// Single pass only (FP16 K <= 32*NSC, TF32 K <= 16*NSC).  With no split
+// windows item i is window i (a.items == nullptr).
+constexpr int kBurstBlocks = 8;
+#ifndef TCS_BURST_WARPS
+#define TCS_BURST_WARPS 4
+#endif
+constexpr int kBW = TCS_BURST_WARPS;  // warps per CTA of the burst kernel
+template <bool TF32, int NSC, int MM, bool OF32, int G>
+__global__ void __launch_bounds__(kBW * 32, kBurstBlocks * kWarps / kBW) sddmm_burst(const SddmmArgs a) {
+    using Elem = typename std::conditional<TF32, float, __half>::type;
+    using Tile = typename std::conditional<TF32, Tf32Tile<NSC>, F16Tile<NSC>>::type;
+    constexpr uint32_t K = TF32 ? 4u : 8u;
+    constexpr int MW = kMaskWords<MM>;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kBW + (threadIdx.x >> 5);
+    const uint64_t idx = gw / a.sub;
+    const uint32_t part = static_cast<uint32_t>(gw % a.sub);
+    if (idx >= a.n_items) return;
+    WorkItem it;
+    uint32_t base, nvw;
+    if (a.items) {
+        it = a.items[idx];
+        base = __ldg(a.rp + it.window);
+        nvw = __ldg(a.rp + it.window + 1) - base;
+    } else {
+        base = __ldg(a.rp + idx);
+        nvw = __ldg(a.rp + idx + 1) - base;
+        it = WorkItem{static_cast<uint32_t>(idx), 0u, nvw, kNoSlot};
+    }
+    const uint64_t arow_i = 8ull * it.window + g;
+    const bool arow_ok = arow_i < a.rows;
+    uint4 ar0[NSC];
+    arow_load<NSC>(static_cast<const Elem*>(a.A) + (arow_ok ? arow_i : 0) * a.lda, arow_ok, 0, t, ar0);
+    const uint32_t* ci = a.ci + base;
+    const uint64_t vbase = 8ull * base;
+    const uint32_t run = ((it.vend - it.vbeg + a.sub - 1) / a.sub + 15u) & ~15u;
+    const uint32_t vbeg = min(it.vend, it.vbeg + part * run);
+    const uint32_t vend = min(it.vend, vbeg + run);
+    for (uint32_t s0 = vbeg; s0 < vend; s0 += 16 * G) {
+        uint32_t c[G][2];
+        Tile x[G];
+        uint32_t mk[G][MW];
+#pragma unroll
+        for (int d = 0; d < G; ++d) {
+            const uint32_t s = s0 + 16 * d;
+            c[d][0] = s + g < vend ? __ldg(ci + s + g) : 0u;
+            c[d][1] = s + g + 8 < vend ? __ldg(ci + s + g + 8) : 0u;
+            if (s < vend) mask_prefetch<K, MM>(a, vbase, nvw, vend, s, g, t, mk[d]);
+        }
+#pragma unroll
+        for (int d = 0; d < G; ++d) {
+            const uint32_t s = s0 + 16 * d;
+            if (s >= vend) continue;
+            if constexpr (TF32) tf32_tile_load<NSC>(a, c[d][0], s + g < vend, c[d][1], s + g + 8 < vend, 0, t, x[d]);
+            else f16_tile_load<NSC>(a, c[d][0], s + g < vend, c[d][1], s + g + 8 < vend, 0, t, x[d]);
+        }
+#pragma unroll
+        for (int d = 0; d < G; ++d) {
+            const uint32_t s = s0 + 16 * d;
+            if (s >= vend) continue;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            if constexpr (TF32) tf32_tile_mma<NSC>(x[d], ar0, acc);
+            else f16_tile_mma<NSC>(x[d], ar0, acc);
+            sddmm_store<K, OF32>(a.out, acc, slow_live<MM>(mk[d], s, vend, g, t), a.dead, vbase, nvw, vend, s, g, t);
+        }
+    }
+}
+
+template <bool TF32, int NSC, int G>
+void launch_sddmm_burst(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
+    const dim3 grid(static_cast<unsigned>((a.n_items * a.sub + kBW - 1) / kBW));
+    if (a.live) {
+        if (of32) sddmm_burst<TF32, NSC, kLive, true, G><<<grid, kBW * 32, 0, s>>>(a);
+        else sddmm_burst<TF32, NSC, kLive, false, G><<<grid, kBW * 32, 0, s>>>(a);
+    } else if (mf32 && of32) sddmm_burst<TF32, NSC, kMaskF32, true, G><<<grid, kBW * 32, 0, s>>>(a);
+    else if (mf32) sddmm_burst<TF32, NSC, kMaskF32, false, G><<<grid, kBW * 32, 0, s>>>(a);
+    else if (of32) sddmm_burst<TF32, NSC, kMaskF16, true, G><<<grid, kBW * 32, 0, s>>>(a);
+    else sddmm_burst<TF32, NSC, kMaskF16, false, G><<<grid, kBW * 32, 0, s>>>(a);
+    TCS_LAUNCHED(TF32 ? "sddmm_tf32_burst" : "sddmm_f16_burst");
+}
+
 template <bool TF32, int NSC>
 void launch_sddmm(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
-    const uint64_t need = (a.n_items * a.sub + kWarps - 1) / kWarps;
-    const dim3 grid(static_cast<unsigned>(a.counter ? std::min<uint64_t>(need, uint64_t(num_sms()) * kMinBlocks<NSC>)
-                                                    : need));
+    const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
+    const dim3 grid(static_cast<unsigned>(std::min<uint64_t>(need, uint64_t(num_sms()) * kMinBlocks<NSC>)));
     const size_t sm32 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF32>();
     const size_t sm16 = kWarps * kRing * ring_slot_bytes<NSC, kMaskF16>();
     const size_t sml = kWarps * kRing * ring_slot_bytes<NSC, kLive>();
@@ -648,28 +728,32 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     int64_t alda = 0, bldb = 0;
     const void* ap = prep(a, a_dtype, lda, a_rows, abuf, alda);
     const void* bp = prep(bt, bt_dtype, ldbt, bt_rows, bbuf, bldb);
-    // direct dispatch (one warp per item, no claim counter) when the items
-    // fit in one wave at the lowest residency of the SDDMM kernels
-    DBuf item_ctr;
-#ifndef TCS_NO_DIRECT_DISPATCH
-    const bool direct = (plan->n_items + kWarps - 1) / kWarps <= uint64_t(num_sms()) * 3;
-#else
-    const bool direct = false;
-#endif
-    if (!direct) {
-        item_ctr = DBuf(dev::kClaimBytes, s);
-        TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, dev::kClaimBytes, s));
-    }
-    // direct dispatch: as many warps per item as one wave holds (<= 8)
-    const uint32_t sub = direct ? static_cast<uint32_t>(std::max<uint64_t>(
-                                      1, std::min<uint64_t>(8, uint64_t(num_sms()) * 3 * kWarps /
-                                                                   std::max<uint64_t>(1, plan->n_items))))
-                                : 1u;
-    SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
-                   ap, alda, bp, bldb, out_values, mask->rows,
-                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr, sub};
     const bool mf32 = mask->value_dtype == TCS_DTYPE_F32, of32 = out_dtype == TCS_DTYPE_F32;
     if (!plan->n_items) return;
+#ifndef TCS_NO_BURST
+    // small single-pass lists: the burst kernel, `sub` warps per item, one wave
+    const uint64_t burst_cap = uint64_t(num_sms()) * kBurstBlocks * kWarps;
+    if (fpad == nsc * sc && nsc <= 2 && plan->seg <= 512 && plan->n_items <= burst_cap) {
+        SddmmArgs b{plan->n_split ? plan->items : nullptr, plan->n_items, mask->row_pointers, mask->column_indices,
+                    mask->values, ap, alda, bp, bldb, out_values, mask->rows, 1, mask->k, nullptr, dead, nullptr,
+                    static_cast<uint32_t>(std::min<uint64_t>(16, burst_cap / plan->n_items))};
+        if (static_mask) b.live = mask_liveness(mask, plan, s);
+        else if (const uint8_t* ex = plan->exact_for(mask->values)) b.live = ex;
+        if (tf32) {
+            if (nsc == 1) launch_sddmm_burst<true, 1, 2>(b, mf32, of32, s);
+            else launch_sddmm_burst<true, 2, 1>(b, mf32, of32, s);
+        } else {
+            if (nsc == 1) launch_sddmm_burst<false, 1, 2>(b, mf32, of32, s);
+            else launch_sddmm_burst<false, 2, 1>(b, mf32, of32, s);
+        }
+        return;
+    }
+#endif
+    DBuf item_ctr(dev::kClaimBytes, s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, dev::kClaimBytes, s));
+    SddmmArgs args{plan->items, plan->n_items, mask->row_pointers, mask->column_indices, mask->values,
+                   ap, alda, bp, bldb, out_values, mask->rows,
+                   static_cast<int>(fpad / (nsc * sc)), mask->k, item_ctr.as<uint32_t>(), dead, nullptr, 1};
     if (static_mask) args.live = mask_liveness(mask, plan, s);
     // binary16 values that lost a tiny nonzero: the exact bytes decide (ref :131)
     else if (const uint8_t* ex = plan->exact_for(mask->values)) args.live = ex;

@@ -93,10 +93,10 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 // each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
 // tail after the last upload (the last chunk's encode + SpMM + download).
 #ifndef TCS_E2E_MAX_CHUNKS
-#define TCS_E2E_MAX_CHUNKS 8
+#define TCS_E2E_MAX_CHUNKS 12
 #endif
-#ifndef TCS_E2E_TAIL_CUT
-#define TCS_E2E_TAIL_CUT 0
+#ifndef TCS_E2E_TAIL_HALVINGS
+#define TCS_E2E_TAIL_HALVINGS 3
 #endif
 #ifndef TCS_E2E_CHUNK_NNZ
 #define TCS_E2E_CHUNK_NNZ (1ull << 20)
@@ -108,6 +108,16 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 // feature slabs of 64 / 128; 0 = the f32-gather kernel everywhere.
 #ifndef TCS_TF32_PACKED
 #define TCS_TF32_PACKED 1
+#endif
+// Sparse-value stream of the packed TF32 kernel with an L2 evict-first
+// policy (A/B knob).
+#ifndef TCS_TF32P_EF
+#define TCS_TF32P_EF 0
+#endif
+// Packed TF32, 128-feature slabs: a lane's two nibble words (chunks 0, 1)
+// adjacent, one 8-byte load instead of two 4-byte loads per gathered row.
+#ifndef TCS_TF32P_LO64
+#define TCS_TF32P_LO64 1
 #endif
 #ifndef TCS_SMALL_SLAB32
 #define TCS_SMALL_SLAB32 1
@@ -343,7 +353,7 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -487,7 +497,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
     const unsigned short* Bl = static_cast<const unsigned short*>(a.B) + feat0 + g;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -672,7 +682,7 @@ __global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_ke
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -740,9 +750,11 @@ __global__ void __launch_bounds__(kWarps * 32, tf32_blocks(NCHUNK)) spmm_tf32_ke
 // after the shuffle from lane 8t+g, features 8g..8g+7 of vectors t and t+4.
 // M-tile j of a chunk holds feature 8g+2j in row g and 8g+2j+1 in row g+8,
 // so the accumulator layout is the FP16 kernel's (f16_epilogue<., 8>).
+// lo64: 128-feature slabs read both chunks' nibble words with one 8-byte
+// load, so within a slab the word of (chunk c, lane p) sits at 8p + 4c.
 __global__ void __launch_bounds__(256) tf32_pack_kernel(const float* __restrict__ b, int64_t ldb, int64_t rows,
                                                         int64_t n, int64_t npad, unsigned char* __restrict__ out,
-                                                        int64_t lds) {
+                                                        int64_t lds, bool lo64) {
     const int64_t groups = npad / 8, total = rows * groups;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = i / groups, f0 = (i - r * groups) * 8;
@@ -759,7 +771,8 @@ __global__ void __launch_bounds__(256) tf32_pack_kernel(const float* __restrict_
         for (int k = 0; k < 8; ++k) lo |= ((w[k] >> 13) & 7u) << (4 * k + 1);  // nibble k = e << 1
         unsigned char* row = out + r * lds;
         *reinterpret_cast<uint4*>(row + 2 * f0) = hi;
-        *reinterpret_cast<uint32_t*>(row + 2 * npad + f0 / 2) = lo;
+        const int64_t lo_off = lo64 ? (f0 / 128) * 64 + ((f0 % 64) / 8) * 8 + ((f0 % 128) / 64) * 4 : f0 / 2;
+        *reinterpret_cast<uint32_t*>(row + 2 * npad + lo_off) = lo;
     }
 }
 
@@ -797,20 +810,43 @@ __device__ __forceinline__ void tf32p_issue(const SpmmArgs& a, const unsigned ch
         for (int c = 0; c < NCHUNK; ++c) {
             st.H[0][c] = ld_gather_128(Bl + o0 + c * 128);
             st.H[1][c] = ld_gather_128(Bl + o1 + c * 128);
-            st.L[0][c] = ld_gather_32(Ll + o0 + c * 32);
-            st.L[1][c] = ld_gather_32(Ll + o1 + c * 32);
+        }
+        if constexpr (NCHUNK == 2 && TCS_TF32P_LO64) {
+            const uint2 l0 = ld_gather_64(Ll + o0), l1 = ld_gather_64(Ll + o1);
+            st.L[0][0] = l0.x; st.L[0][1] = l0.y; st.L[1][0] = l1.x; st.L[1][1] = l1.y;
+        } else {
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                st.L[0][c] = ld_gather_32(Ll + o0 + c * 32);
+                st.L[1][c] = ld_gather_32(Ll + o1 + c * 32);
+            }
         }
         const uint64_t off = vbase + 8ull * s + 4 * g + t;
+#if TCS_TF32P_EF
+        const uint64_t pol = l2_evict_first_policy();
+        x0 = __uint_as_float(ld_stream_ef_u32(fv + off, pol));
+        x1 = __uint_as_float(ld_stream_ef_u32(fv + off + 32, pol));
+#else
         x0 = __uint_as_float(ld_stream_u32(fv + off));
         x1 = __uint_as_float(ld_stream_u32(fv + off + 32));
+#endif
     } else {
         const bool ok0 = s + q < vend, ok1 = s + q + 4 < vend;
 #pragma unroll
         for (int c = 0; c < NCHUNK; ++c) {
             st.H[0][c] = ok0 ? ld_gather_128(Bl + o0 + c * 128) : make_uint4(0, 0, 0, 0);
             st.H[1][c] = ok1 ? ld_gather_128(Bl + o1 + c * 128) : make_uint4(0, 0, 0, 0);
-            st.L[0][c] = ok0 ? ld_gather_32(Ll + o0 + c * 32) : 0u;
-            st.L[1][c] = ok1 ? ld_gather_32(Ll + o1 + c * 32) : 0u;
+        }
+        if constexpr (NCHUNK == 2 && TCS_TF32P_LO64) {
+            const uint2 l0 = ok0 ? ld_gather_64(Ll + o0) : make_uint2(0, 0);
+            const uint2 l1 = ok1 ? ld_gather_64(Ll + o1) : make_uint2(0, 0);
+            st.L[0][0] = l0.x; st.L[0][1] = l0.y; st.L[1][0] = l1.x; st.L[1][1] = l1.y;
+        } else {
+#pragma unroll
+            for (int c = 0; c < NCHUNK; ++c) {
+                st.L[0][c] = ok0 ? ld_gather_32(Ll + o0 + c * 32) : 0u;
+                st.L[1][c] = ok1 ? ld_gather_32(Ll + o1 + c * 32) : 0u;
+            }
         }
         x0 = s + t < vend ? tf32_val_general(fv, vbase, nvw, s + t, g) : 0.f;
         x1 = s + t + 4 < vend ? tf32_val_general(fv, vbase, nvw, s + t + 4, g) : 0.f;
@@ -859,10 +895,11 @@ __global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_
     const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const unsigned char* Bl = static_cast<const unsigned char*>(a.B) + 2 * feat0 + 16 * p;
-    const unsigned char* Ll = static_cast<const unsigned char*>(a.B) + 2 * a.ldp + feat0 / 2 + 4 * p;
+    const unsigned char* Ll = static_cast<const unsigned char*>(a.B) + 2 * a.ldp + feat0 / 2 +
+                              (NCHUNK == 2 && TCS_TF32P_LO64 ? 8 : 4) * p;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
 
-    for (uint32_t idx = dev::first_item(counter, lane); idx < a.n_items; idx = dev::following_item(counter, lane)) {
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
         const uint32_t base = __ldg(a.rp + it.window);
         const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
@@ -909,10 +946,155 @@ __global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_
     }
 }
 
+// ------------------------------------------------ small lists: burst kernels
+//
+// BASELINE configs[0]/[1] (4096^2, 16 nnz/row: 512 windows of ~123 vectors)
+// are latency-bound: one wave of warps, each walking its window through a
+// chain of dependent loads (item -> row pointers -> column indices ->
+// gathers), and the software pipeline of the persistent kernels never
+// reaches steady state.  Here SPLIT warps of one CTA share an item, each
+// takes a contiguous run of its steps and issues ALL of that run's gathers
+// at once (up to MAXS steps per burst), so the chain is row pointers ->
+// column indices -> gathers -> MMA; the partial accumulators are summed in
+// shared memory in part order (deterministic).  With no split windows the
+// plan's item i is window i (a.items == nullptr): one load less.
+constexpr int kBurstRed = 8;  // accumulator floats per lane (32-feature slab)
+// Resident CTAs per SM of the split burst kernels (73 registers: 4 FP16
+// steps of 10 registers in flight without spilling; C1 at SPLIT = 2 is 4096
+// warps, one wave at 7 x 4 x 148).
+constexpr int kBurstBlocks = 7;
+// Warps per CTA of the burst kernels (A/B knob: fewer, larger CTAs launch
+// faster; the per-SM warp budget is the same).
+#ifndef TCS_BURST_WARPS
+#define TCS_BURST_WARPS 4
+#endif
+constexpr int kBW = TCS_BURST_WARPS;
+#ifndef TCS_BURST_FORCE_SPLIT
+#define TCS_BURST_FORCE_SPLIT 0
+#endif
+
+__device__ __forceinline__ WorkItem burst_item(const SpmmArgs& a, uint64_t idx, uint32_t& base, uint32_t& nvw) {
+    WorkItem it;
+    if (a.items) {
+        it = a.items[idx];
+        base = __ldg(a.rp + it.window);
+        nvw = __ldg(a.rp + it.window + 1) - base;
+    } else {
+        base = __ldg(a.rp + idx);
+        nvw = __ldg(a.rp + idx + 1) - base;
+        it = WorkItem{static_cast<uint32_t>(idx), 0u, nvw, kNoSlot};
+    }
+    return it;
+}
+
+// Sums the SPLIT warps' accumulators of each item into part 0 (fixed order).
+template <int SPLIT>
+__device__ __forceinline__ void burst_reduce(float (&acc)[kBurstRed], uint32_t warp, uint32_t lane) {
+    if constexpr (SPLIT > 1) {
+        __shared__ float red[kBW][kBurstRed][32];
+        if (warp % SPLIT)
+#pragma unroll
+            for (int j = 0; j < kBurstRed; ++j) red[warp][j][lane] = acc[j];
+        __syncthreads();
+        if (warp % SPLIT == 0)
+#pragma unroll
+            for (int p = 1; p < SPLIT; ++p)
+#pragma unroll
+                for (int j = 0; j < kBurstRed; ++j) acc[j] += red[warp + p][j][lane];
+    }
+}
+
+template <bool VF32, int SPLIT, int MAXS, bool SMX = false>
+__global__ void __launch_bounds__(kBW * 32, (SPLIT > 1 ? kBurstBlocks : 4) * kWarps / kBW) spmm_f16_burst(const SpmmArgs a) {
+    static_assert(kBW % SPLIT == 0, "parts of an item share a CTA");
+    constexpr int FPL = 4;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t g = lane >> 2, t = lane & 3, q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const uint32_t part = warp % SPLIT;
+    const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * kBW + warp) / SPLIT;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * 32;
+    const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
+    const bool active = idx < a.n_items;  // every warp reaches the reduction barrier
+    float acc[1][FPL / 2][4] = {};
+    WorkItem it{};
+    if (active) {
+        uint32_t base, nvw;
+        it = burst_item(a, idx, base, nvw);
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        float sm = 0.f, sinv = 0.f;  // softmax statistics of this lane's row g (SMX)
+        if constexpr (SMX) {
+            const float2 st2 = a.rowstat[8ull * it.window + g];
+            sm = st2.x;
+            sinv = st2.y;
+        }
+        const uint32_t steps = (it.vend - it.vbeg + 15) / 16, per = (steps + SPLIT - 1) / SPLIT;
+        const uint32_t vend = min(it.vend, it.vbeg + 16 * per * (part + 1));
+        for (uint32_t s0 = it.vbeg + 16 * per * part; s0 < vend; s0 += 16 * MAXS) {
+            uint32_t cp[(MAXS + 1) / 2];
+#pragma unroll
+            for (int j = 0; j < (MAXS + 1) / 2; ++j) cp[j] = load_colpair(ci, s0 + 32 * j, vend, lane);
+            F16Step<1, FPL, VF32> st[MAXS];
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+                if (s0 + 16 * i < vend)
+                    f16_issue<1, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s0 + 16 * i, g, t, q, cp[i / 2], i & 1,
+                                                 st[i]);
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+                if (s0 + 16 * i < vend) f16_compute<1, FPL, VF32, SMX>(st[i], acc, src_lane, a.scale, sm, sinv);
+        }
+    }
+    burst_reduce<SPLIT>(reinterpret_cast<float(&)[kBurstRed]>(acc), warp, lane);
+    if (active && part == 0) f16_epilogue<1, FPL>(a, it, acc, feat0, g, t);
+}
+
+// TF32 (f32 gathers, 8-vector steps; the accumulator layout of
+// tf32_epilogue<1>).
+template <int SPLIT, int MAXS>
+__global__ void __launch_bounds__(kBW * 32, (SPLIT > 1 ? kBurstBlocks : 4) * kWarps / kBW) spmm_tf32_burst(const SpmmArgs a) {
+    static_assert(kBW % SPLIT == 0, "parts of an item share a CTA");
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t g = lane >> 2, t = lane & 3, q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const uint32_t part = warp % SPLIT;
+    const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * kBW + warp) / SPLIT;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * 32;
+    const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
+    const bool active = idx < a.n_items;
+    float acc[1][2][4] = {};
+    WorkItem it{};
+    if (active) {
+        uint32_t base, nvw;
+        it = burst_item(a, idx, base, nvw);
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t steps = (it.vend - it.vbeg + 7) / 8, per = (steps + SPLIT - 1) / SPLIT;
+        const uint32_t vend = min(it.vend, it.vbeg + 8 * per * (part + 1));
+        for (uint32_t s0 = it.vbeg + 8 * per * part; s0 < vend; s0 += 8 * MAXS) {
+            uint32_t cq[(MAXS + 3) / 4];
+#pragma unroll
+            for (int j = 0; j < (MAXS + 3) / 4; ++j) cq[j] = load_colpair(ci, s0 + 32 * j, vend, lane);
+            Tf32Step<1> st[MAXS];
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+                if (s0 + 8 * i < vend)
+                    tf32_issue<1>(a, Bl, vbase, nvw, vend, s0 + 8 * i, g, t, q, cq[i / 4], i & 3, st[i]);
+#pragma unroll
+            for (int i = 0; i < MAXS; ++i)
+                if (s0 + 8 * i < vend) tf32_compute<1>(st[i], acc, src_lane);
+        }
+    }
+    burst_reduce<SPLIT>(reinterpret_cast<float(&)[kBurstRed]>(acc), warp, lane);
+    if (active && part == 0) tf32_epilogue<1>(a, it, acc, feat0, g, t);
+}
+
 // Sums the segments of split windows in segment order (deterministic).
+// n_split_dev (pipelined plans): the real count, on the device.
 __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __restrict__ split, uint64_t n_split,
                                                          const float* __restrict__ partial, int64_t ldp, float* C,
-                                                         int64_t ldc, uint64_t rows, int64_t N) {
+                                                         int64_t ldc, uint64_t rows, int64_t N,
+                                                         const uint32_t* __restrict__ n_split_dev = nullptr) {
+    if (n_split_dev) n_split = *n_split_dev;
     for (uint64_t sw = blockIdx.x; sw < n_split; sw += gridDim.x) {
         const SplitWindow x = split[sw];
         for (int64_t e = threadIdx.x; e < 8 * N; e += blockDim.x) {
@@ -926,28 +1108,58 @@ __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __re
     }
 }
 
+// Claim counters of a pipelined plan: every slab starts at the first real
+// item (Plan::dcounts[0]; the list's real items end at its capacity).
+__global__ void claim_init(uint32_t* __restrict__ counters, int slabs, const uint32_t* __restrict__ dcounts) {
+    for (int i = threadIdx.x; i < slabs * int(dev::kClaimBytes / 4); i += blockDim.x)
+        counters[i] = i % int(dev::kClaimBytes / 4) == 0 ? dcounts[0] : 0u;
+}
+
 // Persistent launch: `bps` CTAs (4 warps each) per SM, shared by the
-// slabs; warps pull items from their slab's counter.  With a.counter ==
-// nullptr (direct dispatch, see direct_dispatch) one warp per item.
+// slabs; warps pull items from their slab's counter.
 template <typename K>
 void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* name, int bps = 4) {
     const uint64_t need = (a.n_items + kWarps - 1) / kWarps;
     const uint64_t per_slab = std::max<uint64_t>(1, uint64_t(num_sms()) * bps / std::max(1, slabs));
-    const dim3 grid(static_cast<unsigned>(a.counter ? std::min(need, per_slab) : need), slabs);
+    const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
     TCS_LAUNCHED(name);
 }
 
-// Direct dispatch when every slab's item list fits in one wave of resident
-// warps at the smallest residency any SpMM kernel runs with (4 CTAs/SM):
-// then a persistent claim loop buys no balance and costs a counter
-// allocation, a memset and an atomic round trip per item.
-bool direct_dispatch(uint64_t n_items, int slabs) {
-#ifdef TCS_NO_DIRECT_DISPATCH
-    return false;
-#else
-    return (n_items + kWarps - 1) / kWarps <= std::max<uint64_t>(1, uint64_t(num_sms()) * 4 / std::max(1, slabs));
+// Feature slab of one warp: 32 / 64 / 128.  Small item lists (BASELINE C1:
+// 512 windows) leave most warp slots idle and each warp walks its window
+// serially: 32-feature slabs give every window npad/32 warps (and the burst
+// kernels below) while the whole launch still fits one wave.
+int feature_slab(const Plan* plan, int64_t npad, tcs_precision prec, bool direct_map) {
+    int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : prec == TCS_FP16 ? TCS_SPMM_SLAB_F16 : TCS_SPMM_SLAB_TF32;
+    if (npad > 32 && !direct_map && TCS_SMALL_SLAB32 && !plan->dcounts &&
+        plan->n_items * uint64_t(npad / 32) <=
+            uint64_t(num_sms()) * kWarps * (prec == TCS_FP16 ? TCS_SPMM_DEEP_BPS : tf32_blocks(1)))
+        slab = 32;
+    return slab;
+}
+
+// Burst kernels (above) for small lists: warps per item so that every
+// (item, 32-feature slab) pair fits one wave; 0 = not a burst case.  Items
+// are at most plan.seg vectors, so seg bounds the bursts per part.
+#ifndef TCS_NO_BURST
+#define TCS_NO_BURST 0
 #endif
+int burst_split(const Plan* plan, int slabs) {
+    if (TCS_NO_BURST || plan->seg > 512) return 0;
+    if (TCS_BURST_FORCE_SPLIT) return TCS_BURST_FORCE_SPLIT;
+    const uint64_t w = plan->n_items * uint64_t(slabs), sms = uint64_t(num_sms());
+    if (w * 4 <= sms * kBurstBlocks * kWarps) return 4;
+    if (w * 2 <= sms * kBurstBlocks * kWarps) return 2;
+    if (w <= sms * 4 * kWarps) return 1;
+    return 0;
+}
+
+template <typename K>
+void launch_burst(K kernel, const SpmmArgs& a, int split, int slabs, cudaStream_t s, const char* name) {
+    const dim3 grid(static_cast<unsigned>((a.n_items * split + kBW - 1) / kBW), slabs);
+    kernel<<<grid, kBW * 32, 0, s>>>(a);
+    TCS_LAUNCHED(name);
 }
 
 }  // namespace
@@ -962,7 +1174,9 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
                       cudaStream_t s) {
     if (n == 0 || S->rows == 0 || !plan->n_items) return;
     const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
-    const int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : 128;
+    // the kernel choice of tcs_spmm on the same list (so the result equals
+    // tcs_spmm on the materialised P bit for bit)
+    const int slab = feature_slab(plan, npad, TCS_FP16, false);
     const bool direct = b_dtype == TCS_DTYPE_F16 && ldb % 8 == 0 && ldb >= npad &&
                         (reinterpret_cast<uintptr_t>(b) & 15) == 0;
     DBuf bpad;
@@ -977,11 +1191,15 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
     DBuf partial;
     if (plan->n_slots) partial = DBuf(plan->n_slots * 8 * npad * sizeof(float), s);
     const int slabs = static_cast<int>(npad / slab);
-    DBuf item_ctr;
-    if (!direct_dispatch(plan->n_items, slabs)) {
-        item_ctr = DBuf(slabs * dev::kClaimBytes, s);
-        TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
-    }
+    if (const int split = slab == 32 ? burst_split(plan, slabs) : 0) {
+        SpmmArgs a{plan->n_split ? plan->items : nullptr, plan->n_items, S->row_pointers, S->column_indices,
+                   S->values, bp, bld, c, ldc, S->rows, n, partial.as<float>(), npad, nullptr, 0, rowstat, scale};
+        if (split == 4) launch_burst(spmm_f16_burst<false, 4, 2, true>, a, 4, slabs, s, "spmm_f16_softmax_burst<4>");
+        else if (split == 2) launch_burst(spmm_f16_burst<false, 2, 4, true>, a, 2, slabs, s, "spmm_f16_softmax_burst<2>");
+        else launch_burst(spmm_f16_burst<false, 1, 8, true>, a, 1, slabs, s, "spmm_f16_softmax_burst<1>");
+    } else {
+    DBuf item_ctr(slabs * dev::kClaimBytes, s);
+    TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
     SpmmArgs a{plan->items, plan->n_items, S->row_pointers, S->column_indices, S->values, bp, bld,
                c, ldc, S->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>(), 0, rowstat, scale};
     if (slab == 128) launch(spmm_f16_kernel<2, 8, false, true>, a, slabs, s, "spmm_f16_softmax<128>");
@@ -990,6 +1208,7 @@ void spmm_f16_softmax(const tcs_mebcrs* S, const Plan* plan, const float2* rowst
         launch(spmm_f16_kernel_deep<1, 4, false, true, TCS_SPMM_DEEP_BPS>, a, slabs, s, "spmm_f16_softmax_deep<32>",
                TCS_SPMM_DEEP_BPS);
     else launch(spmm_f16_kernel<1, 4, false, true>, a, slabs, s, "spmm_f16_softmax<32>", spmm_blocks(1, 4));
+    }
     if (plan->n_split) {
         const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
         spmm_reduce_split<<<grid, 256, 0, s>>>(plan->split, plan->n_split, partial.as<float>(), npad, c, ldc, S->rows,
@@ -1036,15 +1255,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
 
         // Feature padding: 32 / 64 / multiple of 128.
         const int64_t npad = n <= 32 ? 32 : n <= 64 ? 64 : (n + 127) / 128 * 128;
-        int slab = npad <= 32 ? 32 : npad <= 64 ? 64 : A->precision == TCS_FP16 ? TCS_SPMM_SLAB_F16 : TCS_SPMM_SLAB_TF32;
-        // Small item lists (BASELINE C1: 512 windows) leave most warp slots
-        // idle and each warp walks its window serially: 32-feature slabs
-        // give every window npad/32 warps (the FP16 one with three gather
-        // steps in flight) while the whole launch still fits one wave.
-        if (npad > 32 && cfg->mapping != TCS_MAP_DIRECT && TCS_SMALL_SLAB32 &&
-            plan->n_items * uint64_t(npad / 32) <=
-                uint64_t(num_sms()) * kWarps * (A->precision == TCS_FP16 ? TCS_SPMM_DEEP_BPS : tf32_blocks(1)))
-            slab = 32;
+        const int slab = feature_slab(plan, npad, A->precision, cfg->mapping == TCS_MAP_DIRECT);
         const tcs_dtype need = A->precision == TCS_FP16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32;
         const int64_t align_elems = need == TCS_DTYPE_F16 ? 8 : 4;
         const bool aligned = (reinterpret_cast<uintptr_t>(b) & 15) == 0;
@@ -1085,14 +1296,21 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
             bld = npad;
         }
         const int slabs = static_cast<int>(npad / slab);
+        const bool direct_map = cfg->mapping == TCS_MAP_DIRECT && A->precision == TCS_FP16;
+        const int burst = plan->n_items && !launched && !direct_map && slab == 32 && !plan->dcounts
+                              ? burst_split(plan, slabs) : 0;
         DBuf item_ctr;
-        if (!launched && plan->n_items && !direct_dispatch(plan->n_items, slabs)) {
+        if (!launched && !burst && plan->n_items) {
             item_ctr = DBuf(slabs * dev::kClaimBytes, s);
-            TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
+            if (plan->dcounts) {
+                claim_init<<<1, 256, 0, s>>>(item_ctr.as<uint32_t>(), slabs, plan->dcounts);
+                TCS_LAUNCHED("claim_init");
+            } else {
+                TCS_CUDA(cudaMemsetAsync(item_ctr.p, 0, slabs * dev::kClaimBytes, s));
+            }
         }
         SpmmArgs a{plan->items, plan->n_items, A->row_pointers, A->column_indices, A->values, bp, bld,
                    c, ldc, A->rows, n, partial.as<float>(), npad, item_ctr.as<uint32_t>()};
-        const bool direct_map = cfg->mapping == TCS_MAP_DIRECT && A->precision == TCS_FP16;
         if (plan->n_items && !launched && direct_map) {  // ablation: the paper's direct thread mapping
             const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
             if (slab == 128)
@@ -1104,6 +1322,26 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
             else
                 vf32 ? launch(spmm_f16_direct_kernel<2, true>, a, slabs, s, "spmm_f16_direct<32,f32v>")
                      : launch(spmm_f16_direct_kernel<2, false>, a, slabs, s, "spmm_f16_direct<32>");
+        } else if (const int split = burst) {
+            SpmmArgs ab = a;
+            if (!plan->n_split) ab.items = nullptr;  // item i is window i
+            ab.counter = nullptr;
+            if (A->precision == TCS_FP16) {
+                const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
+                if (split == 4)
+                    vf32 ? launch_burst(spmm_f16_burst<true, 4, 2>, ab, 4, slabs, s, "spmm_f16_burst<4,f32v>")
+                         : launch_burst(spmm_f16_burst<false, 4, 2>, ab, 4, slabs, s, "spmm_f16_burst<4>");
+                else if (split == 2)
+                    vf32 ? launch_burst(spmm_f16_burst<true, 2, 4>, ab, 2, slabs, s, "spmm_f16_burst<2,f32v>")
+                         : launch_burst(spmm_f16_burst<false, 2, 4>, ab, 2, slabs, s, "spmm_f16_burst<2>");
+                else
+                    vf32 ? launch_burst(spmm_f16_burst<true, 1, 8>, ab, 1, slabs, s, "spmm_f16_burst<1,f32v>")
+                         : launch_burst(spmm_f16_burst<false, 1, 8>, ab, 1, slabs, s, "spmm_f16_burst<1>");
+            } else {
+                if (split == 4) launch_burst(spmm_tf32_burst<4, 4>, ab, 4, slabs, s, "spmm_tf32_burst<4>");
+                else if (split == 2) launch_burst(spmm_tf32_burst<2, 4>, ab, 2, slabs, s, "spmm_tf32_burst<2>");
+                else launch_burst(spmm_tf32_burst<1, 8>, ab, 1, slabs, s, "spmm_tf32_burst<1>");
+            }
         } else if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
@@ -1127,7 +1365,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                     const int64_t total = b_rows * (npad / 8);
                     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms()) * 16));
                     tf32_pack_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(bp), bld, b_rows, n, npad,
-                                                          packed.as<unsigned char>(), lds);
+                                                          packed.as<unsigned char>(), lds,
+                                                          slab == 128 && TCS_TF32P_LO64);
                     TCS_LAUNCHED("tf32_pack");
                 }
                 SpmmArgs ap = a;
@@ -1144,7 +1383,7 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         if (plan->n_split) {
             const int grid = static_cast<int>(std::min<uint64_t>(plan->n_split, uint64_t(num_sms()) * 8));
             spmm_reduce_split<<<grid, 256, 0, s>>>(plan->split, plan->n_split, partial.as<float>(), npad, c, ldc,
-                                                  A->rows, n);
+                                                  A->rows, n, plan->dcounts ? plan->dcounts + 1 : nullptr);
             TCS_LAUNCHED("spmm_reduce_split");
         }
         if (counters) counters->mma_invocations = A->num_blocks * ((n + 15) / 16);  // ref analysis.hpp:34-38
@@ -1255,18 +1494,28 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         const int64_t b_rows = static_cast<int64_t>(host_csr->cols);
         const uint32_t* hrp = host_csr->row_ptr;
         if (hrp[0] != 0 || hrp[rows] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
+        // row_ptr is validated here, on the host (the chunk cuts and copies
+        // depend on it); column indices are validated by the chunk encodes
+        for (uint64_t r = 0; r < rows; ++r)
+            if (hrp[r + 1] < hrp[r]) fail(TCS_ERR_FORMAT, "row_ptr must be nondecreasing");
         if (rows == 0 || n == 0) return;
 
-        // chunk cut points: windows at nnz quantiles (host row_ptr)
-        // Equal chunks; with TCS_E2E_TAIL_CUT the last one is cut again at
-        // 3/4 (only the work after the last upload is exposed).
-        const uint64_t neq = std::max<uint64_t>(
+        // Chunk cut points: windows at nnz quantiles (host row_ptr).  The
+        // encode of a chunk needs no host round trip (encode_mebcrs_async),
+        // so every chunk's work is queued up front and runs as soon as its
+        // upload lands; only the last chunk's encode + SpMM + download is
+        // exposed after the last upload, so the last unit of work is cut
+        // into halves: 1/2, 1/4, ..., 1/2^T, 1/2^T of a unit.
+        const uint64_t units = std::max<uint64_t>(
             1, std::min<uint64_t>({TCS_E2E_MAX_CHUNKS, W, nnz / (TCS_E2E_CHUNK_NNZ) + 1}));
-        const bool tail_cut = TCS_E2E_TAIL_CUT && neq > 1 && W > neq;
-        const uint64_t nchunks = neq + (tail_cut ? 1 : 0);
+        const int tail = units > 1 && W > units + TCS_E2E_TAIL_HALVINGS ? TCS_E2E_TAIL_HALVINGS : 0;
+        std::vector<double> frac;  // cumulative nnz fraction at each cut
+        for (uint64_t i = 1; i < units; ++i) frac.push_back(double(i) / units);
+        for (int h = 1; h <= tail; ++h) frac.push_back((units - std::ldexp(1.0, -h)) / units);
+        const uint64_t nchunks = frac.size() + 1;
         std::vector<uint64_t> wcut(nchunks + 1, 0);
         for (uint64_t i = 1; i < nchunks; ++i) {
-            const uint64_t target = i < neq ? nnz * i / neq : nnz - nnz / (4 * neq);
+            const uint64_t target = static_cast<uint64_t>(frac[i - 1] * double(nnz));
             uint64_t lo = wcut[i - 1], hi = W;  // first window whose start >= target
             while (lo < hi) {
                 const uint64_t mid = (lo + hi) / 2;
@@ -1284,6 +1533,10 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             d_c(rows * n * 4, s);
         DBuf d_b16;
         if (f16) d_b16 = DBuf(std::max<int64_t>(1, b_rows * n) * 2, s);
+        // pipelined chunks (no host round trip per chunk) unless the tcgen05
+        // path is requested (its launcher sizes the work list on the host)
+        const bool pipelined = !(cfg->flags & TCS_CFG_PATH_TCGEN05);
+        DBuf d_flags(nchunks * 4, s), d_blocks(nchunks * 8, s);
         Streams ss;
         // On any exit (an error in a later chunk included) the side streams'
         // queued copies and kernels finish before the buffers above are
@@ -1348,14 +1601,23 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             }
             tcs_csr chunk{r1 - r0, host_csr->cols, e1 - e0, rp_i, d_ci.as<uint32_t>() + e0, d_v.as<float>() + e0};
             tcs_mebcrs m{};
-            tcs_status rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
-            if (rc != TCS_OK) fail(rc, tcs_last_error());
+            tcs_status rc = TCS_OK;
+            if (pipelined) {
+                encode_mebcrs_async(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, cs,
+                                    d_flags.as<uint32_t>() + i);
+            } else {
+                rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
+                if (rc != TCS_OK) fail(rc, tcs_last_error());
+            }
             if (e2e_trace()) encoded[i].record(cs);
             tcs_counters cn{};
             rc = tcs_spmm(&m, bdev, bdt, n, b_rows, n, d_c.as<float>() + r0 * n, n, cfg, counters ? &cn : nullptr, ks);
+            if (rc == TCS_OK && pipelined && counters)  // this chunk's k-block count, read once at the end
+                rc = cudaMemcpyAsync(d_blocks.as<uint64_t>() + i, static_cast<Plan*>(m.plan)->dcounts + 2, 8,
+                                     cudaMemcpyDeviceToDevice, cs) == cudaSuccess ? TCS_OK : TCS_ERR_CUDA;
             tcs_mebcrs_free(&m, ks);
             if (rc != TCS_OK) fail(rc, tcs_last_error());
-            if (counters) counters->mma_invocations += cn.mma_invocations;
+            if (counters && !pipelined) counters->mma_invocations += cn.mma_invocations;
             done[i].record(cs);
             done[i].wait_on(ss.drain);
             TCS_CUDA(cudaMemcpyAsync(c + r0 * n, d_c.as<float>() + r0 * n, (r1 - r0) * n * 4, cudaMemcpyDeviceToHost,
@@ -1386,6 +1648,17 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         for (auto& e : joined_compute) e.wait_on(s);
         joined_drain.wait_on(s);
         join.joined = true;
+        std::vector<uint32_t> bad(nchunks, 0);
+        std::vector<uint64_t> blocks(nchunks, 0);
+        if (pipelined) {
+            TCS_CUDA(cudaMemcpyAsync(bad.data(), d_flags.p, nchunks * 4, cudaMemcpyDeviceToHost, s));
+            if (counters)
+                TCS_CUDA(cudaMemcpyAsync(blocks.data(), d_blocks.p, nchunks * 8, cudaMemcpyDeviceToHost, s));
+        }
         TCS_CUDA(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < nchunks; ++i)  // the first invalid chunk's validation code (encode.cu kBadMsg)
+            if (bad[i]) fail(TCS_ERR_FORMAT, encode_bad_msg(bad[i]));
+        if (counters && pipelined)
+            for (uint64_t i = 0; i < nchunks; ++i) counters->mma_invocations += blocks[i] * ((n + 15) / 16);
     });
 }

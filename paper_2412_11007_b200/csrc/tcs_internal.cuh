@@ -139,9 +139,19 @@ struct Plan {
     const uint8_t* exact_for(const void* values) const {
         return exact_live && exact_live_src == values ? exact_live : nullptr;
     }
+    // Pipelined plans (build_plan_async, no host round trip): n_items,
+    // n_slots and n_split above are capacities.  The real items sit at the
+    // END of `items`, so a persistent SpMM whose claim counters start at
+    // dcounts[0] (= capacity - real items) walks exactly them; dcounts[1] is
+    // the real number of split windows; dcounts[2..3] the u64 block count.
+    uint32_t* dcounts = nullptr;  // device
 };
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16);
+Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, cudaStream_t s);
+void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
+                         cudaStream_t s, uint32_t* bad_dev);
+const char* encode_bad_msg(uint32_t code);
 void free_plan(Plan* p, cudaStream_t s);
 
 // ------------------------------------------------------------ conversions
@@ -208,12 +218,6 @@ struct StripedClaim {
     uint32_t stripe, tried = 0;
     __device__ __forceinline__ StripedClaim() : stripe(blockIdx.x % NS) {}
     __device__ __forceinline__ bool get(uint32_t* counters, uint64_t n_items, uint32_t& idx) {
-        if (!counters) {  // direct dispatch: one item per warp, in warp order
-            if (tried) return false;
-            tried = NS;
-            idx = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-            return idx < n_items;
-        }
         while (tried < NS) {
             uint32_t k = 0;
             if ((threadIdx.x & 31u) == 0) k = atomicAdd(counters + stripe * kClaimStride, 1u);
@@ -236,20 +240,9 @@ __device__ __forceinline__ uint32_t next_item(uint32_t* counter, uint32_t lane) 
     if (lane == 0) i = atomicAdd(counter, 1u);
     return __shfl_sync(0xffffffffu, i, 0);
 }
-// Direct dispatch (counter == nullptr): the launch holds one warp per work
-// item, so a warp's item is its global warp index along x and there is no
-// second one -- no counter to allocate and zero, and no atomic round trip
-// ahead of the first load.  Chosen by the host when the item list fits in
-// one wave of resident warps (the small configs, e.g. BASELINE C1/C2).
-__device__ __forceinline__ uint32_t first_item(uint32_t* counter, uint32_t lane) {
-    return counter ? next_item(counter, lane) : blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-}
-__device__ __forceinline__ uint32_t following_item(uint32_t* counter, uint32_t lane) {
-    return counter ? next_item(counter, lane) : 0xFFFFFFFFu;
-}
-// The claim counter of slab `slab` (nullptr stays nullptr: direct dispatch).
+// The claim counter of slab `slab`.
 __device__ __forceinline__ uint32_t* slab_counter(uint32_t* counters, uint32_t slab) {
-    return counters ? counters + static_cast<uint64_t>(slab) * (kClaimBytes / 4) : nullptr;
+    return counters + static_cast<uint64_t>(slab) * (kClaimBytes / 4);
 }
 
 // RNE fp32 -> tf32 (cvt.rn.tf32.f32, sm_90+); matches the reference's
@@ -292,6 +285,18 @@ __device__ __forceinline__ uint32_t f2_to_h2(float a, float b) { return h2_bits(
 __device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
     uint32_t v;
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+// L2 evict-first policy (createpolicy) for read-once streams, so they do not
+// displace an L2-resident gathered operand.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint32_t ld_stream_ef_u32(const void* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ uint2 ld_stream_u64(const void* p) {

@@ -118,6 +118,69 @@ def uniform_csr(rows_n, cols_n, density, seed=1, values="real", device="cuda"):
     return rows_n, cols_n, row_ptr, col_idx, _values(col_idx.numel(), values, gen, device)
 
 
+def _mt_stream(seed: int, n: int):
+    """n raw std::mt19937 draws for `seed`: numpy's legacy RandomState seeds
+    with init_genrand(seed) and returns raw 32-bit outputs for a full-range
+    uint32 request, i.e. exactly std::mt19937(seed)()."""
+    import numpy as np
+    return np.random.RandomState(seed & 0xFFFFFFFF).randint(0, 1 << 32, size=n, dtype=np.uint32)
+
+
+def _small_int(draws):
+    import numpy as np
+    m = (draws % 8).astype(np.int64)  # ref generate.hpp:15-18
+    return np.where(m < 4, m - 4, m - 3).astype(np.float32)
+
+
+def _uniform_real(draws):
+    import numpy as np
+    return (draws.astype(np.float32) * np.float32(2.0 ** -31) - np.float32(1.0)).astype(np.float32)  # :20-22
+
+
+def reference_random_csr(rows_n, cols_n, density, seed, values="int"):
+    """The reference's own CSR generator, ``generate_random_sparse`` /
+    ``generate_random_sparse_real`` (ref generate.hpp:29-63): one raw
+    mt19937 draw per position in row-major order, kept when below
+    llround(density * 2^32), a kept position consuming one more draw for its
+    small-integer value; "real" values come from a second stream seeded with
+    seed ^ 0x9e3779b9.  Host numpy (BASELINE configs[0]/[1] size: 16.8 M
+    draws); returns (row_ptr u32, col_idx u32, values f32) numpy arrays."""
+    import numpy as np
+    if rows_n <= 0 or cols_n <= 0 or not (0.0 < density <= 1.0):
+        raise ValueError("rows and cols must be >= 1 and density in (0, 1]")
+    cells = rows_n * cols_n
+    thr = np.uint64(int(density * 4294967296.0 + 0.5))  # llround, density > 0
+    # Draw d[i] is a position test unless it is the value draw of the kept
+    # test right before it.  Over-draw, then walk the kept candidates.
+    n = cells + max(64, int(cells * density * 1.5) + 6 * int((cells * density) ** 0.5) + 64)
+    while True:
+        d = _mt_stream(seed, n)
+        kept, nxt = [], 0
+        for c in np.flatnonzero(d.astype(np.uint64) < thr).tolist():
+            if c >= nxt:  # a test draw, not the value draw of the kept test before it
+                kept.append(c)
+                nxt = c + 2
+        if n - 1 - len(kept) >= cells:  # every cell tested, every kept value drawn
+            break
+        n *= 2
+    kept = np.asarray(kept, dtype=np.int64)
+    pos = kept - np.arange(kept.size, dtype=np.int64)  # cell = draw index - value draws before it
+    kept, pos = kept[pos < cells], pos[pos < cells]
+    vals = _small_int(d[kept + 1])
+    if values == "real":
+        vals = _uniform_real(_mt_stream(seed ^ 0x9E3779B9, kept.size))
+    r = pos // cols_n
+    row_ptr = np.zeros(rows_n + 1, np.uint32)
+    np.cumsum(np.bincount(r, minlength=rows_n), out=row_ptr[1:])
+    return row_ptr, (pos - r * cols_n).astype(np.uint32), vals
+
+
+def reference_random_dense(rows_n, cols_n, seed, values="int"):
+    """ref generate.hpp:65-79 (row-major, one draw per element)."""
+    d = _mt_stream(seed, rows_n * cols_n)
+    return (_uniform_real(d) if values == "real" else _small_int(d)).reshape(rows_n, cols_n)
+
+
 def dense(rows_n, cols_n, seed, values="real", dtype=torch.float16, device="cuda"):
     gen = torch.Generator(device=device)
     gen.manual_seed(seed)

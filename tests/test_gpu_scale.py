@@ -292,3 +292,34 @@ def test_direct_mapping_bit_identical(n, vdt):
         cfg = T.KernelConfig(T.Precision.fp16, mapping=T.ThreadMapping.direct)
         got = T.spmm(me, dense, cfg).output.cpu().numpy()
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("defect", ["descending", "out_of_range"])
+def test_pipelined_host_call_reports_late_chunk_format_errors(defect):
+    """tcs_spmm_csr_host encodes its chunks without host round trips; a
+    malformed row in the LAST chunk must still come back as the reference's
+    FormatError (ref matrix.hpp validate), not as garbage output."""
+    import paper_2412_11007_b200._abi as abi
+
+    spec = G.GraphSpec("mid", 60_000, 3_000_000, alpha=1.2, cap=60.0, seed=7)
+    rows, cols, rp, ci, v = G.power_law_csr(spec, values="int")
+    m = to_oracle(rows, cols, rp, ci, v)
+    ci_h = m.col_idx.copy()
+    r = rows - 3  # a row of the last chunk with >= 2 entries
+    while m.row_ptr[r + 1] - m.row_ptr[r] < 2:
+        r -= 1
+    e = int(m.row_ptr[r])
+    if defect == "descending":
+        ci_h[e], ci_h[e + 1] = ci_h[e + 1], ci_h[e]
+    else:
+        ci_h[int(m.row_ptr[r + 1]) - 1] = cols + 5
+    csr = abi.tcs_csr(rows, cols, m.nnz, m.row_ptr.ctypes.data, ci_h.ctypes.data, m.values.ctypes.data)
+    cfg = abi.tcs_kernel_config(0, 8, 1, 0)
+    B = O.generate_random_dense(cols, 32, 3)
+    Ch = np.empty((rows, 32), np.float32)
+    lib = abi.load()
+    rc = lib.tcs_spmm_csr_host(C.byref(csr), 0, B.ctypes.data, 32, Ch.ctypes.data, C.byref(cfg), None, None)
+    assert rc == abi.TCS_ERR_FORMAT
+    msg = lib.tcs_last_error().decode() if isinstance(lib.tcs_last_error(), bytes) else str(lib.tcs_last_error())
+    assert ("ascending" if defect == "descending" else "out of range") in msg

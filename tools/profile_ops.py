@@ -19,8 +19,10 @@ cfg_name, op = sys.argv[1], sys.argv[2]
 prec = T.Precision.fp16 if (sys.argv[3] if len(sys.argv) > 3 else "fp16") == "fp16" else T.Precision.tf32
 width = int(sys.argv[4]) if len(sys.argv) > 4 else (32 if op.startswith("sddmm") else 128)
 dt = torch.float16 if prec == T.Precision.fp16 else torch.float32
-if cfg_name == "c1":
-    rows, cols, rp, ci, v = G.uniform_csr(4096, 4096, 16.0 / 4096, seed=1, values="real")
+if cfg_name == "c1":  # the reference's own C1 inputs (generate.hpp restated)
+    rows = cols = 4096
+    rp, ci, v = (torch.from_numpy(x.view("int32") if x.dtype.kind == "u" else x).cuda()
+                 for x in G.reference_random_csr(rows, cols, 16.0 / 4096, 1, "real"))
 elif cfg_name == "c3":
     rows, cols, rp, ci, v = G.power_law_csr(G.C3_REDDIT, values="real")
 elif cfg_name == "c4":
