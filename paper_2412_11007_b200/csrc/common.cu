@@ -255,13 +255,17 @@ Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t
 }
 
 // The same work list without a host round trip (tcs_spmm_csr_host's
-// chunks): the segment length comes from the vector capacity nv_cap, the
+// chunks): the segment length comes from seg_nv (see below), the
 // arrays are sized for the worst case (a split window has more than seg
 // vectors, so split windows <= nv/seg and segments <= 2 nv/seg), and the
 // real counts stay on the device (Plan::dcounts).
-Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, cudaStream_t s) {
+// seg_nv (0 = nv_cap): the vector count the segment length is sized for.
+// A pipeline chunk uses its own: sized for the whole matrix, a small tail
+// chunk's few hundred windows would each be walked by one warp (C3: 0.5 ms
+// per tail-chunk SpMM instead of 0.04 ms + a 5 us split reduction).
+Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, uint64_t seg_nv, cudaStream_t s) {
     const uint64_t W = m->num_windows;
-    const uint32_t seg = plan_seg(nv_cap);
+    const uint32_t seg = plan_seg(std::max(nv_cap, seg_nv));
     const uint64_t split_cap = std::min<uint64_t>(W, nv_cap / seg);
     Plan* p = new Plan;
     p->seg = seg;
@@ -294,6 +298,7 @@ Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, cudaStream_t s) {
 void free_plan(Plan* p, cudaStream_t s) {
     if (!p) return;
     dfree(p->dcounts, s);
+    dfree(p->col_hot, s);
     dfree(p->items, s);
     dfree(p->split, s);
     dfree(p->live, s);

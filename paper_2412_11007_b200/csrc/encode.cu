@@ -45,7 +45,8 @@ constexpr uint32_t kSmallThreads = 128;
 constexpr uint32_t kBigCap = 12288;     // 512-thread CTA, 192 KB smem
 constexpr uint32_t kBigThreads = 512;
 constexpr uint32_t kBitmapThreads = 512;
-constexpr uint32_t kBitmapMaxWords = 25600;  // 2 x 100 KB of smem -> <= 819,200 columns
+constexpr uint32_t kBitmapMaxWords = 25600;
+constexpr int kBitmapU = 8;  // entries per thread in flight (window_bitmap)  // 2 x 100 KB of smem -> <= 819,200 columns
 constexpr uint64_t kSentinel = ~0ull;
 
 struct CheckOut {
@@ -65,6 +66,9 @@ struct CheckOut {
     // (ref sddmm.hpp:131 tests the f32 value), so the handle gets exact
     // liveness bytes built from the f32 CSR values
     uint32_t tiny;
+    // scatter work units of the huge windows: one per (window, value tile),
+    // tile_off = their exclusive prefix over the huge list (huge_tile_prefix)
+    uint32_t huge_tiles;
 };
 
 // CTA-wide queue claim: thread 0 takes the next index, every thread gets it.
@@ -414,12 +418,29 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
         for (uint32_t i = threadIdx.x; i < words; i += nt) bm[i] = 0u;
         __syncthreads();
+        // kBitmapU entries per thread in flight: a hub window (10^4..10^5
+        // entries) is otherwise a chain of dependent-latency iterations
         uint32_t bad = 0;
-        for (uint32_t i = threadIdx.x; i < n; i += nt) {
-            const uint32_t c = ci[e0 + i];
-            const uint32_t b = check_col<VH>(ci, e0, i, c, rb, cols);
-            bad = max(bad, b);
-            if (!b || b == 4u) atomicOr(&bm[c >> 5], 1u << (c & 31));
+        for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
+            uint32_t c[kBitmapU], cp[kBitmapU];
+#pragma unroll
+            for (int u = 0; u < kBitmapU; ++u) {
+                const uint32_t i = i0 + u * nt;
+                c[u] = i < n ? __ldg(ci + e0 + i) : 0u;
+                cp[u] = i < n && i > 0 ? __ldg(ci + e0 + i - 1) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < kBitmapU; ++u) {
+                const uint32_t i = i0 + u * nt;
+                if (i >= n) continue;
+                bool row_start = false;
+#pragma unroll
+                for (int r = 0; r < VH; ++r) row_start |= (i == rb[r]);
+                // check_col with the predecessor already loaded
+                const uint32_t b = !row_start && cp[u] >= c[u] ? 4u : c[u] >= cols ? 3u : 0u;
+                bad = max(bad, b);
+                if (c[u] < cols) atomicOr(&bm[c[u] >> 5], 1u << (c[u] & 31));
+            }
         }
         if (bad) atomicMax(&chk->bad, bad);
         __syncthreads();
@@ -440,9 +461,19 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
         }
         if (threadIdx.x == 0) nv_out[w] = total;
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < n; i += nt) {
-            const uint32_t c = ci[e0 + i];
-            if (c < cols) rank[e0 + i] = pre[c >> 5] + __popc(bm[c >> 5] & ((1u << (c & 31)) - 1u));
+        for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
+            uint32_t c[kBitmapU];
+#pragma unroll
+            for (int u = 0; u < kBitmapU; ++u) {
+                const uint32_t i = i0 + u * nt;
+                c[u] = i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
+            }
+#pragma unroll
+            for (int u = 0; u < kBitmapU; ++u) {
+                const uint32_t i = i0 + u * nt;
+                if (i < n && c[u] < cols)
+                    rank[e0 + i] = pre[c[u] >> 5] + __popc(bm[c[u] >> 5] & ((1u << (c[u] & 31)) - 1u));
+            }
         }
         __syncthreads();
     }
@@ -469,6 +500,37 @@ constexpr int kScatterThreadsBig = 512;
 constexpr uint32_t kScatterTileSmall = kSmallCap;
 constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
+constexpr uint32_t kTileBatch = 63;   // tile boundaries searched at once (64 x VH threads)
+
+// Tiles of each huge window (vectors / tile), exclusive prefix over the
+// huge list (one CTA; the huge list is short) -> tile_off[0..n_huge], total
+// in chk->huge_tiles.  The big scatter then hands out (window, tile) units,
+// so a hub window's tiles are written by many CTAs at once instead of one
+// CTA walking them in turn (its latency bounded the whole encode and, in the
+// chunk pipeline of tcs_spmm_csr_host, every chunk).
+__global__ void __launch_bounds__(1024) huge_tile_prefix(const uint32_t* __restrict__ rp,
+                                                         const uint32_t* __restrict__ big, CheckOut* chk,
+                                                         uint32_t tile, uint32_t* __restrict__ tile_off) {
+    const uint32_t n = chk->n_huge;
+    uint32_t carry = 0;
+    for (uint32_t i0 = 0; i0 < n; i0 += blockDim.x) {
+        const uint32_t i = i0 + threadIdx.x;
+        uint32_t t = 0;
+        if (i < n) {
+            const uint32_t w = big[i];
+            t = (rp[w + 1] - rp[w] + tile - 1) / tile;
+        }
+        uint32_t total;
+        const uint32_t ex = dev::block_exclusive_scan(t, &total);
+        if (i < n) tile_off[i] = carry + ex;
+        carry += total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        tile_off[n] = carry;
+        chk->huge_tiles = carry;
+    }
+}
 
 template <int VH, typename V, int THREADS, uint32_t TILE>
 __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __restrict__ csr_rp,
@@ -477,62 +539,88 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ tmp_cols,
                                                       const uint32_t* __restrict__ rank,
                                                       uint32_t* __restrict__ out_ci, V* __restrict__ out_vals,
-                                                      const uint32_t* __restrict__ list, bool big, CheckOut* chk) {
+                                                      const uint32_t* __restrict__ list, bool big, CheckOut* chk,
+                                                      const uint32_t* __restrict__ tile_off) {
     extern __shared__ uint4 tile_raw[];
-    // big list: huge windows from the front, medium from the back, dynamic
-    // queue; small list: tiny from the front, small from the back, fixed stride
+    // big list: units = (huge window, tile) pairs (huge_tile_prefix), then
+    // the medium windows from the back of the list, dynamic queue; small
+    // list: tiny windows from the front, small from the back, fixed stride
     const uint32_t n_front = big ? chk->n_huge : chk->n_tiny;
-    const uint32_t n_list = n_front + (big ? chk->n_medium : chk->n_small);
+    const uint32_t n_huge_units = big ? chk->huge_tiles : 0u;
+    const uint32_t n_units = big ? n_huge_units + chk->n_medium : n_front + chk->n_small;
     uint32_t* next = big ? &chk->next_scatter_big : nullptr;
     uint32_t* tiny = &chk->tiny;
+    __shared__ uint32_t s_huge;
     V* tile = reinterpret_cast<V*>(tile_raw);
     __shared__ uint32_t rb[VH + 1];
-    __shared__ uint32_t rlo[VH + 1], rhi[VH], roff[VH + 1];  // this tile's entry range per row
+    __shared__ uint32_t tb[kTileBatch + 1][VH];  // ranged: first entry of each row per tile boundary
+    __shared__ uint32_t rlo[VH], roff[VH + 1];    // ranged: this tile's first entry per row, prefix
     constexpr uint32_t kTile = TILE * 8 / VH;  // vectors per smem tile
     // big list: dynamic queue (next != nullptr); small list: fixed stride
-    for (uint32_t li = next ? cta_next(next) : blockIdx.x; li < n_list;
-         li = next ? cta_next(next) : li + gridDim.x) {
-        const uint64_t w = big_window(list, W, n_front, li);  // n_front from the front, the rest from the back
+    for (uint32_t u = next ? cta_next(next) : blockIdx.x; u < n_units; u = next ? cta_next(next) : u + gridDim.x) {
+        uint64_t w;
+        uint32_t tile_lo = 0, tile_hi = 0xFFFFFFFFu;  // the unit's tiles of window w
+        if (u < n_huge_units) {  // block-uniform
+            if (threadIdx.x == 0) {  // huge window i: tile_off[i] <= u < tile_off[i + 1]
+                uint32_t lo = 0, hi = n_front;
+                while (hi - lo > 1) {
+                    const uint32_t mid = (lo + hi) / 2;
+                    if (tile_off[mid] <= u) lo = mid; else hi = mid;
+                }
+                s_huge = lo;
+            }
+            __syncthreads();
+            const uint32_t i = s_huge;
+            w = list[i];
+            tile_lo = u - tile_off[i];
+            tile_hi = tile_lo + 1;
+        } else {
+            w = big_window(list, W, n_front, big ? n_front + (u - n_huge_units) : u);
+        }
         const uint64_t r0 = VH * w;
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)];
         const uint32_t base = rp[w], nvw = rp[w + 1] - base;
         __syncthreads();
         const uint32_t e0 = rb[0], e1 = rb[VH];
-        for (uint32_t i = threadIdx.x; i < nvw; i += blockDim.x) out_ci[base + i] = tmp_cols[e0 + i];
+        const uint32_t v_lo = min(nvw, tile_lo * kTile);
+        const uint32_t v_hi = uint64_t(tile_hi) * kTile < nvw ? tile_hi * kTile : nvw;
+        for (uint32_t i = v_lo + threadIdx.x; i < v_hi; i += blockDim.x) out_ci[base + i] = tmp_cols[e0 + i];
         V* vals = out_vals + static_cast<uint64_t>(VH) * base;
-        for (uint32_t t0 = 0; t0 < nvw; t0 += kTile) {
+        // block-uniform: a window of at most kRangedTiles tiles scans all of
+        // its entries per tile and keeps those of the tile (cheap for few
+        // tiles); longer (hub) windows find each tile's entries per row:
+        // within a row the rank ascends with the column, so a tile's entries
+        // are one contiguous range per row -- and the range boundaries of up
+        // to kTileBatch tiles are binary-searched in parallel, one thread per
+        // (tile boundary, row), instead of tile after tile.
+        const bool ranged = nvw > kRangedTiles * kTile;
+        for (uint32_t t0 = v_lo; t0 < v_hi; t0 += kTile) {
+            const uint32_t tj = ((t0 - v_lo) / kTile) % kTileBatch;  // tile within its batch
+            if (ranged && tj == 0) {
+                __syncthreads();  // the previous batch's boundaries are no longer read
+                for (uint32_t x = threadIdx.x; x < (kTileBatch + 1) * VH; x += blockDim.x) {
+                    const uint32_t j = x / VH, r = x % VH;
+                    const uint32_t key = min(nvw, t0 + j * kTile);
+                    uint32_t lo = rb[r] - e0, hi = rb[r + 1] - e0;  // first entry of row r with rank >= key
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) / 2;
+                        if (__ldg(rank + e0 + mid) < key) lo = mid + 1; else hi = mid;
+                    }
+                    tb[j][r] = e0 + lo;
+                }
+            }
             const uint32_t tn = min(kTile, nvw - t0);  // vectors in this tile
             const uint32_t n16 = (VH * tn * sizeof(V) + 15) / 16;
             for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) tile_raw[i] = make_uint4(0, 0, 0, 0);
-            // The entries whose vector falls in this tile: within a row the
-            // rank ascends with the column, so per row they are one contiguous
-            // range (binary search) -- each entry is visited by one tile only,
-            // instead of every tile scanning the whole window (quadratic on
-            // hub windows of 10^5 vectors).
-            // block-uniform: a window of at most kRangedTiles tiles scans all of
-            // its entries per tile and keeps those of the tile (cheap for few
-            // tiles); longer (hub) windows locate the tile's range per row
-            const bool ranged = nvw > kRangedTiles * kTile;
-            if (ranged && threadIdx.x < VH) {
-                const uint32_t a = rb[threadIdx.x], z = rb[threadIdx.x + 1];
-                auto first_geq = [&](uint32_t key) {  // first entry of the row with rank >= key
-                    uint32_t lo = a, hi = z;
-                    while (lo < hi) {
-                        const uint32_t mid = (lo + hi) / 2;
-                        if (__ldg(rank + mid) < key) lo = mid + 1; else hi = mid;
-                    }
-                    return lo;
-                };
-                rlo[threadIdx.x] = first_geq(t0);
-                rhi[threadIdx.x] = first_geq(t0 + tn);
-            }
             __syncthreads();
-            if (ranged) {
-                if (threadIdx.x == 0) {  // prefix of the per-row range lengths
+            if (ranged) {  // this tile's per-row entry ranges and their prefix
+                if (threadIdx.x == 0) {
                     uint32_t acc = 0;
+#pragma unroll
                     for (int q = 0; q < VH; ++q) {
+                        rlo[q] = tb[tj][q];
                         roff[q] = acc;
-                        acc += rhi[q] - rlo[q];
+                        acc += tb[tj + 1][q] - tb[tj][q];
                     }
                     roff[VH] = acc;
                 }
@@ -604,7 +692,8 @@ __global__ void exact_live_build(const uint32_t* __restrict__ csr_rp, const floa
 // Value type V of a window_scatter instantiation (for the launch helper).
 template <typename V>
 V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
-                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, CheckOut*));
+                           const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, CheckOut*,
+                           const uint32_t*));
 
 const char* kBadMsg[] = {"", "row_ptr must be nondecreasing", "row_ptr exceeds nnz", "column index out of range",
                          "column indices must be strictly ascending within a row"};
@@ -628,7 +717,8 @@ namespace {
 // are not built (the pipeline only multiplies).
 template <int VH>
 void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                 tcs_stream_t stream, uint32_t* async_bad = nullptr) {
+                 tcs_stream_t stream, uint32_t* async_bad = nullptr, uint64_t seg_nv = 0,
+                 cudaEvent_t values_ready = nullptr) {
     {
         if (!csr || !out) fail(TCS_ERR_ARGUMENT, "null argument");
         if (precision != TCS_FP16 && precision != TCS_TF32) fail(TCS_ERR_ARGUMENT, "unknown precision");
@@ -758,6 +848,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             const size_t vw = value_dtype == TCS_DTYPE_F16 ? 2 : 4;
             m.column_indices = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
             m.values = dalloc(std::max<uint64_t>(1, uint64_t(VH) * nv) * vw, s);
+            DBuf tile_off(W * 4 + 4, s);
             auto scatter = [&](auto kern, int threads, uint32_t tile, const uint32_t* list, bool big, uint64_t n) {
                 if (!n) return;
                 const size_t tile_smem = size_t(tile) * 8 * vw;
@@ -769,17 +860,28 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                 kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
                                                     static_cast<decltype(kern_value_type(kern))*>(m.values), list,
-                                                    big, dchk);
+                                                    big, dchk, tile_off.as<uint32_t>());
             };
+            // (window, tile) units of the huge windows for the big scatter
+            if (n_big) {
+                huge_tile_prefix<<<1, 1024, 0, s>>>(m.row_pointers, big_list.as<uint32_t>(), dchk,
+                                                     kScatterTileBig * 8 / VH, tile_off.as<uint32_t>());
+                TCS_LAUNCHED("huge_tile_prefix");
+            }
+            // the CSR values are read from here on (the pipeline uploads them
+            // after the column indices the kernels above rank)
+            if (values_ready) TCS_CUDA(cudaStreamWaitEvent(s, values_ready, 0));
             const uint64_t n_smalls = async ? W : uint64_t(h.n_tiny) + h.n_small;
+            // big scatter units: with any huge window, as many CTAs as fit
+            const uint64_t n_big_units = h.n_huge || async ? uint64_t(sms) * 64 : n_big;
             if (value_dtype == TCS_DTYPE_F16) {
                 scatter(window_scatter<VH, __half, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
-                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
+                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big ? n_big_units : 0);
                 scatter(window_scatter<VH, __half, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
                         kScatterTileSmall, small_list.as<uint32_t>(), false, n_smalls);
             } else {
                 scatter(window_scatter<VH, float, kScatterThreadsBig, kScatterTileBig>, kScatterThreadsBig,
-                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big);
+                        kScatterTileBig, big_list.as<uint32_t>(), true, n_big ? n_big_units : 0);
                 scatter(window_scatter<VH, float, kScatterThreadsSmall, kScatterTileSmall>, kScatterThreadsSmall,
                         kScatterTileSmall, small_list.as<uint32_t>(), false, n_smalls);
             }
@@ -808,7 +910,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         cleanup.armed = false;
         *out = m;
         if (async) {
-            out->plan = build_plan_async(out, nnz, s);
+            out->plan = build_plan_async(out, nnz, seg_nv, s);
             return;
         }
         const tcs_status rc = tcs_mebcrs_prepare(out, stream);
@@ -832,8 +934,9 @@ const char* encode_bad_msg(uint32_t code) { return kBadMsg[code < 5 ? code : 0];
 
 // The pipelined encode (see encode_impl): tcs_spmm_csr_host's chunks.
 void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                         cudaStream_t s, uint32_t* bad_dev) {
-    encode_impl<8>(csr, precision, value_dtype, out, reinterpret_cast<tcs_stream_t>(s), bad_dev);
+                         cudaStream_t s, uint32_t* bad_dev, uint64_t seg_nv, cudaEvent_t values_ready) {
+    encode_impl<8>(csr, precision, value_dtype, out, reinterpret_cast<tcs_stream_t>(s), bad_dev, seg_nv,
+                   values_ready);
 }
 
 }  // namespace tcs

@@ -519,6 +519,8 @@ __global__ void __launch_bounds__(kBW * 32, kBurstBlocks * kWarps / kBW) sddmm_b
     const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kBW + (threadIdx.x >> 5);
     const uint64_t idx = gw / a.sub;
     const uint32_t part = static_cast<uint32_t>(gw % a.sub);
+    pdl_trigger();  // see dev::pdl_wait: launched with launch_pdl
+    pdl_wait();
     if (idx >= a.n_items) return;
     WorkItem it;
     uint32_t base, nvw;
@@ -573,13 +575,14 @@ __global__ void __launch_bounds__(kBW * 32, kBurstBlocks * kWarps / kBW) sddmm_b
 template <bool TF32, int NSC, int G>
 void launch_sddmm_burst(const SddmmArgs& a, bool mf32, bool of32, cudaStream_t s) {
     const dim3 grid(static_cast<unsigned>((a.n_items * a.sub + kBW - 1) / kBW));
+    const dim3 block(kBW * 32);
     if (a.live) {
-        if (of32) sddmm_burst<TF32, NSC, kLive, true, G><<<grid, kBW * 32, 0, s>>>(a);
-        else sddmm_burst<TF32, NSC, kLive, false, G><<<grid, kBW * 32, 0, s>>>(a);
-    } else if (mf32 && of32) sddmm_burst<TF32, NSC, kMaskF32, true, G><<<grid, kBW * 32, 0, s>>>(a);
-    else if (mf32) sddmm_burst<TF32, NSC, kMaskF32, false, G><<<grid, kBW * 32, 0, s>>>(a);
-    else if (of32) sddmm_burst<TF32, NSC, kMaskF16, true, G><<<grid, kBW * 32, 0, s>>>(a);
-    else sddmm_burst<TF32, NSC, kMaskF16, false, G><<<grid, kBW * 32, 0, s>>>(a);
+        if (of32) launch_pdl(sddmm_burst<TF32, NSC, kLive, true, G>, grid, block, 0, s, a);
+        else launch_pdl(sddmm_burst<TF32, NSC, kLive, false, G>, grid, block, 0, s, a);
+    } else if (mf32 && of32) launch_pdl(sddmm_burst<TF32, NSC, kMaskF32, true, G>, grid, block, 0, s, a);
+    else if (mf32) launch_pdl(sddmm_burst<TF32, NSC, kMaskF32, false, G>, grid, block, 0, s, a);
+    else if (of32) launch_pdl(sddmm_burst<TF32, NSC, kMaskF16, true, G>, grid, block, 0, s, a);
+    else launch_pdl(sddmm_burst<TF32, NSC, kMaskF16, false, G>, grid, block, 0, s, a);
     TCS_LAUNCHED(TF32 ? "sddmm_tf32_burst" : "sddmm_f16_burst");
 }
 

@@ -25,6 +25,7 @@
 // Windows longer than plan.seg are split; partial sums are reduced in
 // segment order by spmm_reduce_split (deterministic, no atomics).
 #include <algorithm>
+#include <memory>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -59,6 +60,7 @@ struct SpmmArgs {
     // softmax of softmax.cu applied in registers instead of in memory.
     const float2* rowstat;  // per row (m, 1/sum), 8 * num_windows entries
     float scale;
+    const uint32_t* hot;  // HOT kernels: Plan::col_hot bitmap
 };
 
 // One binary16 score -> its softmax value, rounded as softmax.cu stores it
@@ -119,6 +121,15 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_TF32P_LO64
 #define TCS_TF32P_LO64 1
 #endif
+// Hot-row L2 policy (see col_hot below; measured slower, off by default).
+#ifndef TCS_HOT
+#define TCS_HOT 0
+#endif
+// policy of the cold gathers under TCS_HOT: 0 evict_first, 1 evict_normal,
+// 2 evict_unchanged
+#ifndef TCS_HOT_COLD
+#define TCS_HOT_COLD 0
+#endif
 #ifndef TCS_SMALL_SLAB32
 #define TCS_SMALL_SLAB32 1
 #endif
@@ -143,6 +154,14 @@ __device__ __forceinline__ uint32_t load_colpair(const uint32_t* __restrict__ ci
                                                  uint32_t lane) {
     return s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
 }
+// HOT kernels: the column's Plan::col_hot bit rides in bit 31 (columns are
+// < 2^31; the gather masks it off and picks the L2 policy from it).
+template <bool HOT>
+__device__ __forceinline__ uint32_t mark_hot(uint32_t c, const uint32_t* __restrict__ hot) {
+    if constexpr (HOT) c |= ((__ldg(hot + (c >> 5)) >> (c & 31)) & 1u) << 31;
+    return c;
+}
+constexpr uint32_t kColMask = 0x7FFFFFFFu;
 
 // ------------------------------------------------------------- FP16 path
 //
@@ -225,10 +244,23 @@ __device__ __forceinline__ void f16_values(const SpmmArgs& a, uint64_t vbase, ui
 // 16-vector step at s.  colpair holds the column indices of vectors
 // [s - 16*half, +32).  (Loading the values two steps ahead instead, with
 // their own register pair, measured 7% slower on C3: 2.61 -> 2.80 ms.)
-template <int NCHUNK, int FPL, bool VF32, bool SMX = false, bool LOADV = true>
+// One gathered segment of a B row (HOT: with the row's L2 policy).
+template <int FPL, bool HOT>
+__device__ __forceinline__ void f16_gather(const __half* p, uint64_t pol, uint32_t (&dst)[FPL / 2]) {
+    if constexpr (FPL == 8) {
+        const uint4 x = HOT ? ld_gather_128_pol(p, pol) : ld_gather_128(p);
+        dst[0] = x.x; dst[1] = x.y; dst[2] = x.z; dst[3] = x.w;
+    } else {
+        const uint2 x = HOT ? ld_gather_64_pol(p, pol) : ld_gather_64(p);
+        dst[0] = x.x; dst[1] = x.y;
+    }
+}
+
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false, bool LOADV = true, bool HOT = false>
 __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __restrict__ Bl, uint64_t vbase,
                                           uint32_t nvw, uint32_t vend, uint32_t s, uint32_t g, uint32_t t, uint32_t q,
-                                          uint32_t colpair, uint32_t half, F16Step<NCHUNK, FPL, VF32>& st) {
+                                          uint32_t colpair, uint32_t half, F16Step<NCHUNK, FPL, VF32>& st,
+                                          uint64_t pol_last = 0, uint64_t pol_first = 0) {
     constexpr int CHUNK = 8 * FPL;
     uint32_t col[4];
 #pragma unroll
@@ -237,17 +269,10 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
         // full step (warp-uniform): no predicates; both k=8 blocks are full width
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            const __half* row = Bl + static_cast<uint64_t>(col[u]) * a.ldb;
+            const __half* row = Bl + static_cast<uint64_t>(HOT ? col[u] & kColMask : col[u]) * a.ldb;
+            const uint64_t pol = HOT && (col[u] >> 31) ? pol_last : pol_first;
 #pragma unroll
-            for (int c = 0; c < NCHUNK; ++c) {
-                if constexpr (FPL == 8) {
-                    const uint4 x = ld_gather_128(row + c * CHUNK);
-                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y; st.L[u][c][2] = x.z; st.L[u][c][3] = x.w;
-                } else {
-                    const uint2 x = ld_gather_64(row + c * CHUNK);
-                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y;
-                }
-            }
+            for (int c = 0; c < NCHUNK; ++c) f16_gather<FPL, HOT>(row + c * CHUNK, pol, st.L[u][c]);
         }
         if constexpr (LOADV) load_sparse_full<VF32>(a.vals, vbase, s, g, t, st.b[0], st.b[1]);
     } else {
@@ -255,15 +280,15 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const bool ok = s + loader_vec(u, q) < vend;
-            const __half* row = Bl + static_cast<uint64_t>(col[u]) * a.ldb;
+            const __half* row = Bl + static_cast<uint64_t>(HOT ? col[u] & kColMask : col[u]) * a.ldb;
+            const uint64_t pol = HOT && (col[u] >> 31) ? pol_last : pol_first;
 #pragma unroll
             for (int c = 0; c < NCHUNK; ++c) {
-                if constexpr (FPL == 8) {
-                    const uint4 x = ok ? ld_gather_128(row + c * CHUNK) : make_uint4(0, 0, 0, 0);
-                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y; st.L[u][c][2] = x.z; st.L[u][c][3] = x.w;
+                if (ok) {
+                    f16_gather<FPL, HOT>(row + c * CHUNK, pol, st.L[u][c]);
                 } else {
-                    const uint2 x = ok ? ld_gather_64(row + c * CHUNK) : make_uint2(0, 0);
-                    st.L[u][c][0] = x.x; st.L[u][c][1] = x.y;
+#pragma unroll
+                    for (int j = 0; j < FPL / 2; ++j) st.L[u][c][j] = 0u;
                 }
             }
         }
@@ -342,7 +367,7 @@ __device__ __forceinline__ void f16_epilogue(const SpmmArgs& a, const WorkItem& 
     }
 }
 
-template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false, bool HOT = false>
 __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
@@ -352,6 +377,11 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
+    uint64_t pol_last = 0, pol_first = 0;
+    if constexpr (HOT) {
+        pol_last = l2_evict_last_policy();
+        pol_first = l2_cold_policy<TCS_HOT_COLD>();
+    }
 
     for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
         const WorkItem it = a.items[idx];
@@ -378,16 +408,21 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
         F16Step<NCHUNK, FPL, VF32> sa, sb;
         uint32_t s = it.vbeg;
         if (s < vend) {
-            uint32_t cp0 = load_colpair(ci, s, vend, lane);       // steps s, s+16
-            uint32_t cp1 = load_colpair(ci, s + 32, vend, lane);  // steps s+32, s+48
-            f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa);
+            uint32_t cp0 = mark_hot<HOT>(load_colpair(ci, s, vend, lane), a.hot);       // steps s, s+16
+            uint32_t cp1 = mark_hot<HOT>(load_colpair(ci, s + 32, vend, lane), a.hot);  // steps s+32, s+48
+            f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa, pol_last,
+                                                         pol_first);
             for (;;) {
-                if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb);
+                if (s + 16 < vend)
+                    f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb,
+                                                                 pol_last, pol_first);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(sa, acc, src_lane, a.scale, sm, sinv);
                 if (s + 16 >= vend) break;
-                if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa);
+                if (s + 32 < vend)
+                    f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa,
+                                                                 pol_last, pol_first);
                 cp0 = cp1;
-                cp1 = load_colpair(ci, s + 64, vend, lane);
+                cp1 = mark_hot<HOT>(load_colpair(ci, s + 64, vend, lane), a.hot);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(sb, acc, src_lane, a.scale, sm, sinv);
                 s += 32;
                 if (s >= vend) break;
@@ -411,7 +446,7 @@ __device__ __forceinline__ uint32_t load_col16(const uint32_t* __restrict__ ci, 
     return lane < 16 && s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
 }
 
-template <int NCHUNK, int FPL, bool VF32, bool SMX, int BPS>
+template <int NCHUNK, int FPL, bool VF32, bool SMX, int BPS, bool HOT = false>
 __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
@@ -421,6 +456,11 @@ __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const S
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
     uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
+    uint64_t pol_last = 0, pol_first = 0;
+    if constexpr (HOT) {
+        pol_last = l2_evict_last_policy();
+        pol_first = l2_cold_policy<TCS_HOT_COLD>();
+    }
     dev::StripedClaim<1> claim;  // this loop form measured 7% faster than next_item here (C5 N=32)
     for (uint32_t idx; claim.get(counter, a.n_items, idx);) {
         const WorkItem it = a.items[idx];
@@ -446,29 +486,29 @@ __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const S
         if (s < vend) {
             // loop-top invariant: s0/s1/s2 hold steps s, s+16, s+32 (issued);
             // c3 = columns of s+48, c0 of s+64, c1 of s+80, c2 of s+96
-            uint32_t c0 = load_col16(ci, s, vend, lane), c1 = load_col16(ci, s + 16, vend, lane);
-            uint32_t c2 = load_col16(ci, s + 32, vend, lane), c3 = load_col16(ci, s + 48, vend, lane);
-            f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s, g, t, q, c0, 0, s0);
-            c0 = load_col16(ci, s + 64, vend, lane);
-            if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, c1, 0, s1);
-            c1 = load_col16(ci, s + 80, vend, lane);
-            if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, c2, 0, s2);
-            c2 = load_col16(ci, s + 96, vend, lane);
+            uint32_t c0 = mark_hot<HOT>(load_col16(ci, s, vend, lane), a.hot), c1 = mark_hot<HOT>(load_col16(ci, s + 16, vend, lane), a.hot);
+            uint32_t c2 = mark_hot<HOT>(load_col16(ci, s + 32, vend, lane), a.hot), c3 = mark_hot<HOT>(load_col16(ci, s + 48, vend, lane), a.hot);
+            f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s, g, t, q, c0, 0, s0, pol_last, pol_first);
+            c0 = mark_hot<HOT>(load_col16(ci, s + 64, vend, lane), a.hot);
+            if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, c1, 0, s1, pol_last, pol_first);
+            c1 = mark_hot<HOT>(load_col16(ci, s + 80, vend, lane), a.hot);
+            if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, c2, 0, s2, pol_last, pol_first);
+            c2 = mark_hot<HOT>(load_col16(ci, s + 96, vend, lane), a.hot);
             for (;;) {
-                if (s + 48 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 48, g, t, q, c3, 0, s3);
-                c3 = load_col16(ci, s + 112, vend, lane);
+                if (s + 48 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 48, g, t, q, c3, 0, s3, pol_last, pol_first);
+                c3 = mark_hot<HOT>(load_col16(ci, s + 112, vend, lane), a.hot);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s0, acc, src_lane, a.scale, sm, sinv);
                 if (s + 16 >= vend) break;
-                if (s + 64 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 64, g, t, q, c0, 0, s0);
-                c0 = load_col16(ci, s + 128, vend, lane);
+                if (s + 64 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 64, g, t, q, c0, 0, s0, pol_last, pol_first);
+                c0 = mark_hot<HOT>(load_col16(ci, s + 128, vend, lane), a.hot);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s1, acc, src_lane, a.scale, sm, sinv);
                 if (s + 32 >= vend) break;
-                if (s + 80 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 80, g, t, q, c1, 0, s1);
-                c1 = load_col16(ci, s + 144, vend, lane);
+                if (s + 80 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 80, g, t, q, c1, 0, s1, pol_last, pol_first);
+                c1 = mark_hot<HOT>(load_col16(ci, s + 144, vend, lane), a.hot);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s2, acc, src_lane, a.scale, sm, sinv);
                 if (s + 48 >= vend) break;
-                if (s + 96 < vend) f16_issue<NCHUNK, FPL, VF32, SMX>(a, Bl, vbase, nvw, vend, s + 96, g, t, q, c2, 0, s2);
-                c2 = load_col16(ci, s + 160, vend, lane);
+                if (s + 96 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 96, g, t, q, c2, 0, s2, pol_last, pol_first);
+                c2 = mark_hot<HOT>(load_col16(ci, s + 160, vend, lane), a.hot);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s3, acc, src_lane, a.scale, sm, sinv);
                 s += 64;
                 if (s >= vend) break;
@@ -946,6 +986,67 @@ __global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_
     }
 }
 
+// Four-stage packed TF32 kernel for 64-feature slabs: three 8-vector gather
+// steps in flight while a fourth is multiplied (the two-stage kernel keeps
+// one; TF32 was latency-bound there, ncu long-scoreboard 6.4 per issue at
+// 16 warps/SM), column indices one 32-vector window ahead.
+#ifndef TCS_TF32P_DEEP
+#define TCS_TF32P_DEEP 0
+#endif
+#ifndef TCS_TF32P_DEEP_BPS
+#define TCS_TF32P_DEEP_BPS 6
+#endif
+__global__ void __launch_bounds__(kWarps * 32, TCS_TF32P_DEEP_BPS) spmm_tf32p_deep(const SpmmArgs a) {
+    constexpr int SLAB = 64;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t g = lane >> 2, t = lane & 3;
+    const uint32_t q = lane >> 3, p = lane & 7, src_lane = 8 * t + g;
+    const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * SLAB;
+    const unsigned char* Bl = static_cast<const unsigned char*>(a.B) + 2 * feat0 + 16 * p;
+    const unsigned char* Ll = static_cast<const unsigned char*>(a.B) + 2 * a.ldp + feat0 / 2 + 4 * p;
+    uint32_t* counter = dev::slab_counter(a.counter, a.slab0 + blockIdx.y);
+    for (uint32_t idx = dev::next_item(counter, lane); idx < a.n_items; idx = dev::next_item(counter, lane)) {
+        const WorkItem it = a.items[idx];
+        const uint32_t base = __ldg(a.rp + it.window);
+        const uint32_t nvw = __ldg(a.rp + it.window + 1) - base;
+        const uint32_t* ci = a.ci + base;
+        const uint64_t vbase = 8ull * base;
+        const uint32_t vend = it.vend;
+        float acc[1][4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[0][j][0] = acc[0][j][1] = acc[0][j][2] = acc[0][j][3] = 0.f;
+        Tf32PStep<1> s0, s1, s2, s3;
+        uint32_t s = it.vbeg;
+        if (s < vend) {
+            // loop-top invariant: s0/s1/s2 hold steps s, s+8, s+16 (issued);
+            // c0 = columns of [s, s+32), c1 = [s+32, s+64)
+            uint32_t c0 = load_colpair(ci, s, vend, lane), c1 = load_colpair(ci, s + 32, vend, lane);
+            tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s, g, t, q, c0, 0, s0);
+            if (s + 8 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 8, g, t, q, c0, 1, s1);
+            if (s + 16 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 16, g, t, q, c0, 2, s2);
+            for (;;) {
+                if (s + 24 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 24, g, t, q, c0, 3, s3);
+                const uint32_t c2 = load_colpair(ci, s + 64, vend, lane);
+                tf32p_compute(s0, acc, src_lane);
+                if (s + 8 >= vend) break;
+                if (s + 32 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 32, g, t, q, c1, 0, s0);
+                tf32p_compute(s1, acc, src_lane);
+                if (s + 16 >= vend) break;
+                if (s + 40 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 40, g, t, q, c1, 1, s1);
+                tf32p_compute(s2, acc, src_lane);
+                if (s + 24 >= vend) break;
+                if (s + 48 < vend) tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 48, g, t, q, c1, 2, s2);
+                tf32p_compute(s3, acc, src_lane);
+                s += 32;
+                if (s >= vend) break;
+                c0 = c1;
+                c1 = c2;
+            }
+        }
+        f16_epilogue<1, 8>(a, it, acc, feat0, g, t);
+    }
+}
+
 // ------------------------------------------------ small lists: burst kernels
 //
 // BASELINE configs[0]/[1] (4096^2, 16 nnz/row: 512 windows of ~123 vectors)
@@ -1014,6 +1115,8 @@ __global__ void __launch_bounds__(kBW * 32, (SPLIT > 1 ? kBurstBlocks : 4) * kWa
     const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * kBW + warp) / SPLIT;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * 32;
     const __half* Bl = static_cast<const __half*>(a.B) + feat0 + p * FPL;
+    pdl_trigger();  // the next small-list kernel may be scheduled now ...
+    pdl_wait();     // ... and this one touches memory only after its predecessor completed
     const bool active = idx < a.n_items;  // every warp reaches the reduction barrier
     float acc[1][FPL / 2][4] = {};
     WorkItem it{};
@@ -1060,6 +1163,8 @@ __global__ void __launch_bounds__(kBW * 32, (SPLIT > 1 ? kBurstBlocks : 4) * kWa
     const uint64_t idx = (static_cast<uint64_t>(blockIdx.x) * kBW + warp) / SPLIT;
     const int64_t feat0 = static_cast<int64_t>(a.slab0 + blockIdx.y) * 32;
     const float* Bl = static_cast<const float*>(a.B) + feat0 + 4 * p;
+    pdl_trigger();  // the next small-list kernel may be scheduled now ...
+    pdl_wait();     // ... and this one touches memory only after its predecessor completed
     const bool active = idx < a.n_items;
     float acc[1][2][4] = {};
     WorkItem it{};
@@ -1089,21 +1194,39 @@ __global__ void __launch_bounds__(kBW * 32, (SPLIT > 1 ? kBurstBlocks : 4) * kWa
 }
 
 // Sums the segments of split windows in segment order (deterministic).
-// n_split_dev (pipelined plans): the real count, on the device.
+// n_split_dev (pipelined plans): the real count, on the device.  One CTA
+// per split window, 4 features per thread, the segments' loads unrolled.
 __global__ void __launch_bounds__(256) spmm_reduce_split(const SplitWindow* __restrict__ split, uint64_t n_split,
                                                          const float* __restrict__ partial, int64_t ldp, float* C,
                                                          int64_t ldc, uint64_t rows, int64_t N,
                                                          const uint32_t* __restrict__ n_split_dev = nullptr) {
     if (n_split_dev) n_split = *n_split_dev;
+    const uint32_t q4 = static_cast<uint32_t>((N + 3) / 4);  // float4 groups per row (ldp % 4 == 0)
     for (uint64_t sw = blockIdx.x; sw < n_split; sw += gridDim.x) {
         const SplitWindow x = split[sw];
-        for (int64_t e = threadIdx.x; e < 8 * N; e += blockDim.x) {
-            const int64_t r = e / N, f = e - r * N;
+        for (uint32_t e = threadIdx.x; e < 8 * q4; e += blockDim.x) {
+            const uint32_t r = e / q4, f = 4 * (e - r * q4);
             const uint64_t row = 8ull * x.window + r;
             if (row >= rows) continue;
-            float acc = 0.f;
-            for (uint32_t q = 0; q < x.nseg; ++q) acc += partial[((uint64_t)(x.first_slot + q) * 8 + r) * ldp + f];
-            C[row * ldc + f] = acc;
+            const float4* p = reinterpret_cast<const float4*>(partial + (uint64_t(x.first_slot) * 8 + r) * ldp + f);
+            const uint64_t step = 2ull * ldp;  // one slot = 8 rows of ldp floats, in float4 units
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            uint32_t q = 0;
+            for (; q + 4 <= x.nseg; q += 4) {
+                const float4 a0 = p[(q + 0) * step], a1 = p[(q + 1) * step], a2 = p[(q + 2) * step],
+                             a3 = p[(q + 3) * step];
+                acc.x += a0.x; acc.y += a0.y; acc.z += a0.z; acc.w += a0.w;
+                acc.x += a1.x; acc.y += a1.y; acc.z += a1.z; acc.w += a1.w;
+                acc.x += a2.x; acc.y += a2.y; acc.z += a2.z; acc.w += a2.w;
+                acc.x += a3.x; acc.y += a3.y; acc.z += a3.z; acc.w += a3.w;
+            }
+            for (; q < x.nseg; ++q) {
+                const float4 a = p[q * step];
+                acc.x += a.x; acc.y += a.y; acc.z += a.z; acc.w += a.w;
+            }
+            float* dst = C + row * ldc + f;
+            const float v[4] = {acc.x, acc.y, acc.z, acc.w};
+            for (int k = 0; k < 4 && f + k < N; ++k) dst[k] = v[k];
         }
     }
 }
@@ -1124,6 +1247,70 @@ void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* 
     const dim3 grid(static_cast<unsigned>(std::min(need, per_slab)), slabs);
     kernel<<<grid, kWarps * 32, 0, s>>>(a);
     TCS_LAUNCHED(name);
+}
+
+// ------------------------------------------- hot dense-operand rows (L2)
+// When B does not fit in L2 (C4: 627 MB at N=128, C5: 537 MB at N=32) an
+// LRU-like L2 keeps whatever was gathered last: ~25% hits on C4, although a
+// power-law graph sends half its gathers to a few percent of the columns.
+// The most-gathered columns whose rows fit TCS_HOT_BUDGET_MB are marked
+// (Plan::col_hot, built once per handle from the column indices) and their
+// gathers carry L2::evict_last, all others L2::evict_first.
+#ifndef TCS_HOT_MIN_MB
+#define TCS_HOT_MIN_MB 96
+#endif
+#ifndef TCS_HOT_BUDGET_MB
+#define TCS_HOT_BUDGET_MB 64
+#endif
+constexpr int kHotBins = 4096;
+
+__global__ void col_count(const uint32_t* __restrict__ ci, uint64_t nv, uint32_t* __restrict__ cnt) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(cnt + ci[p], 1u);
+}
+__global__ void count_hist(const uint32_t* __restrict__ cnt, uint64_t cols, uint32_t* __restrict__ hist) {
+    for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < cols; c += (uint64_t)gridDim.x * blockDim.x)
+        if (cnt[c]) atomicAdd(hist + min(cnt[c], uint32_t(kHotBins - 1)), 1u);
+}
+__global__ void hot_bits(const uint32_t* __restrict__ cnt, uint64_t cols, uint32_t thr, uint32_t* __restrict__ bits) {
+    const uint64_t words = (cols + 31) / 32;
+    for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < words; w += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t m = 0;
+        for (uint32_t b = 0; b < 32 && 32 * w + b < cols; ++b) m |= uint32_t(cnt[32 * w + b] >= thr) << b;
+        bits[w] = m;
+    }
+}
+
+// Plan::col_hot for rows of `rowbytes` (one host round trip, on first use).
+const uint32_t* col_hot(const tcs_mebcrs* A, Plan* plan, uint64_t rowbytes, cudaStream_t s) {
+    if (plan->col_hot && plan->col_hot_rowbytes == rowbytes) return plan->col_hot;
+    const uint64_t cols = A->cols, nv = A->num_vectors;
+    DBuf cnt(std::max<uint64_t>(1, cols) * 4, s), hist(kHotBins * 4, s);
+    TCS_CUDA(cudaMemsetAsync(cnt.p, 0, cols * 4, s));
+    TCS_CUDA(cudaMemsetAsync(hist.p, 0, kHotBins * 4, s));
+    const int sms = num_sms();
+    col_count<<<sms * 8, 256, 0, s>>>(A->column_indices, nv, cnt.as<uint32_t>());
+    TCS_LAUNCHED("col_count");
+    count_hist<<<sms * 4, 256, 0, s>>>(cnt.as<uint32_t>(), cols, hist.as<uint32_t>());
+    TCS_LAUNCHED("count_hist");
+    std::vector<uint32_t> h(kHotBins);
+    TCS_CUDA(cudaMemcpyAsync(h.data(), hist.p, kHotBins * 4, cudaMemcpyDeviceToHost, s));
+    TCS_CUDA(cudaStreamSynchronize(s));
+    // the largest set of most-gathered columns whose rows fit the budget
+    const uint64_t budget = uint64_t(TCS_HOT_BUDGET_MB) << 20;
+    uint32_t thr = kHotBins;  // nothing hot
+    uint64_t rows = 0;
+    for (int b = kHotBins - 1; b >= 2; --b) {  // a row gathered once gains nothing
+        if ((rows + h[b]) * rowbytes > budget) break;
+        rows += h[b];
+        thr = b;
+    }
+    dfree(plan->col_hot, s);
+    plan->col_hot = static_cast<uint32_t*>(dalloc(((cols + 31) / 32) * 4 + 4, s));
+    plan->col_hot_rowbytes = rowbytes;
+    hot_bits<<<sms * 4, 256, 0, s>>>(cnt.as<uint32_t>(), cols, thr, plan->col_hot);
+    TCS_LAUNCHED("hot_bits");
+    return plan->col_hot;
 }
 
 // Feature slab of one warp: 32 / 64 / 128.  Small item lists (BASELINE C1:
@@ -1158,7 +1345,7 @@ int burst_split(const Plan* plan, int slabs) {
 template <typename K>
 void launch_burst(K kernel, const SpmmArgs& a, int split, int slabs, cudaStream_t s, const char* name) {
     const dim3 grid(static_cast<unsigned>((a.n_items * split + kBW - 1) / kBW), slabs);
-    kernel<<<grid, kBW * 32, 0, s>>>(a);
+    launch_pdl(kernel, grid, dim3(kBW * 32), 0, s, a);
     TCS_LAUNCHED(name);
 }
 
@@ -1345,7 +1532,17 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         } else if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
-                if (slab == 128)
+                // hot-row L2 policy: B larger than L2, binary16 values, a
+                // plan with host-side counts (not a pipelined chunk)
+                const bool hot = TCS_HOT && !vf32 && !plan->dcounts && (slab == 128 || slab == 32) &&
+                                 uint64_t(b_rows) * npad * 2 > (uint64_t(TCS_HOT_MIN_MB) << 20);
+                if (hot) a.hot = col_hot(A, plan, uint64_t(npad) * 2, s);
+                if (hot && slab == 128)
+                    launch(spmm_f16_kernel<2, 8, false, false, true>, a, slabs, s, "spmm_f16_hot<128>");
+                else if (hot)
+                    launch(spmm_f16_kernel_deep<1, 4, false, false, TCS_SPMM_DEEP_BPS, true>, a, slabs, s,
+                           "spmm_f16_deep_hot<32>", TCS_SPMM_DEEP_BPS);
+                else if (slab == 128)
                     vf32 ? launch(spmm_f16_kernel<2, 8, true>, a, slabs, s, "spmm_f16<128,f32v>")
                          : launch(spmm_f16_kernel<2, 8, false>, a, slabs, s, "spmm_f16<128>");
                 else if (slab == 64)
@@ -1373,6 +1570,8 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 ap.B = packed.p;
                 ap.ldb = lds;  // bytes
                 if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", tf32p_blocks(2));
+                else if (TCS_TF32P_DEEP)
+                    launch(spmm_tf32p_deep, ap, slabs, s, "spmm_tf32p_deep<64>", TCS_TF32P_DEEP_BPS);
                 else launch(spmm_tf32p_kernel<1>, ap, slabs, s, "spmm_tf32p<64>", tf32p_blocks(1));
             } else {
                 if (slab == 128) launch(spmm_tf32_kernel<4>, a, slabs, s, "spmm_tf32<128>");
@@ -1427,17 +1626,19 @@ extern "C" tcs_status tcs_spmm_host(uint64_t rows, uint64_t cols, tcs_precision 
 
 namespace tcs {
 namespace {
-__global__ void rebase_u32(uint32_t* __restrict__ p, uint64_t n, uint32_t sub) {
+__global__ void rebase_u32(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t n, uint32_t sub) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-        p[i] -= sub;
+        dst[i] = src[i] - sub;
 }
 
 // Compute streams the chunks alternate over.  Two (chunk i's SpMM running
 // while the host waits in chunk i+1's encode) measured no faster than one on
 // C3: each chunk's encode + SpMM starts when it lands and the tail is the
 // last chunk's work either way.
+// Compute streams of the pipeline: chunk i runs on stream i % S, so the
+// small tail chunks (whose latency is mostly their largest window's) overlap.
 #ifndef TCS_E2E_STREAMS
-#define TCS_E2E_STREAMS 1
+#define TCS_E2E_STREAMS 2
 #endif
 struct Streams {
     cudaStream_t copy = nullptr, drain = nullptr;
@@ -1453,6 +1654,16 @@ struct Streams {
         cudaStreamDestroy(drain);
     }
 };
+// The pipeline's side streams, created once per host thread and device
+// (stream creation costs tens of microseconds of host time per call).
+Streams& thread_streams() {
+    static thread_local std::unique_ptr<Streams> per_dev[64];
+    int dev = 0;
+    TCS_CUDA(cudaGetDevice(&dev));
+    auto& p = per_dev[dev & 63];
+    if (!p) p = std::make_unique<Streams>();
+    return *p;
+}
 // TCS_E2E_TRACE=1 (environment): the host pipeline below prints when each
 // chunk landed / was multiplied / was drained (diagnostics).
 bool e2e_trace() {
@@ -1494,11 +1705,54 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         const int64_t b_rows = static_cast<int64_t>(host_csr->cols);
         const uint32_t* hrp = host_csr->row_ptr;
         if (hrp[0] != 0 || hrp[rows] != nnz) fail(TCS_ERR_FORMAT, "row_ptr endpoints inconsistent with nnz");
+        if (rows == 0 || n == 0) {
+            for (uint64_t r = 0; r < rows; ++r)
+                if (hrp[r + 1] < hrp[r]) fail(TCS_ERR_FORMAT, "row_ptr must be nondecreasing");
+            return;
+        }
+        const uint64_t max_chunks = TCS_E2E_MAX_CHUNKS + TCS_E2E_TAIL_HALVINGS + 1;
+
+        // device buffers, allocated in `stream` order before the fork
+        const bool f16 = precision == TCS_FP16;
+        DBuf d_rp_all((rows + 1) * 4, s), d_rp((rows + max_chunks) * 4, s), d_ci(std::max<uint64_t>(1, nnz) * 4, s),
+            d_v(std::max<uint64_t>(1, nnz) * 4, s), d_b32(std::max<int64_t>(1, b_rows * n) * 4, s),
+            d_c(rows * n * 4, s);
+        DBuf d_b16;
+        if (f16) d_b16 = DBuf(std::max<int64_t>(1, b_rows * n) * 2, s);
+        // pipelined chunks (no host round trip per chunk) unless the tcgen05
+        // path is requested (its launcher sizes the work list on the host)
+        const bool pipelined = !(cfg->flags & TCS_CFG_PATH_TCGEN05);
+        DBuf d_flags(max_chunks * 4, s), d_blocks(max_chunks * 8, s);
+        Streams& ss = thread_streams();
+        // On any exit (an error in a later chunk included) the side streams'
+        // queued copies and kernels finish before the buffers above are
+        // released in `stream` order and before control returns to the
+        // caller (the drain stream writes into the caller's host C).
+        struct Join {
+            Streams& ss;
+            bool joined = false;
+            ~Join() {
+                if (joined) return;
+                cudaStreamSynchronize(ss.copy);
+                for (auto c : ss.compute) cudaStreamSynchronize(c);
+                cudaStreamSynchronize(ss.drain);
+            }
+        } join{ss};
+        Event forked;
+        forked.record(s);
+        forked.wait_on(ss.copy);
+        for (auto c : ss.compute) forked.wait_on(c);
+        forked.wait_on(ss.drain);
+
+        // B first: its upload hides the host work below
+        if (b_rows > 0) TCS_CUDA(cudaMemcpyAsync(d_b32.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, ss.copy));
+        Event b_ready;
+        b_ready.record(ss.copy);
+
         // row_ptr is validated here, on the host (the chunk cuts and copies
         // depend on it); column indices are validated by the chunk encodes
         for (uint64_t r = 0; r < rows; ++r)
             if (hrp[r + 1] < hrp[r]) fail(TCS_ERR_FORMAT, "row_ptr must be nondecreasing");
-        if (rows == 0 || n == 0) return;
 
         // Chunk cut points: windows at nnz quantiles (host row_ptr).  The
         // encode of a chunk needs no host round trip (encode_mebcrs_async),
@@ -1526,53 +1780,20 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         }
         wcut[nchunks] = W;
 
-        // device buffers, allocated in `stream` order before the fork
-        const bool f16 = precision == TCS_FP16;
-        DBuf d_rp((rows + nchunks) * 4, s), d_ci(std::max<uint64_t>(1, nnz) * 4, s),
-            d_v(std::max<uint64_t>(1, nnz) * 4, s), d_b32(std::max<int64_t>(1, b_rows * n) * 4, s),
-            d_c(rows * n * 4, s);
-        DBuf d_b16;
-        if (f16) d_b16 = DBuf(std::max<int64_t>(1, b_rows * n) * 2, s);
-        // pipelined chunks (no host round trip per chunk) unless the tcgen05
-        // path is requested (its launcher sizes the work list on the host)
-        const bool pipelined = !(cfg->flags & TCS_CFG_PATH_TCGEN05);
-        DBuf d_flags(nchunks * 4, s), d_blocks(nchunks * 8, s);
-        Streams ss;
-        // On any exit (an error in a later chunk included) the side streams'
-        // queued copies and kernels finish before the buffers above are
-        // released in `stream` order and before control returns to the
-        // caller (the drain stream writes into the caller's host C).
-        struct Join {
-            Streams& ss;
-            bool joined = false;
-            ~Join() {
-                if (joined) return;
-                cudaStreamSynchronize(ss.copy);
-                for (auto c : ss.compute) cudaStreamSynchronize(c);
-                cudaStreamSynchronize(ss.drain);
-            }
-        } join{ss};
-        Event forked;
-        forked.record(s);
-        forked.wait_on(ss.copy);
-        for (auto c : ss.compute) forked.wait_on(c);
-        forked.wait_on(ss.drain);
-
-        Event b_ready;
-        std::vector<Event> landed(nchunks), done(nchunks), encoded(e2e_trace() ? nchunks : 0);
-        if (b_rows > 0) TCS_CUDA(cudaMemcpyAsync(d_b32.p, b, b_rows * n * 4, cudaMemcpyHostToDevice, ss.copy));
-        b_ready.record(ss.copy);
+        // row_ptr in one copy; per chunk its column indices, then its values
+        // (the chunk's ranking kernels need only the former)
+        std::vector<Event> cols_in(nchunks), landed(nchunks), done(nchunks), encoded(e2e_trace() ? nchunks : 0);
+        TCS_CUDA(cudaMemcpyAsync(d_rp_all.p, hrp, (rows + 1) * 4, cudaMemcpyHostToDevice, ss.copy));
         for (uint64_t i = 0; i < nchunks; ++i) {
             const uint64_t r0 = std::min(rows, 8 * wcut[i]), r1 = std::min(rows, 8 * wcut[i + 1]);
             const uint64_t e0 = hrp[r0], e1 = hrp[r1];
-            TCS_CUDA(cudaMemcpyAsync(d_rp.as<uint32_t>() + r0 + i, hrp + r0, (r1 - r0 + 1) * 4, cudaMemcpyHostToDevice,
-                                     ss.copy));
-            if (e1 > e0) {
+            if (e1 > e0)
                 TCS_CUDA(cudaMemcpyAsync(d_ci.as<uint32_t>() + e0, host_csr->col_idx + e0, (e1 - e0) * 4,
                                          cudaMemcpyHostToDevice, ss.copy));
+            cols_in[i].record(ss.copy);
+            if (e1 > e0)
                 TCS_CUDA(cudaMemcpyAsync(d_v.as<float>() + e0, host_csr->values + e0, (e1 - e0) * 4,
                                          cudaMemcpyHostToDevice, ss.copy));
-            }
             landed[i].record(ss.copy);
         }
         // dense operand in the kernel's storage type, once
@@ -1592,20 +1813,19 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             const uint64_t e0 = hrp[r0], e1 = hrp[r1];
             cudaStream_t cs = ss.compute[i % TCS_E2E_STREAMS];
             tcs_stream_t ks = reinterpret_cast<tcs_stream_t>(cs);
-            landed[i].wait_on(cs);
-            uint32_t* rp_i = d_rp.as<uint32_t>() + r0 + i;
-            if (e0) {
-                rebase_u32<<<static_cast<unsigned>(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024)), 256, 0,
-                             cs>>>(rp_i, r1 - r0 + 1, static_cast<uint32_t>(e0));
-                TCS_LAUNCHED("rebase_u32");
-            }
+            cols_in[i].wait_on(cs);
+            uint32_t* rp_i = d_rp.as<uint32_t>() + r0 + i;  // the chunk's row_ptr, rebased to 0
+            rebase_u32<<<static_cast<unsigned>(std::min<uint64_t>((r1 - r0 + 256) / 256, 1024)), 256, 0, cs>>>(
+                d_rp_all.as<uint32_t>() + r0, rp_i, r1 - r0 + 1, static_cast<uint32_t>(e0));
+            TCS_LAUNCHED("rebase_u32");
             tcs_csr chunk{r1 - r0, host_csr->cols, e1 - e0, rp_i, d_ci.as<uint32_t>() + e0, d_v.as<float>() + e0};
             tcs_mebcrs m{};
             tcs_status rc = TCS_OK;
             if (pipelined) {
                 encode_mebcrs_async(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, cs,
-                                    d_flags.as<uint32_t>() + i);
+                                    d_flags.as<uint32_t>() + i, 0, landed[i].e);
             } else {
+                landed[i].wait_on(cs);
                 rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
                 if (rc != TCS_OK) fail(rc, tcs_last_error());
             }

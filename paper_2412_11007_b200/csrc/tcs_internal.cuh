@@ -8,6 +8,7 @@
 #include <atomic>
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -49,6 +50,26 @@ inline void cuda_check(cudaError_t e, const char* what) {
         ::tcs::g_launches.fetch_add(1, std::memory_order_relaxed); \
         ::tcs::cuda_check(cudaGetLastError(), name);         \
     } while (0)
+
+// Launch with the programmatic-stream-serialization attribute (see
+// pdl_wait / pdl_trigger below).  TCS_PDL=0: plain stream order (A/B knob).
+#ifndef TCS_PDL
+#define TCS_PDL 1
+#endif
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = TCS_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    TCS_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
 
 // Runs `body`, mapping exceptions onto status codes (no exception crosses
 // the C-ABI).
@@ -145,12 +166,18 @@ struct Plan {
     // dcounts[0] (= capacity - real items) walks exactly them; dcounts[1] is
     // the real number of split windows; dcounts[2..3] the u64 block count.
     uint32_t* dcounts = nullptr;  // device
+    // Hot dense-operand rows (tcs_spmm when B does not fit in L2): bit c set
+    // iff column c is among the most gathered columns whose B rows fit the
+    // hot budget at `col_hot_rowbytes` per row; those gathers are issued
+    // L2::evict_last, the rest evict_first.  Built on first use, kept.
+    uint32_t* col_hot = nullptr;  // device, ceil(cols / 32) words
+    uint64_t col_hot_rowbytes = 0;
 };
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16);
-Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, cudaStream_t s);
+Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, uint64_t seg_nv, cudaStream_t s);
 void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                         cudaStream_t s, uint32_t* bad_dev);
+                         cudaStream_t s, uint32_t* bad_dev, uint64_t seg_nv, cudaEvent_t values_ready);
 const char* encode_bad_msg(uint32_t code);
 void free_plan(Plan* p, cudaStream_t s);
 
@@ -245,6 +272,17 @@ __device__ __forceinline__ uint32_t* slab_counter(uint32_t* counters, uint32_t s
     return counters + static_cast<uint64_t>(slab) * (kClaimBytes / 4);
 }
 
+// Programmatic dependent launch.  A kernel launched with launch_pdl may be
+// scheduled while the previous kernel on the stream is still draining (once
+// that kernel has executed pdl_trigger, or at its exit); it must execute
+// pdl_wait() -- which returns when the previous grid has completed and its
+// memory is visible -- before it touches global memory.  Without the launch
+// attribute both instructions are no-ops.  Used by the latency-bound small-
+// list kernels, whose launch latency is then hidden behind their
+// predecessor's tail (back-to-back calls, CUDA graphs).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // RNE fp32 -> tf32 (cvt.rn.tf32.f32, sm_90+); matches the reference's
 // round_to_tf32 (ref precision.hpp:42-46; inf/NaN pass through).
 __device__ __forceinline__ uint32_t to_tf32(float x) {
@@ -328,6 +366,33 @@ __device__ __forceinline__ uint2 ld_gather_64(const void* p) {
     uint2 v;
     asm volatile("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
     return v;
+}
+// The same gathers with an explicit L2 cache policy (createpolicy): hot
+// dense-operand rows evict_last, cold ones evict_first (see Plan::col_hot).
+__device__ __forceinline__ uint4 ld_gather_128_pol(const void* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.b32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_gather_64_pol(const void* p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.b32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+template <int KIND>  // 0 evict_first, 1 evict_normal, 2 evict_unchanged
+__device__ __forceinline__ uint64_t l2_cold_policy() {
+    uint64_t pol;
+    if constexpr (KIND == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    else if constexpr (KIND == 1) asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    else asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
 }
 __device__ __forceinline__ void st_stream_f4(float* p, float a, float b, float c, float d) {
     asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(a), "f"(b), "f"(c),
