@@ -454,8 +454,15 @@ tcs_status tcs_sddmm_host(uint64_t rows, uint64_t cols, tcs_precision precision,
                           tcs_stream_t stream);
 
 /* The reference CLI's spmm pipeline (ref cli.hpp:162-200: encode_mebcrs
- * then spmm) from host buffers: host CSR + host f32 B -> host f32 C.  H2D,
- * GPU conversion, SpMM and D2H all run on `stream`. */
+ * then spmm) from host buffers: host CSR + host f32 B -> host f32 C.
+ * Pipelined over row-window chunks on side streams forked from and joined
+ * back to `stream` (returns when C is in host memory): B uploads first,
+ * then each chunk's column indices and values; a chunk is converted (no
+ * host round trip) and multiplied as soon as it has landed, and its C rows
+ * are copied back while later chunks upload.  row_ptr is validated on the
+ * host before any chunk is queued; column indices are validated by the
+ * chunk conversions, and a violation is reported (FORMAT, the reference's
+ * message) after the pipeline drains -- C is then unspecified. */
 tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision precision, const float* b, int64_t n,
                              float* c, const tcs_kernel_config* cfg, tcs_counters* counters,
                              tcs_stream_t stream);

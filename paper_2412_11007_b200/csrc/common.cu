@@ -299,6 +299,7 @@ void free_plan(Plan* p, cudaStream_t s) {
     if (!p) return;
     dfree(p->dcounts, s);
     dfree(p->col_hot, s);
+    dfree(p->ci_hot, s);
     dfree(p->items, s);
     dfree(p->split, s);
     dfree(p->live, s);

@@ -44,7 +44,10 @@ constexpr uint32_t kSmallCap = 2048;    // entries per window, 128-thread CTA, 3
 constexpr uint32_t kSmallThreads = 128;
 constexpr uint32_t kBigCap = 12288;     // 512-thread CTA, 192 KB smem
 constexpr uint32_t kBigThreads = 512;
-constexpr uint32_t kBitmapThreads = 512;
+#ifndef TCS_ENC_BITMAP_THREADS
+#define TCS_ENC_BITMAP_THREADS 512
+#endif
+constexpr uint32_t kBitmapThreads = TCS_ENC_BITMAP_THREADS;
 constexpr uint32_t kBitmapMaxWords = 25600;
 constexpr int kBitmapU = 8;  // entries per thread in flight (window_bitmap)  // 2 x 100 KB of smem -> <= 819,200 columns
 constexpr uint64_t kSentinel = ~0ull;
@@ -495,8 +498,14 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 // kSmallCap-vector tile, many per SM -- a 512-thread CTA's barriers dominate
 // on windows of a few hundred vectors (R-MAT: 10^6 windows of ~240); big
 // windows get 512 threads and 4096-vector tiles.
-constexpr uint32_t kScatterTileBig = 4096;  // vectors per smem tile (multiple of k)
-constexpr int kScatterThreadsBig = 512;
+#ifndef TCS_ENC_SCATTER_TILE
+#define TCS_ENC_SCATTER_TILE 4096
+#endif
+#ifndef TCS_ENC_SCATTER_THREADS
+#define TCS_ENC_SCATTER_THREADS 512
+#endif
+constexpr uint32_t kScatterTileBig = TCS_ENC_SCATTER_TILE;  // vectors per smem tile (multiple of k)
+constexpr int kScatterThreadsBig = TCS_ENC_SCATTER_THREADS;
 constexpr uint32_t kScatterTileSmall = kSmallCap;
 constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
@@ -815,7 +824,8 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                     const size_t smem = 2 * words * sizeof(uint32_t);
                     TCS_CUDA(cudaFuncSetAttribute(window_bitmap<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(std::max<size_t>(smem, 1))));
-                    const int per_sm = std::max<int>(1, std::min<int>(4, int(200 * 1024 / std::max<size_t>(smem, 1))));
+                    const int per_sm = std::max<int>(
+                        1, std::min<int>(2048 / kBitmapThreads, int(200 * 1024 / std::max<size_t>(smem, 1))));
                     const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
                     window_bitmap<VH><<<g2, kBitmapThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),

@@ -95,7 +95,7 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 // each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
 // tail after the last upload (the last chunk's encode + SpMM + download).
 #ifndef TCS_E2E_MAX_CHUNKS
-#define TCS_E2E_MAX_CHUNKS 12
+#define TCS_E2E_MAX_CHUNKS 16
 #endif
 #ifndef TCS_E2E_TAIL_HALVINGS
 #define TCS_E2E_TAIL_HALVINGS 3
@@ -130,6 +130,21 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_HOT_COLD
 #define TCS_HOT_COLD 0
 #endif
+// The FP16 (128-feature slabs) and packed-TF32 SpMM kernels prefetch the
+// sparse-value and column-index streams into L2 this many vectors ahead of
+// their loads (PF instances), when the dense operand fits comfortably in L2
+// (<= TCS_PREFETCH_MAX_B_MB): the streamed lines then no longer wait on
+// DRAM.  With a larger B the extra L2 traffic costs more than it hides
+// (C3 N=256: +3-7%).  Measured in profiles/r2_prefetch.txt.
+#ifndef TCS_PREFETCH_AHEAD
+#define TCS_PREFETCH_AHEAD 64
+#endif
+#ifndef TCS_PREFETCH_F16
+#define TCS_PREFETCH_F16 128
+#endif
+#ifndef TCS_PREFETCH_MAX_B_MB
+#define TCS_PREFETCH_MAX_B_MB 80
+#endif
 #ifndef TCS_SMALL_SLAB32
 #define TCS_SMALL_SLAB32 1
 #endif
@@ -154,13 +169,9 @@ __device__ __forceinline__ uint32_t load_colpair(const uint32_t* __restrict__ ci
                                                  uint32_t lane) {
     return s + lane < vend ? ld_stream_u32(ci + s + lane) : 0u;
 }
-// HOT kernels: the column's Plan::col_hot bit rides in bit 31 (columns are
-// < 2^31; the gather masks it off and picks the L2 policy from it).
-template <bool HOT>
-__device__ __forceinline__ uint32_t mark_hot(uint32_t c, const uint32_t* __restrict__ hot) {
-    if constexpr (HOT) c |= ((__ldg(hot + (c >> 5)) >> (c & 31)) & 1u) << 31;
-    return c;
-}
+// HOT kernels read Plan::ci_hot, a copy of the column indices whose bit 31
+// marks a hot column (columns are < 2^31; the gather masks it off and picks
+// the L2 policy from it).
 constexpr uint32_t kColMask = 0x7FFFFFFFu;
 
 // ------------------------------------------------------------- FP16 path
@@ -367,7 +378,7 @@ __device__ __forceinline__ void f16_epilogue(const SpmmArgs& a, const WorkItem& 
     }
 }
 
-template <int NCHUNK, int FPL, bool VF32, bool SMX = false, bool HOT = false>
+template <int NCHUNK, int FPL, bool VF32, bool SMX = false, bool HOT = false, bool PF = false>
 __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f16_kernel(const SpmmArgs a) {
     constexpr int NJ = FPL / 2, CHUNK = 8 * FPL, SLAB = NCHUNK * CHUNK;
     const uint32_t lane = threadIdx.x & 31;
@@ -408,11 +419,17 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
         F16Step<NCHUNK, FPL, VF32> sa, sb;
         uint32_t s = it.vbeg;
         if (s < vend) {
-            uint32_t cp0 = mark_hot<HOT>(load_colpair(ci, s, vend, lane), a.hot);       // steps s, s+16
-            uint32_t cp1 = mark_hot<HOT>(load_colpair(ci, s + 32, vend, lane), a.hot);  // steps s+32, s+48
+            uint32_t cp0 = load_colpair(ci, s, vend, lane);       // steps s, s+16
+            uint32_t cp1 = load_colpair(ci, s + 32, vend, lane);  // steps s+32, s+48
             f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s, g, t, q, cp0, 0, sa, pol_last,
                                                          pol_first);
             for (;;) {
+                if constexpr (PF && !VF32) {  // 32 vectors = 512 B of f16 values per iteration
+                    const uint32_t pv = s + TCS_PREFETCH_F16;
+                    if (lane < 4 && pv < vend && blockIdx.y == 0)
+                        prefetch_l2(static_cast<const __half*>(a.vals) + vbase + 8ull * pv + 64 * lane);
+                    if (lane == 4 && pv < vend && blockIdx.y == 0) prefetch_l2(ci + pv);
+                }
                 if (s + 16 < vend)
                     f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, cp0, 1, sb,
                                                                  pol_last, pol_first);
@@ -422,7 +439,7 @@ __global__ void __launch_bounds__(kWarps * 32, spmm_blocks(NCHUNK, FPL)) spmm_f1
                     f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, cp1, 0, sa,
                                                                  pol_last, pol_first);
                 cp0 = cp1;
-                cp1 = mark_hot<HOT>(load_colpair(ci, s + 64, vend, lane), a.hot);
+                cp1 = load_colpair(ci, s + 64, vend, lane);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(sb, acc, src_lane, a.scale, sm, sinv);
                 s += 32;
                 if (s >= vend) break;
@@ -486,29 +503,29 @@ __global__ void __launch_bounds__(kWarps * 32, BPS) spmm_f16_kernel_deep(const S
         if (s < vend) {
             // loop-top invariant: s0/s1/s2 hold steps s, s+16, s+32 (issued);
             // c3 = columns of s+48, c0 of s+64, c1 of s+80, c2 of s+96
-            uint32_t c0 = mark_hot<HOT>(load_col16(ci, s, vend, lane), a.hot), c1 = mark_hot<HOT>(load_col16(ci, s + 16, vend, lane), a.hot);
-            uint32_t c2 = mark_hot<HOT>(load_col16(ci, s + 32, vend, lane), a.hot), c3 = mark_hot<HOT>(load_col16(ci, s + 48, vend, lane), a.hot);
+            uint32_t c0 = load_col16(ci, s, vend, lane), c1 = load_col16(ci, s + 16, vend, lane);
+            uint32_t c2 = load_col16(ci, s + 32, vend, lane), c3 = load_col16(ci, s + 48, vend, lane);
             f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s, g, t, q, c0, 0, s0, pol_last, pol_first);
-            c0 = mark_hot<HOT>(load_col16(ci, s + 64, vend, lane), a.hot);
+            c0 = load_col16(ci, s + 64, vend, lane);
             if (s + 16 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 16, g, t, q, c1, 0, s1, pol_last, pol_first);
-            c1 = mark_hot<HOT>(load_col16(ci, s + 80, vend, lane), a.hot);
+            c1 = load_col16(ci, s + 80, vend, lane);
             if (s + 32 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 32, g, t, q, c2, 0, s2, pol_last, pol_first);
-            c2 = mark_hot<HOT>(load_col16(ci, s + 96, vend, lane), a.hot);
+            c2 = load_col16(ci, s + 96, vend, lane);
             for (;;) {
                 if (s + 48 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 48, g, t, q, c3, 0, s3, pol_last, pol_first);
-                c3 = mark_hot<HOT>(load_col16(ci, s + 112, vend, lane), a.hot);
+                c3 = load_col16(ci, s + 112, vend, lane);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s0, acc, src_lane, a.scale, sm, sinv);
                 if (s + 16 >= vend) break;
                 if (s + 64 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 64, g, t, q, c0, 0, s0, pol_last, pol_first);
-                c0 = mark_hot<HOT>(load_col16(ci, s + 128, vend, lane), a.hot);
+                c0 = load_col16(ci, s + 128, vend, lane);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s1, acc, src_lane, a.scale, sm, sinv);
                 if (s + 32 >= vend) break;
                 if (s + 80 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 80, g, t, q, c1, 0, s1, pol_last, pol_first);
-                c1 = mark_hot<HOT>(load_col16(ci, s + 144, vend, lane), a.hot);
+                c1 = load_col16(ci, s + 144, vend, lane);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s2, acc, src_lane, a.scale, sm, sinv);
                 if (s + 48 >= vend) break;
                 if (s + 96 < vend) f16_issue<NCHUNK, FPL, VF32, SMX, true, HOT>(a, Bl, vbase, nvw, vend, s + 96, g, t, q, c2, 0, s2, pol_last, pol_first);
-                c2 = mark_hot<HOT>(load_col16(ci, s + 160, vend, lane), a.hot);
+                c2 = load_col16(ci, s + 160, vend, lane);
                 f16_compute<NCHUNK, FPL, VF32, SMX>(s3, acc, src_lane, a.scale, sm, sinv);
                 s += 64;
                 if (s >= vend) break;
@@ -927,7 +944,7 @@ __device__ __forceinline__ void tf32p_compute(const Tf32PStep<NCHUNK>& st, float
 #endif
 constexpr int tf32p_blocks(int nchunk) { return nchunk == 1 ? TCS_TF32P_BPS_NARROW : TCS_TF32P_BPS_WIDE; }
 // a.B = packed rows (tf32_pack_kernel), a.ldb = their stride in BYTES.
-template <int NCHUNK>
+template <int NCHUNK, bool PF = false>
 __global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_kernel(const SpmmArgs a) {
     constexpr int SLAB = NCHUNK * 64;
     const uint32_t lane = threadIdx.x & 31;
@@ -961,6 +978,12 @@ __global__ void __launch_bounds__(kWarps * 32, tf32p_blocks(NCHUNK)) spmm_tf32p_
             uint32_t nxt = load_colpair(ci, s0 + 32, vend, lane);
             tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s, g, t, q, cur, 0, sa);
             for (;;) {
+                if constexpr (PF) {  // 16 vectors = 512 B of f32 values per iteration
+                    const uint32_t pv = s + TCS_PREFETCH_AHEAD;
+                    if (lane < 4 && pv < vend && blockIdx.y == 0)  // one slab prefetches for all
+                        prefetch_l2(static_cast<const float*>(a.vals) + vbase + 8ull * pv + 32 * lane);
+                    if (lane == 4 && pv < vend && blockIdx.y == 0) prefetch_l2(ci + pv);
+                }
                 if (s + 8 < vend) {
                     const uint32_t sub = (s + 8 - s0) >> 3;
                     tf32p_issue(a, Bl, Ll, vbase, nvw, vend, s + 8, g, t, q, sub < 4 ? cur : nxt, sub & 3, sb);
@@ -1263,6 +1286,7 @@ void launch(K kernel, const SpmmArgs& a, int slabs, cudaStream_t s, const char* 
 #define TCS_HOT_BUDGET_MB 64
 #endif
 constexpr int kHotBins = 4096;
+constexpr uint64_t kPrefetchMaxB = uint64_t(TCS_PREFETCH_MAX_B_MB) << 20;
 
 __global__ void col_count(const uint32_t* __restrict__ ci, uint64_t nv, uint32_t* __restrict__ cnt) {
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x)
@@ -1281,9 +1305,18 @@ __global__ void hot_bits(const uint32_t* __restrict__ cnt, uint64_t cols, uint32
     }
 }
 
-// Plan::col_hot for rows of `rowbytes` (one host round trip, on first use).
+__global__ void mark_hot_cols(const uint32_t* __restrict__ ci, uint64_t nv, const uint32_t* __restrict__ bits,
+                              uint32_t* __restrict__ out) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < nv; p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = ci[p];
+        out[p] = c | (((bits[c >> 5] >> (c & 31)) & 1u) << 31);
+    }
+}
+
+// Plan::col_hot / Plan::ci_hot for rows of `rowbytes` (one host round trip,
+// on first use); returns the marked column indices.
 const uint32_t* col_hot(const tcs_mebcrs* A, Plan* plan, uint64_t rowbytes, cudaStream_t s) {
-    if (plan->col_hot && plan->col_hot_rowbytes == rowbytes) return plan->col_hot;
+    if (plan->ci_hot && plan->col_hot_rowbytes == rowbytes) return plan->ci_hot;
     const uint64_t cols = A->cols, nv = A->num_vectors;
     DBuf cnt(std::max<uint64_t>(1, cols) * 4, s), hist(kHotBins * 4, s);
     TCS_CUDA(cudaMemsetAsync(cnt.p, 0, cols * 4, s));
@@ -1306,11 +1339,15 @@ const uint32_t* col_hot(const tcs_mebcrs* A, Plan* plan, uint64_t rowbytes, cuda
         thr = b;
     }
     dfree(plan->col_hot, s);
+    dfree(plan->ci_hot, s);
     plan->col_hot = static_cast<uint32_t*>(dalloc(((cols + 31) / 32) * 4 + 4, s));
+    plan->ci_hot = static_cast<uint32_t*>(dalloc(std::max<uint64_t>(1, nv) * 4, s));
     plan->col_hot_rowbytes = rowbytes;
     hot_bits<<<sms * 4, 256, 0, s>>>(cnt.as<uint32_t>(), cols, thr, plan->col_hot);
     TCS_LAUNCHED("hot_bits");
-    return plan->col_hot;
+    mark_hot_cols<<<sms * 8, 256, 0, s>>>(A->column_indices, nv, plan->col_hot, plan->ci_hot);
+    TCS_LAUNCHED("mark_hot_cols");
+    return plan->ci_hot;
 }
 
 // Feature slab of one warp: 32 / 64 / 128.  Small item lists (BASELINE C1:
@@ -1532,16 +1569,19 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
         } else if (plan->n_items && !launched) {
             if (A->precision == TCS_FP16) {
                 const bool vf32 = A->value_dtype == TCS_DTYPE_F32;
+                const uint64_t b_bytes = uint64_t(b_rows) * npad * 2;  // the f16 operand as gathered
                 // hot-row L2 policy: B larger than L2, binary16 values, a
                 // plan with host-side counts (not a pipelined chunk)
                 const bool hot = TCS_HOT && !vf32 && !plan->dcounts && (slab == 128 || slab == 32) &&
                                  uint64_t(b_rows) * npad * 2 > (uint64_t(TCS_HOT_MIN_MB) << 20);
-                if (hot) a.hot = col_hot(A, plan, uint64_t(npad) * 2, s);
+                if (hot) a.ci = col_hot(A, plan, uint64_t(npad) * 2, s);
                 if (hot && slab == 128)
                     launch(spmm_f16_kernel<2, 8, false, false, true>, a, slabs, s, "spmm_f16_hot<128>");
                 else if (hot)
                     launch(spmm_f16_kernel_deep<1, 4, false, false, TCS_SPMM_DEEP_BPS, true>, a, slabs, s,
                            "spmm_f16_deep_hot<32>", TCS_SPMM_DEEP_BPS);
+                else if (slab == 128 && !vf32 && TCS_PREFETCH_F16 > 0 && b_bytes <= kPrefetchMaxB)
+                    launch(spmm_f16_kernel<2, 8, false, false, false, true>, a, slabs, s, "spmm_f16_pf<128>");
                 else if (slab == 128)
                     vf32 ? launch(spmm_f16_kernel<2, 8, true>, a, slabs, s, "spmm_f16<128,f32v>")
                          : launch(spmm_f16_kernel<2, 8, false>, a, slabs, s, "spmm_f16<128>");
@@ -1569,7 +1609,12 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 SpmmArgs ap = a;
                 ap.B = packed.p;
                 ap.ldb = lds;  // bytes
-                if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", tf32p_blocks(2));
+                const bool pf = TCS_PREFETCH_AHEAD > 0 && uint64_t(b_rows) * lds <= kPrefetchMaxB;
+                if (slab == 128 && pf)
+                    launch(spmm_tf32p_kernel<2, true>, ap, slabs, s, "spmm_tf32p_pf<128>", tf32p_blocks(2));
+                else if (slab == 128) launch(spmm_tf32p_kernel<2>, ap, slabs, s, "spmm_tf32p<128>", tf32p_blocks(2));
+                else if (pf && !TCS_TF32P_DEEP)
+                    launch(spmm_tf32p_kernel<1, true>, ap, slabs, s, "spmm_tf32p_pf<64>", tf32p_blocks(1));
                 else if (TCS_TF32P_DEEP)
                     launch(spmm_tf32p_deep, ap, slabs, s, "spmm_tf32p_deep<64>", TCS_TF32P_DEEP_BPS);
                 else launch(spmm_tf32p_kernel<1>, ap, slabs, s, "spmm_tf32p<64>", tf32p_blocks(1));

@@ -171,6 +171,7 @@ struct Plan {
     // hot budget at `col_hot_rowbytes` per row; those gathers are issued
     // L2::evict_last, the rest evict_first.  Built on first use, kept.
     uint32_t* col_hot = nullptr;  // device, ceil(cols / 32) words
+    uint32_t* ci_hot = nullptr;   // device, column indices with the hot bit in bit 31
     uint64_t col_hot_rowbytes = 0;
 };
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
@@ -324,6 +325,11 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const void* p) {
     uint32_t v;
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
+}
+// L2 prefetch of one line (the sparse value / column streams, a few steps
+// ahead of their loads, so those hit L2 instead of waiting on DRAM).
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 // L2 evict-first policy (createpolicy) for read-once streams, so they do not
 // displace an L2-resident gathered operand.
