@@ -603,8 +603,11 @@ def run_ours(args, rank, world, device):
                      "traffic": dram["bytes_per_launch"] if dram else None, "peak_source": peak_src,
                      "bytes_alg_per_launch": balg, "bytes_min_per_launch": bmin,
                      "frac_bytes_min": round(bmin / (step_ms / 1e3) / 1e9 / peak, 4),
-                     "kernel": "spmm_f16_kernel<2,8> (mma.sync, + spmm_reduce_split)" if prec == 0 else "spmm_tf32_kernel<4>",
-                     "binding_resource": "l2_gather" if prec == 0 else "dram latency (31% of gather sectors miss L2)",
+                     "kernel": ("spmm_f16_kernel<2,8> (mma.sync; L2-prefetch instance when B <= 80 MB) + claim-counter "
+                                "memset + spmm_reduce_split") if prec == 0 else
+                               "tf32_pack_kernel + spmm_tf32p_kernel<2> (mma.sync on the 2.5-byte packed operand)",
+                     "binding_resource": ("l2_gather (L1 data pipe: one LDG + one SHFL wavefront per 128 B)" if prec == 0
+                                          else "gather latency (long-scoreboard; 16 warps/SM at 121 registers)"),
                      "dram": _with_frac(dram, step_ms),
                      "l2_gather": {"gather_bytes_per_launch": gather_bytes,
                                    "achieved_gbs": round(gather_bytes / (step_ms / 1e3) / 1e9, 1),
