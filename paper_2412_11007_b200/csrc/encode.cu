@@ -406,20 +406,25 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
                                                                 uint32_t* __restrict__ rank,
                                                                 uint32_t* __restrict__ nv_out, CheckOut* chk,
                                                                 const uint32_t* __restrict__ big) {
-    extern __shared__ uint32_t bm_smem[];
+    extern __shared__ uint4 bm_smem4[];
     const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
-    const uint32_t words = static_cast<uint32_t>((cols + 31) / 32);
-    uint32_t* bm = bm_smem;
-    uint32_t* pre = bm_smem + words;
+    // the word arrays are walked as uint4 quads (a quarter of the
+    // instructions of the clear / scan / emit loops, which dominated: ncu
+    // issue-active 62%); words padded to a multiple of 4
+    const uint32_t quads = static_cast<uint32_t>((cols + 127) / 128);
+    uint4* bm4 = bm_smem4;
+    uint4* pre4 = bm_smem4 + quads;
+    const uint32_t* bm = reinterpret_cast<const uint32_t*>(bm4);
+    const uint32_t* pre = reinterpret_cast<const uint32_t*>(pre4);
     __shared__ uint32_t rb[VH + 1];
-    const uint32_t nt = blockDim.x, wpt = (words + nt - 1) / nt;
+    const uint32_t nt = blockDim.x, qpt = (quads + nt - 1) / nt;
     for (uint32_t bi = cta_next(&chk->next_bitmap); bi < n_big; bi = cta_next(&chk->next_bitmap)) {
         const uint64_t w = big_window(big, W, n_huge, bi);
         const uint64_t r0 = VH * w;
         const uint32_t e0 = csr_rp[r0];
         const uint32_t n = csr_rp[min(r0 + VH, rows)] - e0;
         if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
-        for (uint32_t i = threadIdx.x; i < words; i += nt) bm[i] = 0u;
+        for (uint32_t i = threadIdx.x; i < quads; i += nt) bm4[i] = make_uint4(0, 0, 0, 0);
         __syncthreads();
         // kBitmapU entries per thread in flight: a hub window (10^4..10^5
         // entries) is otherwise a chain of dependent-latency iterations
@@ -442,24 +447,34 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
                 // check_col with the predecessor already loaded
                 const uint32_t b = !row_start && cp[u] >= c[u] ? 4u : c[u] >= cols ? 3u : 0u;
                 bad = max(bad, b);
-                if (c[u] < cols) atomicOr(&bm[c[u] >> 5], 1u << (c[u] & 31));
+                if (c[u] < cols) atomicOr(reinterpret_cast<uint32_t*>(bm4) + (c[u] >> 5), 1u << (c[u] & 31));
             }
         }
         if (bad) atomicMax(&chk->bad, bad);
         __syncthreads();
-        // prefix popcount over this thread's contiguous chunk of words
-        const uint32_t w0 = min(words, threadIdx.x * wpt), w1 = min(words, w0 + wpt);
+        // prefix popcount over this thread's contiguous run of quads
+        const uint32_t q0 = min(quads, threadIdx.x * qpt), q1 = min(quads, q0 + qpt);
         uint32_t cnt = 0;
-        for (uint32_t i = w0; i < w1; ++i) cnt += __popc(bm[i]);
+        for (uint32_t i = q0; i < q1; ++i) {
+            const uint4 x = bm4[i];
+            cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        }
         uint32_t total;
         uint32_t run = dev::block_exclusive_scan(cnt, &total);
-        for (uint32_t i = w0; i < w1; ++i) {
-            pre[i] = run;
-            uint32_t bits = bm[i];
-            while (bits) {  // sorted unique columns of the window
-                const uint32_t b = __ffs(bits) - 1;
-                tmp_cols[e0 + run++] = 32 * i + b;
-                bits &= bits - 1;
+        for (uint32_t i = q0; i < q1; ++i) {
+            const uint4 x = bm4[i];
+            const uint32_t p0 = run, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
+            pre4[i] = make_uint4(p0, p1, p2, p3);
+            if ((x.x | x.y | x.z | x.w) == 0u) continue;
+            const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t bits = wv[k];
+                while (bits) {  // sorted unique columns of the window
+                    const uint32_t b = __ffs(bits) - 1;
+                    tmp_cols[e0 + run++] = 32 * (4 * i + k) + b;
+                    bits &= bits - 1;
+                }
             }
         }
         if (threadIdx.x == 0) nv_out[w] = total;
@@ -510,6 +525,7 @@ constexpr uint32_t kScatterTileSmall = kSmallCap;
 constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
 constexpr uint32_t kTileBatch = 63;   // tile boundaries searched at once (64 x VH threads)
+constexpr int kScatterU = 8;          // entries in flight per thread (window_scatter)
 
 // Tiles of each huge window (vectors / tile), exclusive prefix over the
 // huge list (one CTA; the huge list is short) -> tile_off[0..n_huge], total
@@ -593,7 +609,21 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
         const uint32_t e0 = rb[0], e1 = rb[VH];
         const uint32_t v_lo = min(nvw, tile_lo * kTile);
         const uint32_t v_hi = uint64_t(tile_hi) * kTile < nvw ? tile_hi * kTile : nvw;
-        for (uint32_t i = v_lo + threadIdx.x; i < v_hi; i += blockDim.x) out_ci[base + i] = tmp_cols[e0 + i];
+        // the column copy, 8 loads in flight per thread (one at a time it was
+        // the kernel's top stall: a DRAM latency per 512 columns)
+        for (uint32_t i0 = v_lo + threadIdx.x; i0 < v_hi; i0 += 8 * blockDim.x) {
+            uint32_t cc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                cc[u] = i < v_hi ? __ldg(tmp_cols + e0 + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                if (i < v_hi) out_ci[base + i] = cc[u];
+            }
+        }
         V* vals = out_vals + static_cast<uint64_t>(VH) * base;
         // block-uniform: a window of at most kRangedTiles tiles scans all of
         // its entries per tile and keeps those of the tile (cheap for few
@@ -636,12 +666,12 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                 __syncthreads();
             }
             const uint32_t total = ranged ? roff[VH] : e1 - e0;
-            // 4 entries in flight per thread (coalesced per sub-step)
-            for (uint32_t i4 = 0; i4 < total; i4 += 4 * blockDim.x) {
-                uint32_t v[4], e[4];
-                float x[4];
+            // kScatterU entries in flight per thread (coalesced per sub-step)
+            for (uint32_t i4 = 0; i4 < total; i4 += kScatterU * blockDim.x) {
+                uint32_t v[kScatterU], e[kScatterU];
+                float x[kScatterU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kScatterU; ++u) {
                     const uint32_t i = i4 + u * blockDim.x + threadIdx.x;
                     e[u] = 0xFFFFFFFFu;
                     if (i < total) {
@@ -658,7 +688,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                     x[u] = e[u] != 0xFFFFFFFFu ? __ldg(csr_vals + e[u]) : 0.f;
                 }
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < kScatterU; ++u) {
                     if (e[u] == 0xFFFFFFFFu || v[u] < t0 || v[u] >= t0 + tn) continue;
                     uint32_t r = 0;
 #pragma unroll
@@ -821,7 +851,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             if (n_big) {
                 const uint64_t words = (cols + 31) / 32;
                 if (words <= kBitmapMaxWords) {
-                    const size_t smem = 2 * words * sizeof(uint32_t);
+                    const size_t smem = 2 * ((words + 3) / 4) * sizeof(uint4);
                     TCS_CUDA(cudaFuncSetAttribute(window_bitmap<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(std::max<size_t>(smem, 1))));
                     const int per_sm = std::max<int>(
