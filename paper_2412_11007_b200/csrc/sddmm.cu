@@ -504,6 +504,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinBlocks<NSC>) sddmm_kernel(con
 // Single pass only (FP16 K <= 32*NSC, TF32 K <= 16*NSC).  With no split
 // windows item i is window i (a.items == nullptr).
 constexpr int kBurstBlocks = 8;
+// groups per burst of the single-super-chunk SDDMM burst kernel (A/B knob)
+#ifndef TCS_SDDMM_BURST_G
+#define TCS_SDDMM_BURST_G 2
+#endif
 #ifndef TCS_BURST_WARPS
 #define TCS_BURST_WARPS 4
 #endif
@@ -743,10 +747,10 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
         if (static_mask) b.live = mask_liveness(mask, plan, s);
         else if (const uint8_t* ex = plan->exact_for(mask->values)) b.live = ex;
         if (tf32) {
-            if (nsc == 1) launch_sddmm_burst<true, 1, 2>(b, mf32, of32, s);
+            if (nsc == 1) launch_sddmm_burst<true, 1, TCS_SDDMM_BURST_G>(b, mf32, of32, s);
             else launch_sddmm_burst<true, 2, 1>(b, mf32, of32, s);
         } else {
-            if (nsc == 1) launch_sddmm_burst<false, 1, 2>(b, mf32, of32, s);
+            if (nsc == 1) launch_sddmm_burst<false, 1, TCS_SDDMM_BURST_G>(b, mf32, of32, s);
             else launch_sddmm_burst<false, 2, 1>(b, mf32, of32, s);
         }
         return;

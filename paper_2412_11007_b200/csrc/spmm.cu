@@ -145,6 +145,10 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_PREFETCH_MAX_B_MB
 #define TCS_PREFETCH_MAX_B_MB 80
 #endif
+// B-row gathers with L1::no_allocate (A/B knob; 0 = plain ld.global.nc).
+#ifndef TCS_GATHER_NA
+#define TCS_GATHER_NA 0
+#endif
 #ifndef TCS_SMALL_SLAB32
 #define TCS_SMALL_SLAB32 1
 #endif
@@ -259,7 +263,7 @@ __device__ __forceinline__ void f16_values(const SpmmArgs& a, uint64_t vbase, ui
 template <int FPL, bool HOT>
 __device__ __forceinline__ void f16_gather(const __half* p, uint64_t pol, uint32_t (&dst)[FPL / 2]) {
     if constexpr (FPL == 8) {
-        const uint4 x = HOT ? ld_gather_128_pol(p, pol) : ld_gather_128(p);
+        const uint4 x = HOT ? ld_gather_128_pol(p, pol) : TCS_GATHER_NA ? ld_gather_128_na(p) : ld_gather_128(p);
         dst[0] = x.x; dst[1] = x.y; dst[2] = x.z; dst[3] = x.w;
     } else {
         const uint2 x = HOT ? ld_gather_64_pol(p, pol) : ld_gather_64(p);
@@ -865,8 +869,8 @@ __device__ __forceinline__ void tf32p_issue(const SpmmArgs& a, const unsigned ch
     if (s + 8 <= vend) {
 #pragma unroll
         for (int c = 0; c < NCHUNK; ++c) {
-            st.H[0][c] = ld_gather_128(Bl + o0 + c * 128);
-            st.H[1][c] = ld_gather_128(Bl + o1 + c * 128);
+            st.H[0][c] = TCS_GATHER_NA ? ld_gather_128_na(Bl + o0 + c * 128) : ld_gather_128(Bl + o0 + c * 128);
+            st.H[1][c] = TCS_GATHER_NA ? ld_gather_128_na(Bl + o1 + c * 128) : ld_gather_128(Bl + o1 + c * 128);
         }
         if constexpr (NCHUNK == 2 && TCS_TF32P_LO64) {
             const uint2 l0 = ld_gather_64(Ll + o0), l1 = ld_gather_64(Ll + o1);

@@ -368,6 +368,14 @@ __device__ __forceinline__ uint32_t ld_gather_32(const void* p) {
     asm volatile("ld.global.nc.b32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
+// The gather without L1 allocation (A/B knob TCS_GATHER_NA).
+__device__ __forceinline__ uint4 ld_gather_128_na(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
 __device__ __forceinline__ uint2 ld_gather_64(const void* p) {
     uint2 v;
     asm volatile("ld.global.nc.v2.b32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));

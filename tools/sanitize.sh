@@ -6,3 +6,8 @@ timeout 2400 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 
 timeout 1800 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_layers.py tests/test_gpu_scale.py -m gpu -q -x -k "not config3 and not config5 and not midsize" > $OUT/memcheck_layers.log 2>&1; echo "rc=$?" >> $OUT/memcheck_layers.log
 timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "known_answer" > $OUT/racecheck.log 2>&1; echo "rc=$?" >> $OUT/racecheck.log
 timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_layers.py -m gpu -q -x -k "attend or aggregate" > $OUT/racecheck_layers.log 2>&1; echo "rc=$?" >> $OUT/racecheck_layers.log
+# round 2: the pipelined host-buffer path (sync-free chunk encode, side streams) and its late-chunk errors
+timeout 2400 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_scale.py -m gpu -q -x -k "pipelined or midsize" > $OUT/memcheck_pipeline.log 2>&1; echo "rc=$?" >> $OUT/memcheck_pipeline.log
+# round 2: the small-list burst kernels (shared-memory part reduction, PDL launches)
+timeout 1200 compute-sanitizer --tool racecheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "known_answer or config1 or acceptance2" > $OUT/racecheck_burst.log 2>&1; echo "rc=$?" >> $OUT/racecheck_burst.log
+timeout 1200 compute-sanitizer --tool synccheck --print-limit 20 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "known_answer or config1" > $OUT/synccheck_burst.log 2>&1; echo "rc=$?" >> $OUT/synccheck_burst.log
