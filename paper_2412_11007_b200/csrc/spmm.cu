@@ -97,6 +97,9 @@ constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_N
 #ifndef TCS_E2E_MAX_CHUNKS
 #define TCS_E2E_MAX_CHUNKS 16
 #endif
+#ifndef TCS_E2E_DRAIN_LATE
+#define TCS_E2E_DRAIN_LATE 0
+#endif
 #ifndef TCS_E2E_TAIL_HALVINGS
 #define TCS_E2E_TAIL_HALVINGS 3
 #endif
@@ -1889,6 +1892,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             if (counters && !pipelined) counters->mma_invocations += cn.mma_invocations;
             done[i].record(cs);
             done[i].wait_on(ss.drain);
+            if (TCS_E2E_DRAIN_LATE) landed[nchunks - 1].wait_on(ss.drain);  // diagnostic: downloads after all uploads
             TCS_CUDA(cudaMemcpyAsync(c + r0 * n, d_c.as<float>() + r0 * n, (r1 - r0) * n * 4, cudaMemcpyDeviceToHost,
                                      ss.drain));
         }
