@@ -90,18 +90,21 @@ constexpr int spmm_blocks(int nchunk, int fpl) { return nchunk * fpl <= 4 ? 8 : 
 #define TCS_SPMM_TF32_BPS_WIDE 4
 #endif
 constexpr int tf32_blocks(int nchunk) { return nchunk <= 2 ? TCS_SPMM_TF32_BPS_NARROW : TCS_SPMM_TF32_BPS_WIDE; }
-// Feature slab of the FP16 kernel for N > 64 (experiment knob: 128 or 64).
-// Host pipeline of tcs_spmm_csr_host: at most this many window-range chunks,
-// each of at least TCS_E2E_CHUNK_NNZ entries.  Smaller chunks shorten the
-// tail after the last upload (the last chunk's encode + SpMM + download).
+// Host pipeline of tcs_spmm_csr_host: at most this many equal window-range
+// units (each of at least TCS_E2E_CHUNK_NNZ entries), the last one cut into
+// halves TCS_E2E_TAIL_HALVINGS times.  Every chunk is two uploads (column
+// indices, values) with ~12 us of copy overhead each, while only the last
+// chunk's encode + SpMM + download is exposed after the last upload: few
+// large units plus a geometric tail (4 + 6: 10 chunks) measured best
+// (profiles/r2_e2e.txt).
 #ifndef TCS_E2E_MAX_CHUNKS
-#define TCS_E2E_MAX_CHUNKS 16
+#define TCS_E2E_MAX_CHUNKS 4
 #endif
 #ifndef TCS_E2E_DRAIN_LATE
 #define TCS_E2E_DRAIN_LATE 0
 #endif
 #ifndef TCS_E2E_TAIL_HALVINGS
-#define TCS_E2E_TAIL_HALVINGS 3
+#define TCS_E2E_TAIL_HALVINGS 6
 #endif
 #ifndef TCS_E2E_CHUNK_NNZ
 #define TCS_E2E_CHUNK_NNZ (1ull << 20)
