@@ -1716,6 +1716,14 @@ Streams& thread_streams() {
     int dev = 0;
     TCS_CUDA(cudaGetDevice(&dev));
     auto& p = per_dev[dev & 63];
+    if (p) {  // a device reset since the last call invalidates the handles
+        const cudaError_t e = cudaStreamQuery(p->copy);
+        if (e != cudaSuccess && e != cudaErrorNotReady) {
+            cudaGetLastError();
+            p.reset();  // the handles died with the old context (their destroy calls just fail)
+            cudaGetLastError();
+        }
+    }
     if (!p) p = std::make_unique<Streams>();
     return *p;
 }
