@@ -42,8 +42,18 @@ constexpr uint32_t kTinyCap = TCS_ENC_TINY_CAP;  // entries per window, one warp
 constexpr int kTinyWarps = 8;           // warps per CTA of window_sort_warp
 constexpr uint32_t kSmallCap = 2048;    // entries per window, 128-thread CTA, 32 KB smem
 constexpr uint32_t kSmallThreads = 128;
-constexpr uint32_t kBigCap = 12288;     // 512-thread CTA, 192 KB smem
-constexpr uint32_t kBigThreads = 512;
+constexpr uint32_t kBigCap = 12288;     // medium / huge class boundary (entries)
+// window_sort_big (column spaces too wide for the bitmap): windows of up to
+// kSortCap entries merge in shared memory (2 x 8 B per entry), longer ones in
+// global scratch
+#ifndef TCS_ENC_SORT_CAP
+#define TCS_ENC_SORT_CAP 12288
+#endif
+#ifndef TCS_ENC_SORT_THREADS
+#define TCS_ENC_SORT_THREADS 512
+#endif
+constexpr uint32_t kSortCap = TCS_ENC_SORT_CAP;
+constexpr uint32_t kBigThreads = TCS_ENC_SORT_THREADS;
 #ifndef TCS_ENC_BITMAP_THREADS
 #define TCS_ENC_BITMAP_THREADS 512
 #endif
@@ -387,8 +397,8 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
         // two inlined call sites, so that the shared-memory one compiles to
         // LDS/STS instead of generic loads and stores
-        if (n <= kBigCap) {
-            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + kBigCap, tmp_cols, rank, nv_out,
+        if (n <= kSortCap) {
+            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + kSortCap, tmp_cols, rank, nv_out,
                                  chk);
         } else {
             uint64_t* a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
@@ -526,6 +536,10 @@ constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
 constexpr uint32_t kTileBatch = 63;   // tile boundaries searched at once (64 x VH threads)
 constexpr int kScatterU = 8;          // entries in flight per thread (window_scatter)
+#ifndef TCS_ENC_SCATTER_TINY_WARP
+#define TCS_ENC_SCATTER_TINY_WARP 1
+#endif
+constexpr bool kScatterTinyByWarp = TCS_ENC_SCATTER_TINY_WARP;
 
 // Tiles of each huge window (vectors / tile), exclusive prefix over the
 // huge list (one CTA; the huge list is short) -> tile_off[0..n_huge], total
@@ -557,6 +571,81 @@ __global__ void __launch_bounds__(1024) huge_tile_prefix(const uint32_t* __restr
     }
 }
 
+// Tiny windows (<= kTinyCap entries, so <= kTinyCap vectors; R-MAT's 10^6
+// windows are mostly these): one warp per window, its value blocks
+// assembled in a per-warp shared-memory tile, no CTA barriers.  A CTA per
+// window (window_scatter) spent its time in three barriers and three
+// dependent global latencies per window (C5: 2.9 ms for 10^6 windows).
+// warps per CTA: as many per-warp tiles as fit 32 KB of static shared memory
+template <int VH, typename V>
+constexpr int scatter_warps() {
+    return int(32768 / (kTinyCap * VH * sizeof(V))) < 8 ? int(32768 / (kTinyCap * VH * sizeof(V))) : 8;
+}
+template <int VH, typename V>
+__global__ void __launch_bounds__(scatter_warps<VH, V>() * 32) window_scatter_warp(
+    const uint32_t* __restrict__ csr_rp, const float* __restrict__ csr_vals, uint64_t rows, uint32_t k,
+    const uint32_t* __restrict__ rp, const uint32_t* __restrict__ tmp_cols, const uint32_t* __restrict__ rank,
+    uint32_t* __restrict__ out_ci, V* __restrict__ out_vals, const uint32_t* __restrict__ list, CheckOut* chk) {
+    constexpr uint32_t kTileBytes = kTinyCap * VH * sizeof(V);
+    constexpr int kScatterWarps = scatter_warps<VH, V>();
+    __shared__ __align__(16) unsigned char tiles[kScatterWarps][kTileBytes];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char* tile_b = tiles[wid];
+    V* tile = reinterpret_cast<V*>(tile_b);
+    const uint32_t n_tiny = chk->n_tiny;
+    uint32_t tiny_flag = 0;
+    for (uint32_t i = blockIdx.x * kScatterWarps + wid; i < n_tiny; i += gridDim.x * kScatterWarps) {
+        const uint64_t w = list[i], r0 = VH * w;
+        uint32_t b = 0;  // lane q <= VH: row boundary q (absolute entry index)
+        if (lane <= VH) b = __ldg(csr_rp + min(r0 + lane, rows));
+        const uint32_t base = __ldg(rp + w), nvw = __ldg(rp + w + 1) - base;
+        const uint32_t e0 = __shfl_sync(0xffffffffu, b, 0), e1 = __shfl_sync(0xffffffffu, b, VH);
+        const uint32_t n = e1 - e0;
+        // loads first (column copy, ranks, values), then the tile
+        constexpr uint32_t kPer = kTinyCap / 32;
+        uint32_t cc[kPer], v[kPer];
+        float x[kPer];
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t j = lane + 32 * u;
+            cc[u] = j < nvw ? __ldg(tmp_cols + e0 + j) : 0u;
+            v[u] = j < n ? __ldg(rank + e0 + j) : 0u;
+            x[u] = j < n ? __ldg(csr_vals + e0 + j) : 0.f;
+        }
+        const uint32_t n16 = (VH * nvw * static_cast<uint32_t>(sizeof(V)) + 15) / 16;
+        for (uint32_t j = lane; j < n16; j += 32) reinterpret_cast<uint4*>(tile_b)[j] = make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t j = lane + 32 * u;
+            if (j < nvw) out_ci[base + j] = cc[u];
+        }
+        uint32_t rbq[VH];  // row boundaries, in every lane (shuffled before any divergence)
+#pragma unroll
+        for (int q = 0; q < VH; ++q) rbq[q] = __shfl_sync(0xffffffffu, b, q);
+        __syncwarp();
+#pragma unroll
+        for (uint32_t u = 0; u < kPer; ++u) {
+            const uint32_t j = lane + 32 * u;
+            if (j >= n || v[u] >= nvw) continue;  // (an invalid entry never leaves its window's tile)
+            uint32_t r = 0;  // row of entry j: boundaries rb[1..VH-1] at or below e0 + j
+#pragma unroll
+            for (int q = 1; q < VH; ++q) r += (e0 + j >= rbq[q]) ? 1u : 0u;
+            const uint32_t blk = v[u] / k, jj = v[u] - blk * k;
+            const uint32_t width = min(k, nvw - blk * k);
+            const V y = store_cvt<V>(x[u]);
+            tile[blk * k * VH + r * width + jj] = y;
+            if constexpr (sizeof(V) == 2)  // nonzero f32 that rounds to a binary16 zero
+                if ((__float_as_uint(x[u]) & 0x7FFFFFFFu) && !(__half_as_ushort(y) & 0x7FFFu)) tiny_flag = 1;
+        }
+        __syncwarp();
+        uint4* dst = reinterpret_cast<uint4*>(out_vals + static_cast<uint64_t>(VH) * base);  // 16-B aligned
+        const uint32_t full16 = (VH * nvw * static_cast<uint32_t>(sizeof(V))) / 16;
+        for (uint32_t j = lane; j < full16; j += 32) dst[j] = reinterpret_cast<const uint4*>(tile_b)[j];
+        __syncwarp();  // the tile is reused by the warp's next window
+    }
+    if (tiny_flag) atomicOr(&chk->tiny, 1u);
+}
+
 template <int VH, typename V, int THREADS, uint32_t TILE>
 __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __restrict__ csr_rp,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
@@ -573,6 +662,8 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
     const uint32_t n_front = big ? chk->n_huge : chk->n_tiny;
     const uint32_t n_huge_units = big ? chk->huge_tiles : 0u;
     const uint32_t n_units = big ? n_huge_units + chk->n_medium : n_front + chk->n_small;
+    // small list: the tiny windows (front) belong to window_scatter_warp
+    const uint32_t u_first = big || !kScatterTinyByWarp ? 0u : n_front;
     uint32_t* next = big ? &chk->next_scatter_big : nullptr;
     uint32_t* tiny = &chk->tiny;
     __shared__ uint32_t s_huge;
@@ -582,7 +673,8 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
     __shared__ uint32_t rlo[VH], roff[VH + 1];    // ranged: this tile's first entry per row, prefix
     constexpr uint32_t kTile = TILE * 8 / VH;  // vectors per smem tile
     // big list: dynamic queue (next != nullptr); small list: fixed stride
-    for (uint32_t u = next ? cta_next(next) : blockIdx.x; u < n_units; u = next ? cta_next(next) : u + gridDim.x) {
+    for (uint32_t u = next ? cta_next(next) : u_first + blockIdx.x; u < n_units;
+         u = next ? cta_next(next) : u + gridDim.x) {
         uint64_t w;
         uint32_t tile_lo = 0, tile_hi = 0xFFFFFFFFu;  // the unit's tiles of window w
         if (u < n_huge_units) {  // block-uniform
@@ -863,11 +955,12 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                     TCS_LAUNCHED("window_bitmap");
                 } else {
                     DBuf scratch;
-                    if (h.max_window_entries > kBigCap) scratch = DBuf(2 * nnz * 8, s);
-                    const size_t smem = 2 * kBigCap * sizeof(uint64_t);
+                    if (h.max_window_entries > kSortCap) scratch = DBuf(2 * nnz * 8, s);
+                    const size_t smem = 2 * kSortCap * sizeof(uint64_t);
                     TCS_CUDA(cudaFuncSetAttribute(window_sort_big<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(smem)));
-                    const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms)));
+                    const int per_sm = std::max<int>(1, std::min<int>(2048 / kBigThreads, int(220 * 1024 / smem)));
+                    const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
                     window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
                                                                    scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
                                                                    rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk,
@@ -912,6 +1005,24 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             // after the column indices the kernels above rank)
             if (values_ready) TCS_CUDA(cudaStreamWaitEvent(s, values_ready, 0));
             const uint64_t n_smalls = async ? W : uint64_t(h.n_tiny) + h.n_small;
+            if (kScatterTinyByWarp && h.n_tiny) {  // tiny windows: one warp each
+                auto gw = [&](int warps) {
+                    return static_cast<int>(
+                        std::min<uint64_t>((h.n_tiny + warps - 1) / warps, uint64_t(sms) * (64 / warps)));
+                };
+                constexpr int w16 = scatter_warps<VH, __half>(), w32 = scatter_warps<VH, float>();
+                if (value_dtype == TCS_DTYPE_F16)
+                    window_scatter_warp<VH, __half><<<gw(w16), w16 * 32, 0, s>>>(
+                        csr->row_ptr, csr->values, rows, k, m.row_pointers, tmp_cols.as<uint32_t>(),
+                        rank.as<uint32_t>(), m.column_indices, static_cast<__half*>(m.values),
+                        small_list.as<uint32_t>(), dchk);
+                else
+                    window_scatter_warp<VH, float><<<gw(w32), w32 * 32, 0, s>>>(
+                        csr->row_ptr, csr->values, rows, k, m.row_pointers, tmp_cols.as<uint32_t>(),
+                        rank.as<uint32_t>(), m.column_indices, static_cast<float*>(m.values),
+                        small_list.as<uint32_t>(), dchk);
+                TCS_LAUNCHED("window_scatter_warp");
+            }
             // big scatter units: with any huge window, as many CTAs as fit
             const uint64_t n_big_units = h.n_huge || async ? uint64_t(sms) * 64 : n_big;
             if (value_dtype == TCS_DTYPE_F16) {

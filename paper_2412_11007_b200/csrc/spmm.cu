@@ -1595,6 +1595,9 @@ extern "C" tcs_status tcs_spmm(const tcs_mebcrs* A, const void* b, tcs_dtype b_d
                 else if (slab == 128)
                     vf32 ? launch(spmm_f16_kernel<2, 8, true>, a, slabs, s, "spmm_f16<128,f32v>")
                          : launch(spmm_f16_kernel<2, 8, false>, a, slabs, s, "spmm_f16<128>");
+                else if (slab == 64 && !vf32 && TCS_PREFETCH_F16 > 0 && b_bytes <= kPrefetchMaxB)
+                    launch(spmm_f16_kernel<1, 8, false, false, false, true>, a, slabs, s, "spmm_f16_pf<64>",
+                           spmm_blocks(1, 8));
                 else if (slab == 64)
                     vf32 ? launch(spmm_f16_kernel<1, 8, true>, a, slabs, s, "spmm_f16<64,f32v>", spmm_blocks(1, 8))
                          : launch(spmm_f16_kernel<1, 8, false>, a, slabs, s, "spmm_f16<64>", spmm_blocks(1, 8));

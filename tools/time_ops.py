@@ -40,6 +40,10 @@ if "c3" in which:
         C = torch.empty(rows, 128, device="cuda")
         out[f"c3_spmm_{prec.name}_n128"] = timed(lambda: T.spmm(me, B, T.KernelConfig(prec), out=C))
         if prec == T.Precision.fp16:
+            B1 = G.dense(cols, 64, 2, dtype=dt)
+            C1 = torch.empty(rows, 64, device="cuda")
+            out["c3_spmm_fp16_n64"] = timed(lambda: T.spmm(me, B1, T.KernelConfig(prec), out=C1))
+            del B1, C1
             B2 = G.dense(cols, 256, 2, dtype=dt)
             C2 = torch.empty(rows, 256, device="cuda")
             out["c3_spmm_fp16_n256"] = timed(lambda: T.spmm(me, B2, T.KernelConfig(prec), out=C2))
