@@ -53,6 +53,11 @@ constexpr uint32_t kBigCap = 12288;     // medium / huge class boundary (entries
 #define TCS_ENC_SORT_THREADS 512
 #endif
 constexpr uint32_t kSortCap = TCS_ENC_SORT_CAP;
+// hub windows of wide column spaces ranked with a global-memory bitmap
+// (A/B knob; 0 = merged in global scratch)
+#ifndef TCS_ENC_HUB_BITMAP
+#define TCS_ENC_HUB_BITMAP 1
+#endif
 constexpr uint32_t kBigThreads = TCS_ENC_SORT_THREADS;
 #ifndef TCS_ENC_BITMAP_THREADS
 #define TCS_ENC_BITMAP_THREADS 512
@@ -381,25 +386,42 @@ __global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32
 }
 
 template <int VH>
+__device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ csr_rp,
+                                                   const uint32_t* __restrict__ ci, uint64_t rows, uint64_t cols,
+                                                   uint64_t w, uint4* bm4, uint4* pre4, uint32_t quads,
+                                                   uint32_t* __restrict__ tmp_cols, uint32_t* __restrict__ rank,
+                                                   uint32_t* __restrict__ nv_out, CheckOut* chk);
+
+// Column spaces too wide for a shared-memory bitmap (R-MAT scale 23: 8.4 M
+// columns).  Windows of up to kSortCap entries merge their VH sorted rows
+// in shared memory; longer (hub) windows are ranked with a CTA-private
+// bitmap in global memory (bscratch: 2 x quads uint4 per CTA), or -- when
+// that would be larger than 2 x nnz keys -- merged in global scratch.
+template <int VH>
 __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* __restrict__ csr_rp,
                                                                const uint32_t* __restrict__ ci, uint64_t rows,
                                                                uint64_t cols, uint64_t W,
                                                                uint64_t* __restrict__ scratch,
+                                                               uint4* __restrict__ bscratch,
                                                                uint32_t* __restrict__ tmp_cols,
                                                                uint32_t* __restrict__ rank,
                                                                uint32_t* __restrict__ nv_out, CheckOut* chk,
                                                                const uint32_t* __restrict__ big) {
     extern __shared__ uint64_t smem_keys[];
     const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
+    const uint32_t quads = static_cast<uint32_t>((cols + 127) / 128);
     for (uint32_t i = cta_next(&chk->next_sort_big); i < n_big; i = cta_next(&chk->next_sort_big)) {
         const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
-        // two inlined call sites, so that the shared-memory one compiles to
-        // LDS/STS instead of generic loads and stores
+        // separate inlined call sites, so that the shared-memory one compiles
+        // to LDS/STS instead of generic loads and stores
         if (n <= kSortCap) {
             window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + kSortCap, tmp_cols, rank, nv_out,
                                  chk);
+        } else if (bscratch) {
+            uint4* bm4 = bscratch + 2ull * quads * blockIdx.x;
+            bitmap_rank_window<VH>(csr_rp, ci, rows, cols, w, bm4, bm4 + quads, quads, tmp_cols, rank, nv_out, chk);
         } else {
             uint64_t* a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
             window_sort_rank<VH>(csr_rp, ci, rows, cols, w, a, a + n, tmp_cols, rank, nv_out, chk);
@@ -407,7 +429,102 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
     }
 }
 
-// Bitmap ranking for windows with more than kSmallCap entries.
+// Bitmap ranking of one window by the whole CTA: set one bit per column in
+// bm4 (quads x uint4, zeroed here), prefix-popcount into pre4, emit the
+// window's sorted distinct columns to tmp_cols and each entry's rank.  bm4 /
+// pre4 are shared memory (window_bitmap) or a CTA-private global slice
+// (window_sort_big's hub windows when the column space exceeds shared
+// memory: clearing and scanning cols/32 words in L2 beats three global
+// merge passes over 10^4..10^5 entries).  The word arrays are walked as
+// uint4 quads (words padded to a multiple of 4).
+template <int VH>
+__device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ csr_rp,
+                                                   const uint32_t* __restrict__ ci, uint64_t rows, uint64_t cols,
+                                                   uint64_t w, uint4* bm4, uint4* pre4, uint32_t quads,
+                                                   uint32_t* __restrict__ tmp_cols, uint32_t* __restrict__ rank,
+                                                   uint32_t* __restrict__ nv_out, CheckOut* chk) {
+    __shared__ uint32_t rb[VH + 1];
+    const uint32_t* bm = reinterpret_cast<const uint32_t*>(bm4);
+    const uint32_t* pre = reinterpret_cast<const uint32_t*>(pre4);
+    const uint32_t nt = blockDim.x, qpt = (quads + nt - 1) / nt;
+    const uint64_t r0 = VH * w;
+    const uint32_t e0 = csr_rp[r0];
+    const uint32_t n = csr_rp[min(r0 + VH, rows)] - e0;
+    if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
+    for (uint32_t i = threadIdx.x; i < quads; i += nt) bm4[i] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    // kBitmapU entries per thread in flight: a hub window (10^4..10^5
+    // entries) is otherwise a chain of dependent-latency iterations
+    uint32_t bad = 0;
+    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
+        uint32_t c[kBitmapU], cp[kBitmapU];
+#pragma unroll
+        for (int u = 0; u < kBitmapU; ++u) {
+            const uint32_t i = i0 + u * nt;
+            c[u] = i < n ? __ldg(ci + e0 + i) : 0u;
+            cp[u] = i < n && i > 0 ? __ldg(ci + e0 + i - 1) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kBitmapU; ++u) {
+            const uint32_t i = i0 + u * nt;
+            if (i >= n) continue;
+            bool row_start = false;
+#pragma unroll
+            for (int r = 0; r < VH; ++r) row_start |= (i == rb[r]);
+            // check_col with the predecessor already loaded
+            const uint32_t b = !row_start && cp[u] >= c[u] ? 4u : c[u] >= cols ? 3u : 0u;
+            bad = max(bad, b);
+            if (c[u] < cols) atomicOr(reinterpret_cast<uint32_t*>(bm4) + (c[u] >> 5), 1u << (c[u] & 31));
+        }
+    }
+    if (bad) atomicMax(&chk->bad, bad);
+    __syncthreads();
+    // prefix popcount over this thread's contiguous run of quads
+    const uint32_t q0 = min(quads, threadIdx.x * qpt), q1 = min(quads, q0 + qpt);
+    uint32_t cnt = 0;
+    for (uint32_t i = q0; i < q1; ++i) {
+        const uint4 x = bm4[i];
+        cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+    }
+    uint32_t total;
+    uint32_t run = dev::block_exclusive_scan(cnt, &total);
+    for (uint32_t i = q0; i < q1; ++i) {
+        const uint4 x = bm4[i];
+        const uint32_t p0 = run, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
+        pre4[i] = make_uint4(p0, p1, p2, p3);
+        if ((x.x | x.y | x.z | x.w) == 0u) continue;
+        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint32_t bits = wv[k];
+            while (bits) {  // sorted unique columns of the window
+                const uint32_t b = __ffs(bits) - 1;
+                tmp_cols[e0 + run++] = 32 * (4 * i + k) + b;
+                bits &= bits - 1;
+            }
+        }
+    }
+    if (threadIdx.x == 0) nv_out[w] = total;
+    __syncthreads();
+    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
+        uint32_t c[kBitmapU];
+#pragma unroll
+        for (int u = 0; u < kBitmapU; ++u) {
+            const uint32_t i = i0 + u * nt;
+            c[u] = i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
+        }
+#pragma unroll
+        for (int u = 0; u < kBitmapU; ++u) {
+            const uint32_t i = i0 + u * nt;
+            if (i < n && c[u] < cols)
+                rank[e0 + i] = pre[c[u] >> 5] + __popc(bm[c[u] >> 5] & ((1u << (c[u] & 31)) - 1u));
+        }
+    }
+    __syncthreads();  // bitmap, prefix and rb are reused by the next window
+}
+
+// Bitmap ranking for windows with more than kSmallCap entries (column
+// space within shared memory).
 template <int VH>
 __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* __restrict__ csr_rp,
                                                                 const uint32_t* __restrict__ ci, uint64_t rows,
@@ -418,93 +535,10 @@ __global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* 
                                                                 const uint32_t* __restrict__ big) {
     extern __shared__ uint4 bm_smem4[];
     const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
-    // the word arrays are walked as uint4 quads (a quarter of the
-    // instructions of the clear / scan / emit loops, which dominated: ncu
-    // issue-active 62%); words padded to a multiple of 4
     const uint32_t quads = static_cast<uint32_t>((cols + 127) / 128);
-    uint4* bm4 = bm_smem4;
-    uint4* pre4 = bm_smem4 + quads;
-    const uint32_t* bm = reinterpret_cast<const uint32_t*>(bm4);
-    const uint32_t* pre = reinterpret_cast<const uint32_t*>(pre4);
-    __shared__ uint32_t rb[VH + 1];
-    const uint32_t nt = blockDim.x, qpt = (quads + nt - 1) / nt;
-    for (uint32_t bi = cta_next(&chk->next_bitmap); bi < n_big; bi = cta_next(&chk->next_bitmap)) {
-        const uint64_t w = big_window(big, W, n_huge, bi);
-        const uint64_t r0 = VH * w;
-        const uint32_t e0 = csr_rp[r0];
-        const uint32_t n = csr_rp[min(r0 + VH, rows)] - e0;
-        if (threadIdx.x <= VH) rb[threadIdx.x] = csr_rp[min(r0 + threadIdx.x, rows)] - e0;
-        for (uint32_t i = threadIdx.x; i < quads; i += nt) bm4[i] = make_uint4(0, 0, 0, 0);
-        __syncthreads();
-        // kBitmapU entries per thread in flight: a hub window (10^4..10^5
-        // entries) is otherwise a chain of dependent-latency iterations
-        uint32_t bad = 0;
-        for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
-            uint32_t c[kBitmapU], cp[kBitmapU];
-#pragma unroll
-            for (int u = 0; u < kBitmapU; ++u) {
-                const uint32_t i = i0 + u * nt;
-                c[u] = i < n ? __ldg(ci + e0 + i) : 0u;
-                cp[u] = i < n && i > 0 ? __ldg(ci + e0 + i - 1) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < kBitmapU; ++u) {
-                const uint32_t i = i0 + u * nt;
-                if (i >= n) continue;
-                bool row_start = false;
-#pragma unroll
-                for (int r = 0; r < VH; ++r) row_start |= (i == rb[r]);
-                // check_col with the predecessor already loaded
-                const uint32_t b = !row_start && cp[u] >= c[u] ? 4u : c[u] >= cols ? 3u : 0u;
-                bad = max(bad, b);
-                if (c[u] < cols) atomicOr(reinterpret_cast<uint32_t*>(bm4) + (c[u] >> 5), 1u << (c[u] & 31));
-            }
-        }
-        if (bad) atomicMax(&chk->bad, bad);
-        __syncthreads();
-        // prefix popcount over this thread's contiguous run of quads
-        const uint32_t q0 = min(quads, threadIdx.x * qpt), q1 = min(quads, q0 + qpt);
-        uint32_t cnt = 0;
-        for (uint32_t i = q0; i < q1; ++i) {
-            const uint4 x = bm4[i];
-            cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-        }
-        uint32_t total;
-        uint32_t run = dev::block_exclusive_scan(cnt, &total);
-        for (uint32_t i = q0; i < q1; ++i) {
-            const uint4 x = bm4[i];
-            const uint32_t p0 = run, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
-            pre4[i] = make_uint4(p0, p1, p2, p3);
-            if ((x.x | x.y | x.z | x.w) == 0u) continue;
-            const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                uint32_t bits = wv[k];
-                while (bits) {  // sorted unique columns of the window
-                    const uint32_t b = __ffs(bits) - 1;
-                    tmp_cols[e0 + run++] = 32 * (4 * i + k) + b;
-                    bits &= bits - 1;
-                }
-            }
-        }
-        if (threadIdx.x == 0) nv_out[w] = total;
-        __syncthreads();
-        for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
-            uint32_t c[kBitmapU];
-#pragma unroll
-            for (int u = 0; u < kBitmapU; ++u) {
-                const uint32_t i = i0 + u * nt;
-                c[u] = i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
-            }
-#pragma unroll
-            for (int u = 0; u < kBitmapU; ++u) {
-                const uint32_t i = i0 + u * nt;
-                if (i < n && c[u] < cols)
-                    rank[e0 + i] = pre[c[u] >> 5] + __popc(bm[c[u] >> 5] & ((1u << (c[u] & 31)) - 1u));
-            }
-        }
-        __syncthreads();
-    }
+    for (uint32_t bi = cta_next(&chk->next_bitmap); bi < n_big; bi = cta_next(&chk->next_bitmap))
+        bitmap_rank_window<VH>(csr_rp, ci, rows, cols, big_window(big, W, n_huge, bi), bm_smem4, bm_smem4 + quads,
+                               quads, tmp_cols, rank, nv_out, chk);
 }
 
 template <typename V>
@@ -954,15 +988,21 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                                                                    nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_bitmap");
                 } else {
-                    DBuf scratch;
-                    if (h.max_window_entries > kSortCap) scratch = DBuf(2 * nnz * 8, s);
                     const size_t smem = 2 * kSortCap * sizeof(uint64_t);
                     TCS_CUDA(cudaFuncSetAttribute(window_sort_big<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                   static_cast<int>(smem)));
                     const int per_sm = std::max<int>(1, std::min<int>(2048 / kBigThreads, int(220 * 1024 / smem)));
                     const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
+                    // hub windows: a global bitmap per CTA, unless 2 x nnz merge keys are smaller
+                    DBuf scratch, bscratch;
+                    const uint64_t bm_bytes = uint64_t(g2) * 2 * ((cols + 127) / 128) * 16;
+                    if (h.max_window_entries > kSortCap) {
+                        if (TCS_ENC_HUB_BITMAP && bm_bytes <= 2 * nnz * 8) bscratch = DBuf(bm_bytes, s);
+                        else scratch = DBuf(2 * nnz * 8, s);
+                    }
                     window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
-                                                                   scratch.as<uint64_t>(), tmp_cols.as<uint32_t>(),
+                                                                   scratch.as<uint64_t>(), bscratch.as<uint4>(),
+                                                                   tmp_cols.as<uint32_t>(),
                                                                    rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk,
                                                                    big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_sort_big");

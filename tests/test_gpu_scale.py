@@ -44,12 +44,14 @@ def dev(m: O.Csr):
                        torch.from_numpy(m.col_idx.view(np.int32)).cuda(), torch.from_numpy(m.values).cuda())
 
 
-def hub_matrix():
+def hub_matrix(cols=40000):
     """Windows of every size class: tiny, > 2048 entries (512-thread merge),
-    > 12288 entries (global scratch), plus windows longer than the SpMM
-    segment (split + deterministic reduction) and empty windows."""
+    > 12288 entries (hub), plus windows longer than the SpMM segment (split +
+    deterministic reduction) and empty windows.  cols > 819,200 takes the
+    wide-column-space paths (window_sort_big: shared-memory merges, hub
+    windows on a global-memory bitmap) instead of the shared-memory bitmap."""
     rng = np.random.default_rng(11)
-    rows, cols = 96, 40000
+    rows = 96
     per_row = [3] * 8 + [400] * 8 + [0] * 8 + [2500] * 8 + [12] * 8 + [6000] * 8 + [1] * 8 + [0] * 8 + \
               [900] * 8 + [30000] * 8 + [5] * 8 + [2] * 8
     rp = np.zeros(rows + 1, np.uint32)
@@ -61,6 +63,27 @@ def hub_matrix():
     ci = np.concatenate(ci_list)
     vals = rng.integers(1, 5, ci.size).astype(np.float32) * rng.choice([-1, 1], ci.size).astype(np.float32)
     return O.Csr(rows, cols, rp, ci, vals)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [0, 1])
+def test_hub_windows_wide_column_space_bit_exact(p):
+    """R-MAT-like column space (> the shared-memory bitmap): the medium
+    windows merge in shared memory, the hub windows (> 12288 entries) are
+    ranked on a CTA-private global-memory bitmap."""
+    m = hub_matrix(cols=1_000_003)
+    ref = O.encode_mebcrs(m, p)
+    for vd in (1, 0) if p == 0 else (1,):
+        me = T.encode_mebcrs(dev(m), T.Precision(p), vd)
+        rp, ci, v = me.to_host()
+        assert np.array_equal(rp, ref.row_pointers) and np.array_equal(ci, ref.column_indices)
+        if vd == 1:
+            assert np.array_equal(v.view(np.uint32), ref.values.view(np.uint32))
+    B = O.generate_random_dense(m.cols, 64, 5)
+    want = O.spmm(ref, B)
+    me = T.encode_mebcrs(dev(m), T.Precision(p), 1)
+    got = T.spmm(me, torch.from_numpy(B).cuda(), T.KernelConfig(T.Precision(p))).output.cpu().numpy()
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
 @pytest.mark.parametrize("p", [0, 1])
