@@ -53,6 +53,10 @@ constexpr uint32_t kBigCap = 12288;     // medium / huge class boundary (entries
 #define TCS_ENC_SORT_THREADS 512
 #endif
 constexpr uint32_t kSortCap = TCS_ENC_SORT_CAP;
+#ifndef TCS_ENC_SORT_SPLIT
+#define TCS_ENC_SORT_SPLIT 6144
+#endif
+constexpr uint32_t kSortCapA = TCS_ENC_SORT_SPLIT;  // 0: one launch
 // hub windows of wide column spaces ranked with a global-memory bitmap
 // (A/B knob; 0 = merged in global scratch)
 #ifndef TCS_ENC_HUB_BITMAP
@@ -79,6 +83,7 @@ struct CheckOut {
     // dynamic window queues of the big-window kernels (a hub window of 10^5+
     // entries must not delay the windows behind it on a fixed CTA stride)
     uint32_t next_sort_big, next_bitmap, next_scatter_big;
+    uint32_t next_sort_big2;  // window_sort_big's second (large-window) launch
     // set by the F16 scatter when a nonzero f32 value rounds to a binary16
     // zero (0 < |v| <= 2^-25): the reference still samples it in SDDMM
     // (ref sddmm.hpp:131 tests the f32 value), so the handle gets exact
@@ -397,7 +402,11 @@ __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ 
 // in shared memory; longer (hub) windows are ranked with a CTA-private
 // bitmap in global memory (bscratch: 2 x quads uint4 per CTA), or -- when
 // that would be larger than 2 x nnz keys -- merged in global scratch.
-template <int VH>
+// Launched twice (kSortSplit): windows of up to kSortCapA entries with
+// CAP = kSortCapA (half the shared memory, two CTAs per SM), then the rest
+// with CAP = kSortCap; each launch skips the other's windows (n_min < n <=
+// n_max) and has its own queue.
+template <int VH, uint32_t CAP>
 __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* __restrict__ csr_rp,
                                                                const uint32_t* __restrict__ ci, uint64_t rows,
                                                                uint64_t cols, uint64_t W,
@@ -406,18 +415,20 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                                                uint32_t* __restrict__ tmp_cols,
                                                                uint32_t* __restrict__ rank,
                                                                uint32_t* __restrict__ nv_out, CheckOut* chk,
-                                                               const uint32_t* __restrict__ big) {
+                                                               const uint32_t* __restrict__ big, uint32_t n_min,
+                                                               uint32_t n_max, uint32_t* queue) {
     extern __shared__ uint64_t smem_keys[];
     const uint32_t n_huge = chk->n_huge, n_big = chk->n_huge + chk->n_medium;
     const uint32_t quads = static_cast<uint32_t>((cols + 127) / 128);
-    for (uint32_t i = cta_next(&chk->next_sort_big); i < n_big; i = cta_next(&chk->next_sort_big)) {
+    for (uint32_t i = cta_next(queue); i < n_big; i = cta_next(queue)) {
         const uint64_t w = big_window(big, W, n_huge, i);
         const uint32_t e0 = csr_rp[VH * w];
         const uint32_t n = csr_rp[min(VH * w + VH, rows)] - e0;
+        if (n <= n_min || n > n_max) continue;  // the other launch's window (block-uniform)
         // separate inlined call sites, so that the shared-memory one compiles
         // to LDS/STS instead of generic loads and stores
-        if (n <= kSortCap) {
-            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + kSortCap, tmp_cols, rank, nv_out,
+        if (n <= CAP) {
+            window_sort_rank<VH>(csr_rp, ci, rows, cols, w, smem_keys, smem_keys + CAP, tmp_cols, rank, nv_out,
                                  chk);
         } else if (bscratch) {
             uint4* bm4 = bscratch + 2ull * quads * blockIdx.x;
@@ -988,23 +999,36 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                                                                    nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_bitmap");
                 } else {
-                    const size_t smem = 2 * kSortCap * sizeof(uint64_t);
-                    TCS_CUDA(cudaFuncSetAttribute(window_sort_big<VH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                  static_cast<int>(smem)));
-                    const int per_sm = std::max<int>(1, std::min<int>(2048 / kBigThreads, int(220 * 1024 / smem)));
-                    const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
-                    // hub windows: a global bitmap per CTA, unless 2 x nnz merge keys are smaller
-                    DBuf scratch, bscratch;
-                    const uint64_t bm_bytes = uint64_t(g2) * 2 * ((cols + 127) / 128) * 16;
-                    if (h.max_window_entries > kSortCap) {
-                        if (TCS_ENC_HUB_BITMAP && bm_bytes <= 2 * nnz * 8) bscratch = DBuf(bm_bytes, s);
-                        else scratch = DBuf(2 * nnz * 8, s);
+                    auto sort_launch = [&](auto kern, uint32_t cap, uint32_t n_min, uint32_t n_max, uint32_t* queue,
+                                           bool hubs) {
+                        const size_t smem = 2 * size_t(cap) * sizeof(uint64_t);
+                        TCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                      static_cast<int>(smem)));
+                        const int per_sm =
+                            std::max<int>(1, std::min<int>(2048 / kBigThreads, int(220 * 1024 / smem)));
+                        const int g2 = static_cast<int>(std::min<uint64_t>(n_big, uint64_t(sms) * per_sm));
+                        // hub windows: a global bitmap per CTA, unless 2 x nnz merge keys are smaller
+                        DBuf scratch, bscratch;
+                        const uint64_t bm_bytes = uint64_t(g2) * 2 * ((cols + 127) / 128) * 16;
+                        if (hubs && h.max_window_entries > cap) {
+                            if (TCS_ENC_HUB_BITMAP && bm_bytes <= 2 * nnz * 8) bscratch = DBuf(bm_bytes, s);
+                            else scratch = DBuf(2 * nnz * 8, s);
+                        }
+                        kern<<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
+                                                           scratch.as<uint64_t>(), bscratch.as<uint4>(),
+                                                           tmp_cols.as<uint32_t>(), rank.as<uint32_t>(),
+                                                           nvw.as<uint32_t>(), dchk, big_list.as<uint32_t>(), n_min,
+                                                           n_max, queue);
+                    };
+                    if (kSortCapA) {
+                        sort_launch(window_sort_big<VH, kSortCapA>, kSortCapA, 0, kSortCapA, &dchk->next_sort_big,
+                                    false);
+                        sort_launch(window_sort_big<VH, kSortCap>, kSortCap, kSortCapA, 0xFFFFFFFFu,
+                                    &dchk->next_sort_big2, true);
+                    } else {
+                        sort_launch(window_sort_big<VH, kSortCap>, kSortCap, 0, 0xFFFFFFFFu, &dchk->next_sort_big,
+                                    true);
                     }
-                    window_sort_big<VH><<<g2, kBigThreads, smem, s>>>(csr->row_ptr, csr->col_idx, rows, cols, W,
-                                                                   scratch.as<uint64_t>(), bscratch.as<uint4>(),
-                                                                   tmp_cols.as<uint32_t>(),
-                                                                   rank.as<uint32_t>(), nvw.as<uint32_t>(), dchk,
-                                                                   big_list.as<uint32_t>());
                     TCS_LAUNCHED("window_sort_big");
                 }
             }
