@@ -60,7 +60,6 @@ struct SpmmArgs {
     // softmax of softmax.cu applied in registers instead of in memory.
     const float2* rowstat;  // per row (m, 1/sum), 8 * num_windows entries
     float scale;
-    const uint32_t* hot;  // HOT kernels: Plan::col_hot bitmap
 };
 
 // One binary16 score -> its softmax value, rounded as softmax.cu stores it
