@@ -190,6 +190,65 @@ __global__ void plan_fill(const uint32_t* __restrict__ rp, uint64_t W, uint32_t 
     }
 }
 
+// The whole pipelined work list of a small chunk (W <= kPlanSmallW) in one
+// CTA: window counts, the two exclusive scans and the fill, one launch
+// instead of eight (the tail chunks of tcs_spmm_csr_host are a chain of
+// short dependent launches).  Same items, order and counts as plan_count +
+// scans + plan_fill.
+constexpr uint64_t kPlanSmallW = 32768;
+__global__ void __launch_bounds__(1024) plan_async_small(const uint32_t* __restrict__ rp, uint64_t W, uint32_t seg,
+                                                         uint32_t k, WorkItem* __restrict__ items,
+                                                         SplitWindow* __restrict__ split, uint64_t cap,
+                                                         uint32_t* __restrict__ dcounts) {
+    __shared__ unsigned long long s_blocks;
+    if (threadIdx.x == 0) s_blocks = 0;
+    __syncthreads();
+    uint32_t slots = 0, splits = 0;
+    unsigned long long blocks = 0;
+    for (uint64_t w = threadIdx.x; w < W; w += blockDim.x) {
+        const uint32_t nv = rp[w + 1] - rp[w];
+        if (nv > seg) {
+            slots += (nv + seg - 1) / seg;
+            splits += 1;
+        }
+        blocks += (nv + k - 1) / k;
+    }
+    atomicAdd(&s_blocks, blocks);
+    uint32_t n_slots, n_split;
+    dev::block_exclusive_scan(slots, &n_slots);
+    __syncthreads();
+    dev::block_exclusive_scan(splits, &n_split);
+    __syncthreads();
+    const uint64_t off = cap - (uint64_t(n_slots) + (W - n_split));
+    if (threadIdx.x == 0) {
+        dcounts[0] = static_cast<uint32_t>(off);
+        dcounts[1] = n_split;
+        *reinterpret_cast<unsigned long long*>(dcounts + 2) = s_blocks;
+    }
+    uint32_t carry_slot = 0, carry_split = 0;
+    for (uint64_t base = 0; base < W; base += blockDim.x) {
+        const uint64_t w = base + threadIdx.x;
+        const uint32_t nv = w < W ? rp[w + 1] - rp[w] : 0u;
+        const uint32_t nseg = nv > seg ? (nv + seg - 1) / seg : 0u;  // 0: not split
+        uint32_t t_slot, t_split;
+        const uint32_t so = carry_slot + dev::block_exclusive_scan(nseg, &t_slot);
+        __syncthreads();
+        const uint32_t sp = carry_split + dev::block_exclusive_scan(nseg ? 1u : 0u, &t_split);
+        __syncthreads();
+        if (w < W) {
+            if (nseg) {
+                for (uint32_t i = 0; i < nseg; ++i)
+                    items[off + so + i] = WorkItem{(uint32_t)w, i * seg, min(nv, (i + 1) * seg), so + i};
+                split[sp] = SplitWindow{(uint32_t)w, so, nseg, 0};
+            } else {
+                items[off + n_slots + (w - sp)] = WorkItem{(uint32_t)w, 0, nv, kNoSlot};
+            }
+        }
+        carry_slot += t_slot;
+        carry_split += t_split;
+    }
+}
+
 __global__ void plan_blocks_out(const PlanTotals* __restrict__ tot, uint32_t* __restrict__ dcounts) {
     *reinterpret_cast<unsigned long long*>(dcounts + 2) = tot->blocks_k;
 }
@@ -275,6 +334,12 @@ Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, uint64_t seg_nv, cu
     p->items = static_cast<WorkItem*>(dalloc(std::max<uint64_t>(1, p->n_items) * sizeof(WorkItem), s));
     p->split = static_cast<SplitWindow*>(dalloc(std::max<uint64_t>(1, split_cap) * sizeof(SplitWindow), s));
     p->dcounts = static_cast<uint32_t*>(dalloc(16, s));
+    if (W && W <= kPlanSmallW) {
+        plan_async_small<<<1, 1024, 0, s>>>(m->row_pointers, W, seg, m->k, p->items, p->split, p->n_items,
+                                            p->dcounts);
+        TCS_LAUNCHED("plan_async_small");
+        return p;
+    }
     TCS_CUDA(cudaMemsetAsync(p->dcounts, 0, 16, s));
     if (W) {
         DBuf nslot((W + 1) * 4, s), nsplit((W + 1) * 4, s), slot_off((W + 1) * 4, s), split_off((W + 1) * 4, s);
