@@ -29,6 +29,7 @@
 //                     rounds with __float2half_rn (== ref round_to_fp16, checked
 //                     exhaustively on device by the tests); F32 keeps raw bits.
 #include <algorithm>
+#include <cstddef>
 
 #include "tcs_internal.cuh"
 
@@ -123,14 +124,18 @@ __device__ __forceinline__ void list_push(bool mine, uint32_t w, uint32_t* count
     }
 }
 
+// nvw_zero (pipelined encode): every window's vector count starts at 0, so
+// a window that fails validation (in no list) scans as empty.
 template <int VH>
 __global__ void window_stats(const uint32_t* __restrict__ rp, uint64_t rows, uint64_t W, uint64_t nnz,
-                             CheckOut* out, uint32_t* __restrict__ small, uint32_t* __restrict__ big) {
+                             CheckOut* out, uint32_t* __restrict__ small, uint32_t* __restrict__ big,
+                             uint32_t* __restrict__ nvw_zero) {
     uint32_t mx = 0, bad = 0;
     const uint64_t W32 = (W + 31) / 32 * 32;  // whole warps iterate (ballots below)
     for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < W32; w += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t n = 0;
         bool ok = false;
+        if (nvw_zero && w < W) nvw_zero[w] = 0u;
         if (w < W) {
             const uint64_t r0 = VH * w, r1 = min(r0 + VH, rows);
             uint32_t prev = rp[r0];
@@ -882,18 +887,20 @@ using namespace tcs;
 namespace tcs {
 namespace {
 
-// async_bad == nullptr: the API encode (exact sizes; validation errors are
+// async_chk == nullptr: the API encode (exact sizes; validation errors are
 // thrown before it returns; three host round trips).  Otherwise the
 // pipelined encode of tcs_spmm_csr_host: no host round trip at all -- the
 // size-class kernels run on capacity grids and read their counts on the
 // device, the ME-BCRS arrays are allocated for nv <= nnz, the work list is
 // built with device-side counts (build_plan_async), and the validation code
-// lands in *async_bad (device) for the caller to check once at the end.
+// (CheckOut::bad) lands in the caller-owned, pre-zeroed async_chk block
+// (encode_check_bytes() of device memory) for the caller to check once at
+// the end -- no per-chunk memset or flag copy.
 // The handle's num_vectors is then a capacity, and SDDMM liveness extras
 // are not built (the pipeline only multiplies).
 template <int VH>
 void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                 tcs_stream_t stream, uint32_t* async_bad = nullptr, uint64_t seg_nv = 0,
+                 tcs_stream_t stream, void* async_chk = nullptr, uint64_t seg_nv = 0,
                  cudaEvent_t values_ready = nullptr) {
     {
         if (!csr || !out) fail(TCS_ERR_ARGUMENT, "null argument");
@@ -904,7 +911,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         if (!csr->row_ptr || (csr->nnz && (!csr->col_idx || !csr->values))) fail(TCS_ERR_ARGUMENT, "null CSR array");
         if (csr->nnz >= (1ull << 32)) fail(TCS_ERR_FORMAT, "nnz exceeds u32 row_ptr");
         cudaStream_t s = st(stream);
-        const bool async = async_bad != nullptr;
+        const bool async = async_chk != nullptr;
         const uint64_t rows = csr->rows, W = (rows + VH - 1) / VH, nnz = csr->nnz, cols = csr->cols;
         const uint32_t k = precision == TCS_FP16 ? 8 : 4;
         const int sms = num_sms();
@@ -941,16 +948,22 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
         } live_cleanup{exact_live, s};
         if (W) {
             // K0: row_ptr invariants + size-class window lists
-            DBuf chk(sizeof(CheckOut), s), small_list(W * 4, s), big_list(W * 4, s);
-            TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
+            DBuf chk, small_list(W * 4, s), big_list(W * 4, s);
+            CheckOut* dchk = static_cast<CheckOut*>(async_chk);
+            if (!async) {
+                chk = DBuf(sizeof(CheckOut), s);
+                TCS_CUDA(cudaMemsetAsync(chk.p, 0, sizeof(CheckOut), s));
+                dchk = chk.as<CheckOut>();
+            }
+            DBuf nvw(W * 4, s);
             const int g0 = static_cast<int>(std::min<uint64_t>((W + 255) / 256, uint64_t(sms) * 8));
-            window_stats<VH><<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, chk.as<CheckOut>(),
-                                                small_list.as<uint32_t>(), big_list.as<uint32_t>());
+            window_stats<VH><<<g0, 256, 0, s>>>(csr->row_ptr, rows, W, nnz, dchk, small_list.as<uint32_t>(),
+                                                big_list.as<uint32_t>(), async ? nvw.as<uint32_t>() : nullptr);
             TCS_LAUNCHED("window_stats");
             CheckOut h{};
             if (!async) {
                 uint32_t ends[2] = {0, 0};
-                TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaMemcpyAsync(&h, dchk, sizeof(h), cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaMemcpyAsync(&ends[0], csr->row_ptr, 4, cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaMemcpyAsync(&ends[1], csr->row_ptr + rows, 4, cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaStreamSynchronize(s));
@@ -964,11 +977,8 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             }
 
             DBuf tmp_cols(std::max<uint64_t>(1, nnz) * 4, s), rank(std::max<uint64_t>(1, nnz) * 4, s);
-            DBuf nvw(W * 4, s);
-            // windows that fail validation are in no list: 0 vectors (the
-            // pipelined encode scans before anyone looks at the flag)
-            if (async) TCS_CUDA(cudaMemsetAsync(nvw.p, 0, W * 4, s));
-            CheckOut* dchk = chk.as<CheckOut>();
+            // (pipelined encode: window_stats zeroed nvw -- windows that fail
+            // validation are in no list, so they scan as 0 vectors)
             const uint64_t n_big = uint64_t(h.n_medium) + h.n_huge;
             if (h.n_tiny) {
                 const int gt = static_cast<int>(
@@ -1035,7 +1045,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             exclusive_scan_u32(nvw.as<uint32_t>(), m.row_pointers, W, s);
             if (!async) {
                 TCS_CUDA(cudaMemcpyAsync(&nv, m.row_pointers + W, 4, cudaMemcpyDeviceToHost, s));
-                TCS_CUDA(cudaMemcpyAsync(&h, chk.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+                TCS_CUDA(cudaMemcpyAsync(&h, dchk, sizeof(h), cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaStreamSynchronize(s));
                 if (h.bad) fail(TCS_ERR_FORMAT, kBadMsg[h.bad < 5 ? h.bad : 0]);
             } else {
@@ -1101,9 +1111,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                         kScatterTileSmall, small_list.as<uint32_t>(), false, n_smalls);
             }
             TCS_LAUNCHED("window_scatter");
-            if (async) {
-                TCS_CUDA(cudaMemcpyAsync(async_bad, &dchk->bad, 4, cudaMemcpyDeviceToDevice, s));
-            } else if (value_dtype == TCS_DTYPE_F16 && VH == 8) {
+            if (!async && value_dtype == TCS_DTYPE_F16 && VH == 8) {
                 uint32_t tiny = 0;
                 TCS_CUDA(cudaMemcpyAsync(&tiny, &dchk->tiny, 4, cudaMemcpyDeviceToHost, s));
                 TCS_CUDA(cudaStreamSynchronize(s));
@@ -1120,7 +1128,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
             TCS_CUDA(cudaMemsetAsync(m.row_pointers, 0, 4, s));
             m.column_indices = static_cast<uint32_t*>(dalloc(4, s));
             m.values = dalloc(4, s);
-            if (async) TCS_CUDA(cudaMemsetAsync(async_bad, 0, 4, s));
+
         }
         cleanup.armed = false;
         *out = m;
@@ -1146,11 +1154,13 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
 }  // namespace
 
 const char* encode_bad_msg(uint32_t code) { return kBadMsg[code < 5 ? code : 0]; }
+size_t encode_check_bytes() { return (sizeof(CheckOut) + 15) / 16 * 16; }
+size_t encode_check_bad_offset() { return offsetof(CheckOut, bad); }
 
 // The pipelined encode (see encode_impl): tcs_spmm_csr_host's chunks.
 void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                         cudaStream_t s, uint32_t* bad_dev, uint64_t seg_nv, cudaEvent_t values_ready) {
-    encode_impl<8>(csr, precision, value_dtype, out, reinterpret_cast<tcs_stream_t>(s), bad_dev, seg_nv,
+                         cudaStream_t s, void* check_dev, uint64_t seg_nv, cudaEvent_t values_ready) {
+    encode_impl<8>(csr, precision, value_dtype, out, reinterpret_cast<tcs_stream_t>(s), check_dev, seg_nv,
                    values_ready);
 }
 

@@ -25,6 +25,7 @@
 // Windows longer than plan.seg are split; partial sums are reduced in
 // segment order by spmm_reduce_split (deterministic, no atomics).
 #include <algorithm>
+#include <cstring>
 #include <memory>
 #include <cstdio>
 #include <cstdlib>
@@ -1787,7 +1788,10 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         // pipelined chunks (no host round trip per chunk) unless the tcgen05
         // path is requested (its launcher sizes the work list on the host)
         const bool pipelined = !(cfg->flags & TCS_CFG_PATH_TCGEN05);
-        DBuf d_flags(max_chunks * 4, s), d_blocks(max_chunks * 8, s);
+        // per-chunk encode validation blocks, zeroed once
+        const size_t chk_bytes = encode_check_bytes();
+        DBuf d_checks(max_chunks * chk_bytes, s), d_blocks(max_chunks * 8, s);
+        TCS_CUDA(cudaMemsetAsync(d_checks.p, 0, max_chunks * chk_bytes, s));
         Streams& ss = thread_streams();
         // On any exit (an error in a later chunk included) the side streams'
         // queued copies and kernels finish before the buffers above are
@@ -1888,7 +1892,7 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
             tcs_status rc = TCS_OK;
             if (pipelined) {
                 encode_mebcrs_async(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, cs,
-                                    d_flags.as<uint32_t>() + i, 0, landed[i].e);
+                                    d_checks.as<unsigned char>() + i * chk_bytes, 0, landed[i].e);
             } else {
                 landed[i].wait_on(cs);
                 rc = tcs_mebcrs_encode(&chunk, precision, f16 ? TCS_DTYPE_F16 : TCS_DTYPE_F32, &m, ks);
@@ -1934,16 +1938,19 @@ extern "C" tcs_status tcs_spmm_csr_host(const tcs_csr* host_csr, tcs_precision p
         for (auto& e : joined_compute) e.wait_on(s);
         joined_drain.wait_on(s);
         join.joined = true;
-        std::vector<uint32_t> bad(nchunks, 0);
+        std::vector<unsigned char> checks(nchunks * chk_bytes, 0);
         std::vector<uint64_t> blocks(nchunks, 0);
         if (pipelined) {
-            TCS_CUDA(cudaMemcpyAsync(bad.data(), d_flags.p, nchunks * 4, cudaMemcpyDeviceToHost, s));
+            TCS_CUDA(cudaMemcpyAsync(checks.data(), d_checks.p, nchunks * chk_bytes, cudaMemcpyDeviceToHost, s));
             if (counters)
                 TCS_CUDA(cudaMemcpyAsync(blocks.data(), d_blocks.p, nchunks * 8, cudaMemcpyDeviceToHost, s));
         }
         TCS_CUDA(cudaStreamSynchronize(s));
-        for (uint64_t i = 0; i < nchunks; ++i)  // the first invalid chunk's validation code (encode.cu kBadMsg)
-            if (bad[i]) fail(TCS_ERR_FORMAT, encode_bad_msg(bad[i]));
+        for (uint64_t i = 0; i < nchunks; ++i) {  // the first invalid chunk's validation code (encode.cu kBadMsg)
+            uint32_t bad = 0;
+            std::memcpy(&bad, checks.data() + i * chk_bytes + encode_check_bad_offset(), 4);
+            if (bad) fail(TCS_ERR_FORMAT, encode_bad_msg(bad));
+        }
         if (counters && pipelined)
             for (uint64_t i = 0; i < nchunks; ++i) counters->mma_invocations += blocks[i] * ((n + 15) / 16);
     });

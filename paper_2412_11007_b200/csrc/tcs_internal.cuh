@@ -177,9 +177,13 @@ struct Plan {
 Plan* build_plan(const tcs_mebcrs* m, cudaStream_t s, uint32_t* max_nv, uint64_t* blocks_k,
                  uint64_t* groups16);
 Plan* build_plan_async(const tcs_mebcrs* m, uint64_t nv_cap, uint64_t seg_nv, cudaStream_t s);
+// check_dev: a caller-owned, zeroed block of encode_check_bytes() device
+// bytes; its validation code sits at encode_check_bad_offset() (u32).
 void encode_mebcrs_async(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dtype, tcs_mebcrs* out,
-                         cudaStream_t s, uint32_t* bad_dev, uint64_t seg_nv, cudaEvent_t values_ready);
+                         cudaStream_t s, void* check_dev, uint64_t seg_nv, cudaEvent_t values_ready);
 const char* encode_bad_msg(uint32_t code);
+size_t encode_check_bytes();
+size_t encode_check_bad_offset();
 void free_plan(Plan* p, cudaStream_t s);
 
 // ------------------------------------------------------------ conversions
