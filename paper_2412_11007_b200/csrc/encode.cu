@@ -18,12 +18,13 @@
 //      window_bitmap  long windows when the column space fits shared memory
 //                     (<= 819,200 columns): set one bit per column, prefix-
 //                     popcount the words -> rank(c) = prefix[c/32] +
-//                     popc(word & below(c)); sorted unique columns fall out of
-//                     the word scan.  O(cols/32 + entries) per window.
+//                     popc(word & below(c)).  O(cols/32 + entries) per window.
 //                     Both validate the column indices of their window (range,
 //                     strictly ascending within a row).
 //   K2 scan           row_pointers = exclusive scan of nv_w (u32, as the ref).
-//   K3 window_scatter CTA per window: column_indices, and every CSR value to
+//   K3 window_scatter CTA per window: column_indices (each entry stores its
+//                     column at slot rank; duplicates store the same value),
+//                     and every CSR value to
 //                     8*(rp[w]+b*k) + r*width_b + j, width_b = min(k, nv_w-b*k)
 //                     (ref mebcrs.hpp:46-56); all other slots 0.  F16 storage
 //                     rounds with __float2half_rn (== ref round_to_fp16, checked
@@ -69,7 +70,28 @@ constexpr uint32_t kBigThreads = TCS_ENC_SORT_THREADS;
 #endif
 constexpr uint32_t kBitmapThreads = TCS_ENC_BITMAP_THREADS;
 constexpr uint32_t kBitmapMaxWords = 25600;
-constexpr int kBitmapU = 8;  // entries per thread in flight (window_bitmap)  // 2 x 100 KB of smem -> <= 819,200 columns
+// resident CTAs per SM the register budget is sized for (C3's 233 K-column
+// bitmap + prefix take 58 KB of shared memory, so three fit)
+#ifndef TCS_ENC_BITMAP_MINB
+#define TCS_ENC_BITMAP_MINB 3
+#endif
+constexpr int kBitmapMinBlocks = TCS_ENC_BITMAP_MINB;
+#ifndef TCS_ENC_BITMAP_KEEP
+#define TCS_ENC_BITMAP_KEEP 1
+#endif
+constexpr bool kBitmapKeep = TCS_ENC_BITMAP_KEEP;
+// column_indices written by the entries (every entry stores its column at
+// slot base + rank; entries sharing a column store the same value) instead of
+// a copy of the rank kernels' distinct-column list: the bitmap ranking then
+// writes no column list at all, and the CTA scatter has no copy pass
+#ifndef TCS_ENC_COLS_FROM_ENTRIES
+#define TCS_ENC_COLS_FROM_ENTRIES 1
+#endif
+constexpr bool kColsFromEntries = TCS_ENC_COLS_FROM_ENTRIES;
+#ifndef TCS_ENC_BITMAP_U
+#define TCS_ENC_BITMAP_U 4
+#endif
+constexpr int kBitmapU = TCS_ENC_BITMAP_U;  // entries per thread in flight (window_bitmap)  // 2 x 100 KB of smem -> <= 819,200 columns
 constexpr uint64_t kSentinel = ~0ull;
 
 struct CheckOut {
@@ -277,7 +299,7 @@ __device__ __forceinline__ void window_sort_rank(const uint32_t* __restrict__ cs
         const uint64_t key = bufB[p];
         const uint32_t col = static_cast<uint32_t>(key >> 32);
         if (p == 0 || col != static_cast<uint32_t>(bufB[p - 1] >> 32)) {
-            tmp_cols[e0 + run] = col;
+            if (!kColsFromEntries) tmp_cols[e0 + run] = col;  // else the scatter's entries write them
             ++run;
         }
         rank[e0 + static_cast<uint32_t>(key)] = run - 1;
@@ -470,25 +492,43 @@ __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ 
     for (uint32_t i = threadIdx.x; i < quads; i += nt) bm4[i] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     // kBitmapU entries per thread in flight: a hub window (10^4..10^5
-    // entries) is otherwise a chain of dependent-latency iterations
+    // entries) is otherwise a chain of dependent-latency iterations.  The
+    // first batch's columns stay in registers for the rank pass (a window of
+    // up to kBitmapU * nt entries reads its columns once).
+    const uint32_t lane = threadIdx.x & 31;
     uint32_t bad = 0;
-    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
-        uint32_t c[kBitmapU], cp[kBitmapU];
+    uint32_t keep[kBitmapU];
+    // warp-uniform trip count (i0 - lane): the predecessor shuffle needs
+    // every lane of the warp
+    for (uint32_t i0 = threadIdx.x; i0 - lane < n; i0 += kBitmapU * nt) {
+        uint32_t c[kBitmapU], cp0[kBitmapU];
 #pragma unroll
         for (int u = 0; u < kBitmapU; ++u) {
             const uint32_t i = i0 + u * nt;
-            c[u] = i < n ? __ldg(ci + e0 + i) : 0u;
-            cp[u] = i < n && i > 0 ? __ldg(ci + e0 + i - 1) : 0u;
+            c[u] = i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
+            // predecessor: lane - 1's column (consecutive lanes hold
+            // consecutive entries), loaded only by lane 0
+            cp0[u] = lane == 0 && i < n && i > 0 ? __ldg(ci + e0 + i - 1) : 0u;
+        }
+        if (kBitmapKeep && i0 == threadIdx.x) {
+#pragma unroll
+            for (int u = 0; u < kBitmapU; ++u) keep[u] = c[u];
         }
 #pragma unroll
         for (int u = 0; u < kBitmapU; ++u) {
             const uint32_t i = i0 + u * nt;
+            uint32_t cp = __shfl_up_sync(0xffffffffu, c[u], 1);
+            if (lane == 0) cp = cp0[u];
             if (i >= n) continue;
-            bool row_start = false;
+            // check_col: a non-ascending pair is legal only across a row
+            // boundary (rare, so the boundary test is off the common path)
+            uint32_t b = c[u] >= cols ? 3u : 0u;
+            if (i > 0 && cp >= c[u]) {
+                bool row_start = false;
 #pragma unroll
-            for (int r = 0; r < VH; ++r) row_start |= (i == rb[r]);
-            // check_col with the predecessor already loaded
-            const uint32_t b = !row_start && cp[u] >= c[u] ? 4u : c[u] >= cols ? 3u : 0u;
+                for (int r = 1; r < VH; ++r) row_start |= (i == rb[r]);
+                if (!row_start) b = 4u;
+            }
             bad = max(bad, b);
             if (c[u] < cols) atomicOr(reinterpret_cast<uint32_t*>(bm4) + (c[u] >> 5), 1u << (c[u] & 31));
         }
@@ -503,37 +543,34 @@ __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ 
         cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
     }
     uint32_t total;
-    uint32_t run = dev::block_exclusive_scan(cnt, &total);
+    const uint32_t run = dev::block_exclusive_scan(cnt, &total);
+    uint32_t p = run;
     for (uint32_t i = q0; i < q1; ++i) {
         const uint4 x = bm4[i];
-        const uint32_t p0 = run, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
+        const uint32_t p0 = p, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
         pre4[i] = make_uint4(p0, p1, p2, p3);
-        if ((x.x | x.y | x.z | x.w) == 0u) continue;
-        const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            uint32_t bits = wv[k];
-            while (bits) {  // sorted unique columns of the window
-                const uint32_t b = __ffs(bits) - 1;
-                tmp_cols[e0 + run++] = 32 * (4 * i + k) + b;
-                bits &= bits - 1;
-            }
-        }
+        p = p3 + __popc(x.w);
     }
     if (threadIdx.x == 0) nv_out[w] = total;
     __syncthreads();
+    // ranks, and the window's sorted distinct columns: every entry writes
+    // its column to slot rank (entries sharing a column write the same
+    // value), so every slot < total is written and no bit scan is needed
     for (uint32_t i0 = threadIdx.x; i0 < n; i0 += kBitmapU * nt) {
         uint32_t c[kBitmapU];
 #pragma unroll
         for (int u = 0; u < kBitmapU; ++u) {
             const uint32_t i = i0 + u * nt;
-            c[u] = i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
+            c[u] = kBitmapKeep && i0 == threadIdx.x ? keep[u] : i < n ? __ldg(ci + e0 + i) : 0xFFFFFFFFu;
         }
 #pragma unroll
         for (int u = 0; u < kBitmapU; ++u) {
             const uint32_t i = i0 + u * nt;
-            if (i < n && c[u] < cols)
-                rank[e0 + i] = pre[c[u] >> 5] + __popc(bm[c[u] >> 5] & ((1u << (c[u] & 31)) - 1u));
+            if (i < n && c[u] < cols) {
+                const uint32_t r = pre[c[u] >> 5] + __popc(bm[c[u] >> 5] & ((1u << (c[u] & 31)) - 1u));
+                rank[e0 + i] = r;
+                if (!kColsFromEntries) tmp_cols[e0 + r] = c[u];
+            }
         }
     }
     __syncthreads();  // bitmap, prefix and rb are reused by the next window
@@ -542,7 +579,7 @@ __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ 
 // Bitmap ranking for windows with more than kSmallCap entries (column
 // space within shared memory).
 template <int VH>
-__global__ void __launch_bounds__(kBitmapThreads) window_bitmap(const uint32_t* __restrict__ csr_rp,
+__global__ void __launch_bounds__(kBitmapThreads, kBitmapMinBlocks) window_bitmap(const uint32_t* __restrict__ csr_rp,
                                                                 const uint32_t* __restrict__ ci, uint64_t rows,
                                                                 uint64_t cols, uint64_t W,
                                                                 uint32_t* __restrict__ tmp_cols,
@@ -581,6 +618,10 @@ __device__ __forceinline__ __half store_cvt<__half>(float x) { return __float2ha
 #endif
 constexpr uint32_t kScatterTileBig = TCS_ENC_SCATTER_TILE;  // vectors per smem tile (multiple of k)
 constexpr int kScatterThreadsBig = TCS_ENC_SCATTER_THREADS;
+#ifndef TCS_ENC_SCATTER_MINB
+#define TCS_ENC_SCATTER_MINB 3
+#endif
+constexpr int kScatterMinBlocksBig = TCS_ENC_SCATTER_MINB;  // 3 x 64 KB half tiles per SM
 constexpr uint32_t kScatterTileSmall = kSmallCap;
 constexpr int kScatterThreadsSmall = 128;
 constexpr uint32_t kRangedTiles = 4;  // windows beyond this many tiles use per-row ranges
@@ -697,7 +738,8 @@ __global__ void __launch_bounds__(scatter_warps<VH, V>() * 32) window_scatter_wa
 }
 
 template <int VH, typename V, int THREADS, uint32_t TILE>
-__global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __restrict__ csr_rp,
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? kScatterMinBlocksBig : 8) window_scatter(const uint32_t* __restrict__ csr_rp,
+                                                      const uint32_t* __restrict__ csr_ci,
                                                       const float* __restrict__ csr_vals, uint64_t rows, uint64_t W,
                                                       uint32_t k, const uint32_t* __restrict__ rp,
                                                       const uint32_t* __restrict__ tmp_cols,
@@ -706,6 +748,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                                                       const uint32_t* __restrict__ list, bool big, CheckOut* chk,
                                                       const uint32_t* __restrict__ tile_off) {
     extern __shared__ uint4 tile_raw[];
+    const uint32_t ks = __ffs(k) - 1;  // log2 k
     // big list: units = (huge window, tile) pairs (huge_tile_prefix), then
     // the medium windows from the back of the list, dynamic queue; small
     // list: tiny windows from the front, small from the back, fixed stride
@@ -753,7 +796,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
         const uint32_t v_hi = uint64_t(tile_hi) * kTile < nvw ? tile_hi * kTile : nvw;
         // the column copy, 8 loads in flight per thread (one at a time it was
         // the kernel's top stall: a DRAM latency per 512 columns)
-        for (uint32_t i0 = v_lo + threadIdx.x; i0 < v_hi; i0 += 8 * blockDim.x) {
+        for (uint32_t i0 = v_lo + threadIdx.x; !kColsFromEntries && i0 < v_hi; i0 += 8 * blockDim.x) {
             uint32_t cc[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -810,7 +853,7 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
             const uint32_t total = ranged ? roff[VH] : e1 - e0;
             // kScatterU entries in flight per thread (coalesced per sub-step)
             for (uint32_t i4 = 0; i4 < total; i4 += kScatterU * blockDim.x) {
-                uint32_t v[kScatterU], e[kScatterU];
+                uint32_t v[kScatterU], e[kScatterU], c[kScatterU];
                 float x[kScatterU];
 #pragma unroll
                 for (int u = 0; u < kScatterU; ++u) {
@@ -828,17 +871,19 @@ __global__ void __launch_bounds__(THREADS) window_scatter(const uint32_t* __rest
                     }
                     v[u] = e[u] != 0xFFFFFFFFu ? __ldg(rank + e[u]) : 0u;
                     x[u] = e[u] != 0xFFFFFFFFu ? __ldg(csr_vals + e[u]) : 0.f;
+                    c[u] = kColsFromEntries && e[u] != 0xFFFFFFFFu ? __ldg(csr_ci + e[u]) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < kScatterU; ++u) {
                     if (e[u] == 0xFFFFFFFFu || v[u] < t0 || v[u] >= t0 + tn) continue;
+                    if (kColsFromEntries) out_ci[base + v[u]] = c[u];
                     uint32_t r = 0;
 #pragma unroll
                     for (int q = 1; q < VH; ++q) r += (e[u] >= rb[q]) ? 1u : 0u;
-                    const uint32_t b = v[u] / k, j = v[u] - b * k;
-                    const uint32_t width = min(k, nvw - b * k);
+                    const uint32_t b = v[u] >> ks, j = v[u] & (k - 1);  // k is 4 or 8
+                    const uint32_t width = min(k, nvw - (b << ks));
                     const V y = store_cvt<V>(x[u]);
-                    tile[(b * k - t0) * VH + r * width + j] = y;
+                    tile[((b << ks) - t0) * VH + r * width + j] = y;
                     if constexpr (sizeof(V) == 2) {  // nonzero f32 that rounds to a binary16 zero
                         if ((__float_as_uint(x[u]) & 0x7FFFFFFFu) && !(__half_as_ushort(y) & 0x7FFFu)) atomicOr(tiny, 1u);
                     }
@@ -872,7 +917,7 @@ __global__ void exact_live_build(const uint32_t* __restrict__ csr_rp, const floa
 
 // Value type V of a window_scatter instantiation (for the launch helper).
 template <typename V>
-V kern_value_type(void (*)(const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
+V kern_value_type(void (*)(const uint32_t*, const uint32_t*, const float*, uint64_t, uint64_t, uint32_t, const uint32_t*,
                            const uint32_t*, const uint32_t*, uint32_t*, V*, const uint32_t*, bool, CheckOut*,
                            const uint32_t*));
 
@@ -1064,7 +1109,7 @@ void encode_impl(const tcs_csr* csr, tcs_precision precision, tcs_dtype value_dt
                 const int g3 = static_cast<int>(std::min<uint64_t>(n, uint64_t(sms) * per_sm));
                 TCS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               static_cast<int>(tile_smem)));
-                kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->values, rows, W, k, m.row_pointers,
+                kern<<<g3, threads, tile_smem, s>>>(csr->row_ptr, csr->col_idx, csr->values, rows, W, k, m.row_pointers,
                                                     tmp_cols.as<uint32_t>(), rank.as<uint32_t>(), m.column_indices,
                                                     static_cast<decltype(kern_value_type(kern))*>(m.values), list,
                                                     big, dchk, tile_off.as<uint32_t>());
