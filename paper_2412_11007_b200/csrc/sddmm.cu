@@ -512,6 +512,10 @@ constexpr int kBurstBlocks = 8;
 #define TCS_BURST_WARPS 4
 #endif
 constexpr int kBW = TCS_BURST_WARPS;  // warps per CTA of the burst kernel
+// most warps sharing one item (A/B knob)
+#ifndef TCS_SDDMM_BURST_SUB
+#define TCS_SDDMM_BURST_SUB 16
+#endif
 template <bool TF32, int NSC, int MM, bool OF32, int G>
 __global__ void __launch_bounds__(kBW * 32, kBurstBlocks * kWarps / kBW) sddmm_burst(const SddmmArgs a) {
     using Elem = typename std::conditional<TF32, float, __half>::type;
@@ -743,7 +747,7 @@ void sddmm_launch(const tcs_mebcrs* mask, Plan* plan, const void* a, tcs_dtype a
     if (fpad == nsc * sc && nsc <= 2 && plan->seg <= 512 && plan->n_items <= burst_cap) {
         SddmmArgs b{plan->n_split ? plan->items : nullptr, plan->n_items, mask->row_pointers, mask->column_indices,
                     mask->values, ap, alda, bp, bldb, out_values, mask->rows, 1, mask->k, nullptr, dead, nullptr,
-                    static_cast<uint32_t>(std::min<uint64_t>(16, burst_cap / plan->n_items))};
+                    static_cast<uint32_t>(std::min<uint64_t>(TCS_SDDMM_BURST_SUB, burst_cap / plan->n_items))};
         if (static_mask) b.live = mask_liveness(mask, plan, s);
         else if (const uint8_t* ex = plan->exact_for(mask->values)) b.live = ex;
         if (tf32) {

@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(kWarps * 32, 4) spmm_f16_direct_kernel(const S
 template <int NCHUNK>
 struct Tf32Step {
     uint4 L[2][NCHUNK];  // loader slots: vector q + 4u, features 32c + 4p .. +3
-    uint32_t b[2];       // sparse fragment: row g, vectors t, t+4
+    uint32_t b[2];       // sparse fragment: row g, vectors t, t+4 (raw f32 bits)
 };
 
 __device__ __forceinline__ float tf32_val_general(const float* vals, uint64_t vbase, uint32_t nvw, uint32_t v,
@@ -689,8 +689,11 @@ __device__ __forceinline__ void tf32_issue(const SpmmArgs& a, const float* __res
         x0 = s + t < vend ? tf32_val_general(fv, vbase, nvw, s + t, g) : 0.f;
         x1 = s + t + 4 < vend ? tf32_val_general(fv, vbase, nvw, s + t + 4, g) : 0.f;
     }
-    st.b[0] = to_tf32(x0);
-    st.b[1] = to_tf32(x1);
+    // raw f32 bits: rounded to TF32 in the compute step, so the conversion
+    // does not wait here for the value loads (ncu, C3 N=128: 57% of the
+    // stall samples sat on this conversion, before the previous step's MMAs)
+    st.b[0] = __float_as_uint(x0);
+    st.b[1] = __float_as_uint(x1);
 }
 
 __device__ __forceinline__ uint4 shfl4(uint4 v, uint32_t src) {
@@ -701,13 +704,14 @@ __device__ __forceinline__ uint4 shfl4(uint4 v, uint32_t src) {
 template <int NCHUNK>
 __device__ __forceinline__ void tf32_compute(const Tf32Step<NCHUNK>& st, float (&acc)[NCHUNK][2][4],
                                              uint32_t src_lane) {
+    const uint32_t b0 = to_tf32(__uint_as_float(st.b[0])), b1 = to_tf32(__uint_as_float(st.b[1]));
 #pragma unroll
     for (int c = 0; c < NCHUNK; ++c) {
         const uint4 x = shfl4(st.L[0][c], src_lane), y = shfl4(st.L[1][c], src_lane);
         mma_tf32_1688(acc[c][0], to_tf32(__uint_as_float(x.x)), to_tf32(__uint_as_float(x.y)),
-                      to_tf32(__uint_as_float(y.x)), to_tf32(__uint_as_float(y.y)), st.b[0], st.b[1]);
+                      to_tf32(__uint_as_float(y.x)), to_tf32(__uint_as_float(y.y)), b0, b1);
         mma_tf32_1688(acc[c][1], to_tf32(__uint_as_float(x.z)), to_tf32(__uint_as_float(x.w)),
-                      to_tf32(__uint_as_float(y.z)), to_tf32(__uint_as_float(y.w)), st.b[0], st.b[1]);
+                      to_tf32(__uint_as_float(y.z)), to_tf32(__uint_as_float(y.w)), b0, b1);
     }
 }
 
@@ -859,7 +863,7 @@ template <int NCHUNK>
 struct Tf32PStep {
     uint4 H[2][NCHUNK];     // loader slots: vector q + 4u, hi of features 64c + 8p .. +7
     uint32_t L[2][NCHUNK];  // their nibbles
-    uint32_t b[2];          // sparse fragment: row g, vectors t, t+4
+    uint32_t b[2];          // sparse fragment: row g, vectors t, t+4 (raw f32 bits)
 };
 
 template <int NCHUNK>
@@ -918,13 +922,17 @@ __device__ __forceinline__ void tf32p_issue(const SpmmArgs& a, const unsigned ch
         x0 = s + t < vend ? tf32_val_general(fv, vbase, nvw, s + t, g) : 0.f;
         x1 = s + t + 4 < vend ? tf32_val_general(fv, vbase, nvw, s + t + 4, g) : 0.f;
     }
-    st.b[0] = to_tf32(x0);
-    st.b[1] = to_tf32(x1);
+    // raw f32 bits: rounded to TF32 in the compute step, so the conversion
+    // does not wait here for the value loads (ncu, C3 N=128: 57% of the
+    // stall samples sat on this conversion, before the previous step's MMAs)
+    st.b[0] = __float_as_uint(x0);
+    st.b[1] = __float_as_uint(x1);
 }
 
 template <int NCHUNK>
 __device__ __forceinline__ void tf32p_compute(const Tf32PStep<NCHUNK>& st, float (&acc)[NCHUNK][4][4],
                                               uint32_t src_lane) {
+    const uint32_t b0 = to_tf32(__uint_as_float(st.b[0])), b1 = to_tf32(__uint_as_float(st.b[1]));
 #pragma unroll
     for (int c = 0; c < NCHUNK; ++c) {
         const uint4 x = shfl4(st.H[0][c], src_lane), y = shfl4(st.H[1][c], src_lane);
@@ -932,13 +940,13 @@ __device__ __forceinline__ void tf32p_compute(const Tf32PStep<NCHUNK>& st, float
         const uint32_t ly = __shfl_sync(0xffffffffu, st.L[1][c], src_lane);
         const uint32_t sx = lx << 4, sy = ly << 4;
         mma_tf32_1688(acc[c][0], tf32p_even<0>(x.x, sx), tf32p_odd<0>(x.x, lx), tf32p_even<0>(y.x, sy),
-                      tf32p_odd<0>(y.x, ly), st.b[0], st.b[1]);
+                      tf32p_odd<0>(y.x, ly), b0, b1);
         mma_tf32_1688(acc[c][1], tf32p_even<1>(x.y, sx), tf32p_odd<1>(x.y, lx), tf32p_even<1>(y.y, sy),
-                      tf32p_odd<1>(y.y, ly), st.b[0], st.b[1]);
+                      tf32p_odd<1>(y.y, ly), b0, b1);
         mma_tf32_1688(acc[c][2], tf32p_even<2>(x.z, sx), tf32p_odd<2>(x.z, lx), tf32p_even<2>(y.z, sy),
-                      tf32p_odd<2>(y.z, ly), st.b[0], st.b[1]);
+                      tf32p_odd<2>(y.z, ly), b0, b1);
         mma_tf32_1688(acc[c][3], tf32p_even<3>(x.w, sx), tf32p_odd<3>(x.w, lx), tf32p_even<3>(y.w, sy),
-                      tf32p_odd<3>(y.w, ly), st.b[0], st.b[1]);
+                      tf32p_odd<3>(y.w, ly), b0, b1);
     }
 }
 
