@@ -525,6 +525,31 @@ def run_ours(args, rank, world, device):
                 ts.append(a.elapsed_time(b))
             paths[path] = round(sum(ts) / len(ts), 4)
 
+    # the same SpMM in TF32 (BASELINE configs: C3 TF32 N = 64/128/256): its own
+    # ME-BCRS (f32 values, k = 4) and an f32 dense operand, L2 flushed per call
+    tf32 = None
+    if not args.quick and prec == T.Precision.fp16:
+        me32 = T.encode_mebcrs(local_csr, T.Precision.tf32)
+        B32 = G.dense(cols, N, 3, values="real", dtype=torch.float32, device=device)
+        c32 = T.KernelConfig(T.Precision.tf32)
+        T.spmm(me32, B32, c32, out=out)
+        ts = []
+        for _ in range(10):
+            flush.zero_()
+            a.record()
+            T.spmm(me32, B32, c32, out=out)
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms32 = sorted(ts)[len(ts) // 2]
+        b32 = bytes_alg_spmm(me32.num_windows, me32.num_vectors, l_rows, N, 4, 4)
+        tf32 = {"N": N, "ms": round(ms32, 4), "gflops": round(2.0 * nnz_local * N / (ms32 / 1e3) / 1e9, 1),
+                "bytes_alg_per_launch": b32, "frac": round(b32 / (ms32 / 1e3) / 1e9 / peaks()[0], 4),
+                "kernel": "tf32_pack_kernel + spmm_tf32p_kernel<2> (mma.sync m16n8k8 on the 2.5-byte packed operand)",
+                "dram": _with_frac(dram_traffic("c3_tf32_n128_g1") if N == 128 and world == 1 else None, ms32)}
+        me32.free()
+        del B32
+
     # SDDMM on the same pattern (BASELINE metric covers SpMM/SDDMM; F = 32 as configs[1])
     sddmm = None
     if True:
@@ -607,7 +632,7 @@ def run_ours(args, rank, world, device):
                                 "memset + spmm_reduce_split") if prec == 0 else
                                "tf32_pack_kernel + spmm_tf32p_kernel<2> (mma.sync on the 2.5-byte packed operand)",
                      "binding_resource": ("l2_gather (L1 data pipe: one LDG + one SHFL wavefront per 128 B)" if prec == 0
-                                          else "gather latency (long-scoreboard; 16 warps/SM at 121 registers)"),
+                                          else "gather latency (long-scoreboard; 16 warps/SM at 117 registers)"),
                      "dram": _with_frac(dram, step_ms),
                      "l2_gather": {"gather_bytes_per_launch": gather_bytes,
                                    "achieved_gbs": round(gather_bytes / (step_ms / 1e3) / 1e9, 1),
@@ -628,6 +653,7 @@ def run_ours(args, rank, world, device):
         "encode_ms": round(max(g["encode_ms"] for g in gathered), 3),
         "back_to_back_ms": round(b2b_ms, 4),
         "path_ms": paths,
+        "tf32": tf32,
         "sddmm": sddmm,
         "broadcast_ms": round(bcast_ms, 3),
         "shards": [{"nnz": g["nnz"], "nv": g["nv"], "step_ms": round(g["step_ms"], 4)} for g in gathered],

@@ -81,6 +81,7 @@ struct AttStep {
     uint4 h[2][NC];  // vectors g (half 0) and g + 8 (half 1), features 32c + 8t .. +7
     float rn[2];     // inverse norms of those two vectors
     uint32_t live[2];  // their liveness bytes
+    uint32_t ok;       // bit hf: vector of half hf is inside the item (else h / live count as 0)
 };
 
 // cols: column indices of vectors [s0, s0 + 32) of the window, one per lane.
@@ -93,11 +94,17 @@ __device__ __forceinline__ void att_issue(const AttendArgs& a, uint32_t base, ui
         const uint32_t v = s + 8 * hf + g;
         const uint32_t col = __shfl_sync(0xffffffffu, cols, off + 8 * hf + g);
         const bool ok = v < vend;
-        const __half* r = a.h + static_cast<uint64_t>(col) * a.ldh + 8 * t;
+        // Unconditional loads (past the item: column 0's row, slot s -- both
+        // in bounds); att_compute zeroes them by `ok`.  Selecting the zero
+        // here made the issue wait for its own loads (ncu, C5: 24% of the
+        // stall samples on that select), before the previous step's MMAs.
+        const __half* r = a.h + static_cast<uint64_t>(ok ? col : 0u) * a.ldh + 8 * t;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) st.h[hf][c] = ok ? ld_gather_128(r + 32 * c) : make_uint4(0, 0, 0, 0);
-        st.rn[hf] = ok ? __ldg(a.rn + col) : 0.f;
-        st.live[hf] = ok ? static_cast<uint32_t>(__ldg(a.live + base + v)) : 0u;
+        for (int c = 0; c < NC; ++c) st.h[hf][c] = ld_gather_128(r + 32 * c);
+        st.rn[hf] = __ldg(a.rn + (ok ? col : 0u));
+        st.live[hf] = static_cast<uint32_t>(__ldg(a.live + base + (ok ? v : s)));
+        if (hf == 0) st.ok = ok ? 1u : 0u;
+        else st.ok |= ok ? 2u : 0u;
     }
 }
 
@@ -126,10 +133,18 @@ template <int NC>
 __device__ __forceinline__ void att_compute(const AttStep<NC>& st, const uint4 (&hi)[NC], const float (&qs)[2],
                                             uint32_t lane, float (&m)[2], float (&l)[2], float (&o)[NC][2][4]) {
     const uint32_t t = lane & 3;
+    const bool ok0 = st.ok & 1u, ok1 = st.ok & 2u;
+    uint4 h0[NC], h1[NC];  // vectors past the item contribute zero rows
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        h0[c] = ok0 ? st.h[0][c] : make_uint4(0, 0, 0, 0);
+        h1[c] = ok1 ? st.h[1][c] : make_uint4(0, 0, 0, 0);
+    }
+    const uint32_t lv[2] = {ok0 ? st.live[0] : 0u, ok1 ? st.live[1] : 0u};
     float acc[4];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        const uint4 &x = st.h[0][c], &y = st.h[1][c];
+        const uint4 &x = h0[c], &y = h1[c];
         if (c == 0) mma_f16_16816_z(acc, x.x, y.x, x.y, y.y, hi[c].x, hi[c].y);
         else mma_f16_16816(acc, x.x, y.x, x.y, y.y, hi[c].x, hi[c].y);
         mma_f16_16816(acc, x.z, y.z, x.w, y.w, hi[c].z, hi[c].w);
@@ -139,7 +154,7 @@ __device__ __forceinline__ void att_compute(const AttStep<NC>& st, const uint4 (
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         const int hf = e >> 1, r = e & 1;
-        const bool live = (st.live[hf] >> (2 * t + r)) & 1u;
+        const bool live = (lv[hf] >> (2 * t + r)) & 1u;
         z[e] = live ? acc[e] * qs[r] * st.rn[hf] : -INFINITY;
     }
     float mx[2] = {fmaxf(z[0], z[2]), fmaxf(z[1], z[3])};
@@ -174,8 +189,8 @@ __device__ __forceinline__ void att_compute(const AttStep<NC>& st, const uint4 (
             d[1] *= alpha[1];
             d[2] *= alpha[0];
             d[3] *= alpha[1];
-            mma_f16_16816(d, movtrans(comp(st.h[0][c], 2 * q)), movtrans(comp(st.h[0][c], 2 * q + 1)),
-                          movtrans(comp(st.h[1][c], 2 * q)), movtrans(comp(st.h[1][c], 2 * q + 1)), b0, b1);
+            mma_f16_16816(d, movtrans(comp(h0[c], 2 * q)), movtrans(comp(h0[c], 2 * q + 1)),
+                          movtrans(comp(h1[c], 2 * q)), movtrans(comp(h1[c], 2 * q + 1)), b0, b1);
         }
 }
 

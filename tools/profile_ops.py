@@ -4,7 +4,7 @@ kernels are captured; a warm-up call precedes it so the memory pool and the
 plan are settled).
 
   python tools/profile_ops.py CONFIG OP [PRECISION] [N_OR_F]
-    CONFIG: c1 | c3 | c4 | c5      OP: spmm | sddmm | sddmm_static | encode
+    CONFIG: c1 | c3 | c4 | c5      OP: spmm | sddmm | sddmm_static | encode | attend (AGNN, F = N_OR_F)
 """
 import os
 import sys
@@ -41,6 +41,13 @@ elif op.startswith("sddmm"):
     ov = torch.empty(8 * me.num_vectors, device="cuda")
     kc = T.KernelConfig(prec, static_mask=(op == "sddmm_static"))
     call = lambda: T.sddmm(T.SddmmOperands(me, A, Bt), kc, out_values=ov)  # noqa: E731
+elif op == "attend":  # one-pass AGNN attention on the layer's static mask (tools/time_attend.py)
+    import paper_2412_11007_b200.layers as L  # noqa: E402
+
+    layer = L.AGNNLayer(rows, rp, ci, beta=1.0)
+    H = torch.randn(rows, width, device="cuda").half()
+    C = torch.empty(rows, width, device="cuda")
+    call = lambda: T.agnn_attend(layer.mask, H, 1.0, layer.mask_cfg, out=C)  # noqa: E731
 else:
     call = lambda: T.encode_mebcrs(csr, prec)  # noqa: E731
 for _ in range(2):
