@@ -1,7 +1,7 @@
 #!/bin/bash
 # session 5: compute-sanitizer on the final tree (tools/sanitize.sh) plus memcheck of the TF32 tests
-# NOTE: compute-sanitizer is closed on this GPU pool (runs under it returned rc=86 with a refusal message); kept as the command record only.
 # (the deferred-conversion kernels) and racecheck of the AGNN attention
+# NOTE: compute-sanitizer is closed on this GPU pool (runs under it returned rc=86 with a refusal message); kept as the command record only.
 set -u
 bash tools/sanitize.sh r2s5san
 OUT=gpurun_out/r2s5san
