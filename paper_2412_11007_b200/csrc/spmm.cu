@@ -196,11 +196,23 @@ constexpr uint32_t kColMask = 0x7FFFFFFFu;
 // 8t + g loaded in slot u = k-slot, so one shuffle per register moves the
 // data into place and the vector (k) order stays the identity -- the sparse
 // fragment is the natural ME-BCRS pair at 8g + 2t.
+// f32-stored values (VF32) of the 128-feature kernels stay raw in the step
+// and are converted by f16_compute, so the conversion does not wait for the
+// value loads at issue time (the TF32 lesson).  The narrower
+// VF32 kernels keep converting at issue: two more registers per stage
+// spill there.  (A/B knob.)
+#ifndef TCS_VF32_DEFER
+#define TCS_VF32_DEFER 1
+#endif
+template <bool VF32, int NCHUNK>
+constexpr bool vf32_defer() { return VF32 && NCHUNK == 2 && TCS_VF32_DEFER; }
+
 template <int NCHUNK, int FPL, bool VF32>
 struct F16Step {
     static constexpr int NJ = FPL / 2;  // MMAs per chunk == u32 regs per (vector, chunk)
+    static constexpr bool kDefer = vf32_defer<VF32, NCHUNK>();
     uint32_t L[4][NCHUNK][NJ];          // loader slots u = 0..3 (vector v(u, lane/8), features FPL*(lane%8))
-    uint32_t b[2];                      // sparse fragment: rows g, vectors {2t,2t+1}, {2t+8,2t+9}
+    uint32_t b[kDefer ? 4 : 2];         // sparse fragment: rows g, vectors {2t,2t+1}, {2t+8,2t+9} (kDefer: raw f32)
 };
 
 // Vector held by MMA k slot u (0..3 = k 2t, 2t+1, 2t+8, 2t+9) of lane (g, t).
@@ -244,6 +256,28 @@ __device__ __forceinline__ uint32_t f16_val_general(const void* vals, uint64_t v
 // colpair holds the column indices of vectors [s - 16*half, +32).
 // Sparse fragment (both k=8 blocks) of the 16-vector step at s into b:
 // 0 past the item (-inf for a softmax operand, exp(-inf) = 0).
+// Raw f32 fragment (kDefer steps): slots of the 16-vector step at s, 0 past the item.
+__device__ __forceinline__ void f32_values_raw(const SpmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend,
+                                               uint32_t s, uint32_t g, uint32_t t, uint32_t (&b)[4]) {
+    const float* fv = static_cast<const float*>(a.vals);
+    if (s + 16 <= vend) {
+        const uint64_t off = vbase + 8ull * s + 8 * g + 2 * t;
+        const uint2 x = ld_stream_u64(fv + off), y = ld_stream_u64(fv + off + 64);
+        b[0] = x.x; b[1] = x.y; b[2] = y.x; b[3] = y.y;
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t v = s + kslot_vec(u, t);
+            uint32_t x = 0u;
+            if (v < vend && v < nvw) {
+                const uint32_t blk = v >> 3, j = v & 7u, width = min(8u, nvw - 8 * blk);
+                x = __float_as_uint(fv[vbase + 64ull * blk + g * width + j]);
+            }
+            b[u] = x;
+        }
+    }
+}
+
 template <bool VF32, bool SMX>
 __device__ __forceinline__ void f16_values(const SpmmArgs& a, uint64_t vbase, uint32_t nvw, uint32_t vend, uint32_t s,
                                            uint32_t g, uint32_t t, uint32_t (&b)[2]) {
@@ -295,7 +329,10 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
 #pragma unroll
             for (int c = 0; c < NCHUNK; ++c) f16_gather<FPL, HOT>(row + c * CHUNK, pol, st.L[u][c]);
         }
-        if constexpr (LOADV) load_sparse_full<VF32>(a.vals, vbase, s, g, t, st.b[0], st.b[1]);
+        if constexpr (LOADV) {
+            if constexpr (F16Step<NCHUNK, FPL, VF32>::kDefer) f32_values_raw(a, vbase, nvw, vend, s, g, t, st.b);
+            else load_sparse_full<VF32>(a.vals, vbase, s, g, t, st.b[0], st.b[1]);
+        }
     } else {
         // residue step: vectors at or past vend contribute zero registers
 #pragma unroll
@@ -313,14 +350,25 @@ __device__ __forceinline__ void f16_issue(const SpmmArgs& a, const __half* __res
                 }
             }
         }
-        if constexpr (LOADV) f16_values<VF32, SMX>(a, vbase, nvw, vend, s, g, t, st.b);
+        if constexpr (LOADV) {
+            if constexpr (F16Step<NCHUNK, FPL, VF32>::kDefer) f32_values_raw(a, vbase, nvw, vend, s, g, t, st.b);
+            else f16_values<VF32, SMX>(a, vbase, nvw, vend, s, g, t, st.b);
+        }
     }
 }
 
 template <int NCHUNK, int FPL, bool VF32, bool SMX = false>
 __device__ __forceinline__ void f16_compute(const F16Step<NCHUNK, FPL, VF32>& st, float (&acc)[NCHUNK][FPL / 2][4],
                                             uint32_t src_lane, float scale = 0.f, float sm = 0.f, float sinv = 0.f) {
-    uint32_t b0 = st.b[0], b1 = st.b[1];
+    uint32_t b0, b1;
+    if constexpr (F16Step<NCHUNK, FPL, VF32>::kDefer) {
+        static_assert(!SMX, "softmax operands are binary16");
+        b0 = f2_to_h2(__uint_as_float(st.b[0]), __uint_as_float(st.b[1]));
+        b1 = f2_to_h2(__uint_as_float(st.b[2]), __uint_as_float(st.b[3]));
+    } else {
+        b0 = st.b[0];
+        b1 = st.b[1];
+    }
     if constexpr (SMX) {  // applied here, when the values have landed
         b0 = smx_h2(b0, scale, sm, sinv);
         b1 = smx_h2(b1, scale, sm, sinv);
