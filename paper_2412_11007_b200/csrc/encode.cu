@@ -65,6 +65,11 @@ constexpr uint32_t kSortCapA = TCS_ENC_SORT_SPLIT;  // 0: one launch
 #define TCS_ENC_HUB_BITMAP 1
 #endif
 constexpr uint32_t kBigThreads = TCS_ENC_SORT_THREADS;
+// the global-memory hub bitmap's popcount / prefix passes as coalesced warp
+// scans (A/B knob; 0 = thread-contiguous runs, as the shared-memory bitmap)
+#ifndef TCS_ENC_GBM_WARPSCAN
+#define TCS_ENC_GBM_WARPSCAN 1
+#endif
 #ifndef TCS_ENC_BITMAP_THREADS
 #define TCS_ENC_BITMAP_THREADS 512
 #endif
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(kTinyWarps * 32) window_sort_warp(const uint32
     if (bad) atomicMax(&chk->bad, bad);
 }
 
-template <int VH>
+template <int VH, bool GBM = false>
 __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ csr_rp,
                                                    const uint32_t* __restrict__ ci, uint64_t rows, uint64_t cols,
                                                    uint64_t w, uint4* bm4, uint4* pre4, uint32_t quads,
@@ -459,7 +464,8 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
                                  chk);
         } else if (bscratch) {
             uint4* bm4 = bscratch + 2ull * quads * blockIdx.x;
-            bitmap_rank_window<VH>(csr_rp, ci, rows, cols, w, bm4, bm4 + quads, quads, tmp_cols, rank, nv_out, chk);
+            bitmap_rank_window<VH, TCS_ENC_GBM_WARPSCAN>(csr_rp, ci, rows, cols, w, bm4, bm4 + quads, quads, tmp_cols,
+                                                         rank, nv_out, chk);
         } else {
             uint64_t* a = scratch + 2ull * e0;  // window-private slice of a 2*nnz scratch
             window_sort_rank<VH>(csr_rp, ci, rows, cols, w, a, a + n, tmp_cols, rank, nv_out, chk);
@@ -475,7 +481,7 @@ __global__ void __launch_bounds__(kBigThreads) window_sort_big(const uint32_t* _
 // memory: clearing and scanning cols/32 words in L2 beats three global
 // merge passes over 10^4..10^5 entries).  The word arrays are walked as
 // uint4 quads (words padded to a multiple of 4).
-template <int VH>
+template <int VH, bool GBM>
 __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ csr_rp,
                                                    const uint32_t* __restrict__ ci, uint64_t rows, uint64_t cols,
                                                    uint64_t w, uint4* bm4, uint4* pre4, uint32_t quads,
@@ -535,21 +541,65 @@ __device__ __forceinline__ void bitmap_rank_window(const uint32_t* __restrict__ 
     }
     if (bad) atomicMax(&chk->bad, bad);
     __syncthreads();
-    // prefix popcount over this thread's contiguous run of quads
-    const uint32_t q0 = min(quads, threadIdx.x * qpt), q1 = min(quads, q0 + qpt);
-    uint32_t cnt = 0;
-    for (uint32_t i = q0; i < q1; ++i) {
-        const uint4 x = bm4[i];
-        cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
-    }
     uint32_t total;
-    const uint32_t run = dev::block_exclusive_scan(cnt, &total);
-    uint32_t p = run;
-    for (uint32_t i = q0; i < q1; ++i) {
-        const uint4 x = bm4[i];
-        const uint32_t p0 = p, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
-        pre4[i] = make_uint4(p0, p1, p2, p3);
-        p = p3 + __popc(x.w);
+    if constexpr (GBM) {
+        // Global-memory bitmap (hub windows of wide column spaces, 10^5+
+        // quads): a thread-contiguous run of quads would be one dependent
+        // L2/DRAM latency per quad and uncoalesced (ncu, C5: 50% of
+        // window_sort_big's stall samples).  Each warp scans a contiguous
+        // range 32 quads at a time (coalesced, loads unrolled), with a warp
+        // scan per iteration and a block scan of the warp totals.
+        __shared__ uint32_t gbm_wsum[32];
+        const uint32_t warp = threadIdx.x >> 5, nwarps = nt >> 5;
+        const uint32_t per = ((quads + nwarps - 1) / nwarps + 31u) & ~31u;
+        const uint32_t qa = min(quads, warp * per), qb = min(quads, qa + per);
+        uint32_t wc = 0;
+#pragma unroll 4
+        for (uint32_t i = qa + lane; i < qb; i += 32) {
+            const uint4 x = bm4[i];
+            wc += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) wc += __shfl_xor_sync(0xffffffffu, wc, o);
+        if (lane == 0) gbm_wsum[warp] = wc;
+        __syncthreads();
+        uint32_t carry = 0;
+        total = 0;
+        for (uint32_t j = 0; j < nwarps; ++j) {
+            const uint32_t x = gbm_wsum[j];
+            carry += j < warp ? x : 0u;
+            total += x;
+        }
+        for (uint32_t i0 = qa; i0 < qb; i0 += 32) {
+            const uint32_t i = i0 + lane;
+            const uint4 x = i < qb ? bm4[i] : make_uint4(0, 0, 0, 0);
+            const uint32_t c = __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= static_cast<uint32_t>(o)) inc += y;
+            }
+            const uint32_t p0 = carry + inc - c, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
+            if (i < qb) pre4[i] = make_uint4(p0, p1, p2, p3);
+            carry += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    } else {
+        // prefix popcount over this thread's contiguous run of quads
+        const uint32_t q0 = min(quads, threadIdx.x * qpt), q1 = min(quads, q0 + qpt);
+        uint32_t cnt = 0;
+        for (uint32_t i = q0; i < q1; ++i) {
+            const uint4 x = bm4[i];
+            cnt += __popc(x.x) + __popc(x.y) + __popc(x.z) + __popc(x.w);
+        }
+        const uint32_t run = dev::block_exclusive_scan(cnt, &total);
+        uint32_t p = run;
+        for (uint32_t i = q0; i < q1; ++i) {
+            const uint4 x = bm4[i];
+            const uint32_t p0 = p, p1 = p0 + __popc(x.x), p2 = p1 + __popc(x.y), p3 = p2 + __popc(x.z);
+            pre4[i] = make_uint4(p0, p1, p2, p3);
+            p = p3 + __popc(x.w);
+        }
     }
     if (threadIdx.x == 0) nv_out[w] = total;
     __syncthreads();
