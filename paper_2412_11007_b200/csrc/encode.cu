@@ -269,12 +269,39 @@ __device__ __forceinline__ void window_sort_rank(const uint32_t* __restrict__ cs
         }
     }
     uint32_t bad = 0;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const uint32_t c = ci[e0 + i];
-        bad = max(bad, check_col<VH>(ci, e0, i, c, bnd, cols));
-        // an out-of-range column (reported via chk->bad) must not reach the
-        // output: the pipelined encode multiplies before the host sees the flag
-        bufA[i] = (static_cast<uint64_t>(c < cols ? c : 0u) << 32) | i;
+    {
+        // 4 entries per thread in flight; the row-order predecessor is lane
+        // - 1's column (consecutive lanes hold consecutive entries), loaded
+        // only by lane 0.  Warp-uniform trip count (the shuffle needs every lane).
+        constexpr int U = 4;
+        const uint32_t lane = threadIdx.x & 31, nt = blockDim.x;
+        for (uint32_t i0 = threadIdx.x; i0 - lane < n; i0 += U * nt) {
+            uint32_t c[U], cp0[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * nt;
+                c[u] = i < n ? ci[e0 + i] : 0xFFFFFFFFu;
+                cp0[u] = lane == 0 && i < n && i > 0 ? ci[e0 + i - 1] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t i = i0 + u * nt;
+                uint32_t cp = __shfl_up_sync(0xffffffffu, c[u], 1);
+                if (lane == 0) cp = cp0[u];
+                if (i >= n) continue;
+                uint32_t b = c[u] >= cols ? 3u : 0u;
+                if (i > 0 && cp >= c[u]) {
+                    bool row_start = false;
+#pragma unroll
+                    for (int r = 1; r < VH; ++r) row_start |= (i == bnd[r]);
+                    if (!row_start) b = 4u;
+                }
+                bad = max(bad, b);
+                // an out-of-range column (reported via chk->bad) must not reach the
+                // output: the pipelined encode multiplies before the host sees the flag
+                bufA[i] = (static_cast<uint64_t>(c[u] < cols ? c[u] : 0u) << 32) | i;
+            }
+        }
     }
     if (bad) atomicMax(&chk->bad, bad);
     __syncthreads();
