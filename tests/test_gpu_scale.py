@@ -346,3 +346,27 @@ def test_pipelined_host_call_reports_late_chunk_format_errors(defect):
     assert rc == abi.TCS_ERR_FORMAT
     msg = lib.tcs_last_error().decode() if isinstance(lib.tcs_last_error(), bytes) else str(lib.tcs_last_error())
     assert ("ascending" if defect == "descending" else "out of range") in msg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [128, 256, 200, 64, 32])
+def test_f32_value_storage_equals_binary16_storage(n):
+    """FP16 SpMM on f32-stored values (the drop-in adapter's bit-exact
+    storage; the 128-feature kernels convert them to binary16 at the MMA)
+    equals the same SpMM on binary16-stored values bit for bit: both round
+    with RNE (ref precision.hpp round_to_fp16), so the MMA operands are the
+    same.  Real values, hub windows (split items), residue steps."""
+    import paper_2412_11007_b200._abi as abi
+
+    spec = G.GraphSpec("mid_real", 60_000, 3_000_000, alpha=1.2, cap=60.0, seed=11)
+    rows, cols, rp, ci, v = G.power_law_csr(spec, values="real")
+    csr = T.CsrMatrix(rows, cols, rp, ci, v)
+    m32 = T.encode_mebcrs(csr, T.Precision.fp16, abi.TCS_DTYPE_F32)
+    m16 = T.encode_mebcrs(csr, T.Precision.fp16, abi.TCS_DTYPE_F16)
+    B = G.dense(cols, n, 3, values="real", dtype=torch.float16)
+    cfg = T.KernelConfig(T.Precision.fp16)
+    got32 = T.spmm(m32, B, cfg).output
+    got16 = T.spmm(m16, B, cfg).output
+    assert torch.equal(got32.view(torch.int32), got16.view(torch.int32))
+    m32.free()
+    m16.free()
